@@ -1,0 +1,215 @@
+/*
+ * simdx.h — C ABI of the B200-native SIMD-X ACC frontier engine
+ * (arXiv 1812.04070; PAPER.md lines cited as P:<n>).
+ *
+ * The library runs ONE data-parallel hot path: the per-iteration
+ * Active-Compute-Combine (ACC) frontier step over a CSR/CSC graph
+ * (P:913), with just-in-time task management (online + ballot filters and
+ * thread/warp/CTA degree binning), the push/pull direction switch
+ * and push/pull selective kernel fusion held together by a deadlock-free grid
+ * barrier.  Every step runs in hand-written sm_100a CUDA kernels;
+ * there is no CPU fallback: without a usable CUDA device every call returns
+ * SX_E_CUDA.
+ *
+ * Conventions (all functions):
+ *   - extern "C", no C++ exceptions cross the ABI, nothing aborts the process.
+ *   - Return an sx_status; on failure sx_last_error() holds a thread-local
+ *     detail string valid until the next call on that thread.
+ *   - A sticky CUDA error (e.g. an illegal address) poisons the context: every
+ *     later call on it returns SX_E_STATE.
+ *   - Vertex ids are uint32; n must be < 2^32-1 because 0xFFFFFFFF is
+ *     the "unreached / unset" sentinel.  Edge indices are uint64.
+ *   - A context is single-threaded (one host thread at a time); distinct
+ *     contexts are independent.  All work runs on the context's stream and
+ *     every algorithm call synchronises that stream before returning, so
+ *     output buffers are valid on return.
+ *   - Output pointers may be host or device memory (detected with
+ *     cudaPointerGetAttributes); the caller allocates them.
+ */
+#ifndef SIMDX_H
+#define SIMDX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SX_OK = 0,
+    SX_E_INVALID = 1,    /* bad argument: NULL required pointer, src >= n, n >= 2^32-1, k-core on directed, ... */
+    SX_E_OOM = 2,        /* device allocation failed */
+    SX_E_CUDA = 3,       /* CUDA runtime error (no device, launch failure, ...) */
+    SX_E_NCCL = 4,       /* reserved for the multi-GPU layer */
+    SX_E_NO_REVERSE = 5, /* pull needed on a directed graph uploaded without CSC */
+    SX_E_WEIGHT = 6,     /* SSSP on an unweighted graph or with a zero weight ("positive edge weights") */
+    SX_E_BARRIER = 7,    /* co-resident grid impossible, or the grid-barrier watchdog fired */
+    SX_E_STATE = 8       /* context poisoned by an earlier sticky CUDA error */
+} sx_status;
+
+/* Static string naming a status code. Never NULL. */
+const char* sx_status_str(int status);
+/* Thread-local detail of the last failure on this thread ("" if none). Never NULL. */
+const char* sx_last_error(void);
+/* ABI version: (major << 16) | minor. */
+int sx_version(void);
+
+typedef struct sx_ctx_s* sx_ctx;     /* one device + one stream */
+typedef struct sx_graph_s* sx_graph; /* device-resident graph owned by one ctx */
+
+/*
+ * Create a context on CUDA device `device`, issuing all work on `cuda_stream`
+ * (a cudaStream_t; NULL = the legacy default stream).  The stream is borrowed:
+ * it must outlive the context.  Errors: SX_E_CUDA (no such device / not
+ * sm_100), SX_E_INVALID (out == NULL), SX_E_OOM.
+ */
+sx_status sx_ctx_create(int device, void* cuda_stream, sx_ctx* out);
+/* Release a context (NULL is a no-op).  Graphs of the ctx must be freed first. */
+void sx_ctx_destroy(sx_ctx ctx);
+
+/*
+ * Device facts the engine sizes itself from (Eq. 1 generalised):
+ * the persistent kernels are launched cooperatively with
+ * ctas = occupancy(kernel) * sm_count, so every CTA is co-resident and the
+ * software grid barrier cannot deadlock (the Fig. 10 failure).
+ */
+typedef struct {
+    int device, sm_count, cc_major, cc_minor;
+    int regs_per_sm, max_threads_per_sm;
+    int block_threads;       /* threads per CTA of the persistent kernels */
+    int push_ctas_per_sm;    /* occupancy of the fused push kernel */
+    int pull_ctas_per_sm;    /* occupancy of the fused pull kernel */
+    int push_regs, pull_regs; /* registers/thread of those kernels (Table 2 analogue) */
+} sx_device_info;
+sx_status sx_ctx_info(sx_ctx ctx, sx_device_info* out);
+
+/* ------------------------------------------------------------------ graphs */
+enum {
+    SX_DIRECTED = 1,    /* csc_* describe the in-neighbour rows; otherwise the graph is symmetric and CSR serves as CSC */
+    SX_DEVICE_PTRS = 2, /* row_ptr/col/w (and csc_*) are device pointers */
+    SX_BORROW = 4       /* with SX_DEVICE_PTRS: do not copy; the caller keeps the arrays alive until sx_graph_free */
+};
+
+/*
+ * A CSR graph.  Layout: row_ptr u64[n+1] with row_ptr[0] = 0,
+ * non-decreasing, row_ptr[n] = m; col u32[m] neighbour ids < n; w = edge
+ * weights, w_bytes = 1 (u8) or 4 (u32) per edge, or w = NULL (unweighted).
+ * For SX_DIRECTED graphs csc_ptr/csc_idx/csc_w give the in-neighbour rows in
+ * the same layout (csc_w uses w_bytes); they may be NULL, in which case pull
+ * (PageRank, SpMV, BP, pull-mode BFS) returns SX_E_NO_REVERSE.
+ */
+typedef struct {
+    uint64_t n, m;
+    const uint64_t* row_ptr;
+    const uint32_t* col;
+    const void* w;
+    uint32_t w_bytes;
+    const uint64_t* csc_ptr;
+    const uint32_t* csc_idx;
+    const void* csc_w;
+    uint32_t flags;
+} sx_csr_desc;
+
+/*
+ * Upload (copy) a CSR graph to the device, validate it (row_ptr monotone,
+ * row_ptr[0] = 0, row_ptr[n] = m, col < n) and precompute per-vertex degree
+ * arrays (step a1/a3 of SURVEY.md §8(a)).  The caller's arrays are not
+ * retained unless SX_BORROW.  Errors: SX_E_INVALID (bad layout, n >= 2^32-1),
+ * SX_E_OOM, SX_E_CUDA.
+ */
+sx_status sx_graph_upload(sx_ctx ctx, const sx_csr_desc* desc, sx_graph* out);
+/* n, m and the owned vertex range [v_begin, v_end) (= [0, n) on one GPU). Any out pointer may be NULL. */
+sx_status sx_graph_info(sx_graph g, uint64_t* n, uint64_t* m, uint64_t* v_begin, uint64_t* v_end);
+/* Free a graph and its workspace (NULL is a no-op). */
+void sx_graph_free(sx_graph g);
+
+/* -------------------------------------------------------------- run knobs */
+typedef struct {
+    uint32_t iter;       /* 1-based iteration number */
+    uint32_t dir;        /* 0 push, 1 pull */
+    uint32_t filter;     /* how the NEXT list was produced: 0 online, 1 ballot, 2 static (pull-all lists) */
+    uint32_t launch;     /* 0-based index of the kernel launch that ran this iteration */
+    uint32_t n_active[4];/* next-iteration list sizes: small / medium / large / huge;
+                            in pull these are the remaining candidate (unvisited) lists */
+    uint64_t n_frontier; /* |F'|: vertices activated by this iteration */
+    uint64_t m_active;   /* sum of out-degrees of F' (m_f of the direction heuristic) */
+    uint64_t aux;        /* algorithm-specific: BFS unvisited edges m_u; SSSP bucket upper bound; k-core level k */
+} sx_trace_rec;
+
+typedef struct {
+    uint32_t overflow_threshold; /* online-filter bin capacity per warp; default 64 */
+    uint32_t sep_small;          /* degree separator thread|warp; default 32 */
+    uint32_t sep_large;          /* degree separator warp|CTA; default 128 */
+    uint32_t sep_huge;           /* degree separator CTA|grid-split (B200 addition); default 16384 */
+    float alpha, beta;           /* push->pull when m_f > m_u/alpha, pull->push when n_f < n/beta (Beamer; reading 8); 14, 24 */
+    int32_t force_filter;        /* 0 JIT, 1 online only, 2 ballot only */
+    int32_t force_dir;           /* 0 auto, 1 push only, 2 pull only */
+    int32_t fusion;              /* 1 selective push/pull fusion (default); 0 no fusion (one launch per iteration) */
+    uint32_t max_iters;          /* 0 = unlimited */
+    sx_trace_rec* trace;         /* nullable host buffer of trace_cap records (P:623-626 activation patterns) */
+    uint64_t trace_cap;
+} sx_opts;
+
+typedef struct {
+    uint32_t iterations;         /* BSP iterations executed */
+    uint32_t launches;           /* persistent-kernel launches (Table 2: selective fusion -> 3 for BFS) */
+    uint32_t ballot_iters;       /* iterations whose next list came from the ballot filter */
+    uint32_t pull_iters;         /* iterations run in pull direction */
+    uint64_t edges_examined;     /* edges whose Compute ran (push: all out-edges of F; pull: scanned up to early exit) */
+    uint64_t vertices_scanned;   /* vertices covered by ballot scans */
+    uint64_t list_entries;       /* active-list entries consumed */
+    double bytes_model;          /* algorithmic bytes of the executed schedule (SURVEY.md §8(d) rule) */
+    double ms;                   /* device time of the run, CUDA events on the ctx stream (init + all kernels, no readback) */
+    double ms_push, ms_pull;     /* device time inside push / pull persistent kernels (CUDA events around each launch) */
+    double bytes_push, bytes_pull; /* bytes_model split by the direction of the launch that moved them */
+    uint32_t launches_push, launches_pull;
+} sx_stats;
+
+/* Fill `o` with the defaults above. */
+void sx_opts_default(sx_opts* o);
+
+/* ------------------------------------------------------------- algorithms
+ * opts may be NULL (defaults); stats may be NULL.  Results are written to the
+ * caller's buffer of n elements (host or device memory).
+ */
+
+/* BFS (voting combine P:345): level_out[v] = hop distance from src,
+ * 0xFFFFFFFF if unreachable.  Push/pull switch per opts.
+ * Errors: SX_E_INVALID (src >= n, NULL level_out), SX_E_NO_REVERSE (pull on a directed graph without CSC). */
+sx_status sx_bfs(sx_graph g, uint32_t src, const sx_opts* opts, uint32_t* level_out, sx_stats* stats);
+
+/* SSSP: dist_out[v] = min path weight from src
+ * (u32, 0xFFFFFFFF unreachable).  delta-stepping with bucket width `delta` (0 = infinity:
+ * frontier Bellman-Ford; reading 9).  Distances are delta-independent.
+ * Errors: SX_E_WEIGHT (unweighted graph or a zero weight), SX_E_INVALID. */
+sx_status sx_sssp(sx_graph g, uint32_t src, uint32_t delta, const sx_opts* opts, uint32_t* dist_out,
+                  sx_stats* stats);
+
+/* PageRank (reading 14): `iters` Jacobi steps of
+ *   r(u) = (1-d)/N + d*(sum_{v in in(u)} r(v)/outdeg(v) + D/N), D = dangling mass, r_0 = 1/N,
+ * pull with sum combine; iters >= 1.  rank_out: f32[n].  Errors: SX_E_INVALID (iters = 0, damping outside [0,1]), SX_E_NO_REVERSE. */
+sx_status sx_pagerank(sx_graph g, float damping, uint32_t iters, const sx_opts* opts, float* rank_out,
+                      sx_stats* stats);
+
+/* k-core (reading 6): k > 0 -> core_out[v] = 1 if v is in the k-core (minimum degree >= k,
+ * duplicate edges counted) else 0; k = 0 -> core_out[v] = coreness of v.  Undirected graphs only.
+ * Errors: SX_E_INVALID (directed graph). */
+sx_status sx_kcore(sx_graph g, uint32_t k, const sx_opts* opts, uint32_t* core_out, sx_stats* stats);
+
+/* SpMV (north_star; not in the paper): y[u] = sum_{(v,u) in E} w(v,u) * x[v] (w = 1 if unweighted),
+ * repeated `iters` >= 1 times with the same x (pull, sum combine).  x: f32[n] host or device.
+ * Errors: SX_E_INVALID, SX_E_NO_REVERSE. */
+sx_status sx_spmv(sx_graph g, const float* x, uint32_t iters, const sx_opts* opts, float* y_out,
+                  sx_stats* stats);
+
+/* Belief propagation (model = reading 15 of SURVEY.md §8(c)): `iters` Jacobi steps of
+ *   l(u) = logit(p_u) + sum_{v in in(u)} log((c b + (1-c)(1-b)) / (c (1-b) + (1-c) b)),
+ *   b = sigmoid(l(v)), c = 0.25 + 0.5*(weight-1)/254 (unweighted: c = 0.75), l_0 = logit(p).
+ * prior: f32[n] in (0,1), host or device; iters >= 1.  Errors: SX_E_INVALID, SX_E_NO_REVERSE. */
+sx_status sx_bp(sx_graph g, const float* prior, uint32_t iters, const sx_opts* opts, float* logodds_out,
+                sx_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SIMDX_H */

@@ -1,0 +1,324 @@
+// capi.cu — contexts, graph upload/validation, launch plumbing and the common
+// run bookkeeping behind include/simdx.h.
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "internal.h"
+
+using namespace sx;
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+namespace sxh {
+
+sx_status fail(sx_status st, const std::string& msg) {
+    g_last_error = msg;
+    return st;
+}
+
+sx_status cuda_fail(cudaError_t e, const char* what) {
+    g_last_error = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+    if (e == cudaErrorMemoryAllocation) return SX_E_OOM;
+    if (e == cudaErrorCooperativeLaunchTooLarge) return SX_E_BARRIER;
+    return SX_E_CUDA;
+}
+
+sx_status check_ctx(sx_ctx c) {
+    if (!c) return fail(SX_E_INVALID, "NULL context");
+    if (c->poisoned) return fail(SX_E_STATE, "context poisoned by an earlier sticky CUDA error");
+    SX_CU(cudaSetDevice(c->device));
+    return SX_OK;
+}
+
+static bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+sx_status copy_out(sx_graph g, void* dst, const void* src_dev, size_t bytes) {
+    if (bytes == 0) return SX_OK;
+    SX_CU(cudaMemcpyAsync(dst, src_dev, bytes, cudaMemcpyDefault, g->ctx->stream));
+    SX_CU(cudaStreamSynchronize(g->ctx->stream));
+    return SX_OK;
+}
+
+sx_status copy_in(sx_graph g, void* dst_dev, const void* src, size_t bytes) {
+    if (bytes == 0) return SX_OK;
+    SX_CU(cudaMemcpyAsync(dst_dev, src, bytes, cudaMemcpyDefault, g->ctx->stream));
+    return SX_OK;
+}
+
+DevGraph dev_graph(const sx_graph g) {
+    DevGraph d;
+    d.n = g->n;
+    d.m = g->m;
+    d.rp = g->rp;
+    d.ci = g->ci;
+    d.w8 = g->wbytes == 1 ? (const uint8_t*)g->w : nullptr;
+    d.w32 = g->wbytes == 4 ? (const uint32_t*)g->w : nullptr;
+    d.irp = g->irp;
+    d.ici = g->ici;
+    d.iw8 = g->wbytes == 1 ? (const uint8_t*)g->iw : nullptr;
+    d.iw32 = g->wbytes == 4 ? (const uint32_t*)g->iw : nullptr;
+    d.dout = g->dout;
+    d.din = g->din;
+    d.nz_in = g->nz_in;
+    return d;
+}
+
+sx_opts resolve_opts(const sx_opts* o) {
+    sx_opts r;
+    sx_opts_default(&r);
+    if (o) r = *o;
+    if (r.overflow_threshold == 0) r.overflow_threshold = 64;
+    if (r.sep_small == 0) r.sep_small = 32;
+    if (r.sep_large == 0) r.sep_large = 128;
+    if (r.sep_huge == 0) r.sep_huge = 16384;
+    if (r.sep_large < r.sep_small) r.sep_large = r.sep_small;
+    if (r.sep_huge < r.sep_large) r.sep_huge = r.sep_large;
+    if (!(r.alpha > 0)) r.alpha = 14.f;
+    if (!(r.beta > 0)) r.beta = 24.f;
+    return r;
+}
+
+int coop_grid(sx_graph g, const void* fn) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, BLOCK, 0) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int grid = per_sm * g->ctx->prop.multiProcessorCount;
+    if (grid > MAX_GRID) grid = MAX_GRID;
+    return grid;
+}
+
+Sched make_sched(const sx_graph g, const sx_opts& o) {
+    Sched s;
+    s.ctl = g->ctl;
+    s.lists[0] = g->lists[0];
+    s.lists[1] = g->lists[1];
+    for (int i = 0; i < 3; ++i) s.bm[i] = g->bm[i];
+    s.cta_cnt = g->cta_cnt;
+    s.trace = o.trace ? g->trace : nullptr;
+    s.trace_cap = o.trace ? (uint32_t)std::min<uint64_t>(o.trace_cap, g->trace_cap) : 0;
+    s.nwords = g->nwords;
+    s.sep_small = o.sep_small;
+    s.sep_large = o.sep_large;
+    s.sep_huge = o.sep_huge;
+    // online capacity per class: threshold x warps of the persistent grid
+    // (the paper's per-thread bin of 64, aggregated per warp)
+    const uint64_t warps = (uint64_t)g->ctx->prop.multiProcessorCount * (2048 / 32);
+    uint64_t cap = (uint64_t)o.overflow_threshold * warps;
+    if (o.force_filter == 1 || cap > g->n) cap = g->n;  // online only: never overflows
+    s.online_cap = (uint32_t)cap;
+    s.alpha = o.alpha;
+    s.beta = o.beta;
+    s.force_filter = o.force_filter;
+    s.force_dir = o.force_dir;
+    s.fusion = o.fusion;
+    s.max_iters = o.max_iters;
+    return s;
+}
+
+sx_status coop_launch(sx_graph g, const void* fn, void** args, int* grid_out) {
+    const int grid = coop_grid(g, fn);
+    if (grid <= 0) return fail(SX_E_BARRIER, "persistent kernel cannot be co-resident (occupancy 0)");
+    if (grid_out) *grid_out = grid;
+    cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BLOCK), args, 0, g->ctx->stream);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return cuda_fail(e, "cudaLaunchCooperativeKernel");
+    }
+    return SX_OK;
+}
+
+sx_status Run::begin() {
+    sx_ctx c = g->ctx;
+    if (o.trace && o.trace_cap > g->trace_cap) {
+        if (g->trace) cudaFree(g->trace);
+        g->trace = nullptr;
+        g->trace_cap = 0;
+        SX_CU(cudaMalloc(&g->trace, o.trace_cap * sizeof(TraceRec)));
+        g->trace_cap = (uint32_t)o.trace_cap;
+    }
+    SX_CU(cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), c->stream));
+    std::memset(c->h_ctl, 0, sizeof(Ctl));
+    std::memset(&prev, 0, sizeof(prev));
+    SX_CU(cudaEventRecord(c->ev0, c->stream));
+    return SX_OK;
+}
+
+sx_status Run::launch(const void* fn, void** args, bool pull) {
+    sx_ctx c = g->ctx;
+    SX_CU(cudaEventRecord(c->evk0, c->stream));
+    sx_status rc = coop_launch(g, fn, args, nullptr);
+    if (rc != SX_OK) return rc;
+    SX_CU(cudaEventRecord(c->evk1, c->stream));
+    SX_CU(cudaMemcpyAsync(c->h_ctl, g->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->stream));
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) {
+        c->poisoned = true;
+        return cuda_fail(e, "persistent kernel");
+    }
+    float ms = 0;
+    SX_CU(cudaEventElapsedTime(&ms, c->evk0, c->evk1));
+    const Ctl& h = *c->h_ctl;
+    Counters& k = pull ? c_pull : c_push;
+    k.entries += (double)(h.st_entries - prev.st_entries);
+    k.edges += (double)(h.st_edges - prev.st_edges);
+    k.reached += (double)(h.st_reached - prev.st_reached);
+    k.scanned += (double)(h.st_scanned - prev.st_scanned);
+    k.iters += (double)(h.st_iters - prev.st_iters);
+    k.pull += (double)(h.st_pull - prev.st_pull);
+    k.ballot += (double)(h.st_ballot - prev.st_ballot);
+    prev = h;
+    (pull ? ms_pull : ms_push) += ms;
+    ++(pull ? launches_pull : launches_push);
+    ++launches;
+    if (h.error) return fail(SX_E_BARRIER, "grid barrier watchdog fired");
+    if (launches > 1000000) return fail(SX_E_STATE, "runaway launch loop");
+    return SX_OK;
+}
+
+sx_status Run::end(BytesFn bytes) {
+    sx_ctx c = g->ctx;
+    SX_CU(cudaEventRecord(c->ev1, c->stream));
+    SX_CU(cudaEventSynchronize(c->ev1));
+    float ms = 0;
+    SX_CU(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    const Ctl& h = *c->h_ctl;
+    if (st) {
+        std::memset(st, 0, sizeof(*st));
+        st->iterations = h.st_iters;
+        st->launches = launches;
+        st->ballot_iters = h.st_ballot;
+        st->pull_iters = h.st_pull;
+        st->edges_examined = h.st_edges;
+        st->vertices_scanned = h.st_scanned;
+        st->list_entries = h.st_entries;
+        st->bytes_push = bytes(g, c_push);
+        st->bytes_pull = bytes(g, c_pull);
+        st->bytes_model = st->bytes_push + st->bytes_pull;
+        st->ms = ms;
+        st->ms_push = ms_push;
+        st->ms_pull = ms_pull;
+        st->launches_push = launches_push;
+        st->launches_pull = launches_pull;
+    }
+    if (o.trace && o.trace_cap) {
+        const uint64_t nrec = std::min<uint64_t>(std::min<uint64_t>(h.ntrace, o.trace_cap), g->trace_cap);
+        std::memset(o.trace, 0, o.trace_cap * sizeof(sx_trace_rec));
+        if (nrec) {
+            SX_CU(cudaMemcpyAsync(o.trace, g->trace, nrec * sizeof(TraceRec), cudaMemcpyDefault, c->stream));
+            SX_CU(cudaStreamSynchronize(c->stream));
+        }
+    }
+    return SX_OK;
+}
+
+}  // namespace sxh
+
+// ====================================================================== C ABI
+static_assert(sizeof(sx_trace_rec) == sizeof(TraceRec), "trace record layout");
+
+extern "C" {
+
+const char* sx_status_str(int s) {
+    switch (s) {
+        case SX_OK: return "SX_OK";
+        case SX_E_INVALID: return "SX_E_INVALID";
+        case SX_E_OOM: return "SX_E_OOM";
+        case SX_E_CUDA: return "SX_E_CUDA";
+        case SX_E_NCCL: return "SX_E_NCCL";
+        case SX_E_NO_REVERSE: return "SX_E_NO_REVERSE";
+        case SX_E_WEIGHT: return "SX_E_WEIGHT";
+        case SX_E_BARRIER: return "SX_E_BARRIER";
+        case SX_E_STATE: return "SX_E_STATE";
+        default: return "SX_E_UNKNOWN";
+    }
+}
+
+const char* sx_last_error(void) { return g_last_error.c_str(); }
+
+int sx_version(void) { return (0 << 16) | 1; }
+
+void sx_opts_default(sx_opts* o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof(*o));
+    o->overflow_threshold = 64;
+    o->sep_small = 32;
+    o->sep_large = 128;
+    o->sep_huge = 16384;
+    o->alpha = 14.f;
+    o->beta = 24.f;
+    o->force_filter = 0;
+    o->force_dir = 0;
+    o->fusion = 1;
+    o->max_iters = 0;
+    o->trace = nullptr;
+    o->trace_cap = 0;
+}
+
+sx_status sx_ctx_create(int device, void* cuda_stream, sx_ctx* out) {
+    if (!out) return sxh::fail(SX_E_INVALID, "sx_ctx_create: out == NULL");
+    *out = nullptr;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return sxh::fail(SX_E_CUDA, "sx_ctx_create: no CUDA device (there is no CPU fallback)");
+    }
+    if (device < 0 || device >= ndev) return sxh::fail(SX_E_INVALID, "sx_ctx_create: bad device index");
+    SX_CU(cudaSetDevice(device));
+    sx_ctx c = new sx_ctx_s();
+    c->device = device;
+    c->stream = (cudaStream_t)cuda_stream;
+    if ((e = cudaGetDeviceProperties(&c->prop, device)) != cudaSuccess) {
+        delete c;
+        return sxh::cuda_fail(e, "cudaGetDeviceProperties");
+    }
+    if (c->prop.major < 10) {
+        delete c;
+        return sxh::fail(SX_E_CUDA, "sx_ctx_create: device is not sm_100 (this library is built for sm_100a only)");
+    }
+    if (!c->prop.cooperativeLaunch) {
+        delete c;
+        return sxh::fail(SX_E_BARRIER, "sx_ctx_create: device lacks cooperative launch");
+    }
+    cudaEvent_t* evs[] = {&c->ev0, &c->ev1, &c->evk0, &c->evk1};
+    for (auto* ev : evs) {
+        if ((e = cudaEventCreate(ev)) != cudaSuccess) {
+            sx_ctx_destroy(c);
+            return sxh::cuda_fail(e, "cudaEventCreate");
+        }
+    }
+    if ((e = cudaMallocHost(&c->h_ctl, sizeof(Ctl))) != cudaSuccess) {
+        sx_ctx_destroy(c);
+        return sxh::cuda_fail(e, "cudaMallocHost");
+    }
+    std::memset(c->h_ctl, 0, sizeof(Ctl));
+    *out = c;
+    return SX_OK;
+}
+
+void sx_ctx_destroy(sx_ctx c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->evk0) cudaEventDestroy(c->evk0);
+    if (c->evk1) cudaEventDestroy(c->evk1);
+    if (c->h_ctl) cudaFreeHost(c->h_ctl);
+    delete c;
+}
+
+sx_status sx_ctx_info(sx_ctx c, sx_device_info* out);
+
+}  // extern "C"

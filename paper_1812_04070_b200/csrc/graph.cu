@@ -1,0 +1,219 @@
+// graph.cu — graph residency: upload, validation, degree
+// arrays, the in-degree>0 bitmap, and the per-graph workspace of the engine.
+//
+// Layout in HBM: row_ptr u64[n+1], col u32[m],
+// weights u8 or u32 [m] (u32 ids, u64 indices); for symmetric graphs
+// the CSR serves as CSC.  Workspace: 2 list buffers of 4 class regions
+// x n u32, 3 rotating frontier bitmaps + 1 auxiliary bitmap, the control block,
+// 4 state arrays of n x 4 B.
+#include <cstring>
+
+#include "internal.h"
+
+using namespace sx;
+
+namespace {
+
+__global__ void k_validate(const uint64_t* rp, const uint32_t* ci, uint64_t n, uint64_t m, const void* w,
+                           uint32_t wbytes, uint32_t* flags) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+    uint32_t f = 0;
+    if (t == 0 && (rp[0] != 0 || rp[n] != m)) f |= 4;
+    for (uint64_t i = t; i < n; i += T) {
+        const uint64_t a = rp[i], b = rp[i + 1];
+        if (a > b) f |= 1;
+        if (b - a >= 0xFFFFFFFFull) f |= 16;
+    }
+    for (uint64_t e = t; e < m; e += T) {
+        if (ci[e] >= n) f |= 2;
+        if (w) {
+            const uint32_t x = wbytes == 1 ? ((const uint8_t*)w)[e] : ((const uint32_t*)w)[e];
+            if (x == 0) f |= 8;
+        }
+    }
+    if (f) atomicOr(flags, f);
+}
+
+__global__ void k_degrees(const uint64_t* rp, uint64_t n, uint32_t* deg) {
+    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += T)
+        deg[i] = (uint32_t)(rp[i + 1] - rp[i]);
+}
+
+__global__ void k_nz_bitmap(const uint32_t* deg, uint64_t n, uint64_t nwords, uint32_t* bm) {
+    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords; w += T) {
+        uint32_t x = 0;
+        for (int b = 0; b < 32; ++b) {
+            const uint64_t v = (w << 5) + b;
+            if (v < n && deg[v] > 0) x |= 1u << b;
+        }
+        bm[w] = x;
+    }
+}
+
+template <class T> sx_status dalloc(T** p, size_t count) {
+    cudaError_t e = cudaMalloc((void**)p, (count ? count : 1) * sizeof(T));
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        return sxh::cuda_fail(e, "cudaMalloc");
+    }
+    return SX_OK;
+}
+
+bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+sx_status sx_graph_upload(sx_ctx ctx, const sx_csr_desc* d, sx_graph* out) {
+    if (!out || !d) return sxh::fail(SX_E_INVALID, "sx_graph_upload: NULL argument");
+    *out = nullptr;
+    sx_status rc = sxh::check_ctx(ctx);
+    if (rc != SX_OK) return rc;
+    if (d->n >= 0xFFFFFFFFull) return sxh::fail(SX_E_INVALID, "sx_graph_upload: n >= 2^32-1 (0xFFFFFFFF is reserved)");
+    if (!d->row_ptr || (d->m && !d->col)) return sxh::fail(SX_E_INVALID, "sx_graph_upload: NULL row_ptr/col");
+    if (d->w && d->w_bytes != 1 && d->w_bytes != 4) return sxh::fail(SX_E_INVALID, "sx_graph_upload: w_bytes must be 1 or 4");
+    const bool directed = d->flags & SX_DIRECTED;
+    const bool devp = d->flags & SX_DEVICE_PTRS;
+    const bool borrow = devp && (d->flags & SX_BORROW) && aligned16(d->col) && (!directed || !d->csc_idx || aligned16(d->csc_idx));
+    cudaStream_t s = ctx->stream;
+    sx_graph g = new sx_graph_s();
+    g->ctx = ctx;
+    g->n = d->n;
+    g->m = d->m;
+    g->directed = directed;
+    g->wbytes = d->w ? d->w_bytes : 0;
+    g->borrowed = borrow;
+    const uint64_t n = d->n, m = d->m;
+    auto bail = [&](sx_status st) {
+        sx_graph_free(g);
+        return st;
+    };
+#define TRY(x)                          \
+    do {                                \
+        sx_status r__ = (x);            \
+        if (r__ != SX_OK) return bail(r__); \
+    } while (0)
+    auto take = [&](auto** dst, const auto* src, size_t count, size_t elem) -> sx_status {
+        if (borrow) {
+            *dst = (std::remove_pointer_t<decltype(dst)>)src;
+            return SX_OK;
+        }
+        sx_status r = dalloc((char**)dst, count * elem);
+        if (r != SX_OK) return r;
+        if (count) SX_CU(cudaMemcpyAsync(*dst, src, count * elem, cudaMemcpyDefault, s));
+        return SX_OK;
+    };
+    TRY(take(&g->rp, d->row_ptr, n + 1, 8));
+    TRY(take(&g->ci, d->col, m, 4));
+    if (d->w) TRY(take((char**)&g->w, (const char*)d->w, m, d->w_bytes));
+    if (directed) {
+        if (d->csc_ptr && d->csc_idx) {
+            uint64_t mi = 0;
+            if (devp) SX_CU(cudaMemcpy(&mi, d->csc_ptr + n, 8, cudaMemcpyDefault));
+            else mi = d->csc_ptr[n];
+            g->mi = mi;
+            TRY(take(&g->irp, d->csc_ptr, n + 1, 8));
+            TRY(take(&g->ici, d->csc_idx, mi, 4));
+            if (d->w && d->csc_w) TRY(take((char**)&g->iw, (const char*)d->csc_w, mi, d->w_bytes));
+            g->has_rev = true;
+        } else {
+            g->has_rev = false;
+            g->irp = g->rp;
+            g->ici = g->ci;
+            g->iw = g->w;
+            g->mi = m;
+        }
+    } else {
+        g->irp = g->rp;
+        g->ici = g->ci;
+        g->iw = g->w;
+        g->mi = m;
+    }
+    // validation (SPEC.md S:35-38 invariants) on the device
+    uint32_t* dflags = nullptr;
+    TRY(dalloc(&dflags, 1));
+    SX_CU(cudaMemsetAsync(dflags, 0, 4, s));
+    const int vb = 256, vg = 4 * ctx->prop.multiProcessorCount;
+    k_validate<<<vg, vb, 0, s>>>(g->rp, g->ci, n, m, g->w, g->wbytes, dflags);
+    if (directed && g->has_rev) k_validate<<<vg, vb, 0, s>>>(g->irp, g->ici, n, g->mi, g->iw, g->wbytes, dflags);
+    uint32_t hflags = 0;
+    SX_CU(cudaMemcpyAsync(&hflags, dflags, 4, cudaMemcpyDeviceToHost, s));
+    cudaError_t e = cudaStreamSynchronize(s);
+    cudaFree(dflags);
+    if (e != cudaSuccess) return bail(sxh::cuda_fail(e, "graph validation"));
+    if (hflags & 7) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "sx_graph_upload: invalid CSR (%s%s%s)", (hflags & 1) ? "row_ptr decreasing; " : "",
+                 (hflags & 2) ? "col >= n; " : "", (hflags & 4) ? "row_ptr[0] != 0 or row_ptr[n] != m" : "");
+        return bail(sxh::fail(SX_E_INVALID, buf));
+    }
+    if (hflags & 16) return bail(sxh::fail(SX_E_INVALID, "sx_graph_upload: a degree exceeds 2^32-2"));
+    g->has_zero_w = (hflags & 8) != 0;
+    // degrees + in-degree>0 bitmap
+    g->nwords = ((n + 31) / 32 + TILE_WORDS - 1) / TILE_WORDS * TILE_WORDS;
+    if (g->nwords == 0) g->nwords = TILE_WORDS;
+    TRY(dalloc(&g->dout, n));
+    k_degrees<<<vg, vb, 0, s>>>(g->rp, n, g->dout);
+    if (directed && g->has_rev) {
+        TRY(dalloc(&g->din, n));
+        k_degrees<<<vg, vb, 0, s>>>(g->irp, n, g->din);
+    } else {
+        g->din = g->dout;
+    }
+    TRY(dalloc(&g->nz_in, g->nwords));
+    k_nz_bitmap<<<vg, vb, 0, s>>>(g->din, n, g->nwords, g->nz_in);
+    // workspace
+    for (int i = 0; i < 2; ++i) TRY(dalloc(&g->lists[i], NCLS * (n ? n : 1)));
+    for (int i = 0; i < 3; ++i) TRY(dalloc(&g->bm[i], g->nwords));
+    TRY(dalloc(&g->aux_bm, g->nwords));
+    TRY(dalloc(&g->cta_cnt, NCLS * MAX_GRID));
+    TRY(dalloc((char**)&g->ctl, sizeof(Ctl)));
+    for (int i = 0; i < 4; ++i) TRY(dalloc(&g->st[i], n));
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return bail(sxh::cuda_fail(e, "graph upload"));
+#undef TRY
+    *out = g;
+    return SX_OK;
+}
+
+sx_status sx_graph_info(sx_graph g, uint64_t* n, uint64_t* m, uint64_t* v_begin, uint64_t* v_end) {
+    if (!g) return sxh::fail(SX_E_INVALID, "sx_graph_info: NULL graph");
+    if (n) *n = g->n;
+    if (m) *m = g->m;
+    if (v_begin) *v_begin = 0;
+    if (v_end) *v_end = g->n;
+    return SX_OK;
+}
+
+void sx_graph_free(sx_graph g) {
+    if (!g) return;
+    cudaSetDevice(g->ctx->device);
+    cudaStreamSynchronize(g->ctx->stream);
+    if (!g->borrowed) {
+        if (g->irp && g->irp != g->rp) cudaFree(g->irp);
+        if (g->ici && g->ici != g->ci) cudaFree(g->ici);
+        if (g->iw && g->iw != g->w) cudaFree(g->iw);
+        cudaFree(g->rp);
+        cudaFree(g->ci);
+        if (g->w) cudaFree(g->w);
+    }
+    if (g->din && g->din != g->dout) cudaFree(g->din);
+    cudaFree(g->dout);
+    cudaFree(g->nz_in);
+    for (auto* p : g->lists) cudaFree(p);
+    for (auto* p : g->bm) cudaFree(p);
+    cudaFree(g->aux_bm);
+    cudaFree(g->cta_cnt);
+    cudaFree(g->ctl);
+    cudaFree(g->trace);
+    for (auto* p : g->st) cudaFree(p);
+    cudaFree(g->hacc);
+    cudaFree(g->dstate);
+    delete g;
+}
+
+}  // extern "C"

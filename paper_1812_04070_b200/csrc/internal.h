@@ -1,0 +1,96 @@
+// internal.h — host-side structures shared by the C-ABI translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/simdx.h"
+#include "engine.cuh"
+
+struct sx_ctx_s {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaDeviceProp prop{};
+    bool poisoned = false;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, evk0 = nullptr, evk1 = nullptr;
+    sx::Ctl* h_ctl = nullptr;  // pinned host mirror of the control block
+};
+
+struct sx_graph_s {
+    sx_ctx ctx = nullptr;
+    uint64_t n = 0, m = 0, mi = 0;
+    bool directed = false, has_rev = true;
+    uint32_t wbytes = 0;
+    bool borrowed = false;
+    bool has_zero_w = false;
+    // device graph arrays
+    uint64_t* rp = nullptr;
+    uint32_t* ci = nullptr;
+    void* w = nullptr;
+    uint64_t* irp = nullptr;
+    uint32_t* ici = nullptr;
+    void* iw = nullptr;
+    uint32_t* dout = nullptr;
+    uint32_t* din = nullptr;
+    uint32_t* nz_in = nullptr;
+    // workspace
+    uint64_t nwords = 0;
+    uint32_t* lists[2] = {nullptr, nullptr};
+    uint32_t* bm[3] = {nullptr, nullptr, nullptr};
+    uint32_t* aux_bm = nullptr;   // BFS visited / SSSP far pile
+    uint32_t* cta_cnt = nullptr;
+    sx::Ctl* ctl = nullptr;
+    sx::TraceRec* trace = nullptr;
+    uint32_t trace_cap = 0;
+    uint32_t* st[4] = {nullptr, nullptr, nullptr, nullptr};  // 4N-byte state arrays
+    double* hacc = nullptr;       // n doubles, pull-all huge accumulators (lazy)
+    double* dstate = nullptr;     // 2n doubles, BP beliefs (lazy)
+};
+
+namespace sxh {
+
+sx_status fail(sx_status st, const std::string& msg);
+sx_status cuda_fail(cudaError_t e, const char* what);
+#define SX_CU(call)                                              \
+    do {                                                         \
+        cudaError_t e__ = (call);                                \
+        if (e__ != cudaSuccess) return sxh::cuda_fail(e__, #call); \
+    } while (0)
+
+sx::DevGraph dev_graph(const sx_graph g);
+// Fill the scheduling parameters common to every persistent kernel.
+sx::Sched make_sched(const sx_graph g, const sx_opts& o);
+sx_opts resolve_opts(const sx_opts* o);
+
+// Cooperative launch of a persistent kernel with occupancy x SMs CTAs (Eq. 1
+// generalised).  Returns SX_E_BARRIER when co-residency is impossible.
+sx_status coop_launch(sx_graph g, const void* fn, void** args, int* grid_out);
+int coop_grid(sx_graph g, const void* fn);
+
+// Device counters of one direction (deltas of the control block's st_* fields).
+struct Counters {
+    double entries = 0, edges = 0, reached = 0, scanned = 0, iters = 0, pull = 0, ballot = 0;
+};
+using BytesFn = double (*)(const sx_graph g, const Counters& c);
+
+// Per-run bookkeeping: events, trace copy-out, stats.
+struct Run {
+    sx_graph g;
+    sx_opts o;
+    sx_stats* st;
+    float ms_push = 0, ms_pull = 0;
+    uint32_t launches = 0, launches_push = 0, launches_pull = 0;
+    Counters c_push, c_pull;
+    sx::Ctl prev{};
+    sx_status begin();
+    // Launch one persistent kernel (timed), then read back the control block.
+    sx_status launch(const void* fn, void** args, bool pull);
+    sx_status end(BytesFn bytes);
+};
+
+sx_status copy_out(sx_graph g, void* dst, const void* src_dev, size_t bytes);
+sx_status copy_in(sx_graph g, void* dst_dev, const void* src, size_t bytes);
+sx_status check_ctx(sx_ctx c);
+
+}  // namespace sxh

@@ -1,0 +1,222 @@
+// kcore.cu — k-core / coreness as an ACC algorithm (
+// SURVEY.md §8(c) readings 6, 7).
+//
+// Peeling by levels k = 0, 1, 2, ...: at a level start the ballot filter
+// (coalesced scan + __ballot_sync) selects the alive vertices with
+// residual degree <= k (their coreness is k); each BSP sub-round then pushes
+// the removals:
+//   Active  : vertices removed in the previous sub-round
+//   Compute : update_{v->u} = -1 for every alive neighbour u
+//   Combine : aggregation (sum) with atomicSub on the residual degree; the one
+//             thread that sees the residual cross k+1 -> k removes u (coreness k)
+//             and records it — exactly once, so results are order-independent.
+// When a level empties, k jumps to the minimum residual degree among the alive
+// vertices (a grid min-reduction).  k > 0 ("fixed k") runs the single level
+// k-1 and reports the survivors; k = 0 runs the full decomposition.
+// k-Core uses the ballot filter in its first iterations and online afterwards
+// — the same JIT controller as BFS/SSSP decides.
+#include "internal.h"
+
+namespace sx {
+
+struct KcoreP {
+    DevGraph g;
+    Sched s;
+    uint32_t* res;   // residual degree
+    uint32_t* core;  // coreness, INF while alive
+    uint32_t kfix;   // 0 = decomposition
+};
+
+__global__ void kcore_init(KcoreP p) {
+    Ctl* c = p.s.ctl;
+    for (int i = 0; i < 3; ++i) reset_line(&c->line[i]);
+    for (int i = 0; i < NCLS; ++i) c->cur_count[i] = 0;
+    c->k = 0;
+    c->iter = 0;
+    c->done = 0;
+    c->dir = DIR_PUSH;
+}
+
+__global__ void k_copy_deg(const uint32_t* deg, uint64_t n, uint32_t* res) {
+    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += T) res[i] = deg[i];
+}
+
+struct LevelPred {
+    const uint32_t* core;
+    const uint32_t* res;
+    uint32_t k;
+    __device__ __forceinline__ bool operator()(uint64_t v) const { return core[v] == INF && res[v] <= k; }
+};
+
+__global__ void __launch_bounds__(BLOCK, 4) kcore_push(KcoreP p) {
+    Ctl* c = p.s.ctl;
+    if (vload(&c->done)) return;
+    const uint64_t n = p.g.n;
+    uint32_t it = vload(&c->iter);
+    uint32_t k = vload(&c->k);
+    uint32_t cnt[NCLS];
+    for (int i = 0; i < NCLS; ++i) cnt[i] = vload(&c->cur_count[i]);
+    Stats st;
+    uint32_t done = 0;
+    bool level_started = it > 0 || sum4(cnt) > 0;
+    for (;;) {
+        CntLine* nx = &c->line[(it + 1) % 3];
+        if (sum4(cnt) == 0) {
+            // ---- level start: min residual degree over alive vertices
+            if (p.kfix && level_started) {
+                done = 1;
+                break;
+            }
+            uint32_t mn = INF;
+            uint64_t alive = 0;
+            for (uint64_t v = gtid(); v < n; v += gthreads()) {
+                if (p.core[v] == INF) {
+                    mn = min(mn, p.res[v]);
+                    ++alive;
+                }
+            }
+            mn = block_min(mn);
+            {
+                uint64_t a[1] = {alive};
+                block_sum<1>(a);
+                alive = a[0];
+            }
+            if (threadIdx.x == 0) {
+                if (mn != INF) atomicMin(&nx->minv, mn);
+                if (alive) atomicAdd(&nx->alive, (unsigned int)alive);
+            }
+            st.scanned += n;
+            if (!grid_sync(c)) return;
+            mn = vload(&nx->minv);
+            const uint32_t nalive = vload(&nx->alive);
+            if (nalive == 0) {
+                done = 1;
+                break;
+            }
+            if (p.kfix) {
+                if (mn >= p.kfix) {
+                    done = 1;
+                    break;
+                }
+                k = p.kfix - 1;
+            } else {
+                k = max(k, mn);
+            }
+            level_started = true;
+            // ---- ballot filter selects the level's seeds; their coreness is k
+            ++st.ballot;
+            st.scanned += n;
+            BallotWords<LevelPred> src{LevelPred{p.core, p.res, k}, n};
+            if (!ballot_filter(src, p.s, BallotOut{p.s.lists[it & 1], n, p.g.dout}, cnt,
+                               [&](uint32_t v, uint32_t) { p.core[v] = k; }))
+                return;
+            if (!grid_sync(c)) return;
+            trace_put(p.s, it, DIR_PUSH, 1u, cnt, sum4(cnt), 0, k);
+        }
+        // ---- one sub-round: removals push -1 to alive neighbours
+        if (lead()) reset_line(&c->line[(it + 2) % 3]);
+        clear_bitmap(p.s.bm[(it + 2) % 3], p.s.nwords);
+        uint32_t* nlists = p.s.lists[(it + 1) & 1];
+        uint32_t* nbm = p.s.bm[(it + 1) % 3];
+        uint64_t edges = 0;
+        const uint32_t kk = k;
+        for_tasks(p.s.lists[it & 1], n, cnt, [&](uint32_t v, uint64_t rank, uint64_t size, uint32_t) {
+            const uint64_t beg = __ldg(p.g.rp + v), end = __ldg(p.g.rp + v + 1);
+            for_edges(p.g.ci, beg, end, rank, size, [&](uint64_t, uint32_t u) {
+                ++edges;
+                if (p.core[u] != INF) return;
+                const uint32_t old = atomicSub(p.res + u, 1u);
+                if (old == kk + 1) {
+                    p.core[u] = kk;
+                    bm_set(nbm, u);
+                    online_record(nx, nlists, n, p.s.online_cap, u, cls_of(__ldg(p.g.dout + u), p.s));
+                }
+            });
+        });
+        st.edges += edges;
+        if (lead()) st.entries += sum4(cnt);
+        if (!grid_sync(c)) return;
+        uint32_t ncnt[NCLS];
+        for (int i = 0; i < NCLS; ++i) ncnt[i] = vload(&nx->cnt[i]);
+        const uint64_t nf = sum4(ncnt);
+        bool overflow = false;
+        for (int i = 0; i < NCLS; ++i) overflow |= ncnt[i] > p.s.online_cap;
+        if (p.s.force_filter == 2) overflow = true;
+        ++it;
+        ++st.iters;
+        trace_put(p.s, it, DIR_PUSH, overflow ? 1u : 0u, ncnt, nf, 0, k);
+        if (nf > 0 && overflow) {
+            ++st.ballot;
+            st.scanned += p.s.nwords * 32;
+            if (!ballot_filter(BitmapWords{nbm}, p.s, BallotOut{p.s.lists[it & 1], n, p.g.dout}, cnt)) return;
+            if (!grid_sync(c)) return;
+        } else {
+            for (int i = 0; i < NCLS; ++i) cnt[i] = ncnt[i];
+        }
+        if (p.s.max_iters && it >= p.s.max_iters) {
+            done = 1;
+            break;
+        }
+        if (!p.s.fusion) break;
+    }
+    flush_stats(c, st);
+    if (lead()) {
+        c->iter = it;
+        c->k = k;
+        c->done = done;
+        for (int i = 0; i < NCLS; ++i) c->cur_count[i] = cnt[i];
+        c->launch += 1;
+    }
+}
+
+__global__ void k_kcore_out(const uint32_t* core, uint64_t n, uint32_t kfix, uint32_t* out) {
+    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += T)
+        out[i] = kfix ? (core[i] == INF ? 1u : 0u) : core[i];
+}
+
+}  // namespace sx
+
+using namespace sx;
+
+// Algorithmic bytes: per list entry 4 B list + 16 B row_ptr pair;
+// per edge 4 B col + 4 B core(u) + 4 B residual RMW; level scans 8 B (core +
+// residual) per scanned vertex; per iteration one bitmap clear (n/8).
+static double kcore_bytes(const sx_graph g, const sxh::Counters& c) {
+    return 20.0 * c.entries + 12.0 * c.edges + 8.0 * c.scanned + c.iters * (double)g->n / 8.0;
+}
+
+extern "C" sx_status sx_kcore(sx_graph g, uint32_t k, const sx_opts* opts, uint32_t* core_out, sx_stats* stats) {
+    if (!g || !core_out) return sxh::fail(SX_E_INVALID, "sx_kcore: NULL graph or core_out");
+    sx_status rc = sxh::check_ctx(g->ctx);
+    if (rc != SX_OK) return rc;
+    if (g->directed) return sxh::fail(SX_E_INVALID, "sx_kcore: k-core is defined on undirected graphs");
+    if (g->n == 0) return SX_OK;
+    sxh::Run run{g, sxh::resolve_opts(opts), stats};
+    cudaStream_t s = g->ctx->stream;
+    KcoreP p;
+    if ((rc = run.begin()) != SX_OK) return rc;
+    p.g = sxh::dev_graph(g);
+    p.s = sxh::make_sched(g, run.o);
+    p.res = g->st[0];
+    p.core = g->st[1];
+    p.kfix = k;
+    SX_CU(cudaMemsetAsync(p.core, 0xFF, g->n * 4, s));
+    for (int i = 0; i < 3; ++i) SX_CU(cudaMemsetAsync(p.s.bm[i], 0, g->nwords * 4, s));
+    const int eg = 4 * g->ctx->prop.multiProcessorCount;
+    k_copy_deg<<<eg, 256, 0, s>>>(g->dout, g->n, p.res);
+    kcore_init<<<1, 1, 0, s>>>(p);
+    SX_CU(cudaGetLastError());
+    void* args[] = {&p};
+    g->ctx->h_ctl->done = 0;
+    for (;;) {
+        if ((rc = run.launch((const void*)kcore_push, args, false)) != SX_OK) return rc;
+        if (g->ctx->h_ctl->done) break;
+    }
+    if ((rc = run.end(kcore_bytes)) != SX_OK) return rc;
+    uint32_t* tmp = g->st[2];
+    k_kcore_out<<<eg, 256, 0, s>>>(p.core, g->n, k, tmp);
+    SX_CU(cudaGetLastError());
+    return sxh::copy_out(g, core_out, tmp, g->n * 4);
+}

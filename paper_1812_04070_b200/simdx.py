@@ -1,0 +1,325 @@
+"""ctypes binding of include/simdx.h — argument marshalling only.
+
+Every step of the hot path runs in libsimdx.so (hand-written sm_100a CUDA);
+this module only converts numpy arrays / torch tensors to pointers and status
+codes to exceptions.  There is NO fallback: if the extension is missing this
+module raises at import time, and on a machine without a B200 every call
+returns SX_E_CUDA.
+
+Function names follow the C ABI (sx_ctx_create, sx_graph_upload, sx_bfs, ...);
+`Context` / `Graph` are thin conveniences over them.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsimdx.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build the CUDA extension first "
+                      "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback")
+_lib = ctypes.CDLL(LIB_PATH)
+
+# ---------------------------------------------------------------- constants
+SX_OK, SX_E_INVALID, SX_E_OOM, SX_E_CUDA, SX_E_NCCL, SX_E_NO_REVERSE, SX_E_WEIGHT, SX_E_BARRIER, SX_E_STATE = range(9)
+SX_DIRECTED, SX_DEVICE_PTRS, SX_BORROW = 1, 2, 4
+INF = 0xFFFFFFFF
+
+_u64, _u32, _i32, _f32, _vp = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int32, ctypes.c_float, ctypes.c_void_p
+
+
+class sx_csr_desc(ctypes.Structure):
+    _fields_ = [("n", _u64), ("m", _u64), ("row_ptr", _vp), ("col", _vp), ("w", _vp), ("w_bytes", _u32),
+                ("csc_ptr", _vp), ("csc_idx", _vp), ("csc_w", _vp), ("flags", _u32)]
+
+
+class sx_trace_rec(ctypes.Structure):
+    _fields_ = [("iter", _u32), ("dir", _u32), ("filter", _u32), ("launch", _u32), ("n_active", _u32 * 4),
+                ("n_frontier", _u64), ("m_active", _u64), ("aux", _u64)]
+
+
+class sx_opts(ctypes.Structure):
+    _fields_ = [("overflow_threshold", _u32), ("sep_small", _u32), ("sep_large", _u32), ("sep_huge", _u32),
+                ("alpha", _f32), ("beta", _f32), ("force_filter", _i32), ("force_dir", _i32), ("fusion", _i32),
+                ("max_iters", _u32), ("trace", ctypes.POINTER(sx_trace_rec)), ("trace_cap", _u64)]
+
+
+class sx_stats(ctypes.Structure):
+    _fields_ = [("iterations", _u32), ("launches", _u32), ("ballot_iters", _u32), ("pull_iters", _u32),
+                ("edges_examined", _u64), ("vertices_scanned", _u64), ("list_entries", _u64),
+                ("bytes_model", ctypes.c_double), ("ms", ctypes.c_double), ("ms_push", ctypes.c_double),
+                ("ms_pull", ctypes.c_double), ("bytes_push", ctypes.c_double), ("bytes_pull", ctypes.c_double),
+                ("launches_push", _u32), ("launches_pull", _u32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class sx_device_info(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_int) for k in ("device", "sm_count", "cc_major", "cc_minor", "regs_per_sm",
+                                            "max_threads_per_sm", "block_threads", "push_ctas_per_sm",
+                                            "pull_ctas_per_sm", "push_regs", "pull_regs")]
+
+
+_P = ctypes.POINTER
+_lib.sx_status_str.argtypes = [ctypes.c_int]
+_lib.sx_status_str.restype = ctypes.c_char_p
+_lib.sx_last_error.argtypes = []
+_lib.sx_last_error.restype = ctypes.c_char_p
+_lib.sx_version.restype = ctypes.c_int
+_lib.sx_ctx_create.argtypes = [ctypes.c_int, _vp, _P(_vp)]
+_lib.sx_ctx_destroy.argtypes = [_vp]
+_lib.sx_ctx_destroy.restype = None
+_lib.sx_ctx_info.argtypes = [_vp, _P(sx_device_info)]
+_lib.sx_graph_upload.argtypes = [_vp, _P(sx_csr_desc), _P(_vp)]
+_lib.sx_graph_info.argtypes = [_vp, _P(_u64), _P(_u64), _P(_u64), _P(_u64)]
+_lib.sx_graph_free.argtypes = [_vp]
+_lib.sx_graph_free.restype = None
+_lib.sx_opts_default.argtypes = [_P(sx_opts)]
+_lib.sx_opts_default.restype = None
+_lib.sx_bfs.argtypes = [_vp, _u32, _P(sx_opts), _vp, _P(sx_stats)]
+_lib.sx_sssp.argtypes = [_vp, _u32, _u32, _P(sx_opts), _vp, _P(sx_stats)]
+_lib.sx_pagerank.argtypes = [_vp, _f32, _u32, _P(sx_opts), _vp, _P(sx_stats)]
+_lib.sx_kcore.argtypes = [_vp, _u32, _P(sx_opts), _vp, _P(sx_stats)]
+_lib.sx_spmv.argtypes = [_vp, _vp, _u32, _P(sx_opts), _vp, _P(sx_stats)]
+_lib.sx_bp.argtypes = [_vp, _vp, _u32, _P(sx_opts), _vp, _P(sx_stats)]
+for _f in ("sx_ctx_create", "sx_ctx_info", "sx_graph_upload", "sx_graph_info", "sx_bfs", "sx_sssp", "sx_pagerank",
+           "sx_kcore", "sx_spmv", "sx_bp"):
+    getattr(_lib, _f).restype = ctypes.c_int
+
+EXPORTED = ["sx_status_str", "sx_last_error", "sx_version", "sx_ctx_create", "sx_ctx_destroy", "sx_ctx_info",
+            "sx_graph_upload", "sx_graph_info", "sx_graph_free", "sx_opts_default", "sx_bfs", "sx_sssp",
+            "sx_pagerank", "sx_kcore", "sx_spmv", "sx_bp"]
+
+
+class SimdxError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        detail = _lib.sx_last_error().decode()
+        super().__init__(f"{where}: {_lib.sx_status_str(status).decode()} — {detail}")
+
+
+def _check(rc: int, where: str):
+    if rc != SX_OK:
+        raise SimdxError(rc, where)
+
+
+# ---------------------------------------------------------------- pointer helpers
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def _ptr(x) -> Optional[int]:
+    if x is None:
+        return None
+    if _is_torch(x):
+        assert x.is_contiguous()
+        return x.data_ptr()
+    assert isinstance(x, np.ndarray) and x.flags["C_CONTIGUOUS"], "host arrays must be C-contiguous numpy arrays"
+    return x.ctypes.data
+
+
+def _on_device(x) -> bool:
+    return _is_torch(x) and x.is_cuda
+
+
+# ---------------------------------------------------------------- C-named wrappers
+def sx_version() -> int:
+    return _lib.sx_version()
+
+
+def sx_status_str(s: int) -> str:
+    return _lib.sx_status_str(s).decode()
+
+
+def sx_last_error() -> str:
+    return _lib.sx_last_error().decode()
+
+
+def sx_opts_default() -> sx_opts:
+    o = sx_opts()
+    _lib.sx_opts_default(ctypes.byref(o))
+    return o
+
+
+def make_opts(**kw) -> sx_opts:
+    o = sx_opts_default()
+    for k, v in kw.items():
+        if k == "trace":
+            continue
+        setattr(o, k, v)
+    return o
+
+
+def sx_ctx_create(device: int = 0, stream: int = 0):
+    h = _vp()
+    _check(_lib.sx_ctx_create(device, _vp(stream) if stream else None, ctypes.byref(h)), "sx_ctx_create")
+    return h
+
+
+def sx_ctx_destroy(ctx) -> None:
+    _lib.sx_ctx_destroy(ctx)
+
+
+def sx_ctx_info(ctx) -> dict:
+    info = sx_device_info()
+    _check(_lib.sx_ctx_info(ctx, ctypes.byref(info)), "sx_ctx_info")
+    return {k: getattr(info, k) for k, _ in info._fields_}
+
+
+def sx_graph_upload(ctx, n, row_ptr, col, w=None, csc_ptr=None, csc_idx=None, csc_w=None, directed=False,
+                    borrow=False):
+    """row_ptr u64[n+1], col u32[m], w u8/u32[m] or None — numpy (host) or torch CUDA tensors (device)."""
+    dev = _on_device(row_ptr)
+    d = sx_csr_desc()
+    d.n = n
+    d.m = int(row_ptr[-1])
+    d.row_ptr, d.col, d.w = _ptr(row_ptr), _ptr(col), _ptr(w)
+    d.w_bytes = 0 if w is None else w.element_size() if _is_torch(w) else w.dtype.itemsize
+    d.csc_ptr, d.csc_idx, d.csc_w = _ptr(csc_ptr), _ptr(csc_idx), _ptr(csc_w)
+    d.flags = (SX_DIRECTED if directed else 0) | (SX_DEVICE_PTRS if dev else 0) | (SX_BORROW if borrow else 0)
+    h = _vp()
+    _check(_lib.sx_graph_upload(ctx, ctypes.byref(d), ctypes.byref(h)), "sx_graph_upload")
+    return h
+
+
+def sx_graph_free(g) -> None:
+    _lib.sx_graph_free(g)
+
+
+def sx_graph_info(g):
+    a, b, c, d = _u64(), _u64(), _u64(), _u64()
+    _check(_lib.sx_graph_info(g, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), ctypes.byref(d)),
+           "sx_graph_info")
+    return a.value, b.value, c.value, d.value
+
+
+def _run(fn, name, g, out, opts, args_before, args_after=()):
+    st = sx_stats()
+    o = opts if opts is not None else sx_opts_default()
+    _check(fn(g, *args_before, ctypes.byref(o), *args_after, _ptr(out), ctypes.byref(st)), name)
+    return st
+
+
+def sx_bfs(g, src, opts, level_out):
+    return _run(_lib.sx_bfs, "sx_bfs", g, level_out, opts, (src,))
+
+
+def sx_sssp(g, src, delta, opts, dist_out):
+    return _run(_lib.sx_sssp, "sx_sssp", g, dist_out, opts, (src, delta))
+
+
+def sx_pagerank(g, damping, iters, opts, rank_out):
+    return _run(_lib.sx_pagerank, "sx_pagerank", g, rank_out, opts, (damping, iters))
+
+
+def sx_kcore(g, k, opts, core_out):
+    return _run(_lib.sx_kcore, "sx_kcore", g, core_out, opts, (k,))
+
+
+def sx_spmv(g, x, iters, opts, y_out):
+    return _run(_lib.sx_spmv, "sx_spmv", g, y_out, opts, (_ptr(x), iters))
+
+
+def sx_bp(g, prior, iters, opts, out):
+    return _run(_lib.sx_bp, "sx_bp", g, out, opts, (_ptr(prior), iters))
+
+
+# ---------------------------------------------------------------- conveniences
+class Context:
+    def __init__(self, device: int = 0, stream: int = 0):
+        self.h = sx_ctx_create(device, stream)
+
+    def info(self) -> dict:
+        return sx_ctx_info(self.h)
+
+    def upload(self, csr) -> "Graph":
+        """Upload a simgen.CSR-like object (fields n,row_ptr,col,w,directed,csc_*)."""
+        h = sx_graph_upload(self.h, csr.n, csr.row_ptr, csr.col, csr.w,
+                            getattr(csr, "csc_ptr", None), getattr(csr, "csc_idx", None),
+                            getattr(csr, "csc_w", None), bool(getattr(csr, "directed", False)))
+        return Graph(self, h, csr.n)
+
+    def close(self):
+        if self.h:
+            sx_ctx_destroy(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+class Graph:
+    def __init__(self, ctx: Context, h, n: int):
+        self.ctx, self.h, self.n = ctx, h, n
+
+    def free(self):
+        if self.h:
+            sx_graph_free(self.h)
+            self.h = None
+
+    def _opts(self, kw):
+        trace_cap = kw.pop("trace_cap", 0)
+        o = make_opts(**kw)
+        buf = None
+        if trace_cap:
+            buf = (sx_trace_rec * trace_cap)()
+            o.trace = ctypes.cast(buf, ctypes.POINTER(sx_trace_rec))
+            o.trace_cap = trace_cap
+        return o, buf
+
+    @staticmethod
+    def _trace(buf, st):
+        if buf is None:
+            return None
+        recs = []
+        for r in buf:
+            if r.iter == 0:
+                break
+            recs.append(dict(iter=r.iter, dir=r.dir, filter=r.filter, launch=r.launch, n_active=list(r.n_active),
+                             n_frontier=r.n_frontier, m_active=r.m_active, aux=r.aux))
+        return recs
+
+    def bfs(self, src: int, out=None, **kw):
+        out = np.empty(self.n, np.uint32) if out is None else out
+        o, buf = self._opts(dict(kw))
+        st = sx_bfs(self.h, src, o, out)
+        return out, st.as_dict(), self._trace(buf, st)
+
+    def sssp(self, src: int, delta: int = 0, out=None, **kw):
+        out = np.empty(self.n, np.uint32) if out is None else out
+        o, buf = self._opts(dict(kw))
+        st = sx_sssp(self.h, src, delta, o, out)
+        return out, st.as_dict(), self._trace(buf, st)
+
+    def pagerank(self, damping: float = 0.85, iters: int = 20, out=None, **kw):
+        out = np.empty(self.n, np.float32) if out is None else out
+        o, buf = self._opts(dict(kw))
+        st = sx_pagerank(self.h, damping, iters, o, out)
+        return out, st.as_dict(), self._trace(buf, st)
+
+    def kcore(self, k: int = 0, out=None, **kw):
+        out = np.empty(self.n, np.uint32) if out is None else out
+        o, buf = self._opts(dict(kw))
+        st = sx_kcore(self.h, k, o, out)
+        return out, st.as_dict(), self._trace(buf, st)
+
+    def spmv(self, x, iters: int = 1, out=None, **kw):
+        out = np.empty(self.n, np.float32) if out is None else out
+        o, buf = self._opts(dict(kw))
+        st = sx_spmv(self.h, x, iters, o, out)
+        return out, st.as_dict(), self._trace(buf, st)
+
+    def bp(self, prior, iters: int = 10, out=None, **kw):
+        out = np.empty(self.n, np.float32) if out is None else out
+        o, buf = self._opts(dict(kw))
+        st = sx_bp(self.h, prior, iters, o, out)
+        return out, st.as_dict(), self._trace(buf, st)

@@ -1,0 +1,229 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by
+element on the same seeded inputs (bit-exact for BFS / SSSP / k-core, the
+north_star tolerances for PageRank / SpMV / BP), across the forced modes of the
+JIT filter, the direction switch and the fusion."""
+import numpy as np
+import pytest
+
+import oracle
+import simgen
+
+pytestmark = pytest.mark.gpu
+INF = 0xFFFFFFFF
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import torch
+    from paper_1812_04070_b200 import simdx
+    assert torch.cuda.is_available()
+    torch.cuda.set_device(0)
+    c = simdx.Context(0, torch.cuda.current_stream().cuda_stream)
+    yield c
+    c.close()
+
+
+def up(ctx, g):
+    return ctx.upload(g)
+
+
+# ---------------------------------------------------------------- tiny adversarial graphs
+def tiny_graphs():
+    gs = {}
+    gs["single"] = simgen.from_edges(1, [], [])
+    gs["path"] = simgen.from_edges(6, [(i, i + 1) for i in range(5)], [3, 1, 4, 1, 5])
+    gs["two_comp"] = simgen.from_edges(7, [(0, 1), (1, 2), (3, 4), (4, 5), (5, 6)], [1, 2, 3, 4, 5])
+    gs["loops_dups"] = simgen.from_edges(5, [(0, 0), (0, 1), (0, 1), (1, 2), (2, 2), (2, 3), (3, 4), (3, 4)],
+                                         [9, 2, 7, 1, 1, 5, 3, 2])
+    gs["clique40"] = simgen.from_edges(40, [(a, b) for a in range(40) for b in range(a + 1, 40)],
+                                       [1 + (a * 7 + b) % 255 for a in range(40) for b in range(a + 1, 40)])
+    # bin boundaries: hubs of degree exactly 31/32/127/128 chained by a path
+    edges, w, base = [], [], 4
+    for i, d in enumerate((31, 32, 127, 128)):
+        for j in range(d - (1 if i in (0, 3) else 2)):
+            edges.append((i, base))
+            w.append(1 + j % 200)
+            base += 1
+    edges += [(0, 1), (1, 2), (2, 3)]
+    w += [5, 5, 5]
+    gs["bins"] = simgen.from_edges(base, edges, w)
+    # star with a hub of degree 100000 (grid-split "huge" class)
+    k = 100000
+    gs["star"] = simgen.from_edges(k + 1, [(0, i) for i in range(1, k + 1)], [1 + i % 255 for i in range(1, k + 1)])
+    return gs
+
+
+TINY = tiny_graphs()
+
+
+@pytest.mark.parametrize("name", sorted(TINY))
+def test_tiny_bfs_sssp_kcore(ctx, name):
+    g = TINY[name]
+    G = up(ctx, g)
+    try:
+        for src in sorted({0, g.n - 1, g.n // 2}):
+            lv, _, _ = G.bfs(src)
+            assert np.array_equal(lv, oracle.bfs(g, src)), (name, src)
+            for delta in (0, 4, 1024):
+                d, _, _ = G.sssp(src, delta)
+                assert np.array_equal(d, oracle.sssp(g, src)), (name, src, delta)
+        core, _, _ = G.kcore(0)
+        assert np.array_equal(core, oracle.coreness(g)), name
+        for k in (1, 2, 3, 32):
+            m, _, _ = G.kcore(k)
+            assert np.array_equal(m, oracle.kcore_mask(g, k)), (name, k)
+    finally:
+        G.free()
+
+
+def test_fig1_reconstruction_sssp(ctx):
+    g = simgen.from_edges(9, [(0, 1), (0, 3), (1, 2), (2, 3), (3, 4), (2, 5), (4, 5), (4, 6), (4, 7), (4, 8)],
+                          [5, 1, 2, 1, 3, 6, 2, 1, 4, 2])
+    G = up(ctx, g)
+    d, st, tr = G.sssp(0, 0, trace_cap=64)
+    assert list(d) == [0, 4, 2, 1, 4, 6, 5, 8, 6]
+    assert list(d) == list(oracle.sssp(g, 0))
+    G.free()
+
+
+# ---------------------------------------------------------------- BFS forced modes
+MODES = [dict(), dict(force_dir=1), dict(force_dir=2), dict(force_filter=1), dict(force_filter=2),
+         dict(fusion=0), dict(overflow_threshold=1), dict(overflow_threshold=1 << 20),
+         dict(sep_small=4, sep_large=8, sep_huge=64), dict(force_dir=2, fusion=0)]
+
+
+@pytest.fixture(scope="module")
+def rmat14():
+    return simgen.rmat(14, 16, seed=3, wmin=1, wmax=255)
+
+
+@pytest.mark.parametrize("mode", MODES, ids=[str(m) for m in MODES])
+def test_bfs_modes_rmat(ctx, rmat14, mode):
+    G = up(ctx, rmat14)
+    ref = oracle.bfs(rmat14, 0)
+    for src in (0, 77):
+        r = oracle.bfs(rmat14, src) if src else ref
+        lv, st, tr = G.bfs(src, trace_cap=256, **mode)
+        assert np.array_equal(lv, r), mode
+        # per-level frontier sizes = the oracle's level histogram (exact)
+        hist = oracle.level_histogram(r)
+        got = [t["n_frontier"] for t in tr]
+        assert got[:len(hist) - 1] == list(hist[1:]), (got, hist)
+    G.free()
+
+
+@pytest.mark.parametrize("mode", MODES[:6], ids=[str(m) for m in MODES[:6]])
+def test_sssp_kcore_modes_rmat(ctx, rmat14, mode):
+    G = up(ctx, rmat14)
+    m = {k: v for k, v in mode.items() if k != "force_dir"}
+    for delta in (0, 64, 1024):
+        d, _, _ = G.sssp(0, delta, **m)
+        assert np.array_equal(d, oracle.sssp(rmat14, 0)), (mode, delta)
+    core, _, _ = G.kcore(0, **m)
+    assert np.array_equal(core, oracle.coreness(rmat14)), mode
+    mk, _, _ = G.kcore(16, **m)
+    assert np.array_equal(mk, oracle.kcore_mask(rmat14, 16)), mode
+    G.free()
+
+
+# ---------------------------------------------------------------- pull-all (PR / SpMV / BP)
+def pr_check(r, o):
+    assert np.max(np.abs(r.astype(np.float64) - o) / o) <= 1e-5
+
+
+@pytest.mark.parametrize("name", ["rmat14", "star", "clique40", "directed"])
+def test_pagerank_spmv_bp(ctx, rmat14, name):
+    if name == "rmat14":
+        g = rmat14
+    elif name == "directed":
+        g = simgen.random_graph(3000, 20000, 5, wmin=1, wmax=255, symmetric=False)
+    else:
+        g = TINY[name]
+    G = up(ctx, g)
+    for T in (1, 20):
+        r, st, tr = G.pagerank(0.85, T, trace_cap=64)
+        pr_check(r, oracle.pagerank(g, 0.85, T))
+        assert tr[0]["filter"] == 1 and all(t["filter"] == 2 for t in tr[1:])  # ballot exactly in iteration 1
+    x = simgen.uniform_f32(7, 1, g.n, 0.0, 1.0)
+    y, _, _ = G.spmv(x, 3)
+    o = oracle.spmv(g, x)
+    assert np.all(np.abs(y - o) <= 1e-5 * np.maximum(np.abs(o), 1e-30))
+    p = simgen.bp_prior(11, g.n)
+    for T in (1, 10):
+        l, _, _ = G.bp(p, T)
+        o, at = oracle.bp(g, p, T, with_abs_terms=True)
+        assert np.all(np.abs(l - o) <= 1e-5 * (np.abs(o) + at) + 1e-6), T
+    G.free()
+
+
+# ---------------------------------------------------------------- errors and edge cases
+def test_errors(ctx):
+    from paper_1812_04070_b200 import simdx
+    g = simgen.from_edges(3, [(0, 1), (1, 2)])
+    G = up(ctx, g)
+    with pytest.raises(simdx.SimdxError) as e:
+        G.bfs(3)
+    assert e.value.status == simdx.SX_E_INVALID
+    with pytest.raises(simdx.SimdxError) as e:
+        G.sssp(0)
+    assert e.value.status == simdx.SX_E_WEIGHT
+    G.free()
+    gz = simgen.from_edges(3, [(0, 1), (1, 2)], [1, 0])
+    Gz = up(ctx, gz)
+    with pytest.raises(simdx.SimdxError) as e:
+        Gz.sssp(0)
+    assert e.value.status == simdx.SX_E_WEIGHT
+    Gz.free()
+    gd = simgen.from_edges(3, [(0, 1), (1, 2)], symmetric=False)
+    from paper_1812_04070_b200.simdx import sx_graph_upload, sx_graph_free, Graph
+    h = sx_graph_upload(ctx.h, gd.n, gd.row_ptr, gd.col, None, None, None, None, True)
+    Gd = Graph(ctx, h, gd.n)
+    with pytest.raises(simdx.SimdxError) as e:
+        Gd.pagerank()
+    assert e.value.status == simdx.SX_E_NO_REVERSE
+    with pytest.raises(simdx.SimdxError) as e:
+        Gd.kcore(0)
+    assert e.value.status == simdx.SX_E_INVALID
+    lv, _, _ = Gd.bfs(0, force_dir=1)
+    assert list(lv) == [0, 1, 2]
+    Gd.free()
+    bad = simgen.from_edges(3, [(0, 1)])
+    bad.col = bad.col.copy()
+    bad.col[0] = 7
+    with pytest.raises(simdx.SimdxError) as e:
+        up(ctx, bad)
+    assert e.value.status == simdx.SX_E_INVALID
+
+
+def test_directed_bfs_sssp_with_csc(ctx):
+    g = simgen.random_graph(2000, 12000, 9, wmin=1, wmax=255, symmetric=False)
+    G = up(ctx, g)
+    for mode in (dict(), dict(force_dir=2), dict(force_dir=1)):
+        lv, _, _ = G.bfs(0, **mode)
+        assert np.array_equal(lv, oracle.bfs(g, 0)), mode
+    d, _, _ = G.sssp(0, 128)
+    assert np.array_equal(d, oracle.sssp(g, 0))
+    G.free()
+
+
+def test_device_info(ctx):
+    info = ctx.info()
+    assert info["sm_count"] >= 100 and info["cc_major"] == 10
+    assert info["push_ctas_per_sm"] >= 1 and info["pull_ctas_per_sm"] >= 1
+    # Eq. 1 generalised: grid = ctas/SM x SMs fits the register file
+    assert info["push_ctas_per_sm"] * info["block_threads"] * info["push_regs"] <= info["regs_per_sm"]
+
+
+def test_device_pointers_in_and_out(ctx, rmat14):
+    import torch
+    from paper_1812_04070_b200.simdx import sx_graph_upload, Graph
+    dev = torch.device("cuda:0")
+    rp = torch.from_numpy(rmat14.row_ptr.view(np.int64)).to(dev)
+    ci = torch.from_numpy(rmat14.col.view(np.int32)).to(dev)
+    w = torch.from_numpy(rmat14.w).to(dev)
+    h = sx_graph_upload(ctx.h, rmat14.n, rp, ci, w, borrow=True)
+    G = Graph(ctx, h, rmat14.n)
+    out = torch.empty(rmat14.n, dtype=torch.int32, device=dev)
+    G.bfs(0, out=out)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), oracle.bfs(rmat14, 0))
+    G.free()
