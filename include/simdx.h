@@ -83,6 +83,15 @@ typedef struct {
 } sx_device_info;
 sx_status sx_ctx_info(sx_ctx ctx, sx_device_info* out);
 
+/*
+ * Barrier roofline: launch the persistent configuration and
+ * time `iters` back-to-back grid barriers with no work between them.
+ * us_per_barrier receives the mean latency in microseconds; ctas (nullable)
+ * the co-resident grid size used.  Errors: SX_E_INVALID (iters == 0 or NULL
+ * out), SX_E_BARRIER (watchdog), SX_E_CUDA.
+ */
+sx_status sx_barrier_bench(sx_ctx ctx, uint32_t iters, double* us_per_barrier, int* ctas);
+
 /* ------------------------------------------------------------------ graphs */
 enum {
     SX_DIRECTED = 1,    /* csc_* describe the in-neighbour rows; otherwise the graph is symmetric and CSR serves as CSC */
@@ -134,6 +143,7 @@ typedef struct {
     uint64_t n_frontier; /* |F'|: vertices activated by this iteration */
     uint64_t m_active;   /* sum of out-degrees of F' (m_f of the direction heuristic) */
     uint64_t aux;        /* algorithm-specific: BFS unvisited edges m_u; SSSP bucket upper bound; k-core level k */
+    uint64_t t_ns;       /* device %globaltimer (ns) when the iteration's decision was taken */
 } sx_trace_rec;
 
 typedef struct {

@@ -21,6 +21,7 @@ struct BfsP {
     Sched s;
     uint32_t* level;
     uint32_t* visited;
+    int sym;  // symmetric graph: in-degree == out-degree
 };
 
 __global__ void bfs_init(BfsP p, uint32_t src, uint32_t dir) {
@@ -40,13 +41,14 @@ __global__ void bfs_init(BfsP p, uint32_t src, uint32_t dir) {
     c->lists_ready = dir == DIR_PUSH ? 1u : 0u;
     c->iter = 0;
     c->done = 0;
-    c->st_reached = 1;
+    c->st[0].reached = 1;
 }
 
-__device__ __forceinline__ void bfs_exit(const BfsP& p, uint32_t it, uint64_t m_u, uint32_t nf_prev, uint32_t dir,
-                                         uint32_t done, uint32_t ready, const uint32_t (&cnt)[NCLS], Stats& st) {
+__device__ __forceinline__ void bfs_exit(const BfsP& p, uint32_t kdir, uint32_t it, uint64_t m_u, uint32_t nf_prev,
+                                         uint32_t dir, uint32_t done, uint32_t ready, const uint32_t (&cnt)[NCLS],
+                                         Stats& st) {
     Ctl* c = p.s.ctl;
-    flush_stats(c, st);
+    flush_stats(c, st, kdir);
     if (lead()) {
         c->iter = it;
         c->m_u = m_u;
@@ -143,134 +145,171 @@ __global__ void __launch_bounds__(BLOCK, 4) bfs_push(BfsP p) {
         }
         if (!p.s.fusion) break;
     }
-    bfs_exit(p, it, m_u, nf_prev, dir, done, ready, cnt, st);
+    bfs_exit(p, DIR_PUSH, it, m_u, nf_prev, dir, done, ready, cnt, st);
 }
 
 // ------------------------------------------------------------------ pull
-// Candidates = unvisited vertices with in-edges (ballot filter over
-// ~visited & nz at entry); a candidate that finds no frontier in-neighbour is
-// re-recorded for the next level (online, exactly once).
+// Bottom-up step over tiles of 32 consecutive vertices: a warp owns one word of
+// the visited bitmap per tile, so the active set of the tile is the word
+// ~visited & (in-degree > 0) — the ballot filter's output for that tile
+// without materialising a list.  Inside the tile the candidates are binned by
+// in-degree: small ones are scanned by their own lane with 4
+// independent loads in flight per round (thread granularity), medium and
+// larger ones by the whole warp, 32 edges per step (warp granularity).  Both stop
+// at the first frontier in-neighbour (voting early exit).  The warp
+// writes the tile's visited / next-frontier words with plain stores: no atomics.
+constexpr int PROBE = 4;
+
 __global__ void __launch_bounds__(BLOCK, 4) bfs_pull(BfsP p) {
     Ctl* c = p.s.ctl;
     if (vload(&c->done) || vload(&c->dir) != DIR_PULL) return;
     const uint64_t n = p.g.n;
+    const uint64_t nw = (n + 31) >> 5;
     uint32_t it = vload(&c->iter);
     uint64_t m_u = vload(&c->m_u);
     uint32_t nf_prev = vload(&c->nf_prev);
-    uint32_t cnt[NCLS];
+    uint32_t cnt[NCLS] = {0, 0, 0, 0};
     Stats st;
-    uint32_t dir = DIR_PULL, done = 0, ready = 1;
-    if (!vload(&c->lists_ready)) {
-        if (!ballot_filter(CandidateWords{p.visited, p.g.nz_in}, p.s, BallotOut{p.s.lists[it & 1], n, p.g.din}, cnt))
-            return;
-        st.scanned += p.s.nwords * 32;
-        if (!grid_sync(c)) return;
-    } else {
-        for (int i = 0; i < NCLS; ++i) cnt[i] = vload(&c->cur_count[i]);
-    }
-    __shared__ uint32_t s_hit;
+    uint32_t dir = DIR_PULL, done = 0;
+    const uint32_t lane = lane_id();
     for (;;) {
         CntLine* nx = &c->line[(it + 1) % 3];
         if (lead()) reset_line(&c->line[(it + 2) % 3]);
         clear_bitmap(p.s.bm[(it + 2) % 3], p.s.nwords);
         const uint32_t* cur = p.s.bm[it % 3];
         uint32_t* nbm = p.s.bm[(it + 1) % 3];
-        uint32_t* nlists = p.s.lists[(it + 1) & 1];
-        const uint32_t* L = p.s.lists[it & 1];
         const uint32_t lvl = it + 1;
-        uint64_t mdeg = 0, edges = 0;
-        uint32_t found = 0;
-        auto mark = [&](uint32_t u) {
-            p.level[u] = lvl;
-            bm_set(p.visited, u);
-            bm_set(nbm, u);
-            mdeg += __ldg(p.g.dout + u);
-            ++found;
+        uint64_t mdeg = 0, edges = 0, cand_small = 0, cand_warp = 0;
+        uint32_t found_cnt = 0;
+        // one probe round: up to PROBE in-edges [e, end) of this lane's candidate, loads in flight together
+        auto probe = [&](uint64_t& e, uint64_t end, bool& found) {
+            uint32_t u[PROBE];
+#pragma unroll
+            for (int k = 0; k < PROBE; ++k) u[k] = (e + k < end) ? __ldg(p.g.ici + e + k) : INF;
+            uint32_t w[PROBE];
+#pragma unroll
+            for (int k = 0; k < PROBE; ++k) w[k] = u[k] != INF ? cur[u[k] >> 5] : 0u;
+#pragma unroll
+            for (int k = 0; k < PROBE; ++k) found |= u[k] != INF && ((w[k] >> (u[k] & 31)) & 1u);
+            const uint64_t k = min((uint64_t)PROBE, end - e);
+            edges += k;
+            e += k;
         };
-        // CTA granularity: large and huge candidates (early exit with __syncthreads_or)
-        const uint32_t nbig = cnt[2] + cnt[3];
-        for (uint32_t i = blockIdx.x; i < nbig; i += gridDim.x) {
-            const uint32_t k = i < cnt[2] ? 2u : 3u;
-            const uint32_t u = L[(uint64_t)k * n + (k == 2 ? i : i - cnt[2])];
-            const uint64_t beg = __ldg(p.g.irp + u), end = __ldg(p.g.irp + u + 1);
-            bool hit = false;
-            for (uint64_t b = beg; b < end; b += BLOCK) {
-                const uint64_t e = b + threadIdx.x;
-                bool h = false;
-                if (e < end) {
-                    ++edges;
-                    h = bm_test(cur, __ldg(p.g.ici + e));
-                }
-                if (__syncthreads_or(h)) {
-                    hit = true;
-                    break;
+        // Dynamic chunks of 32 tiles (1024 vertices): one coalesced load brings the
+        // 32 candidate words, empty tiles are skipped by a ballot, and within the
+        // chunk the next tile's row pointers are loaded while the current tile is
+        // probed.  The next chunk index is fetched one chunk ahead.
+        const uint64_t nchunks = (nw + 31) >> 5;
+        uint32_t chunk = 0;
+        if (lane == 0) chunk = atomicAdd(&nx->tile, 1u);
+        chunk = __shfl_sync(FULL, chunk, 0);
+        while (chunk < nchunks) {
+            uint32_t chunk_n = 0;
+            if (lane == 0) chunk_n = atomicAdd(&nx->tile, 1u);
+            const uint64_t w0 = (uint64_t)chunk << 5;
+            const uint64_t wl = w0 + lane;
+            const uint32_t vis_l = wl < nw ? p.visited[wl] : FULL;
+            const uint32_t cand_l = wl < nw ? (~vis_l & __ldg(p.g.nz_in + wl)) : 0u;
+            uint32_t tiles = __ballot_sync(FULL, cand_l != 0);
+            uint64_t beg = 0, end = 0, beg_n = 0, end_n = 0;
+            uint32_t cand = 0, cand_n = 0;
+            int j = 0, jn = 0;
+            if (tiles) {
+                jn = __ffs(tiles) - 1;
+                tiles &= tiles - 1;
+                cand_n = __shfl_sync(FULL, cand_l, jn);
+                if ((cand_n >> lane) & 1u) {
+                    beg_n = __ldg(p.g.irp + ((w0 + jn) << 5) + lane);
+                    end_n = __ldg(p.g.irp + ((w0 + jn) << 5) + lane + 1);
                 }
             }
-            if (threadIdx.x == 0) {
-                if (hit) mark(u);
-                else online_record(nx, nlists, n, (uint32_t)n, u, k);
+            while (cand_n) {
+                cand = cand_n;
+                j = jn;
+                beg = beg_n;
+                end = end_n;
+                cand_n = 0;
+                beg_n = end_n = 0;
+                if (tiles) {
+                    jn = __ffs(tiles) - 1;
+                    tiles &= tiles - 1;
+                    cand_n = __shfl_sync(FULL, cand_l, jn);
+                }
+                const uint64_t wi = w0 + j;
+                const uint32_t v = (uint32_t)(wi << 5) + lane;
+                const bool mine = (cand >> lane) & 1u;
+                bool found = false;
+                uint64_t e = beg;
+                if (mine) probe(e, end, found);  // first round for every candidate
+                if ((cand_n >> lane) & 1u) {
+                    beg_n = __ldg(p.g.irp + ((w0 + jn) << 5) + lane);
+                    end_n = __ldg(p.g.irp + ((w0 + jn) << 5) + lane + 1);
+                }
+                // thread granularity: small candidates continue on their lane
+                const bool small = mine && (end - beg) < p.s.sep_small;
+                if (small) {
+                    ++cand_small;
+                    while (!found && e < end) probe(e, end, found);
+                }
+                // warp granularity: medium / large candidates still open, 32 edges per step
+                uint32_t todo = __ballot_sync(FULL, mine && !small && !found && e < end);
+                while (todo) {
+                    const int l = __ffs(todo) - 1;
+                    todo &= todo - 1;
+                    const uint64_t b0 = __shfl_sync(FULL, e, l), e0 = __shfl_sync(FULL, end, l);
+                    bool hit = false;
+                    for (uint64_t b = b0; b < e0; b += 32) {
+                        const uint64_t x = b + lane;
+                        bool h = false;
+                        if (x < e0) {
+                            ++edges;
+                            h = bm_test(cur, __ldg(p.g.ici + x));
+                        }
+                        if (__any_sync(FULL, h)) {
+                            hit = true;
+                            break;
+                        }
+                    }
+                    if ((int)lane == l) found = hit;
+                    ++cand_warp;
+                }
+                const uint32_t fm = __ballot_sync(FULL, found);
+                if (found) {
+                    p.level[v] = lvl;
+                    mdeg += p.sym ? (end - beg) : __ldg(p.g.dout + v);
+                }
+                const uint32_t vis = __shfl_sync(FULL, vis_l, j);
+                if (lane == 0 && fm) {
+                    p.visited[wi] = vis | fm;  // this warp owns the word during the level
+                    nbm[wi] = fm;
+                    found_cnt += __popc(fm);
+                }
             }
+            chunk = __shfl_sync(FULL, chunk_n, 0);
         }
-        // warp granularity: medium candidates (__any_sync early exit)
-        for (uint64_t i = gwarp(); i < cnt[1]; i += gwarps()) {
-            const uint32_t u = L[n + i];
-            const uint64_t beg = __ldg(p.g.irp + u), end = __ldg(p.g.irp + u + 1);
-            bool hit = false;
-            for (uint64_t b = beg; b < end; b += 32) {
-                const uint64_t e = b + lane_id();
-                bool h = false;
-                if (e < end) {
-                    ++edges;
-                    h = bm_test(cur, __ldg(p.g.ici + e));
-                }
-                if (__any_sync(FULL, h)) {
-                    hit = true;
-                    break;
-                }
-            }
-            if (lane_id() == 0) {
-                if (hit) mark(u);
-                else online_record(nx, nlists, n, (uint32_t)n, u, 1u);
-            }
-        }
-        // thread granularity: small candidates
-        for (uint64_t i = gtid(); i < cnt[0]; i += gthreads()) {
-            const uint32_t u = L[i];
-            const uint64_t beg = __ldg(p.g.irp + u), end = __ldg(p.g.irp + u + 1);
-            bool hit = false;
-            for (uint64_t e = beg; e < end; ++e) {
-                ++edges;
-                if (bm_test(cur, __ldg(p.g.ici + e))) {
-                    hit = true;
-                    break;
-                }
-            }
-            if (hit) mark(u);
-            else online_record(nx, nlists, n, (uint32_t)n, u, 0u);
-        }
-        (void)s_hit;
         st.edges += edges;
-        st.reached += found;
-        if (lead()) st.entries += sum4(cnt);
+        st.reached += found_cnt;
         {
-            uint64_t v[2] = {mdeg, found};
-            block_sum<2>(v);
+            uint64_t v3[4] = {mdeg, found_cnt, cand_small, cand_warp};
+            block_sum<4>(v3);
             if (threadIdx.x == 0) {
-                if (v[0]) atomicAdd(&nx->mdeg, (unsigned long long)v[0]);
-                if (v[1]) atomicAdd(&nx->found, (unsigned int)v[1]);
+                if (v3[0]) atomicAdd(&nx->mdeg, (unsigned long long)v3[0]);
+                if (v3[1]) atomicAdd(&nx->found, (unsigned int)v3[1]);
+                if (v3[2]) atomicAdd(&nx->cnt[0], (unsigned int)v3[2]);
+                if (v3[3]) atomicAdd(&nx->cnt[1], (unsigned int)(v3[3] / 32));
             }
         }
+        st.entries += cand_small + cand_warp / 32;
+        st.scanned += (lead() ? nw * 32 : 0);
         if (!grid_sync(c)) return;
-        uint32_t ncnt[NCLS];
-        for (int i = 0; i < NCLS; ++i) ncnt[i] = vload(&nx->cnt[i]);
         const uint64_t nf = vload(&nx->found);
         const uint64_t mf = vload(&nx->mdeg);
+        uint32_t tc[NCLS] = {vload(&nx->cnt[0]), vload(&nx->cnt[1]), 0u, 0u};
         m_u -= mf;
         ++it;
         ++st.iters;
         ++st.pull;
-        trace_put(p.s, it, DIR_PULL, 0u, ncnt, nf, mf, m_u);
-        for (int i = 0; i < NCLS; ++i) cnt[i] = ncnt[i];
+        trace_put(p.s, it, DIR_PULL, 1u, tc, nf, mf, m_u);
         if (nf == 0 || (p.s.max_iters && it >= p.s.max_iters)) {
             done = 1;
             break;
@@ -280,12 +319,11 @@ __global__ void __launch_bounds__(BLOCK, 4) bfs_pull(BfsP p) {
         nf_prev = (uint32_t)nf;
         if (to_push) {
             dir = DIR_PUSH;
-            ready = 0;
             break;
         }
         if (!p.s.fusion) break;
     }
-    bfs_exit(p, it, m_u, nf_prev, dir, done, ready, cnt, st);
+    bfs_exit(p, DIR_PULL, it, m_u, nf_prev, dir, done, 0u, cnt, st);
 }
 
 }  // namespace sx
@@ -297,9 +335,13 @@ using namespace sx;
 // per list entry 4 B (list) + 16 B (row_ptr pair); per examined edge 4 B (col);
 // per reached vertex 4 B (level write); per iteration one frontier-bitmap clear
 // (n/8); per pull iteration one frontier-bitmap read (n/8); ballot scans n/8.
+// Pull (tile scan): per candidate 16 B (row_ptr pair); per examined edge 4 B;
+// per reached vertex 4 B; per iteration visited + in-degree>0 + frontier bitmaps
+// and one bitmap clear (4 n/8).
 static double bfs_bytes(const sx_graph g, const sxh::Counters& c) {
     const double n = (double)g->n;
-    return 20.0 * c.entries + 4.0 * c.edges + 4.0 * c.reached + (c.iters + c.pull) * n / 8.0 + c.scanned / 8.0;
+    if (c.pull > 0) return 16.0 * c.entries + 4.0 * c.edges + 4.0 * c.reached + c.pull * 4.0 * n / 8.0;
+    return 20.0 * c.entries + 4.0 * c.edges + 4.0 * c.reached + c.iters * n / 8.0 + c.scanned / 8.0;
 }
 
 extern "C" sx_status sx_bfs(sx_graph g, uint32_t src, const sx_opts* opts, uint32_t* level_out, sx_stats* stats) {
@@ -316,8 +358,11 @@ extern "C" sx_status sx_bfs(sx_graph g, uint32_t src, const sx_opts* opts, uint3
     if ((rc = run.begin()) != SX_OK) return rc;
     p.g = sxh::dev_graph(g);
     p.s = sxh::make_sched(g, run.o);
-    p.level = g->st[0];
+    // write levels straight into a device output buffer (no copy-out)
+    const bool dev_out = sxh::is_device_ptr(level_out);
+    p.level = dev_out ? level_out : g->st[0];
     p.visited = g->aux_bm;
+    p.sym = !g->directed;
     SX_CU(cudaMemsetAsync(p.level, 0xFF, g->n * 4, s));
     SX_CU(cudaMemsetAsync(p.visited, 0, g->nwords * 4, s));
     for (int i = 0; i < 3; ++i) SX_CU(cudaMemsetAsync(p.s.bm[i], 0, g->nwords * 4, s));
@@ -325,15 +370,23 @@ extern "C" sx_status sx_bfs(sx_graph g, uint32_t src, const sx_opts* opts, uint3
     bfs_init<<<1, 1, 0, s>>>(p, src, dir0);
     SX_CU(cudaGetLastError());
     void* args[] = {&p};
-    g->ctx->h_ctl->dir = dir0;
-    g->ctx->h_ctl->done = 0;
+    // Selective fusion: the direction-optimising BFS runs push -> pull
+    // -> push; the three persistent launches are enqueued back to back
+    // without a host round trip — a launch whose direction does not match the
+    // device-side state exits at once — and the host syncs once per sequence.
+    uint32_t dir = dir0;
     for (;;) {
-        const bool pull = g->ctx->h_ctl->dir == DIR_PULL;
-        if ((rc = run.launch(pull ? (const void*)bfs_pull : (const void*)bfs_push, args, pull)) != SX_OK) return rc;
+        const void* first = dir == DIR_PULL ? (const void*)bfs_pull : (const void*)bfs_push;
+        const void* second = dir == DIR_PULL ? (const void*)bfs_push : (const void*)bfs_pull;
+        if ((rc = run.launch(first, args, dir == DIR_PULL)) != SX_OK) return rc;
+        if ((rc = run.launch(second, args, dir != DIR_PULL)) != SX_OK) return rc;
+        if ((rc = run.launch(first, args, dir == DIR_PULL)) != SX_OK) return rc;
+        if ((rc = run.sync()) != SX_OK) return rc;
         if (g->ctx->h_ctl->done) break;
+        dir = g->ctx->h_ctl->dir;
     }
     if ((rc = run.end(bfs_bytes)) != SX_OK) return rc;
-    return sxh::copy_out(g, level_out, p.level, g->n * 4);
+    return dev_out ? SX_OK : sxh::copy_out(g, level_out, p.level, g->n * 4);
 }
 
 extern "C" sx_status sx_ctx_info(sx_ctx c, sx_device_info* out) {

@@ -33,7 +33,7 @@ sx_status check_ctx(sx_ctx c) {
     return SX_OK;
 }
 
-static bool is_device_ptr(const void* p) {
+bool is_device_ptr(const void* p) {
     cudaPointerAttributes a{};
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
         cudaGetLastError();
@@ -150,45 +150,63 @@ sx_status Run::begin() {
     }
     SX_CU(cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), c->stream));
     std::memset(c->h_ctl, 0, sizeof(Ctl));
-    std::memset(&prev, 0, sizeof(prev));
     SX_CU(cudaEventRecord(c->ev0, c->stream));
     return SX_OK;
 }
 
 sx_status Run::launch(const void* fn, void** args, bool pull) {
     sx_ctx c = g->ctx;
-    SX_CU(cudaEventRecord(c->evk0, c->stream));
+    if (npending == EV_POOL) {
+        sx_status rc = sync();
+        if (rc != SX_OK) return rc;
+    }
+    SX_CU(cudaEventRecord(c->evp[2 * npending], c->stream));
     sx_status rc = coop_launch(g, fn, args, nullptr);
     if (rc != SX_OK) return rc;
-    SX_CU(cudaEventRecord(c->evk1, c->stream));
+    SX_CU(cudaEventRecord(c->evp[2 * npending + 1], c->stream));
+    pend_pull[npending++] = pull;
+    ++(pull ? launches_pull : launches_push);
+    ++launches;
+    if (launches > 10000000) return fail(SX_E_STATE, "runaway launch loop");
+    return SX_OK;
+}
+
+sx_status Run::sync() {
+    sx_ctx c = g->ctx;
     SX_CU(cudaMemcpyAsync(c->h_ctl, g->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->stream));
     cudaError_t e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) {
         c->poisoned = true;
         return cuda_fail(e, "persistent kernel");
     }
-    float ms = 0;
-    SX_CU(cudaEventElapsedTime(&ms, c->evk0, c->evk1));
-    const Ctl& h = *c->h_ctl;
-    Counters& k = pull ? c_pull : c_push;
-    k.entries += (double)(h.st_entries - prev.st_entries);
-    k.edges += (double)(h.st_edges - prev.st_edges);
-    k.reached += (double)(h.st_reached - prev.st_reached);
-    k.scanned += (double)(h.st_scanned - prev.st_scanned);
-    k.iters += (double)(h.st_iters - prev.st_iters);
-    k.pull += (double)(h.st_pull - prev.st_pull);
-    k.ballot += (double)(h.st_ballot - prev.st_ballot);
-    prev = h;
-    (pull ? ms_pull : ms_push) += ms;
-    ++(pull ? launches_pull : launches_push);
-    ++launches;
-    if (h.error) return fail(SX_E_BARRIER, "grid barrier watchdog fired");
-    if (launches > 1000000) return fail(SX_E_STATE, "runaway launch loop");
+    for (int i = 0; i < npending; ++i) {
+        float ms = 0;
+        SX_CU(cudaEventElapsedTime(&ms, c->evp[2 * i], c->evp[2 * i + 1]));
+        (pend_pull[i] ? ms_pull : ms_push) += ms;
+    }
+    npending = 0;
+    if (c->h_ctl->error) return fail(SX_E_BARRIER, "grid barrier watchdog fired");
     return SX_OK;
+}
+
+static Counters counters_of(const Ctl::StatBlock& b) {
+    Counters k;
+    k.entries = (double)b.entries;
+    k.edges = (double)b.edges;
+    k.reached = (double)b.reached;
+    k.scanned = (double)b.scanned;
+    k.iters = (double)b.iters;
+    k.pull = (double)b.pull;
+    k.ballot = (double)b.ballot;
+    return k;
 }
 
 sx_status Run::end(BytesFn bytes) {
     sx_ctx c = g->ctx;
+    if (npending) {
+        sx_status rc = sync();
+        if (rc != SX_OK) return rc;
+    }
     SX_CU(cudaEventRecord(c->ev1, c->stream));
     SX_CU(cudaEventSynchronize(c->ev1));
     float ms = 0;
@@ -196,15 +214,17 @@ sx_status Run::end(BytesFn bytes) {
     const Ctl& h = *c->h_ctl;
     if (st) {
         std::memset(st, 0, sizeof(*st));
-        st->iterations = h.st_iters;
+        const Ctl::StatBlock& a = h.st[0];
+        const Ctl::StatBlock& b = h.st[1];
+        st->iterations = a.iters + b.iters;
         st->launches = launches;
-        st->ballot_iters = h.st_ballot;
-        st->pull_iters = h.st_pull;
-        st->edges_examined = h.st_edges;
-        st->vertices_scanned = h.st_scanned;
-        st->list_entries = h.st_entries;
-        st->bytes_push = bytes(g, c_push);
-        st->bytes_pull = bytes(g, c_pull);
+        st->ballot_iters = a.ballot + b.ballot;
+        st->pull_iters = a.pull + b.pull;
+        st->edges_examined = a.edges + b.edges;
+        st->vertices_scanned = a.scanned + b.scanned;
+        st->list_entries = a.entries + b.entries;
+        st->bytes_push = bytes(g, counters_of(a));
+        st->bytes_pull = bytes(g, counters_of(b));
         st->bytes_model = st->bytes_push + st->bytes_pull;
         st->ms = ms;
         st->ms_push = ms_push;
@@ -292,8 +312,8 @@ sx_status sx_ctx_create(int device, void* cuda_stream, sx_ctx* out) {
         delete c;
         return sxh::fail(SX_E_BARRIER, "sx_ctx_create: device lacks cooperative launch");
     }
-    cudaEvent_t* evs[] = {&c->ev0, &c->ev1, &c->evk0, &c->evk1};
-    for (auto* ev : evs) {
+    for (int i = 0; i < 2 + 2 * sxh::EV_POOL; ++i) {
+        cudaEvent_t* ev = i == 0 ? &c->ev0 : i == 1 ? &c->ev1 : &c->evp[i - 2];
         if ((e = cudaEventCreate(ev)) != cudaSuccess) {
             sx_ctx_destroy(c);
             return sxh::cuda_fail(e, "cudaEventCreate");
@@ -313,8 +333,8 @@ void sx_ctx_destroy(sx_ctx c) {
     cudaSetDevice(c->device);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
-    if (c->evk0) cudaEventDestroy(c->evk0);
-    if (c->evk1) cudaEventDestroy(c->evk1);
+    for (auto ev : c->evp)
+        if (ev) cudaEventDestroy(ev);
     if (c->h_ctl) cudaFreeHost(c->h_ctl);
     delete c;
 }

@@ -54,6 +54,7 @@ struct alignas(128) CntLine {
     double dsum;                     // PageRank dangling mass accumulator
     unsigned int minv;               // min reduction scratch (SSSP far min, k-core min residual)
     unsigned int alive;              // k-core alive count
+    unsigned int tile;               // dynamic work counter (chunks of tiles / tasks)
 };
 
 struct Ctl {
@@ -72,15 +73,12 @@ struct Ctl {
     unsigned long long m_u;          // BFS: edges incident to unvisited vertices
     unsigned long long hi;           // SSSP: current bucket upper bound (exclusive)
     unsigned int cur_count[NCLS];    // list sizes for iteration `iter`
-    // --- run statistics (accumulated with one atomic per CTA per launch)
-    alignas(128) unsigned long long st_edges;
-    unsigned long long st_entries;
-    unsigned long long st_scanned;
-    unsigned int st_ballot;
-    unsigned int st_pull;
-    unsigned int st_iters;
-    unsigned long long st_reached;
     unsigned int ntrace;
+    // --- run statistics per direction of the launch (0 push, 1 pull), one atomic per CTA per launch
+    struct alignas(128) StatBlock {
+        unsigned long long edges, entries, scanned, reached;
+        unsigned int ballot, pull, iters;
+    } st[2];
 };
 
 struct TraceRec {  // mirrors sx_trace_rec
@@ -89,6 +87,7 @@ struct TraceRec {  // mirrors sx_trace_rec
     uint64_t n_frontier;
     uint64_t m_active;
     uint64_t aux;
+    uint64_t t_ns;
 };
 
 // ---------------------------------------------------------------- graph view
@@ -473,18 +472,19 @@ struct Stats {
 };
 
 // Per-CTA partial counters -> one atomic per CTA; uniform counters from CTA 0.
-__device__ __forceinline__ void flush_stats(Ctl* c, Stats& st) {
+__device__ __forceinline__ void flush_stats(Ctl* c, Stats& st, uint32_t dir) {
     uint64_t v[3] = {st.edges, st.entries, st.reached};
     block_sum<3>(v);
     if (threadIdx.x == 0) {
-        if (v[0]) atomicAdd(&c->st_edges, (unsigned long long)v[0]);
-        if (v[1]) atomicAdd(&c->st_entries, (unsigned long long)v[1]);
-        if (v[2]) atomicAdd(&c->st_reached, (unsigned long long)v[2]);
+        Ctl::StatBlock& b = c->st[dir];
+        if (v[0]) atomicAdd(&b.edges, (unsigned long long)v[0]);
+        if (v[1]) atomicAdd(&b.entries, (unsigned long long)v[1]);
+        if (v[2]) atomicAdd(&b.reached, (unsigned long long)v[2]);
         if (blockIdx.x == 0) {
-            c->st_scanned += st.scanned;
-            c->st_ballot += st.ballot;
-            c->st_pull += st.pull;
-            c->st_iters += st.iters;
+            b.scanned += st.scanned;
+            b.ballot += st.ballot;
+            b.pull += st.pull;
+            b.iters += st.iters;
         }
     }
 }
@@ -498,6 +498,7 @@ __device__ __forceinline__ void reset_line(CntLine* L) {
     L->dsum = 0.0;
     L->minv = INF;
     L->alive = 0;
+    L->tile = 0;
 }
 
 __device__ __forceinline__ bool lead() { return blockIdx.x == 0 && threadIdx.x == 0; }
@@ -517,6 +518,7 @@ __device__ __forceinline__ void trace_put(const Sched& s, uint32_t iter, uint32_
             r.n_frontier = nf;
             r.m_active = mf;
             r.aux = aux;
+            r.t_ns = globaltimer();
             s.trace[i] = r;
         }
     }

@@ -13,7 +13,8 @@ struct sx_ctx_s {
     cudaStream_t stream = nullptr;
     cudaDeviceProp prop{};
     bool poisoned = false;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr, evk0 = nullptr, evk1 = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t evp[2 * 32] = {};  // per-launch event pairs (sxh::EV_POOL)
     sx::Ctl* h_ctl = nullptr;  // pinned host mirror of the control block
 };
 
@@ -75,22 +76,26 @@ struct Counters {
 using BytesFn = double (*)(const sx_graph g, const Counters& c);
 
 // Per-run bookkeeping: events, trace copy-out, stats.
+constexpr int EV_POOL = 32;  // event pairs per ctx (launches in flight between two syncs)
 struct Run {
     sx_graph g;
     sx_opts o;
     sx_stats* st;
     float ms_push = 0, ms_pull = 0;
     uint32_t launches = 0, launches_push = 0, launches_pull = 0;
-    Counters c_push, c_pull;
-    sx::Ctl prev{};
+    int npending = 0;
+    bool pend_pull[EV_POOL] = {};
     sx_status begin();
-    // Launch one persistent kernel (timed), then read back the control block.
+    // Enqueue one persistent kernel (timed with an event pair); no host sync.
     sx_status launch(const void* fn, void** args, bool pull);
+    // Read back the control block, accumulate the pending launches' times, check errors.
+    sx_status sync();
     sx_status end(BytesFn bytes);
 };
 
 sx_status copy_out(sx_graph g, void* dst, const void* src_dev, size_t bytes);
 sx_status copy_in(sx_graph g, void* dst_dev, const void* src, size_t bytes);
 sx_status check_ctx(sx_ctx c);
+bool is_device_ptr(const void* p);
 
 }  // namespace sxh

@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(BLOCK, 4) kcore_push(KcoreP p) {
         }
         if (!p.s.fusion) break;
     }
-    flush_stats(c, st);
+    flush_stats(c, st, DIR_PUSH);
     if (lead()) {
         c->iter = it;
         c->k = k;
@@ -212,6 +212,7 @@ extern "C" sx_status sx_kcore(sx_graph g, uint32_t k, const sx_opts* opts, uint3
     g->ctx->h_ctl->done = 0;
     for (;;) {
         if ((rc = run.launch((const void*)kcore_push, args, false)) != SX_OK) return rc;
+        if ((rc = run.sync()) != SX_OK) return rc;
         if (g->ctx->h_ctl->done) break;
     }
     if ((rc = run.end(kcore_bytes)) != SX_OK) return rc;

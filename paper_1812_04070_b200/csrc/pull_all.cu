@@ -183,7 +183,7 @@ template <class Op> __global__ void __launch_bounds__(BLOCK, 4) pull_all(PullP<O
         trace_put(p.s, t + 1, DIR_PULL, t == 0 ? 1u : 2u, cnt, n, 0, 0);
     }
     st.pull = st.iters;
-    flush_stats(c, st);
+    flush_stats(c, st, DIR_PULL);
     if (lead()) {
         c->iter = p.iters;
         c->done = 1;

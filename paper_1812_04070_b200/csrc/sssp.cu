@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_push(SsspP p) {
         }
         if (!p.s.fusion) break;
     }
-    flush_stats(c, st);
+    flush_stats(c, st, DIR_PUSH);
     if (lead()) {
         c->iter = it;
         c->hi = hi;
@@ -198,6 +198,7 @@ extern "C" sx_status sx_sssp(sx_graph g, uint32_t src, uint32_t delta, const sx_
     g->ctx->h_ctl->done = 0;
     for (;;) {
         if ((rc = run.launch((const void*)sssp_push, args, false)) != SX_OK) return rc;
+        if ((rc = run.sync()) != SX_OK) return rc;
         if (g->ctx->h_ctl->done) break;
     }
     if ((rc = run.end(sssp_bytes)) != SX_OK) return rc;

@@ -40,7 +40,7 @@ class sx_csr_desc(ctypes.Structure):
 
 class sx_trace_rec(ctypes.Structure):
     _fields_ = [("iter", _u32), ("dir", _u32), ("filter", _u32), ("launch", _u32), ("n_active", _u32 * 4),
-                ("n_frontier", _u64), ("m_active", _u64), ("aux", _u64)]
+                ("n_frontier", _u64), ("m_active", _u64), ("aux", _u64), ("t_ns", _u64)]
 
 
 class sx_opts(ctypes.Structure):
@@ -88,13 +88,14 @@ _lib.sx_pagerank.argtypes = [_vp, _f32, _u32, _P(sx_opts), _vp, _P(sx_stats)]
 _lib.sx_kcore.argtypes = [_vp, _u32, _P(sx_opts), _vp, _P(sx_stats)]
 _lib.sx_spmv.argtypes = [_vp, _vp, _u32, _P(sx_opts), _vp, _P(sx_stats)]
 _lib.sx_bp.argtypes = [_vp, _vp, _u32, _P(sx_opts), _vp, _P(sx_stats)]
+_lib.sx_barrier_bench.argtypes = [_vp, _u32, _P(ctypes.c_double), _P(ctypes.c_int)]
 for _f in ("sx_ctx_create", "sx_ctx_info", "sx_graph_upload", "sx_graph_info", "sx_bfs", "sx_sssp", "sx_pagerank",
-           "sx_kcore", "sx_spmv", "sx_bp"):
+           "sx_kcore", "sx_spmv", "sx_bp", "sx_barrier_bench"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 EXPORTED = ["sx_status_str", "sx_last_error", "sx_version", "sx_ctx_create", "sx_ctx_destroy", "sx_ctx_info",
             "sx_graph_upload", "sx_graph_info", "sx_graph_free", "sx_opts_default", "sx_bfs", "sx_sssp",
-            "sx_pagerank", "sx_kcore", "sx_spmv", "sx_bp"]
+            "sx_pagerank", "sx_kcore", "sx_spmv", "sx_bp", "sx_barrier_bench"]
 
 
 class SimdxError(RuntimeError):
@@ -170,6 +171,12 @@ def sx_ctx_info(ctx) -> dict:
     info = sx_device_info()
     _check(_lib.sx_ctx_info(ctx, ctypes.byref(info)), "sx_ctx_info")
     return {k: getattr(info, k) for k, _ in info._fields_}
+
+
+def sx_barrier_bench(ctx, iters: int = 10000):
+    us, ctas = ctypes.c_double(), ctypes.c_int()
+    _check(_lib.sx_barrier_bench(ctx, iters, ctypes.byref(us), ctypes.byref(ctas)), "sx_barrier_bench")
+    return us.value, ctas.value
 
 
 def sx_graph_upload(ctx, n, row_ptr, col, w=None, csc_ptr=None, csc_idx=None, csc_w=None, directed=False,
@@ -285,7 +292,7 @@ class Graph:
             if r.iter == 0:
                 break
             recs.append(dict(iter=r.iter, dir=r.dir, filter=r.filter, launch=r.launch, n_active=list(r.n_active),
-                             n_frontier=r.n_frontier, m_active=r.m_active, aux=r.aux))
+                             n_frontier=r.n_frontier, m_active=r.m_active, aux=r.aux, t_ns=r.t_ns))
         return recs
 
     def bfs(self, src: int, out=None, **kw):

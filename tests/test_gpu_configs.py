@@ -1,0 +1,112 @@
+"""GPU parity at BASELINE.json's full single-GPU sizes (configs C1-C4), in the
+launch configuration bench.py times (default opts: JIT filter, auto direction,
+selective fusion).  Every output element is compared with the oracle."""
+import numpy as np
+import pytest
+
+import oracle
+import simgen
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+INF = 0xFFFFFFFF
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import torch
+    from paper_1812_04070_b200 import simdx
+    torch.cuda.set_device(0)
+    c = simdx.Context(0, torch.cuda.current_stream().cuda_stream)
+    yield c
+    c.close()
+
+
+def test_c1_bfs_rmat16(ctx):
+    """C1: BFS from vertex 0, R-MAT scale 16 ef 16."""
+    g = simgen.rmat(16, 16, 1)
+    G = ctx.upload(g)
+    lv, st, tr = G.bfs(0, trace_cap=64)
+    ref = oracle.bfs(g, 0)
+    assert np.array_equal(lv, ref)
+    hist = oracle.level_histogram(ref)
+    assert [t["n_frontier"] for t in tr][:len(hist) - 1] == list(hist[1:])
+    # selective fusion: push -> pull -> push = 3 launches (Table 2)
+    dirs = [t["dir"] for t in tr]
+    switches = sum(1 for a, b in zip(dirs, dirs[1:]) if a != b)
+    assert len({t["launch"] for t in tr}) == 1 + switches
+    G.free()
+
+
+def test_c2_sssp_road_grid(ctx):
+    """C2: SSSP, 2048 x 2048 grid, integer weights 1..255, src 0 (corner); distances delta-independent."""
+    g = simgen.grid(2048, 2048, seed=1, wmin=1, wmax=255)
+    ref = oracle.sssp(g, 0)
+    G = ctx.upload(g)
+    for delta in (0, 1024):
+        d, st, tr = G.sssp(0, delta, trace_cap=16)
+        assert np.array_equal(d, ref), delta
+        if delta == 0:
+            # high-diameter grid: the online filter handles every iteration
+            assert st["ballot_iters"] == 0 and st["iterations"] > 4000
+    G.free()
+
+
+def test_c3_pagerank_rmat22(ctx):
+    """C3: PageRank 20 iterations, d = 0.85, R-MAT scale 22: max relative error <= 1e-5 vs fp64."""
+    g = simgen.rmat(22, 16, 1)
+    G = ctx.upload(g)
+    r, st, tr = G.pagerank(0.85, 20, trace_cap=32)
+    o = oracle.pagerank(g, 0.85, 20)
+    rel = np.abs(r.astype(np.float64) - o) / o
+    assert rel.max() <= 1e-5, rel.max()
+    assert abs(float(r.astype(np.float64).sum()) - 1.0) < 1e-4  # mass conservation (fp32 storage)
+    assert [t["filter"] for t in tr][:2] == [1, 2]  # ballot exactly in iteration 1
+    G.free()
+
+
+@pytest.fixture(scope="module")
+def rmat24():
+    return simgen.rmat(24, 16, 1)
+
+
+def test_c4_kcore_rmat24(ctx, rmat24):
+    """C4: k-core decomposition (coreness) and the k = 16 core on R-MAT scale 24."""
+    G = ctx.upload(rmat24)
+    core, st, _ = G.kcore(0)
+    ref = oracle.coreness(rmat24)
+    assert np.array_equal(core, ref)
+    m16, _, _ = G.kcore(16)
+    assert np.array_equal(m16, (ref >= 16).astype(np.uint32))
+    G.free()
+
+
+def test_bench_config_bfs_rmat24(ctx, rmat24):
+    """The bench.py workload itself: BFS from 0 on R-MAT scale 24, device output buffer."""
+    import torch
+    G = ctx.upload(rmat24)
+    out = torch.empty(rmat24.n, dtype=torch.int32, device="cuda:0")
+    G.bfs(0, out=out)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), oracle.bfs(rmat24, 0))
+    G.free()
+
+
+def test_spmv_bp_rmat20(ctx):
+    g = simgen.rmat(20, 16, 2, wmin=1, wmax=255)
+    G = ctx.upload(g)
+    x = simgen.uniform_f32(5, 2, g.n, -1.0, 1.0)
+    y, _, _ = G.spmv(x, 2)
+    o = oracle.spmv(g, x)
+    # mixed-sign x: relative to the sum of |terms| (conditioned; fp64 accumulation, fp32 out)
+    scale = oracle.spmv(g, np.abs(x))
+    assert np.all(np.abs(y - o) <= 1e-5 * np.maximum(scale, 1e-30))
+    p = simgen.bp_prior(3, g.n)
+    l, _, _ = G.bp(p, 10)
+    o, at = oracle.bp(g, p, 10, with_abs_terms=True)
+    assert np.all(np.abs(l - o) <= 1e-5 * (np.abs(o) + at) + 1e-6)
+    G.free()
+
+
+def test_barrier_roofline(ctx):
+    from paper_1812_04070_b200 import simdx
+    us, ctas = simdx.sx_barrier_bench(ctx.h, 20000)
+    assert ctas >= 148 and 0.1 < us < 50.0
