@@ -5,7 +5,7 @@
 //   Combine : vote — any one update suffices; push claims u exactly once
 //             with atomicOr on the visited bitmap; pull stops scanning u's
 //             in-neighbours at the first frontier hit (collaborative early
-//             termination) using __any_sync / __syncthreads_or.
+//             termination) using __any_sync.
 //
 // Selective fusion: one persistent cooperative kernel per direction
 // run; it loops over BSP iterations with the grid barrier and exits only when
@@ -26,7 +26,9 @@ struct BfsP {
 
 __global__ void bfs_init(BfsP p, uint32_t src, uint32_t dir) {
     Ctl* c = p.s.ctl;
-    for (int i = 0; i < 3; ++i) reset_line(&c->line[i]);
+    if (threadIdx.x < 32)
+        for (int i = 0; i < 3; ++i) reset_line_warp(&c->line[i]);
+    if (threadIdx.x != 0) return;
     p.level[src] = 0;
     p.visited[src >> 5] |= 1u << (src & 31);
     p.s.bm[0][src >> 5] |= 1u << (src & 31);
@@ -34,19 +36,20 @@ __global__ void bfs_init(BfsP p, uint32_t src, uint32_t dir) {
     const uint32_t k = cls_of(d, p.s);
     for (int i = 0; i < NCLS; ++i) c->cur_count[i] = 0;
     c->cur_count[k] = 1;
-    p.s.lists[0][(uint64_t)k * p.g.n] = src;
+    p.s.lists[0][(uint64_t)k * p.s.cstride] = src;
     c->m_u = p.g.m - d;
     c->nf_prev = 1;
     c->dir = dir;
     c->lists_ready = dir == DIR_PUSH ? 1u : 0u;
+    c->slotted = 0;
     c->iter = 0;
     c->done = 0;
     c->st[0].reached = 1;
 }
 
 __device__ __forceinline__ void bfs_exit(const BfsP& p, uint32_t kdir, uint32_t it, uint64_t m_u, uint32_t nf_prev,
-                                         uint32_t dir, uint32_t done, uint32_t ready, const uint32_t (&cnt)[NCLS],
-                                         Stats& st) {
+                                         uint32_t dir, uint32_t done, uint32_t ready, uint32_t slotted,
+                                         const uint32_t (&cnt)[NCLS], Stats& st) {
     Ctl* c = p.s.ctl;
     flush_stats(c, st, kdir);
     if (lead()) {
@@ -56,7 +59,9 @@ __device__ __forceinline__ void bfs_exit(const BfsP& p, uint32_t kdir, uint32_t 
         c->dir = dir;
         c->done = done;
         c->lists_ready = ready;
+        c->slotted = slotted;
         for (int i = 0; i < NCLS; ++i) c->cur_count[i] = cnt[i];
+        grid_end(c);
         c->launch += 1;
     }
 }
@@ -65,30 +70,35 @@ __device__ __forceinline__ void bfs_exit(const BfsP& p, uint32_t kdir, uint32_t 
 __global__ void __launch_bounds__(BLOCK, 4) bfs_push(BfsP p) {
     Ctl* c = p.s.ctl;
     if (vload(&c->done) || vload(&c->dir) != DIR_PUSH) return;
-    const uint64_t n = p.g.n;
+    grid_begin(c);
     uint32_t it = vload(&c->iter);
     uint64_t m_u = vload(&c->m_u);
     uint32_t nf_prev = vload(&c->nf_prev);
     uint32_t cnt[NCLS];
     Stats st;
-    uint32_t dir = DIR_PUSH, done = 0, ready = 1;
+    uint32_t dir = DIR_PUSH, done = 0, ready = 1, slotted = 0;
     if (!vload(&c->lists_ready)) {
         // entering push from pull: the frontier exists only as a bitmap -> ballot filter
-        if (!ballot_filter(BitmapWords{p.s.bm[it % 3]}, p.s, BallotOut{p.s.lists[it & 1], n, p.g.dout}, cnt)) return;
+        if (!ballot_filter(BitmapWords{p.s.bm[it % 3]}, p.s, BallotOut{p.s.lists[it & 1], p.s.cstride, p.g.dout}, cnt))
+            return;
         st.scanned += p.s.nwords * 32;
         if (!grid_sync(c)) return;
+        view_contig(cnt);
+    } else if (vload(&c->slotted)) {
+        view_slots(&c->line[it % 3], p.s, cnt);
     } else {
         for (int i = 0; i < NCLS; ++i) cnt[i] = vload(&c->cur_count[i]);
+        view_contig(cnt);
     }
     for (;;) {
-        CntLine* nx = &c->line[(it + 1) % 3];
-        if (lead()) reset_line(&c->line[(it + 2) % 3]);
+        IterLine* nx = &c->line[(it + 1) % 3];
+        maybe_reset_line(&c->line[(it + 2) % 3]);
         clear_bitmap(p.s.bm[(it + 2) % 3], p.s.nwords);
         uint32_t* nlists = p.s.lists[(it + 1) & 1];
         uint32_t* nbm = p.s.bm[(it + 1) % 3];
         const uint32_t lvl = it + 1;
         uint64_t mdeg = 0, edges = 0, reached = 0;
-        for_tasks(p.s.lists[it & 1], n, cnt, [&](uint32_t v, uint64_t rank, uint64_t size, uint32_t) {
+        for_tasks(p.s.lists[it & 1], p.s, cnt, [&](uint32_t v, uint64_t rank, uint64_t size, uint32_t) {
             const uint64_t beg = __ldg(p.g.rp + v), end = __ldg(p.g.rp + v + 1);
             for_edges(p.g.ci, beg, end, rank, size, [&](uint64_t, uint32_t u) {
                 ++edges;
@@ -99,7 +109,7 @@ __global__ void __launch_bounds__(BLOCK, 4) bfs_push(BfsP p) {
                 const uint32_t du = __ldg(p.g.dout + u);
                 mdeg += du;
                 ++reached;
-                online_record(nx, nlists, n, p.s.online_cap, u, cls_of(du, p.s));
+                online_record(nx, nlists, p.s, u, cls_of(du, p.s));
             });
         });
         st.edges += edges;
@@ -108,23 +118,25 @@ __global__ void __launch_bounds__(BLOCK, 4) bfs_push(BfsP p) {
         {
             uint64_t v[1] = {mdeg};
             block_sum<1>(v);
-            if (threadIdx.x == 0 && v[0]) atomicAdd(&nx->mdeg, (unsigned long long)v[0]);
+            if (threadIdx.x == 0 && v[0]) atomicAdd(&nx->s[my_slot()].mdeg, (unsigned long long)v[0]);
         }
         if (!grid_sync(c)) return;
-        uint32_t ncnt[NCLS];
-        for (int i = 0; i < NCLS; ++i) ncnt[i] = vload(&nx->cnt[i]);
-        const uint64_t nf = sum4(ncnt);
-        const uint64_t mf = vload(&nx->mdeg);
+        LineSum ls;
+        uint32_t vcnt[NCLS];
+        read_line_view(nx, p.s, ls, vcnt);
+        const uint64_t nf = sum4(ls.cnt);
+        const uint64_t mf = ls.mdeg;
         bool overflow = false;
-        for (int i = 0; i < NCLS; ++i) overflow |= ncnt[i] > p.s.online_cap;
+        for (int i = 0; i < NCLS; ++i) overflow |= ls.cntmax[i] > p.s.cap_s;
         if (p.s.force_filter == 2) overflow = true;
         m_u -= mf;
         ++it;
         ++st.iters;
-        trace_put(p.s, it, DIR_PUSH, overflow ? 1u : 0u, ncnt, nf, mf, m_u);
+        trace_put(p.s, it, DIR_PUSH, overflow ? 1u : 0u, ls.cnt, nf, mf, m_u);
         if (nf == 0 || (p.s.max_iters && it >= p.s.max_iters)) {
             done = 1;
             for (int i = 0; i < NCLS; ++i) cnt[i] = 0;
+            slotted = 0;
             break;
         }
         const bool to_pull = p.s.force_dir == 2 ||
@@ -138,31 +150,39 @@ __global__ void __launch_bounds__(BLOCK, 4) bfs_push(BfsP p) {
         if (overflow) {
             ++st.ballot;
             st.scanned += p.s.nwords * 32;
-            if (!ballot_filter(BitmapWords{nbm}, p.s, BallotOut{p.s.lists[it & 1], n, p.g.dout}, cnt)) return;
+            if (!ballot_filter(BitmapWords{nbm}, p.s, BallotOut{p.s.lists[it & 1], p.s.cstride, p.g.dout}, cnt)) return;
             if (!grid_sync(c)) return;
+            view_contig(cnt);
+            slotted = 0;
         } else {
-            for (int i = 0; i < NCLS; ++i) cnt[i] = ncnt[i];
+            for (int i = 0; i < NCLS; ++i) cnt[i] = vcnt[i];  // view set by read_line_view
+            slotted = 1;
         }
         if (!p.s.fusion) break;
     }
-    bfs_exit(p, DIR_PUSH, it, m_u, nf_prev, dir, done, ready, cnt, st);
+    bfs_exit(p, DIR_PUSH, it, m_u, nf_prev, dir, done, ready, slotted, cnt, st);
 }
 
 // ------------------------------------------------------------------ pull
-// Bottom-up step over tiles of 32 consecutive vertices: a warp owns one word of
-// the visited bitmap per tile, so the active set of the tile is the word
-// ~visited & (in-degree > 0) — the ballot filter's output for that tile
-// without materialising a list.  Inside the tile the candidates are binned by
-// in-degree: small ones are scanned by their own lane with 4
-// independent loads in flight per round (thread granularity), medium and
-// larger ones by the whole warp, 32 edges per step (warp granularity).  Both stop
-// at the first frontier in-neighbour (voting early exit).  The warp
-// writes the tile's visited / next-frontier words with plain stores: no atomics.
+// Bottom-up step over chunks of 32 tiles of 32 consecutive vertices.  A warp
+// owns its chunk's words of the visited bitmap, so the active set of a tile is
+// the word ~visited & (in-degree > 0) — the ballot filter's output for that tile
+// without a grid-wide list.  The warp compacts the chunk's
+// candidates into a shared-memory list in vertex order (popc + exclusive scan:
+// a warp-local ballot filter) and processes them 32 per round, one per lane.
+// Candidates are binned by in-degree: every candidate first
+// probes PROBE in-edges on its own lane; small ones (thread granularity) finish
+// on their lane with PROBE loads in flight per round, medium and larger ones
+// still open continue with the whole warp, 32 edges per step (warp
+// granularity).  All stop at the first frontier in-neighbour (voting early
+// exit).  Found bits are gathered per word in shared memory and written
+// once per chunk with plain stores: no global atomics on the data path.
 constexpr int PROBE = 4;
 
 __global__ void __launch_bounds__(BLOCK, 4) bfs_pull(BfsP p) {
     Ctl* c = p.s.ctl;
     if (vload(&c->done) || vload(&c->dir) != DIR_PULL) return;
+    grid_begin(c);
     const uint64_t n = p.g.n;
     const uint64_t nw = (n + 31) >> 5;
     uint32_t it = vload(&c->iter);
@@ -172,9 +192,13 @@ __global__ void __launch_bounds__(BLOCK, 4) bfs_pull(BfsP p) {
     Stats st;
     uint32_t dir = DIR_PULL, done = 0;
     const uint32_t lane = lane_id();
+    __shared__ uint32_t s_cand[WARPS][1024];
+    __shared__ uint32_t s_found[WARPS][32];
+    uint32_t* s_c = s_cand[warp_id()];
+    uint32_t* s_f = s_found[warp_id()];
     for (;;) {
-        CntLine* nx = &c->line[(it + 1) % 3];
-        if (lead()) reset_line(&c->line[(it + 2) % 3]);
+        IterLine* nx = &c->line[(it + 1) % 3];
+        maybe_reset_line(&c->line[(it + 2) % 3]);
         clear_bitmap(p.s.bm[(it + 2) % 3], p.s.nwords);
         const uint32_t* cur = p.s.bm[it % 3];
         uint32_t* nbm = p.s.bm[(it + 1) % 3];
@@ -195,116 +219,117 @@ __global__ void __launch_bounds__(BLOCK, 4) bfs_pull(BfsP p) {
             edges += k;
             e += k;
         };
-        // Dynamic chunks of 32 tiles (1024 vertices): one coalesced load brings the
-        // 32 candidate words, empty tiles are skipped by a ballot, and within the
-        // chunk the next tile's row pointers are loaded while the current tile is
-        // probed.  The next chunk index is fetched one chunk ahead.
-        const uint64_t nchunks = (nw + 31) >> 5;
+        const uint32_t nchunks = (uint32_t)((nw + 31) >> 5);
+        uint32_t s_cur = my_slot(), tries = 0;
         uint32_t chunk = 0;
-        if (lane == 0) chunk = atomicAdd(&nx->tile, 1u);
+        if (lane == 0) chunk = grab_chunk(nx, nchunks, s_cur, tries);
         chunk = __shfl_sync(FULL, chunk, 0);
-        while (chunk < nchunks) {
+        while (chunk != INF) {
             uint32_t chunk_n = 0;
-            if (lane == 0) chunk_n = atomicAdd(&nx->tile, 1u);
+            if (lane == 0) chunk_n = grab_chunk(nx, nchunks, s_cur, tries);
             const uint64_t w0 = (uint64_t)chunk << 5;
             const uint64_t wl = w0 + lane;
             const uint32_t vis_l = wl < nw ? p.visited[wl] : FULL;
             const uint32_t cand_l = wl < nw ? (~vis_l & __ldg(p.g.nz_in + wl)) : 0u;
-            uint32_t tiles = __ballot_sync(FULL, cand_l != 0);
-            uint64_t beg = 0, end = 0, beg_n = 0, end_n = 0;
-            uint32_t cand = 0, cand_n = 0;
-            int j = 0, jn = 0;
-            if (tiles) {
-                jn = __ffs(tiles) - 1;
-                tiles &= tiles - 1;
-                cand_n = __shfl_sync(FULL, cand_l, jn);
-                if ((cand_n >> lane) & 1u) {
-                    beg_n = __ldg(p.g.irp + ((w0 + jn) << 5) + lane);
-                    end_n = __ldg(p.g.irp + ((w0 + jn) << 5) + lane + 1);
-                }
+            const uint32_t cnt_l = __popc(cand_l);
+            uint32_t incl = cnt_l;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULL, incl, o);
+                if ((int)lane >= o) incl += y;
             }
-            while (cand_n) {
-                cand = cand_n;
-                j = jn;
-                beg = beg_n;
-                end = end_n;
-                cand_n = 0;
-                beg_n = end_n = 0;
-                if (tiles) {
-                    jn = __ffs(tiles) - 1;
-                    tiles &= tiles - 1;
-                    cand_n = __shfl_sync(FULL, cand_l, jn);
+            const uint32_t total = __shfl_sync(FULL, incl, 31);
+            if (total) {
+                uint32_t pos = incl - cnt_l;
+                for (uint32_t w = cand_l; w; w &= w - 1) s_c[pos++] = (uint32_t)(wl << 5) + (__ffs(w) - 1);
+                s_f[lane] = 0;
+                __syncwarp();
+                uint32_t v_n = 0;
+                uint64_t beg_n = 0, end_n = 0;
+                if (lane < total) {
+                    v_n = s_c[lane];
+                    beg_n = __ldg(p.g.irp + v_n);
+                    end_n = __ldg(p.g.irp + v_n + 1);
                 }
-                const uint64_t wi = w0 + j;
-                const uint32_t v = (uint32_t)(wi << 5) + lane;
-                const bool mine = (cand >> lane) & 1u;
-                bool found = false;
-                uint64_t e = beg;
-                if (mine) probe(e, end, found);  // first round for every candidate
-                if ((cand_n >> lane) & 1u) {
-                    beg_n = __ldg(p.g.irp + ((w0 + jn) << 5) + lane);
-                    end_n = __ldg(p.g.irp + ((w0 + jn) << 5) + lane + 1);
-                }
-                // thread granularity: small candidates continue on their lane
-                const bool small = mine && (end - beg) < p.s.sep_small;
-                if (small) {
-                    ++cand_small;
-                    while (!found && e < end) probe(e, end, found);
-                }
-                // warp granularity: medium / large candidates still open, 32 edges per step
-                uint32_t todo = __ballot_sync(FULL, mine && !small && !found && e < end);
-                while (todo) {
-                    const int l = __ffs(todo) - 1;
-                    todo &= todo - 1;
-                    const uint64_t b0 = __shfl_sync(FULL, e, l), e0 = __shfl_sync(FULL, end, l);
-                    bool hit = false;
-                    for (uint64_t b = b0; b < e0; b += 32) {
-                        const uint64_t x = b + lane;
-                        bool h = false;
-                        if (x < e0) {
-                            ++edges;
-                            h = bm_test(cur, __ldg(p.g.ici + x));
-                        }
-                        if (__any_sync(FULL, h)) {
-                            hit = true;
-                            break;
-                        }
+                for (uint32_t r = 0; r < total; r += 32) {
+                    const bool mine = r + lane < total;
+                    const uint32_t v = v_n;
+                    const uint64_t beg = beg_n, end = end_n;
+                    bool found = false;
+                    uint64_t e = beg;
+                    if (mine) probe(e, end, found);  // first round for every candidate
+                    beg_n = end_n = 0;
+                    if (r + 32 + lane < total) {
+                        v_n = s_c[r + 32 + lane];
+                        beg_n = __ldg(p.g.irp + v_n);
+                        end_n = __ldg(p.g.irp + v_n + 1);
                     }
-                    if ((int)lane == l) found = hit;
-                    ++cand_warp;
+                    // thread granularity: small candidates continue on their lane
+                    const bool small = mine && (end - beg) < p.s.sep_small;
+                    if (small) {
+                        ++cand_small;
+                        while (!found && e < end) probe(e, end, found);
+                    }
+                    // warp granularity: medium / large candidates still open, 32 edges per step
+                    uint32_t todo = __ballot_sync(FULL, mine && !small && !found && e < end);
+                    while (todo) {
+                        const int l = __ffs(todo) - 1;
+                        todo &= todo - 1;
+                        const uint64_t b0 = __shfl_sync(FULL, e, l), e0 = __shfl_sync(FULL, end, l);
+                        bool hit = false;
+                        for (uint64_t b = b0; b < e0; b += 32) {
+                            const uint64_t x = b + lane;
+                            bool h = false;
+                            if (x < e0) {
+                                ++edges;
+                                h = bm_test(cur, __ldg(p.g.ici + x));
+                            }
+                            if (__any_sync(FULL, h)) {
+                                hit = true;
+                                break;
+                            }
+                        }
+                        if ((int)lane == l) found = hit;
+                        ++cand_warp;
+                    }
+                    if (found) {
+                        p.level[v] = lvl;
+                        mdeg += p.sym ? (end - beg) : __ldg(p.g.dout + v);
+                        atomicOr(s_f + ((v >> 5) - w0), 1u << (v & 31));
+                    }
                 }
-                const uint32_t fm = __ballot_sync(FULL, found);
-                if (found) {
-                    p.level[v] = lvl;
-                    mdeg += p.sym ? (end - beg) : __ldg(p.g.dout + v);
-                }
-                const uint32_t vis = __shfl_sync(FULL, vis_l, j);
-                if (lane == 0 && fm) {
-                    p.visited[wi] = vis | fm;  // this warp owns the word during the level
-                    nbm[wi] = fm;
+                __syncwarp();
+                const uint32_t fm = s_f[lane];
+                if (fm) {
+                    p.visited[wl] = vis_l | fm;  // this warp owns the chunk's words during the level
+                    nbm[wl] = fm;
                     found_cnt += __popc(fm);
                 }
+                __syncwarp();
             }
             chunk = __shfl_sync(FULL, chunk_n, 0);
         }
         st.edges += edges;
         st.reached += found_cnt;
         {
-            uint64_t v3[4] = {mdeg, found_cnt, cand_small, cand_warp};
-            block_sum<4>(v3);
+            uint64_t v4[4] = {mdeg, found_cnt, cand_small, cand_warp};
+            block_sum<4>(v4);
             if (threadIdx.x == 0) {
-                if (v3[0]) atomicAdd(&nx->mdeg, (unsigned long long)v3[0]);
-                if (v3[1]) atomicAdd(&nx->found, (unsigned int)v3[1]);
-                if (v3[2]) atomicAdd(&nx->cnt[0], (unsigned int)v3[2]);
-                if (v3[3]) atomicAdd(&nx->cnt[1], (unsigned int)(v3[3] / 32));
+                Slot& sl = nx->s[my_slot()];
+                if (v4[0]) atomicAdd(&sl.mdeg, (unsigned long long)v4[0]);
+                if (v4[1]) atomicAdd(&sl.found, (unsigned int)v4[1]);
+                if (v4[2]) atomicAdd(&sl.cnt[0], (unsigned int)v4[2]);
+                if (v4[3]) atomicAdd(&sl.cnt[1], (unsigned int)(v4[3] / 32));
             }
         }
         st.entries += cand_small + cand_warp / 32;
         st.scanned += (lead() ? nw * 32 : 0);
         if (!grid_sync(c)) return;
-        const uint64_t nf = vload(&nx->found);
-        const uint64_t mf = vload(&nx->mdeg);
-        uint32_t tc[NCLS] = {vload(&nx->cnt[0]), vload(&nx->cnt[1]), 0u, 0u};
+        LineSum ls;
+        read_line(nx, ls);
+        const uint64_t nf = ls.found;
+        const uint64_t mf = ls.mdeg;
+        const uint32_t tc[NCLS] = {ls.cnt[0], ls.cnt[1], 0u, 0u};
         m_u -= mf;
         ++it;
         ++st.iters;
@@ -323,7 +348,7 @@ __global__ void __launch_bounds__(BLOCK, 4) bfs_pull(BfsP p) {
         }
         if (!p.s.fusion) break;
     }
-    bfs_exit(p, DIR_PULL, it, m_u, nf_prev, dir, done, 0u, cnt, st);
+    bfs_exit(p, DIR_PULL, it, m_u, nf_prev, dir, done, 0u, 0u, cnt, st);
 }
 
 }  // namespace sx
@@ -331,10 +356,10 @@ __global__ void __launch_bounds__(BLOCK, 4) bfs_pull(BfsP p) {
 // ------------------------------------------------------------------ host driver
 using namespace sx;
 
-// Algorithmic bytes of the executed BFS schedule:
-// per list entry 4 B (list) + 16 B (row_ptr pair); per examined edge 4 B (col);
-// per reached vertex 4 B (level write); per iteration one frontier-bitmap clear
-// (n/8); per pull iteration one frontier-bitmap read (n/8); ballot scans n/8.
+// Algorithmic bytes of the executed BFS schedule.
+// Push: per list entry 4 B (list) + 16 B (row_ptr pair); per examined edge 4 B
+// (col); per reached vertex 4 B (level write); per iteration one frontier-bitmap
+// clear (n/8); ballot scans n/8 per scanned vertex / 8.
 // Pull (tile scan): per candidate 16 B (row_ptr pair); per examined edge 4 B;
 // per reached vertex 4 B; per iteration visited + in-degree>0 + frontier bitmaps
 // and one bitmap clear (4 n/8).
@@ -367,7 +392,7 @@ extern "C" sx_status sx_bfs(sx_graph g, uint32_t src, const sx_opts* opts, uint3
     SX_CU(cudaMemsetAsync(p.visited, 0, g->nwords * 4, s));
     for (int i = 0; i < 3; ++i) SX_CU(cudaMemsetAsync(p.s.bm[i], 0, g->nwords * 4, s));
     const uint32_t dir0 = run.o.force_dir == 2 ? DIR_PULL : DIR_PUSH;
-    bfs_init<<<1, 1, 0, s>>>(p, src, dir0);
+    bfs_init<<<1, 32, 0, s>>>(p, src, dir0);
     SX_CU(cudaGetLastError());
     void* args[] = {&p};
     // Selective fusion: the direction-optimising BFS runs push -> pull

@@ -112,12 +112,14 @@ Sched make_sched(const sx_graph g, const sx_opts& o) {
     s.sep_small = o.sep_small;
     s.sep_large = o.sep_large;
     s.sep_huge = o.sep_huge;
-    // online capacity per class: threshold x warps of the persistent grid
-    // (the paper's per-thread bin of 64, aggregated per warp)
+    // online capacity per class: threshold x warp slots of the GPU (the paper's
+    // per-thread bin of 64, aggregated per warp), split over NSLOT regions
+    s.R = region_size(g->n);
+    s.cstride = (uint64_t)NSLOT * s.R;
     const uint64_t warps = (uint64_t)g->ctx->prop.multiProcessorCount * (2048 / 32);
-    uint64_t cap = (uint64_t)o.overflow_threshold * warps;
-    if (o.force_filter == 1 || cap > g->n) cap = g->n;  // online only: never overflows
-    s.online_cap = (uint32_t)cap;
+    uint64_t cap = ((uint64_t)o.overflow_threshold * warps + NSLOT - 1) / NSLOT;
+    if (o.force_filter == 1 || cap > s.R) cap = s.R;  // online only: regions are never capped below their size
+    s.cap_s = (uint32_t)cap;
     s.alpha = o.alpha;
     s.beta = o.beta;
     s.force_filter = o.force_filter;

@@ -9,8 +9,13 @@
 namespace sx {
 
 __global__ void __launch_bounds__(BLOCK, 4) barrier_loop(Ctl* c, uint32_t iters) {
+    grid_begin(c);
     for (uint32_t i = 0; i < iters; ++i)
         if (!grid_sync(c)) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        grid_end(c);
+        c->launch += 1;
+    }
 }
 
 }  // namespace sx

@@ -13,16 +13,20 @@
 //                guaranteed co-residency (here: cooperative launch of
 //                occupancy x SMs CTAs; Eq. 1 generalised)
 //
-// B200 design notes:
-//   * The paper's thread-private bins become warp-aggregated slot claims
-//     (__match_any_sync + one atomicAdd per class per warp) into class lists in
-//     global memory (L2-resident); "overflow" = a class list exceeding
-//     overflow_threshold x (warps in the grid) entries, after which recording
-//     only counts (the shadow filter of P:654) and the ballot filter rebuilds the
-//     lists.  Exactly-once claims (atomicOr on the frontier bitmap / an atomic
-//     crossing test) keep online lists duplicate-free.
+// B200 design notes (DESIGN.md has the full rationale):
+//   * Same-address atomics serialise in L2 (~4.5 ns each, measured): every
+//     per-iteration counter is therefore spread over NSLOT = 32 "slots" (one
+//     128-B line each), CTA b writing slot b % 32, readers summing the 32 slots
+//     with one warp-wide load.
+//   * The paper's thread-private bins become 32 slot regions per class
+//     list: a warp claims positions with one atomicAdd per class on its slot's
+//     counter (warp-aggregated with __match_any_sync), so a bin is a (slot,
+//     class) region.  Overflow = a region exceeding overflow_threshold x (warps
+//     of the GPU) / 32 entries; recording then only counts (the shadow filter of
+//     P:654) and the ballot filter rebuilds the lists.  Exactly-once claims
+//     (atomicOr on a bitmap, an atomic crossing test) keep online lists unique.
 //   * The ballot filter scans a frontier BITMAP (one u32 word = 32 vertices, so a
-//     lane's word is already the warp ballot of P:555) or evaluates a per-vertex
+//     lane's word already is the warp ballot of P:555) or evaluates a per-vertex
 //     predicate with __ballot_sync; a two-pass grid-wide scan (per-CTA counts ->
 //     barrier -> offsets) writes class-split lists in ascending vertex order.
 #pragma once
@@ -38,41 +42,49 @@ constexpr uint32_t INF = 0xFFFFFFFFu;
 constexpr uint32_t FULL = 0xFFFFFFFFu;
 constexpr int MAX_GRID = 4096;
 constexpr int TILE_WORDS = BLOCK;  // ballot tile: one bitmap word per thread
+constexpr int NSLOT = 32;          // counter slots (L2 lines) per iteration line
+constexpr int BAR_GROUPS = 32;     // two-level barrier: <= 32 groups of CTAs
 
 enum : uint32_t { DIR_PUSH = 0, DIR_PULL = 1 };
 enum : uint32_t { ERR_NONE = 0, ERR_BARRIER = 7 };
 
 // ---------------------------------------------------------------- control block
-// One 128-B line per contended group so that atomics on different groups do not
-// share an L2 line.
-struct alignas(128) CntLine {
-    unsigned int cnt[NCLS];          // class-list fill counters (online filter)
-    unsigned int found;              // |F'| (vertices activated this iteration)
-    unsigned int pad0;
-    unsigned long long mdeg;         // sum of degrees of activated vertices (m_f)
-    unsigned long long edges;        // edges examined this iteration (trace)
-    double dsum;                     // PageRank dangling mass accumulator
+struct alignas(128) Slot {
+    unsigned int cnt[NCLS];          // online-filter fill counters of this slot's list regions
+    unsigned int found;              // |F'| contributions
     unsigned int minv;               // min reduction scratch (SSSP far min, k-core min residual)
     unsigned int alive;              // k-core alive count
-    unsigned int tile;               // dynamic work counter (chunks of tiles / tasks)
+    unsigned int tile;               // dynamic work counter of this slot's chunk range
+    unsigned long long mdeg;         // sum of degrees of activated vertices (m_f)
+    unsigned long long edges;        // edges examined (trace)
+    double dsum;                     // PageRank dangling mass
+};
+struct IterLine {
+    Slot s[NSLOT];
+};
+struct alignas(128) BarLine {
+    unsigned int count;
 };
 
 struct Ctl {
-    alignas(128) unsigned int bar_count;
-    alignas(128) unsigned int bar_gen;
-    alignas(128) CntLine line[3];    // triple-buffered by iteration (it % 3)
+    // grid barrier state, double-buffered by launch parity (the other half is
+    // zeroed by the exiting kernel, so each launch starts from zero counters)
+    BarLine bar_grp[2][BAR_GROUPS];  // per-group monotonic arrival counters
+    BarLine bar_top[2];              // monotonic count of completed group arrivals
+    IterLine line[3];                // per-iteration counters, triple-buffered (it % 3)
     // --- state carried across launches (written by CTA 0 at exit, read at entry)
     alignas(128) unsigned int iter;  // iterations completed
     unsigned int dir;                // direction of the next launch
     unsigned int done;
     unsigned int error;
     unsigned int lists_ready;        // lists for iteration `iter` exist in the current direction's form
+    unsigned int slotted;            // ... as slotted online lists (counts in line[iter % 3]) or contiguous
     unsigned int launch;             // launches so far
     unsigned int nf_prev;            // previous frontier size (Beamer growth test)
     unsigned int k;                  // k-core level
     unsigned long long m_u;          // BFS: edges incident to unvisited vertices
     unsigned long long hi;           // SSSP: current bucket upper bound (exclusive)
-    unsigned int cur_count[NCLS];    // list sizes for iteration `iter`
+    unsigned int cur_count[NCLS];    // contiguous list sizes for iteration `iter`
     unsigned int ntrace;
     // --- run statistics per direction of the launch (0 push, 1 pull), one atomic per CTA per launch
     struct alignas(128) StatBlock {
@@ -109,14 +121,16 @@ struct DevGraph {
 // Common per-launch parameters of every persistent kernel.
 struct Sched {
     Ctl* ctl;
-    uint32_t* lists[2];     // each: NCLS regions of n entries
+    uint32_t* lists[2];     // each: NCLS class regions of cstride entries
     uint32_t* bm[3];        // frontier bitmaps, rotating by iteration
     uint32_t* cta_cnt;      // [NCLS][MAX_GRID] ballot scratch
     TraceRec* trace;        // device trace buffer or null
     uint32_t trace_cap;
     uint64_t nwords;        // words per bitmap (multiple of TILE_WORDS)
+    uint64_t cstride;       // class region stride = NSLOT * R >= n
+    uint32_t R;             // slot region size
+    uint32_t cap_s;         // online capacity of one (slot, class) region
     uint32_t sep_small, sep_large, sep_huge;
-    uint32_t online_cap;    // per class list
     float alpha, beta;
     int force_filter, force_dir, fusion;
     uint32_t max_iters;
@@ -134,6 +148,8 @@ __device__ __forceinline__ uint64_t gtid() { return (uint64_t)blockIdx.x * BLOCK
 __device__ __forceinline__ uint64_t gthreads() { return (uint64_t)gridDim.x * BLOCK; }
 __device__ __forceinline__ uint64_t gwarp() { return (uint64_t)blockIdx.x * WARPS + warp_id(); }
 __device__ __forceinline__ uint64_t gwarps() { return (uint64_t)gridDim.x * WARPS; }
+__device__ __forceinline__ uint32_t my_slot() { return blockIdx.x % NSLOT; }
+__device__ __forceinline__ bool lead() { return blockIdx.x == 0 && threadIdx.x == 0; }
 
 __device__ __forceinline__ uint32_t ld_acquire(const unsigned int* p) {
     uint32_t v;
@@ -156,46 +172,76 @@ __device__ __forceinline__ uint32_t edge_w(const uint8_t* w8, const uint32_t* w3
 }
 
 // ---------------------------------------------------------------- grid barrier
-// Counter + generation barrier (no monitor CTA).  All CTAs are
-// co-resident (cooperative launch), so it cannot deadlock.  Release
-// on arrive, acquire on depart (gpu scope); the acquire fence also invalidates
-// the SM's L1 so later plain loads see other SMs' writes.  A watchdog
-// (globaltimer, 20 s) turns a broken barrier into SX_E_BARRIER instead of a hang.
-__device__ __forceinline__ bool grid_sync(Ctl* c) {
+// Two-level monotonic-counter barrier (no monitor CTA).  All
+// CTAs are co-resident (cooperative launch), so it cannot deadlock.
+// CTA b arrives on group counter b % G (G <= 32, one L2 line each); the last
+// arriver of a group arrives on the top counter; the k-th barrier of a launch
+// completes when the top counter reaches (k+1) G.  (A flat counter serialises
+// ~1200 same-address atomics: 5.3 us measured on B200.)  fence.acq_rel.gpu
+// before arriving (release) and after the poll (acquire; it also invalidates
+// the SM's L1, so later plain loads see other SMs' writes).  A watchdog
+// (globaltimer, 20 s) turns a broken barrier into SX_E_BARRIER.
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+// The launch parity selecting the barrier half, read once at kernel entry.
+__device__ __forceinline__ uint32_t& bar_parity() {
+    __shared__ uint32_t s_parity;
+    return s_parity;
+}
+__device__ __forceinline__ void grid_begin(Ctl* c) {
+    if (threadIdx.x == 0) bar_parity() = vload(&c->launch) & 1u;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        const uint32_t gen = vload(&c->bar_gen);
-        __threadfence();
-        const uint32_t arrived = atomicAdd(&c->bar_count, 1u);
-        if (arrived == gridDim.x - 1) {
-            atomicExch(&c->bar_count, 0u);
-            __threadfence();
-            atomicAdd(&c->bar_gen, 1u);
-        } else {
-            uint32_t spins = 0;
-            uint64_t t0 = 0;
-            while (ld_acquire(&c->bar_gen) == gen) {
-                if (((++spins) & 1023u) == 0) {
-                    uint64_t t = globaltimer();
-                    if (t0 == 0) t0 = t;
-                    else if (t - t0 > 20000000000ull) { atomicExch(&c->error, ERR_BARRIER); break; }
-                    if (vload(&c->error)) break;
-                }
-            }
-        }
-        __threadfence();
-    }
-    __syncthreads();
-    return vload(&c->error) == 0;
+}
+// Called by CTA 0 thread 0 when the kernel exits: zero the other half for the next launch.
+__device__ __forceinline__ void grid_end(Ctl* c) {
+    const uint32_t q = bar_parity() ^ 1u;
+    for (int i = 0; i < BAR_GROUPS; ++i) c->bar_grp[q][i].count = 0;
+    c->bar_top[q].count = 0;
 }
 
-// ---------------------------------------------------------------- block reductions
+__device__ __forceinline__ bool grid_sync(Ctl* c) {
+    __shared__ uint32_t s_err;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t q = bar_parity();
+        const uint32_t G = gridDim.x < (uint32_t)BAR_GROUPS ? gridDim.x : (uint32_t)BAR_GROUPS;
+        const uint32_t grp = blockIdx.x % G;
+        const uint32_t gsize = (gridDim.x - grp + G - 1) / G;  // CTAs b with b % G == grp
+        fence_acq_rel_gpu();
+        uint32_t err = 0;
+        const uint32_t old = atomicAdd(&c->bar_grp[q][grp].count, 1u);
+        const uint32_t k = old / gsize;
+        if (old - k * gsize == gsize - 1) {
+            fence_acq_rel_gpu();  // acquire the group's arrivals, release them with ours
+            atomicAdd(&c->bar_top[q].count, 1u);
+        }
+        const uint32_t target = (k + 1) * G;
+        uint32_t spins = 0;
+        uint64_t t0 = 0;
+        while ((int32_t)(ld_acquire(&c->bar_top[q].count) - target) < 0) {
+            if (((++spins) & 1023u) == 0) {
+                const uint64_t t = globaltimer();
+                if (t0 == 0) t0 = t;
+                else if (t - t0 > 20000000000ull) atomicExch(&c->error, ERR_BARRIER);
+                if (vload(&c->error)) break;
+            }
+        }
+        fence_acq_rel_gpu();
+        if (spins >= 1023u) err = vload(&c->error);
+        s_err = err;
+    }
+    __syncthreads();
+    return s_err == 0;
+}
+
+// ---------------------------------------------------------------- reductions
 template <class T> __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
     return v;
 }
 __device__ __forceinline__ uint32_t warp_min(uint32_t v) { return __reduce_min_sync(FULL, v); }
+__device__ __forceinline__ uint32_t warp_max(uint32_t v) { return __reduce_max_sync(FULL, v); }
 
 // Sum K values across the block; result valid in every thread.
 template <int K, class T> __device__ __forceinline__ void block_sum(T (&v)[K]) {
@@ -231,21 +277,213 @@ __device__ __forceinline__ uint32_t block_min(uint32_t v) {
     return m;
 }
 
+// ---------------------------------------------------------------- iteration lines
+// Zero an iteration line.  Warp-collective: call from warp 0 of CTA 0 only.
+__device__ __forceinline__ void reset_line_warp(IterLine* L) {
+    Slot& s = L->s[lane_id()];
+#pragma unroll
+    for (int c = 0; c < NCLS; ++c) s.cnt[c] = 0;
+    s.found = 0;
+    s.minv = INF;
+    s.alive = 0;
+    s.tile = 0;
+    s.mdeg = 0;
+    s.edges = 0;
+    s.dsum = 0.0;
+}
+__device__ __forceinline__ void maybe_reset_line(IterLine* L) {
+    if (blockIdx.x == 0 && warp_id() == 0) reset_line_warp(L);
+}
+
+// Sum of one iteration line over its slots, computed by warp 0 and shared.
+struct LineSum {
+    uint32_t cnt[NCLS];
+    uint32_t cntmax[NCLS];
+    uint32_t found, minv, alive;
+    uint64_t mdeg, edges;
+    double dsum;
+};
+__device__ __forceinline__ void read_line(const IterLine* L, LineSum& out) {
+    __shared__ LineSum sh;
+    __syncthreads();
+    if (warp_id() == 0) {
+        const Slot& s = L->s[lane_id()];
+        LineSum r;
+#pragma unroll
+        for (int c = 0; c < NCLS; ++c) {
+            const uint32_t x = vload(&s.cnt[c]);
+            r.cnt[c] = warp_sum(x);
+            r.cntmax[c] = warp_max(x);
+        }
+        r.found = warp_sum(vload(&s.found));
+        r.minv = warp_min(vload(&s.minv));
+        r.alive = warp_sum(vload(&s.alive));
+        r.mdeg = warp_sum((uint64_t)vload(&s.mdeg));
+        r.edges = warp_sum((uint64_t)vload(&s.edges));
+        r.dsum = warp_sum(vload(&s.dsum));
+        if (lane_id() == 0) sh = r;
+    }
+    __syncthreads();
+    out = sh;
+}
+
+// ---------------------------------------------------------------- task views
+struct TaskView;
+__device__ __forceinline__ TaskView& task_view();
+// How the current iteration's class lists are laid out: per class, NSLOT
+// segments (online, slotted) or one contiguous segment (ballot output).
+struct TaskView {
+    uint32_t pre[NCLS][NSLOT + 1];  // exclusive prefix of segment sizes
+    uint32_t base[NCLS][NSLOT];     // segment offsets inside the class region
+};
+__device__ __forceinline__ TaskView& task_view() {
+    __shared__ TaskView tv;
+    return tv;
+}
+// contiguous lists of tot[c] entries (all threads call; ends with __syncthreads)
+__device__ __forceinline__ void view_contig(const uint32_t (&tot)[NCLS]) {
+    TaskView& tv = task_view();
+    __syncthreads();
+    if (warp_id() == 0) {
+        const uint32_t l = lane_id();
+#pragma unroll
+        for (int c = 0; c < NCLS; ++c) {
+            tv.pre[c][l] = l == 0 ? 0u : tot[c];
+            tv.base[c][l] = 0;
+            if (l == 0) tv.pre[c][NSLOT] = tot[c];
+        }
+    }
+    __syncthreads();
+}
+// slotted online lists whose sizes are the line's slot counters (capped)
+__device__ __forceinline__ void view_slots(const IterLine* L, const Sched& s, uint32_t (&tot)[NCLS]) {
+    TaskView& tv = task_view();
+    __shared__ uint32_t sh_tot[NCLS];
+    __syncthreads();
+    if (warp_id() == 0) {
+        const uint32_t l = lane_id();
+#pragma unroll
+        for (int c = 0; c < NCLS; ++c) {
+            const uint32_t x = min(vload(&L->s[l].cnt[c]), s.cap_s);
+            uint32_t inc = x;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULL, inc, o);
+                if ((int)l >= o) inc += y;
+            }
+            tv.pre[c][l] = inc - x;
+            tv.base[c][l] = l * s.R;
+            if (l == 31) {
+                tv.pre[c][NSLOT] = inc;
+                sh_tot[c] = inc;
+            }
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < NCLS; ++c) tot[c] = sh_tot[c];
+}
+// read_line + view_slots in one warp-wide pass over the slots (one L2 round
+// trip after the barrier instead of two).  vcnt receives the view's class sizes.
+__device__ __forceinline__ void read_line_view(const IterLine* L, const Sched& s, LineSum& out, uint32_t (&vcnt)[NCLS]) {
+    __shared__ LineSum sh;
+    __shared__ uint32_t sh_tot[NCLS];
+    TaskView& tv = task_view();
+    __syncthreads();
+    if (warp_id() == 0) {
+        const uint32_t l = lane_id();
+        const Slot& sl = L->s[l];
+        uint32_t x[NCLS];
+#pragma unroll
+        for (int c = 0; c < NCLS; ++c) x[c] = vload(&sl.cnt[c]);
+        const uint32_t found = vload(&sl.found), minv = vload(&sl.minv), alive = vload(&sl.alive);
+        const uint64_t mdeg = vload(&sl.mdeg), edges = vload(&sl.edges);
+        const double dsum = vload(&sl.dsum);
+        LineSum r;
+#pragma unroll
+        for (int c = 0; c < NCLS; ++c) {
+            r.cnt[c] = warp_sum(x[c]);
+            r.cntmax[c] = warp_max(x[c]);
+            const uint32_t xc = min(x[c], s.cap_s);
+            uint32_t inc = xc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULL, inc, o);
+                if ((int)l >= o) inc += y;
+            }
+            tv.pre[c][l] = inc - xc;
+            tv.base[c][l] = l * s.R;
+            if (l == 31) {
+                tv.pre[c][NSLOT] = inc;
+                sh_tot[c] = inc;
+            }
+        }
+        r.found = warp_sum(found);
+        r.minv = warp_min(minv);
+        r.alive = warp_sum(alive);
+        r.mdeg = warp_sum(mdeg);
+        r.edges = warp_sum(edges);
+        r.dsum = warp_sum(dsum);
+        if (l == 0) sh = r;
+    }
+    __syncthreads();
+    out = sh;
+#pragma unroll
+    for (int c = 0; c < NCLS; ++c) vcnt[c] = sh_tot[c];
+}
+
+// the i-th task of class c under the current view
+__device__ __forceinline__ uint32_t task_at(const uint32_t* lists, const Sched& s, uint32_t c, uint32_t i) {
+    const TaskView& tv = task_view();
+    int lo = 0, hi = NSLOT;  // largest lo with pre[lo] <= i
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int mid = (lo + hi) >> 1;
+        if (tv.pre[c][mid] <= i) lo = mid;
+        else hi = mid;
+    }
+    return lists[(uint64_t)c * s.cstride + tv.base[c][lo] + (i - tv.pre[c][lo])];
+}
+
 // ---------------------------------------------------------------- online filter
-// Record vertex u of class c into the next lists.  Warp-aggregated:
-// lanes of the same class share one atomicAdd.  Entries beyond online_cap are
-// not stored (overflow); the counter keeps counting so the JIT
-// controller sees the overflow at the barrier.
-__device__ __forceinline__ void online_record(CntLine* L, uint32_t* lists, uint64_t n, uint32_t cap, uint32_t u,
-                                              uint32_t c) {
+// Record vertex u of class c into the next lists: region (slot of
+// this CTA, class c).  Warp-aggregated: lanes of the same class share one
+// atomicAdd.  Entries beyond cap_s are not stored (overflow); the
+// counter keeps counting so the JIT controller sees the overflow at the barrier.
+__device__ __forceinline__ void online_record(IterLine* L, uint32_t* lists, const Sched& s, uint32_t u, uint32_t c) {
+    const uint32_t slot = my_slot();
     const uint32_t active = __activemask();
     const uint32_t peers = __match_any_sync(active, c);
     const int leader = __ffs(peers) - 1;
     uint32_t base = 0;
-    if ((int)lane_id() == leader) base = atomicAdd(&L->cnt[c], (uint32_t)__popc(peers));
+    if ((int)lane_id() == leader) base = atomicAdd(&L->s[slot].cnt[c], (uint32_t)__popc(peers));
     base = __shfl_sync(peers, base, leader);
     const uint32_t pos = base + __popc(peers & lanemask_lt());
-    if (pos < cap) lists[(uint64_t)c * n + pos] = u;
+    if (pos < s.cap_s) lists[(uint64_t)c * s.cstride + (uint64_t)slot * s.R + pos] = u;
+}
+
+// One CTA-level total added to this CTA's slot (thread 0 after a block_sum).
+template <class T> __device__ __forceinline__ void slot_add(T* field_of_slot0, T v) {
+    // field_of_slot0 points at the field inside slot 0; slots are sizeof(Slot) apart
+    T* p = (T*)((char*)field_of_slot0 + (size_t)my_slot() * sizeof(Slot));
+    if (v) atomicAdd(p, v);
+}
+
+// Dynamic work distribution: chunks [0, nchunks) split into NSLOT ranges; a
+// warp takes chunks from its CTA's slot range, then steals from at most three
+// other slots (an exhausted range is detected with a plain load first).
+__device__ __forceinline__ uint32_t grab_chunk(IterLine* L, uint32_t nchunks, uint32_t& s_cur, uint32_t& tries) {
+    const uint32_t per = (nchunks + NSLOT - 1) / NSLOT;
+    while (tries < 4) {
+        if (vload(&L->s[s_cur].tile) < per) {
+            const uint32_t k = atomicAdd(&L->s[s_cur].tile, 1u);
+            const uint32_t ch = s_cur * per + k;
+            if (k < per && ch < nchunks) return ch;
+        }
+        s_cur = (s_cur + 7 + tries * 6) % NSLOT;
+        ++tries;
+    }
+    return INF;
 }
 
 // ---------------------------------------------------------------- ballot filter
@@ -253,11 +491,6 @@ __device__ __forceinline__ void online_record(CntLine* L, uint32_t* lists, uint6
 struct BitmapWords {  // frontier bitmap
     const uint32_t* bm;
     __device__ __forceinline__ uint32_t word(uint64_t wi) const { return bm[wi]; }
-};
-struct CandidateWords {  // BFS pull candidates: unvisited and in-degree > 0
-    const uint32_t* visited;
-    const uint32_t* nz;
-    __device__ __forceinline__ uint32_t word(uint64_t wi) const { return ~visited[wi] & __ldg(nz + wi); }
 };
 struct AllWords {  // every vertex < n (pull-all algorithms: P:626, ballot in exactly iteration 1)
     uint64_t n;
@@ -288,8 +521,8 @@ template <class Pred> struct BallotWords {
 };
 
 struct BallotOut {
-    uint32_t* lists;      // NCLS regions of n
-    uint64_t n;
+    uint32_t* lists;      // NCLS class regions of cstride entries
+    uint64_t cstride;
     const uint32_t* deg;  // degree used for classification
 };
 
@@ -393,7 +626,7 @@ __device__ void ballot_write(const Src& src, const Sched& s, const BallotOut& ou
             ww &= ww - 1;
             const uint32_t v = (uint32_t)(vb + b);
             const uint32_t c = cls_of(__ldg(out.deg + v), s);
-            out.lists[(uint64_t)c * out.n + pos[c]++] = v;
+            out.lists[(uint64_t)c * out.cstride + pos[c]++] = v;
             on_vertex(v, c);
         }
 #pragma unroll
@@ -453,16 +686,42 @@ __device__ __forceinline__ void for_edges(const uint32_t* __restrict__ col, uint
     for (uint64_t e = a + 4 * nvec + rank; e < end; e += size) fn(e, __ldg(col + e));
 }
 
-// Visit the four class lists with thread / warp / CTA / grid granularity.
-// The functor gets (v, rank, size) and loops over v's edges itself.  Huge
-// vertices (grid-split, B200 addition) go first so the whole GPU shares them,
-// small ones last so they fill the tail.
+// One thread sums term(e, col[e]) over [beg, end) with 16 neighbour ids (four
+// 128-bit loads) and their 16 gathers in flight per step.
+template <class Term>
+__device__ __forceinline__ double seq_sum(const uint32_t* __restrict__ col, uint64_t beg, uint64_t end, Term&& term) {
+    double acc = 0.0;
+    uint64_t e = beg;
+    const uint64_t a = min((uint64_t)((beg + 3) & ~3ull), end);
+    for (; e < a; ++e) acc += term(e, __ldg(col + e));
+    for (; e + 16 <= end; e += 16) {
+        const uint4* c4 = reinterpret_cast<const uint4*>(col + e);
+        const uint4 q0 = __ldg(c4), q1 = __ldg(c4 + 1), q2 = __ldg(c4 + 2), q3 = __ldg(c4 + 3);
+        const double t0 = term(e, q0.x) + term(e + 1, q0.y) + term(e + 2, q0.z) + term(e + 3, q0.w);
+        const double t1 = term(e + 4, q1.x) + term(e + 5, q1.y) + term(e + 6, q1.z) + term(e + 7, q1.w);
+        const double t2 = term(e + 8, q2.x) + term(e + 9, q2.y) + term(e + 10, q2.z) + term(e + 11, q2.w);
+        const double t3 = term(e + 12, q3.x) + term(e + 13, q3.y) + term(e + 14, q3.z) + term(e + 15, q3.w);
+        acc += (t0 + t1) + (t2 + t3);
+    }
+    for (; e + 4 <= end; e += 4) {
+        const uint4 q = __ldg(reinterpret_cast<const uint4*>(col + e));
+        acc += term(e, q.x) + term(e + 1, q.y) + term(e + 2, q.z) + term(e + 3, q.w);
+    }
+    for (; e < end; ++e) acc += term(e, __ldg(col + e));
+    return acc;
+}
+
+// Visit the four class lists of the current view with thread / warp / CTA /
+// grid granularity.  The functor gets (v, rank, size, class) and loops
+// over v's edges itself.  Huge vertices (grid-split, B200 addition) go first so
+// the whole GPU shares them, small ones last so they fill the tail.
 template <class VFn>
-__device__ __forceinline__ void for_tasks(const uint32_t* lists, uint64_t n, const uint32_t (&cnt)[NCLS], VFn&& vf) {
-    for (uint32_t i = 0; i < cnt[3]; ++i) vf(lists[3 * n + i], gtid(), gthreads(), 3u);
-    for (uint32_t i = blockIdx.x; i < cnt[2]; i += gridDim.x) vf(lists[2 * n + i], (uint64_t)threadIdx.x, (uint64_t)BLOCK, 2u);
-    for (uint64_t i = gwarp(); i < cnt[1]; i += gwarps()) vf(lists[n + i], (uint64_t)lane_id(), 32ull, 1u);
-    for (uint64_t i = gtid(); i < cnt[0]; i += gthreads()) vf(lists[i], 0ull, 1ull, 0u);
+__device__ __forceinline__ void for_tasks(const uint32_t* lists, const Sched& s, const uint32_t (&cnt)[NCLS], VFn&& vf) {
+    for (uint32_t i = 0; i < cnt[3]; ++i) vf(task_at(lists, s, 3, i), gtid(), gthreads(), 3u);
+    for (uint32_t i = blockIdx.x; i < cnt[2]; i += gridDim.x)
+        vf(task_at(lists, s, 2, i), (uint64_t)threadIdx.x, (uint64_t)BLOCK, 2u);
+    for (uint64_t i = gwarp(); i < cnt[1]; i += gwarps()) vf(task_at(lists, s, 1, (uint32_t)i), (uint64_t)lane_id(), 32ull, 1u);
+    for (uint64_t i = gtid(); i < cnt[0]; i += gthreads()) vf(task_at(lists, s, 0, (uint32_t)i), 0ull, 1ull, 0u);
 }
 
 // ---------------------------------------------------------------- bookkeeping
@@ -488,20 +747,6 @@ __device__ __forceinline__ void flush_stats(Ctl* c, Stats& st, uint32_t dir) {
         }
     }
 }
-
-__device__ __forceinline__ void reset_line(CntLine* L) {
-#pragma unroll
-    for (int c = 0; c < NCLS; ++c) L->cnt[c] = 0;
-    L->found = 0;
-    L->mdeg = 0;
-    L->edges = 0;
-    L->dsum = 0.0;
-    L->minv = INF;
-    L->alive = 0;
-    L->tile = 0;
-}
-
-__device__ __forceinline__ bool lead() { return blockIdx.x == 0 && threadIdx.x == 0; }
 
 __device__ __forceinline__ void trace_put(const Sched& s, uint32_t iter, uint32_t dir, uint32_t filter,
                                           const uint32_t (&cnt)[NCLS], uint64_t nf, uint64_t mf, uint64_t aux) {

@@ -167,7 +167,7 @@ sx_status sx_graph_upload(sx_ctx ctx, const sx_csr_desc* d, sx_graph* out) {
     TRY(dalloc(&g->nz_in, g->nwords));
     k_nz_bitmap<<<vg, vb, 0, s>>>(g->din, n, g->nwords, g->nz_in);
     // workspace
-    for (int i = 0; i < 2; ++i) TRY(dalloc(&g->lists[i], NCLS * (n ? n : 1)));
+    for (int i = 0; i < 2; ++i) TRY(dalloc(&g->lists[i], (uint64_t)NCLS * NSLOT * sxh::region_size(n)));
     for (int i = 0; i < 3; ++i) TRY(dalloc(&g->bm[i], g->nwords));
     TRY(dalloc(&g->aux_bm, g->nwords));
     TRY(dalloc(&g->cta_cnt, NCLS * MAX_GRID));
@@ -213,6 +213,8 @@ void sx_graph_free(sx_graph g) {
     for (auto* p : g->st) cudaFree(p);
     cudaFree(g->hacc);
     cudaFree(g->dstate);
+    cudaFree(g->loff);
+    cudaFree(g->scratch64);
     delete g;
 }
 

@@ -47,6 +47,8 @@ struct sx_graph_s {
     uint32_t* st[4] = {nullptr, nullptr, nullptr, nullptr};  // 4N-byte state arrays
     double* hacc = nullptr;       // n doubles, pull-all huge accumulators (lazy)
     double* dstate = nullptr;     // 2n doubles, BP beliefs (lazy)
+    uint64_t* loff = nullptr;     // n+1 prefix sums, pull-all big-list stream (lazy)
+    uint64_t* scratch64 = nullptr; // MAX_GRID u64 scan scratch (lazy)
 };
 
 namespace sxh {
@@ -60,6 +62,8 @@ sx_status cuda_fail(cudaError_t e, const char* what);
     } while (0)
 
 sx::DevGraph dev_graph(const sx_graph g);
+// Slot region size of a class list: NSLOT regions of R entries cover n.
+inline uint32_t region_size(uint64_t n) { return (uint32_t)((n + sx::NSLOT - 1) / sx::NSLOT + 3) & ~3u; }
 // Fill the scheduling parameters common to every persistent kernel.
 sx::Sched make_sched(const sx_graph g, const sx_opts& o);
 sx_opts resolve_opts(const sx_opts* o);

@@ -29,11 +29,14 @@ struct KcoreP {
 
 __global__ void kcore_init(KcoreP p) {
     Ctl* c = p.s.ctl;
-    for (int i = 0; i < 3; ++i) reset_line(&c->line[i]);
+    if (threadIdx.x < 32)
+        for (int i = 0; i < 3; ++i) reset_line_warp(&c->line[i]);
+    if (threadIdx.x != 0) return;
     for (int i = 0; i < NCLS; ++i) c->cur_count[i] = 0;
     c->k = 0;
     c->iter = 0;
     c->done = 0;
+    c->slotted = 0;
     c->dir = DIR_PUSH;
 }
 
@@ -52,16 +55,23 @@ struct LevelPred {
 __global__ void __launch_bounds__(BLOCK, 4) kcore_push(KcoreP p) {
     Ctl* c = p.s.ctl;
     if (vload(&c->done)) return;
+    grid_begin(c);
     const uint64_t n = p.g.n;
     uint32_t it = vload(&c->iter);
     uint32_t k = vload(&c->k);
     uint32_t cnt[NCLS];
-    for (int i = 0; i < NCLS; ++i) cnt[i] = vload(&c->cur_count[i]);
+    uint32_t slotted = vload(&c->slotted);
+    if (slotted) {
+        view_slots(&c->line[it % 3], p.s, cnt);
+    } else {
+        for (int i = 0; i < NCLS; ++i) cnt[i] = vload(&c->cur_count[i]);
+        view_contig(cnt);
+    }
     Stats st;
     uint32_t done = 0;
     bool level_started = it > 0 || sum4(cnt) > 0;
     for (;;) {
-        CntLine* nx = &c->line[(it + 1) % 3];
+        IterLine* nx = &c->line[(it + 1) % 3];
         if (sum4(cnt) == 0) {
             // ---- level start: min residual degree over alive vertices
             if (p.kfix && level_started) {
@@ -83,14 +93,16 @@ __global__ void __launch_bounds__(BLOCK, 4) kcore_push(KcoreP p) {
                 alive = a[0];
             }
             if (threadIdx.x == 0) {
-                if (mn != INF) atomicMin(&nx->minv, mn);
-                if (alive) atomicAdd(&nx->alive, (unsigned int)alive);
+                Slot& sl = nx->s[my_slot()];
+                if (mn != INF) atomicMin(&sl.minv, mn);
+                if (alive) atomicAdd(&sl.alive, (unsigned int)alive);
             }
             st.scanned += n;
             if (!grid_sync(c)) return;
-            mn = vload(&nx->minv);
-            const uint32_t nalive = vload(&nx->alive);
-            if (nalive == 0) {
+            LineSum ls;
+            read_line(nx, ls);
+            mn = ls.minv;
+            if (ls.alive == 0) {
                 done = 1;
                 break;
             }
@@ -108,20 +120,21 @@ __global__ void __launch_bounds__(BLOCK, 4) kcore_push(KcoreP p) {
             ++st.ballot;
             st.scanned += n;
             BallotWords<LevelPred> src{LevelPred{p.core, p.res, k}, n};
-            if (!ballot_filter(src, p.s, BallotOut{p.s.lists[it & 1], n, p.g.dout}, cnt,
+            if (!ballot_filter(src, p.s, BallotOut{p.s.lists[it & 1], p.s.cstride, p.g.dout}, cnt,
                                [&](uint32_t v, uint32_t) { p.core[v] = k; }))
                 return;
             if (!grid_sync(c)) return;
+            view_contig(cnt);
             trace_put(p.s, it, DIR_PUSH, 1u, cnt, sum4(cnt), 0, k);
         }
         // ---- one sub-round: removals push -1 to alive neighbours
-        if (lead()) reset_line(&c->line[(it + 2) % 3]);
+        maybe_reset_line(&c->line[(it + 2) % 3]);
         clear_bitmap(p.s.bm[(it + 2) % 3], p.s.nwords);
         uint32_t* nlists = p.s.lists[(it + 1) & 1];
         uint32_t* nbm = p.s.bm[(it + 1) % 3];
         uint64_t edges = 0;
         const uint32_t kk = k;
-        for_tasks(p.s.lists[it & 1], n, cnt, [&](uint32_t v, uint64_t rank, uint64_t size, uint32_t) {
+        for_tasks(p.s.lists[it & 1], p.s, cnt, [&](uint32_t v, uint64_t rank, uint64_t size, uint32_t) {
             const uint64_t beg = __ldg(p.g.rp + v), end = __ldg(p.g.rp + v + 1);
             for_edges(p.g.ci, beg, end, rank, size, [&](uint64_t, uint32_t u) {
                 ++edges;
@@ -130,29 +143,33 @@ __global__ void __launch_bounds__(BLOCK, 4) kcore_push(KcoreP p) {
                 if (old == kk + 1) {
                     p.core[u] = kk;
                     bm_set(nbm, u);
-                    online_record(nx, nlists, n, p.s.online_cap, u, cls_of(__ldg(p.g.dout + u), p.s));
+                    online_record(nx, nlists, p.s, u, cls_of(__ldg(p.g.dout + u), p.s));
                 }
             });
         });
         st.edges += edges;
         if (lead()) st.entries += sum4(cnt);
         if (!grid_sync(c)) return;
-        uint32_t ncnt[NCLS];
-        for (int i = 0; i < NCLS; ++i) ncnt[i] = vload(&nx->cnt[i]);
-        const uint64_t nf = sum4(ncnt);
+        LineSum ls;
+        uint32_t vcnt[NCLS];
+        read_line_view(nx, p.s, ls, vcnt);
+        const uint64_t nf = sum4(ls.cnt);
         bool overflow = false;
-        for (int i = 0; i < NCLS; ++i) overflow |= ncnt[i] > p.s.online_cap;
+        for (int i = 0; i < NCLS; ++i) overflow |= ls.cntmax[i] > p.s.cap_s;
         if (p.s.force_filter == 2) overflow = true;
         ++it;
         ++st.iters;
-        trace_put(p.s, it, DIR_PUSH, overflow ? 1u : 0u, ncnt, nf, 0, k);
+        trace_put(p.s, it, DIR_PUSH, overflow ? 1u : 0u, ls.cnt, nf, 0, k);
         if (nf > 0 && overflow) {
             ++st.ballot;
             st.scanned += p.s.nwords * 32;
-            if (!ballot_filter(BitmapWords{nbm}, p.s, BallotOut{p.s.lists[it & 1], n, p.g.dout}, cnt)) return;
+            if (!ballot_filter(BitmapWords{nbm}, p.s, BallotOut{p.s.lists[it & 1], p.s.cstride, p.g.dout}, cnt)) return;
             if (!grid_sync(c)) return;
+            view_contig(cnt);
+            slotted = 0;
         } else {
-            for (int i = 0; i < NCLS; ++i) cnt[i] = ncnt[i];
+            for (int i = 0; i < NCLS; ++i) cnt[i] = vcnt[i];  // view set by read_line_view
+            slotted = 1;
         }
         if (p.s.max_iters && it >= p.s.max_iters) {
             done = 1;
@@ -165,7 +182,9 @@ __global__ void __launch_bounds__(BLOCK, 4) kcore_push(KcoreP p) {
         c->iter = it;
         c->k = k;
         c->done = done;
+        c->slotted = slotted;
         for (int i = 0; i < NCLS; ++i) c->cur_count[i] = cnt[i];
+        grid_end(c);
         c->launch += 1;
     }
 }
@@ -206,7 +225,7 @@ extern "C" sx_status sx_kcore(sx_graph g, uint32_t k, const sx_opts* opts, uint3
     for (int i = 0; i < 3; ++i) SX_CU(cudaMemsetAsync(p.s.bm[i], 0, g->nwords * 4, s));
     const int eg = 4 * g->ctx->prop.multiProcessorCount;
     k_copy_deg<<<eg, 256, 0, s>>>(g->dout, g->n, p.res);
-    kcore_init<<<1, 1, 0, s>>>(p);
+    kcore_init<<<1, 32, 0, s>>>(p);
     SX_CU(cudaGetLastError());
     void* args[] = {&p};
     g->ctx->h_ctl->done = 0;
@@ -216,8 +235,13 @@ extern "C" sx_status sx_kcore(sx_graph g, uint32_t k, const sx_opts* opts, uint3
         if (g->ctx->h_ctl->done) break;
     }
     if ((rc = run.end(kcore_bytes)) != SX_OK) return rc;
-    uint32_t* tmp = g->st[2];
-    k_kcore_out<<<eg, 256, 0, s>>>(p.core, g->n, k, tmp);
+    const bool dev_out = sxh::is_device_ptr(core_out);
+    uint32_t* out = dev_out ? core_out : g->st[2];
+    k_kcore_out<<<eg, 256, 0, s>>>(p.core, g->n, k, out);
     SX_CU(cudaGetLastError());
-    return sxh::copy_out(g, core_out, tmp, g->n * 4);
+    if (dev_out) {
+        SX_CU(cudaStreamSynchronize(s));
+        return SX_OK;
+    }
+    return sxh::copy_out(g, core_out, out, g->n * 4);
 }

@@ -25,15 +25,18 @@ struct SsspP {
 
 __global__ void sssp_init(SsspP p, uint32_t src) {
     Ctl* c = p.s.ctl;
-    for (int i = 0; i < 3; ++i) reset_line(&c->line[i]);
+    if (threadIdx.x < 32)
+        for (int i = 0; i < 3; ++i) reset_line_warp(&c->line[i]);
+    if (threadIdx.x != 0) return;
     p.dist[src] = 0;
     const uint32_t k = cls_of(p.g.dout[src], p.s);
     for (int i = 0; i < NCLS; ++i) c->cur_count[i] = 0;
     c->cur_count[k] = 1;
-    p.s.lists[0][(uint64_t)k * p.g.n] = src;
+    p.s.lists[0][(uint64_t)k * p.s.cstride] = src;
     c->hi = p.delta ? (unsigned long long)p.delta : 0xFFFFFFFFull + 1;
     c->dir = DIR_PUSH;
     c->lists_ready = 1;
+    c->slotted = 0;
     c->iter = 0;
     c->done = 0;
 }
@@ -57,21 +60,27 @@ struct FarWords {
 __global__ void __launch_bounds__(BLOCK, 4) sssp_push(SsspP p) {
     Ctl* c = p.s.ctl;
     if (vload(&c->done)) return;
-    const uint64_t n = p.g.n;
+    grid_begin(c);
     uint32_t it = vload(&c->iter);
     uint64_t hi = vload(&c->hi);
     uint32_t cnt[NCLS];
-    for (int i = 0; i < NCLS; ++i) cnt[i] = vload(&c->cur_count[i]);
+    uint32_t slotted = vload(&c->slotted);
+    if (slotted) {
+        view_slots(&c->line[it % 3], p.s, cnt);
+    } else {
+        for (int i = 0; i < NCLS; ++i) cnt[i] = vload(&c->cur_count[i]);
+        view_contig(cnt);
+    }
     Stats st;
     uint32_t done = 0;
     for (;;) {
-        CntLine* nx = &c->line[(it + 1) % 3];
-        if (lead()) reset_line(&c->line[(it + 2) % 3]);
+        IterLine* nx = &c->line[(it + 1) % 3];
+        maybe_reset_line(&c->line[(it + 2) % 3]);
         clear_bitmap(p.s.bm[(it + 2) % 3], p.s.nwords);
         uint32_t* nlists = p.s.lists[(it + 1) & 1];
         uint32_t* nbm = p.s.bm[(it + 1) % 3];
         uint64_t edges = 0;
-        for_tasks(p.s.lists[it & 1], n, cnt, [&](uint32_t v, uint64_t rank, uint64_t size, uint32_t) {
+        for_tasks(p.s.lists[it & 1], p.s, cnt, [&](uint32_t v, uint64_t rank, uint64_t size, uint32_t) {
             const uint64_t beg = __ldg(p.g.rp + v), end = __ldg(p.g.rp + v + 1);
             const uint32_t dv = p.dist[v];
             for_edges(p.g.ci, beg, end, rank, size, [&](uint64_t e, uint32_t u) {
@@ -81,7 +90,7 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_push(SsspP p) {
                 const uint32_t old = atomicMin(p.dist + u, nd);
                 if (nd >= old) return;
                 if ((uint64_t)nd < hi) {
-                    if (bm_claim(nbm, u)) online_record(nx, nlists, n, p.s.online_cap, u, cls_of(__ldg(p.g.dout + u), p.s));
+                    if (bm_claim(nbm, u)) online_record(nx, nlists, p.s, u, cls_of(__ldg(p.g.dout + u), p.s));
                 } else {
                     bm_set(p.far, u);
                 }
@@ -90,11 +99,12 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_push(SsspP p) {
         st.edges += edges;
         if (lead()) st.entries += sum4(cnt);
         if (!grid_sync(c)) return;
-        uint32_t ncnt[NCLS];
-        for (int i = 0; i < NCLS; ++i) ncnt[i] = vload(&nx->cnt[i]);
-        const uint64_t nf = sum4(ncnt);
+        LineSum ls;
+        uint32_t vcnt[NCLS];
+        read_line_view(nx, p.s, ls, vcnt);
+        const uint64_t nf = sum4(ls.cnt);
         bool overflow = false;
-        for (int i = 0; i < NCLS; ++i) overflow |= ncnt[i] > p.s.online_cap;
+        for (int i = 0; i < NCLS; ++i) overflow |= ls.cntmax[i] > p.s.cap_s;
         if (p.s.force_filter == 2) overflow = true;
         ++it;
         ++st.iters;
@@ -102,10 +112,13 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_push(SsspP p) {
         if (nf > 0 && overflow) {
             ++st.ballot;
             st.scanned += p.s.nwords * 32;
-            if (!ballot_filter(BitmapWords{nbm}, p.s, BallotOut{p.s.lists[it & 1], n, p.g.dout}, cnt)) return;
+            if (!ballot_filter(BitmapWords{nbm}, p.s, BallotOut{p.s.lists[it & 1], p.s.cstride, p.g.dout}, cnt)) return;
             if (!grid_sync(c)) return;
+            view_contig(cnt);
+            slotted = 0;
         } else {
-            for (int i = 0; i < NCLS; ++i) cnt[i] = ncnt[i];
+            for (int i = 0; i < NCLS; ++i) cnt[i] = vcnt[i];  // view set by read_line_view
+            slotted = 1;
         }
         if (nf == 0) {
             if (p.delta == 0) {
@@ -113,7 +126,7 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_push(SsspP p) {
                 done = 1;
                 break;
             }
-            // bucket advance: min distance over the far pile
+            // bucket advance: min distance over the far pile (into this line's minv slots)
             uint32_t mn = INF;
             for (uint64_t wi = gtid(); wi < p.s.nwords; wi += gthreads()) {
                 uint32_t w = p.far[wi];
@@ -124,10 +137,11 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_push(SsspP p) {
                 }
             }
             mn = block_min(mn);
-            if (threadIdx.x == 0 && mn != INF) atomicMin(&nx->minv, mn);
+            if (threadIdx.x == 0 && mn != INF) atomicMin(&nx->s[my_slot()].minv, mn);
             st.scanned += p.s.nwords * 32;
             if (!grid_sync(c)) return;
-            mn = vload(&nx->minv);
+            read_line(nx, ls);
+            mn = ls.minv;
             if (mn == INF) {
                 trace_put(p.s, it, DIR_PUSH, filt, cnt, nf, 0, hi);
                 done = 1;
@@ -136,10 +150,12 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_push(SsspP p) {
             hi = ((uint64_t)mn / p.delta + 1) * p.delta;
             ++st.ballot;
             FarWords src{p.far, p.dist, hi};
-            if (!ballot_filter(src, p.s, BallotOut{p.s.lists[it & 1], n, p.g.dout}, cnt,
+            if (!ballot_filter(src, p.s, BallotOut{p.s.lists[it & 1], p.s.cstride, p.g.dout}, cnt,
                                [&](uint32_t v, uint32_t) { p.far[v >> 5] &= ~(1u << (v & 31)); }))
                 return;
             if (!grid_sync(c)) return;
+            view_contig(cnt);
+            slotted = 0;
             filt = 1;
         }
         trace_put(p.s, it, DIR_PUSH, filt, cnt, nf, 0, hi);
@@ -154,7 +170,9 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_push(SsspP p) {
         c->iter = it;
         c->hi = hi;
         c->done = done;
+        c->slotted = slotted;
         for (int i = 0; i < NCLS; ++i) c->cur_count[i] = cnt[i];
+        grid_end(c);
         c->launch += 1;
     }
 }
@@ -186,13 +204,14 @@ extern "C" sx_status sx_sssp(sx_graph g, uint32_t src, uint32_t delta, const sx_
     if ((rc = run.begin()) != SX_OK) return rc;
     p.g = sxh::dev_graph(g);
     p.s = sxh::make_sched(g, run.o);
-    p.dist = g->st[0];
+    const bool dev_out = sxh::is_device_ptr(dist_out);
+    p.dist = dev_out ? dist_out : g->st[0];
     p.far = g->aux_bm;
     p.delta = delta;
     SX_CU(cudaMemsetAsync(p.dist, 0xFF, g->n * 4, s));
     SX_CU(cudaMemsetAsync(p.far, 0, g->nwords * 4, s));
     for (int i = 0; i < 3; ++i) SX_CU(cudaMemsetAsync(p.s.bm[i], 0, g->nwords * 4, s));
-    sssp_init<<<1, 1, 0, s>>>(p, src);
+    sssp_init<<<1, 32, 0, s>>>(p, src);
     SX_CU(cudaGetLastError());
     void* args[] = {&p};
     g->ctx->h_ctl->done = 0;
@@ -202,5 +221,5 @@ extern "C" sx_status sx_sssp(sx_graph g, uint32_t src, uint32_t delta, const sx_
         if (g->ctx->h_ctl->done) break;
     }
     if ((rc = run.end(sssp_bytes)) != SX_OK) return rc;
-    return sxh::copy_out(g, dist_out, p.dist, g->n * 4);
+    return dev_out ? SX_OK : sxh::copy_out(g, dist_out, p.dist, g->n * 4);
 }
