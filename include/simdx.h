@@ -219,6 +219,56 @@ sx_status sx_spmv(sx_graph g, const float* x, uint32_t iters, const sx_opts* opt
 sx_status sx_bp(sx_graph g, const float* prior, uint32_t iters, const sx_opts* opts, float* logodds_out,
                 sx_stats* stats);
 
+/* ------------------------------------------------------------ multi-GPU layer
+ * SURVEY.md §8(e); the paper itself is single-GPU.  1D vertex-range
+ * partition: rank r of P owns vertices [r V, min(n, (r+1) V)), V = ceil(n/P)
+ * rounded up to a multiple of 32.  Each rank holds the CSR rows of its owned
+ * vertices with GLOBAL column ids (symmetric graphs: those rows are also the
+ * in-rows used by pull).  Per BSP level the ranks exchange frontier-bitmap
+ * slices (allgather for pull, alltoall + local OR for push), SSSP candidate
+ * distances (reduce-scatter with min) and the (|F'|, m_f) counters (allreduce),
+ * all on the ctx stream.  Collective: every rank calls the same function with
+ * the same arguments (except its own slice / outputs).
+ */
+typedef struct sx_dist_s* sx_dist;
+
+/* 128-byte NCCL unique id for ncclCommInitRank; rank 0 creates it and the
+ * caller broadcasts it (e.g. with torch.distributed).  Errors: SX_E_NCCL. */
+sx_status sx_nccl_unique_id(void* out128);
+
+/*
+ * Create the distribution of an n_global-vertex graph over `nranks` ranks, of
+ * which this process drives ranks [rank0, rank0 + nlocal):
+ *   nlocal == 1 (nranks > 1): one rank per process, exchanges over an NCCL
+ *     communicator built from `nccl_id` (one process per GPU, NVLink/NVSwitch);
+ *   nlocal == nranks: every rank in this process on the ctx's device ("virtual
+ *     ranks": the same kernels and schedule, device-to-device copies in place
+ *     of the collectives; for tests of the partitioned path on one GPU).
+ * Errors: SX_E_INVALID (bad layout), SX_E_NCCL, SX_E_OOM, SX_E_CUDA.
+ */
+sx_status sx_dist_create(sx_ctx ctx, uint64_t n_global, int nranks, int rank0, int nlocal, const void* nccl_id,
+                         sx_dist* out);
+/* Owned vertex range [v_begin, v_end) of local rank `local_rank`. */
+sx_status sx_dist_range(sx_dist d, int local_rank, uint64_t* v_begin, uint64_t* v_end);
+/*
+ * Upload local rank `local_rank`'s slice: desc->n = owned row count (v_end -
+ * v_begin), desc->row_ptr local (starting at 0), desc->col GLOBAL ids < n_global,
+ * desc->w optional (same width on every rank).  Symmetric graphs only.
+ * Copies; validates like sx_graph_upload.  Errors: SX_E_INVALID, SX_E_OOM.
+ */
+sx_status sx_dist_upload(sx_dist d, int local_rank, const sx_csr_desc* desc);
+/* Free (collective for NCCL communicators; NULL is a no-op). */
+void sx_dist_free(sx_dist d);
+/*
+ * Distributed BFS with the push/pull switch (Beamer
+ * alpha/beta from opts): level_out[i] receives local rank i's owned slice
+ * (v_end - v_begin entries, host or device).  Errors as sx_bfs.
+ */
+sx_status sx_dist_bfs(sx_dist d, uint32_t src, const sx_opts* opts, uint32_t* const* level_out, sx_stats* stats);
+/* Distributed SSSP, delta-stepping as sx_sssp; dist_out[i] = local rank i's owned slice. */
+sx_status sx_dist_sssp(sx_dist d, uint32_t src, uint32_t delta, const sx_opts* opts, uint32_t* const* dist_out,
+                       sx_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

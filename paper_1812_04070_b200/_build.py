@@ -14,6 +14,23 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-Xcompiler", "-O2", "-shared", "-diag-suppress", "177,550"]
 
 
+def nccl_dir() -> str:
+    """NCCL 2.28 shipped with the torch wheel (nvidia-nccl-cu12): headers + libnccl.so.2."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in (spec.submodule_search_locations if spec else []):
+        d = os.path.join(base, "nccl")
+        if os.path.exists(os.path.join(d, "include", "nccl.h")):
+            return d
+    raise RuntimeError("nccl.h not found (expected the nvidia-nccl wheel next to torch)")
+
+
+def link_flags():
+    d = nccl_dir()
+    lib = os.path.join(d, "lib")
+    return ["-I", os.path.join(d, "include"), "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib}"]
+
+
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
@@ -28,7 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         t = os.path.getmtime(LIB)
         if all(os.path.getmtime(d) <= t for d in deps()):
             return LIB
-    cmd = [NVCC, *FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-o", LIB + ".tmp", *sources()]
+    cmd = [NVCC, *FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-o", LIB + ".tmp", *sources(), *link_flags()]
     subprocess.check_call(cmd)
     os.replace(LIB + ".tmp", LIB)
     return LIB

@@ -1,0 +1,833 @@
+// dist.cu — the multi-GPU layer.
+//
+// 1D vertex-range partition: rank r owns vertices [r*V, min(N, (r+1)*V)), V =
+// ceil(N/P) rounded up to a multiple of 32 so every bitmap slice is whole
+// words.  Each rank holds the CSR rows of its owned vertices with GLOBAL column
+// ids (for a symmetric graph those rows are also the in-neighbour rows).
+// Traversal shards naturally by vertex range; the per-iteration exchange is:
+//   BFS pull level : allgather of the frontier-bitmap slices (N/8/P bytes each),
+//                    then a local bottom-up pass over owned unvisited vertices;
+//   BFS push level : each rank marks targets in a global-size bitmap; alltoall of
+//                    the per-owner slices; the owner ORs them and keeps the
+//                    unvisited bits (NCCL has no bitwise-OR reduction);
+//   SSSP iteration : candidate distances for remote targets min-combined into a
+//                    global-size array, reduce-scatter(min) to the owners;
+//   every level    : allreduce of (|F'|, m_f) — termination and the Beamer
+//                    direction decision are taken identically on every rank.
+// Exchange backends: NCCL (one rank per process, ncclComm from a unique id the
+// caller broadcasts, collectives on the ctx stream) or, with all ranks in one
+// process on one device ("virtual ranks", for tests), the same schedule with
+// device-to-device copies standing in for the collectives.
+#include <nccl.h>
+
+#include <cstring>
+#include <vector>
+
+#include "internal.h"
+
+using namespace sx;
+
+namespace {
+
+constexpr int DIST_MAX_LOCAL = 64;
+constexpr int KGRID_PER_SM = 4;
+
+struct DistRank {
+    uint64_t nl = 0, ml = 0, lo = 0;  // owned rows, local edges, first owned vertex
+    uint64_t* rp = nullptr;
+    uint32_t* ci = nullptr;
+    void* w = nullptr;
+    uint32_t* deg = nullptr;          // out-degree of owned rows
+    uint32_t* nz = nullptr;           // owned words: degree > 0
+    uint32_t* state = nullptr;        // level / dist of owned rows
+    uint32_t* visited = nullptr;      // owned words (BFS visited / SSSP far pile)
+    uint32_t* front[2] = {nullptr, nullptr};  // owned words
+    uint32_t* gfront = nullptr;       // NW global words (pull: allgathered frontier)
+    uint32_t* sendmap = nullptr;      // NW global words (push targets)
+    uint32_t* recv = nullptr;         // P * nwl words (alltoall receive)
+    uint32_t* sendbest = nullptr;     // P * V candidate distances (SSSP, lazy)
+    uint32_t* recvbest = nullptr;     // V (SSSP, lazy)
+    unsigned long long* cnt = nullptr;  // device counters
+    bool has_zero_w = false;
+};
+
+}  // namespace
+
+struct sx_dist_s {
+    sx_ctx ctx = nullptr;
+    int P = 1, rank0 = 0, nlocal = 1;
+    uint64_t N = 0, V = 0, nwl = 0, NW = 0;
+    uint32_t wbytes = 0;
+    bool nccl = false;
+    ncclComm_t comm = nullptr;
+    DistRank r[DIST_MAX_LOCAL];
+    unsigned long long* hcnt = nullptr;  // pinned host counters [nlocal][8]
+    unsigned long long* dred = nullptr;  // device allreduce buffer (8)
+};
+
+namespace {
+
+sx_status nccl_fail(ncclResult_t r, const char* what) {
+    return sxh::fail(SX_E_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
+}
+#define SX_NC(call)                                               \
+    do {                                                          \
+        ncclResult_t r__ = (call);                                \
+        if (r__ != ncclSuccess) return nccl_fail(r__, #call);     \
+    } while (0)
+
+template <class T> sx_status dmalloc(T** p, size_t count) {
+    cudaError_t e = cudaMalloc((void**)p, (count ? count : 1) * sizeof(T));
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        return sxh::cuda_fail(e, "cudaMalloc");
+    }
+    return SX_OK;
+}
+
+int kgrid(sx_dist d) { return KGRID_PER_SM * d->ctx->prop.multiProcessorCount; }
+
+// ------------------------------------------------------------------ kernels
+struct RankView {
+    uint64_t nl, lo, nwl;
+    const uint64_t* __restrict__ rp;
+    const uint32_t* __restrict__ ci;
+    const uint8_t* __restrict__ w8;
+    const uint32_t* __restrict__ w32;
+    const uint32_t* __restrict__ deg;
+    const uint32_t* __restrict__ nz;
+    uint32_t* state;
+    uint32_t* visited;
+    uint32_t* cur;
+    uint32_t* nxt;
+    uint32_t* gfront;
+    uint32_t* sendmap;
+    const uint32_t* recv;
+    uint32_t* sendbest;
+    const uint32_t* recvbest;
+    unsigned long long* cnt;
+    uint32_t P;
+    uint64_t V;
+    uint32_t sep_small;
+};
+
+// Visit the owned vertices whose bit is set in `bits` (owned words): small rows
+// on the lane (thread granularity), larger rows by the whole warp.
+template <class EdgeFn>
+__device__ __forceinline__ void dist_for_active(const RankView& r, const uint32_t* bits, EdgeFn&& fn) {
+    const uint32_t lane = lane_id();
+    for (uint64_t wi = gwarp(); wi < r.nwl; wi += gwarps()) {
+        const uint32_t word = bits[wi];
+        if (!word) continue;  // warp-uniform
+        const uint64_t vl = (wi << 5) + lane;
+        const bool mine = (word >> lane) & 1u;
+        uint64_t beg = 0, end = 0;
+        if (mine) {
+            beg = __ldg(r.rp + vl);
+            end = __ldg(r.rp + vl + 1);
+        }
+        const bool small = mine && end - beg < r.sep_small;
+        if (small)
+            for (uint64_t e = beg; e < end; ++e) fn(vl, e, __ldg(r.ci + e));
+        uint32_t todo = __ballot_sync(FULL, mine && !small);
+        while (todo) {
+            const int l = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const uint64_t b0 = __shfl_sync(FULL, beg, l), e0 = __shfl_sync(FULL, end, l);
+            const uint64_t v0 = (wi << 5) + l;
+            for (uint64_t e = b0 + lane; e < e0; e += 32) fn(v0, e, __ldg(r.ci + e));
+        }
+    }
+}
+
+__global__ void k_bfs_push(RankView r) {
+    unsigned long long edges = 0;
+    dist_for_active(r, r.cur, [&](uint64_t, uint64_t, uint32_t u) {
+        ++edges;
+        const uint64_t ul = (uint64_t)u - r.lo;
+        if (ul < r.nl && bm_test(r.visited, (uint32_t)ul)) return;  // owned and already visited
+        bm_set(r.sendmap, u);
+    });
+    uint64_t a[1] = {edges};
+    block_sum<1>(a);
+    if (threadIdx.x == 0 && a[0]) atomicAdd(r.cnt + 2, (unsigned long long)a[0]);
+}
+
+// owner side of a push level: OR the P received slices, keep the unvisited bits
+__global__ void k_bfs_apply(RankView r, uint32_t lvl) {
+    unsigned long long found = 0, mdeg = 0;
+    for (uint64_t wi = gtid(); wi < r.nwl; wi += gthreads()) {
+        uint32_t m = 0;
+        for (uint32_t q = 0; q < r.P; ++q) m |= r.recv[(uint64_t)q * r.nwl + wi];
+        const uint64_t v0 = wi << 5;
+        if (v0 + 32 > r.nl) m &= v0 >= r.nl ? 0u : ((1u << (uint32_t)(r.nl - v0)) - 1u);
+        m &= ~r.visited[wi];
+        r.nxt[wi] = m;
+        if (m) {
+            r.visited[wi] |= m;
+            found += __popc(m);
+            for (uint32_t x = m; x; x &= x - 1) {
+                const uint64_t vl = v0 + (__ffs(x) - 1);
+                r.state[vl] = lvl;
+                mdeg += __ldg(r.deg + vl);
+            }
+        }
+    }
+    uint64_t a[2] = {found, mdeg};
+    block_sum<2>(a);
+    if (threadIdx.x == 0) {
+        if (a[0]) atomicAdd(r.cnt + 0, (unsigned long long)a[0]);
+        if (a[1]) atomicAdd(r.cnt + 1, (unsigned long long)a[1]);
+    }
+}
+
+// bottom-up over owned unvisited candidates against the allgathered frontier
+__global__ void k_bfs_pull(RankView r, uint32_t lvl) {
+    const uint32_t lane = lane_id();
+    unsigned long long found = 0, mdeg = 0, edges = 0;
+    for (uint64_t wi = gwarp(); wi < r.nwl; wi += gwarps()) {
+        const uint32_t vis = r.visited[wi];
+        const uint32_t cand = ~vis & __ldg(r.nz + wi);
+        if (!cand) continue;
+        const uint64_t vl = (wi << 5) + lane;
+        const bool mine = (cand >> lane) & 1u;
+        uint64_t beg = 0, end = 0;
+        if (mine) {
+            beg = __ldg(r.rp + vl);
+            end = __ldg(r.rp + vl + 1);
+        }
+        bool hit = false;
+        const bool small = mine && end - beg < r.sep_small;
+        if (small) {
+            for (uint64_t e = beg; e < end && !hit; ++e) {
+                ++edges;
+                hit = bm_test(r.gfront, __ldg(r.ci + e));
+            }
+        }
+        uint32_t todo = __ballot_sync(FULL, mine && !small);
+        while (todo) {
+            const int l = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const uint64_t b0 = __shfl_sync(FULL, beg, l), e0 = __shfl_sync(FULL, end, l);
+            bool any = false;
+            for (uint64_t b = b0; b < e0; b += 32) {
+                const uint64_t e = b + lane;
+                bool h = false;
+                if (e < e0) {
+                    ++edges;
+                    h = bm_test(r.gfront, __ldg(r.ci + e));
+                }
+                if (__any_sync(FULL, h)) {
+                    any = true;
+                    break;
+                }
+            }
+            if ((int)lane == l) hit = any;
+        }
+        const uint32_t fm = __ballot_sync(FULL, hit);
+        if (hit) {
+            r.state[vl] = lvl;
+            mdeg += end - beg;
+        }
+        if (lane == 0) {
+            r.nxt[wi] = fm;
+            if (fm) {
+                r.visited[wi] = vis | fm;
+                found += __popc(fm);
+            }
+        }
+    }
+    uint64_t a[3] = {found, mdeg, edges};
+    block_sum<3>(a);
+    if (threadIdx.x == 0) {
+        if (a[0]) atomicAdd(r.cnt + 0, (unsigned long long)a[0]);
+        if (a[1]) atomicAdd(r.cnt + 1, (unsigned long long)a[1]);
+        if (a[2]) atomicAdd(r.cnt + 2, (unsigned long long)a[2]);
+    }
+}
+
+// SSSP push over owned active vertices: local targets relaxed in place
+// (atomicMin), remote ones min-combined into the global candidate array.
+__global__ void k_sssp_push(RankView r, unsigned long long hi) {
+    unsigned long long edges = 0;
+    dist_for_active(r, r.cur, [&](uint64_t vl, uint64_t e, uint32_t u) {
+        ++edges;
+        const uint32_t nd = r.state[vl] + edge_w(r.w8, r.w32, e);
+        const uint64_t ul = (uint64_t)u - r.lo;
+        if (ul < r.nl) {
+            if (nd >= r.state[ul]) return;
+            const uint32_t old = atomicMin(r.state + ul, nd);
+            if (nd >= old) return;
+            if ((unsigned long long)nd < hi) bm_set(r.nxt, (uint32_t)ul);
+            else bm_set(r.visited, (uint32_t)ul);
+        } else {
+            // candidate array laid out by owner: owner q's slot of u at q*V + (u - q*V) = u
+            if (nd < r.sendbest[u]) atomicMin(r.sendbest + u, nd);
+        }
+    });
+    uint64_t a[1] = {edges};
+    block_sum<1>(a);
+    if (threadIdx.x == 0 && a[0]) atomicAdd(r.cnt + 2, (unsigned long long)a[0]);
+}
+
+// owner side of an SSSP iteration: apply the reduce-scattered minima, count the next frontier
+__global__ void k_sssp_apply(RankView r, unsigned long long hi) {
+    unsigned long long active = 0;
+    for (uint64_t wi = gtid(); wi < r.nwl; wi += gthreads()) {
+        uint32_t nx = r.nxt[wi], fa = 0;
+        const uint64_t v0 = wi << 5;
+        for (uint32_t b = 0; b < 32; ++b) {
+            const uint64_t vl = v0 + b;
+            if (vl >= r.nl) break;
+            const uint32_t cnd = r.recvbest[vl];
+            if (cnd < r.state[vl]) {
+                r.state[vl] = cnd;
+                if ((unsigned long long)cnd < hi) nx |= 1u << b;
+                else fa |= 1u << b;
+            }
+        }
+        r.nxt[wi] = nx;
+        if (fa) r.visited[wi] |= fa;
+        active += __popc(nx);
+    }
+    uint64_t a[1] = {active};
+    block_sum<1>(a);
+    if (threadIdx.x == 0 && a[0]) atomicAdd(r.cnt + 0, (unsigned long long)a[0]);
+}
+
+__global__ void k_far_min(RankView r) {
+    uint32_t mn = INF;
+    for (uint64_t wi = gtid(); wi < r.nwl; wi += gthreads())
+        for (uint32_t x = r.visited[wi]; x; x &= x - 1) mn = min(mn, r.state[(wi << 5) + (__ffs(x) - 1)]);
+    mn = block_min(mn);
+    if (threadIdx.x == 0 && mn != INF) atomicMin(r.cnt + 3, (unsigned long long)mn);
+}
+
+__global__ void k_far_move(RankView r, unsigned long long hi) {
+    unsigned long long active = 0;
+    for (uint64_t wi = gtid(); wi < r.nwl; wi += gthreads()) {
+        uint32_t f = r.visited[wi], mv = 0;
+        for (uint32_t x = f; x; x &= x - 1) {
+            const int b = __ffs(x) - 1;
+            if ((unsigned long long)r.state[(wi << 5) + b] < hi) mv |= 1u << b;
+        }
+        if (mv) {
+            r.visited[wi] = f & ~mv;
+            r.nxt[wi] |= mv;
+        }
+        active += __popc(r.nxt[wi]);
+    }
+    uint64_t a[1] = {active};
+    block_sum<1>(a);
+    if (threadIdx.x == 0 && a[0]) atomicAdd(r.cnt + 0, (unsigned long long)a[0]);
+}
+
+__global__ void k_min_slices(uint32_t* out, const uint32_t* in, uint64_t len, uint64_t stride, uint32_t nslices) {
+    // out[i] = min_s in[s*stride + i] (virtual-rank reduce-scatter)
+    for (uint64_t i = gtid(); i < len; i += gthreads()) {
+        uint32_t m = INF;
+        for (uint32_t s = 0; s < nslices; ++s) m = min(m, in[(uint64_t)s * stride + i]);
+        out[i] = m;
+    }
+}
+
+__global__ void k_validate_slice(const uint64_t* rp, const uint32_t* ci, uint64_t n, uint64_t m, uint64_t N,
+                                 const void* w, uint32_t wbytes, uint32_t* flags) {
+    const uint64_t t = gtid(), T = gthreads();
+    uint32_t f = 0;
+    if (t == 0 && (rp[0] != 0 || rp[n] != m)) f |= 4;
+    for (uint64_t i = t; i < n; i += T)
+        if (rp[i] > rp[i + 1]) f |= 1;
+    for (uint64_t e = t; e < m; e += T) {
+        if (ci[e] >= N) f |= 2;
+        if (w && (wbytes == 1 ? ((const uint8_t*)w)[e] : ((const uint32_t*)w)[e]) == 0) f |= 8;
+    }
+    if (f) atomicOr(flags, f);
+}
+
+__global__ void k_deg_nz(const uint64_t* rp, uint64_t n, uint64_t nwl, uint32_t* deg, uint32_t* nz) {
+    for (uint64_t i = gtid(); i < n; i += gthreads()) deg[i] = (uint32_t)(rp[i + 1] - rp[i]);
+    for (uint64_t wi = gtid(); wi < nwl; wi += gthreads()) {
+        uint32_t x = 0;
+        for (int b = 0; b < 32; ++b) {
+            const uint64_t v = (wi << 5) + b;
+            if (v < n && rp[v + 1] > rp[v]) x |= 1u << b;
+        }
+        nz[wi] = x;
+    }
+}
+
+// ------------------------------------------------------------------ host helpers
+RankView view_of(sx_dist d, int i, uint32_t cur, const sx_opts& o) {
+    DistRank& k = d->r[i];
+    RankView v;
+    v.nl = k.nl;
+    v.lo = k.lo;
+    v.nwl = d->nwl;
+    v.rp = k.rp;
+    v.ci = k.ci;
+    v.w8 = d->wbytes == 1 ? (const uint8_t*)k.w : nullptr;
+    v.w32 = d->wbytes == 4 ? (const uint32_t*)k.w : nullptr;
+    v.deg = k.deg;
+    v.nz = k.nz;
+    v.state = k.state;
+    v.visited = k.visited;
+    v.cur = k.front[cur];
+    v.nxt = k.front[cur ^ 1];
+    v.gfront = k.gfront;
+    v.sendmap = k.sendmap;
+    v.recv = k.recv;
+    v.sendbest = k.sendbest;
+    v.recvbest = k.recvbest;
+    v.cnt = k.cnt;
+    v.P = (uint32_t)d->P;
+    v.V = d->V;
+    v.sep_small = o.sep_small;
+    return v;
+}
+
+// allreduce of the ranks' 8 counters: slot 3 is a min, the others sums
+sx_status reduce_counters(sx_dist d, unsigned long long (&out)[8]) {
+    cudaStream_t s = d->ctx->stream;
+    if (d->nccl) {
+        DistRank& k = d->r[0];
+        SX_NC(ncclAllReduce(k.cnt, d->dred, 3, ncclUint64, ncclSum, d->comm, s));
+        SX_NC(ncclAllReduce(k.cnt + 3, d->dred + 3, 1, ncclUint64, ncclMin, d->comm, s));
+        SX_CU(cudaMemcpyAsync(d->hcnt, d->dred, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        SX_CU(cudaStreamSynchronize(s));
+        std::memcpy(out, d->hcnt, sizeof(out));
+    } else {
+        for (int i = 0; i < d->nlocal; ++i)
+            SX_CU(cudaMemcpyAsync(d->hcnt + 8 * i, d->r[i].cnt, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        SX_CU(cudaStreamSynchronize(s));
+        for (int j = 0; j < 8; ++j) out[j] = j == 3 ? ~0ull : 0ull;
+        for (int i = 0; i < d->nlocal; ++i)
+            for (int j = 0; j < 8; ++j) {
+                const unsigned long long x = d->hcnt[8 * i + j];
+                if (j == 3) out[j] = x < out[j] ? x : out[j];
+                else out[j] += x;
+            }
+    }
+    for (int i = 0; i < d->nlocal; ++i) {
+        SX_CU(cudaMemsetAsync(d->r[i].cnt, 0, 8 * sizeof(unsigned long long), s));
+        SX_CU(cudaMemsetAsync(d->r[i].cnt + 3, 0xFF, sizeof(unsigned long long), s));
+    }
+    return SX_OK;
+}
+
+// allgather of the owned frontier slices into every rank's global frontier bitmap
+sx_status ex_allgather(sx_dist d, uint32_t cur) {
+    cudaStream_t s = d->ctx->stream;
+    if (d->nccl) {
+        SX_NC(ncclAllGather(d->r[0].front[cur], d->r[0].gfront, d->nwl, ncclUint32, d->comm, s));
+    } else {
+        for (int i = 0; i < d->nlocal; ++i)
+            for (int q = 0; q < d->nlocal; ++q)
+                SX_CU(cudaMemcpyAsync(d->r[i].gfront + (uint64_t)q * d->nwl, d->r[q].front[cur], d->nwl * 4,
+                                      cudaMemcpyDeviceToDevice, s));
+    }
+    return SX_OK;
+}
+
+// alltoall of per-owner slices of the push-target bitmaps
+sx_status ex_alltoall(sx_dist d) {
+    cudaStream_t s = d->ctx->stream;
+    if (d->nccl) {
+        SX_NC(ncclAlltoAll(d->r[0].sendmap, d->r[0].recv, d->nwl, ncclUint32, d->comm, s));
+    } else {
+        for (int i = 0; i < d->nlocal; ++i)
+            for (int q = 0; q < d->nlocal; ++q)
+                SX_CU(cudaMemcpyAsync(d->r[i].recv + (uint64_t)q * d->nwl, d->r[q].sendmap + (uint64_t)i * d->nwl,
+                                      d->nwl * 4, cudaMemcpyDeviceToDevice, s));
+    }
+    return SX_OK;
+}
+
+// reduce-scatter(min) of the candidate-distance arrays to the owners
+sx_status ex_reduce_scatter_min(sx_dist d) {
+    cudaStream_t s = d->ctx->stream;
+    if (d->nccl) {
+        SX_NC(ncclReduceScatter(d->r[0].sendbest, d->r[0].recvbest, d->V, ncclUint32, ncclMin, d->comm, s));
+    } else {
+        // slices are contiguous in each rank's sendbest: stage the P slices destined
+        // to owner i after rank i's own array, then take the element-wise min
+        for (int i = 0; i < d->nlocal; ++i) {
+            // stage the P slices destined to owner i contiguously in the scratch area after sendbest
+            uint32_t* stage = d->r[i].sendbest + (uint64_t)d->P * d->V;
+            for (int q = 0; q < d->nlocal; ++q)
+                SX_CU(cudaMemcpyAsync(stage + (uint64_t)q * d->V, d->r[q].sendbest + (uint64_t)i * d->V, d->V * 4,
+                                      cudaMemcpyDeviceToDevice, s));
+            k_min_slices<<<kgrid(d), BLOCK, 0, s>>>(d->r[i].recvbest, stage, d->V, d->V, (uint32_t)d->nlocal);
+            SX_CU(cudaGetLastError());
+        }
+    }
+    return SX_OK;
+}
+
+sx_status ensure_sssp_buffers(sx_dist d) {
+    for (int i = 0; i < d->nlocal; ++i) {
+        DistRank& k = d->r[i];
+        if (!k.sendbest) {
+            // P*V candidates (+ P*V staging for the virtual reduce-scatter)
+            const uint64_t extra = d->nccl ? 0 : (uint64_t)d->P * d->V;
+            sx_status rc = dmalloc(&k.sendbest, (uint64_t)d->P * d->V + extra);
+            if (rc != SX_OK) return rc;
+            rc = dmalloc(&k.recvbest, d->V);
+            if (rc != SX_OK) return rc;
+        }
+    }
+    return SX_OK;
+}
+
+sx_status check_dist(sx_dist d) {
+    if (!d) return sxh::fail(SX_E_INVALID, "NULL dist handle");
+    sx_status rc = sxh::check_ctx(d->ctx);
+    if (rc != SX_OK) return rc;
+    for (int i = 0; i < d->nlocal; ++i)
+        if (!d->r[i].rp) return sxh::fail(SX_E_INVALID, "sx_dist: a local rank's slice was not uploaded");
+    return SX_OK;
+}
+
+sx_status copy_owned(sx_dist d, uint32_t* const* out) {
+    cudaStream_t s = d->ctx->stream;
+    for (int i = 0; i < d->nlocal; ++i)
+        if (out[i] && d->r[i].nl) SX_CU(cudaMemcpyAsync(out[i], d->r[i].state, d->r[i].nl * 4, cudaMemcpyDefault, s));
+    SX_CU(cudaStreamSynchronize(s));
+    return SX_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+sx_status sx_nccl_unique_id(void* out128) {
+    if (!out128) return sxh::fail(SX_E_INVALID, "sx_nccl_unique_id: NULL");
+    ncclUniqueId id;
+    SX_NC(ncclGetUniqueId(&id));
+    std::memcpy(out128, &id, sizeof(id));
+    return SX_OK;
+}
+
+sx_status sx_dist_create(sx_ctx ctx, uint64_t n_global, int nranks, int rank0, int nlocal, const void* nccl_id,
+                         sx_dist* out) {
+    if (!out) return sxh::fail(SX_E_INVALID, "sx_dist_create: out == NULL");
+    *out = nullptr;
+    sx_status rc = sxh::check_ctx(ctx);
+    if (rc != SX_OK) return rc;
+    if (nranks < 1 || nlocal < 1 || nlocal > DIST_MAX_LOCAL || rank0 < 0 || rank0 + nlocal > nranks)
+        return sxh::fail(SX_E_INVALID, "sx_dist_create: bad rank layout");
+    if (!(nlocal == nranks || nlocal == 1)) return sxh::fail(SX_E_INVALID, "sx_dist_create: nlocal must be 1 or nranks");
+    if (nlocal == 1 && nranks > 1 && !nccl_id) return sxh::fail(SX_E_INVALID, "sx_dist_create: NCCL id required");
+    if (n_global >= 0xFFFFFFFFull) return sxh::fail(SX_E_INVALID, "sx_dist_create: n >= 2^32-1");
+    sx_dist d = new sx_dist_s();
+    d->ctx = ctx;
+    d->P = nranks;
+    d->rank0 = rank0;
+    d->nlocal = nlocal;
+    d->N = n_global;
+    d->V = ((n_global + nranks - 1) / nranks + 31) / 32 * 32;
+    if (d->V == 0) d->V = 32;
+    d->nwl = d->V / 32;
+    d->NW = d->nwl * nranks;
+    d->nccl = nlocal < nranks;
+    if (d->nccl) {
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id, sizeof(id));
+        ncclResult_t r = ncclCommInitRank(&d->comm, nranks, id, rank0);
+        if (r != ncclSuccess) {
+            delete d;
+            return nccl_fail(r, "ncclCommInitRank");
+        }
+    }
+    cudaError_t e = cudaMallocHost(&d->hcnt, 8 * sizeof(unsigned long long) * nlocal);
+    if (e == cudaSuccess) e = cudaMalloc(&d->dred, 8 * sizeof(unsigned long long));
+    if (e != cudaSuccess) {
+        sx_dist_free(d);
+        return sxh::cuda_fail(e, "sx_dist_create");
+    }
+    for (int i = 0; i < nlocal; ++i) {
+        d->r[i].lo = (uint64_t)(rank0 + i) * d->V;
+        const uint64_t hi = std::min<uint64_t>(n_global, d->r[i].lo + d->V);
+        d->r[i].nl = hi > d->r[i].lo ? hi - d->r[i].lo : 0;
+    }
+    *out = d;
+    return SX_OK;
+}
+
+sx_status sx_dist_range(sx_dist d, int local_rank, uint64_t* v_begin, uint64_t* v_end) {
+    if (!d || local_rank < 0 || local_rank >= d->nlocal) return sxh::fail(SX_E_INVALID, "sx_dist_range: bad argument");
+    if (v_begin) *v_begin = d->r[local_rank].lo;
+    if (v_end) *v_end = d->r[local_rank].lo + d->r[local_rank].nl;
+    return SX_OK;
+}
+
+sx_status sx_dist_upload(sx_dist d, int local_rank, const sx_csr_desc* desc) {
+    if (!d || !desc || local_rank < 0 || local_rank >= d->nlocal)
+        return sxh::fail(SX_E_INVALID, "sx_dist_upload: bad argument");
+    sx_status rc = sxh::check_ctx(d->ctx);
+    if (rc != SX_OK) return rc;
+    DistRank& k = d->r[local_rank];
+    if (desc->n != k.nl) return sxh::fail(SX_E_INVALID, "sx_dist_upload: desc->n must equal the owned row count");
+    if (desc->flags & SX_DIRECTED) return sxh::fail(SX_E_INVALID, "sx_dist_upload: symmetric graphs only (1D rows serve as in-rows)");
+    if (desc->w && desc->w_bytes != 1 && desc->w_bytes != 4) return sxh::fail(SX_E_INVALID, "sx_dist_upload: w_bytes");
+    if (local_rank > 0 && d->wbytes != (desc->w ? desc->w_bytes : 0))
+        return sxh::fail(SX_E_INVALID, "sx_dist_upload: all slices need the same weight width");
+    d->wbytes = desc->w ? desc->w_bytes : 0;
+    cudaStream_t s = d->ctx->stream;
+    k.ml = desc->m;
+    if ((rc = dmalloc(&k.rp, k.nl + 1)) != SX_OK) return rc;
+    if ((rc = dmalloc(&k.ci, k.ml)) != SX_OK) return rc;
+    SX_CU(cudaMemcpyAsync(k.rp, desc->row_ptr, (k.nl + 1) * 8, cudaMemcpyDefault, s));
+    if (k.ml) SX_CU(cudaMemcpyAsync(k.ci, desc->col, k.ml * 4, cudaMemcpyDefault, s));
+    if (desc->w) {
+        if ((rc = dmalloc((char**)&k.w, k.ml * desc->w_bytes)) != SX_OK) return rc;
+        if (k.ml) SX_CU(cudaMemcpyAsync(k.w, desc->w, k.ml * desc->w_bytes, cudaMemcpyDefault, s));
+    }
+    uint32_t* flags = nullptr;
+    if ((rc = dmalloc(&flags, 1)) != SX_OK) return rc;
+    SX_CU(cudaMemsetAsync(flags, 0, 4, s));
+    k_validate_slice<<<kgrid(d), BLOCK, 0, s>>>(k.rp, k.ci, k.nl, k.ml, d->N, k.w, d->wbytes, flags);
+    uint32_t hf = 0;
+    SX_CU(cudaMemcpyAsync(&hf, flags, 4, cudaMemcpyDeviceToHost, s));
+    SX_CU(cudaStreamSynchronize(s));
+    cudaFree(flags);
+    if (hf & 7) return sxh::fail(SX_E_INVALID, "sx_dist_upload: invalid CSR slice (row_ptr / col >= n_global)");
+    k.has_zero_w = hf & 8;
+    if ((rc = dmalloc(&k.deg, k.nl)) != SX_OK) return rc;
+    if ((rc = dmalloc(&k.nz, d->nwl)) != SX_OK) return rc;
+    k_deg_nz<<<kgrid(d), BLOCK, 0, s>>>(k.rp, k.nl, d->nwl, k.deg, k.nz);
+    if ((rc = dmalloc(&k.state, d->V)) != SX_OK) return rc;
+    if ((rc = dmalloc(&k.visited, d->nwl)) != SX_OK) return rc;
+    for (int j = 0; j < 2; ++j)
+        if ((rc = dmalloc(&k.front[j], d->nwl)) != SX_OK) return rc;
+    if ((rc = dmalloc(&k.gfront, d->NW)) != SX_OK) return rc;
+    if ((rc = dmalloc(&k.sendmap, d->NW)) != SX_OK) return rc;
+    if ((rc = dmalloc(&k.recv, d->NW)) != SX_OK) return rc;
+    if ((rc = dmalloc(&k.cnt, 8)) != SX_OK) return rc;
+    SX_CU(cudaMemsetAsync(k.cnt, 0, 64, s));
+    SX_CU(cudaMemsetAsync(k.cnt + 3, 0xFF, 8, s));
+    SX_CU(cudaStreamSynchronize(s));
+    return SX_OK;
+}
+
+void sx_dist_free(sx_dist d) {
+    if (!d) return;
+    cudaSetDevice(d->ctx->device);
+    cudaStreamSynchronize(d->ctx->stream);
+    for (int i = 0; i < d->nlocal; ++i) {
+        DistRank& k = d->r[i];
+        void* ps[] = {k.rp, k.ci, k.w, k.deg, k.nz, k.state, k.visited, k.front[0], k.front[1], k.gfront, k.sendmap,
+                      k.recv, k.sendbest, k.recvbest, k.cnt};
+        for (void* p : ps)
+            if (p) cudaFree(p);
+    }
+    if (d->hcnt) cudaFreeHost(d->hcnt);
+    if (d->dred) cudaFree(d->dred);
+    if (d->comm) ncclCommDestroy(d->comm);
+    delete d;
+}
+
+sx_status sx_dist_bfs(sx_dist d, uint32_t src, const sx_opts* opts, uint32_t* const* level_out, sx_stats* stats) {
+    sx_status rc = check_dist(d);
+    if (rc != SX_OK) return rc;
+    if (!level_out) return sxh::fail(SX_E_INVALID, "sx_dist_bfs: NULL level_out");
+    if (src >= d->N) return sxh::fail(SX_E_INVALID, "sx_dist_bfs: src >= n");
+    const sx_opts o = sxh::resolve_opts(opts);
+    sx_ctx c = d->ctx;
+    cudaStream_t s = c->stream;
+    const int G = kgrid(d);
+    SX_CU(cudaEventRecord(c->ev0, s));
+    // state init: levels INF, bitmaps zero, the source on its owner
+    unsigned long long m_local = 0;
+    for (int i = 0; i < d->nlocal; ++i) {
+        DistRank& k = d->r[i];
+        SX_CU(cudaMemsetAsync(k.state, 0xFF, d->V * 4, s));
+        SX_CU(cudaMemsetAsync(k.visited, 0, d->nwl * 4, s));
+        SX_CU(cudaMemsetAsync(k.front[0], 0, d->nwl * 4, s));
+        SX_CU(cudaMemsetAsync(k.front[1], 0, d->nwl * 4, s));
+        SX_CU(cudaMemsetAsync(k.sendmap, 0, d->NW * 4, s));
+        SX_CU(cudaMemsetAsync(k.cnt, 0, 64, s));
+        SX_CU(cudaMemsetAsync(k.cnt + 3, 0xFF, 8, s));
+        m_local += k.ml;
+        if (src >= k.lo && src < k.lo + k.nl) {
+            const uint64_t sl = src - k.lo;
+            const uint32_t zero = 0, bit = 1u << (sl & 31);
+            SX_CU(cudaMemcpyAsync(k.state + sl, &zero, 4, cudaMemcpyHostToDevice, s));
+            SX_CU(cudaMemcpyAsync(k.visited + (sl >> 5), &bit, 4, cudaMemcpyHostToDevice, s));
+            SX_CU(cudaMemcpyAsync(k.front[0] + (sl >> 5), &bit, 4, cudaMemcpyHostToDevice, s));
+            SX_CU(cudaStreamSynchronize(s));
+        }
+    }
+    SX_CU(cudaStreamSynchronize(s));
+    // global edge count and the source degree (allreduced once)
+    unsigned long long msum = m_local, dsrc = 0;
+    {
+        for (int i = 0; i < d->nlocal; ++i) {
+            DistRank& k = d->r[i];
+            if (src >= k.lo && src < k.lo + k.nl) {
+                uint64_t rp2[2];
+                SX_CU(cudaMemcpy(rp2, k.rp + (src - k.lo), 16, cudaMemcpyDeviceToHost));
+                dsrc = rp2[1] - rp2[0];
+            }
+        }
+        if (d->nccl) {
+            unsigned long long hv[2] = {msum, dsrc};
+            SX_CU(cudaMemcpyAsync(d->dred, hv, 16, cudaMemcpyHostToDevice, s));
+            SX_NC(ncclAllReduce(d->dred, d->dred, 2, ncclUint64, ncclSum, d->comm, s));
+            SX_CU(cudaMemcpyAsync(hv, d->dred, 16, cudaMemcpyDeviceToHost, s));
+            SX_CU(cudaStreamSynchronize(s));
+            msum = hv[0];
+            dsrc = hv[1];
+        }
+    }
+    unsigned long long m_u = msum - dsrc, nf_prev = 1;
+    uint32_t dir = o.force_dir == 2 ? DIR_PULL : DIR_PUSH, cur = 0, it = 0, launches = 0, pulls = 0;
+    unsigned long long edges_total = 0, reached = 1;
+    for (;;) {
+        const uint32_t lvl = it + 1;
+        if (dir == DIR_PUSH) {
+            for (int i = 0; i < d->nlocal; ++i) {
+                k_bfs_push<<<G, BLOCK, 0, s>>>(view_of(d, i, cur, o));
+                ++launches;
+            }
+            if ((rc = ex_alltoall(d)) != SX_OK) return rc;
+            for (int i = 0; i < d->nlocal; ++i) {
+                SX_CU(cudaMemsetAsync(d->r[i].sendmap, 0, d->NW * 4, s));
+                k_bfs_apply<<<G, BLOCK, 0, s>>>(view_of(d, i, cur, o), lvl);
+                ++launches;
+            }
+        } else {
+            if ((rc = ex_allgather(d, cur)) != SX_OK) return rc;
+            for (int i = 0; i < d->nlocal; ++i) {
+                k_bfs_pull<<<G, BLOCK, 0, s>>>(view_of(d, i, cur, o), lvl);
+                ++launches;
+            }
+            ++pulls;
+        }
+        SX_CU(cudaGetLastError());
+        unsigned long long cnt[8];
+        if ((rc = reduce_counters(d, cnt)) != SX_OK) return rc;
+        const unsigned long long nf = cnt[0], mf = cnt[1];
+        edges_total += cnt[2];
+        reached += nf;
+        ++it;
+        m_u -= mf;
+        // the new frontier is front[cur ^ 1]; the old one becomes next iteration's output and is cleared
+        for (int i = 0; i < d->nlocal; ++i) SX_CU(cudaMemsetAsync(d->r[i].front[cur], 0, d->nwl * 4, s));
+        cur ^= 1;
+        if (nf == 0 || (o.max_iters && it >= o.max_iters)) break;
+        if (dir == DIR_PUSH) {
+            if (o.force_dir == 2 || (o.force_dir == 0 && (double)mf > (double)m_u / o.alpha && nf > nf_prev)) dir = DIR_PULL;
+        } else {
+            if (o.force_dir == 1 || (o.force_dir == 0 && (double)nf < (double)d->N / o.beta && nf < nf_prev)) dir = DIR_PUSH;
+        }
+        nf_prev = nf;
+    }
+    SX_CU(cudaEventRecord(c->ev1, s));
+    SX_CU(cudaEventSynchronize(c->ev1));
+    float ms = 0;
+    SX_CU(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    if (stats) {
+        std::memset(stats, 0, sizeof(*stats));
+        stats->iterations = it;
+        stats->launches = launches;
+        stats->pull_iters = pulls;
+        stats->edges_examined = edges_total;
+        stats->list_entries = reached;
+        stats->ms = ms;
+        // bytes exchanged per rank: pull levels allgather N/8, push levels alltoall N/8 (+ counters)
+        stats->bytes_model = (double)it * (double)d->NW * 4.0;
+    }
+    return copy_owned(d, level_out);
+}
+
+sx_status sx_dist_sssp(sx_dist d, uint32_t src, uint32_t delta, const sx_opts* opts, uint32_t* const* dist_out,
+                       sx_stats* stats) {
+    sx_status rc = check_dist(d);
+    if (rc != SX_OK) return rc;
+    if (!dist_out) return sxh::fail(SX_E_INVALID, "sx_dist_sssp: NULL dist_out");
+    if (src >= d->N) return sxh::fail(SX_E_INVALID, "sx_dist_sssp: src >= n");
+    if (d->wbytes == 0) return sxh::fail(SX_E_WEIGHT, "sx_dist_sssp: graph has no edge weights");
+    for (int i = 0; i < d->nlocal; ++i)
+        if (d->r[i].has_zero_w) return sxh::fail(SX_E_WEIGHT, "sx_dist_sssp: zero edge weight");
+    if ((rc = ensure_sssp_buffers(d)) != SX_OK) return rc;
+    const sx_opts o = sxh::resolve_opts(opts);
+    sx_ctx c = d->ctx;
+    cudaStream_t s = c->stream;
+    const int G = kgrid(d);
+    SX_CU(cudaEventRecord(c->ev0, s));
+    for (int i = 0; i < d->nlocal; ++i) {
+        DistRank& k = d->r[i];
+        SX_CU(cudaMemsetAsync(k.state, 0xFF, d->V * 4, s));
+        SX_CU(cudaMemsetAsync(k.visited, 0, d->nwl * 4, s));  // far pile
+        SX_CU(cudaMemsetAsync(k.front[0], 0, d->nwl * 4, s));
+        SX_CU(cudaMemsetAsync(k.front[1], 0, d->nwl * 4, s));
+        SX_CU(cudaMemsetAsync(k.sendbest, 0xFF, (uint64_t)d->P * d->V * 4, s));
+        SX_CU(cudaMemsetAsync(k.cnt, 0, 64, s));
+        SX_CU(cudaMemsetAsync(k.cnt + 3, 0xFF, 8, s));
+        if (src >= k.lo && src < k.lo + k.nl) {
+            const uint64_t sl = src - k.lo;
+            const uint32_t zero = 0, bit = 1u << (sl & 31);
+            SX_CU(cudaMemcpyAsync(k.state + sl, &zero, 4, cudaMemcpyHostToDevice, s));
+            SX_CU(cudaMemcpyAsync(k.front[0] + (sl >> 5), &bit, 4, cudaMemcpyHostToDevice, s));
+            SX_CU(cudaStreamSynchronize(s));
+        }
+    }
+    unsigned long long hi = delta ? (unsigned long long)delta : 0x100000000ull;
+    uint32_t cur = 0, it = 0, launches = 0, advances = 0;
+    unsigned long long edges_total = 0;
+    for (;;) {
+        for (int i = 0; i < d->nlocal; ++i) {
+            k_sssp_push<<<G, BLOCK, 0, s>>>(view_of(d, i, cur, o), hi);
+            ++launches;
+        }
+        if ((rc = ex_reduce_scatter_min(d)) != SX_OK) return rc;
+        for (int i = 0; i < d->nlocal; ++i) {
+            SX_CU(cudaMemsetAsync(d->r[i].sendbest, 0xFF, (uint64_t)d->P * d->V * 4, s));
+            k_sssp_apply<<<G, BLOCK, 0, s>>>(view_of(d, i, cur, o), hi);
+            ++launches;
+        }
+        SX_CU(cudaGetLastError());
+        unsigned long long cnt[8];
+        if ((rc = reduce_counters(d, cnt)) != SX_OK) return rc;
+        edges_total += cnt[2];
+        ++it;
+        for (int i = 0; i < d->nlocal; ++i) SX_CU(cudaMemsetAsync(d->r[i].front[cur], 0, d->nwl * 4, s));
+        cur ^= 1;
+        unsigned long long active = cnt[0];
+        if (active == 0) {
+            if (delta == 0) break;
+            for (int i = 0; i < d->nlocal; ++i) k_far_min<<<G, BLOCK, 0, s>>>(view_of(d, i, cur, o));
+            if ((rc = reduce_counters(d, cnt)) != SX_OK) return rc;
+            const unsigned long long mn = cnt[3];
+            if (mn >= 0xFFFFFFFFull) break;
+            hi = (mn / delta + 1) * delta;
+            // move the far vertices below hi into the current frontier (front[cur])
+            for (int i = 0; i < d->nlocal; ++i) {
+                RankView v = view_of(d, i, cur ^ 1, o);  // nxt = front[cur]
+                k_far_move<<<G, BLOCK, 0, s>>>(v, hi);
+            }
+            if ((rc = reduce_counters(d, cnt)) != SX_OK) return rc;
+            ++advances;
+            if (cnt[0] == 0) break;
+        }
+        if (o.max_iters && it >= o.max_iters) break;
+    }
+    SX_CU(cudaEventRecord(c->ev1, s));
+    SX_CU(cudaEventSynchronize(c->ev1));
+    float ms = 0;
+    SX_CU(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    if (stats) {
+        std::memset(stats, 0, sizeof(*stats));
+        stats->iterations = it;
+        stats->launches = launches;
+        stats->ballot_iters = advances;
+        stats->edges_examined = edges_total;
+        stats->ms = ms;
+        stats->bytes_model = (double)it * (double)d->P * d->V * 4.0;
+    }
+    return copy_owned(d, dist_out);
+}
+
+}  // extern "C"

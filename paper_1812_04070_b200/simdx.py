@@ -89,13 +89,23 @@ _lib.sx_kcore.argtypes = [_vp, _u32, _P(sx_opts), _vp, _P(sx_stats)]
 _lib.sx_spmv.argtypes = [_vp, _vp, _u32, _P(sx_opts), _vp, _P(sx_stats)]
 _lib.sx_bp.argtypes = [_vp, _vp, _u32, _P(sx_opts), _vp, _P(sx_stats)]
 _lib.sx_barrier_bench.argtypes = [_vp, _u32, _P(ctypes.c_double), _P(ctypes.c_int)]
+_lib.sx_nccl_unique_id.argtypes = [_vp]
+_lib.sx_dist_create.argtypes = [_vp, _u64, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _P(_vp)]
+_lib.sx_dist_range.argtypes = [_vp, ctypes.c_int, _P(_u64), _P(_u64)]
+_lib.sx_dist_upload.argtypes = [_vp, ctypes.c_int, _P(sx_csr_desc)]
+_lib.sx_dist_free.argtypes = [_vp]
+_lib.sx_dist_free.restype = None
+_lib.sx_dist_bfs.argtypes = [_vp, _u32, _P(sx_opts), _P(_vp), _P(sx_stats)]
+_lib.sx_dist_sssp.argtypes = [_vp, _u32, _u32, _P(sx_opts), _P(_vp), _P(sx_stats)]
 for _f in ("sx_ctx_create", "sx_ctx_info", "sx_graph_upload", "sx_graph_info", "sx_bfs", "sx_sssp", "sx_pagerank",
-           "sx_kcore", "sx_spmv", "sx_bp", "sx_barrier_bench"):
+           "sx_kcore", "sx_spmv", "sx_bp", "sx_barrier_bench", "sx_nccl_unique_id", "sx_dist_create", "sx_dist_range",
+           "sx_dist_upload", "sx_dist_bfs", "sx_dist_sssp"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 EXPORTED = ["sx_status_str", "sx_last_error", "sx_version", "sx_ctx_create", "sx_ctx_destroy", "sx_ctx_info",
             "sx_graph_upload", "sx_graph_info", "sx_graph_free", "sx_opts_default", "sx_bfs", "sx_sssp",
-            "sx_pagerank", "sx_kcore", "sx_spmv", "sx_bp", "sx_barrier_bench"]
+            "sx_pagerank", "sx_kcore", "sx_spmv", "sx_bp", "sx_barrier_bench", "sx_nccl_unique_id",
+            "sx_dist_create", "sx_dist_range", "sx_dist_upload", "sx_dist_free", "sx_dist_bfs", "sx_dist_sssp"]
 
 
 class SimdxError(RuntimeError):
@@ -330,3 +340,77 @@ class Graph:
         o, buf = self._opts(dict(kw))
         st = sx_bp(self.h, prior, iters, o, out)
         return out, st.as_dict(), self._trace(buf, st)
+
+
+# ---------------------------------------------------------------- multi-GPU layer
+def sx_nccl_unique_id() -> bytes:
+    buf = (ctypes.c_char * 128)()
+    _check(_lib.sx_nccl_unique_id(buf), "sx_nccl_unique_id")
+    return bytes(buf)
+
+
+def partition(n: int, nranks: int, rank: int):
+    """Owned vertex range of `rank` (the rule of sx_dist_create: V = ceil(n/P) rounded up to 32)."""
+    V = ((n + nranks - 1) // nranks + 31) // 32 * 32 or 32
+    lo = min(n, rank * V)
+    return lo, min(n, lo + V)
+
+
+class Dist:
+    """A graph distributed by 1D vertex ranges.
+
+    nlocal == nranks: all ranks in this process on one device (virtual ranks);
+    nlocal == 1: this process is rank `rank0` of an NCCL job (`nccl_id` from rank 0).
+    """
+
+    def __init__(self, ctx: Context, n: int, nranks: int, rank0: int = 0, nlocal: Optional[int] = None,
+                 nccl_id: Optional[bytes] = None):
+        nlocal = nranks if nlocal is None else nlocal
+        self.ctx, self.n, self.nranks, self.rank0, self.nlocal = ctx, n, nranks, rank0, nlocal
+        h = _vp()
+        idbuf = None if nccl_id is None else ctypes.create_string_buffer(nccl_id, 128)
+        _check(_lib.sx_dist_create(ctx.h, n, nranks, rank0, nlocal, idbuf, ctypes.byref(h)), "sx_dist_create")
+        self.h = h
+
+    def range(self, local_rank: int):
+        a, b = _u64(), _u64()
+        _check(_lib.sx_dist_range(self.h, local_rank, ctypes.byref(a), ctypes.byref(b)), "sx_dist_range")
+        return a.value, b.value
+
+    def upload(self, local_rank: int, csr_slice) -> None:
+        """csr_slice: rows [v_lo, v_hi) (simgen.CSR with v_lo/v_hi), global column ids."""
+        d = sx_csr_desc()
+        d.n = int(csr_slice.row_ptr.shape[0] - 1)
+        d.m = int(csr_slice.row_ptr[-1])
+        d.row_ptr, d.col, d.w = _ptr(csr_slice.row_ptr), _ptr(csr_slice.col), _ptr(csr_slice.w)
+        d.w_bytes = 0 if csr_slice.w is None else csr_slice.w.dtype.itemsize
+        d.flags = 0
+        _check(_lib.sx_dist_upload(self.h, local_rank, ctypes.byref(d)), "sx_dist_upload")
+
+    def _outs(self, outs):
+        if outs is None:
+            outs = []
+            for i in range(self.nlocal):
+                lo, hi = self.range(i)
+                outs.append(np.empty(hi - lo, np.uint32))
+        arr = (_vp * self.nlocal)(*[_ptr(o) for o in outs])
+        return outs, arr
+
+    def bfs(self, src: int, outs=None, **kw):
+        outs, arr = self._outs(outs)
+        st = sx_stats()
+        o = make_opts(**kw)
+        _check(_lib.sx_dist_bfs(self.h, src, ctypes.byref(o), arr, ctypes.byref(st)), "sx_dist_bfs")
+        return outs, st.as_dict()
+
+    def sssp(self, src: int, delta: int = 0, outs=None, **kw):
+        outs, arr = self._outs(outs)
+        st = sx_stats()
+        o = make_opts(**kw)
+        _check(_lib.sx_dist_sssp(self.h, src, delta, ctypes.byref(o), arr, ctypes.byref(st)), "sx_dist_sssp")
+        return outs, st.as_dict()
+
+    def free(self):
+        if self.h:
+            _lib.sx_dist_free(self.h)
+            self.h = None

@@ -1,0 +1,91 @@
+"""The multi-GPU layer on one GPU: P virtual ranks run the
+same partitioned kernels and exchange schedule with device copies in place of
+the NCCL collectives.  Results must equal the oracle for every P."""
+import numpy as np
+import pytest
+
+import oracle
+import simgen
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import torch
+    from paper_1812_04070_b200 import simdx
+    torch.cuda.set_device(0)
+    c = simdx.Context(0, torch.cuda.current_stream().cuda_stream)
+    yield c
+    c.close()
+
+
+def build_dist(ctx, g, P):
+    from paper_1812_04070_b200 import simdx
+    D = simdx.Dist(ctx, g.n, P)
+    for r in range(P):
+        lo, hi = D.range(r)
+        assert (lo, hi) == simdx.partition(g.n, P, r)
+        rp = (g.row_ptr[lo:hi + 1] - g.row_ptr[lo]).astype(np.uint64)
+        sl = simgen.CSR(n=g.n, row_ptr=rp, col=g.col[g.row_ptr[lo]:g.row_ptr[hi]].copy(),
+                        w=None if g.w is None else g.w[g.row_ptr[lo]:g.row_ptr[hi]].copy(), v_lo=lo, v_hi=hi)
+        D.upload(r, sl)
+    return D
+
+
+@pytest.fixture(scope="module")
+def rmat14():
+    return simgen.rmat(14, 16, seed=5, wmin=1, wmax=255)
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 8])
+def test_dist_bfs_rmat(ctx, rmat14, P):
+    D = build_dist(ctx, rmat14, P)
+    for src in (0, 1234):
+        ref = oracle.bfs(rmat14, src)
+        for mode in (dict(), dict(force_dir=1), dict(force_dir=2)):
+            outs, st = D.bfs(src, **mode)
+            assert np.array_equal(np.concatenate(outs), ref), (P, src, mode)
+    D.free()
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_dist_sssp_rmat(ctx, rmat14, P):
+    D = build_dist(ctx, rmat14, P)
+    ref = oracle.sssp(rmat14, 0)
+    for delta in (0, 64, 1024):
+        outs, st = D.sssp(0, delta)
+        assert np.array_equal(np.concatenate(outs), ref), (P, delta)
+    D.free()
+
+
+def test_dist_sssp_grid(ctx):
+    g = simgen.grid(96, 80, seed=2)
+    ref = oracle.sssp(g, 0)
+    for P in (2, 5):
+        D = build_dist(ctx, g, P)
+        outs, _ = D.sssp(0, 512)
+        assert np.array_equal(np.concatenate(outs), ref)
+        outs, _ = D.bfs(0)
+        assert np.array_equal(np.concatenate(outs), oracle.bfs(g, 0))
+        D.free()
+
+
+def test_dist_matches_single_gpu_at_scale20(ctx):
+    g = simgen.rmat(20, 16, seed=1)
+    ref = oracle.bfs(g, 0)
+    D = build_dist(ctx, g, 4)
+    outs, st = D.bfs(0)
+    assert np.array_equal(np.concatenate(outs), ref)
+    assert st["pull_iters"] >= 1  # the direction switch happens across ranks too
+    D.free()
+
+
+def test_dist_errors(ctx, rmat14):
+    from paper_1812_04070_b200 import simdx
+    with pytest.raises(simdx.SimdxError):
+        simdx.Dist(ctx, rmat14.n, 4, 0, 2)  # nlocal must be 1 or nranks
+    D = simdx.Dist(ctx, rmat14.n, 2)
+    with pytest.raises(simdx.SimdxError):
+        D.bfs(0)  # slices not uploaded
+    D.free()
