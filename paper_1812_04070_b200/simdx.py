@@ -255,6 +255,17 @@ class Context:
     def info(self) -> dict:
         return sx_ctx_info(self.h)
 
+    def upload_device(self, dcsr, borrow: bool = False) -> "Graph":
+        """Upload from raw device pointers (e.g. simgen.DeviceCSR); borrow = no copy."""
+        d = sx_csr_desc()
+        d.n, d.m = dcsr.v_hi - dcsr.v_lo, dcsr.m
+        d.row_ptr, d.col, d.w = dcsr.row_ptr_ptr, dcsr.col_ptr, dcsr.w_ptr
+        d.w_bytes = dcsr.wbytes
+        d.flags = SX_DEVICE_PTRS | (SX_BORROW if borrow else 0)
+        h = _vp()
+        _check(_lib.sx_graph_upload(self.h, ctypes.byref(d), ctypes.byref(h)), "sx_graph_upload")
+        return Graph(self, h, d.n)
+
     def upload(self, csr) -> "Graph":
         """Upload a simgen.CSR-like object (fields n,row_ptr,col,w,directed,csc_*)."""
         h = sx_graph_upload(self.h, csr.n, csr.row_ptr, csr.col, csr.w,
@@ -376,6 +387,15 @@ class Dist:
         a, b = _u64(), _u64()
         _check(_lib.sx_dist_range(self.h, local_rank, ctypes.byref(a), ctypes.byref(b)), "sx_dist_range")
         return a.value, b.value
+
+    def upload_device(self, local_rank: int, dcsr) -> None:
+        """Upload a rank's slice from raw device pointers (simgen.DeviceCSR with v_lo/v_hi)."""
+        d = sx_csr_desc()
+        d.n, d.m = dcsr.v_hi - dcsr.v_lo, dcsr.m
+        d.row_ptr, d.col, d.w = dcsr.row_ptr_ptr, dcsr.col_ptr, dcsr.w_ptr
+        d.w_bytes = dcsr.wbytes
+        d.flags = SX_DEVICE_PTRS
+        _check(_lib.sx_dist_upload(self.h, local_rank, ctypes.byref(d)), "sx_dist_upload")
 
     def upload(self, local_rank: int, csr_slice) -> None:
         """csr_slice: rows [v_lo, v_hi) (simgen.CSR with v_lo/v_hi), global column ids."""

@@ -107,6 +107,85 @@ class CSR:
         return self.w if self.csc_idx is None else self.csc_w
 
 
+# ---------------------------------------------------------------- GPU generator
+_SO_GPU = os.path.join(_HERE, "libsimgen_gpu.so")
+_lib_gpu = None
+
+
+def build_gpu(force: bool = False) -> str:
+    """nvcc-compile gpu_gen.cu (the same generator on the GPU) for sm_100a."""
+    src = os.path.join(_HERE, "gpu_gen.cu")
+    if force or not os.path.exists(_SO_GPU) or os.path.getmtime(_SO_GPU) < os.path.getmtime(src):
+        subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
+                               "-std=c++17", "-Xcompiler", "-fPIC", "-shared", src, "-o", _SO_GPU])
+    return _SO_GPU
+
+
+def _LG():
+    global _lib_gpu
+    if _lib_gpu is None:
+        build_gpu()
+        lib = ctypes.CDLL(_SO_GPU)
+        vp = ctypes.c_void_p
+        lib.simgen_gpu_rmat_csr.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint32,
+                                            ctypes.c_uint32, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, vp,
+                                            ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                            ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_int)]
+        lib.simgen_gpu_rmat_csr.restype = ctypes.c_int
+        lib.simgen_gpu_free.argtypes = [vp]
+        lib.simgen_gpu_free.restype = None
+        lib.simgen_gpu_to_host.argtypes = [vp, vp, ctypes.c_uint64]
+        lib.simgen_gpu_to_host.restype = ctypes.c_int
+        _lib_gpu = lib
+    return _lib_gpu
+
+
+class DeviceCSR:
+    """Rows [v_lo, v_hi) of a graph in device memory (raw cudaMalloc pointers)."""
+
+    def __init__(self, n, v_lo, v_hi, row_ptr, col, w, m, wbytes):
+        self.n, self.v_lo, self.v_hi = n, v_lo, v_hi
+        self.row_ptr_ptr, self.col_ptr, self.w_ptr = row_ptr, col, w
+        self.m, self.wbytes = m, wbytes
+
+    def to_host(self) -> CSR:
+        L = _LG()
+        nl = self.v_hi - self.v_lo
+        rp = np.empty(nl + 1, np.uint64)
+        col = np.empty(self.m, np.uint32)
+        L.simgen_gpu_to_host(_p(rp), self.row_ptr_ptr, rp.nbytes)
+        if self.m:
+            L.simgen_gpu_to_host(_p(col), self.col_ptr, col.nbytes)
+        w = None
+        if self.wbytes:
+            w = np.empty(self.m, np.uint8 if self.wbytes == 1 else np.uint32)
+            if self.m:
+                L.simgen_gpu_to_host(_p(w), self.w_ptr, w.nbytes)
+        return CSR(n=self.n, row_ptr=rp, col=col, w=w, v_lo=self.v_lo, v_hi=self.v_hi)
+
+    def free(self):
+        L = _LG()
+        for p in (self.row_ptr_ptr, self.col_ptr, self.w_ptr):
+            if p:
+                L.simgen_gpu_free(p)
+        self.row_ptr_ptr = self.col_ptr = self.w_ptr = None
+
+
+def rmat_gpu(scale: int, ef: int = 16, seed: int = 1, wmin: int = 0, wmax: int = 0, relabel_ids: bool = True,
+             v_lo: int = 0, v_hi: Optional[int] = None, stream: int = 0) -> DeviceCSR:
+    """rmat(...) built on the current CUDA device (bit-identical CSR, tests/test_gpu_gen.py)."""
+    n = 1 << scale
+    v_hi = n if v_hi is None else v_hi
+    rp, col, w = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+    m, wb = ctypes.c_uint64(), ctypes.c_int()
+    rc = _LG().simgen_gpu_rmat_csr(scale, ef, seed, wmin, wmax, int(relabel_ids), v_lo, v_hi,
+                                   ctypes.c_void_p(stream) if stream else None, ctypes.byref(rp), ctypes.byref(col),
+                                   ctypes.byref(w), ctypes.byref(m), ctypes.byref(wb))
+    if rc != 0:
+        raise RuntimeError("simgen_gpu_rmat_csr failed (see stderr)")
+    return DeviceCSR(n, v_lo, v_hi, rp.value, col.value, w.value, m.value, wb.value)
+
+
 def philox(c0: int, c1: int, c2: int, c3: int, seed: int) -> tuple:
     out = (ctypes.c_uint32 * 4)()
     _L().simgen_philox(c0, c1, c2, c3, seed, out)
