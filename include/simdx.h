@@ -158,6 +158,11 @@ typedef struct {
     uint32_t max_iters;          /* 0 = unlimited */
     sx_trace_rec* trace;         /* nullable host buffer of trace_cap records (P:623-626 activation patterns) */
     uint64_t trace_cap;
+    uint32_t local_chain;        /* SSSP / k-core push (B200 addition): a thread that activates a vertex may
+                                    process it at once instead of recording it, up to this many in a row
+                                    (chaotic relaxation, reading 12; results unchanged); 0 = strict BSP.
+                                    Ignored by BFS (levels are BSP-exact). Default 0: measured on the 2048^2
+                                    grid, chains cut iterations 1.6x but lengthened each one more. */
 } sx_opts;
 
 typedef struct {

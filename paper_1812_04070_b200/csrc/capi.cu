@@ -126,6 +126,7 @@ Sched make_sched(const sx_graph g, const sx_opts& o) {
     s.force_dir = o.force_dir;
     s.fusion = o.fusion;
     s.max_iters = o.max_iters;
+    s.local_chain = o.local_chain;
     return s;
 }
 
@@ -286,6 +287,7 @@ void sx_opts_default(sx_opts* o) {
     o->max_iters = 0;
     o->trace = nullptr;
     o->trace_cap = 0;
+    o->local_chain = 0;
 }
 
 sx_status sx_ctx_create(int device, void* cuda_stream, sx_ctx* out) {

@@ -134,6 +134,7 @@ struct Sched {
     float alpha, beta;
     int force_filter, force_dir, fusion;
     uint32_t max_iters;
+    uint32_t local_chain;   // SSSP / k-core: vertices a thread may process in a row within one iteration
 };
 
 // ---------------------------------------------------------------- small helpers
@@ -684,6 +685,44 @@ __device__ __forceinline__ void for_edges(const uint32_t* __restrict__ col, uint
         fn(e + 3, q.w);
     }
     for (uint64_t e = a + 4 * nvec + rank; e < end; e += size) fn(e, __ldg(col + e));
+}
+
+// for_edges with the edge weight: in the aligned body the four u8 weights of a
+// 128-bit group of ids arrive in one 32-bit load (u32 weights: one 128-bit load).
+template <class Fn>
+__device__ __forceinline__ void for_edges_w(const uint32_t* __restrict__ col, const uint8_t* __restrict__ w8,
+                                            const uint32_t* __restrict__ w32, uint64_t beg, uint64_t end,
+                                            uint64_t rank, uint64_t size, Fn&& fn) {
+    uint64_t a = (beg + 3) & ~3ull;
+    if (a > end) a = end;
+    for (uint64_t e = beg + rank; e < a; e += size) fn(e, __ldg(col + e), edge_w(w8, w32, e));
+    const uint64_t nvec = (end - a) >> 2;
+    const uint4* c4 = reinterpret_cast<const uint4*>(col + a);
+    for (uint64_t i = rank; i < nvec; i += size) {
+        const uint4 q = __ldg(c4 + i);
+        const uint64_t e = a + 4 * i;
+        uint32_t w0, w1, w2, w3;
+        if (w8) {
+            const uint32_t ww = __ldg(reinterpret_cast<const uint32_t*>(w8 + e));
+            w0 = ww & 0xFF;
+            w1 = (ww >> 8) & 0xFF;
+            w2 = (ww >> 16) & 0xFF;
+            w3 = ww >> 24;
+        } else if (w32) {
+            const uint4 ww = __ldg(reinterpret_cast<const uint4*>(w32 + e));
+            w0 = ww.x;
+            w1 = ww.y;
+            w2 = ww.z;
+            w3 = ww.w;
+        } else {
+            w0 = w1 = w2 = w3 = 1u;
+        }
+        fn(e, q.x, w0);
+        fn(e + 1, q.y, w1);
+        fn(e + 2, q.z, w2);
+        fn(e + 3, q.w, w3);
+    }
+    for (uint64_t e = a + 4 * nvec + rank; e < end; e += size) fn(e, __ldg(col + e), edge_w(w8, w32, e));
 }
 
 // One thread sums term(e, col[e]) over [beg, end) with 16 neighbour ids (four

@@ -134,18 +134,36 @@ __global__ void __launch_bounds__(BLOCK, 4) kcore_push(KcoreP p) {
         uint32_t* nbm = p.s.bm[(it + 1) % 3];
         uint64_t edges = 0;
         const uint32_t kk = k;
+        auto record = [&](uint32_t u) {
+            bm_set(nbm, u);
+            online_record(nx, nlists, p.s, u, cls_of(__ldg(p.g.dout + u), p.s));
+        };
         for_tasks(p.s.lists[it & 1], p.s, cnt, [&](uint32_t v, uint64_t rank, uint64_t size, uint32_t) {
-            const uint64_t beg = __ldg(p.g.rp + v), end = __ldg(p.g.rp + v + 1);
-            for_edges(p.g.ci, beg, end, rank, size, [&](uint64_t, uint32_t u) {
-                ++edges;
-                if (p.core[u] != INF) return;
-                const uint32_t old = atomicSub(p.res + u, 1u);
-                if (old == kk + 1) {
-                    p.core[u] = kk;
-                    bm_set(nbm, u);
-                    online_record(nx, nlists, p.s, u, cls_of(__ldg(p.g.dout + u), p.s));
+            // Local chain (B200 addition, reading 12): a removal that a thread-granularity
+            // task triggers is processed at once (the cascade continues within the
+            // iteration) instead of being recorded; each vertex is still removed and
+            // processed exactly once (the crossing test), so coreness is unchanged.
+            for (uint32_t depth = 0;; ++depth) {
+                const uint64_t beg = __ldg(p.g.rp + v), end = __ldg(p.g.rp + v + 1);
+                if (depth > 0 && end - beg >= p.s.sep_small) {
+                    record(v);
+                    break;
                 }
-            });
+                const bool can_chain = size == 1 && depth < p.s.local_chain;
+                uint32_t next = INF;
+                for_edges(p.g.ci, beg, end, rank, size, [&](uint64_t, uint32_t u) {
+                    ++edges;
+                    if (p.core[u] != INF) return;
+                    const uint32_t old = atomicSub(p.res + u, 1u);
+                    if (old == kk + 1) {
+                        p.core[u] = kk;
+                        if (can_chain && next == INF) next = u;
+                        else record(u);
+                    }
+                });
+                if (next == INF) break;
+                v = next;
+            }
         });
         st.edges += edges;
         if (lead()) st.entries += sum4(cnt);

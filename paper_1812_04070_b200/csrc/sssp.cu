@@ -2,15 +2,22 @@
 //
 //   Active  : vertices whose distance changed in the previous iteration
 //   Compute : update_{v->u} = dist(v) + w(v,u)
-//   Combine : min, applied with atomicMin on u32 distances — order
-//             independent, so results are bit-exact (SURVEY.md §8(c) reading 11)
-//   delta-stepping ([Meyer & Sanders]): an improved vertex with
-//   dist < hi joins the next active list (claimed exactly once per iteration on
-//   the next-frontier bitmap); otherwise it goes to the far pile (a bitmap).
-//   When the near lists run dry the bucket advances to the smallest pending
-//   distance: hi = (min_far / delta + 1) * delta, and the far vertices below hi
-//   are moved to the active list by a ballot pass over the far bitmap.
-//   delta = 0 means delta = infinity: frontier Bellman-Ford (reading 9).
+//   Combine : min
+//     push: atomicMin on u32 distances — order independent, so results are
+//           bit-exact (SURVEY.md §8(c) reading 11);
+//     pull: every vertex u folds min over its in-neighbours in the frontier and
+//           its single owner writes dist(u) — atomic-free; in-degrees
+//           >= sep_huge are folded grid-wide first (block min + one atomicMin).
+//   "BFS and SSSP utilize push in the first and last iterations, and pull in
+//   between": push -> pull when the frontier's out-edges exceed m/alpha,
+//   pull -> push when |F| < n/beta and shrinking (reading 8); selective fusion
+//   = one persistent launch per direction phase.
+//   delta-stepping: an improved vertex with dist < hi joins the next
+//   frontier; otherwise it goes to the far pile (a bitmap).  When the frontier
+//   runs dry the bucket advances to the smallest pending distance:
+//   hi = (min_far / delta + 1) * delta, and the far vertices below hi are moved
+//   to the active list by a ballot pass over the far bitmap.  delta = 0 means
+//   delta = infinity: frontier Bellman-Ford (reading 9).
 #include "internal.h"
 
 namespace sx {
@@ -20,7 +27,10 @@ struct SsspP {
     Sched s;
     uint32_t* dist;
     uint32_t* far;
+    uint32_t* hlist;  // vertices with in-degree >= sep_huge (pull: grid-wide folds)
+    uint32_t nh;
     uint32_t delta;
+    int sym;
 };
 
 __global__ void sssp_init(SsspP p, uint32_t src) {
@@ -29,6 +39,7 @@ __global__ void sssp_init(SsspP p, uint32_t src) {
         for (int i = 0; i < 3; ++i) reset_line_warp(&c->line[i]);
     if (threadIdx.x != 0) return;
     p.dist[src] = 0;
+    p.s.bm[0][src >> 5] |= 1u << (src & 31);
     const uint32_t k = cls_of(p.g.dout[src], p.s);
     for (int i = 0; i < NCLS; ++i) c->cur_count[i] = 0;
     c->cur_count[k] = 1;
@@ -37,8 +48,14 @@ __global__ void sssp_init(SsspP p, uint32_t src) {
     c->dir = DIR_PUSH;
     c->lists_ready = 1;
     c->slotted = 0;
+    c->nf_prev = 1;
     c->iter = 0;
     c->done = 0;
+}
+
+__global__ void k_huge_list(const uint32_t* din, uint64_t n, uint32_t sep, uint32_t* list, uint32_t* count) {
+    for (uint64_t v = gtid(); v < n; v += gthreads())
+        if (din[v] >= sep) list[atomicAdd(count, 1u)] = (uint32_t)v;
 }
 
 // Far-pile source for the bucket advance: far vertices with dist < hi.
@@ -57,58 +74,127 @@ struct FarWords {
     }
 };
 
+__device__ __forceinline__ void sssp_exit(const SsspP& p, uint32_t kdir, uint32_t it, uint64_t hi, uint32_t nf_prev,
+                                          uint32_t dir, uint32_t done, uint32_t ready, uint32_t slotted,
+                                          const uint32_t (&cnt)[NCLS], Stats& st) {
+    Ctl* c = p.s.ctl;
+    flush_stats(c, st, kdir);
+    if (lead()) {
+        c->iter = it;
+        c->hi = hi;
+        c->nf_prev = nf_prev;
+        c->dir = dir;
+        c->done = done;
+        c->lists_ready = ready;
+        c->slotted = slotted;
+        for (int i = 0; i < NCLS; ++i) c->cur_count[i] = cnt[i];
+        grid_end(c);
+        c->launch += 1;
+    }
+}
+
+// ------------------------------------------------------------------ push
 __global__ void __launch_bounds__(BLOCK, 4) sssp_push(SsspP p) {
     Ctl* c = p.s.ctl;
-    if (vload(&c->done)) return;
+    if (vload(&c->done) || vload(&c->dir) != DIR_PUSH) return;
     grid_begin(c);
     uint32_t it = vload(&c->iter);
     uint64_t hi = vload(&c->hi);
+    uint32_t nf_prev = vload(&c->nf_prev);
     uint32_t cnt[NCLS];
-    uint32_t slotted = vload(&c->slotted);
-    if (slotted) {
+    uint32_t slotted = 0;
+    Stats st;
+    if (!vload(&c->lists_ready)) {
+        // entering push from pull: the frontier exists only as a bitmap -> ballot filter
+        if (!ballot_filter(BitmapWords{p.s.bm[it % 3]}, p.s, BallotOut{p.s.lists[it & 1], p.s.cstride, p.g.dout}, cnt))
+            return;
+        st.scanned += p.s.nwords * 32;
+        if (!grid_sync(c)) return;
+        view_contig(cnt);
+    } else if (vload(&c->slotted)) {
+        slotted = 1;
         view_slots(&c->line[it % 3], p.s, cnt);
     } else {
         for (int i = 0; i < NCLS; ++i) cnt[i] = vload(&c->cur_count[i]);
         view_contig(cnt);
     }
-    Stats st;
-    uint32_t done = 0;
+    uint32_t dir = DIR_PUSH, done = 0, ready = 1;
     for (;;) {
         IterLine* nx = &c->line[(it + 1) % 3];
         maybe_reset_line(&c->line[(it + 2) % 3]);
         clear_bitmap(p.s.bm[(it + 2) % 3], p.s.nwords);
         uint32_t* nlists = p.s.lists[(it + 1) & 1];
         uint32_t* nbm = p.s.bm[(it + 1) % 3];
-        uint64_t edges = 0;
+        uint64_t edges = 0, mdeg = 0;
+        // record u for the next iteration (claimed once per iteration on the bitmap)
+        auto record = [&](uint32_t u) {
+            if (!bm_test(nbm, u) && bm_claim(nbm, u)) {
+                const uint32_t du = __ldg(p.g.dout + u);
+                mdeg += du;
+                online_record(nx, nlists, p.s, u, cls_of(du, p.s));
+            }
+        };
         for_tasks(p.s.lists[it & 1], p.s, cnt, [&](uint32_t v, uint64_t rank, uint64_t size, uint32_t) {
-            const uint64_t beg = __ldg(p.g.rp + v), end = __ldg(p.g.rp + v + 1);
-            const uint32_t dv = p.dist[v];
-            for_edges(p.g.ci, beg, end, rank, size, [&](uint64_t e, uint32_t u) {
-                ++edges;
-                const uint32_t nd = dv + edge_w(p.g.w8, p.g.w32, e);
-                if (nd >= p.dist[u]) return;
-                const uint32_t old = atomicMin(p.dist + u, nd);
-                if (nd >= old) return;
-                if ((uint64_t)nd < hi) {
-                    if (bm_claim(nbm, u)) online_record(nx, nlists, p.s, u, cls_of(__ldg(p.g.dout + u), p.s));
-                } else {
-                    bm_set(p.far, u);
+            // Local chain (B200 addition, reading 12): a thread-granularity task that
+            // improves a vertex below hi processes it at once instead of recording it,
+            // up to local_chain vertices in a row.  A later improvement by another
+            // thread finds the vertex unclaimed and records it, so nothing is lost.
+            for (uint32_t depth = 0;; ++depth) {
+                const uint64_t beg = __ldg(p.g.rp + v), end = __ldg(p.g.rp + v + 1);
+                if (depth > 0 && end - beg >= p.s.sep_small) {  // a chained vertex too big for one thread
+                    record(v);
+                    break;
                 }
-            });
+                const uint32_t dv = p.dist[v];
+                const bool can_chain = size == 1 && depth < p.s.local_chain;
+                uint32_t next = INF;
+                for_edges_w(p.g.ci, p.g.w8, p.g.w32, beg, end, rank, size, [&](uint64_t, uint32_t u, uint32_t w) {
+                    ++edges;
+                    const uint32_t nd = dv + w;
+                    if (nd >= p.dist[u]) return;
+                    const uint32_t old = atomicMin(p.dist + u, nd);
+                    if (nd >= old) return;
+                    if ((uint64_t)nd < hi) {
+                        if (can_chain && next == INF) next = u;
+                        else record(u);
+                    } else if (!bm_test(p.far, u)) {
+                        bm_set(p.far, u);
+                    }
+                });
+                if (next == INF) break;
+                v = next;
+            }
         });
         st.edges += edges;
         if (lead()) st.entries += sum4(cnt);
+        {
+            uint64_t v[1] = {mdeg};
+            block_sum<1>(v);
+            if (threadIdx.x == 0 && v[0]) atomicAdd(&nx->s[my_slot()].mdeg, (unsigned long long)v[0]);
+        }
         if (!grid_sync(c)) return;
         LineSum ls;
         uint32_t vcnt[NCLS];
         read_line_view(nx, p.s, ls, vcnt);
         const uint64_t nf = sum4(ls.cnt);
+        const uint64_t mf = ls.mdeg;
         bool overflow = false;
         for (int i = 0; i < NCLS; ++i) overflow |= ls.cntmax[i] > p.s.cap_s;
         if (p.s.force_filter == 2) overflow = true;
         ++it;
         ++st.iters;
         uint32_t filt = overflow ? 1u : 0u;
+        // SSSP pull has no early exit: it visits all m in-edges, push visits m_f
+        // out-edges with atomics.  Measured crossover on R-MAT s24: m_f ~ m/3.
+        const bool to_pull = nf > 0 && p.s.force_dir != 1 &&
+                             (p.s.force_dir == 2 || 3.0 * (double)mf > (double)p.g.m);
+        if (to_pull) {
+            trace_put(p.s, it, DIR_PUSH, filt, ls.cnt, nf, mf, hi);
+            nf_prev = (uint32_t)nf;
+            dir = DIR_PULL;
+            ready = 0;
+            break;
+        }
         if (nf > 0 && overflow) {
             ++st.ballot;
             st.scanned += p.s.nwords * 32;
@@ -149,43 +235,229 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_push(SsspP p) {
             }
             hi = ((uint64_t)mn / p.delta + 1) * p.delta;
             ++st.ballot;
+            // moved vertices become this iteration's frontier: list entries AND bitmap bits
+            uint32_t* fbm = p.s.bm[it % 3];
             FarWords src{p.far, p.dist, hi};
             if (!ballot_filter(src, p.s, BallotOut{p.s.lists[it & 1], p.s.cstride, p.g.dout}, cnt,
-                               [&](uint32_t v, uint32_t) { p.far[v >> 5] &= ~(1u << (v & 31)); }))
+                               [&](uint32_t v, uint32_t) {
+                                   p.far[v >> 5] &= ~(1u << (v & 31));
+                                   fbm[v >> 5] |= 1u << (v & 31);
+                               }))
                 return;
             if (!grid_sync(c)) return;
             view_contig(cnt);
             slotted = 0;
             filt = 1;
         }
-        trace_put(p.s, it, DIR_PUSH, filt, cnt, nf, 0, hi);
+        trace_put(p.s, it, DIR_PUSH, filt, cnt, nf, mf, hi);
+        nf_prev = (uint32_t)(nf ? nf : sum4(cnt));
         if (p.s.max_iters && it >= p.s.max_iters) {
             done = 1;
             break;
         }
         if (!p.s.fusion) break;
     }
-    flush_stats(c, st, DIR_PUSH);
-    if (lead()) {
-        c->iter = it;
-        c->hi = hi;
-        c->done = done;
-        c->slotted = slotted;
-        for (int i = 0; i < NCLS; ++i) c->cur_count[i] = cnt[i];
-        grid_end(c);
-        c->launch += 1;
+    sssp_exit(p, DIR_PUSH, it, hi, nf_prev, dir, done, ready, slotted, cnt, st);
+}
+
+// ------------------------------------------------------------------ pull
+// Every vertex with in-edges folds min(dist(v) + w) over its in-neighbours v in
+// the frontier bitmap.  Vertices are visited in chunks of 1024 (dynamic, one
+// warp per chunk), compacted into a shared-memory list and processed 32 per
+// round: in-degree < sep_small on the lane (thread granularity, 128-bit loads),
+// larger rows by the warp (warp granularity, 128 edges per step, min tree),
+// in-degree >= sep_huge beforehand by the whole grid.
+__global__ void __launch_bounds__(BLOCK, 4) sssp_pull(SsspP p) {
+    Ctl* c = p.s.ctl;
+    if (vload(&c->done) || vload(&c->dir) != DIR_PULL) return;
+    grid_begin(c);
+    const uint64_t n = p.g.n;
+    const uint64_t nw = (n + 31) >> 5;
+    uint32_t it = vload(&c->iter);
+    const uint64_t hi = vload(&c->hi);
+    uint32_t nf_prev = vload(&c->nf_prev);
+    uint32_t cnt[NCLS] = {0, 0, 0, 0};
+    Stats st;
+    uint32_t dir = DIR_PULL, done = 0;
+    const uint32_t lane = lane_id();
+    __shared__ uint32_t s_cand[WARPS][1024];
+    __shared__ uint32_t s_found[WARPS][32];
+    __shared__ uint32_t s_far[WARPS][32];
+    uint32_t* s_c = s_cand[warp_id()];
+    uint32_t* s_f = s_found[warp_id()];
+    uint32_t* s_r = s_far[warp_id()];
+    auto relax_term = [&](const uint32_t* cur, uint32_t u, uint32_t w) -> uint32_t {
+        return bm_test(cur, u) ? p.dist[u] + w : INF;
+    };
+    for (;;) {
+        IterLine* nx = &c->line[(it + 1) % 3];
+        maybe_reset_line(&c->line[(it + 2) % 3]);
+        clear_bitmap(p.s.bm[(it + 2) % 3], p.s.nwords);
+        const uint32_t* cur = p.s.bm[it % 3];
+        uint32_t* nbm = p.s.bm[(it + 1) % 3];
+        uint64_t mdeg = 0, edges = 0;
+        uint32_t found = 0;
+        // grid granularity: huge in-degree rows, block-min then one atomicMin
+        for (uint32_t i = 0; i < p.nh; ++i) {
+            const uint32_t u = p.hlist[i];
+            const uint64_t beg = __ldg(p.g.irp + u), end = __ldg(p.g.irp + u + 1);
+            uint32_t best = INF;
+            for_edges_w(p.g.ici, p.g.iw8, p.g.iw32, beg, end, gtid(), gthreads(), [&](uint64_t, uint32_t v, uint32_t w) {
+                best = min(best, relax_term(cur, v, w));
+            });
+            best = block_min(best);
+            if (threadIdx.x == 0 && best != INF) {
+                const uint32_t old = atomicMin(p.dist + u, best);
+                if (best < old) {
+                    if ((uint64_t)best < hi) {
+                        if (!(atomicOr(nbm + (u >> 5), 1u << (u & 31)) & (1u << (u & 31)))) {
+                            ++found;
+                            mdeg += __ldg(p.g.dout + u);
+                        }
+                    } else {
+                        bm_set(p.far, u);
+                    }
+                }
+            }
+            if (lead()) edges += end - beg;
+        }
+        // thread / warp granularity over chunks of 1024 vertices
+        const uint32_t nchunks = (uint32_t)((nw + 31) >> 5);
+        uint32_t s_cur = my_slot(), tries = 0;
+        uint32_t chunk = 0;
+        if (lane == 0) chunk = grab_chunk(nx, nchunks, s_cur, tries);
+        chunk = __shfl_sync(FULL, chunk, 0);
+        while (chunk != INF) {
+            uint32_t chunk_n = 0;
+            if (lane == 0) chunk_n = grab_chunk(nx, nchunks, s_cur, tries);
+            const uint64_t w0 = (uint64_t)chunk << 5;
+            const uint64_t wl = w0 + lane;
+            const uint32_t cand_l = wl < nw ? __ldg(p.g.nz_in + wl) : 0u;
+            const uint32_t cnt_l = __popc(cand_l);
+            uint32_t incl = cnt_l;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULL, incl, o);
+                if ((int)lane >= o) incl += y;
+            }
+            const uint32_t total = __shfl_sync(FULL, incl, 31);
+            if (total) {
+                uint32_t pos = incl - cnt_l;
+                for (uint32_t w = cand_l; w; w &= w - 1) s_c[pos++] = (uint32_t)(wl << 5) + (__ffs(w) - 1);
+                s_f[lane] = 0;
+                s_r[lane] = 0;
+                __syncwarp();
+                uint32_t v_n = 0;
+                uint64_t beg_n = 0, end_n = 0;
+                if (lane < total) {
+                    v_n = s_c[lane];
+                    beg_n = __ldg(p.g.irp + v_n);
+                    end_n = __ldg(p.g.irp + v_n + 1);
+                }
+                for (uint32_t r = 0; r < total; r += 32) {
+                    const uint32_t v = v_n;
+                    const uint64_t beg = beg_n, end = end_n;
+                    const bool mine = r + lane < total && end - beg < p.s.sep_huge;
+                    beg_n = end_n = 0;
+                    if (r + 32 + lane < total) {
+                        v_n = s_c[r + 32 + lane];
+                        beg_n = __ldg(p.g.irp + v_n);
+                        end_n = __ldg(p.g.irp + v_n + 1);
+                    }
+                    const bool small = mine && end - beg < p.s.sep_small;
+                    uint32_t best = INF;
+                    if (small) {
+                        for_edges_w(p.g.ici, p.g.iw8, p.g.iw32, beg, end, 0, 1, [&](uint64_t, uint32_t u, uint32_t w) {
+                            best = min(best, relax_term(cur, u, w));
+                        });
+                        edges += end - beg;
+                    }
+                    uint32_t todo = __ballot_sync(FULL, mine && !small);
+                    while (todo) {
+                        const int l = __ffs(todo) - 1;
+                        todo &= todo - 1;
+                        const uint64_t b0 = __shfl_sync(FULL, beg, l), e0 = __shfl_sync(FULL, end, l);
+                        uint32_t wb = INF;
+                        for_edges_w(p.g.ici, p.g.iw8, p.g.iw32, b0, e0, lane, 32, [&](uint64_t, uint32_t u, uint32_t w) {
+                            wb = min(wb, relax_term(cur, u, w));
+                        });
+                        wb = warp_min(wb);
+                        if ((int)lane == l) {
+                            best = wb;
+                            edges += e0 - b0;
+                        }
+                    }
+                    if (mine && best < p.dist[v]) {
+                        p.dist[v] = best;  // single owner
+                        if ((uint64_t)best < hi) {
+                            atomicOr(s_f + ((v >> 5) - w0), 1u << (v & 31));
+                            mdeg += p.sym ? (end - beg) : __ldg(p.g.dout + v);
+                        } else {
+                            atomicOr(s_r + ((v >> 5) - w0), 1u << (v & 31));
+                        }
+                    }
+                }
+                __syncwarp();
+                const uint32_t fm = s_f[lane], fa = s_r[lane];
+                if (fm) {
+                    atomicOr(nbm + wl, fm);  // the grid-wide fold may own bits of the same word
+                    found += __popc(fm);
+                }
+                if (fa) atomicOr(p.far + wl, fa);
+                __syncwarp();
+            }
+            chunk = __shfl_sync(FULL, chunk_n, 0);
+        }
+        st.edges += edges;
+        {
+            uint64_t v2[2] = {mdeg, found};
+            block_sum<2>(v2);
+            if (threadIdx.x == 0) {
+                Slot& sl = nx->s[my_slot()];
+                if (v2[0]) atomicAdd(&sl.mdeg, (unsigned long long)v2[0]);
+                if (v2[1]) atomicAdd(&sl.found, (unsigned int)v2[1]);
+            }
+        }
+        st.scanned += (lead() ? nw * 32 : 0);
+        if (!grid_sync(c)) return;
+        LineSum ls;
+        read_line(nx, ls);
+        const uint64_t nf = ls.found;
+        ++it;
+        ++st.iters;
+        ++st.pull;
+        const uint32_t tc[NCLS] = {0u, 0u, 0u, 0u};
+        trace_put(p.s, it, DIR_PULL, 1u, tc, nf, ls.mdeg, hi);
+        if (p.s.max_iters && it >= p.s.max_iters) {
+            done = 1;
+            break;
+        }
+        // an empty frontier goes back to push, which owns the bucket advance
+        const bool to_push = nf == 0 || p.s.force_dir == 1 ||
+                             (p.s.force_dir == 0 && 3.0 * (double)ls.mdeg <= (double)p.g.m);
+        nf_prev = (uint32_t)nf;
+        if (to_push) {
+            dir = DIR_PUSH;
+            break;
+        }
+        if (!p.s.fusion) break;
     }
+    sssp_exit(p, DIR_PULL, it, hi, nf_prev, dir, done, 0u, 0u, cnt, st);
 }
 
 }  // namespace sx
 
 using namespace sx;
 
-// Algorithmic bytes: per list entry 4 B list + 16 B row_ptr pair +
-// 4 B dist(v); per edge 4 B col + weight + 4 B dist(u); per iteration one
-// bitmap clear (n/8); ballot / far scans n/8.
+// Algorithmic bytes: push — per list entry 4 B list + 16 B row_ptr
+// pair + 4 B dist(v); per edge 4 B col + weight + 4 B dist(u); per iteration one
+// bitmap clear (n/8); ballot / far scans n/8.  Pull — every in-edge of every
+// vertex once (4 B col + weight) + the frontier bitmap + row_ptr + dist, per
+// pull iteration.
 static double sssp_bytes(const sx_graph g, const sxh::Counters& c) {
     const double n = (double)g->n;
+    if (c.pull > 0)
+        return c.pull * ((4.0 + g->wbytes) * (double)g->mi + 12.0 * n + 2.0 * n / 8.0) + c.scanned / 8.0;
     return 24.0 * c.entries + (8.0 + g->wbytes) * c.edges + c.iters * n / 8.0 + c.scanned / 8.0;
 }
 
@@ -199,6 +471,7 @@ extern "C" sx_status sx_sssp(sx_graph g, uint32_t src, uint32_t delta, const sx_
     if (!g->w || g->wbytes == 0) return sxh::fail(SX_E_WEIGHT, "sx_sssp: graph has no edge weights");
     if (g->has_zero_w) return sxh::fail(SX_E_WEIGHT, "sx_sssp: zero edge weight (P:361 assumes positive weights)");
     sxh::Run run{g, sxh::resolve_opts(opts), stats};
+    if (g->directed && !g->has_rev) run.o.force_dir = 1;  // no in-rows: push only
     cudaStream_t s = g->ctx->stream;
     SsspP p;
     if ((rc = run.begin()) != SX_OK) return rc;
@@ -207,18 +480,32 @@ extern "C" sx_status sx_sssp(sx_graph g, uint32_t src, uint32_t delta, const sx_
     const bool dev_out = sxh::is_device_ptr(dist_out);
     p.dist = dev_out ? dist_out : g->st[0];
     p.far = g->aux_bm;
+    p.hlist = g->st[3];
     p.delta = delta;
+    p.sym = !g->directed;
     SX_CU(cudaMemsetAsync(p.dist, 0xFF, g->n * 4, s));
     SX_CU(cudaMemsetAsync(p.far, 0, g->nwords * 4, s));
     for (int i = 0; i < 3; ++i) SX_CU(cudaMemsetAsync(p.s.bm[i], 0, g->nwords * 4, s));
+    // the grid-wide (huge in-degree) fold list of the pull kernel
+    uint32_t* dcount = g->st[2];
+    SX_CU(cudaMemsetAsync(dcount, 0, 4, s));
+    k_huge_list<<<4 * g->ctx->prop.multiProcessorCount, 256, 0, s>>>(g->din, g->n, run.o.sep_huge, p.hlist, dcount);
+    SX_CU(cudaMemcpyAsync(&p.nh, dcount, 4, cudaMemcpyDeviceToHost, s));
+    SX_CU(cudaStreamSynchronize(s));
     sssp_init<<<1, 32, 0, s>>>(p, src);
     SX_CU(cudaGetLastError());
     void* args[] = {&p};
     g->ctx->h_ctl->done = 0;
+    uint32_t dir = DIR_PUSH;
     for (;;) {
-        if ((rc = run.launch((const void*)sssp_push, args, false)) != SX_OK) return rc;
+        const void* first = dir == DIR_PULL ? (const void*)sssp_pull : (const void*)sssp_push;
+        const void* second = dir == DIR_PULL ? (const void*)sssp_push : (const void*)sssp_pull;
+        if ((rc = run.launch(first, args, dir == DIR_PULL)) != SX_OK) return rc;
+        if ((rc = run.launch(second, args, dir != DIR_PULL)) != SX_OK) return rc;
+        if ((rc = run.launch(first, args, dir == DIR_PULL)) != SX_OK) return rc;
         if ((rc = run.sync()) != SX_OK) return rc;
         if (g->ctx->h_ctl->done) break;
+        dir = g->ctx->h_ctl->dir;
     }
     if ((rc = run.end(sssp_bytes)) != SX_OK) return rc;
     return dev_out ? SX_OK : sxh::copy_out(g, dist_out, p.dist, g->n * 4);

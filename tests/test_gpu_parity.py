@@ -112,13 +112,21 @@ def test_bfs_modes_rmat(ctx, rmat14, mode):
     G.free()
 
 
-@pytest.mark.parametrize("mode", MODES[:6], ids=[str(m) for m in MODES[:6]])
+SK_MODES = MODES[:6] + [dict(force_dir=2, fusion=0), dict(local_chain=0), dict(local_chain=100000),
+                        dict(local_chain=3, force_filter=2)]
+
+
+@pytest.mark.parametrize("mode", SK_MODES, ids=[str(m) for m in SK_MODES])
 def test_sssp_kcore_modes_rmat(ctx, rmat14, mode):
     G = up(ctx, rmat14)
     m = {k: v for k, v in mode.items() if k != "force_dir"}
     for delta in (0, 64, 1024):
-        d, _, _ = G.sssp(0, delta, **m)
+        d, st, _ = G.sssp(0, delta, **mode)
         assert np.array_equal(d, oracle.sssp(rmat14, 0)), (mode, delta)
+        if mode.get("force_dir") == 2:
+            assert st["pull_iters"] > 0
+        if mode.get("force_dir") == 1:
+            assert st["pull_iters"] == 0
     core, _, _ = G.kcore(0, **m)
     assert np.array_equal(core, oracle.coreness(rmat14)), mode
     mk, _, _ = G.kcore(16, **m)
