@@ -135,7 +135,7 @@ void sx_graph_free(sx_graph g);
 /* -------------------------------------------------------------- run knobs */
 typedef struct {
     uint32_t iter;       /* 1-based iteration number */
-    uint32_t dir;        /* 0 push, 1 pull */
+    uint32_t dir;        /* 0 push, 1 pull, 2 push on one thread-block cluster (cluster_enter) */
     uint32_t filter;     /* how the NEXT list was produced: 0 online, 1 ballot, 2 static (pull-all lists) */
     uint32_t launch;     /* 0-based index of the kernel launch that ran this iteration */
     uint32_t n_active[4];/* next-iteration list sizes: small / medium / large / huge;
@@ -163,6 +163,11 @@ typedef struct {
                                     (chaotic relaxation, reading 12; results unchanged); 0 = strict BSP.
                                     Ignored by BFS (levels are BSP-exact). Default 0: measured on the 2048^2
                                     grid, chains cut iterations 1.6x but lengthened each one more. */
+    uint32_t cluster_enter;      /* SSSP push (B200 addition): when the next frontier has at most this many
+                                    vertices the iterations continue on ONE thread-block cluster of 8 CTAs
+                                    synchronised by the hardware cluster barrier instead of the grid
+                                    barrier; back to the full grid above 8x this size.  0 = never.
+                                    Default 2048. */
 } sx_opts;
 
 typedef struct {

@@ -127,6 +127,7 @@ Sched make_sched(const sx_graph g, const sx_opts& o) {
     s.fusion = o.fusion;
     s.max_iters = o.max_iters;
     s.local_chain = o.local_chain;
+    s.cluster_enter = o.cluster_enter;
     return s;
 }
 
@@ -171,6 +172,27 @@ sx_status Run::launch(const void* fn, void** args, bool pull) {
     ++(pull ? launches_pull : launches_push);
     ++launches;
     if (launches > 10000000) return fail(SX_E_STATE, "runaway launch loop");
+    return SX_OK;
+}
+
+sx_status Run::launch_plain(const void* fn, void** args, int grid, int block, bool pull) {
+    sx_ctx c = g->ctx;
+    if (npending == EV_POOL) {
+        sx_status rc = sync();
+        if (rc != SX_OK) return rc;
+    }
+    // cluster kernels of 16 CTAs need the non-portable size opt-in (idempotent)
+    SX_CU(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    SX_CU(cudaEventRecord(c->evp[2 * npending], c->stream));
+    cudaError_t e = cudaLaunchKernel(fn, dim3(grid), dim3(block), args, 0, c->stream);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return cuda_fail(e, "cudaLaunchKernel");
+    }
+    SX_CU(cudaEventRecord(c->evp[2 * npending + 1], c->stream));
+    pend_pull[npending++] = pull;
+    ++(pull ? launches_pull : launches_push);
+    ++launches;
     return SX_OK;
 }
 
@@ -288,6 +310,7 @@ void sx_opts_default(sx_opts* o) {
     o->trace = nullptr;
     o->trace_cap = 0;
     o->local_chain = 0;
+    o->cluster_enter = 2048;
 }
 
 sx_status sx_ctx_create(int device, void* cuda_stream, sx_ctx* out) {

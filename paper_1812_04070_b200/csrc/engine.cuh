@@ -45,7 +45,9 @@ constexpr int TILE_WORDS = BLOCK;  // ballot tile: one bitmap word per thread
 constexpr int NSLOT = 32;          // counter slots (L2 lines) per iteration line
 constexpr int BAR_GROUPS = 32;     // two-level barrier: <= 32 groups of CTAs
 
-enum : uint32_t { DIR_PUSH = 0, DIR_PULL = 1 };
+enum : uint32_t { DIR_PUSH = 0, DIR_PULL = 1, DIR_CLUSTER = 2 };
+constexpr int CL_CTAS = 16;      // CTAs of the small-frontier cluster kernel (non-portable size 16)
+constexpr int CL_BLOCK = 1024;   // threads per CTA of the cluster kernel
 enum : uint32_t { ERR_NONE = 0, ERR_BARRIER = 7 };
 
 // ---------------------------------------------------------------- control block
@@ -86,6 +88,11 @@ struct Ctl {
     unsigned long long hi;           // SSSP: current bucket upper bound (exclusive)
     unsigned int cur_count[NCLS];    // contiguous list sizes for iteration `iter`
     unsigned int ntrace;
+    // --- small-frontier cluster mode: list counts by iteration (it % 3) and a min scratch
+    struct alignas(128) ClusterLine {
+        unsigned int cnt[3];
+        unsigned int minv;
+    } cl;
     // --- run statistics per direction of the launch (0 push, 1 pull), one atomic per CTA per launch
     struct alignas(128) StatBlock {
         unsigned long long edges, entries, scanned, reached;
@@ -135,6 +142,7 @@ struct Sched {
     int force_filter, force_dir, fusion;
     uint32_t max_iters;
     uint32_t local_chain;   // SSSP / k-core: vertices a thread may process in a row within one iteration
+    uint32_t cluster_enter; // SSSP: frontier size at or below which one thread-block cluster continues
 };
 
 // ---------------------------------------------------------------- small helpers
@@ -759,8 +767,15 @@ __device__ __forceinline__ void for_tasks(const uint32_t* lists, const Sched& s,
     for (uint32_t i = 0; i < cnt[3]; ++i) vf(task_at(lists, s, 3, i), gtid(), gthreads(), 3u);
     for (uint32_t i = blockIdx.x; i < cnt[2]; i += gridDim.x)
         vf(task_at(lists, s, 2, i), (uint64_t)threadIdx.x, (uint64_t)BLOCK, 2u);
-    for (uint64_t i = gwarp(); i < cnt[1]; i += gwarps()) vf(task_at(lists, s, 1, (uint32_t)i), (uint64_t)lane_id(), 32ull, 1u);
-    for (uint64_t i = gtid(); i < cnt[0]; i += gthreads()) vf(task_at(lists, s, 0, (uint32_t)i), 0ull, 1ull, 0u);
+    // CTA-major spreading: consecutive warp tasks / 32-task chunks go to different
+    // CTAs, so a small frontier runs on many SMs instead of the first few.
+    const uint64_t wslot = blockIdx.x + (uint64_t)warp_id() * gridDim.x;
+    for (uint64_t i = wslot; i < cnt[1]; i += gwarps()) vf(task_at(lists, s, 1, (uint32_t)i), (uint64_t)lane_id(), 32ull, 1u);
+    const uint64_t nch = ((uint64_t)cnt[0] + 31) >> 5;
+    for (uint64_t ch = wslot; ch < nch; ch += gwarps()) {
+        const uint64_t i = (ch << 5) + lane_id();
+        if (i < cnt[0]) vf(task_at(lists, s, 0, (uint32_t)i), 0ull, 1ull, 0u);
+    }
 }
 
 // ---------------------------------------------------------------- bookkeeping

@@ -102,7 +102,8 @@ sx_status sx_graph_upload(sx_ctx ctx, const sx_csr_desc* d, sx_graph* out) {
             *dst = (std::remove_pointer_t<decltype(dst)>)src;
             return SX_OK;
         }
-        sx_status r = dalloc((char**)dst, count * elem);
+        // +16 B: kernels read whole aligned 16-B groups of ids / weights (masked)
+        sx_status r = dalloc((char**)dst, count * elem + 16);
         if (r != SX_OK) return r;
         if (count) SX_CU(cudaMemcpyAsync(*dst, src, count * elem, cudaMemcpyDefault, s));
         return SX_OK;

@@ -92,6 +92,8 @@ struct Run {
     sx_status begin();
     // Enqueue one persistent kernel (timed with an event pair); no host sync.
     sx_status launch(const void* fn, void** args, bool pull);
+    // Same for a non-cooperative launch with an explicit shape (e.g. one cluster).
+    sx_status launch_plain(const void* fn, void** args, int grid, int block, bool pull);
     // Read back the control block, accumulate the pending launches' times, check errors.
     sx_status sync();
     sx_status end(BytesFn bytes);

@@ -148,19 +148,63 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_push(SsspP p) {
                 const uint32_t dv = p.dist[v];
                 const bool can_chain = size == 1 && depth < p.s.local_chain;
                 uint32_t next = INF;
-                for_edges_w(p.g.ci, p.g.w8, p.g.w32, beg, end, rank, size, [&](uint64_t, uint32_t u, uint32_t w) {
-                    ++edges;
-                    const uint32_t nd = dv + w;
-                    if (nd >= p.dist[u]) return;
-                    const uint32_t old = atomicMin(p.dist + u, nd);
-                    if (nd >= old) return;
+                auto improved = [&](uint32_t u, uint32_t nd) {
                     if ((uint64_t)nd < hi) {
                         if (can_chain && next == INF) next = u;
                         else record(u);
                     } else if (!bm_test(p.far, u)) {
                         bm_set(p.far, u);
                     }
-                });
+                };
+                if (size == 1) {
+                    // thread granularity: 4 edges per step with their loads and
+                    // atomics in flight together (one aligned 128-bit id load, one
+                    // 32-bit weight load); the edges' chains would otherwise serialise
+                    for (uint64_t e = beg; e < end;) {
+                        const uint64_t a = e & ~3ull;
+                        const uint4 q = __ldg(reinterpret_cast<const uint4*>(p.g.ci + a));
+                        const uint32_t u[4] = {q.x, q.y, q.z, q.w};
+                        uint32_t w[4];
+                        if (p.g.w8) {
+                            const uint32_t ww = __ldg(reinterpret_cast<const uint32_t*>(p.g.w8 + a));
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) w[k] = (ww >> (8 * k)) & 0xFF;
+                        } else {
+                            const uint4 ww = __ldg(reinterpret_cast<const uint4*>(p.g.w32 + a));
+                            w[0] = ww.x;
+                            w[1] = ww.y;
+                            w[2] = ww.z;
+                            w[3] = ww.w;
+                        }
+                        bool ok[4];
+                        uint32_t nd[4], cur[4], old[4];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            ok[k] = a + k >= e && a + k < end;
+                            nd[k] = dv + w[k];
+                            cur[k] = ok[k] ? p.dist[u[k]] : 0u;
+                        }
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            ok[k] = ok[k] && nd[k] < cur[k];
+                            old[k] = ok[k] ? atomicMin(p.dist + u[k], nd[k]) : 0u;
+                        }
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            if (ok[k] && nd[k] < old[k]) improved(u[k], nd[k]);
+                        const uint64_t stop = min(end, a + 4);
+                        edges += stop - e;
+                        e = stop;
+                    }
+                } else {
+                    for_edges_w(p.g.ci, p.g.w8, p.g.w32, beg, end, rank, size, [&](uint64_t, uint32_t u, uint32_t w) {
+                        ++edges;
+                        const uint32_t nd = dv + w;
+                        if (nd >= p.dist[u]) return;
+                        const uint32_t old = atomicMin(p.dist + u, nd);
+                        if (nd < old) improved(u, nd);
+                    });
+                }
                 if (next == INF) break;
                 v = next;
             }
@@ -192,6 +236,14 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_push(SsspP p) {
             trace_put(p.s, it, DIR_PUSH, filt, ls.cnt, nf, mf, hi);
             nf_prev = (uint32_t)nf;
             dir = DIR_PULL;
+            ready = 0;
+            break;
+        }
+        if (nf > 0 && nf <= p.s.cluster_enter && p.s.force_filter != 2 && p.s.fusion) {
+            // small frontier: continue on one thread-block cluster (frontier handed over as bm[it % 3])
+            trace_put(p.s, it, DIR_PUSH, filt, ls.cnt, nf, mf, hi);
+            nf_prev = (uint32_t)nf;
+            dir = DIR_CLUSTER;
             ready = 0;
             break;
         }
@@ -445,6 +497,221 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_pull(SsspP p) {
     sssp_exit(p, DIR_PULL, it, hi, nf_prev, dir, done, 0u, 0u, cnt, st);
 }
 
+// ------------------------------------------------------------------ small-frontier cluster mode
+// When the frontier is small the grid barrier (~3 us for 600+ CTAs) dominates an
+// iteration.  The push then continues on ONE thread-block cluster of 8 CTAs x
+// 1024 threads whose barrier is the hardware cluster barrier
+// (barrier.cluster.arrive.release / wait.acquire): same ACC step, online filter
+// into one list, same delta-stepping, no grid barrier.  It hands the frontier
+// back to the grid kernels (as the bitmap bm[it % 3]) once it exceeds
+// 8 x cluster_enter vertices.  Bitmap invariant kept for the grid kernels:
+// consumers clear their frontier bits, so bm[(it+1)%3] and bm[(it+2)%3] are zero.
+__device__ __forceinline__ void cluster_barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// warp-aggregated append to a list with a global counter
+__device__ __forceinline__ void cl_append(uint32_t* list, unsigned int* cnt, uint32_t u) {
+    const uint32_t m = __activemask();
+    const int leader = __ffs(m) - 1;
+    uint32_t base = 0;
+    if ((int)lane_id() == leader) base = atomicAdd(cnt, (uint32_t)__popc(m));
+    base = __shfl_sync(m, base, leader);
+    list[base + __popc(m & lanemask_lt())] = u;
+}
+
+__global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) sssp_cluster(SsspP p) {
+    Ctl* c = p.s.ctl;
+    if (vload(&c->done) || vload(&c->dir) != DIR_CLUSTER) return;
+    constexpr uint32_t T = CL_CTAS * CL_BLOCK;
+    const uint32_t tid = cluster_rank() * CL_BLOCK + threadIdx.x;
+    const bool lead0 = tid == 0;
+    const uint64_t n = p.g.n;
+    const uint64_t nw = (n + 31) >> 5;
+    uint32_t it = vload(&c->iter);
+    uint64_t hi = vload(&c->hi);
+    Ctl::ClusterLine* cl = &c->cl;
+    uint64_t edges = 0, entries = 0;
+    uint32_t iters = 0, ballots = 0, done = 0, dir = DIR_CLUSTER;
+    // entry: zero the counters and the stale bitmap, list the frontier bitmap
+    if (lead0) {
+        cl->cnt[0] = cl->cnt[1] = cl->cnt[2] = 0;
+        cl->minv = INF;
+    }
+    for (uint64_t wi = tid; wi < p.s.nwords; wi += T) p.s.bm[(it + 2) % 3][wi] = 0;
+    cluster_barrier();
+    {
+        uint32_t* L = p.s.lists[it & 1];
+        for (uint64_t wi = tid; wi < nw; wi += T) {
+            const uint32_t w = p.s.bm[it % 3][wi];
+            if (!w) continue;
+            const uint32_t base = atomicAdd(&cl->cnt[it % 3], (uint32_t)__popc(w));
+            uint32_t k = 0;
+            for (uint32_t x = w; x; x &= x - 1) L[base + k++] = (uint32_t)(wi << 5) + (__ffs(x) - 1);
+        }
+    }
+    cluster_barrier();
+    for (;;) {
+        const uint32_t ncur = vload(&cl->cnt[it % 3]);
+        if (lead0) cl->cnt[(it + 2) % 3] = 0;
+        const uint32_t* L = p.s.lists[it & 1];
+        uint32_t* NL = p.s.lists[(it + 1) & 1];
+        uint32_t* cur = p.s.bm[it % 3];
+        uint32_t* nbm = p.s.bm[(it + 1) % 3];
+        unsigned int* ncnt = &cl->cnt[(it + 1) % 3];
+        for (uint32_t i = tid; i < ncur; i += T) {
+            const uint32_t v = L[i];
+            atomicAnd(cur + (v >> 5), ~(1u << (v & 31)));  // consumed: keep the bitmaps clean
+            const uint64_t beg = __ldg(p.g.rp + v), end = __ldg(p.g.rp + v + 1);
+            const uint32_t dv = p.dist[v];
+            ++entries;
+            // 4 edges per step, their loads and atomics in flight together
+            for (uint64_t e = beg; e < end;) {
+                const uint64_t a = e & ~3ull;
+                const uint4 q = __ldg(reinterpret_cast<const uint4*>(p.g.ci + a));
+                const uint32_t u[4] = {q.x, q.y, q.z, q.w};
+                uint32_t w[4];
+                if (p.g.w8) {
+                    const uint32_t ww = __ldg(reinterpret_cast<const uint32_t*>(p.g.w8 + a));
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) w[k] = (ww >> (8 * k)) & 0xFF;
+                } else {
+                    const uint4 ww = __ldg(reinterpret_cast<const uint4*>(p.g.w32 + a));
+                    w[0] = ww.x;
+                    w[1] = ww.y;
+                    w[2] = ww.z;
+                    w[3] = ww.w;
+                }
+                bool ok[4];
+                uint32_t nd[4], cu[4], old[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    ok[k] = a + k >= e && a + k < end;
+                    nd[k] = dv + w[k];
+                    cu[k] = ok[k] ? p.dist[u[k]] : 0u;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    ok[k] = ok[k] && nd[k] < cu[k];
+                    old[k] = ok[k] ? atomicMin(p.dist + u[k], nd[k]) : 0u;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (!(ok[k] && nd[k] < old[k])) continue;
+                    if ((uint64_t)nd[k] < hi) {
+                        if (!bm_test(nbm, u[k]) && bm_claim(nbm, u[k])) cl_append(NL, ncnt, u[k]);
+                    } else if (!bm_test(p.far, u[k])) {
+                        bm_set(p.far, u[k]);
+                    }
+                }
+                const uint64_t stop = min(end, a + 4);
+                edges += stop - e;
+                e = stop;
+            }
+        }
+        cluster_barrier();
+        uint32_t nnext = vload(ncnt);
+        ++it;
+        ++iters;
+        uint32_t filt = 0;
+        if (nnext == 0) {
+            if (p.delta == 0) {
+                done = 1;
+            } else {
+                // bucket advance over the far pile
+                uint32_t mn = INF;
+                for (uint64_t wi = tid; wi < nw; wi += T)
+                    for (uint32_t x = p.far[wi]; x; x &= x - 1) mn = min(mn, p.dist[(wi << 5) + (__ffs(x) - 1)]);
+                mn = warp_min(mn);
+                if (lane_id() == 0 && mn != INF) atomicMin(&cl->minv, mn);
+                cluster_barrier();
+                mn = vload(&cl->minv);
+                cluster_barrier();
+                if (lead0) cl->minv = INF;
+                if (mn == INF) {
+                    done = 1;
+                } else {
+                    hi = ((uint64_t)mn / p.delta + 1) * p.delta;
+                    uint32_t* L2 = p.s.lists[it & 1];
+                    unsigned int* c2 = &cl->cnt[it % 3];
+                    uint32_t* fbm = p.s.bm[it % 3];
+                    for (uint64_t wi = tid; wi < nw; wi += T) {
+                        const uint32_t f = p.far[wi];
+                        uint32_t mv = 0;
+                        for (uint32_t x = f; x; x &= x - 1) {
+                            const int b = __ffs(x) - 1;
+                            if ((uint64_t)p.dist[(wi << 5) + b] < hi) mv |= 1u << b;
+                        }
+                        if (mv) {
+                            p.far[wi] = f & ~mv;  // single owner of the word
+                            fbm[wi] |= mv;
+                            for (uint32_t x = mv; x; x &= x - 1) cl_append(L2, c2, (uint32_t)(wi << 5) + (__ffs(x) - 1));
+                        }
+                    }
+                    cluster_barrier();
+                    nnext = vload(c2);
+                    ++ballots;
+                    filt = 1;
+                }
+            }
+        }
+        if (lead0 && p.s.trace) {
+            const uint32_t tc[NCLS] = {nnext, 0u, 0u, 0u};
+            const uint32_t i = c->ntrace++;
+            if (i < p.s.trace_cap) {
+                TraceRec r;
+                r.iter = it;
+                r.dir = DIR_CLUSTER;
+                r.filter = filt;
+                r.launch = c->launch;
+                for (int k = 0; k < NCLS; ++k) r.n_active[k] = tc[k];
+                r.n_frontier = nnext;
+                r.m_active = 0;
+                r.aux = hi;
+                r.t_ns = globaltimer();
+                p.s.trace[i] = r;
+            }
+        }
+        if (done) break;
+        if (p.s.max_iters && it >= p.s.max_iters) {
+            done = 1;
+            break;
+        }
+        if (nnext > 8u * p.s.cluster_enter) {  // frontier too big for one cluster: back to the grid
+            dir = DIR_PUSH;
+            break;
+        }
+    }
+    // statistics: warp sums, one atomic per warp
+    const uint64_t e = warp_sum(edges), en = warp_sum(entries);
+    if (lane_id() == 0) {
+        if (e) atomicAdd(&c->st[0].edges, (unsigned long long)e);
+        if (en) atomicAdd(&c->st[0].entries, (unsigned long long)en);
+    }
+    cluster_barrier();
+    if (lead0) {
+        c->st[0].iters += iters;
+        c->st[0].ballot += ballots;
+        c->st[0].scanned += (uint64_t)ballots * p.s.nwords * 32;
+        c->iter = it;
+        c->hi = hi;
+        c->done = done;
+        c->dir = dir;
+        c->lists_ready = 0;  // the grid kernels rebuild their lists from bm[it % 3]
+        c->slotted = 0;
+        c->nf_prev = vload(&cl->cnt[it % 3]);
+        for (int h = 0; h < 2; ++h) {  // leave both grid-barrier halves zeroed
+            for (int i = 0; i < BAR_GROUPS; ++i) c->bar_grp[h][i].count = 0;
+            c->bar_top[h].count = 0;
+        }
+        c->launch += 1;
+    }
+}
+
 }  // namespace sx
 
 using namespace sx;
@@ -496,13 +763,18 @@ extern "C" sx_status sx_sssp(sx_graph g, uint32_t src, uint32_t delta, const sx_
     SX_CU(cudaGetLastError());
     void* args[] = {&p};
     g->ctx->h_ctl->done = 0;
+    // Selective fusion: one launch per direction phase (push grid, pull grid, push
+    // on one cluster); a launch whose phase does not match the device state exits
+    // at once, so the likely next phases are enqueued without a host round trip.
     uint32_t dir = DIR_PUSH;
+    auto enqueue = [&](uint32_t d) -> sx_status {
+        if (d == DIR_CLUSTER) return run.launch_plain((const void*)sssp_cluster, args, CL_CTAS, CL_BLOCK, false);
+        return run.launch(d == DIR_PULL ? (const void*)sssp_pull : (const void*)sssp_push, args, d == DIR_PULL);
+    };
     for (;;) {
-        const void* first = dir == DIR_PULL ? (const void*)sssp_pull : (const void*)sssp_push;
-        const void* second = dir == DIR_PULL ? (const void*)sssp_push : (const void*)sssp_pull;
-        if ((rc = run.launch(first, args, dir == DIR_PULL)) != SX_OK) return rc;
-        if ((rc = run.launch(second, args, dir != DIR_PULL)) != SX_OK) return rc;
-        if ((rc = run.launch(first, args, dir == DIR_PULL)) != SX_OK) return rc;
+        const uint32_t seq[3] = {dir, dir == DIR_PUSH ? DIR_PULL : DIR_PUSH, dir == DIR_PUSH ? DIR_CLUSTER : dir};
+        for (uint32_t d : seq)
+            if ((rc = enqueue(d)) != SX_OK) return rc;
         if ((rc = run.sync()) != SX_OK) return rc;
         if (g->ctx->h_ctl->done) break;
         dir = g->ctx->h_ctl->dir;

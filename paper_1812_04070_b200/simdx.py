@@ -47,7 +47,7 @@ class sx_opts(ctypes.Structure):
     _fields_ = [("overflow_threshold", _u32), ("sep_small", _u32), ("sep_large", _u32), ("sep_huge", _u32),
                 ("alpha", _f32), ("beta", _f32), ("force_filter", _i32), ("force_dir", _i32), ("fusion", _i32),
                 ("max_iters", _u32), ("trace", ctypes.POINTER(sx_trace_rec)), ("trace_cap", _u64),
-                ("local_chain", _u32)]
+                ("local_chain", _u32), ("cluster_enter", _u32)]
 
 
 class sx_stats(ctypes.Structure):
