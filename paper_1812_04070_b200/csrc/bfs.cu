@@ -21,8 +21,34 @@ struct BfsP {
     Sched s;
     uint32_t* level;
     uint32_t* visited;
+    const uint32_t* __restrict__ hub;  // per vertex: its in-neighbour of largest out-degree (INF: none)
     int sym;  // symmetric graph: in-degree == out-degree
 };
+
+// Hub-first probe table, built once per graph: hub(v) = the in-neighbour of
+// largest out-degree among v's first HUB_SCAN in-edges (ties: smallest id).
+// The bottom-up step tests it before touching v's row; a high-degree neighbour
+// is the one most likely to sit in a large frontier, so in the dense middle
+// levels a candidate usually costs one coalesced 4-B load instead of a row-pointer
+// pair plus a random row sector.  Probe order does not change the result (any
+// frontier in-neighbour proves level(v) = it + 1).
+constexpr uint32_t HUB_SCAN = 64;
+constexpr int HUB_ILP = 4;  // bottom-up: hub-probe rounds in flight per warp
+__global__ void __launch_bounds__(BLOCK) bfs_hub(DevGraph g, uint32_t* hub) {
+    const uint32_t lane = lane_id();
+    const uint64_t nwarp = (uint64_t)gridDim.x * WARPS;
+    for (uint64_t v = (uint64_t)blockIdx.x * WARPS + warp_id(); v < g.n; v += nwarp) {
+        const uint64_t beg = __ldg(g.irp + v), end = min(__ldg(g.irp + v + 1), beg + HUB_SCAN);
+        uint64_t best = 0;
+        for (uint64_t e = beg + lane; e < end; e += 32) {
+            const uint32_t u = __ldg(g.ici + e);
+            best = max(best, ((uint64_t)(__ldg(g.dout + u) + 1u) << 32) | (uint64_t)(~u));
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) best = max(best, __shfl_xor_sync(FULL, best, o));
+        if (lane == 0) hub[v] = best ? ~(uint32_t)best : INF;
+    }
+}
 
 __global__ void bfs_init(BfsP p, uint32_t src, uint32_t dir) {
     Ctl* c = p.s.ctl;
@@ -203,7 +229,7 @@ __global__ void __launch_bounds__(BLOCK, 4) bfs_pull(BfsP p) {
         const uint32_t* cur = p.s.bm[it % 3];
         uint32_t* nbm = p.s.bm[(it + 1) % 3];
         const uint32_t lvl = it + 1;
-        uint64_t mdeg = 0, edges = 0, cand_small = 0, cand_warp = 0;
+        uint64_t mdeg = 0, edges = 0, cand_small = 0, cand_warp = 0, rows = 0;
         uint32_t found_cnt = 0;
         // one probe round: up to PROBE in-edges [e, end) of this lane's candidate, loads in flight together
         auto probe = [&](uint64_t& e, uint64_t end, bool& found) {
@@ -244,34 +270,72 @@ __global__ void __launch_bounds__(BLOCK, 4) bfs_pull(BfsP p) {
                 for (uint32_t w = cand_l; w; w &= w - 1) s_c[pos++] = (uint32_t)(wl << 5) + (__ffs(w) - 1);
                 s_f[lane] = 0;
                 __syncwarp();
+                // phase 1 — hub-first probe, HUB_ILP rounds of 32 candidates in flight:
+                // one coalesced 4-B load per candidate, then one bitmap test.  Found
+                // candidates finish here; open ones are compacted in place at the
+                // front of the list (stable, so still in vertex order).
+                uint32_t nopen = 0;
+                for (uint32_t r0 = 0; r0 < total; r0 += 32 * HUB_ILP) {
+                    uint32_t v[HUB_ILP], h[HUB_ILP], d[HUB_ILP], wd[HUB_ILP];
+#pragma unroll
+                    for (int k = 0; k < HUB_ILP; ++k) {
+                        const uint32_t i = r0 + 32 * k + lane;
+                        v[k] = i < total ? s_c[i] : INF;
+                    }
+#pragma unroll
+                    for (int k = 0; k < HUB_ILP; ++k) {
+                        h[k] = v[k] != INF ? __ldg(p.hub + v[k]) : INF;
+                        d[k] = v[k] != INF ? __ldg(p.g.dout + v[k]) : 0u;
+                    }
+#pragma unroll
+                    for (int k = 0; k < HUB_ILP; ++k) wd[k] = h[k] != INF ? cur[h[k] >> 5] : 0u;
+                    __syncwarp();
+#pragma unroll
+                    for (int k = 0; k < HUB_ILP; ++k) {
+                        const bool f = h[k] != INF && ((wd[k] >> (h[k] & 31)) & 1u);
+                        edges += h[k] != INF;
+                        if (f) {
+                            p.level[v[k]] = lvl;
+                            mdeg += d[k];
+                            atomicOr(s_f + ((v[k] >> 5) - w0), 1u << (v[k] & 31));
+                        }
+                        const bool open = v[k] != INF && !f;
+                        const uint32_t bal = __ballot_sync(FULL, open);
+                        if (open) s_c[nopen + __popc(bal & lanemask_lt())] = v[k];
+                        nopen += __popc(bal);
+                    }
+                    __syncwarp();
+                }
+                // phase 2 — the open candidates walk their in-edge rows
                 uint32_t v_n = 0;
                 uint64_t beg_n = 0, end_n = 0;
-                if (lane < total) {
+                if (lane < nopen) {
                     v_n = s_c[lane];
                     beg_n = __ldg(p.g.irp + v_n);
                     end_n = __ldg(p.g.irp + v_n + 1);
                 }
-                for (uint32_t r = 0; r < total; r += 32) {
-                    const bool mine = r + lane < total;
+                for (uint32_t r = 0; r < nopen; r += 32) {
+                    const bool open = r + lane < nopen;
                     const uint32_t v = v_n;
                     const uint64_t beg = beg_n, end = end_n;
                     bool found = false;
                     uint64_t e = beg;
-                    if (mine) probe(e, end, found);  // first round for every candidate
+                    rows += open;
+                    if (open) probe(e, end, found);  // first row round
                     beg_n = end_n = 0;
-                    if (r + 32 + lane < total) {
+                    if (r + 32 + lane < nopen) {
                         v_n = s_c[r + 32 + lane];
                         beg_n = __ldg(p.g.irp + v_n);
                         end_n = __ldg(p.g.irp + v_n + 1);
                     }
                     // thread granularity: small candidates continue on their lane
-                    const bool small = mine && (end - beg) < p.s.sep_small;
+                    const bool small = open && (end - beg) < p.s.sep_small;
                     if (small) {
                         ++cand_small;
                         while (!found && e < end) probe(e, end, found);
                     }
                     // warp granularity: medium / large candidates still open, 32 edges per step
-                    uint32_t todo = __ballot_sync(FULL, mine && !small && !found && e < end);
+                    uint32_t todo = __ballot_sync(FULL, open && !small && !found && e < end);
                     while (todo) {
                         const int l = __ffs(todo) - 1;
                         todo &= todo - 1;
@@ -322,7 +386,7 @@ __global__ void __launch_bounds__(BLOCK, 4) bfs_pull(BfsP p) {
                 if (v4[3]) atomicAdd(&sl.cnt[1], (unsigned int)(v4[3] / 32));
             }
         }
-        st.entries += cand_small + cand_warp / 32;
+        st.entries += rows;
         st.scanned += (lead() ? nw * 32 : 0);
         if (!grid_sync(c)) return;
         LineSum ls;
@@ -360,12 +424,12 @@ using namespace sx;
 // Push: per list entry 4 B (list) + 16 B (row_ptr pair); per examined edge 4 B
 // (col); per reached vertex 4 B (level write); per iteration one frontier-bitmap
 // clear (n/8); ballot scans n/8 per scanned vertex / 8.
-// Pull (tile scan): per candidate 16 B (row_ptr pair); per examined edge 4 B;
-// per reached vertex 4 B; per iteration visited + in-degree>0 + frontier bitmaps
-// and one bitmap clear (4 n/8).
+// Pull (tile scan): per row visit 16 B (row_ptr pair); per examined edge 4 B (the
+// hub probe counts as one); per reached vertex 8 B (level write + out-degree);
+// per iteration visited + in-degree>0 + frontier bitmaps and one bitmap clear (4 n/8).
 static double bfs_bytes(const sx_graph g, const sxh::Counters& c) {
     const double n = (double)g->n;
-    if (c.pull > 0) return 16.0 * c.entries + 4.0 * c.edges + 4.0 * c.reached + c.pull * 4.0 * n / 8.0;
+    if (c.pull > 0) return 16.0 * c.entries + 4.0 * c.edges + 8.0 * c.reached + c.pull * 4.0 * n / 8.0;
     return 20.0 * c.entries + 4.0 * c.edges + 4.0 * c.reached + c.iters * n / 8.0 + c.scanned / 8.0;
 }
 
@@ -380,13 +444,19 @@ extern "C" sx_status sx_bfs(sx_graph g, uint32_t src, const sx_opts* opts, uint3
         return sxh::fail(SX_E_NO_REVERSE, "sx_bfs: pull needs in-neighbour rows (CSC); use force_dir=1 (push)");
     cudaStream_t s = g->ctx->stream;
     BfsP p;
-    if ((rc = run.begin()) != SX_OK) return rc;
     p.g = sxh::dev_graph(g);
+    if (!g->hub && g->has_rev) {  // first BFS on this graph: build the hub-first probe table
+        SX_CU(cudaMalloc(&g->hub, g->n * 4 + 16));
+        bfs_hub<<<g->ctx->prop.multiProcessorCount * 8, BLOCK, 0, s>>>(p.g, g->hub);
+        SX_CU(cudaGetLastError());
+    }
+    if ((rc = run.begin()) != SX_OK) return rc;
     p.s = sxh::make_sched(g, run.o);
     // write levels straight into a device output buffer (no copy-out)
     const bool dev_out = sxh::is_device_ptr(level_out);
     p.level = dev_out ? level_out : g->st[0];
     p.visited = g->aux_bm;
+    p.hub = g->hub;
     p.sym = !g->directed;
     SX_CU(cudaMemsetAsync(p.level, 0xFF, g->n * 4, s));
     SX_CU(cudaMemsetAsync(p.visited, 0, g->nwords * 4, s));

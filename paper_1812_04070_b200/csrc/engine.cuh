@@ -47,6 +47,7 @@ constexpr int BAR_GROUPS = 32;     // two-level barrier: <= 32 groups of CTAs
 
 enum : uint32_t { DIR_PUSH = 0, DIR_PULL = 1, DIR_CLUSTER = 2 };
 constexpr int CL_CTAS = 16;      // CTAs of the small-frontier cluster kernel (non-portable size 16)
+constexpr uint32_t CL_BIG = 64;  // cluster mode: out-degree above which a task's edges are split cluster-wide
 constexpr int CL_BLOCK = 1024;   // threads per CTA of the cluster kernel
 enum : uint32_t { ERR_NONE = 0, ERR_BARRIER = 7 };
 
@@ -92,6 +93,7 @@ struct Ctl {
     struct alignas(128) ClusterLine {
         unsigned int cnt[3];
         unsigned int minv;
+        unsigned int nbig[3];  // tasks of degree > CL_BIG deferred to the cluster-wide edge loop
     } cl;
     // --- run statistics per direction of the launch (0 push, 1 pull), one atomic per CTA per launch
     struct alignas(128) StatBlock {

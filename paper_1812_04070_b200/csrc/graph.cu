@@ -216,6 +216,7 @@ void sx_graph_free(sx_graph g) {
     cudaFree(g->dstate);
     cudaFree(g->loff);
     cudaFree(g->scratch64);
+    cudaFree(g->hub);
     delete g;
 }
 

@@ -49,6 +49,7 @@ struct sx_graph_s {
     double* dstate = nullptr;     // 2n doubles, BP beliefs (lazy)
     uint64_t* loff = nullptr;     // n+1 prefix sums, pull-all big-list stream (lazy)
     uint64_t* scratch64 = nullptr; // MAX_GRID u64 scan scratch (lazy)
+    uint32_t* hub = nullptr;      // n entries, BFS hub-first probe table (lazy)
 };
 
 namespace sxh {

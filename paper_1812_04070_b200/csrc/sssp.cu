@@ -540,6 +540,7 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
     // entry: zero the counters and the stale bitmap, list the frontier bitmap
     if (lead0) {
         cl->cnt[0] = cl->cnt[1] = cl->cnt[2] = 0;
+        cl->nbig[0] = cl->nbig[1] = cl->nbig[2] = 0;
         cl->minv = INF;
     }
     for (uint64_t wi = tid; wi < p.s.nwords; wi += T) p.s.bm[(it + 2) % 3][wi] = 0;
@@ -555,9 +556,41 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
         }
     }
     cluster_barrier();
+    const uint64_t lcap = (uint64_t)NCLS * p.s.cstride;  // entries per list; deferred big tasks fill it from the top
+    // relax edges [e0, e1) of v, 8 in flight per step: the chain is
+    // ids/weights -> atomicMin -> claim (atomicOr) -> append
+    auto relax = [&](uint32_t dv, uint64_t e0, uint64_t e1, uint64_t step, uint32_t* nbm, uint32_t* NL,
+                     unsigned int* ncnt) {
+        for (uint64_t e = e0; e < e1; e += 8 * step) {
+            uint32_t u[8], nd[8], old[8];
+            bool ok[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint64_t ek = e + k * step;
+                ok[k] = ek < e1;
+                u[k] = ok[k] ? __ldg(p.g.ci + ek) : 0u;
+                nd[k] = dv + (ok[k] ? (p.g.w8 ? (uint32_t)__ldg(p.g.w8 + ek) : __ldg(p.g.w32 + ek)) : 0u);
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) old[k] = ok[k] ? atomicMin(p.dist + u[k], nd[k]) : 0u;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                edges += ok[k];
+                if (!(ok[k] && nd[k] < old[k])) continue;
+                if ((uint64_t)nd[k] < hi) {
+                    if (bm_claim(nbm, u[k])) cl_append(NL, ncnt, u[k]);
+                } else {
+                    bm_set(p.far, u[k]);
+                }
+            }
+        }
+    };
     for (;;) {
         const uint32_t ncur = vload(&cl->cnt[it % 3]);
-        if (lead0) cl->cnt[(it + 2) % 3] = 0;
+        if (lead0) {
+            cl->cnt[(it + 2) % 3] = 0;
+            cl->nbig[(it + 1) % 3] = 0;
+        }
         const uint32_t* L = p.s.lists[it & 1];
         uint32_t* NL = p.s.lists[(it + 1) & 1];
         uint32_t* cur = p.s.bm[it % 3];
@@ -567,53 +600,22 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
             const uint32_t v = L[i];
             atomicAnd(cur + (v >> 5), ~(1u << (v & 31)));  // consumed: keep the bitmaps clean
             const uint64_t beg = __ldg(p.g.rp + v), end = __ldg(p.g.rp + v + 1);
-            const uint32_t dv = p.dist[v];
             ++entries;
-            // 4 edges per step, their loads and atomics in flight together
-            for (uint64_t e = beg; e < end;) {
-                const uint64_t a = e & ~3ull;
-                const uint4 q = __ldg(reinterpret_cast<const uint4*>(p.g.ci + a));
-                const uint32_t u[4] = {q.x, q.y, q.z, q.w};
-                uint32_t w[4];
-                if (p.g.w8) {
-                    const uint32_t ww = __ldg(reinterpret_cast<const uint32_t*>(p.g.w8 + a));
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) w[k] = (ww >> (8 * k)) & 0xFF;
-                } else {
-                    const uint4 ww = __ldg(reinterpret_cast<const uint4*>(p.g.w32 + a));
-                    w[0] = ww.x;
-                    w[1] = ww.y;
-                    w[2] = ww.z;
-                    w[3] = ww.w;
-                }
-                bool ok[4];
-                uint32_t nd[4], cu[4], old[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    ok[k] = a + k >= e && a + k < end;
-                    nd[k] = dv + w[k];
-                    cu[k] = ok[k] ? p.dist[u[k]] : 0u;
-                }
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    ok[k] = ok[k] && nd[k] < cu[k];
-                    old[k] = ok[k] ? atomicMin(p.dist + u[k], nd[k]) : 0u;
-                }
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    if (!(ok[k] && nd[k] < old[k])) continue;
-                    if ((uint64_t)nd[k] < hi) {
-                        if (!bm_test(nbm, u[k]) && bm_claim(nbm, u[k])) cl_append(NL, ncnt, u[k]);
-                    } else if (!bm_test(p.far, u[k])) {
-                        bm_set(p.far, u[k]);
-                    }
-                }
-                const uint64_t stop = min(end, a + 4);
-                edges += stop - e;
-                e = stop;
+            if (end - beg > CL_BIG) {
+                NL[lcap - 1 - atomicAdd(&cl->nbig[it % 3], 1u)] = v;
+                continue;
             }
+            relax(p.dist[v], beg, end, 1, nbm, NL, ncnt);
         }
         cluster_barrier();
+        const uint32_t nbig = vload(&cl->nbig[it % 3]);
+        if (nbig) {  // high-degree tasks: their edges spread over the whole cluster
+            for (uint32_t j = 0; j < nbig; ++j) {
+                const uint32_t v = NL[lcap - 1 - j];
+                relax(p.dist[v], __ldg(p.g.rp + v) + tid, __ldg(p.g.rp + v + 1), T, nbm, NL, ncnt);
+            }
+            cluster_barrier();
+        }
         uint32_t nnext = vload(ncnt);
         ++it;
         ++iters;

@@ -47,8 +47,8 @@ def main():
             us, ctas = simdx.sx_barrier_bench(ctx.h, it)
             print(f"== barrier: {us:.3f} us per grid barrier ({ctas} CTAs, {it} iterations)")
     if what in ("bfs24", "all"):
-        g = simgen.rmat(24, 16, 1)
-        G = ctx.upload(g)
+        g = simgen.rmat_gpu(24, 16, 1)
+        G = ctx.upload_device(g)
         out = torch.empty(g.n, dtype=torch.int32, device="cuda:0")
         for _ in range(3):
             G.bfs(0, out=out)
@@ -71,8 +71,8 @@ def main():
         show("c3 pagerank s22", st, tr, 8)
         G.free()
     if what in ("c4", "all"):
-        g = simgen.rmat(24, 16, 1)
-        G = ctx.upload(g)
+        g = simgen.rmat_gpu(24, 16, 1)
+        G = ctx.upload_device(g)
         _, st, tr = G.kcore(0, trace_cap=8192)
         show("c4 kcore s24 k=0", st, tr, 16)
         _, st, tr = G.kcore(16, trace_cap=8192)
