@@ -91,6 +91,11 @@ sx_status sx_ctx_info(sx_ctx ctx, sx_device_info* out);
  * out), SX_E_BARRIER (watchdog), SX_E_CUDA.
  */
 sx_status sx_barrier_bench(sx_ctx ctx, uint32_t iters, double* us_per_barrier, int* ctas);
+/* Diagnostic: cost of the small-frontier cluster mode's pieces on one 16-CTA
+   cluster.  mode 0: empty launch; 1: one cluster barrier (reps barriers in one
+   launch); 2: zero a bitmap of nwords words; 3: zero + compact an empty bitmap.
+   *us = microseconds per launch (modes 0, 2, 3) or per barrier (mode 1). */
+sx_status sx_cluster_bench(sx_ctx ctx, uint64_t nwords, uint32_t mode, uint32_t reps, double* us);
 
 /* ------------------------------------------------------------------ graphs */
 enum {
@@ -163,11 +168,12 @@ typedef struct {
                                     (chaotic relaxation, reading 12; results unchanged); 0 = strict BSP.
                                     Ignored by BFS (levels are BSP-exact). Default 0: measured on the 2048^2
                                     grid, chains cut iterations 1.6x but lengthened each one more. */
-    uint32_t cluster_enter;      /* SSSP push (B200 addition): when the next frontier has at most this many
-                                    vertices the iterations continue on ONE thread-block cluster of 8 CTAs
+    uint32_t cluster_enter;      /* BFS / SSSP push (B200 addition): when the next frontier has at most this
+                                    many vertices (BFS: and at most 128x this many out-edges) the iterations
+                                    continue on ONE thread-block cluster of 16 CTAs x 1024 threads
                                     synchronised by the hardware cluster barrier instead of the grid
-                                    barrier; back to the full grid above 8x this size.  0 = never.
-                                    Default 2048. */
+                                    barrier; back to the full grid above 8x this size (BFS: or 256x this
+                                    many out-edges).  Results unchanged.  0 = never.  Default 4096. */
 } sx_opts;
 
 typedef struct {

@@ -50,6 +50,12 @@ __global__ void __launch_bounds__(BLOCK) bfs_hub(DevGraph g, uint32_t* hub) {
     }
 }
 
+constexpr uint32_t CL_EDGES = 32;
+__device__ __forceinline__ bool cluster_ok(const Sched& s, uint64_t nf, uint64_t mf) {
+    return s.cluster_enter && s.fusion && s.force_filter != 2 && s.force_dir != 2 && nf > 0 &&
+           nf <= s.cluster_enter && mf <= (uint64_t)CL_EDGES * s.cluster_enter;
+}
+
 __global__ void bfs_init(BfsP p, uint32_t src, uint32_t dir) {
     Ctl* c = p.s.ctl;
     if (threadIdx.x < 32)
@@ -65,6 +71,7 @@ __global__ void bfs_init(BfsP p, uint32_t src, uint32_t dir) {
     p.s.lists[0][(uint64_t)k * p.s.cstride] = src;
     c->m_u = p.g.m - d;
     c->nf_prev = 1;
+    if (dir == DIR_PUSH && cluster_ok(p.s, 1, d)) dir = DIR_CLUSTER;  // low-degree source: start on one cluster
     c->dir = dir;
     c->lists_ready = dir == DIR_PUSH ? 1u : 0u;
     c->slotted = 0;
@@ -170,6 +177,11 @@ __global__ void __launch_bounds__(BLOCK, 4) bfs_push(BfsP p) {
         nf_prev = (uint32_t)nf;
         if (to_pull) {
             dir = DIR_PULL;
+            ready = 0;
+            break;
+        }
+        if (cluster_ok(p.s, nf, mf)) {
+            dir = DIR_CLUSTER;
             ready = 0;
             break;
         }
@@ -407,12 +419,138 @@ __global__ void __launch_bounds__(BLOCK, 4) bfs_pull(BfsP p) {
                              (p.s.force_dir == 0 && (double)nf < (double)n / p.s.beta && nf < nf_prev);
         nf_prev = (uint32_t)nf;
         if (to_push) {
-            dir = DIR_PUSH;
+            dir = cluster_ok(p.s, nf, mf) ? DIR_CLUSTER : DIR_PUSH;
             break;
         }
         if (!p.s.fusion) break;
     }
     bfs_exit(p, DIR_PULL, it, m_u, nf_prev, dir, done, 0u, 0u, cnt, st);
+}
+
+
+// ------------------------------------------------------------------ small-frontier cluster mode
+// Push on one 16-CTA cluster (engine.cuh: cluster_entry / cluster_leave) while
+// the frontier is small: the start from a low-degree source and the tail after
+// the bottom-up levels.  Vertices of out-degree > CL_BIG have their edges spread
+// over the whole cluster.  Back to the grid push once the next frontier exceeds
+// 8 x cluster_enter vertices or CL_EDGES x cluster_enter out-edges.
+__global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) bfs_cluster(BfsP p) {
+    Ctl* c = p.s.ctl;
+    if (vload(&c->done) || vload(&c->dir) != DIR_CLUSTER) return;
+    constexpr uint32_t T = CL_CTAS * CL_BLOCK;
+    const uint32_t tid = cluster_rank() * CL_BLOCK + threadIdx.x;
+    const bool lead0 = tid == 0;
+    uint32_t it = vload(&c->iter);
+    uint64_t m_u = vload(&c->m_u);
+    Ctl::ClusterLine* cl = &c->cl;
+    uint64_t edges = 0, entries = 0, reached = 0;
+    uint32_t iters = 0, done = 0, dir = DIR_CLUSTER, nnext = 0;
+    cluster_entry(p.s, it, tid, T);
+    const uint64_t lcap = (uint64_t)NCLS * p.s.cstride;  // deferred big tasks fill the next list from the top
+    for (;;) {
+        const uint32_t ncur = vload(&cl->cnt[it % 3]);
+        if (lead0) {
+            cl->cnt[(it + 2) % 3] = 0;
+            cl->nbig[(it + 1) % 3] = 0;
+            cl->mf[(it + 1) % 3] = 0;
+        }
+        const uint32_t* L = p.s.lists[it & 1];
+        uint32_t* NL = p.s.lists[(it + 1) & 1];
+        uint32_t* cur = p.s.bm[it % 3];
+        uint32_t* nbm = p.s.bm[(it + 1) % 3];
+        unsigned int* ncnt = &cl->cnt[(it + 1) % 3];
+        const uint32_t lvl = it + 1;
+        uint64_t mdeg = 0;
+        // visit edges [e0, e1) with stride `step`, 8 in flight: ids -> visited words -> claims
+        auto visit = [&](uint64_t e0, uint64_t e1, uint64_t step) {
+            for (uint64_t e = e0; e < e1; e += 8 * step) {
+                uint32_t u[8], vw[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) u[k] = e + k * step < e1 ? __ldg(p.g.ci + e + k * step) : INF;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) vw[k] = u[k] != INF ? p.visited[u[k] >> 5] : FULL;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    edges += u[k] != INF;
+                    if ((vw[k] >> (u[k] & 31)) & 1u) continue;
+                    if (!bm_claim(p.visited, u[k])) continue;
+                    p.level[u[k]] = lvl;
+                    bm_set(nbm, u[k]);
+                    mdeg += __ldg(p.g.dout + u[k]);
+                    ++reached;
+                    cl_append(NL, ncnt, u[k]);
+                }
+            }
+        };
+        for (uint32_t i = tid; i < ncur; i += T) {
+            const uint32_t v = L[i];
+            atomicAnd(cur + (v >> 5), ~(1u << (v & 31)));  // consumed: keep the bitmaps clean
+            const uint64_t beg = __ldg(p.g.rp + v), end = __ldg(p.g.rp + v + 1);
+            ++entries;
+            if (end - beg > CL_BIG) {
+                NL[lcap - 1 - atomicAdd(&cl->nbig[it % 3], 1u)] = v;
+                continue;
+            }
+            visit(beg, end, 1);
+        }
+        cluster_barrier();
+        const uint32_t nbig = vload(&cl->nbig[it % 3]);
+        if (nbig) {  // high-degree tasks: their edges spread over the whole cluster
+            for (uint32_t j = 0; j < nbig; ++j) {
+                const uint32_t v = NL[lcap - 1 - j];
+                visit(__ldg(p.g.rp + v) + tid, __ldg(p.g.rp + v + 1), T);
+            }
+        }
+        mdeg = warp_sum(mdeg);
+        if (lane_id() == 0 && mdeg) atomicAdd(&cl->mf[(it + 1) % 3], (unsigned long long)mdeg);
+        cluster_barrier();
+        nnext = vload(ncnt);
+        const uint64_t mf = vload(&cl->mf[(it + 1) % 3]);
+        m_u -= mf;
+        ++it;
+        ++iters;
+        if (lead0 && p.s.trace) {
+            const uint32_t i = c->ntrace++;
+            if (i < p.s.trace_cap) {
+                TraceRec r;
+                r.iter = it;
+                r.dir = DIR_CLUSTER;
+                r.filter = 0;
+                r.launch = c->launch;
+                r.n_active[0] = nnext;
+                r.n_active[1] = r.n_active[2] = r.n_active[3] = 0;
+                r.n_frontier = nnext;
+                r.m_active = mf;
+                r.aux = m_u;
+                r.t_ns = globaltimer();
+                p.s.trace[i] = r;
+            }
+        }
+        if (nnext == 0 || (p.s.max_iters && it >= p.s.max_iters)) {
+            done = 1;
+            break;
+        }
+        if (nnext > 8u * p.s.cluster_enter || mf > (uint64_t)CL_EDGES * 2u * p.s.cluster_enter) {
+            dir = DIR_PUSH;  // too big for one cluster: back to the grid
+            break;
+        }
+    }
+    const uint64_t e = warp_sum(edges), en = warp_sum(entries), rc = warp_sum(reached);
+    if (lane_id() == 0) {
+        if (e) atomicAdd(&c->st[0].edges, (unsigned long long)e);
+        if (en) atomicAdd(&c->st[0].entries, (unsigned long long)en);
+        if (rc) atomicAdd(&c->st[0].reached, (unsigned long long)rc);
+    }
+    cluster_barrier();
+    if (lead0) {
+        c->st[0].iters += iters;
+        c->iter = it;
+        c->m_u = m_u;
+        c->done = done;
+        c->dir = dir;
+        c->nf_prev = nnext;
+        cluster_leave(c);
+    }
 }
 
 }  // namespace sx
@@ -469,13 +607,27 @@ extern "C" sx_status sx_bfs(sx_graph g, uint32_t src, const sx_opts* opts, uint3
     // -> push; the three persistent launches are enqueued back to back
     // without a host round trip — a launch whose direction does not match the
     // device-side state exits at once — and the host syncs once per sequence.
-    uint32_t dir = dir0;
-    for (;;) {
-        const void* first = dir == DIR_PULL ? (const void*)bfs_pull : (const void*)bfs_push;
-        const void* second = dir == DIR_PULL ? (const void*)bfs_push : (const void*)bfs_pull;
-        if ((rc = run.launch(first, args, dir == DIR_PULL)) != SX_OK) return rc;
-        if ((rc = run.launch(second, args, dir != DIR_PULL)) != SX_OK) return rc;
-        if ((rc = run.launch(first, args, dir == DIR_PULL)) != SX_OK) return rc;
+    // likely successor of each phase: push -> pull -> cluster tail (-> push)
+    const bool cl_on = run.o.cluster_enter && run.o.fusion && run.o.force_filter != 2 && run.o.force_dir != 2;
+    auto next = [&](uint32_t d) -> uint32_t {
+        if (d == DIR_PUSH) return DIR_PULL;
+        if (d == DIR_PULL) return cl_on ? DIR_CLUSTER : DIR_PUSH;
+        return DIR_PUSH;
+    };
+    auto enqueue = [&](uint32_t d) -> sx_status {
+        if (d == DIR_CLUSTER) return run.launch_plain((const void*)bfs_cluster, args, CL_CTAS, CL_BLOCK, false);
+        return run.launch(d == DIR_PULL ? (const void*)bfs_pull : (const void*)bfs_push, args, d == DIR_PULL);
+    };
+    g->ctx->h_ctl->done = 0;
+    // the device picks cluster mode at init for a low-degree source; the host
+    // learns the direction only at a sync, so the first sequence starts with it
+    uint32_t dir = dir0 == DIR_PUSH && cl_on ? DIR_CLUSTER : dir0;
+    for (bool first = true;; first = false) {
+        // first sequence from a cluster start: cluster, push, pull, cluster (covers
+        // both a low- and a high-degree source); later ones three phases deep
+        const int len = first && dir == DIR_CLUSTER ? 4 : 3;
+        for (int i = 0, d = (int)dir; i < len; ++i, d = (int)next((uint32_t)d))
+            if ((rc = enqueue((uint32_t)d)) != SX_OK) return rc;
         if ((rc = run.sync()) != SX_OK) return rc;
         if (g->ctx->h_ctl->done) break;
         dir = g->ctx->h_ctl->dir;

@@ -310,7 +310,7 @@ void sx_opts_default(sx_opts* o) {
     o->trace = nullptr;
     o->trace_cap = 0;
     o->local_chain = 0;
-    o->cluster_enter = 2048;
+    o->cluster_enter = 4096;
 }
 
 sx_status sx_ctx_create(int device, void* cuda_stream, sx_ctx* out) {

@@ -58,3 +58,55 @@ extern "C" sx_status sx_barrier_bench(sx_ctx c, uint32_t iters, double* us_per_b
     *us_per_barrier = (double)ms * 1e3 / iters;
     return SX_OK;
 }
+
+// ---------------------------------------------------------------- cluster-mode micro-benchmark
+namespace sx {
+__global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1)
+    cluster_loop(Ctl* c, uint32_t* a, uint32_t* b, uint64_t nwords, uint32_t mode, uint32_t iters) {
+    constexpr uint32_t T = CL_CTAS * CL_BLOCK;
+    const uint32_t tid = cluster_rank() * CL_BLOCK + threadIdx.x;
+    if (mode == 1) {
+        for (uint32_t i = 0; i < iters; ++i) cluster_barrier();
+        return;
+    }
+    if (mode >= 2) {
+        uint4* z = reinterpret_cast<uint4*>(a);
+        for (uint64_t q = tid; q < nwords / 4; q += T) z[q] = make_uint4(0u, 0u, 0u, 0u);
+        cluster_barrier();
+    }
+    if (mode >= 3) {
+        cluster_compact(b, nwords, tid, T, &c->cl.cnt[0], a, [](uint64_t, uint32_t w) { return w; });
+        cluster_barrier();
+    }
+}
+}  // namespace sx
+
+extern "C" sx_status sx_cluster_bench(sx_ctx c, uint64_t nwords, uint32_t mode, uint32_t reps, double* us) {
+    if (!us || reps == 0 || mode > 3) return sxh::fail(SX_E_INVALID, "sx_cluster_bench: bad argument");
+    sx_status rc = sxh::check_ctx(c);
+    if (rc != SX_OK) return rc;
+    nwords = (nwords + TILE_WORDS - 1) / TILE_WORDS * TILE_WORDS;
+    Ctl* d = nullptr;
+    uint32_t *a = nullptr, *b = nullptr;
+    SX_CU(cudaMalloc(&d, sizeof(Ctl)));
+    SX_CU(cudaMalloc(&a, nwords * 4 + 16));
+    SX_CU(cudaMalloc(&b, nwords * 4 + 16));
+    SX_CU(cudaMemsetAsync(d, 0, sizeof(Ctl), c->stream));
+    SX_CU(cudaMemsetAsync(b, 0, nwords * 4, c->stream));
+    SX_CU(cudaFuncSetAttribute((const void*)cluster_loop, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    const uint32_t inner = mode == 1 ? reps : 1;
+    const uint32_t outer = mode == 1 ? 1 : reps;
+    cluster_loop<<<CL_CTAS, CL_BLOCK, 0, c->stream>>>(d, a, b, nwords, mode, 1);  // warm-up
+    SX_CU(cudaEventRecord(c->ev0, c->stream));
+    for (uint32_t i = 0; i < outer; ++i) cluster_loop<<<CL_CTAS, CL_BLOCK, 0, c->stream>>>(d, a, b, nwords, mode, inner);
+    SX_CU(cudaEventRecord(c->ev1, c->stream));
+    cudaError_t e = cudaEventSynchronize(c->ev1);
+    cudaFree(d);
+    cudaFree(a);
+    cudaFree(b);
+    if (e != cudaSuccess) return sxh::cuda_fail(e, "cluster_loop");
+    float ms = 0;
+    SX_CU(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    *us = (double)ms * 1e3 / reps;
+    return SX_OK;
+}

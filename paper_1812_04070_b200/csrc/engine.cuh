@@ -94,6 +94,7 @@ struct Ctl {
         unsigned int cnt[3];
         unsigned int minv;
         unsigned int nbig[3];  // tasks of degree > CL_BIG deferred to the cluster-wide edge loop
+        unsigned long long mf[3];  // BFS: sum of out-degrees of the next frontier
     } cl;
     // --- run statistics per direction of the launch (0 push, 1 pull), one atomic per CTA per launch
     struct alignas(128) StatBlock {
@@ -826,5 +827,171 @@ __device__ __forceinline__ void trace_put(const Sched& s, uint32_t iter, uint32_
 }
 
 __device__ __forceinline__ uint32_t sum4(const uint32_t (&c)[NCLS]) { return c[0] + c[1] + c[2] + c[3]; }
+
+// ---------------------------------------------------------------- small-frontier cluster mode
+// When the frontier is small the grid barrier (~3 us for 600+ CTAs) dominates an
+// iteration.  The push then continues on ONE thread-block cluster of CL_CTAS x
+// CL_BLOCK threads whose barrier is the hardware cluster barrier: same ACC step,
+// online filter into one list, no grid barrier.  Frontier hand-over with the grid
+// kernels is the bitmap bm[it % 3]; consumers clear the bits they consume, so
+// bm[(it+1)%3] and bm[(it+2)%3] stay zero as the grid kernels expect.
+__device__ __forceinline__ void cluster_barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// warp-aggregated append to a list with a global counter
+__device__ __forceinline__ void cl_append(uint32_t* list, unsigned int* cnt, uint32_t u) {
+    const uint32_t m = __activemask();
+    const int leader = __ffs(m) - 1;
+    uint32_t base = 0;
+    if ((int)lane_id() == leader) base = atomicAdd(cnt, (uint32_t)__popc(m));
+    base = __shfl_sync(m, base, leader);
+    list[base + __popc(m & lanemask_lt())] = u;
+}
+// Visit the nonzero words of a bitmap (nwords a multiple of 4) with 128-bit
+// loads, 4 in flight per thread: f(word index, word).
+template <class F>
+__device__ __forceinline__ void cluster_words(const uint32_t* bm, uint64_t nwords, uint32_t tid, uint32_t T, F&& f) {
+    const uint4* q = reinterpret_cast<const uint4*>(bm);
+    const uint64_t nq = nwords / 4;
+    for (uint64_t q0 = tid; q0 < nq; q0 += 4ull * T) {
+        uint4 w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) w[k] = q0 + k * T < nq ? q[q0 + k * T] : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint64_t b = (q0 + k * T) * 4;
+            if (w[k].x) f(b, w[k].x);
+            if (w[k].y) f(b + 1, w[k].y);
+            if (w[k].z) f(b + 2, w[k].z);
+            if (w[k].w) f(b + 3, w[k].w);
+        }
+    }
+}
+
+// Exclusive scan over the 1024 threads of a cluster CTA; *total = CTA sum.
+__device__ __forceinline__ uint32_t cta_scan_1024(uint32_t v, uint32_t* total) {
+    __shared__ uint32_t s_ws[32];
+    __shared__ uint32_t s_tot;
+    const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, incl, o);
+        if ((int)lane >= o) incl += y;
+    }
+    if (lane == 31) s_ws[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        const uint32_t x = s_ws[lane];
+        uint32_t sx = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, sx, o);
+            if ((int)lane >= o) sx += y;
+        }
+        s_ws[lane] = sx - x;
+        if (lane == 31) s_tot = sx;
+    }
+    __syncthreads();
+    const uint32_t excl = s_ws[wid] + incl - v;
+    *total = s_tot;
+    __syncthreads();  // s_ws / s_tot reuse by the next call
+    return excl;
+}
+// Cluster-wide compaction of a bitmap into a list: the bits mask(word index,
+// word) keeps (words read with 128-bit loads, 16 per thread per round) are
+// appended to L at positions claimed with ONE atomicAdd per CTA per round.
+// Every thread of the cluster must call it (CTA barriers inside).
+template <class M>
+__device__ __forceinline__ void cluster_compact(const uint32_t* bm, uint64_t nwords, uint32_t tid, uint32_t T,
+                                                unsigned int* cnt, uint32_t* L, M&& mask) {
+    __shared__ uint32_t s_base;
+    const uint4* q = reinterpret_cast<const uint4*>(bm);
+    const uint64_t nq = nwords / 4;
+    const uint64_t rounds = (nq + 4ull * T - 1) / (4ull * T);
+    for (uint64_t r = 0; r < rounds; ++r) {
+        const uint64_t q0 = r * 4ull * T + tid;
+        uint32_t w[16];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint4 x = q0 + k * T < nq ? q[q0 + k * T] : make_uint4(0u, 0u, 0u, 0u);
+            w[4 * k] = x.x;
+            w[4 * k + 1] = x.y;
+            w[4 * k + 2] = x.z;
+            w[4 * k + 3] = x.w;
+        }
+        uint32_t pc = 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            if (w[j]) w[j] = mask((q0 + (j >> 2) * T) * 4 + (j & 3), w[j]);
+            pc += __popc(w[j]);
+        }
+        uint32_t tot;
+        uint32_t pos = cta_scan_1024(pc, &tot);
+        if (tot == 0) continue;  // CTA-uniform
+        if (threadIdx.x == 0) s_base = atomicAdd(cnt, tot);
+        __syncthreads();
+        pos += s_base;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            for (uint32_t x = w[j]; x; x &= x - 1)
+                L[pos++] = (uint32_t)((((q0 + (j >> 2) * T) * 4 + (j & 3)) << 5) + (__ffs(x) - 1));
+        __syncthreads();  // s_base reuse
+    }
+}
+// Per-vertex values of the set bits of word wi (32 consecutive vertices = one
+// 128-B line): the 4-vertex quads holding set bits are loaded together.
+template <class F>
+__device__ __forceinline__ void word_values(const uint32_t* a, uint64_t wi, uint32_t x, F&& f) {
+    const uint4* q = reinterpret_cast<const uint4*>(a + (wi << 5));
+    uint4 v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = (x >> (4 * j)) & 0xFu ? q[j] : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t nib = (x >> (4 * j)) & 0xFu;
+        if (nib & 1u) f(4 * j, v[j].x);
+        if (nib & 2u) f(4 * j + 1, v[j].y);
+        if (nib & 4u) f(4 * j + 2, v[j].z);
+        if (nib & 8u) f(4 * j + 3, v[j].w);
+    }
+}
+
+// Entry: zero the cluster counters and the stale bitmap bm[(it+2)%3], list the
+// frontier bitmap bm[it % 3] into lists[it & 1] (count in cl.cnt[it % 3]).
+__device__ __forceinline__ void cluster_entry(const Sched& s, uint32_t it, uint32_t tid, uint32_t T) {
+    Ctl::ClusterLine* cl = &s.ctl->cl;
+    if (tid == 0) {
+        for (int i = 0; i < 3; ++i) {
+            cl->cnt[i] = 0;
+            cl->nbig[i] = 0;
+            cl->mf[i] = 0;
+        }
+        cl->minv = INF;
+    }
+    uint4* z = reinterpret_cast<uint4*>(s.bm[(it + 2) % 3]);
+    const uint64_t nq = s.nwords / 4;
+    for (uint64_t q = tid; q < nq; q += T) z[q] = make_uint4(0u, 0u, 0u, 0u);
+    cluster_barrier();
+    cluster_compact(s.bm[it % 3], s.nwords, tid, T, &cl->cnt[it % 3], s.lists[it & 1],
+                    [](uint64_t, uint32_t w) { return w; });
+    cluster_barrier();
+}
+// Exit (one thread): the grid kernels rebuild their lists from bm[it % 3] and
+// start from zeroed grid-barrier counters.
+__device__ __forceinline__ void cluster_leave(Ctl* c) {
+    c->lists_ready = 0;
+    c->slotted = 0;
+    for (int h = 0; h < 2; ++h) {
+        for (int i = 0; i < BAR_GROUPS; ++i) c->bar_grp[h][i].count = 0;
+        c->bar_top[h].count = 0;
+    }
+    c->launch += 1;
+}
 
 }  // namespace sx

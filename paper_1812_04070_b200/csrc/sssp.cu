@@ -498,64 +498,21 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_pull(SsspP p) {
 }
 
 // ------------------------------------------------------------------ small-frontier cluster mode
-// When the frontier is small the grid barrier (~3 us for 600+ CTAs) dominates an
-// iteration.  The push then continues on ONE thread-block cluster of 8 CTAs x
-// 1024 threads whose barrier is the hardware cluster barrier
-// (barrier.cluster.arrive.release / wait.acquire): same ACC step, online filter
-// into one list, same delta-stepping, no grid barrier.  It hands the frontier
-// back to the grid kernels (as the bitmap bm[it % 3]) once it exceeds
-// 8 x cluster_enter vertices.  Bitmap invariant kept for the grid kernels:
-// consumers clear their frontier bits, so bm[(it+1)%3] and bm[(it+2)%3] are zero.
-__device__ __forceinline__ void cluster_barrier() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-// warp-aggregated append to a list with a global counter
-__device__ __forceinline__ void cl_append(uint32_t* list, unsigned int* cnt, uint32_t u) {
-    const uint32_t m = __activemask();
-    const int leader = __ffs(m) - 1;
-    uint32_t base = 0;
-    if ((int)lane_id() == leader) base = atomicAdd(cnt, (uint32_t)__popc(m));
-    base = __shfl_sync(m, base, leader);
-    list[base + __popc(m & lanemask_lt())] = u;
-}
-
+// (engine.cuh: cluster_entry / cluster_leave).  Delta-stepping continues inside
+// the cluster, bucket advances included; the frontier goes back to the grid
+// kernels once it exceeds 8 x cluster_enter vertices.
 __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) sssp_cluster(SsspP p) {
     Ctl* c = p.s.ctl;
     if (vload(&c->done) || vload(&c->dir) != DIR_CLUSTER) return;
     constexpr uint32_t T = CL_CTAS * CL_BLOCK;
     const uint32_t tid = cluster_rank() * CL_BLOCK + threadIdx.x;
     const bool lead0 = tid == 0;
-    const uint64_t n = p.g.n;
-    const uint64_t nw = (n + 31) >> 5;
     uint32_t it = vload(&c->iter);
     uint64_t hi = vload(&c->hi);
     Ctl::ClusterLine* cl = &c->cl;
     uint64_t edges = 0, entries = 0;
     uint32_t iters = 0, ballots = 0, done = 0, dir = DIR_CLUSTER;
-    // entry: zero the counters and the stale bitmap, list the frontier bitmap
-    if (lead0) {
-        cl->cnt[0] = cl->cnt[1] = cl->cnt[2] = 0;
-        cl->nbig[0] = cl->nbig[1] = cl->nbig[2] = 0;
-        cl->minv = INF;
-    }
-    for (uint64_t wi = tid; wi < p.s.nwords; wi += T) p.s.bm[(it + 2) % 3][wi] = 0;
-    cluster_barrier();
-    {
-        uint32_t* L = p.s.lists[it & 1];
-        for (uint64_t wi = tid; wi < nw; wi += T) {
-            const uint32_t w = p.s.bm[it % 3][wi];
-            if (!w) continue;
-            const uint32_t base = atomicAdd(&cl->cnt[it % 3], (uint32_t)__popc(w));
-            uint32_t k = 0;
-            for (uint32_t x = w; x; x &= x - 1) L[base + k++] = (uint32_t)(wi << 5) + (__ffs(x) - 1);
-        }
-    }
-    cluster_barrier();
+    cluster_entry(p.s, it, tid, T);
     const uint64_t lcap = (uint64_t)NCLS * p.s.cstride;  // entries per list; deferred big tasks fill it from the top
     // relax edges [e0, e1) of v, 8 in flight per step: the chain is
     // ids/weights -> atomicMin -> claim (atomicOr) -> append
@@ -626,8 +583,9 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
             } else {
                 // bucket advance over the far pile
                 uint32_t mn = INF;
-                for (uint64_t wi = tid; wi < nw; wi += T)
-                    for (uint32_t x = p.far[wi]; x; x &= x - 1) mn = min(mn, p.dist[(wi << 5) + (__ffs(x) - 1)]);
+                cluster_words(p.far, p.s.nwords, tid, T, [&](uint64_t wi, uint32_t x) {
+                    word_values(p.dist, wi, x, [&](int, uint32_t d) { mn = min(mn, d); });
+                });
                 mn = warp_min(mn);
                 if (lane_id() == 0 && mn != INF) atomicMin(&cl->minv, mn);
                 cluster_barrier();
@@ -641,19 +599,17 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
                     uint32_t* L2 = p.s.lists[it & 1];
                     unsigned int* c2 = &cl->cnt[it % 3];
                     uint32_t* fbm = p.s.bm[it % 3];
-                    for (uint64_t wi = tid; wi < nw; wi += T) {
-                        const uint32_t f = p.far[wi];
+                    cluster_compact(p.far, p.s.nwords, tid, T, c2, L2, [&](uint64_t wi, uint32_t f) {
                         uint32_t mv = 0;
-                        for (uint32_t x = f; x; x &= x - 1) {
-                            const int b = __ffs(x) - 1;
-                            if ((uint64_t)p.dist[(wi << 5) + b] < hi) mv |= 1u << b;
-                        }
+                        word_values(p.dist, wi, f, [&](int b, uint32_t d) {
+                            if ((uint64_t)d < hi) mv |= 1u << b;
+                        });
                         if (mv) {
                             p.far[wi] = f & ~mv;  // single owner of the word
                             fbm[wi] |= mv;
-                            for (uint32_t x = mv; x; x &= x - 1) cl_append(L2, c2, (uint32_t)(wi << 5) + (__ffs(x) - 1));
                         }
-                    }
+                        return mv;
+                    });
                     cluster_barrier();
                     nnext = vload(c2);
                     ++ballots;
@@ -703,14 +659,8 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
         c->hi = hi;
         c->done = done;
         c->dir = dir;
-        c->lists_ready = 0;  // the grid kernels rebuild their lists from bm[it % 3]
-        c->slotted = 0;
         c->nf_prev = vload(&cl->cnt[it % 3]);
-        for (int h = 0; h < 2; ++h) {  // leave both grid-barrier halves zeroed
-            for (int i = 0; i < BAR_GROUPS; ++i) c->bar_grp[h][i].count = 0;
-            c->bar_top[h].count = 0;
-        }
-        c->launch += 1;
+        cluster_leave(c);
     }
 }
 

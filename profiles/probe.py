@@ -30,8 +30,8 @@ def show(name, st, tr, maxlines=40):
     for t in tr:
         dt = (t["t_ns"] - prev) / 1e3 if prev is not None else float("nan")
         prev = t["t_ns"]
-        lines.append(f"  it{t['iter']:5d} {'pull' if t['dir'] else 'push'} f{t['filter']} L{t['launch']} "
-                     f"|F'|={t['n_frontier']:9d} act={t['n_active']} aux={t['aux']} dt={dt:8.1f}us")
+        lines.append(f"  it{t['iter']:5d} {('push', 'pull', 'clus')[t['dir']]} f{t['filter']} L{t['launch']} "
+                     f"|F'|={t['n_frontier']:9d} act={t['n_active']} mf={t['m_active']} aux={t['aux']} dt={dt:8.1f}us")
     if len(lines) > maxlines:
         lines = lines[:maxlines // 2] + ["  ..."] + lines[-maxlines // 2:]
     print("\n".join(lines))

@@ -89,7 +89,8 @@ def test_fig1_reconstruction_sssp(ctx):
 # ---------------------------------------------------------------- BFS forced modes
 MODES = [dict(), dict(force_dir=1), dict(force_dir=2), dict(force_filter=1), dict(force_filter=2),
          dict(fusion=0), dict(overflow_threshold=1), dict(overflow_threshold=1 << 20),
-         dict(sep_small=4, sep_large=8, sep_huge=64), dict(force_dir=2, fusion=0)]
+         dict(sep_small=4, sep_large=8, sep_huge=64), dict(force_dir=2, fusion=0),
+         dict(cluster_enter=0), dict(cluster_enter=64), dict(cluster_enter=1 << 20)]
 
 
 @pytest.fixture(scope="module")
@@ -113,7 +114,33 @@ def test_bfs_modes_rmat(ctx, rmat14, mode):
 
 
 SK_MODES = MODES[:6] + [dict(force_dir=2, fusion=0), dict(local_chain=0), dict(local_chain=100000),
-                        dict(local_chain=3, force_filter=2)]
+                        dict(local_chain=3, force_filter=2), dict(cluster_enter=0), dict(cluster_enter=1 << 20)]
+
+
+@pytest.mark.parametrize("ce", [0, 16, 2048, 1 << 20])
+def test_cluster_mode_grid_and_star(ctx, ce):
+    # small-frontier cluster mode: a grid (long diameter, frontiers in and out of
+    # the cluster range) and a star (one task of degree > CL_BIG split cluster-wide)
+    g = simgen.grid(96, 80, 5, 1, 255)
+    star = simgen.from_edges(3000, [(0, i) for i in range(1, 3000)] + [(i, i + 1) for i in range(1, 2999)],
+                             [7] * 2999 + [1] * 2998)
+    for gr, srcs in ((g, (0, 4000)), (star, (0, 5))):
+        G = up(ctx, gr)
+        try:
+            for src in srcs:
+                lv, st, tr = G.bfs(src, cluster_enter=ce, trace_cap=20000)
+                assert np.array_equal(lv, oracle.bfs(gr, src)), (ce, src)
+                hist = oracle.level_histogram(lv)
+                assert [t["n_frontier"] for t in tr][:len(hist) - 1] == list(hist[1:])
+                if ce == 0:
+                    assert all(t["dir"] != 2 for t in tr)
+                for delta in (0, 3, 600):
+                    d, _, tr = G.sssp(src, delta, cluster_enter=ce, trace_cap=20000)
+                    assert np.array_equal(d, oracle.sssp(gr, src)), (ce, src, delta)
+                    if ce == 0:
+                        assert all(t["dir"] != 2 for t in tr)
+        finally:
+            G.free()
 
 
 @pytest.mark.parametrize("mode", SK_MODES, ids=[str(m) for m in SK_MODES])
