@@ -33,7 +33,16 @@ struct BfsP {
 // pair plus a random row sector.  Probe order does not change the result (any
 // frontier in-neighbour proves level(v) = it + 1).
 constexpr uint32_t HUB_SCAN = 64;
-constexpr int HUB_ILP = 4;  // bottom-up: hub-probe rounds in flight per warp
+#ifndef SX_HUB_ILP
+#define SX_HUB_ILP 4
+#endif
+#ifndef SX_PROBE
+#define SX_PROBE 4
+#endif
+#ifndef SX_PULL_MINB
+#define SX_PULL_MINB 4
+#endif
+constexpr int HUB_ILP = SX_HUB_ILP;  // bottom-up: hub-probe rounds in flight per warp
 __global__ void __launch_bounds__(BLOCK) bfs_hub(DevGraph g, uint32_t* hub) {
     const uint32_t lane = lane_id();
     const uint64_t nwarp = (uint64_t)gridDim.x * WARPS;
@@ -56,14 +65,51 @@ __device__ __forceinline__ bool cluster_ok(const Sched& s, uint64_t nf, uint64_t
            nf <= s.cluster_enter && mf <= (uint64_t)CL_EDGES * s.cluster_enter;
 }
 
-__global__ void bfs_init(BfsP p, uint32_t src, uint32_t dir) {
+// Per-run state in one grid-stride pass: level = INF (0 at src), visited and
+// the three frontier bitmaps zero (src's bit set in visited and bm[0]); block 0
+// also seeds the control block and the first list.
+__global__ void __launch_bounds__(BLOCK) bfs_init(BfsP p, uint32_t src, uint32_t dir) {
+    const uint64_t n = p.g.n, T = gthreads(), tid = gtid();
+    if (((uintptr_t)p.level & 15u) == 0) {
+        uint4* L4 = reinterpret_cast<uint4*>(p.level);
+        for (uint64_t q = tid; q < n / 4; q += T) {
+            uint4 v = make_uint4(INF, INF, INF, INF);
+            if (q == src >> 2) {
+                const uint32_t k = src & 3u;
+                v.x = k == 0 ? 0u : INF;
+                v.y = k == 1 ? 0u : INF;
+                v.z = k == 2 ? 0u : INF;
+                v.w = k == 3 ? 0u : INF;
+            }
+            L4[q] = v;
+        }
+        for (uint64_t i = n / 4 * 4 + tid; i < n; i += T) p.level[i] = i == src ? 0u : INF;
+    } else {
+        for (uint64_t i = tid; i < n; i += T) p.level[i] = i == src ? 0u : INF;
+    }
+    uint32_t* bms[4] = {p.visited, p.s.bm[0], p.s.bm[1], p.s.bm[2]};
+    const uint64_t nq = p.s.nwords / 4;  // nwords is a multiple of TILE_WORDS
+    const uint64_t sq = src >> 7;        // the quad holding src's word
+    const uint32_t bit = 1u << (src & 31), sw = (src >> 5) & 3u;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        uint4* B4 = reinterpret_cast<uint4*>(bms[b]);
+        for (uint64_t q = tid; q < nq; q += T) {
+            uint4 v = make_uint4(0u, 0u, 0u, 0u);
+            if (q == sq && b < 2) {
+                v.x = sw == 0 ? bit : 0u;
+                v.y = sw == 1 ? bit : 0u;
+                v.z = sw == 2 ? bit : 0u;
+                v.w = sw == 3 ? bit : 0u;
+            }
+            B4[q] = v;
+        }
+    }
+    if (blockIdx.x != 0) return;
     Ctl* c = p.s.ctl;
     if (threadIdx.x < 32)
         for (int i = 0; i < 3; ++i) reset_line_warp(&c->line[i]);
     if (threadIdx.x != 0) return;
-    p.level[src] = 0;
-    p.visited[src >> 5] |= 1u << (src & 31);
-    p.s.bm[0][src >> 5] |= 1u << (src & 31);
     const uint32_t d = p.g.dout[src];
     const uint32_t k = cls_of(d, p.s);
     for (int i = 0; i < NCLS; ++i) c->cur_count[i] = 0;
@@ -215,9 +261,9 @@ __global__ void __launch_bounds__(BLOCK, 4) bfs_push(BfsP p) {
 // granularity).  All stop at the first frontier in-neighbour (voting early
 // exit).  Found bits are gathered per word in shared memory and written
 // once per chunk with plain stores: no global atomics on the data path.
-constexpr int PROBE = 4;
+constexpr int PROBE = SX_PROBE;
 
-__global__ void __launch_bounds__(BLOCK, 4) bfs_pull(BfsP p) {
+__global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) bfs_pull(BfsP p) {
     Ctl* c = p.s.ctl;
     if (vload(&c->done) || vload(&c->dir) != DIR_PULL) return;
     grid_begin(c);
@@ -596,11 +642,8 @@ extern "C" sx_status sx_bfs(sx_graph g, uint32_t src, const sx_opts* opts, uint3
     p.visited = g->aux_bm;
     p.hub = g->hub;
     p.sym = !g->directed;
-    SX_CU(cudaMemsetAsync(p.level, 0xFF, g->n * 4, s));
-    SX_CU(cudaMemsetAsync(p.visited, 0, g->nwords * 4, s));
-    for (int i = 0; i < 3; ++i) SX_CU(cudaMemsetAsync(p.s.bm[i], 0, g->nwords * 4, s));
     const uint32_t dir0 = run.o.force_dir == 2 ? DIR_PULL : DIR_PUSH;
-    bfs_init<<<1, 32, 0, s>>>(p, src, dir0);
+    bfs_init<<<g->ctx->prop.multiProcessorCount * 8, BLOCK, 0, s>>>(p, src, dir0);
     SX_CU(cudaGetLastError());
     void* args[] = {&p};
     // Selective fusion: the direction-optimising BFS runs push -> pull

@@ -1,5 +1,6 @@
 // capi.cu — contexts, graph upload/validation, launch plumbing and the common
 // run bookkeeping behind include/simdx.h.
+#include <cstddef>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -198,7 +199,12 @@ sx_status Run::launch_plain(const void* fn, void** args, int grid, int block, bo
 
 sx_status Run::sync() {
     sx_ctx c = g->ctx;
-    SX_CU(cudaMemcpyAsync(c->h_ctl, g->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->stream));
+    // end-of-run event and the host-visible tail of the control block (from
+    // `iter` on: run state, cluster line, statistics), one stream sync
+    SX_CU(cudaEventRecord(c->ev1, c->stream));
+    constexpr size_t off = offsetof(Ctl, iter);
+    SX_CU(cudaMemcpyAsync(reinterpret_cast<char*>(c->h_ctl) + off, reinterpret_cast<const char*>(g->ctl) + off,
+                          sizeof(Ctl) - off, cudaMemcpyDeviceToHost, c->stream));
     cudaError_t e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) {
         c->poisoned = true;
@@ -228,13 +234,11 @@ static Counters counters_of(const Ctl::StatBlock& b) {
 
 sx_status Run::end(BytesFn bytes) {
     sx_ctx c = g->ctx;
-    if (npending) {
+    if (npending || launches == 0) {
         sx_status rc = sync();
         if (rc != SX_OK) return rc;
     }
-    SX_CU(cudaEventRecord(c->ev1, c->stream));
-    SX_CU(cudaEventSynchronize(c->ev1));
-    float ms = 0;
+    float ms = 0;  // ev1 was recorded by the last sync()
     SX_CU(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
     const Ctl& h = *c->h_ctl;
     if (st) {

@@ -18,7 +18,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsimdx.so")
+LIB_PATH = os.environ.get("SIMDX_LIB") or os.path.join(_HERE, "libsimdx.so")  # SIMDX_LIB: variant builds (profiles/)
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build the CUDA extension first "
