@@ -148,25 +148,26 @@ __device__ __forceinline__ void bfs_exit(const BfsP& p, uint32_t kdir, uint32_t 
 // ------------------------------------------------------------------ push
 __global__ void __launch_bounds__(BLOCK, 4) bfs_push(BfsP p) {
     Ctl* c = p.s.ctl;
-    if (vload(&c->done) || vload(&c->dir) != DIR_PUSH) return;
-    grid_begin(c);
-    uint32_t it = vload(&c->iter);
-    uint64_t m_u = vload(&c->m_u);
-    uint32_t nf_prev = vload(&c->nf_prev);
+    const RunState& rs = run_state(c);
+    if (rs.done || rs.dir != DIR_PUSH) return;
+    grid_begin(rs.launch);
+    uint32_t it = rs.iter;
+    uint64_t m_u = rs.m_u;
+    uint32_t nf_prev = rs.nf_prev;
     uint32_t cnt[NCLS];
     Stats st;
     uint32_t dir = DIR_PUSH, done = 0, ready = 1, slotted = 0;
-    if (!vload(&c->lists_ready)) {
+    if (!rs.lists_ready) {
         // entering push from pull: the frontier exists only as a bitmap -> ballot filter
         if (!ballot_filter(BitmapWords{p.s.bm[it % 3]}, p.s, BallotOut{p.s.lists[it & 1], p.s.cstride, p.g.dout}, cnt))
             return;
         st.scanned += p.s.nwords * 32;
         if (!grid_sync(c)) return;
         view_contig(cnt);
-    } else if (vload(&c->slotted)) {
+    } else if (rs.slotted) {
         view_slots(&c->line[it % 3], p.s, cnt);
     } else {
-        for (int i = 0; i < NCLS; ++i) cnt[i] = vload(&c->cur_count[i]);
+        for (int i = 0; i < NCLS; ++i) cnt[i] = rs.cur_count[i];
         view_contig(cnt);
     }
     for (;;) {
@@ -179,16 +180,34 @@ __global__ void __launch_bounds__(BLOCK, 4) bfs_push(BfsP p) {
         uint64_t mdeg = 0, edges = 0, reached = 0;
         for_tasks(p.s.lists[it & 1], p.s, cnt, [&](uint32_t v, uint64_t rank, uint64_t size, uint32_t) {
             const uint64_t beg = __ldg(p.g.rp + v), end = __ldg(p.g.rp + v + 1);
-            for_edges(p.g.ci, beg, end, rank, size, [&](uint64_t, uint32_t u) {
-                ++edges;
-                if (bm_test(p.visited, u)) return;
-                if (!bm_claim(p.visited, u)) return;
-                p.level[u] = lvl;
-                bm_set(nbm, u);
-                const uint32_t du = __ldg(p.g.dout + u);
-                mdeg += du;
-                ++reached;
-                online_record(nx, nlists, p.s, u, cls_of(du, p.s));
+            // up to 4 edges per step: visited words, claims and the claimed
+            // vertices' degrees are each issued together
+            for_edges_b(p.g.ci, beg, end, rank, size, [&](const uint32_t (&u)[4], uint32_t k) {
+                edges += k;
+                uint32_t vw[4], du[4];
+                bool cl[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) vw[j] = j < (int)k ? p.visited[u[j] >> 5] : FULL;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t bit = 1u << (u[j] & 31);
+                    cl[j] = j < (int)k && !(vw[j] & bit) && !(atomicOr(p.visited + (u[j] >> 5), bit) & bit);
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    du[j] = 0;
+                    if (!cl[j]) continue;
+                    p.level[u[j]] = lvl;
+                    bm_set(nbm, u[j]);
+                    du[j] = __ldg(p.g.dout + u[j]);
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (!cl[j]) continue;
+                    mdeg += du[j];
+                    ++reached;
+                    online_record(nx, nlists, p.s, u[j], cls_of(du[j], p.s));
+                }
             });
         });
         st.edges += edges;
@@ -265,13 +284,14 @@ constexpr int PROBE = SX_PROBE;
 
 __global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) bfs_pull(BfsP p) {
     Ctl* c = p.s.ctl;
-    if (vload(&c->done) || vload(&c->dir) != DIR_PULL) return;
-    grid_begin(c);
+    const RunState& rs = run_state(c);
+    if (rs.done || rs.dir != DIR_PULL) return;
+    grid_begin(rs.launch);
     const uint64_t n = p.g.n;
     const uint64_t nw = (n + 31) >> 5;
-    uint32_t it = vload(&c->iter);
-    uint64_t m_u = vload(&c->m_u);
-    uint32_t nf_prev = vload(&c->nf_prev);
+    uint32_t it = rs.iter;
+    uint64_t m_u = rs.m_u;
+    uint32_t nf_prev = rs.nf_prev;
     uint32_t cnt[NCLS] = {0, 0, 0, 0};
     Stats st;
     uint32_t dir = DIR_PULL, done = 0;
@@ -482,12 +502,13 @@ __global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) bfs_pull(BfsP p) {
 // 8 x cluster_enter vertices or CL_EDGES x cluster_enter out-edges.
 __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) bfs_cluster(BfsP p) {
     Ctl* c = p.s.ctl;
-    if (vload(&c->done) || vload(&c->dir) != DIR_CLUSTER) return;
+    const RunState& rs = run_state(c);
+    if (rs.done || rs.dir != DIR_CLUSTER) return;
     constexpr uint32_t T = CL_CTAS * CL_BLOCK;
     const uint32_t tid = cluster_rank() * CL_BLOCK + threadIdx.x;
     const bool lead0 = tid == 0;
-    uint32_t it = vload(&c->iter);
-    uint64_t m_u = vload(&c->m_u);
+    uint32_t it = rs.iter;
+    uint64_t m_u = rs.m_u;
     Ctl::ClusterLine* cl = &c->cl;
     uint64_t edges = 0, entries = 0, reached = 0;
     uint32_t iters = 0, done = 0, dir = DIR_CLUSTER, nnext = 0;

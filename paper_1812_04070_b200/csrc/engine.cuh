@@ -30,6 +30,7 @@
 //     predicate with __ballot_sync; a two-pass grid-wide scan (per-CTA counts ->
 //     barrier -> offsets) writes class-split lists in ascending vertex order.
 #pragma once
+#include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -102,6 +103,21 @@ struct Ctl {
         unsigned int ballot, pull, iters;
     } st[2];
 };
+
+// The run state carried across launches (Ctl from `iter` to `ntrace`), as one
+// CTA sees it: run_state() reads the 128-B line once per CTA (warp 0, lane l
+// word l) instead of every thread loading each field from the same L2 line.
+struct RunState {
+    uint32_t iter, dir, done, error, lists_ready, slotted, launch, nf_prev, k;
+    uint64_t m_u, hi;
+    uint32_t cur_count[NCLS];
+    uint32_t ntrace;
+};
+static_assert(offsetof(Ctl, m_u) - offsetof(Ctl, iter) == offsetof(RunState, m_u), "RunState layout");
+static_assert(offsetof(Ctl, hi) - offsetof(Ctl, iter) == offsetof(RunState, hi), "RunState layout");
+static_assert(offsetof(Ctl, cur_count) - offsetof(Ctl, iter) == offsetof(RunState, cur_count), "RunState layout");
+static_assert(offsetof(Ctl, ntrace) - offsetof(Ctl, iter) == offsetof(RunState, ntrace), "RunState layout");
+static_assert(sizeof(RunState) <= 128 && offsetof(Ctl, cl) - offsetof(Ctl, iter) >= 128, "RunState fits one line");
 
 struct TraceRec {  // mirrors sx_trace_rec
     uint32_t iter, dir, filter, launch;
@@ -203,6 +219,17 @@ __device__ __forceinline__ uint32_t& bar_parity() {
 __device__ __forceinline__ void grid_begin(Ctl* c) {
     if (threadIdx.x == 0) bar_parity() = vload(&c->launch) & 1u;
     __syncthreads();
+}
+__device__ __forceinline__ void grid_begin(uint32_t launch) {
+    if (threadIdx.x == 0) bar_parity() = launch & 1u;
+    __syncthreads();
+}
+__device__ __forceinline__ const RunState& run_state(const Ctl* c) {
+    __shared__ alignas(16) uint32_t w[32];
+    __syncthreads();
+    if (threadIdx.x < 32) w[threadIdx.x] = vload(reinterpret_cast<const uint32_t*>(&c->iter) + threadIdx.x);
+    __syncthreads();
+    return *reinterpret_cast<const RunState*>(w);
 }
 // Called by CTA 0 thread 0 when the kernel exits: zero the other half for the next launch.
 __device__ __forceinline__ void grid_end(Ctl* c) {
@@ -308,6 +335,48 @@ __device__ __forceinline__ void maybe_reset_line(IterLine* L) {
 }
 
 // Sum of one iteration line over its slots, computed by warp 0 and shared.
+// One slot's counters in four 128-bit volatile loads (one L2 request each
+// instead of one per field: every CTA of the grid reads every slot).
+__device__ __forceinline__ uint4 vload4(const void* p) {
+    uint4 r;
+    asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+struct SlotSnap {
+    uint32_t cnt[NCLS];
+    uint32_t found, minv, alive;
+    uint64_t mdeg, edges;
+    double dsum;
+};
+__device__ __forceinline__ SlotSnap load_slot(const Slot& sl) {
+    static_assert(offsetof(Slot, found) == 16 && offsetof(Slot, mdeg) == 32 && offsetof(Slot, dsum) == 48, "Slot layout");
+    const char* b = reinterpret_cast<const char*>(&sl);
+    const uint4 a = vload4(b), q = vload4(b + 16), m = vload4(b + 32), d = vload4(b + 48);
+    SlotSnap r;
+    r.cnt[0] = a.x;
+    r.cnt[1] = a.y;
+    r.cnt[2] = a.z;
+    r.cnt[3] = a.w;
+    r.found = q.x;
+    r.minv = q.y;
+    r.alive = q.z;
+    r.mdeg = ((uint64_t)m.y << 32) | m.x;
+    r.edges = ((uint64_t)m.w << 32) | m.z;
+    r.dsum = __hiloint2double((int)d.y, (int)d.x);
+    return r;
+}
+__device__ __forceinline__ SlotSnap load_slot_cnt(const Slot& sl) {
+    const uint4 a = vload4(&sl);
+    SlotSnap r{};
+    r.cnt[0] = a.x;
+    r.cnt[1] = a.y;
+    r.cnt[2] = a.z;
+    r.cnt[3] = a.w;
+    return r;
+}
+
 struct LineSum {
     uint32_t cnt[NCLS];
     uint32_t cntmax[NCLS];
@@ -319,20 +388,19 @@ __device__ __forceinline__ void read_line(const IterLine* L, LineSum& out) {
     __shared__ LineSum sh;
     __syncthreads();
     if (warp_id() == 0) {
-        const Slot& s = L->s[lane_id()];
+        const SlotSnap x = load_slot(L->s[lane_id()]);
         LineSum r;
 #pragma unroll
         for (int c = 0; c < NCLS; ++c) {
-            const uint32_t x = vload(&s.cnt[c]);
-            r.cnt[c] = warp_sum(x);
-            r.cntmax[c] = warp_max(x);
+            r.cnt[c] = warp_sum(x.cnt[c]);
+            r.cntmax[c] = warp_max(x.cnt[c]);
         }
-        r.found = warp_sum(vload(&s.found));
-        r.minv = warp_min(vload(&s.minv));
-        r.alive = warp_sum(vload(&s.alive));
-        r.mdeg = warp_sum((uint64_t)vload(&s.mdeg));
-        r.edges = warp_sum((uint64_t)vload(&s.edges));
-        r.dsum = warp_sum(vload(&s.dsum));
+        r.found = warp_sum(x.found);
+        r.minv = warp_min(x.minv);
+        r.alive = warp_sum(x.alive);
+        r.mdeg = warp_sum(x.mdeg);
+        r.edges = warp_sum(x.edges);
+        r.dsum = warp_sum(x.dsum);
         if (lane_id() == 0) sh = r;
     }
     __syncthreads();
@@ -374,9 +442,10 @@ __device__ __forceinline__ void view_slots(const IterLine* L, const Sched& s, ui
     __syncthreads();
     if (warp_id() == 0) {
         const uint32_t l = lane_id();
+        const SlotSnap sn = load_slot_cnt(L->s[l]);
 #pragma unroll
         for (int c = 0; c < NCLS; ++c) {
-            const uint32_t x = min(vload(&L->s[l].cnt[c]), s.cap_s);
+            const uint32_t x = min(sn.cnt[c], s.cap_s);
             uint32_t inc = x;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -404,13 +473,13 @@ __device__ __forceinline__ void read_line_view(const IterLine* L, const Sched& s
     __syncthreads();
     if (warp_id() == 0) {
         const uint32_t l = lane_id();
-        const Slot& sl = L->s[l];
+        const SlotSnap sn = load_slot(L->s[l]);
         uint32_t x[NCLS];
 #pragma unroll
-        for (int c = 0; c < NCLS; ++c) x[c] = vload(&sl.cnt[c]);
-        const uint32_t found = vload(&sl.found), minv = vload(&sl.minv), alive = vload(&sl.alive);
-        const uint64_t mdeg = vload(&sl.mdeg), edges = vload(&sl.edges);
-        const double dsum = vload(&sl.dsum);
+        for (int c = 0; c < NCLS; ++c) x[c] = sn.cnt[c];
+        const uint32_t found = sn.found, minv = sn.minv, alive = sn.alive;
+        const uint64_t mdeg = sn.mdeg, edges = sn.edges;
+        const double dsum = sn.dsum;
         LineSum r;
 #pragma unroll
         for (int c = 0; c < NCLS; ++c) {
@@ -696,6 +765,30 @@ __device__ __forceinline__ void for_edges(const uint32_t* __restrict__ col, uint
         fn(e + 3, q.w);
     }
     for (uint64_t e = a + 4 * nvec + rank; e < end; e += size) fn(e, __ldg(col + e));
+}
+
+// for_edges in batches: fn(u, k) gets k (1..4) neighbour ids u[0..k) whose
+// dependent loads / atomics the caller issues together (ILP across a vector).
+template <class Fn>
+__device__ __forceinline__ void for_edges_b(const uint32_t* __restrict__ col, uint64_t beg, uint64_t end,
+                                            uint64_t rank, uint64_t size, Fn&& fn) {
+    uint64_t a = (beg + 3) & ~3ull;
+    if (a > end) a = end;
+    for (uint64_t e = beg + rank; e < a; e += size) {
+        const uint32_t u[4] = {__ldg(col + e), INF, INF, INF};
+        fn(u, 1);
+    }
+    const uint64_t nvec = (end - a) >> 2;
+    const uint4* c4 = reinterpret_cast<const uint4*>(col + a);
+    for (uint64_t i = rank; i < nvec; i += size) {
+        const uint4 q = __ldg(c4 + i);
+        const uint32_t u[4] = {q.x, q.y, q.z, q.w};
+        fn(u, 4);
+    }
+    for (uint64_t e = a + 4 * nvec + rank; e < end; e += size) {
+        const uint32_t u[4] = {__ldg(col + e), INF, INF, INF};
+        fn(u, 1);
+    }
 }
 
 // for_edges with the edge weight: in the aligned body the four u8 weights of a

@@ -54,17 +54,18 @@ struct LevelPred {
 
 __global__ void __launch_bounds__(BLOCK, 4) kcore_push(KcoreP p) {
     Ctl* c = p.s.ctl;
-    if (vload(&c->done)) return;
-    grid_begin(c);
+    const RunState& rs = run_state(c);
+    if (rs.done) return;
+    grid_begin(rs.launch);
     const uint64_t n = p.g.n;
-    uint32_t it = vload(&c->iter);
-    uint32_t k = vload(&c->k);
+    uint32_t it = rs.iter;
+    uint32_t k = rs.k;
     uint32_t cnt[NCLS];
-    uint32_t slotted = vload(&c->slotted);
+    uint32_t slotted = rs.slotted;
     if (slotted) {
         view_slots(&c->line[it % 3], p.s, cnt);
     } else {
-        for (int i = 0; i < NCLS; ++i) cnt[i] = vload(&c->cur_count[i]);
+        for (int i = 0; i < NCLS; ++i) cnt[i] = rs.cur_count[i];
         view_contig(cnt);
     }
     Stats st;

@@ -96,26 +96,27 @@ __device__ __forceinline__ void sssp_exit(const SsspP& p, uint32_t kdir, uint32_
 // ------------------------------------------------------------------ push
 __global__ void __launch_bounds__(BLOCK, 4) sssp_push(SsspP p) {
     Ctl* c = p.s.ctl;
-    if (vload(&c->done) || vload(&c->dir) != DIR_PUSH) return;
-    grid_begin(c);
-    uint32_t it = vload(&c->iter);
-    uint64_t hi = vload(&c->hi);
-    uint32_t nf_prev = vload(&c->nf_prev);
+    const RunState& rs = run_state(c);
+    if (rs.done || rs.dir != DIR_PUSH) return;
+    grid_begin(rs.launch);
+    uint32_t it = rs.iter;
+    uint64_t hi = rs.hi;
+    uint32_t nf_prev = rs.nf_prev;
     uint32_t cnt[NCLS];
     uint32_t slotted = 0;
     Stats st;
-    if (!vload(&c->lists_ready)) {
+    if (!rs.lists_ready) {
         // entering push from pull: the frontier exists only as a bitmap -> ballot filter
         if (!ballot_filter(BitmapWords{p.s.bm[it % 3]}, p.s, BallotOut{p.s.lists[it & 1], p.s.cstride, p.g.dout}, cnt))
             return;
         st.scanned += p.s.nwords * 32;
         if (!grid_sync(c)) return;
         view_contig(cnt);
-    } else if (vload(&c->slotted)) {
+    } else if (rs.slotted) {
         slotted = 1;
         view_slots(&c->line[it % 3], p.s, cnt);
     } else {
-        for (int i = 0; i < NCLS; ++i) cnt[i] = vload(&c->cur_count[i]);
+        for (int i = 0; i < NCLS; ++i) cnt[i] = rs.cur_count[i];
         view_contig(cnt);
     }
     uint32_t dir = DIR_PUSH, done = 0, ready = 1;
@@ -321,13 +322,14 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_push(SsspP p) {
 // in-degree >= sep_huge beforehand by the whole grid.
 __global__ void __launch_bounds__(BLOCK, 4) sssp_pull(SsspP p) {
     Ctl* c = p.s.ctl;
-    if (vload(&c->done) || vload(&c->dir) != DIR_PULL) return;
-    grid_begin(c);
+    const RunState& rs = run_state(c);
+    if (rs.done || rs.dir != DIR_PULL) return;
+    grid_begin(rs.launch);
     const uint64_t n = p.g.n;
     const uint64_t nw = (n + 31) >> 5;
-    uint32_t it = vload(&c->iter);
-    const uint64_t hi = vload(&c->hi);
-    uint32_t nf_prev = vload(&c->nf_prev);
+    uint32_t it = rs.iter;
+    const uint64_t hi = rs.hi;
+    uint32_t nf_prev = rs.nf_prev;
     uint32_t cnt[NCLS] = {0, 0, 0, 0};
     Stats st;
     uint32_t dir = DIR_PULL, done = 0;
@@ -503,12 +505,13 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_pull(SsspP p) {
 // kernels once it exceeds 8 x cluster_enter vertices.
 __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) sssp_cluster(SsspP p) {
     Ctl* c = p.s.ctl;
-    if (vload(&c->done) || vload(&c->dir) != DIR_CLUSTER) return;
+    const RunState& rs = run_state(c);
+    if (rs.done || rs.dir != DIR_CLUSTER) return;
     constexpr uint32_t T = CL_CTAS * CL_BLOCK;
     const uint32_t tid = cluster_rank() * CL_BLOCK + threadIdx.x;
     const bool lead0 = tid == 0;
-    uint32_t it = vload(&c->iter);
-    uint64_t hi = vload(&c->hi);
+    uint32_t it = rs.iter;
+    uint64_t hi = rs.hi;
     Ctl::ClusterLine* cl = &c->cl;
     uint64_t edges = 0, entries = 0;
     uint32_t iters = 0, ballots = 0, done = 0, dir = DIR_CLUSTER;
