@@ -96,6 +96,12 @@ sx_status sx_barrier_bench(sx_ctx ctx, uint32_t iters, double* us_per_barrier, i
    launch); 2: zero a bitmap of nwords words; 3: zero + compact an empty bitmap.
    *us = microseconds per launch (modes 0, 2, 3) or per barrier (mode 1). */
 sx_status sx_cluster_bench(sx_ctx ctx, uint64_t nwords, uint32_t mode, uint32_t reps, double* us);
+/* Diagnostic: GPU time per back-to-back launch of an empty kernel in the shape
+   of a fused phase (P:743's launch count is what selective fusion saves).
+   mode 0: plain launch of occupancy x SMs CTAs; 1: the same as a cooperative
+   launch; 2: one 16-CTA cluster.  *us = microseconds per launch.  Errors:
+   SX_E_INVALID (mode > 2, reps == 0, NULL us), SX_E_CUDA. */
+sx_status sx_launch_bench(sx_ctx ctx, uint32_t mode, uint32_t reps, double* us);
 
 /* ------------------------------------------------------------------ graphs */
 enum {

@@ -51,7 +51,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(name: str, defines: list) -> str:
+    """An experiment build (profiles/: loaded with SIMDX_LIB=...), e.g. -DSX_PROBE=8."""
+    out = os.path.join(os.path.dirname(HERE), "build", f"libsimdx_{name}.so")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    subprocess.check_call([NVCC, *FLAGS, *defines, "-o", out, *sources(), *link_flags()])
+    return out
+
+
 if __name__ == "__main__":
     import sys
-    build(force=True, verbose="-v" in sys.argv)
-    print(LIB)
+    if "--variant" in sys.argv:
+        i = sys.argv.index("--variant")
+        print(build_variant(sys.argv[i + 1], sys.argv[i + 2:]))
+    else:
+        build(force=True, verbose="-v" in sys.argv)
+        print(LIB)

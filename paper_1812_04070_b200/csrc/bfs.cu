@@ -31,23 +31,24 @@ struct BfsP {
 // is the one most likely to sit in a large frontier, so in the dense middle
 // levels a candidate usually costs one coalesced 4-B load instead of a row-pointer
 // pair plus a random row sector.  Probe order does not change the result (any
-// frontier in-neighbour proves level(v) = it + 1).
+// frontier in-neighbour proves level(v) = it + 1).  When v has exactly one
+// in-edge, bit 31 (HUB_SOLE; graphs of n <= 2^31) says the hub is the whole row:
+// a failed probe then settles v for the level without a row walk — on R-MAT
+// most candidates left open by the probe are such degree-1 vertices.
 constexpr uint32_t HUB_SCAN = 64;
-#ifndef SX_HUB_ILP
-#define SX_HUB_ILP 4
-#endif
+constexpr uint32_t HUB_SOLE = 0x80000000u;
 #ifndef SX_PROBE
 #define SX_PROBE 4
 #endif
 #ifndef SX_PULL_MINB
 #define SX_PULL_MINB 4
 #endif
-constexpr int HUB_ILP = SX_HUB_ILP;  // bottom-up: hub-probe rounds in flight per warp
 __global__ void __launch_bounds__(BLOCK) bfs_hub(DevGraph g, uint32_t* hub) {
     const uint32_t lane = lane_id();
     const uint64_t nwarp = (uint64_t)gridDim.x * WARPS;
+    const bool flag = g.n <= HUB_SOLE;
     for (uint64_t v = (uint64_t)blockIdx.x * WARPS + warp_id(); v < g.n; v += nwarp) {
-        const uint64_t beg = __ldg(g.irp + v), end = min(__ldg(g.irp + v + 1), beg + HUB_SCAN);
+        const uint64_t beg = __ldg(g.irp + v), end0 = __ldg(g.irp + v + 1), end = min(end0, beg + HUB_SCAN);
         uint64_t best = 0;
         for (uint64_t e = beg + lane; e < end; e += 32) {
             const uint32_t u = __ldg(g.ici + e);
@@ -55,9 +56,12 @@ __global__ void __launch_bounds__(BLOCK) bfs_hub(DevGraph g, uint32_t* hub) {
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1) best = max(best, __shfl_xor_sync(FULL, best, o));
-        if (lane == 0) hub[v] = best ? ~(uint32_t)best : INF;
+        if (lane == 0) hub[v] = best ? (~(uint32_t)best | (flag && end0 - beg == 1 ? HUB_SOLE : 0u)) : INF;
     }
 }
+// the probe target of a hub entry (INF: no in-neighbour) and whether it is v's only in-edge
+__device__ __forceinline__ uint32_t hub_id(uint32_t h) { return h == INF ? INF : h & ~HUB_SOLE; }
+__device__ __forceinline__ bool hub_sole(uint32_t h) { return h != INF && (h & HUB_SOLE); }
 
 constexpr uint32_t CL_EDGES = 32;
 __device__ __forceinline__ bool cluster_ok(const Sched& s, uint64_t nf, uint64_t mf) {
@@ -150,6 +154,7 @@ __global__ void __launch_bounds__(BLOCK, 4) bfs_push(BfsP p) {
     Ctl* c = p.s.ctl;
     const RunState& rs = run_state(c);
     if (rs.done || rs.dir != DIR_PUSH) return;
+    stage_init();
     grid_begin(rs.launch);
     uint32_t it = rs.iter;
     uint64_t m_u = rs.m_u;
@@ -210,6 +215,7 @@ __global__ void __launch_bounds__(BLOCK, 4) bfs_push(BfsP p) {
                 }
             });
         });
+        stage_flush(nx, nlists, p.s);
         st.edges += edges;
         st.reached += reached;
         if (lead()) st.entries += sum4(cnt);
@@ -267,20 +273,39 @@ __global__ void __launch_bounds__(BLOCK, 4) bfs_push(BfsP p) {
 }
 
 // ------------------------------------------------------------------ pull
-// Bottom-up step over chunks of 32 tiles of 32 consecutive vertices.  A warp
-// owns its chunk's words of the visited bitmap, so the active set of a tile is
-// the word ~visited & (in-degree > 0) — the ballot filter's output for that tile
-// without a grid-wide list.  The warp compacts the chunk's
-// candidates into a shared-memory list in vertex order (popc + exclusive scan:
-// a warp-local ballot filter) and processes them 32 per round, one per lane.
-// Candidates are binned by in-degree: every candidate first
-// probes PROBE in-edges on its own lane; small ones (thread granularity) finish
-// on their lane with PROBE loads in flight per round, medium and larger ones
-// still open continue with the whole warp, 32 edges per step (warp
-// granularity).  All stop at the first frontier in-neighbour (voting early
-// exit).  Found bits are gathered per word in shared memory and written
-// once per chunk with plain stores: no global atomics on the data path.
+// Bottom-up step.  The active set of a pull iteration is the unvisited set
+// (candidates: unvisited with in-degree > 0), held the JIT way:
+//  * TILE mode (large candidate sets — the ballot side): chunks of 32 tiles of
+//    32 consecutive vertices.  A warp owns its chunk's words of the visited
+//    bitmap, so a tile's candidates are the word ~visited & (in-degree > 0) —
+//    the ballot filter's output for that tile without a grid-wide
+//    list; the warp compacts them into shared memory in vertex order (popc +
+//    exclusive scan: a warp-local ballot filter).  Found bits are merged per
+//    word in shared memory and stored once: no global atomics.
+//  * LIST mode (small candidate sets — the online side): the candidates still
+//    open at the end of the previous pull iteration were recorded in slotted
+//    lists (online filter); the iteration walks those lists in warp
+//    chunks instead of scanning every tile.  Chosen after the barrier when the
+//    recorded total is <= n / LIST_DIV and no region overflowed.
+// A warp's candidates then go through two phases.  (1) Hub-first probe, HUB_ILP
+// rounds of 32 in flight: one load of hub[v] and one bitmap test each; a sole
+// in-edge probed in vain settles v (still open, no row walk).  (2) Row walks of
+// the others, binned by in-degree: small ones (thread
+// granularity) on their lane with PROBE loads in flight per round, medium and
+// larger ones with the whole warp, 32 edges per step (warp granularity); all
+// stop at the first frontier in-neighbour (voting early exit).
+// m_u on symmetric graphs needs no degree loads: every candidate left open
+// walked its whole row (or had one in-edge), so m_u(next) = sum of the open
+// candidates' degrees and m_f = m_u - m_u(next).
 constexpr int PROBE = SX_PROBE;
+#ifndef SX_HUB_ILP
+#define SX_HUB_ILP 4
+#endif
+constexpr int HUB_ILP = SX_HUB_ILP;             // phase 1: rounds of 32 candidates in flight per warp
+constexpr uint32_t LIST_DIV = 8;       // LIST mode when open candidates <= n / LIST_DIV
+constexpr uint32_t FREC_MAX = 32768;   // record the found vertices as a list when candidates <= this
+constexpr uint32_t CAND_CLS = 2;       // class region of lists[] holding the LIST-mode candidate lists
+constexpr uint32_t REC_STAGE = 256;    // per-warp staging of the LIST-mode record
 
 __global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) bfs_pull(BfsP p) {
     Ctl* c = p.s.ctl;
@@ -298,17 +323,73 @@ __global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) bfs_pull(BfsP p) {
     const uint32_t lane = lane_id();
     __shared__ uint32_t s_cand[WARPS][1024];
     __shared__ uint32_t s_found[WARPS][32];
+    __shared__ uint32_t s_cpre[NSLOT + 1];  // LIST mode: prefix of the candidate regions' counts
+    __shared__ uint32_t s_rec[WARPS][REC_STAGE];
     uint32_t* s_c = s_cand[warp_id()];
+    uint32_t* s_r = s_rec[warp_id()];
     uint32_t* s_f = s_found[warp_id()];
+    uint32_t ncand = 0;    // LIST mode when > 0: candidates recorded by the previous iteration
+    uint32_t handoff = 0;  // the next frontier was recorded as a contiguous list
     for (;;) {
         IterLine* nx = &c->line[(it + 1) % 3];
         maybe_reset_line(&c->line[(it + 2) % 3]);
+        if (lead()) c->cl.cnt[(it + 2) % 3] = 0;  // found-list counter of the next iteration
         clear_bitmap(p.s.bm[(it + 2) % 3], p.s.nwords);
         const uint32_t* cur = p.s.bm[it % 3];
         uint32_t* nbm = p.s.bm[(it + 1) % 3];
         const uint32_t lvl = it + 1;
-        uint64_t mdeg = 0, edges = 0, cand_small = 0, cand_warp = 0, rows = 0;
+        const bool list_mode = ncand > 0;
+        const bool rec_found = list_mode && ncand <= FREC_MAX;
+        uint32_t* cnext = p.s.lists[(it + 1) & 1] + (uint64_t)CAND_CLS * p.s.cstride;
+        uint32_t* flist = p.s.lists[(it + 1) & 1];  // class-0 region: the found list (hand-over)
+        unsigned int* fcnt = &c->cl.cnt[(it + 1) % 3];
+        uint64_t mdeg = 0, mopen = 0, edges = 0, cand_small = 0, cand_warp = 0, rows = 0;
         uint32_t found_cnt = 0;
+        // a found vertex: level, statistics, and (TILE) the word merge in shared
+        // memory or (LIST) the bitmaps plus the online record of the next frontier
+        auto on_found = [&](uint32_t v, uint64_t w0) {
+            p.level[v] = lvl;
+            if (!p.sym) mdeg += __ldg(p.g.dout + v);
+            if (!list_mode) {
+                atomicOr(s_f + ((v >> 5) - w0), 1u << (v & 31));
+                return;
+            }
+            bm_set(p.visited, v);
+            bm_set(nbm, v);
+            ++found_cnt;
+            if (rec_found) {  // warp-aggregated append
+                const uint32_t act = __activemask();
+                const int leader = __ffs(act) - 1;
+                uint32_t base = 0;
+                if ((int)lane == leader) base = atomicAdd(fcnt, (uint32_t)__popc(act));
+                base = __shfl_sync(act, base, leader);
+                flist[base + __popc(act & lanemask_lt())] = v;
+            }
+        };
+        // warp-collective: record the lanes' still-open candidates for a
+        // LIST-mode next iteration — staged in shared memory, then appended to
+        // cnext (region of this CTA's slot) with one atomic per flush instead of
+        // a blocking atomic round trip per probe round
+        uint32_t nrec = 0;
+        auto flush_rec = [&]() {
+            if (!nrec) return;
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(&nx->s[my_slot()].alive, nrec);
+            base = __shfl_sync(FULL, base, 0);
+            for (uint32_t j = lane; j < nrec; j += 32)
+                if (base + j < p.s.R) cnext[(uint64_t)my_slot() * p.s.R + base + j] = s_r[j];
+            __syncwarp();
+            nrec = 0;
+        };
+        auto record_open = [&](bool still, uint32_t v) {
+            const uint32_t bal = __ballot_sync(FULL, still);
+            if (still) s_r[nrec + __popc(bal & lanemask_lt())] = v;
+            nrec += __popc(bal);
+            if (nrec > REC_STAGE - 32) {
+                __syncwarp();
+                flush_rec();
+            }
+        };
         // one probe round: up to PROBE in-edges [e, end) of this lane's candidate, loads in flight together
         auto probe = [&](uint64_t& e, uint64_t end, bool& found) {
             uint32_t u[PROBE];
@@ -323,138 +404,185 @@ __global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) bfs_pull(BfsP p) {
             edges += k;
             e += k;
         };
-        const uint32_t nchunks = (uint32_t)((nw + 31) >> 5);
-        uint32_t s_cur = my_slot(), tries = 0;
-        uint32_t chunk = 0;
-        if (lane == 0) chunk = grab_chunk(nx, nchunks, s_cur, tries);
-        chunk = __shfl_sync(FULL, chunk, 0);
-        while (chunk != INF) {
-            uint32_t chunk_n = 0;
-            if (lane == 0) chunk_n = grab_chunk(nx, nchunks, s_cur, tries);
-            const uint64_t w0 = (uint64_t)chunk << 5;
-            const uint64_t wl = w0 + lane;
-            const uint32_t vis_l = wl < nw ? p.visited[wl] : FULL;
-            const uint32_t cand_l = wl < nw ? (~vis_l & __ldg(p.g.nz_in + wl)) : 0u;
-            const uint32_t cnt_l = __popc(cand_l);
-            uint32_t incl = cnt_l;
+        // the warp's `total` candidates in s_c through phases 1 and 2
+        auto run_cands = [&](uint32_t total, uint64_t w0) {
+            uint32_t nopen = 0;
+            for (uint32_t r0 = 0; r0 < total; r0 += 32 * HUB_ILP) {
+                uint32_t v[HUB_ILP], h[HUB_ILP], wd[HUB_ILP];
+                bool sole[HUB_ILP];
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(FULL, incl, o);
-                if ((int)lane >= o) incl += y;
-            }
-            const uint32_t total = __shfl_sync(FULL, incl, 31);
-            if (total) {
-                uint32_t pos = incl - cnt_l;
-                for (uint32_t w = cand_l; w; w &= w - 1) s_c[pos++] = (uint32_t)(wl << 5) + (__ffs(w) - 1);
-                s_f[lane] = 0;
-                __syncwarp();
-                // phase 1 — hub-first probe, HUB_ILP rounds of 32 candidates in flight:
-                // one coalesced 4-B load per candidate, then one bitmap test.  Found
-                // candidates finish here; open ones are compacted in place at the
-                // front of the list (stable, so still in vertex order).
-                uint32_t nopen = 0;
-                for (uint32_t r0 = 0; r0 < total; r0 += 32 * HUB_ILP) {
-                    uint32_t v[HUB_ILP], h[HUB_ILP], d[HUB_ILP], wd[HUB_ILP];
-#pragma unroll
-                    for (int k = 0; k < HUB_ILP; ++k) {
-                        const uint32_t i = r0 + 32 * k + lane;
-                        v[k] = i < total ? s_c[i] : INF;
-                    }
-#pragma unroll
-                    for (int k = 0; k < HUB_ILP; ++k) {
-                        h[k] = v[k] != INF ? __ldg(p.hub + v[k]) : INF;
-                        d[k] = v[k] != INF ? __ldg(p.g.dout + v[k]) : 0u;
-                    }
-#pragma unroll
-                    for (int k = 0; k < HUB_ILP; ++k) wd[k] = h[k] != INF ? cur[h[k] >> 5] : 0u;
-                    __syncwarp();
-#pragma unroll
-                    for (int k = 0; k < HUB_ILP; ++k) {
-                        const bool f = h[k] != INF && ((wd[k] >> (h[k] & 31)) & 1u);
-                        edges += h[k] != INF;
-                        if (f) {
-                            p.level[v[k]] = lvl;
-                            mdeg += d[k];
-                            atomicOr(s_f + ((v[k] >> 5) - w0), 1u << (v[k] & 31));
-                        }
-                        const bool open = v[k] != INF && !f;
-                        const uint32_t bal = __ballot_sync(FULL, open);
-                        if (open) s_c[nopen + __popc(bal & lanemask_lt())] = v[k];
-                        nopen += __popc(bal);
-                    }
-                    __syncwarp();
+                for (int k = 0; k < HUB_ILP; ++k) {
+                    const uint32_t i = r0 + 32 * k + lane;
+                    v[k] = i < total ? s_c[i] : INF;
                 }
-                // phase 2 — the open candidates walk their in-edge rows
-                uint32_t v_n = 0;
-                uint64_t beg_n = 0, end_n = 0;
-                if (lane < nopen) {
-                    v_n = s_c[lane];
+#pragma unroll
+                for (int k = 0; k < HUB_ILP; ++k) {
+                    const uint32_t x = v[k] != INF ? __ldg(p.hub + v[k]) : INF;
+                    h[k] = hub_id(x);
+                    sole[k] = hub_sole(x);
+                }
+#pragma unroll
+                for (int k = 0; k < HUB_ILP; ++k) wd[k] = h[k] != INF ? cur[h[k] >> 5] : 0u;
+                __syncwarp();
+#pragma unroll
+                for (int k = 0; k < HUB_ILP; ++k) {
+                    const bool f = h[k] != INF && ((wd[k] >> (h[k] & 31)) & 1u);
+                    edges += h[k] != INF;
+                    if (f) on_found(v[k], w0);
+                    const bool settled = v[k] != INF && !f && sole[k];
+                    if (settled) mopen += 1;
+                    record_open(settled, v[k]);
+                    // open ones are compacted in place at the front of s_c (stable)
+                    const bool open = v[k] != INF && !f && !sole[k];
+                    const uint32_t bal = __ballot_sync(FULL, open);
+                    if (open) s_c[nopen + __popc(bal & lanemask_lt())] = v[k];
+                    nopen += __popc(bal);
+                }
+                __syncwarp();
+            }
+            // phase 2 — the open candidates walk their in-edge rows
+            uint32_t v_n = 0;
+            uint64_t beg_n = 0, end_n = 0;
+            if (lane < nopen) {
+                v_n = s_c[lane];
+                beg_n = __ldg(p.g.irp + v_n);
+                end_n = __ldg(p.g.irp + v_n + 1);
+            }
+            for (uint32_t r = 0; r < nopen; r += 32) {
+                const bool open = r + lane < nopen;
+                const uint32_t v = v_n;
+                const uint64_t beg = beg_n, end = end_n;
+                bool found = false;
+                uint64_t e = beg;
+                rows += open;
+                if (open) probe(e, end, found);  // first row round
+                beg_n = end_n = 0;
+                if (r + 32 + lane < nopen) {
+                    v_n = s_c[r + 32 + lane];
                     beg_n = __ldg(p.g.irp + v_n);
                     end_n = __ldg(p.g.irp + v_n + 1);
                 }
-                for (uint32_t r = 0; r < nopen; r += 32) {
-                    const bool open = r + lane < nopen;
-                    const uint32_t v = v_n;
-                    const uint64_t beg = beg_n, end = end_n;
-                    bool found = false;
-                    uint64_t e = beg;
-                    rows += open;
-                    if (open) probe(e, end, found);  // first row round
-                    beg_n = end_n = 0;
-                    if (r + 32 + lane < nopen) {
-                        v_n = s_c[r + 32 + lane];
-                        beg_n = __ldg(p.g.irp + v_n);
-                        end_n = __ldg(p.g.irp + v_n + 1);
-                    }
-                    // thread granularity: small candidates continue on their lane
-                    const bool small = open && (end - beg) < p.s.sep_small;
-                    if (small) {
-                        ++cand_small;
-                        while (!found && e < end) probe(e, end, found);
-                    }
-                    // warp granularity: medium / large candidates still open, 32 edges per step
-                    uint32_t todo = __ballot_sync(FULL, open && !small && !found && e < end);
-                    while (todo) {
-                        const int l = __ffs(todo) - 1;
-                        todo &= todo - 1;
-                        const uint64_t b0 = __shfl_sync(FULL, e, l), e0 = __shfl_sync(FULL, end, l);
-                        bool hit = false;
-                        for (uint64_t b = b0; b < e0; b += 32) {
-                            const uint64_t x = b + lane;
-                            bool h = false;
-                            if (x < e0) {
-                                ++edges;
-                                h = bm_test(cur, __ldg(p.g.ici + x));
-                            }
-                            if (__any_sync(FULL, h)) {
-                                hit = true;
-                                break;
-                            }
+                // thread granularity: small candidates continue on their lane
+                const bool small = open && (end - beg) < p.s.sep_small;
+                if (small) {
+                    ++cand_small;
+                    while (!found && e < end) probe(e, end, found);
+                }
+                // warp granularity: medium / large candidates still open, 32 edges per step
+                uint32_t todo = __ballot_sync(FULL, open && !small && !found && e < end);
+                while (todo) {
+                    const int l = __ffs(todo) - 1;
+                    todo &= todo - 1;
+                    const uint64_t b0 = __shfl_sync(FULL, e, l), e0 = __shfl_sync(FULL, end, l);
+                    bool hit = false;
+                    for (uint64_t b = b0; b < e0; b += 32) {
+                        const uint64_t x = b + lane;
+                        bool hh = false;
+                        if (x < e0) {
+                            ++edges;
+                            hh = bm_test(cur, __ldg(p.g.ici + x));
                         }
-                        if ((int)lane == l) found = hit;
-                        ++cand_warp;
+                        if (__any_sync(FULL, hh)) {
+                            hit = true;
+                            break;
+                        }
                     }
-                    if (found) {
-                        p.level[v] = lvl;
-                        mdeg += p.sym ? (end - beg) : __ldg(p.g.dout + v);
-                        atomicOr(s_f + ((v >> 5) - w0), 1u << (v & 31));
-                    }
+                    if ((int)lane == l) found = hit;
+                    ++cand_warp;
                 }
-                __syncwarp();
-                const uint32_t fm = s_f[lane];
-                if (fm) {
-                    p.visited[wl] = vis_l | fm;  // this warp owns the chunk's words during the level
-                    nbm[wl] = fm;
-                    found_cnt += __popc(fm);
-                }
-                __syncwarp();
+                if (found) on_found(v, w0);
+                const bool still = open && !found;
+                if (still) mopen += end - beg;
+                record_open(still, v);
             }
-            chunk = __shfl_sync(FULL, chunk_n, 0);
+        };
+        uint32_t s_cur = my_slot(), tries = 0;
+        uint32_t chunk = 0;
+        if (list_mode) {
+            // chunks of the recorded candidates; the chunk size adapts so that
+            // every warp of the grid gets work when the list is short
+            const uint32_t* ccur = p.s.lists[it & 1] + (uint64_t)CAND_CLS * p.s.cstride;
+            if (threadIdx.x < 32) {
+                const uint32_t x = min(vload(&c->line[it % 3].s[lane].alive), p.s.R);
+                uint32_t inc = x;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(FULL, inc, o);
+                    if ((int)lane >= o) inc += y;
+                }
+                s_cpre[lane] = inc - x;
+                if (lane == 31) s_cpre[NSLOT] = inc;
+            }
+            __syncthreads();
+            const uint64_t per_warp = (ncand + gwarps() - 1) / gwarps();
+            const uint32_t csz = per_warp >= 192 ? 256u : per_warp >= 96 ? 128u : per_warp >= 48 ? 64u : 32u;
+            const uint32_t nchunks = (ncand + csz - 1) / csz;
+            if (lane == 0) chunk = grab_chunk(nx, nchunks, s_cur, tries);
+            chunk = __shfl_sync(FULL, chunk, 0);
+            while (chunk != INF) {
+                uint32_t chunk_n = 0;
+                if (lane == 0) chunk_n = grab_chunk(nx, nchunks, s_cur, tries);
+                const uint32_t i0 = chunk * csz;
+                const uint32_t total = min(csz, ncand - i0);
+                for (uint32_t j = lane; j < total; j += 32) {
+                    const uint32_t i = i0 + j;
+                    int lo = 0, hi = NSLOT;  // largest lo with s_cpre[lo] <= i
+#pragma unroll
+                    for (int q = 0; q < 5; ++q) {
+                        const int mid = (lo + hi) >> 1;
+                        if (s_cpre[mid] <= i) lo = mid;
+                        else hi = mid;
+                    }
+                    s_c[j] = ccur[(uint64_t)lo * p.s.R + (i - s_cpre[lo])];
+                }
+                __syncwarp();
+                run_cands(total, 0);
+                __syncwarp();
+                flush_rec();
+                chunk = __shfl_sync(FULL, chunk_n, 0);
+            }
+        } else {
+            const uint32_t nchunks = (uint32_t)((nw + 31) >> 5);
+            if (lane == 0) chunk = grab_chunk(nx, nchunks, s_cur, tries);
+            chunk = __shfl_sync(FULL, chunk, 0);
+            while (chunk != INF) {
+                uint32_t chunk_n = 0;
+                if (lane == 0) chunk_n = grab_chunk(nx, nchunks, s_cur, tries);
+                const uint64_t w0 = (uint64_t)chunk << 5;
+                const uint64_t wl = w0 + lane;
+                const uint32_t vis_l = wl < nw ? p.visited[wl] : FULL;
+                const uint32_t cand_l = wl < nw ? (~vis_l & __ldg(p.g.nz_in + wl)) : 0u;
+                const uint32_t cnt_l = __popc(cand_l);
+                uint32_t incl = cnt_l;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(FULL, incl, o);
+                    if ((int)lane >= o) incl += y;
+                }
+                const uint32_t total = __shfl_sync(FULL, incl, 31);
+                if (total) {
+                    uint32_t pos = incl - cnt_l;
+                    for (uint32_t w = cand_l; w; w &= w - 1) s_c[pos++] = (uint32_t)(wl << 5) + (__ffs(w) - 1);
+                    s_f[lane] = 0;
+                    __syncwarp();
+                    run_cands(total, w0);
+                    __syncwarp();
+                    flush_rec();
+                    const uint32_t fm = s_f[lane];
+                    if (fm) {
+                        p.visited[wl] = vis_l | fm;  // this warp owns the chunk's words during the level
+                        nbm[wl] = fm;
+                        found_cnt += __popc(fm);
+                    }
+                    __syncwarp();
+                }
+                chunk = __shfl_sync(FULL, chunk_n, 0);
+            }
         }
         st.edges += edges;
         st.reached += found_cnt;
         {
-            uint64_t v4[4] = {mdeg, found_cnt, cand_small, cand_warp};
+            uint64_t v4[4] = {p.sym ? mopen : mdeg, found_cnt, cand_small, cand_warp};
             block_sum<4>(v4);
             if (threadIdx.x == 0) {
                 Slot& sl = nx->s[my_slot()];
@@ -465,18 +593,20 @@ __global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) bfs_pull(BfsP p) {
             }
         }
         st.entries += rows;
-        st.scanned += (lead() ? nw * 32 : 0);
+        st.scanned += (lead() && !list_mode ? nw * 32 : 0);
         if (!grid_sync(c)) return;
         LineSum ls;
         read_line(nx, ls);
         const uint64_t nf = ls.found;
-        const uint64_t mf = ls.mdeg;
-        const uint32_t tc[NCLS] = {ls.cnt[0], ls.cnt[1], 0u, 0u};
+        // symmetric: the line holds sum deg(still unvisited); else sum deg(found)
+        const uint64_t mf = p.sym ? m_u - ls.mdeg : ls.mdeg;
+        const uint32_t nopen_all = ls.alive;
+        const uint32_t tc[NCLS] = {ls.cnt[0], ls.cnt[1], 0u, nopen_all};
         m_u -= mf;
         ++it;
         ++st.iters;
         ++st.pull;
-        trace_put(p.s, it, DIR_PULL, 1u, tc, nf, mf, m_u);
+        trace_put(p.s, it, DIR_PULL, list_mode ? 0u : 1u, tc, nf, mf, m_u);
         if (nf == 0 || (p.s.max_iters && it >= p.s.max_iters)) {
             done = 1;
             break;
@@ -486,9 +616,34 @@ __global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) bfs_pull(BfsP p) {
         nf_prev = (uint32_t)nf;
         if (to_push) {
             dir = cluster_ok(p.s, nf, mf) ? DIR_CLUSTER : DIR_PUSH;
+            if (dir == DIR_CLUSTER && rec_found && p.s.force_filter != 2) {
+                // hand the frontier over as the list recorded in flist / fcnt: the
+                // cluster kernel skips its bitmap scan; the stale bitmap it would
+                // clear is cleared here by the whole grid
+                handoff = 1;
+                clear_bitmap(p.s.bm[(it + 2) % 3], p.s.nwords);
+            }
             break;
         }
         if (!p.s.fusion) break;
+        // LIST mode next when the open candidates are few and every slot region held its share
+        ncand = 0;
+        if (p.s.force_filter != 2 && nopen_all > 0 && nopen_all <= n / LIST_DIV) {
+            __shared__ uint32_t s_ok;
+            if (threadIdx.x < 32) {
+                const uint32_t ok = __all_sync(FULL, vload(&nx->s[lane].alive) <= p.s.R);
+                if (lane == 0) s_ok = ok;
+            }
+            __syncthreads();
+            if (s_ok) ncand = nopen_all;
+            __syncthreads();
+        }
+    }
+    if (lead()) {
+        // the found-list counters stay zero outside a hand-over
+        for (int i = 0; i < 3; ++i)
+            if (!(handoff && i == (int)(it % 3))) c->cl.cnt[i] = 0;
+        c->cl.ready = handoff;
     }
     bfs_exit(p, DIR_PULL, it, m_u, nf_prev, dir, done, 0u, 0u, cnt, st);
 }

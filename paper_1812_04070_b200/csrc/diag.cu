@@ -110,3 +110,44 @@ extern "C" sx_status sx_cluster_bench(sx_ctx c, uint64_t nwords, uint32_t mode, 
     *us = (double)ms * 1e3 / reps;
     return SX_OK;
 }
+
+// ---------------------------------------------------------------- launch-cost micro-benchmark
+// GPU time per back-to-back launch of an empty kernel in the fused kernels'
+// shape: mode 0 plain launch, 1 cooperative launch (occupancy x SMs CTAs of
+// BLOCK threads), 2 one 16-CTA cluster — the fixed cost a launch sequence pays
+// per phase, whatever the phase does.
+namespace sx {
+__global__ void __launch_bounds__(BLOCK, 4) k_empty(uint32_t* sink) {
+    if (sink && threadIdx.x == 0 && blockIdx.x == 0xFFFFFFFFu) *sink = 1;
+}
+__global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) k_empty_cluster(uint32_t* sink) {
+    if (sink && threadIdx.x == 0 && blockIdx.x == 0xFFFFFFFFu) *sink = 1;
+}
+}  // namespace sx
+
+extern "C" sx_status sx_launch_bench(sx_ctx c, uint32_t mode, uint32_t reps, double* us) {
+    if (!us || reps == 0 || mode > 2) return sxh::fail(SX_E_INVALID, "sx_launch_bench: bad argument");
+    sx_status rc = sxh::check_ctx(c);
+    if (rc != SX_OK) return rc;
+    int per_sm = 0;
+    SX_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_empty, BLOCK, 0));
+    const int grid = per_sm * c->prop.multiProcessorCount;
+    uint32_t* sink = nullptr;
+    void* args[] = {&sink};
+    SX_CU(cudaFuncSetAttribute((const void*)k_empty_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    auto one = [&]() -> cudaError_t {
+        if (mode == 0) return cudaLaunchKernel((const void*)k_empty, dim3(grid), dim3(BLOCK), args, 0, c->stream);
+        if (mode == 1) return cudaLaunchCooperativeKernel((const void*)k_empty, dim3(grid), dim3(BLOCK), args, 0, c->stream);
+        return cudaLaunchKernel((const void*)k_empty_cluster, dim3(CL_CTAS), dim3(CL_BLOCK), args, 0, c->stream);
+    };
+    for (int i = 0; i < 3; ++i) SX_CU(one());
+    SX_CU(cudaStreamSynchronize(c->stream));
+    SX_CU(cudaEventRecord(c->ev0, c->stream));
+    for (uint32_t i = 0; i < reps; ++i) SX_CU(one());
+    SX_CU(cudaEventRecord(c->ev1, c->stream));
+    SX_CU(cudaEventSynchronize(c->ev1));
+    float ms = 0;
+    SX_CU(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    *us = (double)ms * 1e3 / reps;
+    return SX_OK;
+}

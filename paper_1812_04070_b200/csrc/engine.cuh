@@ -95,6 +95,7 @@ struct Ctl {
         unsigned int cnt[3];
         unsigned int minv;
         unsigned int nbig[3];  // tasks of degree > CL_BIG deferred to the cluster-wide edge loop
+        unsigned int ready;    // BFS: the pull kernel left the frontier as a contiguous list (cnt[iter % 3])
         unsigned long long mf[3];  // BFS: sum of out-degrees of the next frontier
     } cl;
     // --- run statistics per direction of the launch (0 push, 1 pull), one atomic per CTA per launch
@@ -528,10 +529,30 @@ __device__ __forceinline__ uint32_t task_at(const uint32_t* lists, const Sched& 
 
 // ---------------------------------------------------------------- online filter
 // Record vertex u of class c into the next lists: region (slot of
-// this CTA, class c).  Warp-aggregated: lanes of the same class share one
-// atomicAdd.  Entries beyond cap_s are not stored (overflow); the
-// counter keeps counting so the JIT controller sees the overflow at the barrier.
-__device__ __forceinline__ void online_record(IterLine* L, uint32_t* lists, const Sched& s, uint32_t u, uint32_t c) {
+// this CTA, class c).  Two levels, both warp-aggregated (lanes of the same
+// class share one atomic via __match_any_sync):
+//   * a CTA stage in shared memory (STAGE entries per class; a shared-memory
+//     atomic, no L2 round trip on the compute path), appended to the slot
+//     region by stage_flush() before the iteration's barrier — one global
+//     atomic per class per CTA;
+//   * entries beyond the stage go straight to the slot region (global atomic).
+// Region entries beyond cap_s are not stored (overflow); the
+// counter keeps counting, so the JIT controller sees the overflow at the barrier.
+constexpr uint32_t STAGE = 512;
+struct Stage {
+    uint32_t cnt[NCLS];
+    uint32_t e[NCLS][STAGE];
+};
+__device__ __forceinline__ Stage& stage() {
+    __shared__ Stage st;
+    return st;
+}
+// Kernel entry, before the first record (a __syncthreads must follow: grid_begin has one).
+__device__ __forceinline__ void stage_init() {
+    if (threadIdx.x < NCLS) stage().cnt[threadIdx.x] = 0;
+}
+__device__ __forceinline__ void online_record_global(IterLine* L, uint32_t* lists, const Sched& s, uint32_t u,
+                                                     uint32_t c) {
     const uint32_t slot = my_slot();
     const uint32_t active = __activemask();
     const uint32_t peers = __match_any_sync(active, c);
@@ -541,6 +562,39 @@ __device__ __forceinline__ void online_record(IterLine* L, uint32_t* lists, cons
     base = __shfl_sync(peers, base, leader);
     const uint32_t pos = base + __popc(peers & lanemask_lt());
     if (pos < s.cap_s) lists[(uint64_t)c * s.cstride + (uint64_t)slot * s.R + pos] = u;
+}
+__device__ __forceinline__ void online_record(IterLine* L, uint32_t* lists, const Sched& s, uint32_t u, uint32_t c) {
+    Stage& st = stage();
+    const uint32_t active = __activemask();
+    const uint32_t peers = __match_any_sync(active, c);
+    const int leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if ((int)lane_id() == leader) base = atomicAdd(&st.cnt[c], (uint32_t)__popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    const uint32_t pos = base + __popc(peers & lanemask_lt());
+    if (pos < STAGE) st.e[c][pos] = u;
+    else online_record_global(L, lists, s, u, c);
+}
+// All threads, after the iteration's records and before its barrier: append
+// the CTA stage to this CTA's slot regions (warp c copies class c).
+__device__ __forceinline__ void stage_flush(IterLine* L, uint32_t* lists, const Sched& s) {
+    Stage& st = stage();
+    __syncthreads();
+    const uint32_t c = warp_id();
+    if (c < NCLS) {
+        const uint32_t n = min(st.cnt[c], STAGE);
+        if (n) {
+            const uint32_t slot = my_slot();
+            uint32_t base = 0;
+            if (lane_id() == 0) base = atomicAdd(&L->s[slot].cnt[c], n);
+            base = __shfl_sync(FULL, base, 0);
+            uint32_t* dst = lists + (uint64_t)c * s.cstride + (uint64_t)slot * s.R;
+            for (uint32_t j = lane_id(); j < n; j += 32)
+                if (base + j < s.cap_s) dst[base + j] = st.e[c][j];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < NCLS) st.cnt[threadIdx.x] = 0;
 }
 
 // One CTA-level total added to this CTA's slot (thread 0 after a block_sum).
@@ -1059,13 +1113,22 @@ __device__ __forceinline__ void word_values(const uint32_t* a, uint64_t wi, uint
 // frontier bitmap bm[it % 3] into lists[it & 1] (count in cl.cnt[it % 3]).
 __device__ __forceinline__ void cluster_entry(const Sched& s, uint32_t it, uint32_t tid, uint32_t T) {
     Ctl::ClusterLine* cl = &s.ctl->cl;
+    // the BFS pull kernel may hand over the frontier as a ready list (it also
+    // cleared the stale bitmap): then only the counters are reset
+    const bool ready = vload(&cl->ready) != 0;
+    cluster_barrier();  // every CTA has read `ready` before thread 0 clears it
     if (tid == 0) {
         for (int i = 0; i < 3; ++i) {
-            cl->cnt[i] = 0;
+            if (!(ready && i == (int)(it % 3))) cl->cnt[i] = 0;
             cl->nbig[i] = 0;
             cl->mf[i] = 0;
         }
         cl->minv = INF;
+        cl->ready = 0;
+    }
+    if (ready) {
+        cluster_barrier();
+        return;
     }
     uint4* z = reinterpret_cast<uint4*>(s.bm[(it + 2) % 3]);
     const uint64_t nq = s.nwords / 4;
@@ -1078,6 +1141,7 @@ __device__ __forceinline__ void cluster_entry(const Sched& s, uint32_t it, uint3
 // Exit (one thread): the grid kernels rebuild their lists from bm[it % 3] and
 // start from zeroed grid-barrier counters.
 __device__ __forceinline__ void cluster_leave(Ctl* c) {
+    for (int i = 0; i < 3; ++i) c->cl.cnt[i] = 0;  // the BFS pull kernel counts its hand-over list here
     c->lists_ready = 0;
     c->slotted = 0;
     for (int h = 0; h < 2; ++h) {

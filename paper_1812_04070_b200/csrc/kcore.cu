@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(BLOCK, 4) kcore_push(KcoreP p) {
     Ctl* c = p.s.ctl;
     const RunState& rs = run_state(c);
     if (rs.done) return;
+    stage_init();
     grid_begin(rs.launch);
     const uint64_t n = p.g.n;
     uint32_t it = rs.iter;
@@ -166,6 +167,7 @@ __global__ void __launch_bounds__(BLOCK, 4) kcore_push(KcoreP p) {
                 v = next;
             }
         });
+        stage_flush(nx, nlists, p.s);
         st.edges += edges;
         if (lead()) st.entries += sum4(cnt);
         if (!grid_sync(c)) return;

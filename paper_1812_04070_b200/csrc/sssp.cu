@@ -98,6 +98,7 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_push(SsspP p) {
     Ctl* c = p.s.ctl;
     const RunState& rs = run_state(c);
     if (rs.done || rs.dir != DIR_PUSH) return;
+    stage_init();
     grid_begin(rs.launch);
     uint32_t it = rs.iter;
     uint64_t hi = rs.hi;
@@ -210,6 +211,7 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_push(SsspP p) {
                 v = next;
             }
         });
+        stage_flush(nx, nlists, p.s);
         st.edges += edges;
         if (lead()) st.entries += sum4(cnt);
         {

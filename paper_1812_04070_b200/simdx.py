@@ -91,6 +91,7 @@ _lib.sx_spmv.argtypes = [_vp, _vp, _u32, _P(sx_opts), _vp, _P(sx_stats)]
 _lib.sx_bp.argtypes = [_vp, _vp, _u32, _P(sx_opts), _vp, _P(sx_stats)]
 _lib.sx_barrier_bench.argtypes = [_vp, _u32, _P(ctypes.c_double), _P(ctypes.c_int)]
 _lib.sx_cluster_bench.argtypes = [_vp, _u64, _u32, _u32, _P(ctypes.c_double)]
+_lib.sx_launch_bench.argtypes = [_vp, _u32, _u32, _P(ctypes.c_double)]
 _lib.sx_nccl_unique_id.argtypes = [_vp]
 _lib.sx_dist_create.argtypes = [_vp, _u64, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _P(_vp)]
 _lib.sx_dist_range.argtypes = [_vp, ctypes.c_int, _P(_u64), _P(_u64)]
@@ -100,14 +101,14 @@ _lib.sx_dist_free.restype = None
 _lib.sx_dist_bfs.argtypes = [_vp, _u32, _P(sx_opts), _P(_vp), _P(sx_stats)]
 _lib.sx_dist_sssp.argtypes = [_vp, _u32, _u32, _P(sx_opts), _P(_vp), _P(sx_stats)]
 for _f in ("sx_ctx_create", "sx_ctx_info", "sx_graph_upload", "sx_graph_info", "sx_bfs", "sx_sssp", "sx_pagerank",
-           "sx_kcore", "sx_spmv", "sx_bp", "sx_barrier_bench", "sx_cluster_bench", "sx_nccl_unique_id",
-           "sx_dist_create", "sx_dist_range", "sx_dist_upload", "sx_dist_bfs", "sx_dist_sssp"):
+           "sx_kcore", "sx_spmv", "sx_bp", "sx_barrier_bench", "sx_cluster_bench", "sx_launch_bench",
+           "sx_nccl_unique_id", "sx_dist_create", "sx_dist_range", "sx_dist_upload", "sx_dist_bfs", "sx_dist_sssp"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 EXPORTED = ["sx_status_str", "sx_last_error", "sx_version", "sx_ctx_create", "sx_ctx_destroy", "sx_ctx_info",
             "sx_graph_upload", "sx_graph_info", "sx_graph_free", "sx_opts_default", "sx_bfs", "sx_sssp",
-            "sx_pagerank", "sx_kcore", "sx_spmv", "sx_bp", "sx_barrier_bench", "sx_cluster_bench", "sx_nccl_unique_id",
-            "sx_dist_create", "sx_dist_range", "sx_dist_upload", "sx_dist_free", "sx_dist_bfs", "sx_dist_sssp"]
+            "sx_pagerank", "sx_kcore", "sx_spmv", "sx_bp", "sx_barrier_bench", "sx_cluster_bench", "sx_launch_bench",
+            "sx_nccl_unique_id", "sx_dist_create", "sx_dist_range", "sx_dist_upload", "sx_dist_free", "sx_dist_bfs", "sx_dist_sssp"]
 
 
 class SimdxError(RuntimeError):
@@ -188,6 +189,12 @@ def sx_ctx_info(ctx) -> dict:
 def sx_cluster_bench(ctx, nwords: int, mode: int, reps: int = 100) -> float:
     us = ctypes.c_double()
     _check(_lib.sx_cluster_bench(ctx, nwords, mode, reps, ctypes.byref(us)), "sx_cluster_bench")
+    return us.value
+
+
+def sx_launch_bench(ctx, mode: int, reps: int = 200) -> float:
+    us = ctypes.c_double()
+    _check(_lib.sx_launch_bench(ctx, mode, reps, ctypes.byref(us)), "sx_launch_bench")
     return us.value
 
 

@@ -1,6 +1,6 @@
 """Summarise an ncu source page: top CUDA source lines by warp-stall samples.
 
-usage: python profiles/ncu_src_top.py report.ncu-rep [N] [--sass]
+usage: python profiles/ncu_src_top.py report.ncu-rep [N] [--sass] [--kernel=REGEX]
 Reads the interleaved "cuda,sass" source view (needs -lineinfo and
 --import-source on at capture time); a CUDA line's sample count is the sum over
 the SASS instructions listed under it.
@@ -13,7 +13,9 @@ import sys
 rep = sys.argv[1]
 N = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else 25
 show_sass = "--sass" in sys.argv
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+kfilt = [a.split("=", 1)[1] for a in sys.argv if a.startswith("--kernel=")]
+kargs = ["-k", "regex:" + kfilt[0]] if kfilt else []
+out = subprocess.run(["ncu", "-i", rep, *kargs, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 lines, fname, hdr, cur = {}, None, None, None
 sass = []
