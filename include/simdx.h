@@ -138,6 +138,38 @@ typedef struct {
  * SX_E_OOM, SX_E_CUDA.
  */
 sx_status sx_graph_upload(sx_ctx ctx, const sx_csr_desc* desc, sx_graph* out);
+/*
+ * Generate a synthetic graph directly in device memory (SURVEY.md §8(b), §8(d)
+ * input recipe; the paper's Kron/R-MAT workloads) and
+ * return it as a graph of this ctx, prepared exactly like sx_graph_upload.
+ * The generator is the seeded one of simgen/ (Philox-4x32-10, counter = tuple
+ * index), so the CSR is bit-identical to simgen.c's for the same arguments.
+ *
+ * sx_graph_rmat: Graph500 Kronecker/R-MAT, n = 2^scale, edgefactor*2^scale
+ *   tuples with (A,B,C,D) = (.57,.19,.19,.05) (reading 20), symmetrised,
+ *   self-loops dropped, duplicates kept (reading 19), rows sorted by (col, w);
+ *   ids relabelled by a bijective mixer that fixes vertex 0 unless
+ *   SX_GEN_NO_RELABEL.  Weights uniform in [wmin, wmax] per tuple (both
+ *   directions equal; reading 13); wmin = wmax = 0 = unweighted.  Stored u8
+ *   when wmax <= 255.
+ * sx_graph_grid: rows x cols 4-neighbour grid ("road-like", C2), vertex id
+ *   r*cols + c, weight per undirected edge id, same weight rule.
+ * Errors: SX_E_INVALID (scale outside [1,31], edgefactor < 1, n >= 2^32-1,
+ * wmin = 0 < wmax or wmax < wmin, unknown flag), SX_E_OOM, SX_E_CUDA.
+ */
+enum { SX_GEN_NO_RELABEL = 1 };
+sx_status sx_graph_rmat(sx_ctx ctx, int scale, int edgefactor, uint64_t seed, uint32_t wmin, uint32_t wmax,
+                        uint32_t flags, sx_graph* out);
+sx_status sx_graph_grid(sx_ctx ctx, uint32_t rows, uint32_t cols, uint64_t seed, uint32_t wmin, uint32_t wmax,
+                        sx_graph* out);
+/*
+ * Copy a graph's CSR back to caller memory (host or device): row_ptr u64[n+1],
+ * col u32[m], w u32[m] (widened from u8 storage).  Any pointer may be NULL to
+ * skip that array.  This is how the oracle side checks graphs built on the
+ * device.  Errors: SX_E_WEIGHT (w requested of an
+ * unweighted graph), SX_E_INVALID, SX_E_CUDA.
+ */
+sx_status sx_graph_download(sx_graph g, uint64_t* row_ptr, uint32_t* col, uint32_t* w);
 /* n, m and the owned vertex range [v_begin, v_end) (= [0, n) on one GPU). Any out pointer may be NULL. */
 sx_status sx_graph_info(sx_graph g, uint64_t* n, uint64_t* m, uint64_t* v_begin, uint64_t* v_end);
 /* Free a graph and its workspace (NULL is a no-op). */

@@ -80,6 +80,9 @@ _lib.sx_ctx_info.argtypes = [_vp, _P(sx_device_info)]
 _lib.sx_graph_upload.argtypes = [_vp, _P(sx_csr_desc), _P(_vp)]
 _lib.sx_graph_info.argtypes = [_vp, _P(_u64), _P(_u64), _P(_u64), _P(_u64)]
 _lib.sx_graph_free.argtypes = [_vp]
+_lib.sx_graph_rmat.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _u64, _u32, _u32, _u32, _P(_vp)]
+_lib.sx_graph_grid.argtypes = [_vp, _u32, _u32, _u64, _u32, _u32, _P(_vp)]
+_lib.sx_graph_download.argtypes = [_vp, _vp, _vp, _vp]
 _lib.sx_graph_free.restype = None
 _lib.sx_opts_default.argtypes = [_P(sx_opts)]
 _lib.sx_opts_default.restype = None
@@ -100,13 +103,14 @@ _lib.sx_dist_free.argtypes = [_vp]
 _lib.sx_dist_free.restype = None
 _lib.sx_dist_bfs.argtypes = [_vp, _u32, _P(sx_opts), _P(_vp), _P(sx_stats)]
 _lib.sx_dist_sssp.argtypes = [_vp, _u32, _u32, _P(sx_opts), _P(_vp), _P(sx_stats)]
-for _f in ("sx_ctx_create", "sx_ctx_info", "sx_graph_upload", "sx_graph_info", "sx_bfs", "sx_sssp", "sx_pagerank",
+for _f in ("sx_ctx_create", "sx_ctx_info", "sx_graph_upload", "sx_graph_info", "sx_graph_rmat", "sx_graph_grid",
+           "sx_graph_download", "sx_bfs", "sx_sssp", "sx_pagerank",
            "sx_kcore", "sx_spmv", "sx_bp", "sx_barrier_bench", "sx_cluster_bench", "sx_launch_bench",
            "sx_nccl_unique_id", "sx_dist_create", "sx_dist_range", "sx_dist_upload", "sx_dist_bfs", "sx_dist_sssp"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 EXPORTED = ["sx_status_str", "sx_last_error", "sx_version", "sx_ctx_create", "sx_ctx_destroy", "sx_ctx_info",
-            "sx_graph_upload", "sx_graph_info", "sx_graph_free", "sx_opts_default", "sx_bfs", "sx_sssp",
+            "sx_graph_upload", "sx_graph_info", "sx_graph_free", "sx_graph_rmat", "sx_graph_grid", "sx_graph_download", "sx_opts_default", "sx_bfs", "sx_sssp",
             "sx_pagerank", "sx_kcore", "sx_spmv", "sx_bp", "sx_barrier_bench", "sx_cluster_bench", "sx_launch_bench",
             "sx_nccl_unique_id", "sx_dist_create", "sx_dist_range", "sx_dist_upload", "sx_dist_free", "sx_dist_bfs", "sx_dist_sssp"]
 
@@ -220,6 +224,26 @@ def sx_graph_upload(ctx, n, row_ptr, col, w=None, csc_ptr=None, csc_idx=None, cs
     return h
 
 
+SX_GEN_NO_RELABEL = 1
+
+
+def sx_graph_rmat(ctx, scale, edgefactor=16, seed=1, wmin=0, wmax=0, flags=0):
+    h = _vp()
+    _check(_lib.sx_graph_rmat(ctx, scale, edgefactor, seed, wmin, wmax, flags, ctypes.byref(h)), "sx_graph_rmat")
+    return h
+
+
+def sx_graph_grid(ctx, rows, cols, seed=1, wmin=1, wmax=255):
+    h = _vp()
+    _check(_lib.sx_graph_grid(ctx, rows, cols, seed, wmin, wmax, ctypes.byref(h)), "sx_graph_grid")
+    return h
+
+
+def sx_graph_download(g, row_ptr, col, w=None):
+    """Fill caller arrays (numpy host or torch CUDA): row_ptr u64[n+1], col u32[m], w u32[m] or None."""
+    _check(_lib.sx_graph_download(g, _ptr(row_ptr), _ptr(col), _ptr(w)), "sx_graph_download")
+
+
 def sx_graph_free(g) -> None:
     _lib.sx_graph_free(g)
 
@@ -281,6 +305,16 @@ class Context:
         _check(_lib.sx_graph_upload(self.h, ctypes.byref(d), ctypes.byref(h)), "sx_graph_upload")
         return Graph(self, h, d.n)
 
+    def rmat(self, scale: int, edgefactor: int = 16, seed: int = 1, wmin: int = 0, wmax: int = 0,
+             relabel: bool = True) -> "Graph":
+        """sx_graph_rmat: the simgen R-MAT graph built on the device (bit-identical to simgen.rmat)."""
+        h = sx_graph_rmat(self.h, scale, edgefactor, seed, wmin, wmax, 0 if relabel else SX_GEN_NO_RELABEL)
+        return Graph(self, h, 1 << scale)
+
+    def grid(self, rows: int, cols: int, seed: int = 1, wmin: int = 1, wmax: int = 255) -> "Graph":
+        """sx_graph_grid: the simgen rows x cols grid built on the device."""
+        return Graph(self, sx_graph_grid(self.h, rows, cols, seed, wmin, wmax), rows * cols)
+
     def upload(self, csr) -> "Graph":
         """Upload a simgen.CSR-like object (fields n,row_ptr,col,w,directed,csc_*)."""
         h = sx_graph_upload(self.h, csr.n, csr.row_ptr, csr.col, csr.w,
@@ -303,6 +337,19 @@ class Context:
 class Graph:
     def __init__(self, ctx: Context, h, n: int):
         self.ctx, self.h, self.n = ctx, h, n
+
+    def info(self):
+        """(n, m, v_begin, v_end)"""
+        return sx_graph_info(self.h)
+
+    def download(self, weights: bool = True):
+        """Host copy of the CSR: (row_ptr u64[n+1], col u32[m], w u32[m] or None)."""
+        n, m, _, _ = sx_graph_info(self.h)
+        rp = np.empty(n + 1, np.uint64)
+        col = np.empty(m, np.uint32)
+        w = np.empty(m, np.uint32) if weights else None
+        sx_graph_download(self.h, rp, col, w)
+        return rp, col, w
 
     def free(self):
         if self.h:

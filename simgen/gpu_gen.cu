@@ -3,7 +3,9 @@
 // (seed, i) through Philox-4x32-10 with the counters of simgen.c, so the CSR
 // built here is bit-identical to simgen.rmat(...) (tests/test_gpu_gen.py).
 // Used to build the scale-24..27 bench graphs (and each rank's 1D slice) in
-// seconds instead of minutes.
+// seconds instead of minutes, and (compiled into libsimdx with SIMGEN_EMBED,
+// csrc/gen.cu) behind sx_graph_rmat / sx_graph_grid.  The grid generator is
+// simgen.c's simgen_grid_csr, bit-identical (tests/test_gpu_gen.py).
 //
 // Pipeline (device): count the slice's directed edges -> emit (src_local<<32 | dst,
 // weight) -> stable radix sort by weight, then by key (rows ordered by (col, w)
@@ -127,6 +129,54 @@ __global__ void k_narrow(const uint32_t* wv, uint64_t m, uint8_t* w8) {
         w8[e] = (uint8_t)wv[e];
 }
 
+// rows x cols 4-neighbour grid of simgen.c (simgen_grid_csr): vertex id r*cols+c,
+// neighbours in increasing id (up, left, right, down), weight of undirected edge
+// id e = wmin + Philox(e, 0x6121, 0x7A11)[0] % wspan.  row_ptr in closed form:
+// the degree sum of all vertices before v.
+struct Grid {
+    uint32_t rows, cols;
+    uint64_t seed;
+    uint32_t wmin, wspan;
+    int wbytes;
+    uint64_t v_lo, v_hi;
+};
+
+__device__ __forceinline__ uint64_t grid_rp(const Grid& g, uint64_t v) {  // sum_{u < v} deg(u)
+    const uint64_t r = v / g.cols, c = v % g.cols, C = g.cols, R = g.rows;
+    uint64_t s = r * 2 * (C - 1) + (c ? c - 1 : 0) + c;          // horizontal: left + right neighbours
+    s += (r ? (r - 1) * C : 0) + (r ? c : 0);                      // vertical: up neighbours
+    s += (r < R - 1 ? r * C : (R - 1) * C) + (r + 1 < R ? c : 0);  // vertical: down neighbours
+    return s;
+}
+
+__global__ void k_grid(Grid g, uint64_t* rp, uint32_t* col, void* w) {
+    const uint64_t nl = g.v_hi - g.v_lo, C = g.cols;
+    const uint64_t H = (uint64_t)g.rows * (C ? C - 1 : 0), base = grid_rp(g, g.v_lo);
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k <= nl; k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t v = g.v_lo + k;
+        const uint64_t p = grid_rp(g, v) - base;
+        rp[k] = p;
+        if (k == nl) continue;
+        const uint32_t r = (uint32_t)(v / C), c = (uint32_t)(v % C);
+        uint64_t nb[4], eid[4];
+        int d = 0;
+        if (r > 0) { nb[d] = v - C; eid[d] = H + (uint64_t)(r - 1) * C + c; ++d; }
+        if (c > 0) { nb[d] = v - 1; eid[d] = (uint64_t)r * (C - 1) + (c - 1); ++d; }
+        if (c + 1 < C) { nb[d] = v + 1; eid[d] = (uint64_t)r * (C - 1) + c; ++d; }
+        if (r + 1 < g.rows) { nb[d] = v + C; eid[d] = H + (uint64_t)r * C + c; ++d; }
+        for (int j = 0; j < d; ++j) {
+            col[p + j] = (uint32_t)nb[j];
+            if (g.wbytes) {
+                uint32_t o[4];
+                philox((uint32_t)eid[j], (uint32_t)(eid[j] >> 32), 0x6121u, 0x7A11u, g.seed, o);
+                const uint32_t x = g.wmin + (o[0] % g.wspan);
+                if (g.wbytes == 1) ((uint8_t*)w)[p + j] = (uint8_t)x;
+                else ((uint32_t*)w)[p + j] = x;
+            }
+        }
+    }
+}
+
 int bits_for(uint64_t x) {
     int b = 0;
     while (b < 64 && (x >> b)) ++b;
@@ -144,12 +194,24 @@ int bits_for(uint64_t x) {
         }                                                                                \
     } while (0)
 
-extern "C" {
+// Exported C functions; with SIMGEN_EMBED (libsimdx's csrc/gen.cu) they are
+// internal to the including translation unit instead.
+#ifdef SIMGEN_EMBED
+#define SG_BEGIN namespace simgen_embed {
+#define SG_END }
+#define SG_FN static
+#else
+#define SG_BEGIN extern "C" {
+#define SG_END }
+#define SG_FN
+#endif
+
+SG_BEGIN
 
 // Build rows [v_lo, v_hi) of the undirected R-MAT graph of simgen.c on the current
 // device.  Outputs are cudaMalloc'ed (free with simgen_gpu_free): row_ptr u64[nl+1],
 // col u32[m], w u8[m] (wmax <= 255) or u32[m], or NULL when unweighted.  Returns 0.
-int simgen_gpu_rmat_csr(int scale, int ef, uint64_t seed, uint32_t wmin, uint32_t wmax, int relabel, uint64_t v_lo,
+SG_FN int simgen_gpu_rmat_csr(int scale, int ef, uint64_t seed, uint32_t wmin, uint32_t wmax, int relabel, uint64_t v_lo,
                         uint64_t v_hi, void* stream, uint64_t** row_ptr, uint32_t** col, void** w, uint64_t* m_out,
                         int* wbytes_out) {
     cudaStream_t s = (cudaStream_t)stream;
@@ -203,17 +265,17 @@ int simgen_gpu_rmat_csr(int scale, int ef, uint64_t seed, uint32_t wmin, uint32_
     uint64_t* rp = nullptr;
     uint32_t* c = nullptr;
     CK(cudaMalloc(&rp, (nl + 1) * 8));
-    CK(cudaMalloc(&c, (m ? m : 1) * 4));
+    CK(cudaMalloc(&c, m * 4 + 16));  // +16 B: consumers read whole aligned 16-B groups
     k_rowptr<<<grid, block, 0, s>>>(key, m, nl, rp, c);
     void* wout = nullptr;
     int wbytes = 0;
     if (g.weighted) {
         if (wmax <= 255) {
-            CK(cudaMalloc(&wout, m ? m : 1));
+            CK(cudaMalloc(&wout, m + 16));
             k_narrow<<<grid, block, 0, s>>>(wv, m, (uint8_t*)wout);
             wbytes = 1;
         } else {
-            CK(cudaMalloc(&wout, (m ? m : 1) * 4));
+            CK(cudaMalloc(&wout, m * 4 + 16));
             CK(cudaMemcpyAsync(wout, wv, m * 4, cudaMemcpyDeviceToDevice, s));
             wbytes = 4;
         }
@@ -234,12 +296,58 @@ int simgen_gpu_rmat_csr(int scale, int ef, uint64_t seed, uint32_t wmin, uint32_
     return 0;
 }
 
-void simgen_gpu_free(void* p) {
+SG_FN void simgen_gpu_free(void* p) {
     if (p) cudaFree(p);
 }
 
-int simgen_gpu_to_host(void* dst, const void* src, uint64_t bytes) {
+SG_FN int simgen_gpu_to_host(void* dst, const void* src, uint64_t bytes) {
     return cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : -1;
 }
 
-}  // extern "C"
+// Rows [v_lo, v_hi) of simgen.c's rows x cols grid on the current device (see
+// k_grid).  Outputs cudaMalloc'ed like simgen_gpu_rmat_csr.  Returns 0.
+SG_FN int simgen_gpu_grid_csr(uint32_t rows, uint32_t cols, uint64_t seed, uint32_t wmin, uint32_t wmax,
+                              uint64_t v_lo, uint64_t v_hi, void* stream, uint64_t** row_ptr, uint32_t** col,
+                              void** w, uint64_t* m_out, int* wbytes_out) {
+    cudaStream_t s = (cudaStream_t)stream;
+    Grid g;
+    g.rows = rows;
+    g.cols = cols;
+    g.seed = seed;
+    g.wmin = wmin;
+    g.wspan = wmax >= wmin ? wmax - wmin + 1u : 1u;
+    g.wbytes = (wmin == 0 && wmax == 0) ? 0 : (wmax <= 255 ? 1 : 4);
+    g.v_lo = v_lo;
+    g.v_hi = v_hi;
+    const uint64_t nl = v_hi - v_lo;
+    // m from the closed form (host copy of grid_rp)
+    auto rp_host = [&](uint64_t v) -> uint64_t {
+        const uint64_t r = v / cols, c = v % cols, C = cols, R = rows;
+        uint64_t x = r * 2 * (C - 1) + (c ? c - 1 : 0) + c;
+        x += (r ? (r - 1) * C : 0) + (r ? c : 0);
+        x += (r < R - 1 ? r * C : (R - 1) * C) + (r + 1 < R ? c : 0);
+        return x;
+    };
+    const uint64_t m = (rows && cols) ? rp_host(v_hi) - rp_host(v_lo) : 0;
+    uint64_t* rp = nullptr;
+    uint32_t* c = nullptr;
+    void* wout = nullptr;
+    CK(cudaMalloc(&rp, (nl + 1) * 8));
+    CK(cudaMalloc(&c, m * 4 + 16));
+    if (g.wbytes) CK(cudaMalloc(&wout, m * g.wbytes + 16));
+    int dev = 0, sms = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (rows && cols) k_grid<<<sms * 8, 256, 0, s>>>(g, rp, c, wout);
+    else CK(cudaMemsetAsync(rp, 0, (nl + 1) * 8, s));
+    CK(cudaStreamSynchronize(s));
+    CK(cudaGetLastError());
+    *row_ptr = rp;
+    *col = c;
+    *w = wout;
+    *m_out = m;
+    *wbytes_out = g.wbytes;
+    return 0;
+}
+
+SG_END

@@ -60,3 +60,76 @@ def test_upload_device_graph_and_dist_slices():
         D.free()
         for s in slices:
             s.free()
+
+
+def _ctx():
+    import torch
+    from paper_1812_04070_b200 import simdx
+    torch.cuda.set_device(0)
+    return simdx, simdx.Context(0, torch.cuda.current_stream().cuda_stream)
+
+
+@pytest.mark.parametrize("scale,wmin,wmax,relabel", [(11, 1, 255, True), (12, 0, 0, True), (10, 1, 1000, True),
+                                                     (9, 1, 255, False)])
+def test_sx_graph_rmat_is_the_simgen_graph(scale, wmin, wmax, relabel):
+    """sx_graph_rmat builds simgen.rmat's CSR on the device; sx_graph_download returns it."""
+    simdx, ctx = _ctx()
+    with ctx:
+        cpu = simgen.rmat(scale, 16, 5, wmin, wmax, relabel_ids=relabel)
+        G = ctx.rmat(scale, 16, 5, wmin, wmax, relabel=relabel)
+        n, m, lo, hi = G.info()
+        assert (n, m, lo, hi) == (cpu.n, cpu.m, 0, cpu.n)
+        rp, col, w = G.download(weights=bool(wmax))
+        assert np.array_equal(rp, cpu.row_ptr) and np.array_equal(col, cpu.col)
+        if wmax:
+            assert np.array_equal(w, cpu.w.astype(np.uint32))
+        else:
+            with pytest.raises(simdx.SimdxError) as e:
+                G.download(weights=True)
+            assert e.value.status == simdx.SX_E_WEIGHT
+        G.free()
+
+
+@pytest.mark.parametrize("rows,cols,wmax", [(1, 1, 255), (1, 9, 255), (7, 1, 255), (37, 53, 255), (64, 64, 0),
+                                            (5, 6, 70000)])
+def test_sx_graph_grid_is_the_simgen_grid(rows, cols, wmax):
+    simdx, ctx = _ctx()
+    with ctx:
+        wmin = 1 if wmax else 0
+        cpu = simgen.grid(rows, cols, 3, wmin, wmax)
+        G = ctx.grid(rows, cols, 3, wmin, wmax)
+        rp, col, w = G.download(weights=bool(wmax))
+        assert np.array_equal(rp, cpu.row_ptr) and np.array_equal(col, cpu.col)
+        if wmax:
+            assert np.array_equal(w, cpu.w.astype(np.uint32))
+        G.free()
+
+
+def test_generated_graphs_run_the_path():
+    """BFS on sx_graph_rmat and SSSP on sx_graph_grid agree with the oracle on the simgen graphs."""
+    import oracle
+    simdx, ctx = _ctx()
+    with ctx:
+        G = ctx.rmat(12, 16, 2, 1, 255)
+        cpu = simgen.rmat(12, 16, 2, 1, 255)
+        lv, _, _ = G.bfs(0)
+        assert np.array_equal(lv, oracle.bfs(cpu, 0))
+        G.free()
+        G = ctx.grid(40, 70, 2, 1, 255)
+        cpu = simgen.grid(40, 70, 2, 1, 255)
+        d, _, _ = G.sssp(0, 256)
+        assert np.array_equal(d, oracle.sssp(cpu, 0))
+        G.free()
+
+
+def test_generator_argument_errors():
+    simdx, ctx = _ctx()
+    with ctx:
+        for args in ((0, 16, 1, 0, 0, 0), (10, 0, 1, 0, 0, 0), (10, 16, 1, 0, 5, 0), (10, 16, 1, 9, 5, 0),
+                     (10, 16, 1, 0, 0, 8)):
+            with pytest.raises(simdx.SimdxError) as e:
+                simdx.sx_graph_rmat(ctx.h, *args)
+            assert e.value.status == simdx.SX_E_INVALID
+        with pytest.raises(simdx.SimdxError) as e:
+            simdx.sx_graph_grid(ctx.h, 70000, 70000, 1, 1, 255)
+        assert e.value.status == simdx.SX_E_INVALID
