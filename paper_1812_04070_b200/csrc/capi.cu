@@ -89,9 +89,13 @@ sx_opts resolve_opts(const sx_opts* o) {
     return r;
 }
 
-int coop_grid(sx_graph g, const void* fn) {
+int coop_grid(sx_graph g, const void* fn, int smem) {
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, BLOCK, 0) != cudaSuccess) {
+    if (smem > 0 && cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, BLOCK, smem) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
@@ -132,11 +136,11 @@ Sched make_sched(const sx_graph g, const sx_opts& o) {
     return s;
 }
 
-sx_status coop_launch(sx_graph g, const void* fn, void** args, int* grid_out) {
-    const int grid = coop_grid(g, fn);
+sx_status coop_launch(sx_graph g, const void* fn, void** args, int* grid_out, int smem) {
+    const int grid = coop_grid(g, fn, smem);
     if (grid <= 0) return fail(SX_E_BARRIER, "persistent kernel cannot be co-resident (occupancy 0)");
     if (grid_out) *grid_out = grid;
-    cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BLOCK), args, 0, g->ctx->stream);
+    cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(BLOCK), args, (size_t)smem, g->ctx->stream);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return cuda_fail(e, "cudaLaunchCooperativeKernel");
@@ -159,14 +163,14 @@ sx_status Run::begin() {
     return SX_OK;
 }
 
-sx_status Run::launch(const void* fn, void** args, bool pull) {
+sx_status Run::launch(const void* fn, void** args, bool pull, int smem) {
     sx_ctx c = g->ctx;
     if (npending == EV_POOL) {
         sx_status rc = sync();
         if (rc != SX_OK) return rc;
     }
     SX_CU(cudaEventRecord(c->evp[2 * npending], c->stream));
-    sx_status rc = coop_launch(g, fn, args, nullptr);
+    sx_status rc = coop_launch(g, fn, args, nullptr, smem);
     if (rc != SX_OK) return rc;
     SX_CU(cudaEventRecord(c->evp[2 * npending + 1], c->stream));
     pend_pull[npending++] = pull;

@@ -914,7 +914,17 @@ __device__ __forceinline__ double seq_sum(const uint32_t* __restrict__ col, uint
 // the whole GPU shares them, small ones last so they fill the tail.
 template <class VFn>
 __device__ __forceinline__ void for_tasks(const uint32_t* lists, const Sched& s, const uint32_t (&cnt)[NCLS], VFn&& vf) {
-    for (uint32_t i = 0; i < cnt[3]; ++i) vf(task_at(lists, s, 3, i), gtid(), gthreads(), 3u);
+    // huge: the CTAs are split into cnt[3] equal groups, one per task, so the
+    // tasks run side by side (one task at a time over the whole grid left a
+    // dependent row_ptr -> col -> update chain per task exposed: 3.4 us each)
+    if (cnt[3] >= gridDim.x) {
+        for (uint32_t i = blockIdx.x; i < cnt[3]; i += gridDim.x) vf(task_at(lists, s, 3, i), (uint64_t)threadIdx.x, (uint64_t)BLOCK, 3u);
+    } else if (cnt[3] > 0) {
+        const uint64_t T = cnt[3], G = gridDim.x;
+        const uint64_t i = (uint64_t)blockIdx.x * T / G;
+        const uint64_t g0 = (i * G + T - 1) / T, g1 = ((i + 1) * G + T - 1) / T;
+        vf(task_at(lists, s, 3, (uint32_t)i), (blockIdx.x - g0) * BLOCK + threadIdx.x, (g1 - g0) * BLOCK, 3u);
+    }
     for (uint32_t i = blockIdx.x; i < cnt[2]; i += gridDim.x)
         vf(task_at(lists, s, 2, i), (uint64_t)threadIdx.x, (uint64_t)BLOCK, 2u);
     // CTA-major spreading: consecutive warp tasks / 32-task chunks go to different

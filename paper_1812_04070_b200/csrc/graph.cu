@@ -214,9 +214,11 @@ void sx_graph_free(sx_graph g) {
     for (auto* p : g->st) cudaFree(p);
     cudaFree(g->hacc);
     cudaFree(g->dstate);
-    cudaFree(g->loff);
-    cudaFree(g->scratch64);
     cudaFree(g->hub);
+    cudaFree(g->pp_hcol);
+    cudaFree(g->pp_rs);
+    cudaFree(g->pp_hubs);
+    cudaFree(g->pp_tile_seg);
     delete g;
 }
 

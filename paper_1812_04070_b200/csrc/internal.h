@@ -45,11 +45,16 @@ struct sx_graph_s {
     sx::TraceRec* trace = nullptr;
     uint32_t trace_cap = 0;
     uint32_t* st[4] = {nullptr, nullptr, nullptr, nullptr};  // 4N-byte state arrays
-    double* hacc = nullptr;       // n doubles, pull-all huge accumulators (lazy)
+    double* hacc = nullptr;       // n+1 doubles, pull-all split-row partial sums (lazy)
     double* dstate = nullptr;     // 2n doubles, BP beliefs (lazy)
-    uint64_t* loff = nullptr;     // n+1 prefix sums, pull-all big-list stream (lazy)
-    uint64_t* scratch64 = nullptr; // MAX_GRID u64 scan scratch (lazy)
     uint32_t* hub = nullptr;      // n entries, BFS hub-first probe table (lazy)
+    // tiled pull-all plan (lazy, pull_all.cu)
+    uint32_t* pp_hcol = nullptr;  // encoded in-edge sources (padded)
+    uint32_t* pp_rs = nullptr;    // row-start bitmap over in-edges
+    uint32_t* pp_hubs = nullptr;  // hub ids by slot
+    uint32_t* pp_tile_seg = nullptr;
+    uint32_t pp_K = 0;
+    uint64_t pp_ntiles = 0;
 };
 
 namespace sxh {
@@ -71,8 +76,8 @@ sx_opts resolve_opts(const sx_opts* o);
 
 // Cooperative launch of a persistent kernel with occupancy x SMs CTAs (Eq. 1
 // generalised).  Returns SX_E_BARRIER when co-residency is impossible.
-sx_status coop_launch(sx_graph g, const void* fn, void** args, int* grid_out);
-int coop_grid(sx_graph g, const void* fn);
+sx_status coop_launch(sx_graph g, const void* fn, void** args, int* grid_out, int smem = 0);
+int coop_grid(sx_graph g, const void* fn, int smem = 0);
 
 // Device counters of one direction (deltas of the control block's st_* fields).
 struct Counters {
@@ -92,7 +97,7 @@ struct Run {
     bool pend_pull[EV_POOL] = {};
     sx_status begin();
     // Enqueue one persistent kernel (timed with an event pair); no host sync.
-    sx_status launch(const void* fn, void** args, bool pull);
+    sx_status launch(const void* fn, void** args, bool pull, int smem = 0);
     // Same for a non-cooperative launch with an explicit shape (e.g. one cluster).
     sx_status launch_plain(const void* fn, void** args, int grid, int block, bool pull);
     // Read back the control block, accumulate the pending launches' times, check errors.

@@ -24,8 +24,19 @@ struct KcoreP {
     Sched s;
     uint32_t* res;   // residual degree
     uint32_t* core;  // coreness, INF while alive
+    uint32_t* ab;    // alive bitmap (bit v set while core[v] = INF): n/8 bytes, L2-resident
     uint32_t kfix;   // 0 = decomposition
 };
+
+__device__ __forceinline__ bool is_alive(const uint32_t* ab, uint32_t v) { return (ab[v >> 5] >> (v & 31)) & 1u; }
+
+__global__ void k_alive_init(uint32_t* ab, uint64_t n, uint64_t nwords) {
+    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords; w += T) {
+        const uint64_t v0 = w << 5;
+        ab[w] = v0 + 32 <= n ? FULL : v0 >= n ? 0u : (1u << (uint32_t)(n - v0)) - 1u;
+    }
+}
 
 __global__ void kcore_init(KcoreP p) {
     Ctl* c = p.s.ctl;
@@ -45,11 +56,21 @@ __global__ void k_copy_deg(const uint32_t* deg, uint64_t n, uint32_t* res) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += T) res[i] = deg[i];
 }
 
-struct LevelPred {
-    const uint32_t* core;
+// Ballot-filter source of a level start: the alive vertices with residual <= k.
+// Word wi = alive word wi restricted to those bits (dead words cost one load).
+struct LevelWords {
+    const uint32_t* ab;
     const uint32_t* res;
     uint32_t k;
-    __device__ __forceinline__ bool operator()(uint64_t v) const { return core[v] == INF && res[v] <= k; }
+    __device__ __forceinline__ uint32_t word(uint64_t wi) const {
+        uint32_t w = ab[wi], m = 0;
+        for (uint32_t x = w; x;) {
+            const int b = __ffs(x) - 1;
+            x &= x - 1;
+            if (res[(wi << 5) + b] <= k) m |= 1u << b;
+        }
+        return m;
+    }
 };
 
 __global__ void __launch_bounds__(BLOCK, 4) kcore_push(KcoreP p) {
@@ -82,10 +103,13 @@ __global__ void __launch_bounds__(BLOCK, 4) kcore_push(KcoreP p) {
             }
             uint32_t mn = INF;
             uint64_t alive = 0;
-            for (uint64_t v = gtid(); v < n; v += gthreads()) {
-                if (p.core[v] == INF) {
-                    mn = min(mn, p.res[v]);
-                    ++alive;
+            for (uint64_t wi = gtid(); wi < p.s.nwords; wi += gthreads()) {
+                uint32_t w = p.ab[wi];
+                alive += __popc(w);
+                while (w) {
+                    const int b = __ffs(w) - 1;
+                    w &= w - 1;
+                    mn = min(mn, p.res[(wi << 5) + b]);
                 }
             }
             mn = block_min(mn);
@@ -99,11 +123,11 @@ __global__ void __launch_bounds__(BLOCK, 4) kcore_push(KcoreP p) {
                 if (mn != INF) atomicMin(&sl.minv, mn);
                 if (alive) atomicAdd(&sl.alive, (unsigned int)alive);
             }
-            st.scanned += n;
             if (!grid_sync(c)) return;
             LineSum ls;
             read_line(nx, ls);
             mn = ls.minv;
+            if (lead()) st.scanned += 3 * ls.alive;  // residual reads: the min scan + the ballot filter's two passes
             if (ls.alive == 0) {
                 done = 1;
                 break;
@@ -120,14 +144,16 @@ __global__ void __launch_bounds__(BLOCK, 4) kcore_push(KcoreP p) {
             level_started = true;
             // ---- ballot filter selects the level's seeds; their coreness is k
             ++st.ballot;
-            st.scanned += n;
-            BallotWords<LevelPred> src{LevelPred{p.core, p.res, k}, n};
-            if (!ballot_filter(src, p.s, BallotOut{p.s.lists[it & 1], p.s.cstride, p.g.dout}, cnt,
-                               [&](uint32_t v, uint32_t) { p.core[v] = k; }))
+            // the thread owning word v >> 5 in the write pass clears the seeds' alive bits
+            if (!ballot_filter(LevelWords{p.ab, p.res, k}, p.s, BallotOut{p.s.lists[it & 1], p.s.cstride, p.g.dout}, cnt,
+                               [&](uint32_t v, uint32_t) {
+                                   p.core[v] = k;
+                                   p.ab[v >> 5] &= ~(1u << (v & 31));
+                               }))
                 return;
             if (!grid_sync(c)) return;
             view_contig(cnt);
-            trace_put(p.s, it, DIR_PUSH, 1u, cnt, sum4(cnt), 0, k);
+            trace_put(p.s, it + 1, DIR_PUSH, 1u, cnt, sum4(cnt), 0, k);  // level start (seeds)
         }
         // ---- one sub-round: removals push -1 to alive neighbours
         maybe_reset_line(&c->line[(it + 2) % 3]);
@@ -153,14 +179,24 @@ __global__ void __launch_bounds__(BLOCK, 4) kcore_push(KcoreP p) {
                 }
                 const bool can_chain = size == 1 && depth < p.s.local_chain;
                 uint32_t next = INF;
-                for_edges(p.g.ci, beg, end, rank, size, [&](uint64_t, uint32_t u) {
-                    ++edges;
-                    if (p.core[u] != INF) return;
-                    const uint32_t old = atomicSub(p.res + u, 1u);
-                    if (old == kk + 1) {
-                        p.core[u] = kk;
-                        if (can_chain && next == INF) next = u;
-                        else record(u);
+                // four edges per step: alive words, then the residual decrements, then the
+                // crossing tests, each issued together
+                for_edges_b(p.g.ci, beg, end, rank, size, [&](const uint32_t (&u)[4], uint32_t kn) {
+                    edges += kn;
+                    uint32_t aw[4], old[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) aw[j] = j < (int)kn ? p.ab[u[j] >> 5] : 0u;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        old[j] = (j < (int)kn && ((aw[j] >> (u[j] & 31)) & 1u)) ? atomicSub(p.res + u[j], 1u) : 0u;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if (j < (int)kn && old[j] == kk + 1) {
+                            p.core[u[j]] = kk;
+                            atomicAnd(p.ab + (u[j] >> 5), ~(1u << (u[j] & 31)));
+                            if (can_chain && next == INF) next = u[j];
+                            else record(u[j]);
+                        }
                     }
                 });
                 if (next == INF) break;
@@ -183,7 +219,6 @@ __global__ void __launch_bounds__(BLOCK, 4) kcore_push(KcoreP p) {
         trace_put(p.s, it, DIR_PUSH, overflow ? 1u : 0u, ls.cnt, nf, 0, k);
         if (nf > 0 && overflow) {
             ++st.ballot;
-            st.scanned += p.s.nwords * 32;
             if (!ballot_filter(BitmapWords{nbm}, p.s, BallotOut{p.s.lists[it & 1], p.s.cstride, p.g.dout}, cnt)) return;
             if (!grid_sync(c)) return;
             view_contig(cnt);
@@ -221,10 +256,12 @@ __global__ void k_kcore_out(const uint32_t* core, uint64_t n, uint32_t kfix, uin
 using namespace sx;
 
 // Algorithmic bytes: per list entry 4 B list + 16 B row_ptr pair;
-// per edge 4 B col + 4 B core(u) + 4 B residual RMW; level scans 8 B (core +
-// residual) per scanned vertex; per iteration one bitmap clear (n/8).
+// per edge 4 B col + 4 B residual RMW (the alive test reads an n/8 bitmap, once
+// per pass); level starts: 4 B residual per alive vertex per pass (scanned) and
+// the alive bitmap (n/8) per pass, 3 passes; per iteration one bitmap clear (n/8).
 static double kcore_bytes(const sx_graph g, const sxh::Counters& c) {
-    return 20.0 * c.entries + 12.0 * c.edges + 8.0 * c.scanned + c.iters * (double)g->n / 8.0;
+    const double bm = (double)g->n / 8.0;
+    return 20.0 * c.entries + 8.0 * c.edges + 4.0 * c.scanned + 3.0 * c.ballot * bm + c.iters * bm * 2.0;
 }
 
 extern "C" sx_status sx_kcore(sx_graph g, uint32_t k, const sx_opts* opts, uint32_t* core_out, sx_stats* stats) {
@@ -241,11 +278,13 @@ extern "C" sx_status sx_kcore(sx_graph g, uint32_t k, const sx_opts* opts, uint3
     p.s = sxh::make_sched(g, run.o);
     p.res = g->st[0];
     p.core = g->st[1];
+    p.ab = g->aux_bm;
     p.kfix = k;
     SX_CU(cudaMemsetAsync(p.core, 0xFF, g->n * 4, s));
     for (int i = 0; i < 3; ++i) SX_CU(cudaMemsetAsync(p.s.bm[i], 0, g->nwords * 4, s));
     const int eg = 4 * g->ctx->prop.multiProcessorCount;
     k_copy_deg<<<eg, 256, 0, s>>>(g->dout, g->n, p.res);
+    k_alive_init<<<eg, 256, 0, s>>>(p.ab, g->n, g->nwords);
     kcore_init<<<1, 32, 0, s>>>(p);
     SX_CU(cudaGetLastError());
     void* args[] = {&p};

@@ -14,6 +14,9 @@
 //       where a thread's slice ends inside a row, then the owner applies.
 //   Apply   : a single owner writes M_u (atomic-free), Jacobi double
 //             buffering between iterations; fp64 accumulation, fp32 state (BP: fp64).
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
 #include <cmath>
 
 #include "internal.h"
@@ -21,7 +24,13 @@
 namespace sx {
 
 // ---------------------------------------------------------------- operators
+// Each operator splits the edge term into the source value val(v) (what the hub
+// cache holds) and term(e, val) (combined with the edge weight).
 struct PrOp {  // r(u) = (1-d)/N + d (sum_v r(v)/outdeg(v) + D/N)
+    using HubT = float;
+    using TermT = float;     // lane-local partial sums of <= 8 terms in fp32, fp64 from the warp scan on
+    using AuxT = uint32_t;   // out-degree of the destination
+    static constexpr bool kStaticHub = false;
     float* contrib[2];
     float* out;
     const uint32_t* dout;
@@ -30,32 +39,48 @@ struct PrOp {  // r(u) = (1-d)/N + d (sum_v r(v)/outdeg(v) + D/N)
     uint32_t cur;
     double D;
     bool last;
-    __device__ __forceinline__ double edge(const DevGraph&, uint64_t, uint32_t v) const { return (double)contrib[cur][v]; }
+    __device__ __forceinline__ HubT val(uint32_t v) const { return contrib[cur][v]; }
+    __device__ __forceinline__ const HubT* src() const { return contrib[cur]; }
+    __device__ __forceinline__ TermT term(const DevGraph&, uint64_t, HubT x) const { return x; }
+    __device__ __forceinline__ AuxT aux(uint32_t u) const { return dout[u]; }
     __device__ __forceinline__ void init(uint64_t v, double& dpart) const {
         const uint32_t dv = dout[v];
         contrib[0][v] = dv ? (float)(invN / (double)dv) : 0.f;
         if (dv == 0) dpart += invN;
     }
-    __device__ __forceinline__ void apply(uint32_t u, double s, double& dpart) const {
+    bool directed;
+    __device__ __forceinline__ bool empty_each_iter() const { return directed; }
+    // symmetric graph: an empty row is dangling (out-degree 0); its rank is the
+    // same for every such row, so their dangling mass is count x rank
+    __device__ __forceinline__ double empty_dangling(uint32_t ne) const { return (double)ne * ((1.0 - d) * invN + d * D * invN); }
+    __device__ __forceinline__ void apply(uint32_t u, double s, AuxT du, double& dpart) const {
         const double r = (1.0 - d) * invN + d * (s + D * invN);
         if (last) out[u] = (float)r;
-        const uint32_t du = dout[u];
         contrib[cur ^ 1][u] = du ? (float)(r / (double)du) : 0.f;
         if (du == 0) dpart += r;
     }
 };
 
 struct SpmvOp {  // y(u) = sum_v w(v,u) x(v)
+    using HubT = float;
+    using TermT = float;
+    using AuxT = uint32_t;
+    static constexpr bool kStaticHub = true;  // x does not change between iterations
     const float* x;
     float* out;
     uint32_t cur;
     double D;
     bool last;
-    __device__ __forceinline__ double edge(const DevGraph& g, uint64_t e, uint32_t v) const {
-        return (double)edge_w(g.iw8, g.iw32, e) * (double)x[v];
+    __device__ __forceinline__ HubT val(uint32_t v) const { return x[v]; }
+    __device__ __forceinline__ const HubT* src() const { return x; }
+    __device__ __forceinline__ TermT term(const DevGraph& g, uint64_t e, HubT xv) const {
+        return (float)edge_w(g.iw8, g.iw32, e) * xv;
     }
+    __device__ __forceinline__ AuxT aux(uint32_t) const { return 0; }
+    __device__ __forceinline__ bool empty_each_iter() const { return false; }  // y = 0
+    __device__ __forceinline__ double empty_dangling(uint32_t) const { return 0.0; }
     __device__ __forceinline__ void init(uint64_t, double&) const {}
-    __device__ __forceinline__ void apply(uint32_t u, double s, double&) const { out[u] = (float)s; }
+    __device__ __forceinline__ void apply(uint32_t u, double s, AuxT, double&) const { out[u] = (float)s; }
 };
 
 // BP is computed in fp64 end to end (beliefs, couplings, messages), fp32 out.
@@ -63,16 +88,25 @@ struct SpmvOp {  // y(u) = sum_v w(v,u) x(v)
 // the coupling c alone) to ~1e-4 after 10 steps on R-MAT, so fp32 state cannot
 // meet the 1e-5 conditioned tolerance.
 struct BpOp {  // l(u) = logit(p_u) + sum_v log((c b + (1-c)(1-b)) / (c(1-b) + (1-c) b)), b = sigmoid(l(v))
+    using HubT = double;
+    using TermT = double;
+    using AuxT = float;      // prior of the destination
+    static constexpr bool kStaticHub = false;
     double* b[2];
     const float* prior;
     float* out;
     uint32_t cur;
     double D;
     bool last;
-    __device__ __forceinline__ double edge(const DevGraph& g, uint64_t e, uint32_t v) const {
+    __device__ __forceinline__ HubT val(uint32_t v) const { return b[cur][v]; }
+    __device__ __forceinline__ const HubT* src() const { return b[cur]; }
+    __device__ __forceinline__ AuxT aux(uint32_t u) const { return prior[u]; }
+    // l = logit(p): written to b[1] in the first iteration (b[0] by init), out in the last
+    __device__ __forceinline__ bool empty_each_iter() const { return false; }
+    __device__ __forceinline__ double empty_dangling(uint32_t) const { return 0.0; }
+    __device__ __forceinline__ TermT term(const DevGraph& g, uint64_t e, HubT bv) const {
         const double wt = (g.iw8 || g.iw32) ? (double)edge_w(g.iw8, g.iw32, e) : 255.0;
         const double c = 0.25 + 0.5 * (wt - 1.0) / 254.0;
-        const double bv = b[cur][v];
         const double num = c * bv + (1.0 - c) * (1.0 - bv);
         const double den = c * (1.0 - bv) + (1.0 - c) * bv;
         return log(num / den);
@@ -82,72 +116,133 @@ struct BpOp {  // l(u) = logit(p_u) + sum_v log((c b + (1-c)(1-b)) / (c(1-b) + (
         const double l = log(p / (1.0 - p));
         b[0][v] = 1.0 / (1.0 + exp(-l));
     }
-    __device__ __forceinline__ void apply(uint32_t u, double s, double&) const {
-        const double p = (double)prior[u];
+    __device__ __forceinline__ void apply(uint32_t u, double s, AuxT pu, double&) const {
+        const double p = (double)pu;
         const double l = log(p / (1.0 - p)) + s;
         if (last) out[u] = (float)l;
         b[cur ^ 1][u] = 1.0 / (1.0 + exp(-l));
     }
 };
 
+// ---------------------------------------------------------------- schedule
+// The all-active pull as an edge-balanced stream (B200 design; DESIGN.md
+// "Pull-all").  The in-edge array is cut into warp tiles of PT = 32 x PV
+// consecutive edges; lane l of a warp owns PV consecutive edges, loaded with
+// two 128-bit loads.  Per graph (once, graph residency a1):
+//   hcol  : the in-edge sources, the K most-gathered sources (largest out-degree)
+//           re-encoded as HUBBIT | slot — their values are read from a copy in
+//           shared memory instead of L2 (a software cache of the hubs);
+//   rs    : bitmap over in-edges, bit e set iff e is the first edge of a row
+//           (and bit E, a sentinel row start).
+// Per run, iteration 1 (task management: ballot filter in exactly the
+// first iteration): the ballot filter lists the active rows (in-degree > 0)
+// in vertex order (nz) and the rows that need the second phase (sp: empty rows
+// and rows that cross a tile boundary); tile_seg[t] = index in nz of the row
+// holding tile t's first edge.
+// Per iteration:
+//   A: every warp streams tiles; each lane sums its runs of equal destination
+//      (row starts from rs), a warp segmented scan carries partial runs across
+//      lanes; a row that starts and ends inside the tile is applied at once by
+//      the lane holding its last edge (single owner, atomic-free); the
+//      pieces of a row that crosses a tile boundary are added with fp64
+//      atomics to acc[u];
+//   -- grid barrier --
+//   B: the sp rows are applied from acc (then acc is reset to 0);
+//   -- grid barrier --  (Jacobi double buffer between iterations)
+#ifndef SX_PULL_PV
+#define SX_PULL_PV 8
+#endif
+#ifndef SX_PULL_MINB
+#define SX_PULL_MINB 3
+#endif
+constexpr int PV = SX_PULL_PV;  // edges per lane (8 or 16)
+constexpr int PT = 32 * PV;
+static_assert(PV == 8 || PV == 16, "PV");
+constexpr uint32_t HUBBIT = 0x80000000u;
+constexpr uint32_t PULL_HUBS = 12288;  // hub cache entries: 48 KB of fp32 (PR, SpMV) / 96 KB of fp64 (BP) per CTA
+
 template <class Op> struct PullP {
     DevGraph g;
     Sched s;
     Op op;
     uint32_t iters;
-    double* hacc;         // per big-list entry partial sums (fp64)
-    uint64_t* loff;       // prefix sums of in-degrees over the big list (nb + 1 entries)
-    uint64_t* scratch;    // MAX_GRID u64 scan scratch
+    const uint32_t* hcol;   // encoded in-edge sources (>= ntiles * PT entries, zero padded)
+    const uint32_t* rs;     // row-start bitmap over in-edges (bit E set)
+    const uint32_t* hubs;   // K hub vertex ids by slot
+    uint32_t K;
+    uint64_t ntiles, E;     // tiles, in-edges
+    uint32_t* tile_seg;     // ntiles entries
+    uint32_t* nz;           // active rows (in-degree > 0), ascending (+1 sentinel)
+    uint32_t* sp;           // rows applied in phase B, ascending
+    double* acc;            // n fp64 partial sums of split rows (zero between runs)
 };
 
-template <class Op> __device__ __forceinline__ double row_sum(const DevGraph& g, const Op& op, uint64_t beg, uint64_t end,
-                                                              uint64_t rank, uint64_t size) {
-    double acc = 0.0;
-    for_edges(g.ici, beg, end, rank, size, [&](uint64_t e, uint32_t v) { acc += op.edge(g, e, v); });
-    return acc;
+struct NzPred {
+    const uint32_t* din;
+    __device__ __forceinline__ bool operator()(uint64_t v) const { return __ldg(din + v) > 0; }
+};
+struct SpPred {  // empty row, or a row crossing a tile boundary
+    const uint64_t* irp;
+    __device__ __forceinline__ bool operator()(uint64_t v) const {
+        const uint64_t b = __ldg(irp + v), e = __ldg(irp + v + 1);
+        return b == e || b / PT != (e - 1) / PT;
+    }
+};
+
+// Predicated gather (plain global load; 0 when !c), so that a lane's loads are
+// issued back to back instead of one branch-guarded load at a time.
+__device__ __forceinline__ float ld_pred(const float* p, bool c) {
+    float v = 0.f;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.f32 %0, [%1];\n\t}"
+                 : "+f"(v) : "l"(p), "r"((int)c));
+    return v;
 }
-template <class Op> __device__ __forceinline__ double row_seq(const DevGraph& g, const Op& op, uint64_t beg, uint64_t end) {
-    return seq_sum(g.ici, beg, end, [&](uint64_t e, uint32_t v) { return op.edge(g, e, v); });
+__device__ __forceinline__ double ld_pred(const double* p, bool c) {
+    double v = 0.0;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.f64 %0, [%1];\n\t}"
+                 : "+d"(v) : "l"(p), "r"((int)c));
+    return v;
 }
 
-// Block-wide exclusive scan of one u64 per thread; returns the exclusive value and the block total.
-__device__ __forceinline__ uint64_t block_excl_scan_u64(uint64_t x, uint64_t& total) {
-    __shared__ uint64_t ws[WARPS];
-    uint64_t inc = x;
+// Segmented inclusive scan over the warp: a lane holding a row start does not
+// take the partial sum of the lanes before it.
+__device__ __forceinline__ double warp_seg_scan(double v, bool start) {
+    const uint32_t l = lane_id();
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        const uint64_t y = __shfl_up_sync(FULL, inc, o);
-        if ((int)lane_id() >= o) inc += y;
+        const double y = __shfl_up_sync(FULL, v, o);
+        const bool fy = __shfl_up_sync(FULL, start, o);
+        if ((int)l >= o) {
+            if (!start) v += y;
+            start |= fy;
+        }
     }
-    __syncthreads();
-    if (lane_id() == 31) ws[warp_id()] = inc;
-    __syncthreads();
-    uint64_t before = 0, tot = 0;
-#pragma unroll
-    for (int w = 0; w < WARPS; ++w) {
-        if (w < (int)warp_id()) before += ws[w];
-        tot += ws[w];
-    }
-    total = tot;
-    return before + inc - x;
+    return v;
 }
 
-// The large and huge class lists, concatenated ("big" list, nb entries).
-__device__ __forceinline__ uint32_t big_at(const uint32_t* L, uint64_t cs, uint32_t c2, uint32_t i) {
-    return i < c2 ? L[2 * cs + i] : L[3 * cs + (i - c2)];
-}
-
-template <class Op> __global__ void __launch_bounds__(BLOCK, 4) pull_all(PullP<Op> p) {
+template <class Op> __global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) pull_all(PullP<Op> p) {
+    using HubT = typename Op::HubT;
+    using TermT = typename Op::TermT;
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    HubT* s_hub = reinterpret_cast<HubT*>(s_dyn);
     Ctl* c = p.s.ctl;
     grid_begin(c);
-    const uint64_t n = p.g.n;
+    const uint64_t n = p.g.n, E = p.E;
     const uint64_t cs = p.s.cstride;
     Stats st;
+    // ---- iteration-1 task management: two ballot filters, one list each
+    Sched s1 = p.s;
+    s1.sep_small = s1.sep_large = s1.sep_huge = INF;  // one class: plain vertex-ordered lists
     uint32_t cnt[NCLS];
-    // iteration 1 task management: ballot filter over all vertices -> static class lists (in-degree)
-    if (!ballot_filter(AllWords{n}, p.s, BallotOut{p.s.lists[0], cs, p.g.din}, cnt)) return;
-    ++st.ballot;
-    st.scanned += n;
+    if (!ballot_filter(BallotWords<NzPred>{NzPred{p.g.din}, n}, s1, BallotOut{p.nz, cs, p.g.din}, cnt)) return;
+    if (!grid_sync(c)) return;
+    const uint32_t nnz = cnt[0];
+    // second list, two classes by in-degree: 0 = empty rows, 1 = rows split across tiles
+    s1.sep_small = 1;
+    if (!ballot_filter(BallotWords<SpPred>{SpPred{p.g.irp}, n}, s1, BallotOut{p.sp, cs, p.g.din}, cnt)) return;
+    const uint32_t nempty = cnt[0], nsplit = cnt[1];
+    st.ballot += 2;
+    st.scanned += 2 * n;
     {
         double dpart = 0.0;
         for (uint64_t v = gtid(); v < n; v += gthreads()) p.op.init(v, dpart);
@@ -156,54 +251,16 @@ template <class Op> __global__ void __launch_bounds__(BLOCK, 4) pull_all(PullP<O
         if (threadIdx.x == 0 && a[0] != 0.0) atomicAdd(&c->line[0].s[my_slot()].dsum, a[0]);
     }
     if (!grid_sync(c)) return;
-    const uint32_t* L = p.s.lists[0];
-    // CTA / grid granularity for the big list: one edge-balanced stream over the
-    // concatenated rows of the large and huge vertices.  loff = exclusive prefix
-    // sums of their in-degrees (grid scan, once; the lists are static).
-    const uint32_t nb = cnt[2] + cnt[3];
-    {
-        const uint32_t per = (nb + gridDim.x - 1) / gridDim.x;
-        const uint32_t i0 = min(nb, per * blockIdx.x), i1 = min(nb, i0 + per);
-        uint64_t part = 0;
-        for (uint32_t i = i0 + threadIdx.x; i < i1; i += BLOCK) part += __ldg(p.g.din + big_at(L, cs, cnt[2], i));
-        uint64_t a[1] = {part};
-        block_sum<1>(a);
-        if (threadIdx.x == 0) p.scratch[blockIdx.x] = a[0];
-        if (!grid_sync(c)) return;
-        uint64_t r[2] = {0, 0};
-        for (uint32_t b = threadIdx.x; b < gridDim.x; b += BLOCK) {
-            const uint64_t x = vload(p.scratch + b);
-            if (b < blockIdx.x) r[0] += x;
-            r[1] += x;
-        }
-        block_sum<2>(r);
-        uint64_t run = r[0];
-        for (uint32_t t0 = i0; t0 < i1; t0 += BLOCK) {
-            const uint32_t i = t0 + threadIdx.x;
-            const uint64_t d = i < i1 ? __ldg(p.g.din + big_at(L, cs, cnt[2], i)) : 0;
-            uint64_t tt;
-            const uint64_t ex = block_excl_scan_u64(d, tt);
-            if (i < i1) p.loff[i] = run + ex;
-            run += tt;
-        }
-        if (lead()) p.loff[nb] = r[1];
-        if (!grid_sync(c)) return;
+    // tile_seg from the active-row list (ends before the first iteration's barrier below)
+    for (uint64_t k = gtid(); k < nnz; k += gthreads()) {
+        const uint32_t u = p.nz[k];
+        const uint64_t b = __ldg(p.g.irp + u), e = __ldg(p.g.irp + u + 1);
+        for (uint64_t t = (b + PT - 1) / PT; t * PT < e; ++t) p.tile_seg[t] = (uint32_t)k;
     }
-    const uint64_t Eb = nb ? vload(p.loff + nb) : 0;
-    // this thread's slice [x0, x1) of the big stream and its first segment (static)
-    const uint64_t T = gthreads();
-    const uint64_t x0 = Eb * gtid() / T, x1 = Eb * (gtid() + 1) / T;
-    uint32_t seg0 = 0;
-    if (x0 < x1) {
-        uint32_t lo = 0, hi = nb;  // largest i with loff[i] <= x0
-        while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (vload(p.loff + mid) <= x0) lo = mid;
-            else hi = mid;
-        }
-        seg0 = lo;
-    }
+    if (lead()) p.nz[nnz] = INF;  // sentinel row of the sentinel start bit E
+    if (!grid_sync(c)) return;
     Op op = p.op;
+    const uint32_t lane = lane_id();
     for (uint32_t t = 0; t < p.iters; ++t) {
         maybe_reset_line(&c->line[(t + 2) % 3]);
         {
@@ -213,43 +270,146 @@ template <class Op> __global__ void __launch_bounds__(BLOCK, 4) pull_all(PullP<O
         }
         op.cur = t & 1;
         op.last = t + 1 == p.iters;
+        if (!Op::kStaticHub || t == 0) {
+            // hub cache refresh: 8 independent id -> value chains in flight per thread
+            for (uint32_t i0 = threadIdx.x; i0 < p.K; i0 += 8 * BLOCK) {
+                uint32_t hid[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) hid[j] = i0 + j * BLOCK < p.K ? __ldg(p.hubs + i0 + j * BLOCK) : 0u;
+                HubT hvv[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) hvv[j] = ld_pred(op.src() + hid[j], i0 + j * BLOCK < p.K);
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (i0 + j * BLOCK < p.K) s_hub[i0 + j * BLOCK] = hvv[j];
+            }
+            __syncthreads();
+        }
+#ifdef SX_PULL_PHASES
+        trace_put(p.s, t + 1, DIR_PULL, 7u, cnt, 0, 0, 0);  // hub cache refreshed (CTA 0)
+#endif
         double dpart = 0.0;
         uint64_t edges = 0;
-        // big list: edge-balanced slices, fp64 atomics only at segment ends
-        for (uint64_t x = x0, i = seg0; x < x1; ++i) {
-            const uint32_t u = big_at(L, cs, cnt[2], (uint32_t)i);
-            const uint64_t s0 = p.loff[i], s1 = p.loff[i + 1];
-            const uint64_t end = min(s1, x1);
-            const uint64_t base = __ldg(p.g.irp + u) - s0;
-            const double a = row_seq(p.g, op, base + x, base + end);
-            atomicAdd(p.hacc + i, a);
-            edges += end - x;
-            x = end;
-        }
-        // medium: one warp per vertex
-        for (uint64_t i = gwarp(); i < cnt[1]; i += gwarps()) {
-            const uint32_t u = L[cs + i];
-            const uint64_t beg = __ldg(p.g.irp + u), end = __ldg(p.g.irp + u + 1);
-            const double a = warp_sum(row_sum(p.g, op, beg, end, lane_id(), 32));
-            if (lane_id() == 0) {
-                op.apply(u, a, dpart);
-                edges += end - beg;
+        // ---- phase A: edge tiles (software-pipelined: the next tile's ids, row-start
+        // bits and first row are loaded while this tile's gathers are in flight)
+        uint4 nq[PV / 4];
+        uint32_t nrs = 0, nrs1 = 0, nseg = 0;
+        auto fetch = [&](uint64_t tl) {
+            if (tl < p.ntiles) {
+                const uint64_t b = tl * PT, f0 = b + lane * PV;
+#pragma unroll
+                for (int q = 0; q < PV / 4; ++q) nq[q] = __ldg(reinterpret_cast<const uint4*>(p.hcol + f0) + q);
+                nrs = __ldg(p.rs + (f0 >> 5));
+                if (lane == 31) nrs1 = __ldg(p.rs + ((b + PT) >> 5));
+                nseg = __ldg(p.tile_seg + tl);
+            }
+        };
+        fetch(gwarp());
+        for (uint64_t tile = gwarp(); tile < p.ntiles; tile += gwarps()) {
+            const uint64_t base = tile * PT, e0 = base + lane * PV;
+            uint32_t cols[PV];
+#pragma unroll
+            for (int q = 0; q < PV / 4; ++q) {
+                cols[4 * q] = nq[q].x;
+                cols[4 * q + 1] = nq[q].y;
+                cols[4 * q + 2] = nq[q].z;
+                cols[4 * q + 3] = nq[q].w;
+            }
+            const uint32_t rsw = nrs, rsw1 = nrs1, seg0 = nseg;
+            fetch(tile + gwarps());
+            // row starts at e0 .. e0+PV-1
+            const uint32_t byte = (rsw >> (uint32_t)(e0 & 31)) & ((1u << PV) - 1u);
+            uint32_t nxt = __shfl_down_sync(FULL, byte, 1) & 1u;  // start bit of e0+PV
+            if (lane == 31) nxt = rsw1 & 1u;
+            const uint32_t ends = (byte >> 1) | (nxt << (PV - 1));  // bit j: edge e0+j is the last of its row
+            const bool tile_first_start = __shfl_sync(FULL, byte, 0) & 1u;
+            // row starts strictly after the tile's first edge, counted up to each edge
+            const uint32_t mb = lane == 0 ? (byte & ~1u) : byte;
+            uint32_t ex = __popc(mb);
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(FULL, ex, o);
+                if ((int)lane >= o) ex += y;
+            }
+            ex -= __popc(mb);
+            // the lane's first two destination rows and their per-row operands, fetched
+            // while the gathers are in flight (most lanes emit at most two rows)
+            const uint32_t ra = seg0 + ex;
+            const uint32_t u0 = p.nz[ra], u1 = p.nz[ra + 1];
+            const typename Op::AuxT a0 = u0 != INF ? op.aux(u0) : typename Op::AuxT(0);
+            const typename Op::AuxT a1 = u1 != INF ? op.aux(u1) : typename Op::AuxT(0);
+            // all PV gathers issued back to back (predicated, no branches), hubs from shared memory
+            const HubT* src = op.src();
+            HubT hv[PV];
+#pragma unroll
+            for (int j = 0; j < PV; ++j)
+                hv[j] = ld_pred(src + (cols[j] & ~HUBBIT), e0 + j < E && !(cols[j] & HUBBIT));
+#pragma unroll
+            for (int j = 0; j < PV; ++j)
+                if (cols[j] & HUBBIT) hv[j] = s_hub[cols[j] & ~HUBBIT];
+            TermT x[PV];
+            TermT tail = 0;
+#pragma unroll
+            for (int j = 0; j < PV; ++j) {
+                const TermT v = e0 + j < E ? op.term(p.g, e0 + j, hv[j]) : TermT(0);
+                x[j] = v;
+                if ((byte >> j) & 1u) tail = 0;
+                tail += v;
+            }
+            const uint32_t nvalid = e0 >= E ? 0u : (E - e0 >= (uint64_t)PV ? (uint32_t)PV : (uint32_t)(E - e0));
+            edges += nvalid;
+            // carry into this lane = inclusive scan of the previous lane
+            const double incl = warp_seg_scan((double)tail, byte != 0);
+            double carry = __shfl_up_sync(FULL, incl, 1);
+            if (lane == 0 || (byte & 1u)) carry = 0.0;
+            TermT run = 0;
+#pragma unroll
+            for (int j = 0; j < PV; ++j) {
+                if ((byte >> j) & 1u) {
+                    run = 0;
+                    carry = 0.0;
+                }
+                run += x[j];
+                if ((uint32_t)j < nvalid && ((ends >> j) & 1u)) {
+                    const uint32_t k = __popc(mb & ((2u << j) - 1u));  // row offset within the lane
+                    const uint32_t ridx = ra + k;
+                    const uint32_t u = k == 0 ? u0 : k == 1 ? u1 : p.nz[ridx];
+                    if (u != INF) {
+                        const double sum = carry + (double)run;
+                        const bool complete = ridx != seg0 || tile_first_start;
+                        if (complete) op.apply(u, sum, k == 0 ? a0 : k == 1 ? a1 : op.aux(u), dpart);
+                        else atomicAdd(p.acc + u, sum);
+                    }
+                }
+            }
+            // the tile's last run continues into the next tile: its piece goes to acc
+            if (lane == 31 && !nxt && nvalid == PV) {
+                const uint32_t k = __popc(mb);
+                atomicAdd(p.acc + (k == 0 ? u0 : k == 1 ? u1 : p.nz[ra + k]), incl);
             }
         }
-        // small: one thread per vertex
-        for (uint64_t i = gtid(); i < cnt[0]; i += gthreads()) {
-            const uint32_t u = L[i];
-            const uint64_t beg = __ldg(p.g.irp + u), end = __ldg(p.g.irp + u + 1);
-            op.apply(u, row_seq(p.g, op, beg, end), dpart);
-            edges += end - beg;
+        if (!grid_sync(c)) return;
+#ifdef SX_PULL_PHASES
+        trace_put(p.s, t + 1, DIR_PULL, 8u, cnt, 0, 0, 0);  // phase A done
+#endif
+        // ---- phase B: rows split across tiles (from acc), then the empty rows
+        for (uint64_t i = gtid(); i < nsplit; i += gthreads()) {
+            const uint32_t u = p.sp[cs + i];
+            const double a = p.acc[u];
+            p.acc[u] = 0.0;
+            op.apply(u, a, op.aux(u), dpart);
         }
-        if (nb) {
-            if (!grid_sync(c)) return;
-            // owners apply the big vertices' sums
-            for (uint64_t i = gtid(); i < nb; i += gthreads()) {
-                op.apply(big_at(L, cs, cnt[2], (uint32_t)i), p.hacc[i], dpart);
-                p.hacc[i] = 0.0;
+        // An empty row's value depends on no neighbour: it is the same in every
+        // iteration (PageRank: up to the common dangling term), so it is written in
+        // the first and the last iteration only, unless the operator needs it every
+        // iteration (PageRank on a directed graph: an empty in-row can have out-edges).
+        if (t == 0 || op.last || op.empty_each_iter()) {
+            for (uint64_t i = gtid(); i < nempty; i += gthreads()) {
+                const uint32_t u = p.sp[i];
+                op.apply(u, 0.0, op.aux(u), dpart);
             }
+        } else if (lead()) {
+            dpart += op.empty_dangling(nempty);
         }
         {
             double a[1] = {dpart};
@@ -276,30 +436,104 @@ template __global__ void pull_all<PrOp>(PullP<PrOp>);
 template __global__ void pull_all<SpmvOp>(PullP<SpmvOp>);
 template __global__ void pull_all<BpOp>(PullP<BpOp>);
 
+// ---------------------------------------------------------------- per-graph plan kernels
+__global__ void k_hubslot(const uint32_t* hubs, uint32_t K, uint32_t* slot) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < K; i += gridDim.x * blockDim.x) slot[hubs[i]] = i;
+}
+__global__ void k_hcol(const uint32_t* ici, uint64_t E, uint64_t Epad, const uint32_t* slot, uint32_t* hcol) {
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < Epad; e += (uint64_t)gridDim.x * blockDim.x) {
+        if (e >= E) {
+            hcol[e] = 0;
+            continue;
+        }
+        const uint32_t v = ici[e];
+        const uint32_t s = slot ? slot[v] : INF;
+        hcol[e] = s != INF ? (HUBBIT | s) : v;
+    }
+}
+__global__ void k_rowstarts(const uint64_t* irp, uint64_t n, uint64_t E, uint32_t* rs) {
+    for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t b = irp[u];
+        if (b < irp[u + 1]) atomicOr(rs + (b >> 5), 1u << (b & 31));
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(rs + (E >> 5), 1u << (E & 31));
+}
+__global__ void k_iota(uint32_t* a, uint64_t n) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        a[i] = (uint32_t)i;
+}
+
 }  // namespace sx
 
 using namespace sx;
 
 namespace {
 
+// Per-graph plan of the tiled pull (graph residency, built on first use):
+// hub selection (top-K out-degree), encoded sources, row-start bitmap.
 sx_status prep(sx_graph g, const char* who) {
     if (g->directed && !g->has_rev)
         return sxh::fail(SX_E_NO_REVERSE, std::string(who) + ": pull needs in-neighbour rows (CSC)");
-    if (!g->hacc) {
-        SX_CU(cudaMalloc(&g->hacc, (g->n + 1) * sizeof(double)));
-        SX_CU(cudaMemsetAsync(g->hacc, 0, (g->n + 1) * sizeof(double), g->ctx->stream));
-        SX_CU(cudaMalloc(&g->loff, (g->n + 1) * sizeof(uint64_t)));
-        SX_CU(cudaMalloc(&g->scratch64, MAX_GRID * sizeof(uint64_t)));
+    if (g->pp_hcol) return SX_OK;
+    cudaStream_t s = g->ctx->stream;
+    const uint64_t n = g->n, E = g->mi;
+    const uint64_t ntiles = (E + PT - 1) / PT;
+    const uint64_t epad = ntiles * PT + PT;
+    const int eg = 8 * g->ctx->prop.multiProcessorCount;
+    SX_CU(cudaMalloc(&g->hacc, (n + 1) * sizeof(double)));
+    SX_CU(cudaMemsetAsync(g->hacc, 0, (n + 1) * sizeof(double), s));
+    SX_CU(cudaMalloc(&g->pp_tile_seg, (ntiles + 1) * 4));
+    SX_CU(cudaMalloc(&g->pp_hcol, epad * 4));
+    const uint64_t rsw = epad / 32 + 4;
+    SX_CU(cudaMalloc(&g->pp_rs, rsw * 4));
+    SX_CU(cudaMemsetAsync(g->pp_rs, 0, rsw * 4, s));
+    k_rowstarts<<<eg, 256, 0, s>>>(g->irp, n, E, g->pp_rs);
+    // hubs: the K sources of largest out-degree (each is gathered outdeg times per iteration)
+    uint32_t K = (uint32_t)std::min<uint64_t>(PULL_HUBS, n);
+#ifdef SX_PULL_NOHUB
+    K = 0;
+#endif
+    if (n >= HUBBIT) K = 0;  // ids need the top bit free for the encoding
+    SX_CU(cudaMalloc(&g->pp_hubs, (K ? K : 1) * 4));
+    uint32_t* slot = nullptr;
+    if (K) {
+        uint32_t *kin = nullptr, *kout = nullptr, *vin = nullptr, *vout = nullptr;
+        void* tmp = nullptr;
+        size_t tb = 0;
+        SX_CU(cudaMalloc(&kout, n * 4));
+        SX_CU(cudaMalloc(&vin, n * 4));
+        SX_CU(cudaMalloc(&vout, n * 4));
+        kin = g->dout;
+        k_iota<<<eg, 256, 0, s>>>(vin, n);
+        SX_CU(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, kin, kout, vin, vout, (int64_t)n, 0, 32, s));
+        SX_CU(cudaMalloc(&tmp, tb ? tb : 1));
+        SX_CU(cub::DeviceRadixSort::SortPairsDescending(tmp, tb, kin, kout, vin, vout, (int64_t)n, 0, 32, s));
+        SX_CU(cudaMemcpyAsync(g->pp_hubs, vout, K * 4, cudaMemcpyDeviceToDevice, s));
+        SX_CU(cudaMemsetAsync(vin, 0xFF, n * 4, s));
+        slot = vin;
+        k_hubslot<<<eg, 256, 0, s>>>(g->pp_hubs, K, slot);
+        k_hcol<<<eg, 256, 0, s>>>(g->ici, E, epad, slot, g->pp_hcol);
+        SX_CU(cudaStreamSynchronize(s));
+        cudaFree(tmp);
+        cudaFree(kout);
+        cudaFree(vin);
+        cudaFree(vout);
+    } else {
+        k_hcol<<<eg, 256, 0, s>>>(g->ici, E, epad, nullptr, g->pp_hcol);
     }
+    SX_CU(cudaGetLastError());
+    SX_CU(cudaStreamSynchronize(s));
+    g->pp_K = K;
+    g->pp_ntiles = ntiles;
     return SX_OK;
 }
 
 // Algorithmic bytes of one pull-all iteration: every in-edge once
-// (col 4 B + gathered source value + weight bytes), every vertex once
-// (list 4 B + row_ptr 8 B + state read/write); set per operator.
+// (encoded source 4 B + gathered source value + weight bytes + 1/8 B row-start
+// bit), every vertex once (state read/write, set per operator).
 thread_local double t_edge_bytes = 0, t_vertex_bytes = 0;
 static double pull_bytes(const sx_graph g, const sxh::Counters& c) {
-    return c.iters * ((double)g->mi * t_edge_bytes + (double)g->n * t_vertex_bytes) + c.scanned / 8.0;
+    return c.iters * ((double)g->mi * (t_edge_bytes + 0.125) + (double)g->n * t_vertex_bytes) + c.scanned / 8.0;
 }
 
 template <class Op>
@@ -313,11 +547,19 @@ sx_status run_pull(sx_graph g, const sx_opts* opts, sx_stats* stats, const Op& o
     p.s = sxh::make_sched(g, run.o);
     p.op = op;
     p.iters = iters;
-    p.hacc = g->hacc;
-    p.loff = g->loff;
-    p.scratch = g->scratch64;
+    p.hcol = g->pp_hcol;
+    p.rs = g->pp_rs;
+    p.hubs = g->pp_hubs;
+    p.K = g->pp_K;
+    p.ntiles = g->pp_ntiles;
+    p.E = g->mi;
+    p.tile_seg = g->pp_tile_seg;
+    p.nz = g->lists[0];
+    p.sp = g->lists[1];
+    p.acc = g->hacc;
     void* args[] = {&p};
-    if ((rc = run.launch((const void*)pull_all<Op>, args, true)) != SX_OK) return rc;
+    const int smem = (int)(PULL_HUBS * sizeof(typename Op::HubT));
+    if ((rc = run.launch((const void*)pull_all<Op>, args, true, smem)) != SX_OK) return rc;
     t_edge_bytes = edge_bytes;
     t_vertex_bytes = vertex_bytes;
     return run.end(pull_bytes);
@@ -342,11 +584,14 @@ extern "C" sx_status sx_pagerank(sx_graph g, float damping, uint32_t iters, cons
     op.dout = g->dout;
     op.d = damping;
     op.invN = 1.0 / (double)g->n;
+    op.directed = g->directed;
     op.cur = 0;
     op.D = 0;
     op.last = false;
-    // edge: col 4 + contrib 4; vertex: list 4 + row_ptr 8 + contrib write 4 + outdeg 4
-    if ((rc = run_pull(g, opts, stats, op, iters, 8.0, 20.0)) != SX_OK) return rc;
+    // SURVEY §8(d) rule (each array at most once per pass): edge: source id 4 B;
+    // vertex: contrib read 4 + contrib write 4 + outdeg 4 (the gathers of
+    // contrib are bounded by its size, counted per vertex)
+    if ((rc = run_pull(g, opts, stats, op, iters, 4.0, 12.0)) != SX_OK) return rc;
     return dev_out ? SX_OK : sxh::copy_out(g, rank_out, op.out, g->n * 4);
 }
 
@@ -367,7 +612,8 @@ extern "C" sx_status sx_spmv(sx_graph g, const float* x, uint32_t iters, const s
     op.cur = 0;
     op.D = 0;
     op.last = false;
-    if ((rc = run_pull(g, opts, stats, op, iters, 8.0 + g->wbytes, 16.0)) != SX_OK) return rc;
+    // edge: source id 4 + weight; vertex: x 4 + y 4
+    if ((rc = run_pull(g, opts, stats, op, iters, 4.0 + g->wbytes, 8.0)) != SX_OK) return rc;
     return dev_out ? SX_OK : sxh::copy_out(g, y_out, op.out, g->n * 4);
 }
 
@@ -391,7 +637,7 @@ extern "C" sx_status sx_bp(sx_graph g, const float* prior, uint32_t iters, const
     op.cur = 0;
     op.D = 0;
     op.last = false;
-    // edge: col 4 + belief 8 + weight; vertex: list 4 + row_ptr 8 + prior 4 + belief write 8
-    if ((rc = run_pull(g, opts, stats, op, iters, 12.0 + g->wbytes, 24.0)) != SX_OK) return rc;
+    // edge: source id 4 + weight; vertex: belief read 8 + belief write 8 + prior 4
+    if ((rc = run_pull(g, opts, stats, op, iters, 4.0 + g->wbytes, 20.0)) != SX_OK) return rc;
     return dev_out ? SX_OK : sxh::copy_out(g, logodds_out, op.out, g->n * 4);
 }

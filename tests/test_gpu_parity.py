@@ -262,3 +262,52 @@ def test_device_pointers_in_and_out(ctx, rmat14):
     G.bfs(0, out=out)
     assert np.array_equal(out.cpu().numpy().view(np.uint32), oracle.bfs(rmat14, 0))
     G.free()
+
+
+def tile_edge_graph(degs, n_src=3000, seed=3, E_extra=0):
+    """Directed graph whose in-degrees follow `degs` (cycled), sources uniform: rows
+    that end exactly on, straddle and span the pull kernel's 256-edge tiles."""
+    rng = np.random.default_rng(seed)
+    n = n_src
+    edges = []
+    for u in range(n):
+        d = degs[u % len(degs)]
+        for v in rng.integers(0, n, d):
+            if v != u:
+                edges.append((int(v), u))
+    w = [1 + (i * 37) % 255 for i in range(len(edges))]
+    return simgen.from_edges(n, edges, w, symmetric=False)
+
+
+@pytest.mark.parametrize("degs", [[256], [255, 1], [257, 0, 0, 3], [0, 0, 0, 700, 1, 2], [1], [511, 256, 0, 1]])
+def test_tiled_pull_row_boundaries(ctx, degs):
+    """All-active pull (PageRank / SpMV / BP) on rows that end on, straddle and span the
+    256-edge tiles, with empty rows in between (directed: CSC in-rows)."""
+    g = tile_edge_graph(degs, n_src=1500 if max(degs) > 300 else 3000)
+    G = up(ctx, g)
+    r, _, _ = G.pagerank(0.85, 5)
+    pr_check(r, oracle.pagerank(g, 0.85, 5))
+    x = simgen.uniform_f32(2, 1, g.n, 0.0, 1.0)
+    y, _, _ = G.spmv(x, 1)
+    o = oracle.spmv(g, x)
+    assert np.all(np.abs(y - o) <= 1e-5 * np.maximum(np.abs(o), 1e-30))
+    p = simgen.bp_prior(4, g.n)
+    l, _, _ = G.bp(p, 3)
+    o, at = oracle.bp(g, p, 3, with_abs_terms=True)
+    assert np.all(np.abs(l - o) <= 1e-5 * (np.abs(o) + at) + 1e-6)
+    G.free()
+
+
+@pytest.mark.parametrize("m", [1, 255, 256, 257, 511, 512, 8192])
+def test_tiled_pull_tiny_edge_counts(ctx, m):
+    """Edge counts below, on and just past tile multiples (the sentinel row start at E)."""
+    rng = np.random.default_rng(m)
+    n = 64
+    src = rng.integers(0, n, m)
+    dst = rng.integers(0, n, m)
+    edges = [(int(a), int(b)) for a, b in zip(src, dst) if a != b]
+    g = simgen.from_edges(n, edges, [1 + i % 200 for i in range(len(edges))], symmetric=False)
+    G = up(ctx, g)
+    r, _, _ = G.pagerank(0.85, 4)
+    pr_check(r, oracle.pagerank(g, 0.85, 4))
+    G.free()
