@@ -219,6 +219,7 @@ void sx_graph_free(sx_graph g) {
     cudaFree(g->pp_rs);
     cudaFree(g->pp_hubs);
     cudaFree(g->pp_tile_seg);
+    cudaFree(g->pp_nzaux);
     delete g;
 }
 

@@ -53,6 +53,7 @@ struct sx_graph_s {
     uint32_t* pp_rs = nullptr;    // row-start bitmap over in-edges
     uint32_t* pp_hubs = nullptr;  // hub ids by slot
     uint32_t* pp_tile_seg = nullptr;
+    uint32_t* pp_nzaux = nullptr;   // per active row: the operator's per-row operand
     uint32_t pp_K = 0;
     uint64_t pp_ntiles = 0;
 };

@@ -174,6 +174,7 @@ template <class Op> struct PullP {
     uint32_t* tile_seg;     // ntiles entries
     uint32_t* nz;           // active rows (in-degree > 0), ascending (+1 sentinel)
     uint32_t* sp;           // rows applied in phase B, ascending
+    void* nzaux;            // per active row k: op.aux(nz[k]) (n + 2 entries of 4 B), filled per run
     double* acc;            // n fp64 partial sums of split rows (zero between runs)
 };
 
@@ -189,18 +190,39 @@ struct SpPred {  // empty row, or a row crossing a tile boundary
     }
 };
 
-// Predicated gather (plain global load; 0 when !c), so that a lane's loads are
-// issued back to back instead of one branch-guarded load at a time.
-__device__ __forceinline__ float ld_pred(const float* p, bool c) {
-    float v = 0.f;
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.f32 %0, [%1];\n\t}"
-                 : "+f"(v) : "l"(p), "r"((int)c));
+// L2 eviction policies: the in-edge stream is read once per iteration
+// (evict_first), the gathered source values are re-read E/n times per
+// iteration and should stay resident (evict_last) instead of being pushed
+// out by the stream.
+__device__ __forceinline__ uint64_t l2_policy_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint4 ld_stream(const uint4* p, uint64_t pol) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
     return v;
 }
-__device__ __forceinline__ double ld_pred(const double* p, bool c) {
+
+// Predicated gather (plain global load, L2 evict_last; 0 when !c), so that a
+// lane's loads are issued back to back instead of one branch-guarded load at a time.
+__device__ __forceinline__ float ld_pred(const float* p, bool c, uint64_t pol) {
+    float v = 0.f;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.L2::cache_hint.f32 %0, [%1], %3;\n\t}"
+                 : "+f"(v) : "l"(p), "r"((int)c), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ double ld_pred(const double* p, bool c, uint64_t pol) {
     double v = 0.0;
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.f64 %0, [%1];\n\t}"
-                 : "+d"(v) : "l"(p), "r"((int)c));
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.L2::cache_hint.f64 %0, [%1], %3;\n\t}"
+                 : "+d"(v) : "l"(p), "r"((int)c), "l"(pol));
     return v;
 }
 
@@ -223,6 +245,7 @@ __device__ __forceinline__ double warp_seg_scan(double v, bool start) {
 template <class Op> __global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) pull_all(PullP<Op> p) {
     using HubT = typename Op::HubT;
     using TermT = typename Op::TermT;
+    static_assert(sizeof(typename Op::AuxT) == 4, "nzaux holds 4-byte per-row operands");
     extern __shared__ __align__(16) unsigned char s_dyn[];
     HubT* s_hub = reinterpret_cast<HubT*>(s_dyn);
     Ctl* c = p.s.ctl;
@@ -256,11 +279,17 @@ template <class Op> __global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) pull_
         const uint32_t u = p.nz[k];
         const uint64_t b = __ldg(p.g.irp + u), e = __ldg(p.g.irp + u + 1);
         for (uint64_t t = (b + PT - 1) / PT; t * PT < e; ++t) p.tile_seg[t] = (uint32_t)k;
+        reinterpret_cast<typename Op::AuxT*>(p.nzaux)[k] = p.op.aux(u);
     }
-    if (lead()) p.nz[nnz] = INF;  // sentinel row of the sentinel start bit E
+    if (lead()) {
+        p.nz[nnz] = INF;  // sentinel row of the sentinel start bit E
+        reinterpret_cast<typename Op::AuxT*>(p.nzaux)[nnz] = typename Op::AuxT(0);
+        reinterpret_cast<typename Op::AuxT*>(p.nzaux)[nnz + 1] = typename Op::AuxT(0);
+    }
     if (!grid_sync(c)) return;
     Op op = p.op;
     const uint32_t lane = lane_id();
+    const uint64_t pol_first = l2_policy_first(), pol_last = l2_policy_last();
     for (uint32_t t = 0; t < p.iters; ++t) {
         maybe_reset_line(&c->line[(t + 2) % 3]);
         {
@@ -278,7 +307,7 @@ template <class Op> __global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) pull_
                 for (int j = 0; j < 8; ++j) hid[j] = i0 + j * BLOCK < p.K ? __ldg(p.hubs + i0 + j * BLOCK) : 0u;
                 HubT hvv[8];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) hvv[j] = ld_pred(op.src() + hid[j], i0 + j * BLOCK < p.K);
+                for (int j = 0; j < 8; ++j) hvv[j] = ld_pred(op.src() + hid[j], i0 + j * BLOCK < p.K, pol_last);
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
                     if (i0 + j * BLOCK < p.K) s_hub[i0 + j * BLOCK] = hvv[j];
@@ -298,7 +327,7 @@ template <class Op> __global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) pull_
             if (tl < p.ntiles) {
                 const uint64_t b = tl * PT, f0 = b + lane * PV;
 #pragma unroll
-                for (int q = 0; q < PV / 4; ++q) nq[q] = __ldg(reinterpret_cast<const uint4*>(p.hcol + f0) + q);
+                for (int q = 0; q < PV / 4; ++q) nq[q] = ld_stream(reinterpret_cast<const uint4*>(p.hcol + f0) + q, pol_first);
                 nrs = __ldg(p.rs + (f0 >> 5));
                 if (lane == 31) nrs1 = __ldg(p.rs + ((b + PT) >> 5));
                 nseg = __ldg(p.tile_seg + tl);
@@ -336,14 +365,14 @@ template <class Op> __global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) pull_
             // while the gathers are in flight (most lanes emit at most two rows)
             const uint32_t ra = seg0 + ex;
             const uint32_t u0 = p.nz[ra], u1 = p.nz[ra + 1];
-            const typename Op::AuxT a0 = u0 != INF ? op.aux(u0) : typename Op::AuxT(0);
-            const typename Op::AuxT a1 = u1 != INF ? op.aux(u1) : typename Op::AuxT(0);
+            const typename Op::AuxT* nza = reinterpret_cast<const typename Op::AuxT*>(p.nzaux);
+            const typename Op::AuxT a0 = nza[ra], a1 = nza[ra + 1];
             // all PV gathers issued back to back (predicated, no branches), hubs from shared memory
             const HubT* src = op.src();
             HubT hv[PV];
 #pragma unroll
             for (int j = 0; j < PV; ++j)
-                hv[j] = ld_pred(src + (cols[j] & ~HUBBIT), e0 + j < E && !(cols[j] & HUBBIT));
+                hv[j] = ld_pred(src + (cols[j] & ~HUBBIT), e0 + j < E && !(cols[j] & HUBBIT), pol_last);
 #pragma unroll
             for (int j = 0; j < PV; ++j)
                 if (cols[j] & HUBBIT) hv[j] = s_hub[cols[j] & ~HUBBIT];
@@ -483,6 +512,7 @@ sx_status prep(sx_graph g, const char* who) {
     SX_CU(cudaMalloc(&g->hacc, (n + 1) * sizeof(double)));
     SX_CU(cudaMemsetAsync(g->hacc, 0, (n + 1) * sizeof(double), s));
     SX_CU(cudaMalloc(&g->pp_tile_seg, (ntiles + 1) * 4));
+    SX_CU(cudaMalloc(&g->pp_nzaux, (n + 2) * 4));
     SX_CU(cudaMalloc(&g->pp_hcol, epad * 4));
     const uint64_t rsw = epad / 32 + 4;
     SX_CU(cudaMalloc(&g->pp_rs, rsw * 4));
@@ -555,6 +585,7 @@ sx_status run_pull(sx_graph g, const sx_opts* opts, sx_stats* stats, const Op& o
     p.E = g->mi;
     p.tile_seg = g->pp_tile_seg;
     p.nz = g->lists[0];
+    p.nzaux = g->pp_nzaux;
     p.sp = g->lists[1];
     p.acc = g->hacc;
     void* args[] = {&p};
