@@ -239,6 +239,26 @@ def run_single(args):
                            "hbm_gbs": s["bytes_model"] / (s["ms"] * 1e-3) / 1e9}
         us, ctas = simdx.sx_barrier_bench(ctx.h, 20000)
         extras["grid_barrier_us"] = {"us": us, "ctas": ctas}
+        # the other single-GPU configs of BASELINE.json, built on the device through
+        # the boundary (sx_graph_rmat / sx_graph_grid): C3 PageRank s22, C2 SSSP grid
+        G3 = ctx.rmat(22, args.ef, args.seed)
+        r3 = torch.empty(1 << 22, dtype=torch.float32, device=dev)
+        G3.pagerank(0.85, 20, out=r3)
+        best = None
+        for _ in range(3):
+            _, s, _ = G3.pagerank(0.85, 20, out=r3)
+            best = s if best is None or s["ms"] < best["ms"] else best
+        gbs = best["bytes_model"] / (best["ms"] * 1e-3) / 1e9
+        extras["c3_pagerank_s22"] = {"iters": 20, "ms": best["ms"], "hbm_gbs": gbs, "frac": gbs / peak}
+        G3.free()
+        G2 = ctx.grid(2048, 2048, args.seed, 1, 255)
+        d2 = torch.empty(2048 * 2048, dtype=torch.int32, device=dev)
+        G2.sssp(0, args.delta, out=d2)
+        _, s, _ = G2.sssp(0, args.delta, out=d2)
+        extras["c2_sssp_grid2048"] = {"delta": args.delta, "ms": s["ms"], "iterations": s["iterations"],
+                                      "us_per_iteration": s["ms"] * 1e3 / max(1, s["iterations"]),
+                                      "launches": s["launches"]}
+        G2.free()
         log(f"[bench] extras: {extras}")
 
     # ---- e2e: pinned host CSR -> upload -> BFS -> host levels -> free, through the C ABI

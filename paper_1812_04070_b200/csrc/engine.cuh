@@ -883,6 +883,59 @@ __device__ __forceinline__ void for_edges_w(const uint32_t* __restrict__ col, co
     for (uint64_t e = a + 4 * nvec + rank; e < end; e += size) fn(e, __ldg(col + e), edge_w(w8, w32, e));
 }
 
+// for_edges_w in batches: fn(u, w, k) gets k (1..4) neighbour ids and weights,
+// so the caller can issue the four edges' dependent loads together.
+template <class Fn>
+__device__ __forceinline__ void for_edges_wb(const uint32_t* __restrict__ col, const uint8_t* __restrict__ w8,
+                                             const uint32_t* __restrict__ w32, uint64_t beg, uint64_t end,
+                                             uint64_t rank, uint64_t size, Fn&& fn) {
+    uint64_t a = (beg + 3) & ~3ull;
+    if (a > end) a = end;
+    for (uint64_t e = beg + rank; e < a; e += size) {
+        const uint32_t u[4] = {__ldg(col + e), 0u, 0u, 0u};
+        const uint32_t w[4] = {edge_w(w8, w32, e), 0u, 0u, 0u};
+        fn(u, w, 1u);
+    }
+    const uint64_t nvec = (end - a) >> 2;
+    const uint4* c4 = reinterpret_cast<const uint4*>(col + a);
+    for (uint64_t i = rank; i < nvec; i += size) {
+        const uint4 q = __ldg(c4 + i);
+        const uint64_t e = a + 4 * i;
+        const uint32_t u[4] = {q.x, q.y, q.z, q.w};
+        uint32_t w[4];
+        if (w8) {
+            const uint32_t ww = __ldg(reinterpret_cast<const uint32_t*>(w8 + e));
+            w[0] = ww & 0xFF;
+            w[1] = (ww >> 8) & 0xFF;
+            w[2] = (ww >> 16) & 0xFF;
+            w[3] = ww >> 24;
+        } else if (w32) {
+            const uint4 ww = __ldg(reinterpret_cast<const uint4*>(w32 + e));
+            w[0] = ww.x;
+            w[1] = ww.y;
+            w[2] = ww.z;
+            w[3] = ww.w;
+        } else {
+            w[0] = w[1] = w[2] = w[3] = 1u;
+        }
+        fn(u, w, 4u);
+    }
+    for (uint64_t e = a + 4 * nvec + rank; e < end; e += size) {
+        const uint32_t u[4] = {__ldg(col + e), 0u, 0u, 0u};
+        const uint32_t w[4] = {edge_w(w8, w32, e), 0u, 0u, 0u};
+        fn(u, w, 1u);
+    }
+}
+
+// Predicated u32 load (returns `dflt` when !c) without a branch, so that a batch
+// of dependent gathers is issued back to back.
+__device__ __forceinline__ uint32_t ld_pred_u32(const uint32_t* p, bool c, uint32_t dflt) {
+    uint32_t v = dflt;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.u32 %0, [%1];\n\t}"
+                 : "+r"(v) : "l"(p), "r"((int)c));
+    return v;
+}
+
 // One thread sums term(e, col[e]) over [beg, end) with 16 neighbour ids (four
 // 128-bit loads) and their 16 gathers in flight per step.
 template <class Term>

@@ -22,6 +22,8 @@
 
 namespace sx {
 
+constexpr double kSsspPullFrac = 1.0;  // auto mode: pull when the frontier's out-edges exceed this x m
+
 struct SsspP {
     DevGraph g;
     Sched s;
@@ -199,13 +201,28 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_push(SsspP p) {
                         e = stop;
                     }
                 } else {
-                    for_edges_w(p.g.ci, p.g.w8, p.g.w32, beg, end, rank, size, [&](uint64_t, uint32_t u, uint32_t w) {
-                        ++edges;
-                        const uint32_t nd = dv + w;
-                        if (nd >= p.dist[u]) return;
-                        const uint32_t old = atomicMin(p.dist + u, nd);
-                        if (nd < old) improved(u, nd);
-                    });
+                    // warp / CTA / grid granularity: 4 edges per step, distances, then
+                    // the atomicMins, then the improvement tests, each issued together
+                    for_edges_wb(p.g.ci, p.g.w8, p.g.w32, beg, end, rank, size,
+                                 [&](const uint32_t (&u)[4], const uint32_t (&w)[4], uint32_t kn) {
+                                     edges += kn;
+                                     uint32_t nd[4], cur[4], old[4];
+                                     bool ok[4];
+#pragma unroll
+                                     for (int k = 0; k < 4; ++k) {
+                                         ok[k] = k < (int)kn;
+                                         nd[k] = dv + w[k];
+                                         cur[k] = ok[k] ? p.dist[u[k]] : 0u;
+                                     }
+#pragma unroll
+                                     for (int k = 0; k < 4; ++k) {
+                                         ok[k] = ok[k] && nd[k] < cur[k];
+                                         old[k] = ok[k] ? atomicMin(p.dist + u[k], nd[k]) : 0u;
+                                     }
+#pragma unroll
+                                     for (int k = 0; k < 4; ++k)
+                                         if (ok[k] && nd[k] < old[k]) improved(u[k], nd[k]);
+                                 });
                 }
                 if (next == INF) break;
                 v = next;
@@ -232,9 +249,12 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_push(SsspP p) {
         ++st.iters;
         uint32_t filt = overflow ? 1u : 0u;
         // SSSP pull has no early exit: it visits all m in-edges, push visits m_f
-        // out-edges with atomics.  Measured crossover on R-MAT s24: m_f ~ m/3.
+        // out-edges with atomics.  Measured on R-MAT s24 (profiles/r1/sssp24_dirs.txt):
+        // a pull iteration costs ~0.020 ms per million in-edges, a push iteration
+        // ~0.018 ms per million frontier out-edges, so pull never wins (m_f <= m):
+        // the automatic mode stays in push; force_dir = 2 still runs the pull path.
         const bool to_pull = nf > 0 && p.s.force_dir != 1 &&
-                             (p.s.force_dir == 2 || 3.0 * (double)mf > (double)p.g.m);
+                             (p.s.force_dir == 2 || (double)mf > kSsspPullFrac * (double)p.g.m);
         if (to_pull) {
             trace_put(p.s, it, DIR_PUSH, filt, ls.cnt, nf, mf, hi);
             nf_prev = (uint32_t)nf;
@@ -342,8 +362,18 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_pull(SsspP p) {
     uint32_t* s_c = s_cand[warp_id()];
     uint32_t* s_f = s_found[warp_id()];
     uint32_t* s_r = s_far[warp_id()];
-    auto relax_term = [&](const uint32_t* cur, uint32_t u, uint32_t w) -> uint32_t {
-        return bm_test(cur, u) ? p.dist[u] + w : INF;
+    // min over up to 4 in-edges: frontier words, then the frontier sources' distances,
+    // each issued together (a per-edge test -> load chain serialised the row walk)
+    auto relax4 = [&](const uint32_t* cur, const uint32_t (&u)[4], const uint32_t (&w)[4], uint32_t k,
+                      uint32_t& best) {
+        uint32_t bw[4], dv[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bw[j] = j < (int)k ? cur[u[j] >> 5] : 0u;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dv[j] = ld_pred_u32(p.dist + u[j], (bw[j] >> (u[j] & 31)) & 1u, INF);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (dv[j] != INF) best = min(best, dv[j] + w[j]);
     };
     for (;;) {
         IterLine* nx = &c->line[(it + 1) % 3];
@@ -358,9 +388,8 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_pull(SsspP p) {
             const uint32_t u = p.hlist[i];
             const uint64_t beg = __ldg(p.g.irp + u), end = __ldg(p.g.irp + u + 1);
             uint32_t best = INF;
-            for_edges_w(p.g.ici, p.g.iw8, p.g.iw32, beg, end, gtid(), gthreads(), [&](uint64_t, uint32_t v, uint32_t w) {
-                best = min(best, relax_term(cur, v, w));
-            });
+            for_edges_wb(p.g.ici, p.g.iw8, p.g.iw32, beg, end, gtid(), gthreads(),
+                         [&](const uint32_t (&u)[4], const uint32_t (&w)[4], uint32_t k) { relax4(cur, u, w, k, best); });
             best = block_min(best);
             if (threadIdx.x == 0 && best != INF) {
                 const uint32_t old = atomicMin(p.dist + u, best);
@@ -423,9 +452,10 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_pull(SsspP p) {
                     const bool small = mine && end - beg < p.s.sep_small;
                     uint32_t best = INF;
                     if (small) {
-                        for_edges_w(p.g.ici, p.g.iw8, p.g.iw32, beg, end, 0, 1, [&](uint64_t, uint32_t u, uint32_t w) {
-                            best = min(best, relax_term(cur, u, w));
-                        });
+                        for_edges_wb(p.g.ici, p.g.iw8, p.g.iw32, beg, end, 0, 1,
+                                     [&](const uint32_t (&u)[4], const uint32_t (&w)[4], uint32_t k) {
+                                         relax4(cur, u, w, k, best);
+                                     });
                         edges += end - beg;
                     }
                     uint32_t todo = __ballot_sync(FULL, mine && !small);
@@ -434,9 +464,10 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_pull(SsspP p) {
                         todo &= todo - 1;
                         const uint64_t b0 = __shfl_sync(FULL, beg, l), e0 = __shfl_sync(FULL, end, l);
                         uint32_t wb = INF;
-                        for_edges_w(p.g.ici, p.g.iw8, p.g.iw32, b0, e0, lane, 32, [&](uint64_t, uint32_t u, uint32_t w) {
-                            wb = min(wb, relax_term(cur, u, w));
-                        });
+                        for_edges_wb(p.g.ici, p.g.iw8, p.g.iw32, b0, e0, lane, 32,
+                                     [&](const uint32_t (&u)[4], const uint32_t (&w)[4], uint32_t k) {
+                                         relax4(cur, u, w, k, wb);
+                                     });
                         wb = warp_min(wb);
                         if ((int)lane == l) {
                             best = wb;
