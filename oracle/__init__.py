@@ -13,6 +13,7 @@ path) and never imports it; its only inputs are simgen CSR graphs and vectors.
   pagerank   C-P  fp64 Jacobi, T steps          (reading 14)
   spmv       C-V  fp64 y = A^T x over in-edges  (north_star)
   bp         C-BP fp64 log-odds Jacobi          (model = reading 15, "parity unpinned vs paper")
+  wcc        C-W  min vertex id per component   (P:345 names WCC)
   acc_model       the ACC BSP loop and its three filters on tiny graphs
 
 All functions are pinned by tests/test_oracle.py (-m "not gpu").
@@ -51,6 +52,7 @@ def _L():
         lib.oracle_pagerank.argtypes = [u64, vp, vp, vp, ctypes.c_double, u32, vp]
         lib.oracle_spmv.argtypes = [u64, vp, vp, vp, i32, vp, vp]
         lib.oracle_bp.argtypes = [u64, vp, vp, vp, i32, vp, u32, vp, vp]
+        lib.oracle_wcc.argtypes = [u64, vp, vp, vp]
         for f in (lib.oracle_bfs, lib.oracle_sssp, lib.oracle_coreness, lib.oracle_pagerank,
                   lib.oracle_spmv, lib.oracle_bp):
             f.restype = ctypes.c_int
@@ -129,6 +131,14 @@ def bp(g, prior: np.ndarray, iters: int = 10, with_abs_terms: bool = False):
     _chk(_L().oracle_bp(g.n, _p(g.in_ptr()), _p(g.in_idx()), _p(w), 0 if w is None else w.dtype.itemsize,
                         _p(prior), iters, _p(out), _p(at)), "bp")
     return (out, at) if with_abs_terms else out
+
+
+def wcc(g) -> np.ndarray:
+    """oracle.c:oracle_wcc — label(v) = smallest vertex id in v's connected component (undirected graphs)."""
+    assert not getattr(g, "directed", False), "wcc: undirected graphs only"
+    out = np.empty(g.n, np.uint32)
+    _chk(_L().oracle_wcc(g.n, _p(g.row_ptr), _p(g.col), _p(out)), "wcc")
+    return out
 
 
 def level_histogram(level: np.ndarray) -> np.ndarray:

@@ -269,3 +269,33 @@ int oracle_bp(uint64_t n, const uint64_t* in_ptr, const uint32_t* in_idx, const 
     free(l); free(ln); free(lp);
     return 0;
 }
+
+/* C-W, connected components of an undirected graph (WCC, named by the paper
+ * as a voting workload): label(v) = the
+ * smallest vertex id in v's component.  Ids are scanned in increasing order and
+ * a queue BFS labels each component from its first (= smallest) unlabelled
+ * vertex.  Undirected (symmetric) CSR only. */
+int oracle_wcc(uint64_t n, const uint64_t* row_ptr, const uint32_t* col, uint32_t* label) {
+    for (uint64_t v = 0; v < n; ++v) label[v] = INF32;
+    if (n == 0) return 0;
+    uint32_t* q = (uint32_t*)malloc(n * sizeof(uint32_t));
+    if (!q) return -2;
+    for (uint64_t s = 0; s < n; ++s) {
+        if (label[s] != INF32) continue;
+        uint64_t head = 0, tail = 0;
+        label[s] = (uint32_t)s;
+        q[tail++] = (uint32_t)s;
+        while (head < tail) {
+            uint32_t v = q[head++];
+            for (uint64_t e = row_ptr[v]; e < row_ptr[v + 1]; ++e) {
+                uint32_t u = col[e];
+                if (label[u] == INF32) {
+                    label[u] = (uint32_t)s;
+                    q[tail++] = u;
+                }
+            }
+        }
+    }
+    free(q);
+    return 0;
+}

@@ -348,3 +348,44 @@ def test_bp_antisymmetry():
     q = (1.0 - p.astype(np.float64)).astype(np.float32)
     # exact when 1-p is representable as computed; compare with a tolerance from the f32 round trip
     assert np.allclose(a, -b, rtol=1e-5, atol=1e-5)
+
+
+# ---------------------------------------------------------------- WCC (C-W)
+def test_wcc_closed_forms():
+    """path -> one component labelled 0; isolated vertices keep their own id; two components -> 0 and 3."""
+    g = simgen.from_edges(6, [(i, i + 1) for i in range(5)])
+    assert list(oracle.wcc(g)) == [0] * 6
+    g = simgen.from_edges(7, [(0, 1), (1, 2), (3, 4), (4, 5), (5, 6)])
+    assert list(oracle.wcc(g)) == [0, 0, 0, 3, 3, 3, 3]
+    g = simgen.from_edges(5, [(4, 2)])
+    assert list(oracle.wcc(g)) == [0, 1, 2, 3, 2]
+    assert list(oracle.wcc(simgen.from_edges(1, []))) == [0]
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_wcc_vs_scipy_components(seed):
+    """The partition equals scipy's connected components; each label is the component's smallest id."""
+    from scipy.sparse import csr_matrix
+    from scipy.sparse.csgraph import connected_components
+    n = 40 + 7 * seed
+    g = simgen.random_graph(n, max(1, n // 2 + 3 * seed), seed)
+    lab = oracle.wcc(g)
+    A = csr_matrix((np.ones(g.m), g.col.astype(np.int64), g.row_ptr.astype(np.int64)), shape=(n, n))
+    k, comp = connected_components(A, directed=False)
+    for c in range(k):
+        members = np.flatnonzero(comp == c)
+        assert np.all(lab[members] == members.min())
+    assert len(np.unique(lab)) == k
+
+
+def test_wcc_invariants_rmat():
+    """label(u) == label(v) on every edge, label(v) <= v, labels are fixed points."""
+    g = simgen.rmat(12, 16, 3)
+    lab = oracle.wcc(g)
+    src = np.repeat(np.arange(g.n), np.diff(g.row_ptr.astype(np.int64)))
+    assert np.all(lab[src] == lab[g.col])
+    assert np.all(lab <= np.arange(g.n))
+    assert np.all(lab[lab] == lab)
+    # the component of vertex 0 is exactly the vertices BFS from 0 reaches
+    reach = oracle.bfs(g, 0) != 0xFFFFFFFF
+    assert np.array_equal(lab == 0, reach)
