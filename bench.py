@@ -237,6 +237,9 @@ def run_single(args):
         _, s, _ = G.kcore(0, out=out)
         extras["kcore"] = {"k": 0, "ms": s["ms"], "iterations": s["iterations"],
                            "hbm_gbs": s["bytes_model"] / (s["ms"] * 1e-3) / 1e9}
+        G.wcc(out=out)
+        _, s, _ = G.wcc(out=out)
+        extras["wcc"] = {"ms": s["ms"], "iterations": s["iterations"], "launches": s["launches"]}
         us, ctas = simdx.sx_barrier_bench(ctx.h, 20000)
         extras["grid_barrier_us"] = {"us": us, "ctas": ctas}
         # the other single-GPU configs of BASELINE.json, built on the device through

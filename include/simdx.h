@@ -273,6 +273,16 @@ sx_status sx_spmv(sx_graph g, const float* x, uint32_t iters, const sx_opts* opt
 sx_status sx_bp(sx_graph g, const float* prior, uint32_t iters, const sx_opts* opts, float* logodds_out,
                 sx_stats* stats);
 
+/* Connected components (WCC on an undirected graph; the paper names WCC as a
+ * voting workload): label_out[v] = the smallest
+ * vertex id in v's component.  Min-label propagation as an ACC algorithm: every
+ * vertex starts with its own id and active; Compute = the neighbour's label,
+ * Combine = min (atomicMin in push, single-owner min in pull); the same
+ * filters, direction switch and fused kernels as sx_sssp with every weight
+ * read as 0.  Unweighted graphs are fine.  Errors: SX_E_INVALID (directed
+ * graph, NULL label_out). */
+sx_status sx_wcc(sx_graph g, const sx_opts* opts, uint32_t* label_out, sx_stats* stats);
+
 /* ------------------------------------------------------------ multi-GPU layer
  * SURVEY.md §8(e); the paper itself is single-GPU.  1D vertex-range
  * partition: rank r of P owns vertices [r V, min(n, (r+1) V)), V = ceil(n/P)

@@ -806,7 +806,7 @@ extern "C" sx_status sx_bfs(sx_graph g, uint32_t src, const sx_opts* opts, uint3
     BfsP p;
     p.g = sxh::dev_graph(g);
     if (!g->hub && g->has_rev) {  // first BFS on this graph: build the hub-first probe table
-        SX_CU(cudaMalloc(&g->hub, g->n * 4 + 16));
+        if ((rc = sxh::dmalloc(g->ctx, &g->hub, g->n * 4 + 16)) != SX_OK) return rc;
         bfs_hub<<<g->ctx->prop.multiProcessorCount * 8, BLOCK, 0, s>>>(p.g, g->hub);
         SX_CU(cudaGetLastError());
     }

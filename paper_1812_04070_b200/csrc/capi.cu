@@ -148,13 +148,29 @@ sx_status coop_launch(sx_graph g, const void* fn, void** args, int* grid_out, in
     return SX_OK;
 }
 
+sx_status dmalloc(sx_ctx c, void** p, size_t bytes) {
+    cudaError_t e = cudaMallocFromPoolAsync(p, bytes ? bytes : 1, c->pool, c->stream);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *p = nullptr;
+        return e == cudaErrorMemoryAllocation ? fail(SX_E_OOM, "device memory exhausted")
+                                              : cuda_fail(e, "cudaMallocFromPoolAsync");
+    }
+    return SX_OK;
+}
+
+void dfree(sx_ctx c, void* p) {
+    if (p) cudaFreeAsync(p, c->stream);
+}
+
 sx_status Run::begin() {
     sx_ctx c = g->ctx;
     if (o.trace && o.trace_cap > g->trace_cap) {
-        if (g->trace) cudaFree(g->trace);
+        dfree(c, g->trace);
         g->trace = nullptr;
         g->trace_cap = 0;
-        SX_CU(cudaMalloc(&g->trace, o.trace_cap * sizeof(TraceRec)));
+        sx_status rc = dmalloc(c, &g->trace, o.trace_cap * sizeof(TraceRec));
+        if (rc != SX_OK) return rc;
         g->trace_cap = (uint32_t)o.trace_cap;
     }
     SX_CU(cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), c->stream));
@@ -359,6 +375,20 @@ sx_status sx_ctx_create(int device, void* cuda_stream, sx_ctx* out) {
         return sxh::cuda_fail(e, "cudaMallocHost");
     }
     std::memset(c->h_ctl, 0, sizeof(Ctl));
+    {
+        cudaMemPoolProps pp{};
+        pp.allocType = cudaMemAllocationTypePinned;
+        pp.handleTypes = cudaMemHandleTypeNone;
+        pp.location.type = cudaMemLocationTypeDevice;
+        pp.location.id = device;
+        if ((e = cudaMemPoolCreate(&c->pool, &pp)) != cudaSuccess) {
+            c->pool = nullptr;
+            sx_ctx_destroy(c);
+            return sxh::cuda_fail(e, "cudaMemPoolCreate");
+        }
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
     *out = c;
     return SX_OK;
 }
@@ -371,6 +401,10 @@ void sx_ctx_destroy(sx_ctx c) {
     for (auto ev : c->evp)
         if (ev) cudaEventDestroy(ev);
     if (c->h_ctl) cudaFreeHost(c->h_ctl);
+    if (c->pool) {
+        cudaStreamSynchronize(c->stream);
+        cudaMemPoolDestroy(c->pool);
+    }
     delete c;
 }
 

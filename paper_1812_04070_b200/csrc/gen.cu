@@ -37,7 +37,8 @@ sx_status adopt(sx_ctx ctx, uint64_t n, uint64_t m, uint64_t* rp, uint32_t* col,
         if (w) cudaFree(w);
         return rc;
     }
-    (*out)->borrowed = false;  // the graph now owns the generator's arrays
+    (*out)->borrowed = false;  // the graph now owns the generator's arrays (cudaMalloc'ed)
+    (*out)->gen_owned = true;
     return SX_OK;
 }
 
@@ -108,13 +109,16 @@ sx_status sx_graph_download(sx_graph g, uint64_t* row_ptr, uint32_t* col, uint32
         } else {
             uint32_t* tmp = nullptr;
             const bool dev = sxh::is_device_ptr(w);
-            if (!dev) SX_CU(cudaMalloc(&tmp, g->m * 4));
+            if (!dev) {
+                sx_status rc2 = sxh::dmalloc(g->ctx, &tmp, g->m * 4);
+                if (rc2 != SX_OK) return rc2;
+            }
             k_widen_w<<<8 * g->ctx->prop.multiProcessorCount, 256, 0, s>>>((const uint8_t*)g->w, g->m, dev ? w : tmp);
             SX_CU(cudaGetLastError());
             if (!dev) {
                 cudaError_t e = cudaMemcpyAsync(w, tmp, g->m * 4, cudaMemcpyDeviceToHost, s);
                 if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-                cudaFree(tmp);
+                sxh::dfree(g->ctx, tmp);
                 if (e != cudaSuccess) return sxh::cuda_fail(e, "sx_graph_download");
             }
         }

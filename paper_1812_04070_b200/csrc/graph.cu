@@ -6,6 +6,9 @@
 // the CSR serves as CSC.  Workspace: 2 list buffers of 4 class regions
 // x n u32, 3 rotating frontier bitmaps + 1 auxiliary bitmap, the control block,
 // 4 state arrays of n x 4 B.
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.h"
@@ -53,16 +56,27 @@ __global__ void k_nz_bitmap(const uint32_t* deg, uint64_t n, uint64_t nwords, ui
     }
 }
 
-template <class T> sx_status dalloc(T** p, size_t count) {
-    cudaError_t e = cudaMalloc((void**)p, (count ? count : 1) * sizeof(T));
-    if (e != cudaSuccess) {
-        *p = nullptr;
-        return sxh::cuda_fail(e, "cudaMalloc");
-    }
-    return SX_OK;
+template <class T> sx_status dalloc(sx_ctx c, T** p, size_t count) {
+    return sxh::dmalloc(c, (void**)p, (count ? count : 1) * sizeof(T));
 }
 
 bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+// SX_TIMING=1: host timestamps of the upload / free phases on stderr (diagnostic;
+// each mark synchronises the stream first).
+struct PhaseTimer {
+    bool on = getenv("SX_TIMING") != nullptr;
+    cudaStream_t s;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    explicit PhaseTimer(cudaStream_t st) : s(st) {}
+    void mark(const char* what) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        const auto t = std::chrono::steady_clock::now();
+        fprintf(stderr, "[sx_timing] %-28s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+        t0 = t;
+    }
+};
 
 }  // namespace
 
@@ -80,6 +94,7 @@ sx_status sx_graph_upload(sx_ctx ctx, const sx_csr_desc* d, sx_graph* out) {
     const bool devp = d->flags & SX_DEVICE_PTRS;
     const bool borrow = devp && (d->flags & SX_BORROW) && aligned16(d->col) && (!directed || !d->csc_idx || aligned16(d->csc_idx));
     cudaStream_t s = ctx->stream;
+    PhaseTimer pt(s);
     sx_graph g = new sx_graph_s();
     g->ctx = ctx;
     g->n = d->n;
@@ -103,7 +118,7 @@ sx_status sx_graph_upload(sx_ctx ctx, const sx_csr_desc* d, sx_graph* out) {
             return SX_OK;
         }
         // +16 B: kernels read whole aligned 16-B groups of ids / weights (masked)
-        sx_status r = dalloc((char**)dst, count * elem + 16);
+        sx_status r = dalloc(ctx, (char**)dst, count * elem + 16);
         if (r != SX_OK) return r;
         if (count) SX_CU(cudaMemcpyAsync(*dst, src, count * elem, cudaMemcpyDefault, s));
         return SX_OK;
@@ -111,6 +126,7 @@ sx_status sx_graph_upload(sx_ctx ctx, const sx_csr_desc* d, sx_graph* out) {
     TRY(take(&g->rp, d->row_ptr, n + 1, 8));
     TRY(take(&g->ci, d->col, m, 4));
     if (d->w) TRY(take((char**)&g->w, (const char*)d->w, m, d->w_bytes));
+    pt.mark("upload: alloc + copy CSR");
     if (directed) {
         if (d->csc_ptr && d->csc_idx) {
             uint64_t mi = 0;
@@ -136,15 +152,16 @@ sx_status sx_graph_upload(sx_ctx ctx, const sx_csr_desc* d, sx_graph* out) {
     }
     // validation (SPEC.md S:35-38 invariants) on the device
     uint32_t* dflags = nullptr;
-    TRY(dalloc(&dflags, 1));
+    TRY(dalloc(ctx, &dflags, 1));
     SX_CU(cudaMemsetAsync(dflags, 0, 4, s));
     const int vb = 256, vg = 4 * ctx->prop.multiProcessorCount;
     k_validate<<<vg, vb, 0, s>>>(g->rp, g->ci, n, m, g->w, g->wbytes, dflags);
     if (directed && g->has_rev) k_validate<<<vg, vb, 0, s>>>(g->irp, g->ici, n, g->mi, g->iw, g->wbytes, dflags);
+    pt.mark("upload: validate");
     uint32_t hflags = 0;
     SX_CU(cudaMemcpyAsync(&hflags, dflags, 4, cudaMemcpyDeviceToHost, s));
     cudaError_t e = cudaStreamSynchronize(s);
-    cudaFree(dflags);
+    sxh::dfree(ctx, dflags);
     if (e != cudaSuccess) return bail(sxh::cuda_fail(e, "graph validation"));
     if (hflags & 7) {
         char buf[160];
@@ -157,24 +174,26 @@ sx_status sx_graph_upload(sx_ctx ctx, const sx_csr_desc* d, sx_graph* out) {
     // degrees + in-degree>0 bitmap
     g->nwords = ((n + 31) / 32 + TILE_WORDS - 1) / TILE_WORDS * TILE_WORDS;
     if (g->nwords == 0) g->nwords = TILE_WORDS;
-    TRY(dalloc(&g->dout, n));
+    TRY(dalloc(ctx, &g->dout, n));
     k_degrees<<<vg, vb, 0, s>>>(g->rp, n, g->dout);
     if (directed && g->has_rev) {
-        TRY(dalloc(&g->din, n));
+        TRY(dalloc(ctx, &g->din, n));
         k_degrees<<<vg, vb, 0, s>>>(g->irp, n, g->din);
     } else {
         g->din = g->dout;
     }
-    TRY(dalloc(&g->nz_in, g->nwords));
+    TRY(dalloc(ctx, &g->nz_in, g->nwords));
     k_nz_bitmap<<<vg, vb, 0, s>>>(g->din, n, g->nwords, g->nz_in);
     // workspace
-    for (int i = 0; i < 2; ++i) TRY(dalloc(&g->lists[i], (uint64_t)NCLS * NSLOT * sxh::region_size(n)));
-    for (int i = 0; i < 3; ++i) TRY(dalloc(&g->bm[i], g->nwords));
-    TRY(dalloc(&g->aux_bm, g->nwords));
-    TRY(dalloc(&g->cta_cnt, NCLS * MAX_GRID));
-    TRY(dalloc((char**)&g->ctl, sizeof(Ctl)));
-    for (int i = 0; i < 4; ++i) TRY(dalloc(&g->st[i], n));
+    pt.mark("upload: degrees + bitmap");
+    for (int i = 0; i < 2; ++i) TRY(dalloc(ctx, &g->lists[i], (uint64_t)NCLS * NSLOT * sxh::region_size(n)));
+    for (int i = 0; i < 3; ++i) TRY(dalloc(ctx, &g->bm[i], g->nwords));
+    TRY(dalloc(ctx, &g->aux_bm, g->nwords));
+    TRY(dalloc(ctx, &g->cta_cnt, NCLS * MAX_GRID));
+    TRY(dalloc(ctx, (char**)&g->ctl, sizeof(Ctl)));
+    for (int i = 0; i < 4; ++i) TRY(dalloc(ctx, &g->st[i], n));
     e = cudaStreamSynchronize(s);
+    pt.mark("upload: workspace");
     if (e != cudaSuccess) return bail(sxh::cuda_fail(e, "graph upload"));
 #undef TRY
     *out = g;
@@ -192,34 +211,44 @@ sx_status sx_graph_info(sx_graph g, uint64_t* n, uint64_t* m, uint64_t* v_begin,
 
 void sx_graph_free(sx_graph g) {
     if (!g) return;
-    cudaSetDevice(g->ctx->device);
-    cudaStreamSynchronize(g->ctx->stream);
+    sx_ctx c = g->ctx;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    PhaseTimer pt(c->stream);
+    auto F = [&](void* p) { sxh::dfree(c, p); };
     if (!g->borrowed) {
-        if (g->irp && g->irp != g->rp) cudaFree(g->irp);
-        if (g->ici && g->ici != g->ci) cudaFree(g->ici);
-        if (g->iw && g->iw != g->w) cudaFree(g->iw);
-        cudaFree(g->rp);
-        cudaFree(g->ci);
-        if (g->w) cudaFree(g->w);
+        // generator-built arrays were cudaMalloc'ed by the embedded generator
+        auto G = [&](void* p) {
+            if (!p) return;
+            if (g->gen_owned) cudaFree(p);
+            else F(p);
+        };
+        if (g->irp && g->irp != g->rp) G(g->irp);
+        if (g->ici && g->ici != g->ci) G(g->ici);
+        if (g->iw && g->iw != g->w) G(g->iw);
+        G(g->rp);
+        G(g->ci);
+        G(g->w);
     }
-    if (g->din && g->din != g->dout) cudaFree(g->din);
-    cudaFree(g->dout);
-    cudaFree(g->nz_in);
-    for (auto* p : g->lists) cudaFree(p);
-    for (auto* p : g->bm) cudaFree(p);
-    cudaFree(g->aux_bm);
-    cudaFree(g->cta_cnt);
-    cudaFree(g->ctl);
-    cudaFree(g->trace);
-    for (auto* p : g->st) cudaFree(p);
-    cudaFree(g->hacc);
-    cudaFree(g->dstate);
-    cudaFree(g->hub);
-    cudaFree(g->pp_hcol);
-    cudaFree(g->pp_rs);
-    cudaFree(g->pp_hubs);
-    cudaFree(g->pp_tile_seg);
-    cudaFree(g->pp_nzaux);
+    if (g->din && g->din != g->dout) F(g->din);
+    F(g->dout);
+    F(g->nz_in);
+    for (auto* p : g->lists) F(p);
+    for (auto* p : g->bm) F(p);
+    F(g->aux_bm);
+    F(g->cta_cnt);
+    F(g->ctl);
+    F(g->trace);
+    for (auto* p : g->st) F(p);
+    F(g->hacc);
+    F(g->dstate);
+    F(g->hub);
+    F(g->pp_hcol);
+    F(g->pp_rs);
+    F(g->pp_hubs);
+    F(g->pp_tile_seg);
+    F(g->pp_nzaux);
+    pt.mark("free");
     delete g;
 }
 

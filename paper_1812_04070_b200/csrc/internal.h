@@ -16,6 +16,7 @@ struct sx_ctx_s {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaEvent_t evp[2 * 32] = {};  // per-launch event pairs (sxh::EV_POOL)
     sx::Ctl* h_ctl = nullptr;  // pinned host mirror of the control block
+    cudaMemPool_t pool = nullptr;  // stream-ordered pool of graph memory (kept, not returned to the driver)
 };
 
 struct sx_graph_s {
@@ -24,6 +25,7 @@ struct sx_graph_s {
     bool directed = false, has_rev = true;
     uint32_t wbytes = 0;
     bool borrowed = false;
+    bool gen_owned = false;   // rp/ci/w come from the embedded generator (cudaMalloc), not the ctx pool
     bool has_zero_w = false;
     // device graph arrays
     uint64_t* rp = nullptr;
@@ -105,6 +107,14 @@ struct Run {
     sx_status sync();
     sx_status end(BytesFn bytes);
 };
+
+// Graph memory: stream-ordered allocations from the ctx's pool on the ctx
+// stream.  Freed blocks stay in the pool (release threshold = max), so a
+// graph upload after a free reuses them without a driver mapping (the
+// cudaMalloc / cudaFree of a 2.8 GB graph cost 10-60 ms, varying run to run).
+sx_status dmalloc(sx_ctx c, void** p, size_t bytes);
+void dfree(sx_ctx c, void* p);
+template <class T> sx_status dmalloc(sx_ctx c, T** p, size_t bytes) { return dmalloc(c, (void**)p, bytes); }
 
 sx_status copy_out(sx_graph g, void* dst, const void* src_dev, size_t bytes);
 sx_status copy_in(sx_graph g, void* dst_dev, const void* src, size_t bytes);

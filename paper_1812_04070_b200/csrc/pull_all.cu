@@ -504,6 +504,11 @@ namespace {
 
 // Per-graph plan of the tiled pull (graph residency, built on first use):
 // hub selection (top-K out-degree), encoded sources, row-start bitmap.
+#define TRYA(x)                          \
+    do {                                 \
+        sx_status r__ = (x);             \
+        if (r__ != SX_OK) return r__;    \
+    } while (0)
 sx_status prep(sx_graph g, const char* who) {
     if (g->directed && !g->has_rev)
         return sxh::fail(SX_E_NO_REVERSE, std::string(who) + ": pull needs in-neighbour rows (CSC)");
@@ -513,13 +518,13 @@ sx_status prep(sx_graph g, const char* who) {
     const uint64_t ntiles = (E + PT - 1) / PT;
     const uint64_t epad = ntiles * PT + PT;
     const int eg = 8 * g->ctx->prop.multiProcessorCount;
-    SX_CU(cudaMalloc(&g->hacc, (n + 1) * sizeof(double)));
+    TRYA(sxh::dmalloc(g->ctx, &g->hacc, (n + 1) * sizeof(double)));
     SX_CU(cudaMemsetAsync(g->hacc, 0, (n + 1) * sizeof(double), s));
-    SX_CU(cudaMalloc(&g->pp_tile_seg, (ntiles + 1) * 4));
-    SX_CU(cudaMalloc(&g->pp_nzaux, (n + 2) * 4));
-    SX_CU(cudaMalloc(&g->pp_hcol, epad * 4));
+    TRYA(sxh::dmalloc(g->ctx, &g->pp_tile_seg, (ntiles + 1) * 4));
+    TRYA(sxh::dmalloc(g->ctx, &g->pp_nzaux, (n + 2) * 4));
+    TRYA(sxh::dmalloc(g->ctx, &g->pp_hcol, epad * 4));
     const uint64_t rsw = epad / 32 + 4;
-    SX_CU(cudaMalloc(&g->pp_rs, rsw * 4));
+    TRYA(sxh::dmalloc(g->ctx, &g->pp_rs, rsw * 4));
     SX_CU(cudaMemsetAsync(g->pp_rs, 0, rsw * 4, s));
     k_rowstarts<<<eg, 256, 0, s>>>(g->irp, n, E, g->pp_rs);
     // hubs: the K sources of largest out-degree (each is gathered outdeg times per iteration)
@@ -528,19 +533,19 @@ sx_status prep(sx_graph g, const char* who) {
     K = 0;
 #endif
     if (n >= HUBBIT) K = 0;  // ids need the top bit free for the encoding
-    SX_CU(cudaMalloc(&g->pp_hubs, (K ? K : 1) * 4));
+    TRYA(sxh::dmalloc(g->ctx, &g->pp_hubs, (K ? K : 1) * 4));
     uint32_t* slot = nullptr;
     if (K) {
         uint32_t *kin = nullptr, *kout = nullptr, *vin = nullptr, *vout = nullptr;
         void* tmp = nullptr;
         size_t tb = 0;
-        SX_CU(cudaMalloc(&kout, n * 4));
-        SX_CU(cudaMalloc(&vin, n * 4));
-        SX_CU(cudaMalloc(&vout, n * 4));
+        TRYA(sxh::dmalloc(g->ctx, &kout, n * 4));
+        TRYA(sxh::dmalloc(g->ctx, &vin, n * 4));
+        TRYA(sxh::dmalloc(g->ctx, &vout, n * 4));
         kin = g->dout;
         k_iota<<<eg, 256, 0, s>>>(vin, n);
         SX_CU(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, kin, kout, vin, vout, (int64_t)n, 0, 32, s));
-        SX_CU(cudaMalloc(&tmp, tb ? tb : 1));
+        TRYA(sxh::dmalloc(g->ctx, &tmp, tb ? tb : 1));
         SX_CU(cub::DeviceRadixSort::SortPairsDescending(tmp, tb, kin, kout, vin, vout, (int64_t)n, 0, 32, s));
         SX_CU(cudaMemcpyAsync(g->pp_hubs, vout, K * 4, cudaMemcpyDeviceToDevice, s));
         SX_CU(cudaMemsetAsync(vin, 0xFF, n * 4, s));
@@ -548,10 +553,10 @@ sx_status prep(sx_graph g, const char* who) {
         k_hubslot<<<eg, 256, 0, s>>>(g->pp_hubs, K, slot);
         k_hcol<<<eg, 256, 0, s>>>(g->ici, E, epad, slot, g->pp_hcol);
         SX_CU(cudaStreamSynchronize(s));
-        cudaFree(tmp);
-        cudaFree(kout);
-        cudaFree(vin);
-        cudaFree(vout);
+        sxh::dfree(g->ctx, tmp);
+        sxh::dfree(g->ctx, kout);
+        sxh::dfree(g->ctx, vin);
+        sxh::dfree(g->ctx, vout);
     } else {
         k_hcol<<<eg, 256, 0, s>>>(g->ici, E, epad, nullptr, g->pp_hcol);
     }
@@ -660,7 +665,7 @@ extern "C" sx_status sx_bp(sx_graph g, const float* prior, uint32_t iters, const
     if (iters == 0) return sxh::fail(SX_E_INVALID, "sx_bp: iters must be >= 1");
     if (g->n == 0) return SX_OK;
     if ((rc = prep(g, "sx_bp")) != SX_OK) return rc;
-    if (!g->dstate) SX_CU(cudaMalloc(&g->dstate, 2 * g->n * sizeof(double)));
+    if (!g->dstate && (rc = sxh::dmalloc(g->ctx, &g->dstate, 2 * g->n * sizeof(double))) != SX_OK) return rc;
     const bool dev_out = sxh::is_device_ptr(logodds_out);
     BpOp op;
     op.b[0] = g->dstate;

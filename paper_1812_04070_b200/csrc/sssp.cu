@@ -33,6 +33,7 @@ struct SsspP {
     uint32_t nh;
     uint32_t delta;
     int sym;
+    uint32_t wcc;  // connected components: every weight reads as 0, dist = component label (sx_wcc)
 };
 
 __global__ void sssp_init(SsspP p, uint32_t src) {
@@ -51,6 +52,27 @@ __global__ void sssp_init(SsspP p, uint32_t src) {
     c->lists_ready = 1;
     c->slotted = 0;
     c->nf_prev = 1;
+    c->iter = 0;
+    c->done = 0;
+}
+
+// WCC start (label propagation as an ACC algorithm): every vertex is
+// its own label and every vertex with edges is active; the push kernel builds
+// the first lists from the frontier bitmap with the ballot filter.
+__global__ void wcc_init(SsspP p) {
+    Ctl* c = p.s.ctl;
+    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < p.g.n; v += T) p.dist[v] = (uint32_t)v;
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < p.s.nwords; w += T) p.s.bm[0][w] = p.g.nz_in[w];
+    if (blockIdx.x == 0 && threadIdx.x < 32)
+        for (int i = 0; i < 3; ++i) reset_line_warp(&c->line[i]);
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    for (int i = 0; i < NCLS; ++i) c->cur_count[i] = 0;
+    c->hi = 0xFFFFFFFFull + 1;
+    c->dir = DIR_PUSH;
+    c->lists_ready = 0;
+    c->slotted = 0;
+    c->nf_prev = 0xFFFFFFFFu;
     c->iter = 0;
     c->done = 0;
 }
@@ -169,7 +191,10 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_push(SsspP p) {
                         const uint4 q = __ldg(reinterpret_cast<const uint4*>(p.g.ci + a));
                         const uint32_t u[4] = {q.x, q.y, q.z, q.w};
                         uint32_t w[4];
-                        if (p.g.w8) {
+                        if (p.wcc) {
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) w[k] = 0u;
+                        } else if (p.g.w8) {
                             const uint32_t ww = __ldg(reinterpret_cast<const uint32_t*>(p.g.w8 + a));
 #pragma unroll
                             for (int k = 0; k < 4; ++k) w[k] = (ww >> (8 * k)) & 0xFF;
@@ -211,7 +236,7 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_push(SsspP p) {
 #pragma unroll
                                      for (int k = 0; k < 4; ++k) {
                                          ok[k] = k < (int)kn;
-                                         nd[k] = dv + w[k];
+                                         nd[k] = dv + (p.wcc ? 0u : w[k]);
                                          cur[k] = ok[k] ? p.dist[u[k]] : 0u;
                                      }
 #pragma unroll
@@ -373,7 +398,7 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_pull(SsspP p) {
         for (int j = 0; j < 4; ++j) dv[j] = ld_pred_u32(p.dist + u[j], (bw[j] >> (u[j] & 31)) & 1u, INF);
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-            if (dv[j] != INF) best = min(best, dv[j] + w[j]);
+            if (dv[j] != INF) best = min(best, dv[j] + (p.wcc ? 0u : w[j]));
     };
     for (;;) {
         IterLine* nx = &c->line[(it + 1) % 3];
@@ -562,7 +587,7 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
                 const uint64_t ek = e + k * step;
                 ok[k] = ek < e1;
                 u[k] = ok[k] ? __ldg(p.g.ci + ek) : 0u;
-                nd[k] = dv + (ok[k] ? (p.g.w8 ? (uint32_t)__ldg(p.g.w8 + ek) : __ldg(p.g.w32 + ek)) : 0u);
+                nd[k] = dv + (ok[k] && !p.wcc ? (p.g.w8 ? (uint32_t)__ldg(p.g.w8 + ek) : __ldg(p.g.w32 + ek)) : 0u);
             }
 #pragma unroll
             for (int k = 0; k < 8; ++k) old[k] = ok[k] ? atomicMin(p.dist + u[k], nd[k]) : 0u;
@@ -716,15 +741,9 @@ static double sssp_bytes(const sx_graph g, const sxh::Counters& c) {
     return 24.0 * c.entries + (8.0 + g->wbytes) * c.edges + c.iters * n / 8.0 + c.scanned / 8.0;
 }
 
-extern "C" sx_status sx_sssp(sx_graph g, uint32_t src, uint32_t delta, const sx_opts* opts, uint32_t* dist_out,
-                             sx_stats* stats) {
-    if (!g || !dist_out) return sxh::fail(SX_E_INVALID, "sx_sssp: NULL graph or dist_out");
-    sx_status rc = sxh::check_ctx(g->ctx);
-    if (rc != SX_OK) return rc;
-    if (g->n == 0) return sxh::fail(SX_E_INVALID, "sx_sssp: empty graph has no source");
-    if (src >= g->n) return sxh::fail(SX_E_INVALID, "sx_sssp: src >= n");
-    if (!g->w || g->wbytes == 0) return sxh::fail(SX_E_WEIGHT, "sx_sssp: graph has no edge weights");
-    if (g->has_zero_w) return sxh::fail(SX_E_WEIGHT, "sx_sssp: zero edge weight (P:361 assumes positive weights)");
+static sx_status run_sssp(sx_graph g, uint32_t src, uint32_t delta, const sx_opts* opts, uint32_t* dist_out,
+                          sx_stats* stats, bool wcc) {
+    sx_status rc;
     sxh::Run run{g, sxh::resolve_opts(opts), stats};
     if (g->directed && !g->has_rev) run.o.force_dir = 1;  // no in-rows: push only
     cudaStream_t s = g->ctx->stream;
@@ -738,7 +757,8 @@ extern "C" sx_status sx_sssp(sx_graph g, uint32_t src, uint32_t delta, const sx_
     p.hlist = g->st[3];
     p.delta = delta;
     p.sym = !g->directed;
-    SX_CU(cudaMemsetAsync(p.dist, 0xFF, g->n * 4, s));
+    p.wcc = wcc ? 1u : 0u;
+    if (!wcc) SX_CU(cudaMemsetAsync(p.dist, 0xFF, g->n * 4, s));
     SX_CU(cudaMemsetAsync(p.far, 0, g->nwords * 4, s));
     for (int i = 0; i < 3; ++i) SX_CU(cudaMemsetAsync(p.s.bm[i], 0, g->nwords * 4, s));
     // the grid-wide (huge in-degree) fold list of the pull kernel
@@ -747,7 +767,8 @@ extern "C" sx_status sx_sssp(sx_graph g, uint32_t src, uint32_t delta, const sx_
     k_huge_list<<<4 * g->ctx->prop.multiProcessorCount, 256, 0, s>>>(g->din, g->n, run.o.sep_huge, p.hlist, dcount);
     SX_CU(cudaMemcpyAsync(&p.nh, dcount, 4, cudaMemcpyDeviceToHost, s));
     SX_CU(cudaStreamSynchronize(s));
-    sssp_init<<<1, 32, 0, s>>>(p, src);
+    if (wcc) wcc_init<<<4 * g->ctx->prop.multiProcessorCount, 256, 0, s>>>(p);
+    else sssp_init<<<1, 32, 0, s>>>(p, src);
     SX_CU(cudaGetLastError());
     void* args[] = {&p};
     g->ctx->h_ctl->done = 0;
@@ -769,4 +790,25 @@ extern "C" sx_status sx_sssp(sx_graph g, uint32_t src, uint32_t delta, const sx_
     }
     if ((rc = run.end(sssp_bytes)) != SX_OK) return rc;
     return dev_out ? SX_OK : sxh::copy_out(g, dist_out, p.dist, g->n * 4);
+}
+
+extern "C" sx_status sx_sssp(sx_graph g, uint32_t src, uint32_t delta, const sx_opts* opts, uint32_t* dist_out,
+                             sx_stats* stats) {
+    if (!g || !dist_out) return sxh::fail(SX_E_INVALID, "sx_sssp: NULL graph or dist_out");
+    sx_status rc = sxh::check_ctx(g->ctx);
+    if (rc != SX_OK) return rc;
+    if (g->n == 0) return sxh::fail(SX_E_INVALID, "sx_sssp: empty graph has no source");
+    if (src >= g->n) return sxh::fail(SX_E_INVALID, "sx_sssp: src >= n");
+    if (!g->w || g->wbytes == 0) return sxh::fail(SX_E_WEIGHT, "sx_sssp: graph has no edge weights");
+    if (g->has_zero_w) return sxh::fail(SX_E_WEIGHT, "sx_sssp: zero edge weight (P:361 assumes positive weights)");
+    return run_sssp(g, src, delta, opts, dist_out, stats, false);
+}
+
+extern "C" sx_status sx_wcc(sx_graph g, const sx_opts* opts, uint32_t* label_out, sx_stats* stats) {
+    if (!g || !label_out) return sxh::fail(SX_E_INVALID, "sx_wcc: NULL graph or label_out");
+    sx_status rc = sxh::check_ctx(g->ctx);
+    if (rc != SX_OK) return rc;
+    if (g->directed) return sxh::fail(SX_E_INVALID, "sx_wcc: undirected graphs only");
+    if (g->n == 0) return SX_OK;
+    return run_sssp(g, 0, 0, opts, label_out, stats, true);
 }

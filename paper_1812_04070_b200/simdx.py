@@ -92,6 +92,7 @@ _lib.sx_pagerank.argtypes = [_vp, _f32, _u32, _P(sx_opts), _vp, _P(sx_stats)]
 _lib.sx_kcore.argtypes = [_vp, _u32, _P(sx_opts), _vp, _P(sx_stats)]
 _lib.sx_spmv.argtypes = [_vp, _vp, _u32, _P(sx_opts), _vp, _P(sx_stats)]
 _lib.sx_bp.argtypes = [_vp, _vp, _u32, _P(sx_opts), _vp, _P(sx_stats)]
+_lib.sx_wcc.argtypes = [_vp, _P(sx_opts), _vp, _P(sx_stats)]
 _lib.sx_barrier_bench.argtypes = [_vp, _u32, _P(ctypes.c_double), _P(ctypes.c_int)]
 _lib.sx_cluster_bench.argtypes = [_vp, _u64, _u32, _u32, _P(ctypes.c_double)]
 _lib.sx_launch_bench.argtypes = [_vp, _u32, _u32, _P(ctypes.c_double)]
@@ -105,13 +106,13 @@ _lib.sx_dist_bfs.argtypes = [_vp, _u32, _P(sx_opts), _P(_vp), _P(sx_stats)]
 _lib.sx_dist_sssp.argtypes = [_vp, _u32, _u32, _P(sx_opts), _P(_vp), _P(sx_stats)]
 for _f in ("sx_ctx_create", "sx_ctx_info", "sx_graph_upload", "sx_graph_info", "sx_graph_rmat", "sx_graph_grid",
            "sx_graph_download", "sx_bfs", "sx_sssp", "sx_pagerank",
-           "sx_kcore", "sx_spmv", "sx_bp", "sx_barrier_bench", "sx_cluster_bench", "sx_launch_bench",
+           "sx_kcore", "sx_spmv", "sx_bp", "sx_wcc", "sx_barrier_bench", "sx_cluster_bench", "sx_launch_bench",
            "sx_nccl_unique_id", "sx_dist_create", "sx_dist_range", "sx_dist_upload", "sx_dist_bfs", "sx_dist_sssp"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 EXPORTED = ["sx_status_str", "sx_last_error", "sx_version", "sx_ctx_create", "sx_ctx_destroy", "sx_ctx_info",
             "sx_graph_upload", "sx_graph_info", "sx_graph_free", "sx_graph_rmat", "sx_graph_grid", "sx_graph_download", "sx_opts_default", "sx_bfs", "sx_sssp",
-            "sx_pagerank", "sx_kcore", "sx_spmv", "sx_bp", "sx_barrier_bench", "sx_cluster_bench", "sx_launch_bench",
+            "sx_pagerank", "sx_kcore", "sx_spmv", "sx_bp", "sx_wcc", "sx_barrier_bench", "sx_cluster_bench", "sx_launch_bench",
             "sx_nccl_unique_id", "sx_dist_create", "sx_dist_range", "sx_dist_upload", "sx_dist_free", "sx_dist_bfs", "sx_dist_sssp"]
 
 
@@ -282,6 +283,10 @@ def sx_spmv(g, x, iters, opts, y_out):
     return _run(_lib.sx_spmv, "sx_spmv", g, y_out, opts, (_ptr(x), iters))
 
 
+def sx_wcc(g, opts, label_out):
+    return _run(_lib.sx_wcc, "sx_wcc", g, label_out, opts, ())
+
+
 def sx_bp(g, prior, iters, opts, out):
     return _run(_lib.sx_bp, "sx_bp", g, out, opts, (_ptr(prior), iters))
 
@@ -400,6 +405,12 @@ class Graph:
         out = np.empty(self.n, np.uint32) if out is None else out
         o, buf = self._opts(dict(kw))
         st = sx_kcore(self.h, k, o, out)
+        return out, st.as_dict(), self._trace(buf, st)
+
+    def wcc(self, out=None, **kw):
+        out = np.empty(self.n, np.uint32) if out is None else out
+        o, buf = self._opts(dict(kw))
+        st = sx_wcc(self.h, o, out)
         return out, st.as_dict(), self._trace(buf, st)
 
     def spmv(self, x, iters: int = 1, out=None, **kw):

@@ -110,3 +110,11 @@ def test_barrier_roofline(ctx):
     from paper_1812_04070_b200 import simdx
     us, ctas = simdx.sx_barrier_bench(ctx.h, 20000)
     assert ctas >= 148 and 0.1 < us < 50.0
+
+
+def test_wcc_rmat24(ctx, rmat24):
+    """Connected components of the bench graph (R-MAT s24): min-id labels equal the oracle's."""
+    G = ctx.upload(rmat24)
+    lab, st, _ = G.wcc()
+    assert np.array_equal(lab, oracle.wcc(rmat24))
+    G.free()

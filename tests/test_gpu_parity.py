@@ -311,3 +311,48 @@ def test_tiled_pull_tiny_edge_counts(ctx, m):
     r, _, _ = G.pagerank(0.85, 4)
     pr_check(r, oracle.pagerank(g, 0.85, 4))
     G.free()
+
+
+# ---------------------------------------------------------------- WCC (C-W)
+@pytest.mark.parametrize("name", sorted(TINY))
+def test_wcc_tiny(ctx, name):
+    g = TINY[name]
+    G = up(ctx, g)
+    lab, _, _ = G.wcc()
+    assert np.array_equal(lab, oracle.wcc(g)), name
+    G.free()
+
+
+@pytest.mark.parametrize("mode", SK_MODES, ids=[str(m) for m in SK_MODES])
+def test_wcc_modes_rmat(ctx, mode):
+    """R-MAT s14 with many small components (ef 2), across the filter / direction / fusion modes."""
+    g = simgen.rmat(14, 2, seed=5)
+    G = up(ctx, g)
+    lab, st, _ = G.wcc(**mode)
+    assert np.array_equal(lab, oracle.wcc(g)), mode
+    if mode.get("force_dir") == 2:
+        assert st["pull_iters"] > 0
+    G.free()
+
+
+def test_wcc_grid_and_generated(ctx):
+    """A grid (one component, diameter rows + cols) and the generator's unweighted R-MAT."""
+    g = simgen.grid(60, 90, 1, 0, 0)
+    G = up(ctx, g)
+    lab, _, _ = G.wcc()
+    assert not lab.any()
+    G.free()
+    G = ctx.rmat(13, 4, 7)
+    lab, _, _ = G.wcc()
+    assert np.array_equal(lab, oracle.wcc(simgen.rmat(13, 4, 7)))
+    G.free()
+
+
+def test_wcc_rejects_directed(ctx):
+    from paper_1812_04070_b200 import simdx
+    g = simgen.random_graph(100, 300, 2, symmetric=False)
+    G = up(ctx, g)
+    with pytest.raises(simdx.SimdxError) as e:
+        G.wcc()
+    assert e.value.status == simdx.SX_E_INVALID
+    G.free()
