@@ -47,6 +47,8 @@ constexpr int NSLOT = 32;          // counter slots (L2 lines) per iteration lin
 constexpr int BAR_GROUPS = 32;     // two-level barrier: <= 32 groups of CTAs
 
 enum : uint32_t { DIR_PUSH = 0, DIR_PULL = 1, DIR_CLUSTER = 2 };
+constexpr int MPV = 8;          // frontier pulls (SSSP / WCC): in-edges per lane of a warp tile
+constexpr int MPT = 32 * MPV;   // in-edges per warp tile
 constexpr int CL_CTAS = 16;      // CTAs of the small-frontier cluster kernel (non-portable size 16)
 constexpr uint32_t CL_BIG = 64;  // cluster mode: out-degree above which a task's edges are split cluster-wide
 constexpr int CL_BLOCK = 1024;   // threads per CTA of the cluster kernel

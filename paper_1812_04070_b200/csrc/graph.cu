@@ -248,6 +248,8 @@ void sx_graph_free(sx_graph g) {
     F(g->pp_hubs);
     F(g->pp_tile_seg);
     F(g->pp_nzaux);
+    F(g->pp_gnz);
+    F(g->pp_gseg);
     pt.mark("free");
     delete g;
 }

@@ -56,6 +56,9 @@ struct sx_graph_s {
     uint32_t* pp_hubs = nullptr;  // hub ids by slot
     uint32_t* pp_tile_seg = nullptr;
     uint32_t* pp_nzaux = nullptr;   // per active row: the operator's per-row operand
+    uint32_t* pp_gnz = nullptr;     // per graph: rows with in-degree > 0 (+ sentinel), for the frontier pulls
+    uint32_t* pp_gseg = nullptr;    // per graph: tile -> index in pp_gnz of its first edge's row
+    uint64_t pp_gnnz = 0, pp_gntiles = 0;
     uint32_t pp_K = 0;
     uint64_t pp_ntiles = 0;
 };
@@ -115,6 +118,9 @@ struct Run {
 sx_status dmalloc(sx_ctx c, void** p, size_t bytes);
 void dfree(sx_ctx c, void* p);
 template <class T> sx_status dmalloc(sx_ctx c, T** p, size_t bytes) { return dmalloc(c, (void**)p, bytes); }
+
+// Per-graph plan of the tiled frontier pulls (row-start bitmap, active rows, tile map); pull_all.cu.
+sx_status min_pull_plan(sx_graph g);
 
 sx_status copy_out(sx_graph g, void* dst, const void* src_dev, size_t bytes);
 sx_status copy_in(sx_graph g, void* dst_dev, const void* src, size_t bytes);

@@ -15,6 +15,8 @@
 //   Apply   : a single owner writes M_u (atomic-free), Jacobi double
 //             buffering between iterations; fp64 accumulation, fp32 state (BP: fp64).
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 
 #include <algorithm>
 #include <cmath>
@@ -500,6 +502,22 @@ __global__ void k_iota(uint32_t* a, uint64_t n) {
 
 using namespace sx;
 
+// Per-graph active-row list and tile map for the frontier pulls (SSSP / WCC):
+// nz = rows with in-degree > 0 in vertex order, seg[t] = index in nz of the row
+// holding tile t's first in-edge (the pull-all kernel builds the same per run
+// with its iteration-1 ballot filter).
+__global__ void k_tile_seg(const uint64_t* irp, const uint32_t* nz, uint64_t nnz, uint64_t tsz, uint32_t* seg) {
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t u = nz[k];
+        const uint64_t b = irp[u], e = irp[u + 1];
+        for (uint64_t t = (b + tsz - 1) / tsz; t * tsz < e; ++t) seg[t] = (uint32_t)k;
+    }
+}
+struct NzFlag {
+    const uint32_t* din;
+    __host__ __device__ __forceinline__ bool operator()(const uint32_t& v) const { return din[v] > 0; }
+};
+
 namespace {
 
 // Per-graph plan of the tiled pull (graph residency, built on first use):
@@ -509,6 +527,20 @@ namespace {
         sx_status r__ = (x);             \
         if (r__ != SX_OK) return r__;    \
     } while (0)
+// Row-start bitmap over the in-edges (bit e = first edge of a row, bit E = a
+// sentinel start), sized for the largest tile of either pull.
+sx_status prep_rs(sx_graph g) {
+    if (g->pp_rs) return SX_OK;
+    const uint64_t n = g->n, E = g->mi;
+    const uint64_t tmax = PT > MPT ? PT : MPT;
+    const uint64_t rsw = ((E + tmax - 1) / tmax * tmax + tmax) / 32 + 4;
+    TRYA(sxh::dmalloc(g->ctx, &g->pp_rs, rsw * 4));
+    SX_CU(cudaMemsetAsync(g->pp_rs, 0, rsw * 4, g->ctx->stream));
+    k_rowstarts<<<8 * g->ctx->prop.multiProcessorCount, 256, 0, g->ctx->stream>>>(g->irp, n, E, g->pp_rs);
+    SX_CU(cudaGetLastError());
+    return SX_OK;
+}
+
 sx_status prep(sx_graph g, const char* who) {
     if (g->directed && !g->has_rev)
         return sxh::fail(SX_E_NO_REVERSE, std::string(who) + ": pull needs in-neighbour rows (CSC)");
@@ -523,10 +555,7 @@ sx_status prep(sx_graph g, const char* who) {
     TRYA(sxh::dmalloc(g->ctx, &g->pp_tile_seg, (ntiles + 1) * 4));
     TRYA(sxh::dmalloc(g->ctx, &g->pp_nzaux, (n + 2) * 4));
     TRYA(sxh::dmalloc(g->ctx, &g->pp_hcol, epad * 4));
-    const uint64_t rsw = epad / 32 + 4;
-    TRYA(sxh::dmalloc(g->ctx, &g->pp_rs, rsw * 4));
-    SX_CU(cudaMemsetAsync(g->pp_rs, 0, rsw * 4, s));
-    k_rowstarts<<<eg, 256, 0, s>>>(g->irp, n, E, g->pp_rs);
+    TRYA(prep_rs(g));
     // hubs: the K sources of largest out-degree (each is gathered outdeg times per iteration)
     uint32_t K = (uint32_t)std::min<uint64_t>(PULL_HUBS, n);
 #ifdef SX_PULL_NOHUB
@@ -606,6 +635,40 @@ sx_status run_pull(sx_graph g, const sx_opts* opts, sx_stats* stats, const Op& o
 }
 
 }  // namespace
+
+namespace sxh {
+sx_status min_pull_plan(sx_graph g) {
+    if (g->pp_gnz) return SX_OK;
+    TRYA(prep_rs(g));
+    cudaStream_t s = g->ctx->stream;
+    const uint64_t n = g->n;
+    const int eg = 8 * g->ctx->prop.multiProcessorCount;
+    TRYA(sxh::dmalloc(g->ctx, &g->pp_gnz, (n + 2) * 4));
+    const uint64_t gtiles = (g->mi + MPT - 1) / MPT;
+    TRYA(sxh::dmalloc(g->ctx, &g->pp_gseg, (gtiles + 1) * 4));
+    unsigned long long* dcnt = nullptr;
+    TRYA(sxh::dmalloc(g->ctx, &dcnt, 8));
+    cub::CountingInputIterator<uint32_t> it(0);
+    size_t tb = 0;
+    SX_CU(cub::DeviceSelect::If(nullptr, tb, it, g->pp_gnz, dcnt, (int64_t)n, NzFlag{g->din}, s));
+    void* tmp = nullptr;
+    TRYA(sxh::dmalloc(g->ctx, &tmp, tb ? tb : 1));
+    SX_CU(cub::DeviceSelect::If(tmp, tb, it, g->pp_gnz, dcnt, (int64_t)n, NzFlag{g->din}, s));
+    unsigned long long nnz = 0;
+    SX_CU(cudaMemcpyAsync(&nnz, dcnt, 8, cudaMemcpyDeviceToHost, s));
+    SX_CU(cudaStreamSynchronize(s));
+    k_tile_seg<<<eg, 256, 0, s>>>(g->irp, g->pp_gnz, nnz, MPT, g->pp_gseg);
+    const uint32_t sentinel[2] = {INF, INF};  // nz[nnz] = the sentinel row of start bit E
+    SX_CU(cudaMemcpyAsync(g->pp_gnz + nnz, sentinel, 8, cudaMemcpyHostToDevice, s));
+    SX_CU(cudaGetLastError());
+    SX_CU(cudaStreamSynchronize(s));
+    sxh::dfree(g->ctx, tmp);
+    sxh::dfree(g->ctx, dcnt);
+    g->pp_gnnz = nnz;
+    g->pp_gntiles = gtiles;
+    return SX_OK;
+}
+}  // namespace sxh
 
 extern "C" sx_status sx_pagerank(sx_graph g, float damping, uint32_t iters, const sx_opts* opts, float* rank_out,
                                  sx_stats* stats) {

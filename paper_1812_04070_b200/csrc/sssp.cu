@@ -22,15 +22,17 @@
 
 namespace sx {
 
-constexpr double kSsspPullFrac = 1.0;  // auto mode: pull when the frontier's out-edges exceed this x m
+constexpr double kSsspPullFrac = 0.4;  // auto mode: pull while the frontier's out-edges exceed this x m
 
 struct SsspP {
     DevGraph g;
     Sched s;
     uint32_t* dist;
     uint32_t* far;
-    uint32_t* hlist;  // vertices with in-degree >= sep_huge (pull: grid-wide folds)
-    uint32_t nh;
+    const uint32_t* rs;   // pull: row-start bitmap over in-edges (bit E set)
+    const uint32_t* nz;   // pull: rows with in-degree > 0, ascending (+ sentinel)
+    const uint32_t* seg;  // pull: tile -> index in nz of its first edge's row
+    uint64_t ntiles, E;
     uint32_t delta;
     int sym;
     uint32_t wcc;  // connected components: every weight reads as 0, dist = component label (sx_wcc)
@@ -77,10 +79,6 @@ __global__ void wcc_init(SsspP p) {
     c->done = 0;
 }
 
-__global__ void k_huge_list(const uint32_t* din, uint64_t n, uint32_t sep, uint32_t* list, uint32_t* count) {
-    for (uint64_t v = gtid(); v < n; v += gthreads())
-        if (din[v] >= sep) list[atomicAdd(count, 1u)] = (uint32_t)v;
-}
 
 // Far-pile source for the bucket advance: far vertices with dist < hi.
 struct FarWords {
@@ -361,19 +359,39 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_push(SsspP p) {
 }
 
 // ------------------------------------------------------------------ pull
-// Every vertex with in-edges folds min(dist(v) + w) over its in-neighbours v in
-// the frontier bitmap.  Vertices are visited in chunks of 1024 (dynamic, one
-// warp per chunk), compacted into a shared-memory list and processed 32 per
-// round: in-degree < sep_small on the lane (thread granularity, 128-bit loads),
-// larger rows by the warp (warp granularity, 128 edges per step, min tree),
-// in-degree >= sep_huge beforehand by the whole grid.
+// Every vertex u with in-edges folds min(dist(v) + w(v,u)) over its in-neighbours
+// v in the frontier bitmap (P:340 min combine; P:379 atomic-free for a row that
+// one lane owns).  B200 design: the in-edge array is streamed in warp tiles of
+// MPT edges (the PageRank tile machinery, pull_all.cu): lane l owns MPV
+// consecutive in-edges (128-bit id loads), tests their sources' frontier bits,
+// gathers the frontier sources' distances (predicated, issued together), takes
+// the min over its runs of equal destination (row starts from the per-graph
+// row-start bitmap), and a warp segmented min-scan carries partial runs across
+// lanes.  The lane holding a row's last edge in the tile improves the row; a
+// row split across tiles is improved piece by piece — min is idempotent, so
+// each piece does a compare + atomicMin and no second phase is needed.  An
+// improved u joins the next frontier (bitmap claim, exactly once) when
+// dist < hi, else the far pile.
+__device__ __forceinline__ uint32_t warp_seg_min(uint32_t v, bool start) {
+    const uint32_t l = lane_id();
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, v, o);
+        const bool fy = __shfl_up_sync(FULL, start, o);
+        if ((int)l >= o) {
+            if (!start) v = min(v, y);
+            start |= fy;
+        }
+    }
+    return v;
+}
+
 __global__ void __launch_bounds__(BLOCK, 4) sssp_pull(SsspP p) {
     Ctl* c = p.s.ctl;
     const RunState& rs = run_state(c);
     if (rs.done || rs.dir != DIR_PULL) return;
     grid_begin(rs.launch);
-    const uint64_t n = p.g.n;
-    const uint64_t nw = (n + 31) >> 5;
+    const uint64_t n = p.g.n, E = p.E;
     uint32_t it = rs.iter;
     const uint64_t hi = rs.hi;
     uint32_t nf_prev = rs.nf_prev;
@@ -381,25 +399,8 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_pull(SsspP p) {
     Stats st;
     uint32_t dir = DIR_PULL, done = 0;
     const uint32_t lane = lane_id();
-    __shared__ uint32_t s_cand[WARPS][1024];
-    __shared__ uint32_t s_found[WARPS][32];
-    __shared__ uint32_t s_far[WARPS][32];
-    uint32_t* s_c = s_cand[warp_id()];
-    uint32_t* s_f = s_found[warp_id()];
-    uint32_t* s_r = s_far[warp_id()];
-    // min over up to 4 in-edges: frontier words, then the frontier sources' distances,
-    // each issued together (a per-edge test -> load chain serialised the row walk)
-    auto relax4 = [&](const uint32_t* cur, const uint32_t (&u)[4], const uint32_t (&w)[4], uint32_t k,
-                      uint32_t& best) {
-        uint32_t bw[4], dv[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) bw[j] = j < (int)k ? cur[u[j] >> 5] : 0u;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) dv[j] = ld_pred_u32(p.dist + u[j], (bw[j] >> (u[j] & 31)) & 1u, INF);
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (dv[j] != INF) best = min(best, dv[j] + (p.wcc ? 0u : w[j]));
-    };
+    const bool w8_vec = p.g.iw8 && !((uintptr_t)p.g.iw8 & 7u);
+    const bool w32_vec = p.g.iw32 && !((uintptr_t)p.g.iw32 & 15u);
     for (;;) {
         IterLine* nx = &c->line[(it + 1) % 3];
         maybe_reset_line(&c->line[(it + 2) % 3]);
@@ -408,117 +409,100 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_pull(SsspP p) {
         uint32_t* nbm = p.s.bm[(it + 1) % 3];
         uint64_t mdeg = 0, edges = 0;
         uint32_t found = 0;
-        // grid granularity: huge in-degree rows, block-min then one atomicMin
-        for (uint32_t i = 0; i < p.nh; ++i) {
-            const uint32_t u = p.hlist[i];
-            const uint64_t beg = __ldg(p.g.irp + u), end = __ldg(p.g.irp + u + 1);
-            uint32_t best = INF;
-            for_edges_wb(p.g.ici, p.g.iw8, p.g.iw32, beg, end, gtid(), gthreads(),
-                         [&](const uint32_t (&u)[4], const uint32_t (&w)[4], uint32_t k) { relax4(cur, u, w, k, best); });
-            best = block_min(best);
-            if (threadIdx.x == 0 && best != INF) {
-                const uint32_t old = atomicMin(p.dist + u, best);
-                if (best < old) {
-                    if ((uint64_t)best < hi) {
-                        if (!(atomicOr(nbm + (u >> 5), 1u << (u & 31)) & (1u << (u & 31)))) {
-                            ++found;
-                            mdeg += __ldg(p.g.dout + u);
-                        }
-                    } else {
-                        bm_set(p.far, u);
-                    }
+        auto improve = [&](uint32_t u, uint32_t m) {
+            if (m >= p.dist[u]) return;
+            const uint32_t old = atomicMin(p.dist + u, m);
+            if (m >= old) return;
+            if ((uint64_t)m < hi) {
+                if (bm_claim(nbm, u)) {
+                    ++found;
+                    mdeg += __ldg(p.g.dout + u);
                 }
+            } else {
+                bm_set(p.far, u);
             }
-            if (lead()) edges += end - beg;
-        }
-        // thread / warp granularity over chunks of 1024 vertices
-        const uint32_t nchunks = (uint32_t)((nw + 31) >> 5);
-        uint32_t s_cur = my_slot(), tries = 0;
-        uint32_t chunk = 0;
-        if (lane == 0) chunk = grab_chunk(nx, nchunks, s_cur, tries);
-        chunk = __shfl_sync(FULL, chunk, 0);
-        while (chunk != INF) {
-            uint32_t chunk_n = 0;
-            if (lane == 0) chunk_n = grab_chunk(nx, nchunks, s_cur, tries);
-            const uint64_t w0 = (uint64_t)chunk << 5;
-            const uint64_t wl = w0 + lane;
-            const uint32_t cand_l = wl < nw ? __ldg(p.g.nz_in + wl) : 0u;
-            const uint32_t cnt_l = __popc(cand_l);
-            uint32_t incl = cnt_l;
+        };
+        for (uint64_t tile = gwarp(); tile < p.ntiles; tile += gwarps()) {
+            const uint64_t base = tile * MPT, e0 = base + lane * MPV;
+            const bool full = e0 + MPV <= E;
+            uint32_t id[MPV], w[MPV];
+            if (full) {
+                const uint4 qa = __ldg(reinterpret_cast<const uint4*>(p.g.ici + e0));
+                const uint4 qb = __ldg(reinterpret_cast<const uint4*>(p.g.ici + e0 + 4));
+                id[0] = qa.x; id[1] = qa.y; id[2] = qa.z; id[3] = qa.w;
+                id[4] = qb.x; id[5] = qb.y; id[6] = qb.z; id[7] = qb.w;
+            } else {
+#pragma unroll
+                for (int j = 0; j < MPV; ++j) id[j] = e0 + j < E ? __ldg(p.g.ici + e0 + j) : 0u;
+            }
+            if (p.wcc) {
+#pragma unroll
+                for (int j = 0; j < MPV; ++j) w[j] = 0u;
+            } else if (full && w8_vec) {
+                const uint2 q = __ldg(reinterpret_cast<const uint2*>(p.g.iw8 + e0));
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    w[j] = (q.x >> (8 * j)) & 0xFF;
+                    w[4 + j] = (q.y >> (8 * j)) & 0xFF;
+                }
+            } else if (full && w32_vec) {
+                const uint4 qa = __ldg(reinterpret_cast<const uint4*>(p.g.iw32 + e0));
+                const uint4 qb = __ldg(reinterpret_cast<const uint4*>(p.g.iw32 + e0 + 4));
+                w[0] = qa.x; w[1] = qa.y; w[2] = qa.z; w[3] = qa.w;
+                w[4] = qb.x; w[5] = qb.y; w[6] = qb.z; w[7] = qb.w;
+            } else {
+#pragma unroll
+                for (int j = 0; j < MPV; ++j) w[j] = e0 + j < E ? edge_w(p.g.iw8, p.g.iw32, e0 + j) : 0u;
+            }
+            const uint32_t byte = (__ldg(p.rs + (e0 >> 5)) >> (uint32_t)(e0 & 31)) & 0xFFu;  // row starts
+            uint32_t nxt = __shfl_down_sync(FULL, byte, 1) & 1u;
+            if (lane == 31) nxt = __ldg(p.rs + ((base + MPT) >> 5)) & 1u;
+            const uint32_t ends = (byte >> 1) | (nxt << (MPV - 1));
+            const uint32_t seg0 = __ldg(p.seg + tile);
+            const uint32_t mb = lane == 0 ? (byte & ~1u) : byte;
+            uint32_t ex = __popc(mb);
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(FULL, incl, o);
-                if ((int)lane >= o) incl += y;
+                const uint32_t y = __shfl_up_sync(FULL, ex, o);
+                if ((int)lane >= o) ex += y;
             }
-            const uint32_t total = __shfl_sync(FULL, incl, 31);
-            if (total) {
-                uint32_t pos = incl - cnt_l;
-                for (uint32_t w = cand_l; w; w &= w - 1) s_c[pos++] = (uint32_t)(wl << 5) + (__ffs(w) - 1);
-                s_f[lane] = 0;
-                s_r[lane] = 0;
-                __syncwarp();
-                uint32_t v_n = 0;
-                uint64_t beg_n = 0, end_n = 0;
-                if (lane < total) {
-                    v_n = s_c[lane];
-                    beg_n = __ldg(p.g.irp + v_n);
-                    end_n = __ldg(p.g.irp + v_n + 1);
-                }
-                for (uint32_t r = 0; r < total; r += 32) {
-                    const uint32_t v = v_n;
-                    const uint64_t beg = beg_n, end = end_n;
-                    const bool mine = r + lane < total && end - beg < p.s.sep_huge;
-                    beg_n = end_n = 0;
-                    if (r + 32 + lane < total) {
-                        v_n = s_c[r + 32 + lane];
-                        beg_n = __ldg(p.g.irp + v_n);
-                        end_n = __ldg(p.g.irp + v_n + 1);
-                    }
-                    const bool small = mine && end - beg < p.s.sep_small;
-                    uint32_t best = INF;
-                    if (small) {
-                        for_edges_wb(p.g.ici, p.g.iw8, p.g.iw32, beg, end, 0, 1,
-                                     [&](const uint32_t (&u)[4], const uint32_t (&w)[4], uint32_t k) {
-                                         relax4(cur, u, w, k, best);
-                                     });
-                        edges += end - beg;
-                    }
-                    uint32_t todo = __ballot_sync(FULL, mine && !small);
-                    while (todo) {
-                        const int l = __ffs(todo) - 1;
-                        todo &= todo - 1;
-                        const uint64_t b0 = __shfl_sync(FULL, beg, l), e0 = __shfl_sync(FULL, end, l);
-                        uint32_t wb = INF;
-                        for_edges_wb(p.g.ici, p.g.iw8, p.g.iw32, b0, e0, lane, 32,
-                                     [&](const uint32_t (&u)[4], const uint32_t (&w)[4], uint32_t k) {
-                                         relax4(cur, u, w, k, wb);
-                                     });
-                        wb = warp_min(wb);
-                        if ((int)lane == l) {
-                            best = wb;
-                            edges += e0 - b0;
-                        }
-                    }
-                    if (mine && best < p.dist[v]) {
-                        p.dist[v] = best;  // single owner
-                        if ((uint64_t)best < hi) {
-                            atomicOr(s_f + ((v >> 5) - w0), 1u << (v & 31));
-                            mdeg += p.sym ? (end - beg) : __ldg(p.g.dout + v);
-                        } else {
-                            atomicOr(s_r + ((v >> 5) - w0), 1u << (v & 31));
-                        }
-                    }
-                }
-                __syncwarp();
-                const uint32_t fm = s_f[lane], fa = s_r[lane];
-                if (fm) {
-                    atomicOr(nbm + wl, fm);  // the grid-wide fold may own bits of the same word
-                    found += __popc(fm);
-                }
-                if (fa) atomicOr(p.far + wl, fa);
-                __syncwarp();
+            ex -= __popc(mb);
+            // frontier words, then the frontier sources' distances, each issued together
+            uint32_t fw[MPV], dv[MPV];
+#pragma unroll
+            for (int j = 0; j < MPV; ++j) fw[j] = e0 + j < E ? cur[id[j] >> 5] : 0u;
+#pragma unroll
+            for (int j = 0; j < MPV; ++j) dv[j] = ld_pred_u32(p.dist + id[j], (fw[j] >> (id[j] & 31)) & 1u, INF);
+            uint32_t x[MPV];
+            uint32_t tail = INF;
+#pragma unroll
+            for (int j = 0; j < MPV; ++j) {
+                x[j] = dv[j] == INF ? INF : dv[j] + w[j];
+                if ((byte >> j) & 1u) tail = INF;
+                tail = min(tail, x[j]);
             }
-            chunk = __shfl_sync(FULL, chunk_n, 0);
+            const uint32_t nvalid = e0 >= E ? 0u : (E - e0 >= (uint64_t)MPV ? (uint32_t)MPV : (uint32_t)(E - e0));
+            edges += nvalid;
+            const uint32_t incl = warp_seg_min(tail, byte != 0);
+            uint32_t carry = __shfl_up_sync(FULL, incl, 1);
+            if (lane == 0 || (byte & 1u)) carry = INF;
+            uint32_t run = INF;
+#pragma unroll
+            for (int j = 0; j < MPV; ++j) {
+                if ((byte >> j) & 1u) {
+                    run = INF;
+                    carry = INF;
+                }
+                run = min(run, x[j]);
+                if ((uint32_t)j < nvalid && ((ends >> j) & 1u)) {
+                    const uint32_t m = min(run, carry);
+                    if (m != INF) {
+                        const uint32_t u = p.nz[seg0 + ex + __popc(mb & ((2u << j) - 1u))];
+                        if (u != INF) improve(u, m);
+                    }
+                }
+            }
+            if (lane == 31 && !nxt && nvalid == MPV && incl != INF) improve(p.nz[seg0 + ex + __popc(mb)], incl);
         }
         st.edges += edges;
         {
@@ -530,7 +514,6 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_pull(SsspP p) {
                 if (v2[1]) atomicAdd(&sl.found, (unsigned int)v2[1]);
             }
         }
-        st.scanned += (lead() ? nw * 32 : 0);
         if (!grid_sync(c)) return;
         LineSum ls;
         read_line(nx, ls);
@@ -546,7 +529,7 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_pull(SsspP p) {
         }
         // an empty frontier goes back to push, which owns the bucket advance
         const bool to_push = nf == 0 || p.s.force_dir == 1 ||
-                             (p.s.force_dir == 0 && 3.0 * (double)ls.mdeg <= (double)p.g.m);
+                             (p.s.force_dir == 0 && (double)ls.mdeg <= kSsspPullFrac * (double)p.g.m);
         nf_prev = (uint32_t)nf;
         if (to_push) {
             dir = DIR_PUSH;
@@ -554,6 +537,7 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_pull(SsspP p) {
         }
         if (!p.s.fusion) break;
     }
+    (void)n;
     sssp_exit(p, DIR_PULL, it, hi, nf_prev, dir, done, 0u, 0u, cnt, st);
 }
 
@@ -754,19 +738,26 @@ static sx_status run_sssp(sx_graph g, uint32_t src, uint32_t delta, const sx_opt
     const bool dev_out = sxh::is_device_ptr(dist_out);
     p.dist = dev_out ? dist_out : g->st[0];
     p.far = g->aux_bm;
-    p.hlist = g->st[3];
     p.delta = delta;
     p.sym = !g->directed;
     p.wcc = wcc ? 1u : 0u;
     if (!wcc) SX_CU(cudaMemsetAsync(p.dist, 0xFF, g->n * 4, s));
     SX_CU(cudaMemsetAsync(p.far, 0, g->nwords * 4, s));
     for (int i = 0; i < 3; ++i) SX_CU(cudaMemsetAsync(p.s.bm[i], 0, g->nwords * 4, s));
-    // the grid-wide (huge in-degree) fold list of the pull kernel
-    uint32_t* dcount = g->st[2];
-    SX_CU(cudaMemsetAsync(dcount, 0, 4, s));
-    k_huge_list<<<4 * g->ctx->prop.multiProcessorCount, 256, 0, s>>>(g->din, g->n, run.o.sep_huge, p.hlist, dcount);
-    SX_CU(cudaMemcpyAsync(&p.nh, dcount, 4, cudaMemcpyDeviceToHost, s));
-    SX_CU(cudaStreamSynchronize(s));
+    // the tiled pull's per-graph plan (row-start bitmap, active rows, tile map)
+    if (!(g->directed && !g->has_rev) && run.o.force_dir != 1) {
+        if ((rc = sxh::min_pull_plan(g)) != SX_OK) return rc;
+        p.rs = g->pp_rs;
+        p.nz = g->pp_gnz;
+        p.seg = g->pp_gseg;
+        p.ntiles = g->pp_gntiles;
+    } else {
+        p.rs = p.nz = p.seg = nullptr;
+        p.ntiles = 0;
+        run.o.force_dir = 1;
+        p.s.force_dir = 1;
+    }
+    p.E = g->mi;
     if (wcc) wcc_init<<<4 * g->ctx->prop.multiProcessorCount, 256, 0, s>>>(p);
     else sssp_init<<<1, 32, 0, s>>>(p, src);
     SX_CU(cudaGetLastError());
