@@ -111,6 +111,11 @@ __global__ void __launch_bounds__(BLOCK) bfs_init(BfsP p, uint32_t src, uint32_t
     }
     if (blockIdx.x != 0) return;
     Ctl* c = p.s.ctl;
+    {   // the whole control block starts at zero (replaces a host-enqueued memset per call)
+        uint4* C4 = reinterpret_cast<uint4*>(c);
+        for (uint32_t i = threadIdx.x; i < sizeof(Ctl) / 16; i += BLOCK) C4[i] = make_uint4(0u, 0u, 0u, 0u);
+        __syncthreads();
+    }
     if (threadIdx.x < 32)
         for (int i = 0; i < 3; ++i) reset_line_warp(&c->line[i]);
     if (threadIdx.x != 0) return;
@@ -810,7 +815,7 @@ extern "C" sx_status sx_bfs(sx_graph g, uint32_t src, const sx_opts* opts, uint3
         bfs_hub<<<g->ctx->prop.multiProcessorCount * 8, BLOCK, 0, s>>>(p.g, g->hub);
         SX_CU(cudaGetLastError());
     }
-    if ((rc = run.begin()) != SX_OK) return rc;
+    if ((rc = run.begin(/*zero_ctl=*/false)) != SX_OK) return rc;  // bfs_init zeroes the control block
     p.s = sxh::make_sched(g, run.o);
     // write levels straight into a device output buffer (no copy-out)
     const bool dev_out = sxh::is_device_ptr(level_out);

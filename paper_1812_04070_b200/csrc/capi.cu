@@ -163,7 +163,7 @@ void dfree(sx_ctx c, void* p) {
     if (p) cudaFreeAsync(p, c->stream);
 }
 
-sx_status Run::begin() {
+sx_status Run::begin(bool zero_ctl) {
     sx_ctx c = g->ctx;
     if (o.trace && o.trace_cap > g->trace_cap) {
         dfree(c, g->trace);
@@ -173,8 +173,10 @@ sx_status Run::begin() {
         if (rc != SX_OK) return rc;
         g->trace_cap = (uint32_t)o.trace_cap;
     }
-    SX_CU(cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), c->stream));
-    std::memset(c->h_ctl, 0, sizeof(Ctl));
+    if (zero_ctl) SX_CU(cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), c->stream));
+    // only the tail (from `iter` on) is ever copied back and read on the host
+    constexpr size_t off = offsetof(Ctl, iter);
+    std::memset(reinterpret_cast<char*>(c->h_ctl) + off, 0, sizeof(Ctl) - off);
     SX_CU(cudaEventRecord(c->ev0, c->stream));
     return SX_OK;
 }

@@ -101,7 +101,7 @@ struct Run {
     uint32_t launches = 0, launches_push = 0, launches_pull = 0;
     int npending = 0;
     bool pend_pull[EV_POOL] = {};
-    sx_status begin();
+    sx_status begin(bool zero_ctl = true);  // zero_ctl = false: the algorithm's init kernel zeroes it
     // Enqueue one persistent kernel (timed with an event pair); no host sync.
     sx_status launch(const void* fn, void** args, bool pull, int smem = 0);
     // Same for a non-cooperative launch with an explicit shape (e.g. one cluster).

@@ -715,13 +715,14 @@ using namespace sx;
 
 // Algorithmic bytes: push — per list entry 4 B list + 16 B row_ptr
 // pair + 4 B dist(v); per edge 4 B col + weight + 4 B dist(u); per iteration one
-// bitmap clear (n/8); ballot / far scans n/8.  Pull — every in-edge of every
-// vertex once (4 B col + weight) + the frontier bitmap + row_ptr + dist, per
-// pull iteration.
+// bitmap clear (n/8); ballot / far scans n/8.  Pull (tiles) — every in-edge
+// once (4 B id + weight + 1/8 B row-start bit) + per vertex the active-row
+// entry, the distance gathers (bounded by the 4n-byte array) and the
+// improvement (12 B), + frontier and next bitmaps, per pull iteration.
 static double sssp_bytes(const sx_graph g, const sxh::Counters& c) {
     const double n = (double)g->n;
     if (c.pull > 0)
-        return c.pull * ((4.0 + g->wbytes) * (double)g->mi + 12.0 * n + 2.0 * n / 8.0) + c.scanned / 8.0;
+        return c.pull * ((4.125 + g->wbytes) * (double)g->mi + 12.0 * n + 2.0 * n / 8.0) + c.scanned / 8.0;
     return 24.0 * c.entries + (8.0 + g->wbytes) * c.edges + c.iters * n / 8.0 + c.scanned / 8.0;
 }
 

@@ -361,7 +361,13 @@ class Graph:
             sx_graph_free(self.h)
             self.h = None
 
+    _default_opts = None
+
     def _opts(self, kw):
+        if not kw:  # the common call: default options, built once
+            if Graph._default_opts is None:
+                Graph._default_opts = make_opts()
+            return Graph._default_opts, None
         trace_cap = kw.pop("trace_cap", 0)
         o = make_opts(**kw)
         buf = None
