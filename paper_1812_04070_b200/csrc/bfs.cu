@@ -12,6 +12,10 @@
 // the traversal ends or the direction switches (push -> pull -> push).
 #include <cstring>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace sx {
@@ -798,7 +802,30 @@ static double bfs_bytes(const sx_graph g, const sxh::Counters& c) {
     return 20.0 * c.entries + 4.0 * c.edges + 4.0 * c.reached + c.iters * n / 8.0 + c.scanned / 8.0;
 }
 
+// SX_TIMING=2: host-side timestamps of one sx_bfs call on stderr (no syncs added).
+namespace {
+struct HostMarks {
+    bool on;
+    std::chrono::steady_clock::time_point t0, prev;
+    char buf[512];
+    int len = 0;
+    HostMarks() : on([] { const char* e = getenv("SX_TIMING"); return e && e[0] == '2'; }()) {
+        if (on) t0 = prev = std::chrono::steady_clock::now();
+    }
+    void mark(const char* what) {
+        if (!on) return;
+        const auto t = std::chrono::steady_clock::now();
+        len += snprintf(buf + len, sizeof(buf) - len, " %s %.1f", what, std::chrono::duration<double, std::micro>(t - prev).count());
+        prev = t;
+    }
+    ~HostMarks() {
+        if (on) fprintf(stderr, "[sx_bfs host us]%s\n", buf);
+    }
+};
+}  // namespace
+
 extern "C" sx_status sx_bfs(sx_graph g, uint32_t src, const sx_opts* opts, uint32_t* level_out, sx_stats* stats) {
+    HostMarks hm;
     if (!g || !level_out) return sxh::fail(SX_E_INVALID, "sx_bfs: NULL graph or level_out");
     sx_status rc = sxh::check_ctx(g->ctx);
     if (rc != SX_OK) return rc;
@@ -824,6 +851,7 @@ extern "C" sx_status sx_bfs(sx_graph g, uint32_t src, const sx_opts* opts, uint3
     p.hub = g->hub;
     p.sym = !g->directed;
     const uint32_t dir0 = run.o.force_dir == 2 ? DIR_PULL : DIR_PUSH;
+    hm.mark("prologue");
     bfs_init<<<g->ctx->prop.multiProcessorCount * 8, BLOCK, 0, s>>>(p, src, dir0);
     SX_CU(cudaGetLastError());
     void* args[] = {&p};
@@ -852,11 +880,14 @@ extern "C" sx_status sx_bfs(sx_graph g, uint32_t src, const sx_opts* opts, uint3
         const int len = first && dir == DIR_CLUSTER ? 4 : 3;
         for (int i = 0, d = (int)dir; i < len; ++i, d = (int)next((uint32_t)d))
             if ((rc = enqueue((uint32_t)d)) != SX_OK) return rc;
+        hm.mark("enqueue");
         if ((rc = run.sync()) != SX_OK) return rc;
+        hm.mark("sync");
         if (g->ctx->h_ctl->done) break;
         dir = g->ctx->h_ctl->dir;
     }
     if ((rc = run.end(bfs_bytes)) != SX_OK) return rc;
+    hm.mark("end");
     return dev_out ? SX_OK : sxh::copy_out(g, level_out, p.level, g->n * 4);
 }
 

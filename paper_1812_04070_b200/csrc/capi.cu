@@ -219,14 +219,23 @@ sx_status Run::launch_plain(const void* fn, void** args, int grid, int block, bo
     return SX_OK;
 }
 
+__global__ void k_tail_copy(const Ctl* src, Ctl* dst_host) {
+    constexpr size_t off = offsetof(Ctl, iter);
+    constexpr size_t nw = (sizeof(Ctl) - off) / 4;
+    const uint32_t* s = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(src) + off);
+    uint32_t* d = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(dst_host) + off);
+    for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) d[i] = vload(s + i);
+}
+
 sx_status Run::sync() {
     sx_ctx c = g->ctx;
     // end-of-run event and the host-visible tail of the control block (from
     // `iter` on: run state, cluster line, statistics), one stream sync
     SX_CU(cudaEventRecord(c->ev1, c->stream));
-    constexpr size_t off = offsetof(Ctl, iter);
-    SX_CU(cudaMemcpyAsync(reinterpret_cast<char*>(c->h_ctl) + off, reinterpret_cast<const char*>(g->ctl) + off,
-                          sizeof(Ctl) - off, cudaMemcpyDeviceToHost, c->stream));
+    // one small kernel stores the tail into the mapped host mirror (a DMA copy of
+    // these ~0.6 KB cost more per call: copy-engine start-up)
+    k_tail_copy<<<1, 256, 0, c->stream>>>(g->ctl, c->d_hctl);
+    SX_CU(cudaGetLastError());
     cudaError_t e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) {
         c->poisoned = true;
@@ -372,7 +381,8 @@ sx_status sx_ctx_create(int device, void* cuda_stream, sx_ctx* out) {
             return sxh::cuda_fail(e, "cudaEventCreate");
         }
     }
-    if ((e = cudaMallocHost(&c->h_ctl, sizeof(Ctl))) != cudaSuccess) {
+    if ((e = cudaHostAlloc(&c->h_ctl, sizeof(Ctl), cudaHostAllocMapped)) != cudaSuccess ||
+        (e = cudaHostGetDevicePointer((void**)&c->d_hctl, c->h_ctl, 0)) != cudaSuccess) {
         sx_ctx_destroy(c);
         return sxh::cuda_fail(e, "cudaMallocHost");
     }

@@ -15,7 +15,8 @@ struct sx_ctx_s {
     bool poisoned = false;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaEvent_t evp[2 * 32] = {};  // per-launch event pairs (sxh::EV_POOL)
-    sx::Ctl* h_ctl = nullptr;  // pinned host mirror of the control block
+    sx::Ctl* h_ctl = nullptr;  // pinned, device-mapped host mirror of the control block
+    sx::Ctl* d_hctl = nullptr; // device address of h_ctl (the tail-copy kernel writes it directly)
     cudaMemPool_t pool = nullptr;  // stream-ordered pool of graph memory (kept, not returned to the driver)
 };
 

@@ -409,12 +409,23 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_pull(SsspP p) {
         uint32_t* nbm = p.s.bm[(it + 1) % 3];
         uint64_t mdeg = 0, edges = 0;
         uint32_t found = 0;
-        auto improve = [&](uint32_t u, uint32_t m) {
+        // a row that starts and ends inside the tile has this lane as its only
+        // writer in the pull: plain store and a fire-and-forget claim;
+        // the pieces of a row split across tiles use atomicMin + a returning claim
+        auto improve = [&](uint32_t u, uint32_t m, bool owner) {
             if (m >= p.dist[u]) return;
-            const uint32_t old = atomicMin(p.dist + u, m);
-            if (m >= old) return;
+            if (owner) {
+                p.dist[u] = m;
+            } else {
+                const uint32_t old = atomicMin(p.dist + u, m);
+                if (m >= old) return;
+            }
             if ((uint64_t)m < hi) {
-                if (bm_claim(nbm, u)) {
+                if (owner) {
+                    bm_set(nbm, u);
+                    ++found;
+                    mdeg += __ldg(p.g.dout + u);
+                } else if (bm_claim(nbm, u)) {
                     ++found;
                     mdeg += __ldg(p.g.dout + u);
                 }
@@ -459,6 +470,7 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_pull(SsspP p) {
             if (lane == 31) nxt = __ldg(p.rs + ((base + MPT) >> 5)) & 1u;
             const uint32_t ends = (byte >> 1) | (nxt << (MPV - 1));
             const uint32_t seg0 = __ldg(p.seg + tile);
+            const bool tile_first_start = __shfl_sync(FULL, byte, 0) & 1u;
             const uint32_t mb = lane == 0 ? (byte & ~1u) : byte;
             uint32_t ex = __popc(mb);
 #pragma unroll
@@ -497,12 +509,13 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_pull(SsspP p) {
                 if ((uint32_t)j < nvalid && ((ends >> j) & 1u)) {
                     const uint32_t m = min(run, carry);
                     if (m != INF) {
-                        const uint32_t u = p.nz[seg0 + ex + __popc(mb & ((2u << j) - 1u))];
-                        if (u != INF) improve(u, m);
+                        const uint32_t ridx = seg0 + ex + __popc(mb & ((2u << j) - 1u));
+                        const uint32_t u = p.nz[ridx];
+                        if (u != INF) improve(u, m, ridx != seg0 || tile_first_start);
                     }
                 }
             }
-            if (lane == 31 && !nxt && nvalid == MPV && incl != INF) improve(p.nz[seg0 + ex + __popc(mb)], incl);
+            if (lane == 31 && !nxt && nvalid == MPV && incl != INF) improve(p.nz[seg0 + ex + __popc(mb)], incl, false);
         }
         st.edges += edges;
         {
