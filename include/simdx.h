@@ -211,7 +211,9 @@ typedef struct {
                                     continue on ONE thread-block cluster of 16 CTAs x 1024 threads
                                     synchronised by the hardware cluster barrier instead of the grid
                                     barrier; back to the full grid above 8x this size (BFS: or 256x this
-                                    many out-edges).  Results unchanged.  0 = never.  Default 4096. */
+                                    many out-edges).  Results unchanged.  0 = never.  Default
+                                    SX_CLUSTER_AUTO = 4096, except BFS on graphs below 2^21 vertices
+                                    where the tail measured slower (0). */
 } sx_opts;
 
 typedef struct {
@@ -229,6 +231,7 @@ typedef struct {
     uint32_t launches_push, launches_pull;
 } sx_stats;
 
+#define SX_CLUSTER_AUTO 0xFFFFFFFFu
 /* Fill `o` with the defaults above. */
 void sx_opts_default(sx_opts* o);
 

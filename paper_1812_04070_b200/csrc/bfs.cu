@@ -832,6 +832,7 @@ extern "C" sx_status sx_bfs(sx_graph g, uint32_t src, const sx_opts* opts, uint3
     if (g->n == 0) return sxh::fail(SX_E_INVALID, "sx_bfs: empty graph has no source");
     if (src >= g->n) return sxh::fail(SX_E_INVALID, "sx_bfs: src >= n");
     sxh::Run run{g, sxh::resolve_opts(opts), stats};
+    run.o.cluster_enter = sxh::resolve_cluster(run.o.cluster_enter, true, g->n);
     if (g->directed && !g->has_rev && run.o.force_dir != 1)
         return sxh::fail(SX_E_NO_REVERSE, "sx_bfs: pull needs in-neighbour rows (CSC); use force_dir=1 (push)");
     cudaStream_t s = g->ctx->stream;

@@ -78,6 +78,7 @@ sx_opts resolve_opts(const sx_opts* o) {
     sx_opts r;
     sx_opts_default(&r);
     if (o) r = *o;
+    // automatic cluster tail: the algorithm entry resolves it (resolve_cluster)
     if (r.overflow_threshold == 0) r.overflow_threshold = 64;
     if (r.sep_small == 0) r.sep_small = 32;
     if (r.sep_large == 0) r.sep_large = 128;
@@ -102,6 +103,14 @@ int coop_grid(sx_graph g, const void* fn, int smem) {
     int grid = per_sm * g->ctx->prop.multiProcessorCount;
     if (grid > MAX_GRID) grid = MAX_GRID;
     return grid;
+}
+
+uint32_t resolve_cluster(uint32_t ce, bool bfs, uint64_t n) {
+    if (ce != SX_CLUSTER_AUTO) return ce;
+    // measured (profiles/r1/cluster_sweep.txt): the BFS cluster tail pays off on
+    // R-MAT from scale 21 up (s22 -7%, s24 -7%) and costs 1.4-2x below; the SSSP
+    // tail always pays (C2 grid 1.93x)
+    return bfs && n < (1ull << 21) ? 0u : 4096u;
 }
 
 Sched make_sched(const sx_graph g, const sx_opts& o) {
@@ -345,7 +354,7 @@ void sx_opts_default(sx_opts* o) {
     o->trace = nullptr;
     o->trace_cap = 0;
     o->local_chain = 0;
-    o->cluster_enter = 4096;
+    o->cluster_enter = SX_CLUSTER_AUTO;
 }
 
 sx_status sx_ctx_create(int device, void* cuda_stream, sx_ctx* out) {

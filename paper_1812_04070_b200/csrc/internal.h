@@ -80,6 +80,8 @@ inline uint32_t region_size(uint64_t n) { return (uint32_t)((n + sx::NSLOT - 1) 
 // Fill the scheduling parameters common to every persistent kernel.
 sx::Sched make_sched(const sx_graph g, const sx_opts& o);
 sx_opts resolve_opts(const sx_opts* o);
+// cluster_enter == SX_CLUSTER_AUTO -> the measured default for this algorithm and size
+uint32_t resolve_cluster(uint32_t ce, bool bfs, uint64_t n);
 
 // Cooperative launch of a persistent kernel with occupancy x SMs CTAs (Eq. 1
 // generalised).  Returns SX_E_BARRIER when co-residency is impossible.

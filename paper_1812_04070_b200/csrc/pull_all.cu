@@ -158,8 +158,8 @@ struct BpOp {  // l(u) = logit(p_u) + sum_v log((c b + (1-c)(1-b)) / (c(1-b) + (
 #ifndef SX_PULL_PV
 #define SX_PULL_PV 8
 #endif
-#ifndef SX_PULL_MINB
-#define SX_PULL_MINB 3
+#ifndef SX_PALL_MINB
+#define SX_PALL_MINB 3
 #endif
 constexpr int PV = SX_PULL_PV;  // edges per lane (8 or 16)
 constexpr int PT = 32 * PV;
@@ -248,7 +248,7 @@ __device__ __forceinline__ double warp_seg_scan(double v, bool start) {
     return v;
 }
 
-template <class Op> __global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) pull_all(PullP<Op> p) {
+template <class Op> __global__ void __launch_bounds__(BLOCK, SX_PALL_MINB) pull_all(PullP<Op> p) {
     using HubT = typename Op::HubT;
     using TermT = typename Op::TermT;
     static_assert(sizeof(typename Op::AuxT) == 4, "nzaux holds 4-byte per-row operands");
@@ -608,6 +608,7 @@ template <class Op>
 sx_status run_pull(sx_graph g, const sx_opts* opts, sx_stats* stats, const Op& op, uint32_t iters, double edge_bytes,
                    double vertex_bytes) {
     sxh::Run run{g, sxh::resolve_opts(opts), stats};
+    run.o.cluster_enter = sxh::resolve_cluster(run.o.cluster_enter, false, g->n);
     sx_status rc = run.begin();
     if (rc != SX_OK) return rc;
     PullP<Op> p;

@@ -743,6 +743,7 @@ static sx_status run_sssp(sx_graph g, uint32_t src, uint32_t delta, const sx_opt
                           sx_stats* stats, bool wcc) {
     sx_status rc;
     sxh::Run run{g, sxh::resolve_opts(opts), stats};
+    run.o.cluster_enter = sxh::resolve_cluster(run.o.cluster_enter, false, g->n);
     if (g->directed && !g->has_rev) run.o.force_dir = 1;  // no in-rows: push only
     cudaStream_t s = g->ctx->stream;
     SsspP p;
