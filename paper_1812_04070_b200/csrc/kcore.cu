@@ -101,15 +101,35 @@ __global__ void __launch_bounds__(BLOCK, 4) kcore_push(KcoreP p) {
                 done = 1;
                 break;
             }
+            // One pass over the alive bitmap computes the minimum residual AND the
+            // ballot filter's per-CTA class counts for the speculative level kspec:
+            // after a level's cascade every alive vertex has residual > k, so the next
+            // level is k + 1 unless the minimum jumps; then the count pass is redone.
+            const uint32_t kspec = p.kfix ? p.kfix - 1 : (level_started ? k + 1 : k);
+            const LevelWords lw_spec{p.ab, p.res, kspec};
             uint32_t mn = INF;
             uint64_t alive = 0;
-            for (uint64_t wi = gtid(); wi < p.s.nwords; wi += gthreads()) {
-                uint32_t w = p.ab[wi];
-                alive += __popc(w);
-                while (w) {
-                    const int b = __ffs(w) - 1;
-                    w &= w - 1;
-                    mn = min(mn, p.res[(wi << 5) + b]);
+            {
+                uint64_t w0, w1;
+                ballot_chunk(p.s.nwords, w0, w1);
+                uint32_t acc[NCLS] = {0, 0, 0, 0};
+                for (uint64_t t = w0; t < w1; t += TILE_WORDS) {
+                    const uint64_t wi = t + threadIdx.x;
+                    uint32_t w = p.ab[wi];
+                    alive += __popc(w);
+                    while (w) {
+                        const int b = __ffs(w) - 1;
+                        w &= w - 1;
+                        const uint32_t v = (uint32_t)((wi << 5) + b);
+                        const uint32_t r = p.res[v];
+                        mn = min(mn, r);
+                        if (r <= kspec) acc[cls_of(__ldg(p.g.dout + v), p.s)]++;
+                    }
+                }
+                block_sum<NCLS>(acc);
+                if (threadIdx.x == 0) {
+#pragma unroll
+                    for (int cc = 0; cc < NCLS; ++cc) p.s.cta_cnt[cc * MAX_GRID + blockIdx.x] = acc[cc];
                 }
             }
             mn = block_min(mn);
@@ -127,7 +147,6 @@ __global__ void __launch_bounds__(BLOCK, 4) kcore_push(KcoreP p) {
             LineSum ls;
             read_line(nx, ls);
             mn = ls.minv;
-            if (lead()) st.scanned += 3 * ls.alive;  // residual reads: the min scan + the ballot filter's two passes
             if (ls.alive == 0) {
                 done = 1;
                 break;
@@ -145,12 +164,18 @@ __global__ void __launch_bounds__(BLOCK, 4) kcore_push(KcoreP p) {
             // ---- ballot filter selects the level's seeds; their coreness is k
             ++st.ballot;
             // the thread owning word v >> 5 in the write pass clears the seeds' alive bits
-            if (!ballot_filter(LevelWords{p.ab, p.res, k}, p.s, BallotOut{p.s.lists[it & 1], p.s.cstride, p.g.dout}, cnt,
-                               [&](uint32_t v, uint32_t) {
-                                   p.core[v] = k;
-                                   p.ab[v >> 5] &= ~(1u << (v & 31));
-                               }))
-                return;
+            auto seed = [&](uint32_t v, uint32_t) {
+                p.core[v] = k;
+                p.ab[v >> 5] &= ~(1u << (v & 31));
+            };
+            const BallotOut bo{p.s.lists[it & 1], p.s.cstride, p.g.dout};
+            if (k == kspec) {  // the counts of the fused pass stand: write pass only
+                if (lead()) st.scanned += 2 * ls.alive;
+                ballot_write(lw_spec, p.s, bo, cnt, seed);
+            } else {
+                if (lead()) st.scanned += 3 * ls.alive;
+                if (!ballot_filter(LevelWords{p.ab, p.res, k}, p.s, bo, cnt, seed)) return;
+            }
             if (!grid_sync(c)) return;
             view_contig(cnt);
             trace_put(p.s, it + 1, DIR_PUSH, 1u, cnt, sum4(cnt), 0, k);  // level start (seeds)
