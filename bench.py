@@ -253,6 +253,15 @@ def run_single(args):
             best = s if best is None or s["ms"] < best["ms"] else best
         gbs = best["bytes_model"] / (best["ms"] * 1e-3) / 1e9
         extras["c3_pagerank_s22"] = {"iters": 20, "ms": best["ms"], "hbm_gbs": gbs, "frac": gbs / peak}
+        # SpMV (1 product) and BP (10 iterations) on the same graph, the same tiled pull
+        x3 = torch.from_numpy(simgen.uniform_f32(args.seed, 1, 1 << 22, 0.0, 1.0)).to(dev)
+        G3.spmv(x3, 1, out=r3)
+        _, s, _ = G3.spmv(x3, 1, out=r3)
+        extras["spmv_s22"] = {"ms": s["ms"], "hbm_gbs": s["bytes_model"] / (s["ms"] * 1e-3) / 1e9}
+        pr3 = torch.from_numpy(simgen.bp_prior(args.seed, 1 << 22)).to(dev)
+        G3.bp(pr3, 10, out=r3)
+        _, s, _ = G3.bp(pr3, 10, out=r3)
+        extras["bp_s22"] = {"iters": 10, "ms": s["ms"], "hbm_gbs": s["bytes_model"] / (s["ms"] * 1e-3) / 1e9}
         G3.free()
         G2 = ctx.grid(2048, 2048, args.seed, 1, 255)
         d2 = torch.empty(2048 * 2048, dtype=torch.int32, device=dev)

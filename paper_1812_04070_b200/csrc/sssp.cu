@@ -600,8 +600,10 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
             }
         }
     };
+    // the current list's size: read once at entry, then carried from the previous
+    // iteration's count (one L2 round trip less per iteration)
+    uint32_t ncur = vload(&cl->cnt[it % 3]);
     for (;;) {
-        const uint32_t ncur = vload(&cl->cnt[it % 3]);
         if (lead0) {
             cl->cnt[(it + 2) % 3] = 0;
             cl->nbig[(it + 1) % 3] = 0;
@@ -624,14 +626,15 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
         }
         cluster_barrier();
         const uint32_t nbig = vload(&cl->nbig[it % 3]);
+        uint32_t nnext = vload(ncnt);  // issued together with nbig
         if (nbig) {  // high-degree tasks: their edges spread over the whole cluster
             for (uint32_t j = 0; j < nbig; ++j) {
                 const uint32_t v = NL[lcap - 1 - j];
                 relax(p.dist[v], __ldg(p.g.rp + v) + tid, __ldg(p.g.rp + v + 1), T, nbm, NL, ncnt);
             }
             cluster_barrier();
+            nnext = vload(ncnt);
         }
-        uint32_t nnext = vload(ncnt);
         ++it;
         ++iters;
         uint32_t filt = 0;
@@ -701,6 +704,7 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
             dir = DIR_PUSH;
             break;
         }
+        ncur = nnext;
     }
     // statistics: warp sums, one atomic per warp
     const uint64_t e = warp_sum(edges), en = warp_sum(entries);
