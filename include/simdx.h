@@ -321,7 +321,8 @@ sx_status sx_dist_range(sx_dist d, int local_rank, uint64_t* v_begin, uint64_t* 
  * Upload local rank `local_rank`'s slice: desc->n = owned row count (v_end -
  * v_begin), desc->row_ptr local (starting at 0), desc->col GLOBAL ids < n_global,
  * desc->w optional (same width on every rank).  Symmetric graphs only.
- * Copies; validates like sx_graph_upload.  Errors: SX_E_INVALID, SX_E_OOM.
+ * Copies; validates like sx_graph_upload.  Uploading again replaces the rank's
+ * slice (a new graph on the same partition).  Errors: SX_E_INVALID, SX_E_OOM.
  */
 sx_status sx_dist_upload(sx_dist d, int local_rank, const sx_csr_desc* desc);
 /* Free (collective for NCCL communicators; NULL is a no-op). */

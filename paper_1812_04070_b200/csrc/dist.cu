@@ -575,6 +575,17 @@ sx_status sx_dist_upload(sx_dist d, int local_rank, const sx_csr_desc* desc) {
         return sxh::fail(SX_E_INVALID, "sx_dist_upload: all slices need the same weight width");
     d->wbytes = desc->w ? desc->w_bytes : 0;
     cudaStream_t s = d->ctx->stream;
+    if (k.rp) {  // re-upload (a new graph on the same partition): release the previous slice and workspace
+        cudaStreamSynchronize(s);
+        void* ps[] = {k.rp, k.ci, k.w, k.deg, k.nz, k.state, k.visited, k.front[0], k.front[1], k.gfront, k.sendmap,
+                      k.recv, k.sendbest, k.recvbest, k.cnt};
+        for (void* q : ps)
+            if (q) cudaFree(q);
+        const uint64_t nl = k.nl, lo = k.lo;
+        k = DistRank{};
+        k.nl = nl;
+        k.lo = lo;
+    }
     k.ml = desc->m;
     if ((rc = dmalloc(&k.rp, k.nl + 1)) != SX_OK) return rc;
     if ((rc = dmalloc(&k.ci, k.ml)) != SX_OK) return rc;

@@ -99,11 +99,13 @@ struct BpOp {  // l(u) = logit(p_u) + sum_v log((c b + (1-c)(1-b)) / (c(1-b) + (
     using AuxT = float;      // prior of the destination
     static constexpr bool kStaticHub = false;
     double* b[2];
+    const double* ctab;  // coupling c(w) for the 256 u8 weights (same expression, precomputed: no fp64 division per edge)
     const float* prior;
     float* out;
     uint32_t cur;
     double D;
     bool last;
+    __device__ static __forceinline__ double coupling(double wt) { return 0.25 + 0.5 * (wt - 1.0) / 254.0; }
     __device__ __forceinline__ HubT val(uint32_t v) const { return b[cur][v]; }
     __device__ __forceinline__ const HubT* src() const { return b[cur]; }
     __device__ __forceinline__ AuxT aux(uint32_t u) const { return prior[u]; }
@@ -111,8 +113,7 @@ struct BpOp {  // l(u) = logit(p_u) + sum_v log((c b + (1-c)(1-b)) / (c(1-b) + (
     __device__ __forceinline__ bool empty_each_iter() const { return false; }
     __device__ __forceinline__ double empty_dangling(uint32_t) const { return 0.0; }
     __device__ __forceinline__ TermT term(const DevGraph& g, uint64_t e, HubT bv) const {
-        const double wt = (g.iw8 || g.iw32) ? (double)edge_w(g.iw8, g.iw32, e) : 255.0;
-        const double c = 0.25 + 0.5 * (wt - 1.0) / 254.0;
+        const double c = g.iw8 ? __ldg(ctab + __ldg(g.iw8 + e)) : g.iw32 ? coupling((double)__ldg(g.iw32 + e)) : __ldg(ctab + 255);
         const double num = c * bv + (1.0 - c) * (1.0 - bv);
         const double den = c * (1.0 - bv) + (1.0 - c) * bv;
         return log(num / den);
@@ -493,6 +494,9 @@ __global__ void k_rowstarts(const uint64_t* irp, uint64_t n, uint64_t E, uint32_
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(rs + (E >> 5), 1u << (E & 31));
 }
+__global__ void k_bp_ctab(double* ctab) {
+    if (threadIdx.x < 256) ctab[threadIdx.x] = BpOp::coupling((double)threadIdx.x);
+}
 __global__ void k_iota(uint32_t* a, uint64_t n) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
         a[i] = (uint32_t)i;
@@ -729,11 +733,14 @@ extern "C" sx_status sx_bp(sx_graph g, const float* prior, uint32_t iters, const
     if (iters == 0) return sxh::fail(SX_E_INVALID, "sx_bp: iters must be >= 1");
     if (g->n == 0) return SX_OK;
     if ((rc = prep(g, "sx_bp")) != SX_OK) return rc;
-    if (!g->dstate && (rc = sxh::dmalloc(g->ctx, &g->dstate, 2 * g->n * sizeof(double))) != SX_OK) return rc;
+    if (!g->dstate && (rc = sxh::dmalloc(g->ctx, &g->dstate, (2 * g->n + 256) * sizeof(double))) != SX_OK) return rc;
+    k_bp_ctab<<<1, 256, 0, g->ctx->stream>>>(g->dstate + 2 * g->n);
+    SX_CU(cudaGetLastError());
     const bool dev_out = sxh::is_device_ptr(logodds_out);
     BpOp op;
     op.b[0] = g->dstate;
     op.b[1] = g->dstate + g->n;
+    op.ctab = g->dstate + 2 * g->n;
     float* dp = (float*)g->st[2];
     if ((rc = sxh::copy_in(g, dp, prior, g->n * 4)) != SX_OK) return rc;
     op.prior = dp;

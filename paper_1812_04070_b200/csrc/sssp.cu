@@ -71,7 +71,7 @@ __global__ void wcc_init(SsspP p) {
     if (blockIdx.x != 0 || threadIdx.x != 0) return;
     for (int i = 0; i < NCLS; ++i) c->cur_count[i] = 0;
     c->hi = 0xFFFFFFFFull + 1;
-    c->dir = DIR_PUSH;
+    c->dir = (p.rs && p.s.force_dir != 1) ? DIR_PULL : DIR_PUSH;  // every vertex active: m_f = m, pull
     c->lists_ready = 0;
     c->slotted = 0;
     c->nf_prev = 0xFFFFFFFFu;

@@ -89,3 +89,25 @@ def test_dist_errors(ctx, rmat14):
     with pytest.raises(simdx.SimdxError):
         D.bfs(0)  # slices not uploaded
     D.free()
+
+
+def test_dist_reupload_replaces_the_slices(ctx):
+    """sx_dist_upload on an already loaded partition replaces the slices (bench.py's
+    N-GPU e2e step re-uploads every step): BFS / SSSP answer for the new graph."""
+    g1 = simgen.rmat(12, 16, seed=1, wmin=1, wmax=255)
+    g2 = simgen.rmat(12, 8, seed=2, wmin=1, wmax=255)
+    D = build_dist(ctx, g1, 4)
+    outs, _ = D.bfs(0)
+    assert np.array_equal(np.concatenate(outs), oracle.bfs(g1, 0))
+    for rep in range(2):
+        for r in range(4):
+            lo, hi = D.range(r)
+            rp = (g2.row_ptr[lo:hi + 1] - g2.row_ptr[lo]).astype(np.uint64)
+            sl = simgen.CSR(n=g2.n, row_ptr=rp, col=g2.col[g2.row_ptr[lo]:g2.row_ptr[hi]].copy(),
+                            w=g2.w[g2.row_ptr[lo]:g2.row_ptr[hi]].copy(), v_lo=lo, v_hi=hi)
+            D.upload(r, sl)
+        outs, _ = D.bfs(0)
+        assert np.array_equal(np.concatenate(outs), oracle.bfs(g2, 0))
+        outs, _ = D.sssp(0, 256)
+        assert np.array_equal(np.concatenate(outs), oracle.sssp(g2, 0))
+    D.free()
