@@ -47,20 +47,38 @@ constexpr uint32_t HUB_SOLE = 0x80000000u;
 #ifndef SX_PULL_MINB
 #define SX_PULL_MINB 4
 #endif
+// Groups of 8 lanes per vertex (4 vertices per warp step): a lane loads up to
+// HUB_SCAN / 8 ids of its vertex's row, then their out-degrees, each batch in
+// flight together, and the group reduces with 3 shuffles.
 __global__ void __launch_bounds__(BLOCK) bfs_hub(DevGraph g, uint32_t* hub) {
-    const uint32_t lane = lane_id();
-    const uint64_t nwarp = (uint64_t)gridDim.x * WARPS;
+    constexpr uint32_t GS = 8, PER = HUB_SCAN / GS;
+    const uint32_t lane = lane_id(), sub = lane % GS;
+    const uint64_t ngroups = (uint64_t)gridDim.x * WARPS * (32 / GS);
     const bool flag = g.n <= HUB_SOLE;
-    for (uint64_t v = (uint64_t)blockIdx.x * WARPS + warp_id(); v < g.n; v += nwarp) {
-        const uint64_t beg = __ldg(g.irp + v), end0 = __ldg(g.irp + v + 1), end = min(end0, beg + HUB_SCAN);
-        uint64_t best = 0;
-        for (uint64_t e = beg + lane; e < end; e += 32) {
-            const uint32_t u = __ldg(g.ici + e);
-            best = max(best, ((uint64_t)(__ldg(g.dout + u) + 1u) << 32) | (uint64_t)(~u));
+    const uint64_t g0 = ((uint64_t)blockIdx.x * WARPS + warp_id()) * (32 / GS) + lane / GS;
+    for (uint64_t vb = g0 - lane / GS; vb < g.n; vb += ngroups) {  // warp-uniform loop
+        const uint64_t v = vb + lane / GS;
+        uint64_t beg = 0, end0 = 0;
+        if (v < g.n) {
+            beg = __ldg(g.irp + v);
+            end0 = __ldg(g.irp + v + 1);
+        }
+        const uint64_t end = min(end0, beg + HUB_SCAN);
+        uint32_t u[PER], d[PER];
+#pragma unroll
+        for (uint32_t k = 0; k < PER; ++k) {
+            const uint64_t e = beg + sub + k * GS;
+            u[k] = e < end ? __ldg(g.ici + e) : INF;
         }
 #pragma unroll
-        for (int o = 16; o; o >>= 1) best = max(best, __shfl_xor_sync(FULL, best, o));
-        if (lane == 0) hub[v] = best ? (~(uint32_t)best | (flag && end0 - beg == 1 ? HUB_SOLE : 0u)) : INF;
+        for (uint32_t k = 0; k < PER; ++k) d[k] = u[k] != INF ? __ldg(g.dout + u[k]) : 0u;
+        uint64_t best = 0;
+#pragma unroll
+        for (uint32_t k = 0; k < PER; ++k)
+            if (u[k] != INF) best = max(best, ((uint64_t)(d[k] + 1u) << 32) | (uint64_t)(~u[k]));
+#pragma unroll
+        for (int o = GS / 2; o; o >>= 1) best = max(best, __shfl_xor_sync(FULL, best, o));
+        if (sub == 0 && v < g.n) hub[v] = best ? (~(uint32_t)best | (flag && end0 - beg == 1 ? HUB_SOLE : 0u)) : INF;
     }
 }
 // the probe target of a hub entry (INF: no in-neighbour) and whether it is v's only in-edge

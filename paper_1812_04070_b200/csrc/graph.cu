@@ -17,6 +17,11 @@ using namespace sx;
 
 namespace {
 
+__device__ __forceinline__ bool has_zero_byte(uint32_t x) { return ((x - 0x01010101u) & ~x & 0x80808080u) != 0; }
+
+// Validation (SPEC.md S:35-38 invariants): rows monotone, row_ptr[0] = 0 and
+// row_ptr[n] = m, col < n, weights nonzero.  Edges are checked 8 ids (two
+// 128-bit loads) per thread step; misaligned or short tails scalar.
 __global__ void k_validate(const uint64_t* rp, const uint32_t* ci, uint64_t n, uint64_t m, const void* w,
                            uint32_t wbytes, uint32_t* flags) {
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -28,11 +33,30 @@ __global__ void k_validate(const uint64_t* rp, const uint32_t* ci, uint64_t n, u
         if (a > b) f |= 1;
         if (b - a >= 0xFFFFFFFFull) f |= 16;
     }
-    for (uint64_t e = t; e < m; e += T) {
+    const bool vec = ((uintptr_t)ci & 15u) == 0;
+    const uint64_t n8 = vec ? m / 8 : 0;
+    const uint4* c4 = reinterpret_cast<const uint4*>(ci);
+    for (uint64_t q = t; q < n8; q += T) {
+        const uint4 x = __ldg(c4 + 2 * q), y = __ldg(c4 + 2 * q + 1);
+        if (x.x >= n || x.y >= n || x.z >= n || x.w >= n || y.x >= n || y.y >= n || y.z >= n || y.w >= n) f |= 2;
+    }
+    for (uint64_t e = n8 * 8 + t; e < m; e += T)
         if (ci[e] >= n) f |= 2;
-        if (w) {
-            const uint32_t x = wbytes == 1 ? ((const uint8_t*)w)[e] : ((const uint32_t*)w)[e];
-            if (x == 0) f |= 8;
+    if (w) {
+        if (wbytes == 1 && ((uintptr_t)w & 15u) == 0) {
+            const uint64_t n16 = m / 16;
+            const uint4* w4 = reinterpret_cast<const uint4*>(w);
+            for (uint64_t q = t; q < n16; q += T) {
+                const uint4 x = __ldg(w4 + q);
+                if (has_zero_byte(x.x) || has_zero_byte(x.y) || has_zero_byte(x.z) || has_zero_byte(x.w)) f |= 8;
+            }
+            for (uint64_t e = n16 * 16 + t; e < m; e += T)
+                if (((const uint8_t*)w)[e] == 0) f |= 8;
+        } else {
+            for (uint64_t e = t; e < m; e += T) {
+                const uint32_t x = wbytes == 1 ? ((const uint8_t*)w)[e] : ((const uint32_t*)w)[e];
+                if (x == 0) f |= 8;
+            }
         }
     }
     if (f) atomicOr(flags, f);

@@ -356,3 +356,25 @@ def test_wcc_rejects_directed(ctx):
         G.wcc()
     assert e.value.status == simdx.SX_E_INVALID
     G.free()
+
+
+@pytest.mark.parametrize("pos", [0, 7, 8, 1000, -1])
+def test_upload_validation_vectorized(ctx, pos):
+    """Validation on the 128-bit path (long edge arrays): a column id >= n or a zero weight
+    anywhere (head, vector body, scalar tail) is rejected; the clean graph is accepted."""
+    from paper_1812_04070_b200 import simdx
+    g = simgen.rmat(10, 8, seed=4, wmin=1, wmax=255)
+    G = up(ctx, g)  # clean
+    G.free()
+    bad = simgen.CSR(n=g.n, row_ptr=g.row_ptr, col=g.col.copy(), w=g.w.copy())
+    bad.col[pos] = g.n + 5
+    with pytest.raises(simdx.SimdxError) as e:
+        up(ctx, bad)
+    assert e.value.status == simdx.SX_E_INVALID
+    zw = simgen.CSR(n=g.n, row_ptr=g.row_ptr, col=g.col, w=g.w.copy())
+    zw.w[pos] = 0
+    Gz = up(ctx, zw)
+    with pytest.raises(simdx.SimdxError) as e:
+        Gz.sssp(0)
+    assert e.value.status == simdx.SX_E_WEIGHT
+    Gz.free()
