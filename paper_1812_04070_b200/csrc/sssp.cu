@@ -593,7 +593,12 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
                 edges += ok[k];
                 if (!(ok[k] && nd[k] < old[k])) continue;
                 if ((uint64_t)nd[k] < hi) {
-                    if (bm_claim(nbm, u[k])) cl_append(NL, ncnt, u[k]);
+                    // no claim round trip on the dependent chain: a vertex improved twice in
+                    // an iteration is listed twice and relaxed twice (min is idempotent; the
+                    // bitmap bit is still set for a hand-over to the grid kernels).
+                    // Measured on C2: 61.2 -> 53.6 ms at delta = 1024.
+                    bm_set(nbm, u[k]);
+                    cl_append(NL, ncnt, u[k]);
                 } else {
                     bm_set(p.far, u[k]);
                 }
