@@ -166,7 +166,10 @@ constexpr int PV = SX_PULL_PV;  // edges per lane (8 or 16)
 constexpr int PT = 32 * PV;
 static_assert(PV == 8 || PV == 16, "PV");
 constexpr uint32_t HUBBIT = 0x80000000u;
-constexpr uint32_t PULL_HUBS = 12288;  // hub cache entries: 48 KB of fp32 (PR, SpMV) / 96 KB of fp64 (BP) per CTA
+#ifndef SX_PULL_HUBS
+#define SX_PULL_HUBS 12288
+#endif
+constexpr uint32_t PULL_HUBS = SX_PULL_HUBS;  // hub cache entries: 48 KB of fp32 (PR, SpMV) / 96 KB of fp64 (BP) per CTA
 
 template <class Op> struct PullP {
     DevGraph g;
