@@ -167,9 +167,12 @@ constexpr int PT = 32 * PV;
 static_assert(PV == 8 || PV == 16, "PV");
 constexpr uint32_t HUBBIT = 0x80000000u;
 #ifndef SX_PULL_HUBS
-#define SX_PULL_HUBS 12288
+#define SX_PULL_HUBS 8192
 #endif
-constexpr uint32_t PULL_HUBS = SX_PULL_HUBS;  // hub cache entries: 48 KB of fp32 (PR, SpMV) / 96 KB of fp64 (BP) per CTA
+// hub cache entries: 32 KB of fp32 (PR, SpMV) / 64 KB of fp64 (BP) per CTA.  Measured
+// (profiles/r1/pull_hub_sweep.txt, PR s22 / s24): none 17.2 / 84.5 ms, 4K 15.2 / 70.4,
+// 6K 14.9 / 69.3, 8K 14.7 / 68.2, 12K 15.1 / 72.7, 16K 22 ms (occupancy falls)
+constexpr uint32_t PULL_HUBS = SX_PULL_HUBS;
 
 template <class Op> struct PullP {
     DevGraph g;
