@@ -50,6 +50,7 @@ def test_status_strings_and_version():
     o = simdx.sx_opts_default()
     assert (o.overflow_threshold, o.sep_small, o.sep_large) == (64, 32, 128)
     assert o.fusion == 1 and o.force_filter == 0 and o.force_dir == 0
+    assert o.cluster_enter == 0xFFFFFFFF  # SX_CLUSTER_AUTO: resolved per algorithm and graph size
 
 
 def test_no_cpu_fallback_without_gpu():
