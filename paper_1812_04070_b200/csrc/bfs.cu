@@ -45,7 +45,7 @@ constexpr uint32_t HUB_SOLE = 0x80000000u;
 #define SX_PROBE 4
 #endif
 #ifndef SX_PULL_MINB
-#define SX_PULL_MINB 4
+#define SX_PULL_MINB 3  // measured: 3 CTAs x 256 at <= 85 registers beat 4 at 64 (s24 pull 158 -> 154 us)
 #endif
 // Groups of 8 lanes per vertex (4 vertices per warp step): a lane loads up to
 // HUB_SCAN / 8 ids of its vertex's row, then their out-degrees, each batch in
