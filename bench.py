@@ -263,6 +263,27 @@ def run_single(args):
         _, s, _ = G3.bp(pr3, 10, out=r3)
         extras["bp_s22"] = {"iters": 10, "ms": s["ms"], "hbm_gbs": s["bytes_model"] / (s["ms"] * 1e-3) / 1e9}
         G3.free()
+        # C5 at P = 1: R-MAT s27 (4.3 G edges) built on the device; BFS and SSSP device time
+        try:
+            G5 = ctx.rmat(27, args.ef, args.seed, 1, 255)
+            n5 = 1 << 27
+            o5 = torch.empty(n5, dtype=torch.int32, device=dev)
+            G5.bfs(0, out=o5)
+            b5 = min((G5.bfs(0, out=o5)[1] for _ in range(3)), key=lambda x: x["ms"])
+            G5.sssp(0, args.delta, out=o5)
+            s5 = G5.sssp(0, args.delta, out=o5)[1]
+            G5.bfs(0, out=o5)
+            rp5 = torch.empty(n5 + 1, dtype=torch.int64, device=dev)
+            simdx.sx_graph_download(G5.h, rp5, None, None)
+            mcc5 = int((rp5[1:] - rp5[:-1])[o5 != -1].sum().item()) // 2
+            extras["c5_s27_one_gpu"] = {"bfs_ms": b5["ms"], "bfs_gteps": mcc5 / (b5["ms"] * 1e-3) / 1e9,
+                                        "m_cc": mcc5, "sssp_ms": s5["ms"], "sssp_gteps": mcc5 / (s5["ms"] * 1e-3) / 1e9,
+                                        "sssp_iterations": s5["iterations"]}
+            del rp5
+            G5.free()
+            del o5
+        except Exception as ex:  # memory-bound extra: never fail the bench line for it
+            extras["c5_s27_one_gpu"] = {"error": str(ex)[:200]}
         G2 = ctx.grid(2048, 2048, args.seed, 1, 255)
         d2 = torch.empty(2048 * 2048, dtype=torch.int32, device=dev)
         G2.sssp(0, args.delta, out=d2)
