@@ -378,3 +378,33 @@ def test_upload_validation_vectorized(ctx, pos):
         Gz.sssp(0)
     assert e.value.status == simdx.SX_E_WEIGHT
     Gz.free()
+
+
+def test_empty_and_edgeless_graphs(ctx):
+    """Degenerate inputs: n = 0 (upload works; BFS/SSSP reject the missing source,
+    the source-free algorithms return nothing) and m = 0 (every vertex isolated)."""
+    from paper_1812_04070_b200 import simdx
+    g0 = simgen.from_edges(0, [])
+    G0 = up(ctx, g0)
+    with pytest.raises(simdx.SimdxError) as e:
+        G0.bfs(0)
+    assert e.value.status == simdx.SX_E_INVALID
+    for call in (lambda: G0.pagerank(0.85, 3), lambda: G0.kcore(0), lambda: G0.wcc()):
+        out, _, _ = call()
+        assert out.size == 0
+    G0.free()
+    n = 1000
+    ge = simgen.from_edges(n, [], [])
+    Ge = up(ctx, ge)
+    lv, _, _ = Ge.bfs(7)
+    assert lv[7] == 0 and np.all(np.delete(lv, 7) == INF)
+    r, _, _ = Ge.pagerank(0.85, 5)
+    pr_check(r, oracle.pagerank(ge, 0.85, 5))
+    core, _, _ = Ge.kcore(0)
+    assert not core.any()
+    lab, _, _ = Ge.wcc()
+    assert np.array_equal(lab, np.arange(n, dtype=np.uint32))
+    x = simgen.uniform_f32(3, 1, n, 0.0, 1.0)
+    y, _, _ = Ge.spmv(x, 1)
+    assert not y.any()
+    Ge.free()
