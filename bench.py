@@ -179,7 +179,7 @@ def run_single(args):
 
     def step():
         _, s, _ = G.bfs(0, out=level)
-        acc["launches"] += 1 + s["launches"]  # bfs_init + persistent launches
+        acc["launches"] += 2 + s["launches"]  # bfs_init + persistent launches + the control-tail copy kernel
         acc["ms_push"] += s["ms_push"]
         acc["ms_pull"] += s["ms_pull"]
         acc["b_push"] += s["bytes_push"]
