@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(BLOCK) bfs_init(BfsP p, uint32_t src, uint32_t
     c->nf_prev = 1;
     if (dir == DIR_PUSH && cluster_ok(p.s, 1, d)) dir = DIR_CLUSTER;  // low-degree source: start on one cluster
     c->dir = dir;
+    c->k = dir;  // the start direction, for the host (k is unused by BFS)
     c->lists_ready = dir == DIR_PUSH ? 1u : 0u;
     c->slotted = 0;
     c->iter = 0;
@@ -902,7 +903,13 @@ extern "C" sx_status sx_bfs(sx_graph g, uint32_t src, const sx_opts* opts, uint3
     g->ctx->h_ctl->done = 0;
     // the device picks cluster mode at init for a low-degree source; the host
     // learns the direction only at a sync, so the first sequence starts with it
-    uint32_t dir = dir0 == DIR_PUSH && cl_on ? DIR_CLUSTER : dir0;
+    // a repeated source (same graph, source and options): start with the direction
+    // the device chose last time, so no launch exits at once (correctness never
+    // depends on it: a launch of the wrong phase returns and the loop goes on)
+    const uint32_t okey = (uint32_t)cl_on | ((uint32_t)run.o.force_dir << 1) | ((uint32_t)run.o.force_filter << 3);
+    const bool hit = g->bfs_last_src == src && g->bfs_last_key == okey && g->bfs_last_ce == run.o.cluster_enter &&
+                     g->bfs_last_dir0 != INF;
+    uint32_t dir = hit ? g->bfs_last_dir0 : (dir0 == DIR_PUSH && cl_on ? DIR_CLUSTER : dir0);
     for (bool first = true;; first = false) {
         // first sequence from a cluster start: cluster, push, pull, cluster (covers
         // both a low- and a high-degree source); later ones three phases deep
@@ -912,6 +919,12 @@ extern "C" sx_status sx_bfs(sx_graph g, uint32_t src, const sx_opts* opts, uint3
         hm.mark("enqueue");
         if ((rc = run.sync()) != SX_OK) return rc;
         hm.mark("sync");
+        if (first) {
+            g->bfs_last_src = src;
+            g->bfs_last_key = okey;
+            g->bfs_last_ce = run.o.cluster_enter;
+            g->bfs_last_dir0 = g->ctx->h_ctl->k;
+        }
         if (g->ctx->h_ctl->done) break;
         dir = g->ctx->h_ctl->dir;
     }

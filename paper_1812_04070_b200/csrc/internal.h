@@ -57,6 +57,7 @@ struct sx_graph_s {
     uint32_t* pp_hubs = nullptr;  // hub ids by slot
     uint32_t* pp_tile_seg = nullptr;
     uint32_t* pp_nzaux = nullptr;   // per active row: the operator's per-row operand
+    uint32_t bfs_last_src = 0xFFFFFFFFu, bfs_last_key = 0, bfs_last_ce = 0, bfs_last_dir0 = 0xFFFFFFFFu;  // sx_bfs start-direction cache
     uint32_t* pp_gnz = nullptr;     // per graph: rows with in-degree > 0 (+ sentinel), for the frontier pulls
     uint32_t* pp_gseg = nullptr;    // per graph: tile -> index in pp_gnz of its first edge's row
     uint64_t pp_gnnz = 0, pp_gntiles = 0;

@@ -408,3 +408,19 @@ def test_empty_and_edgeless_graphs(ctx):
     y, _, _ = Ge.spmv(x, 1)
     assert not y.any()
     Ge.free()
+
+
+def test_bfs_repeated_source_start_cache(ctx, rmat14):
+    """sx_bfs remembers the start direction of the last (source, options): a repeated
+    call enqueues no launch that exits at once; results never depend on it."""
+    G = up(ctx, rmat14)
+    ref0, ref5 = oracle.bfs(rmat14, 0), oracle.bfs(rmat14, 5)
+    lv, st1, _ = G.bfs(0)
+    assert np.array_equal(lv, ref0)
+    lv, st2, _ = G.bfs(0)
+    assert np.array_equal(lv, ref0) and st2["launches"] <= st1["launches"]
+    for src, ref in ((5, ref5), (0, ref0), (5, ref5)):
+        for kw in ({}, dict(cluster_enter=0), dict(force_dir=1)):
+            lv, _, _ = G.bfs(src, **kw)
+            assert np.array_equal(lv, ref), (src, kw)
+    G.free()
