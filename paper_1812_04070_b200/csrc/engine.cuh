@@ -99,6 +99,7 @@ struct Ctl {
         unsigned int nbig[3];  // tasks of degree > CL_BIG deferred to the cluster-wide edge loop
         unsigned int ready;    // BFS: the pull kernel left the frontier as a contiguous list (cnt[iter % 3])
         unsigned long long mf[3];  // BFS: sum of out-degrees of the next frontier
+        unsigned int fmin[2];      // SSSP: far-pile minimum, kept incrementally (two slots by advance parity)
     } cl;
     // --- run statistics per direction of the launch (0 push, 1 pull), one atomic per CTA per launch
     struct alignas(128) StatBlock {
@@ -1189,6 +1190,7 @@ __device__ __forceinline__ void cluster_entry(const Sched& s, uint32_t it, uint3
             cl->mf[i] = 0;
         }
         cl->minv = INF;
+        cl->fmin[0] = cl->fmin[1] = INF;
         cl->ready = 0;
     }
     if (ready) {

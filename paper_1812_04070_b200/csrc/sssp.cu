@@ -574,6 +574,21 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
     const uint64_t lcap = (uint64_t)NCLS * p.s.cstride;  // entries per list; deferred big tasks fill it from the top
     // relax edges [e0, e1) of v, 8 in flight per step: the chain is
     // ids/weights -> atomicMin -> claim (atomicOr) -> append
+    // Far-pile minimum kept incrementally (B200 addition): every far insertion
+    // min-combines its distance into cl->fmin[fsel]; a bucket advance's compaction
+    // leaves the minimum over the vertices it keeps in the other slot.  A bucket
+    // advance then reads one word instead of scanning the far pile (after the
+    // first advance of a launch: the grid kernels' insertions are not tracked).
+    // The value can only undershoot the true pending minimum (an inserted vertex
+    // improved again below hi); the advance then moves nothing and the next one
+    // reads the exact minimum its compaction left.
+    uint32_t fins = INF, fsel = 0;
+    bool fvalid = false;
+    auto flush_fins = [&]() {
+        const uint32_t m = warp_min(fins);
+        if (lane_id() == 0 && m != INF) atomicMin(&cl->fmin[fsel], m);
+        fins = INF;
+    };
     auto relax = [&](uint32_t dv, uint64_t e0, uint64_t e1, uint64_t step, uint32_t* nbm, uint32_t* NL,
                      unsigned int* ncnt) {
         for (uint64_t e = e0; e < e1; e += 8 * step) {
@@ -601,6 +616,7 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
                     cl_append(NL, ncnt, u[k]);
                 } else {
                     bm_set(p.far, u[k]);
+                    fins = min(fins, nd[k]);
                 }
             }
         }
@@ -629,16 +645,20 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
             }
             relax(p.dist[v], beg, end, 1, nbm, NL, ncnt);
         }
+        flush_fins();
         cluster_barrier();
         const uint32_t nbig = vload(&cl->nbig[it % 3]);
-        uint32_t nnext = vload(ncnt);  // issued together with nbig
+        uint32_t nnext = vload(ncnt);  // issued together with nbig and the far minimum
+        uint32_t fmin = vload(&cl->fmin[fsel]);
         if (nbig) {  // high-degree tasks: their edges spread over the whole cluster
             for (uint32_t j = 0; j < nbig; ++j) {
                 const uint32_t v = NL[lcap - 1 - j];
                 relax(p.dist[v], __ldg(p.g.rp + v) + tid, __ldg(p.g.rp + v + 1), T, nbm, NL, ncnt);
             }
+            flush_fins();
             cluster_barrier();
             nnext = vload(ncnt);
+            fmin = vload(&cl->fmin[fsel]);
         }
         ++it;
         ++iters;
@@ -649,15 +669,19 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
             } else {
                 // bucket advance over the far pile
                 uint32_t mn = INF;
-                cluster_words(p.far, p.s.nwords, tid, T, [&](uint64_t wi, uint32_t x) {
-                    word_values(p.dist, wi, x, [&](int, uint32_t d) { mn = min(mn, d); });
-                });
-                mn = warp_min(mn);
-                if (lane_id() == 0 && mn != INF) atomicMin(&cl->minv, mn);
-                cluster_barrier();
-                mn = vload(&cl->minv);
-                cluster_barrier();
-                if (lead0) cl->minv = INF;
+                if (fvalid) {
+                    mn = fmin;
+                } else {
+                    cluster_words(p.far, p.s.nwords, tid, T, [&](uint64_t wi, uint32_t x) {
+                        word_values(p.dist, wi, x, [&](int, uint32_t d) { mn = min(mn, d); });
+                    });
+                    mn = warp_min(mn);
+                    if (lane_id() == 0 && mn != INF) atomicMin(&cl->minv, mn);
+                    cluster_barrier();
+                    mn = vload(&cl->minv);
+                    cluster_barrier();
+                    if (lead0) cl->minv = INF;
+                }
                 if (mn == INF) {
                     done = 1;
                 } else {
@@ -665,10 +689,12 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
                     uint32_t* L2 = p.s.lists[it & 1];
                     unsigned int* c2 = &cl->cnt[it % 3];
                     uint32_t* fbm = p.s.bm[it % 3];
+                    uint32_t rem = INF;  // minimum over the far vertices that stay
                     cluster_compact(p.far, p.s.nwords, tid, T, c2, L2, [&](uint64_t wi, uint32_t f) {
                         uint32_t mv = 0;
                         word_values(p.dist, wi, f, [&](int b, uint32_t d) {
                             if ((uint64_t)d < hi) mv |= 1u << b;
+                            else rem = min(rem, d);
                         });
                         if (mv) {
                             p.far[wi] = f & ~mv;  // single owner of the word
@@ -676,7 +702,12 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
                         }
                         return mv;
                     });
+                    rem = warp_min(rem);
+                    if (lane_id() == 0 && rem != INF) atomicMin(&cl->fmin[fsel ^ 1u], rem);
                     cluster_barrier();
+                    if (lead0) cl->fmin[fsel] = INF;  // read by everyone before the barrier above
+                    fsel ^= 1u;
+                    fvalid = true;
                     nnext = vload(c2);
                     ++ballots;
                     filt = 1;
