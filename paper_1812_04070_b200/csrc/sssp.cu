@@ -317,7 +317,10 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_push(SsspP p) {
                 while (w) {
                     const int b = __ffs(w) - 1;
                     w &= w - 1;
-                    mn = min(mn, p.dist[(wi << 5) + b]);
+                    // a far-flagged vertex improved below hi since has been processed in
+                    // this bucket: only the pending ones (dist >= hi) set the next bucket
+                    const uint32_t d = p.dist[(wi << 5) + b];
+                    if ((uint64_t)d >= hi) mn = min(mn, d);
                 }
             }
             mn = block_min(mn);
