@@ -178,7 +178,10 @@ __device__ __forceinline__ void bfs_exit(const BfsP& p, uint32_t kdir, uint32_t 
 }
 
 // ------------------------------------------------------------------ push
-__global__ void __launch_bounds__(BLOCK, 4) bfs_push(BfsP p) {
+#ifndef SX_PUSH_MINB
+#define SX_PUSH_MINB 3  // measured: 3 CTAs/SM beat 4 (s24 push 58.6 -> 54.5 us; profiles/r1/bfs_variant_sweep.txt)
+#endif
+__global__ void __launch_bounds__(BLOCK, SX_PUSH_MINB) bfs_push(BfsP p) {
     Ctl* c = p.s.ctl;
     const RunState& rs = run_state(c);
     if (rs.done || rs.dir != DIR_PUSH) return;

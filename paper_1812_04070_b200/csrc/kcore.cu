@@ -73,7 +73,10 @@ struct LevelWords {
     }
 };
 
-__global__ void __launch_bounds__(BLOCK, 4) kcore_push(KcoreP p) {
+#ifndef SX_KCORE_MINB
+#define SX_KCORE_MINB 4
+#endif
+__global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
     Ctl* c = p.s.ctl;
     const RunState& rs = run_state(c);
     if (rs.done) return;

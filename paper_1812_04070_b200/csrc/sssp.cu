@@ -116,7 +116,10 @@ __device__ __forceinline__ void sssp_exit(const SsspP& p, uint32_t kdir, uint32_
 }
 
 // ------------------------------------------------------------------ push
-__global__ void __launch_bounds__(BLOCK, 4) sssp_push(SsspP p) {
+#ifndef SX_SSSP_PUSH_MINB
+#define SX_SSSP_PUSH_MINB 4
+#endif
+__global__ void __launch_bounds__(BLOCK, SX_SSSP_PUSH_MINB) sssp_push(SsspP p) {
     Ctl* c = p.s.ctl;
     const RunState& rs = run_state(c);
     if (rs.done || rs.dir != DIR_PUSH) return;
