@@ -333,7 +333,10 @@ constexpr int PROBE = SX_PROBE;
 #define SX_HUB_ILP 4
 #endif
 constexpr int HUB_ILP = SX_HUB_ILP;             // phase 1: rounds of 32 candidates in flight per warp
-constexpr uint32_t LIST_DIV = 8;       // LIST mode when open candidates <= n / LIST_DIV
+#ifndef SX_LIST_DIV
+#define SX_LIST_DIV 8
+#endif
+constexpr uint32_t LIST_DIV = SX_LIST_DIV;  // LIST mode when open candidates <= n / LIST_DIV
 constexpr uint32_t FREC_MAX = 32768;   // record the found vertices as a list when candidates <= this
 constexpr uint32_t CAND_CLS = 2;       // class region of lists[] holding the LIST-mode candidate lists
 constexpr uint32_t REC_STAGE = 256;    // per-warp staging of the LIST-mode record
