@@ -16,7 +16,7 @@
 //             buffering between iterations; fp64 accumulation, fp32 state (BP: fp64).
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
-#include <cub/iterator/counting_input_iterator.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
 #include <cmath>
@@ -659,7 +659,7 @@ sx_status min_pull_plan(sx_graph g) {
     TRYA(sxh::dmalloc(g->ctx, &g->pp_gseg, (gtiles + 1) * 4));
     unsigned long long* dcnt = nullptr;
     TRYA(sxh::dmalloc(g->ctx, &dcnt, 8));
-    cub::CountingInputIterator<uint32_t> it(0);
+    thrust::counting_iterator<uint32_t> it(0);
     size_t tb = 0;
     SX_CU(cub::DeviceSelect::If(nullptr, tb, it, g->pp_gnz, dcnt, (int64_t)n, NzFlag{g->din}, s));
     void* tmp = nullptr;
