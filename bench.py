@@ -458,7 +458,7 @@ def main():
     ap.add_argument("--scale", type=int, default=24, help="R-MAT scale per GPU")
     ap.add_argument("--ef", type=int, default=16)
     ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--delta", type=int, default=1024)
+    ap.add_argument("--delta", type=int, default=4096)  # measured best for C2 (profiles/r1/delta_sweep.txt)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
     ap.add_argument("--ref-budget-s", type=float, default=60.0)
