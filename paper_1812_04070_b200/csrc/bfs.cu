@@ -727,17 +727,23 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) b
                 for (int k = 0; k < 8; ++k) u[k] = e + k * step < e1 ? __ldg(p.g.ci + e + k * step) : INF;
 #pragma unroll
                 for (int k = 0; k < 8; ++k) vw[k] = u[k] != INF ? p.visited[u[k] >> 5] : FULL;
+                // the unvisited candidates' claims issued together, then one append per warp
+                uint32_t ow[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    ow[k] = (vw[k] >> (u[k] & 31)) & 1u ? FULL : atomicOr(p.visited + (u[k] >> 5), 1u << (u[k] & 31));
+                uint32_t sel = 0;
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     edges += u[k] != INF;
-                    if ((vw[k] >> (u[k] & 31)) & 1u) continue;
-                    if (!bm_claim(p.visited, u[k])) continue;
+                    if ((ow[k] >> (u[k] & 31)) & 1u) continue;
                     p.level[u[k]] = lvl;
                     bm_set(nbm, u[k]);
                     mdeg += __ldg(p.g.dout + u[k]);
                     ++reached;
-                    cl_append(NL, ncnt, u[k]);
+                    sel |= 1u << k;
                 }
+                cl_append8(NL, ncnt, u, sel);
             }
         };
         for (uint32_t i = tid; i < ncur; i += T) {

@@ -1065,6 +1065,28 @@ __device__ __forceinline__ void cl_append(uint32_t* list, unsigned int* cnt, uin
     base = __shfl_sync(m, base, leader);
     list[base + __popc(m & lanemask_lt())] = u;
 }
+// Append the u[k] whose bit k is set in sel (k < 8) with ONE returning atomic
+// per warp: each lane's count goes in as four bit-plane ballots, so the
+// exclusive prefix over a sparse active mask needs no shuffles.
+__device__ __forceinline__ void cl_append8(uint32_t* list, unsigned int* cnt, const uint32_t (&u)[8], uint32_t sel) {
+    const uint32_t m = __activemask();
+    const uint32_t c = __popc(sel), lt = lanemask_lt();
+    uint32_t pre = 0, tot = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const uint32_t bb = __ballot_sync(m, (c >> b) & 1u);
+        pre += __popc(bb & lt) << b;
+        tot += __popc(bb) << b;
+    }
+    if (tot == 0) return;
+    const int leader = __ffs(m) - 1;
+    uint32_t base = 0;
+    if ((int)lane_id() == leader) base = atomicAdd(cnt, tot);
+    base = __shfl_sync(m, base, leader) + pre;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        if (sel >> k & 1u) list[base++] = u[k];
+}
 // Visit the nonzero words of a bitmap (nwords a multiple of 4) with 128-bit
 // loads, 4 in flight per thread: f(word index, word).
 template <class F>

@@ -609,6 +609,7 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
             }
 #pragma unroll
             for (int k = 0; k < 8; ++k) old[k] = ok[k] ? atomicMin(p.dist + u[k], nd[k]) : 0u;
+            uint32_t sel = 0;
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 edges += ok[k];
@@ -619,12 +620,14 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
                     // bitmap bit is still set for a hand-over to the grid kernels).
                     // Measured on C2: 61.2 -> 53.6 ms at delta = 1024.
                     bm_set(nbm, u[k]);
-                    cl_append(NL, ncnt, u[k]);
+                    sel |= 1u << k;
                 } else {
                     bm_set(p.far, u[k]);
                     fins = min(fins, nd[k]);
                 }
             }
+            // the step's appends with one returning atomic per warp, not one per edge slot
+            cl_append8(NL, ncnt, u, sel);
         }
     };
     // the current list's size: read once at entry, then carried from the previous
