@@ -12,7 +12,7 @@ path) and never imports it; its only inputs are simgen CSR graphs and vectors.
   kcore_mask C-K  core(v) >= k
   pagerank   C-P  fp64 Jacobi, T steps          (reading 14)
   spmv       C-V  fp64 y = A^T x over in-edges  (north_star)
-  bp         C-BP fp64 log-odds Jacobi          (model = reading 15, "parity unpinned vs paper")
+  bp         C-BP fp64 log-odds Jacobi          (model = reading 15; T=1..4 closed forms)
   wcc        C-W  min vertex id per component   (P:345 names WCC)
   acc_model       the ACC BSP loop and its three filters on tiny graphs
 

@@ -18,9 +18,11 @@
  * in-neighbour rows (CSC), which for an undirected graph are the CSR itself
  * (P:913).  Vertex-state sentinel for "unreached" is 0xFFFFFFFF.
  *
- * Parity pins: tests/test_oracle.py (all functions pinned; BP is pinned to
- * closed forms/invariants only, its model being this build's reading — see
- * DESIGN.md "parity unpinned vs paper" for BP).
+ * Parity pins: tests/test_oracle.py (all functions pinned).  BP's model is
+ * this build's reading 15 (the paper names no model); its recurrence is
+ * pinned at T = 1..4 by hand-derived closed forms and by exact rational BP in
+ * the tanh form (fractions), which fail if any step feeds the prior instead of
+ * the current log-odds.
  */
 #include <math.h>
 #include <stdint.h>

@@ -102,7 +102,7 @@ def test_spmv_bp_rmat20(ctx):
     p = simgen.bp_prior(3, g.n)
     l, _, _ = G.bp(p, 10)
     o, at = oracle.bp(g, p, 10, with_abs_terms=True)
-    assert np.all(np.abs(l - o) <= 1e-5 * (np.abs(o) + at) + 1e-6)
+    assert np.all(np.abs(l - o) <= 1e-5 * (np.abs(o) + at))
     G.free()
 
 

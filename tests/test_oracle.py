@@ -339,6 +339,85 @@ def test_bp_two_vertex_closed_form():
     assert abs(out[1] - math.log(pb / (1 - pb))) < 1e-15
 
 
+def test_bp_two_vertex_multi_step_closed_form():
+    """T = 1, 2, 3 on one unweighted edge (c = 0.75), priors p_a = 0.75, p_b = 0.375
+    (both exact in f32).  Derived by hand in the magnetisation form of the same
+    recurrence (P:885 reading 15): with q = tanh(l/2) = 2b - 1 and theta = 2c - 1,
+    log((c b + (1-c)(1-b)) / (c (1-b) + (1-c) b)) = 2 artanh(theta * q), so
+    q_u' = (x_u + theta q_v) / (1 + x_u theta q_v), x_u = 2 p_u - 1 = tanh(logit(p_u)/2):
+      x_a = 1/2, x_b = -1/4, theta = 1/2
+      t=1: q_a = (1/2 - 1/8)/(1 - 1/16) = 2/5,   q_b = (-1/4 + 1/4)/(...) = 0
+      t=2: q_a = 1/2,                            q_b = (-1/4 + 1/5)/(1 - 1/20) = -1/19
+      t=3: q_a = (1/2 - 1/38)/(1 - 1/76) = 12/25, q_b = (-1/4 + 1/4)/(...) = 0
+    and l = log((1+q)/(1-q)).  A recurrence that fed the prior (or the previous
+    step's message alone) back instead of the current log-odds stops at t=1's
+    values; one that swapped c and 1-c flips the signs."""
+    g = simgen.from_edges(2, [(0, 1)])
+    p = np.array([0.75, 0.375], np.float32)
+    want = {1: (math.log(7 / 3), 0.0), 2: (math.log(3.0), math.log(9 / 10)), 3: (math.log(37 / 13), 0.0)}
+    for T, (la, lb) in want.items():
+        out = oracle.bp(g, p, T)
+        assert abs(out[0] - la) < 1e-13 and abs(out[1] - lb) < 1e-13, (T, out, la, lb)
+
+
+def test_bp_path3_multi_step_closed_form():
+    """3-vertex path a - b - c with unequal couplings, T = 2 by hand (magnetisation
+    form, see above).  Weights 255 (c = 3/4, theta = 1/2) on a-b and 1 (c = 1/4,
+    theta = -1/2) on b-c; priors 0.75, 0.5, 0.25 -> x = (1/2, 0, -1/2).
+      t=1: q_a = x_a + 0 = 1/2 (b's q is 0);  q_c = -1/2;
+           q_b = tanh(0 + artanh(1/2 * 1/2) + artanh(-1/2 * -1/2)) = (1/4 + 1/4)/(1 + 1/16) = 8/17
+      t=2: q_a = (1/2 + 1/2 * 8/17)/(1 + 1/2 * 1/2 * 8/17) = (25/34)/(19/17) = 25/38
+           q_c = (-1/2 - 1/2 * 8/17)/(1 + (-1/2)(-1/2)(8/17)) = -25/38
+           q_b = same as t=1 (a, c unchanged at t=1): 8/17
+    l = log((1+q)/(1-q)): l_a(2) = log(63/13), l_c(2) = -log(63/13), l_b(2) = log(25/9)."""
+    g = simgen.from_edges(3, [(0, 1), (1, 2)], [255, 1])
+    p = np.array([0.75, 0.5, 0.25], np.float32)
+    out = oracle.bp(g, p, 2)
+    want = [math.log(63 / 13), math.log(25 / 9), -math.log(63 / 13)]
+    assert np.allclose(out, want, rtol=0, atol=1e-13), (out, want)
+    out1 = oracle.bp(g, p, 1)
+    assert np.allclose(out1, [math.log(3.0), math.log(25 / 9), -math.log(3.0)], rtol=0, atol=1e-13)
+
+
+def _bp_exact_rational(n, edges, weights, p, T):
+    """Exact BP in rational arithmetic via the tanh rule (fractions.Fraction):
+    q_u' = tanh(artanh(x_u) + sum_v artanh(theta_uv q_v)) folded with
+    tanh(a + b) = (tanh a + tanh b) / (1 + tanh a tanh b); theta = 2c - 1 with
+    c = 1/4 + (w-1)/508 (reading 15).  Independent of the oracle's log-ratio form."""
+    from fractions import Fraction as F
+    x = [F(float(pi)) * 2 - 1 for pi in p]
+    nb = [[] for _ in range(n)]
+    for (a, b), w in zip(edges, weights):
+        th = 2 * (F(1, 4) + F(w - 1, 508)) - 1
+        nb[a].append((b, th))
+        nb[b].append((a, th))
+    q = list(x)
+    for _ in range(T):
+        qn = []
+        for u in range(n):
+            s = x[u]
+            for v, th in nb[u]:
+                m = th * q[v]
+                s = (s + m) / (1 + s * m)
+            qn.append(s)
+        q = qn
+    return [math.log((1 + qi) / (1 - qi)) for qi in q]
+
+
+def test_bp_loopy_graph_exact_rationals():
+    """A triangle with a pendant and mixed couplings, T = 1..4, against exact
+    rational BP (tanh rule): catches a wrong coupling map, a transposed message,
+    or messages taken from the prior / previous message instead of the current
+    log-odds at every step of a loopy recurrence."""
+    edges = [(0, 1), (1, 2), (2, 0), (2, 3)]
+    weights = [200, 40, 255, 1]
+    p = np.array([0.625, 0.25, 0.875, 0.5], np.float32)
+    g = simgen.from_edges(4, edges, weights)
+    for T in (1, 2, 3, 4):
+        want = _bp_exact_rational(4, edges, weights, p, T)
+        assert np.allclose(oracle.bp(g, p, T), want, rtol=0, atol=1e-12), T
+
+
 def test_bp_antisymmetry():
     # flipping every prior p -> 1-p negates every log-odds (psi is symmetric under x -> 1-x)
     g = simgen.rmat(8, wmin=1, wmax=255)
