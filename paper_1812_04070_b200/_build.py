@@ -40,14 +40,33 @@ def deps():
         [os.path.join(os.path.dirname(HERE), "include", "simdx.h")]
 
 
+def _compile_all(out: str, extra: list) -> None:
+    """One nvcc per translation unit, in parallel (the .cu files are independent:
+    no relocatable device code), then one link into the shared library."""
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = out + ".objs"
+    os.makedirs(objdir, exist_ok=True)
+    cflags = [f for f in FLAGS if f != "-shared"]
+    inc = [f for f in link_flags() if f.startswith("-I")] + [link_flags()[1]]
+
+    def one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        subprocess.check_call([NVCC, *cflags, *extra, "-c", "-o", obj, src, *inc])
+        return obj
+
+    with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(one, sources()))
+    subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
+                           "-o", out + ".tmp", *objs, *link_flags()])
+    os.replace(out + ".tmp", out)
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(LIB):
         t = os.path.getmtime(LIB)
         if all(os.path.getmtime(d) <= t for d in deps()):
             return LIB
-    cmd = [NVCC, *FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-o", LIB + ".tmp", *sources(), *link_flags()]
-    subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
+    _compile_all(LIB, ["-Xptxas", "-v"] if verbose else [])
     return LIB
 
 
@@ -55,7 +74,7 @@ def build_variant(name: str, defines: list) -> str:
     """An experiment build (profiles/: loaded with SIMDX_LIB=...), e.g. -DSX_PROBE=8."""
     out = os.path.join(os.path.dirname(HERE), "build", f"libsimdx_{name}.so")
     os.makedirs(os.path.dirname(out), exist_ok=True)
-    subprocess.check_call([NVCC, *FLAGS, *defines, "-o", out, *sources(), *link_flags()])
+    _compile_all(out, list(defines))
     return out
 
 

@@ -1068,7 +1068,10 @@ __device__ __forceinline__ void cl_append(uint32_t* list, unsigned int* cnt, uin
 // Append the u[k] whose bit k is set in sel (k < 8) with ONE returning atomic
 // per warp: each lane's count goes in as four bit-plane ballots, so the
 // exclusive prefix over a sparse active mask needs no shuffles.
-__device__ __forceinline__ void cl_append8(uint32_t* list, unsigned int* cnt, const uint32_t (&u)[8], uint32_t sel) {
+// Entries at positions >= cap are counted but not written: the caller sees
+// count > cap after its barrier and rebuilds the frontier from the bitmap.
+__device__ __forceinline__ void cl_append8(uint32_t* list, unsigned int* cnt, const uint32_t (&u)[8], uint32_t sel,
+                                           uint32_t cap = 0xFFFFFFFFu) {
     const uint32_t m = __activemask();
     const uint32_t c = __popc(sel), lt = lanemask_lt();
     uint32_t pre = 0, tot = 0;
@@ -1085,7 +1088,10 @@ __device__ __forceinline__ void cl_append8(uint32_t* list, unsigned int* cnt, co
     base = __shfl_sync(m, base, leader) + pre;
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-        if (sel >> k & 1u) list[base++] = u[k];
+        if (sel >> k & 1u) {
+            if (base < cap) list[base] = u[k];
+            ++base;
+        }
 }
 // Visit the nonzero words of a bitmap (nwords a multiple of 4) with 128-bit
 // loads, 4 in flight per thread: f(word index, word).

@@ -578,6 +578,15 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
     uint32_t iters = 0, ballots = 0, done = 0, dir = DIR_CLUSTER;
     cluster_entry(p.s, it, tid, T);
     const uint64_t lcap = (uint64_t)NCLS * p.s.cstride;  // entries per list; deferred big tasks fill it from the top
+    // Without a claim a vertex improved k times in an iteration is listed k
+    // times, so the appends are bounded only by the improvements.  They may fill
+    // the lower half of the list (>= 2n entries); the deferred big tasks come
+    // from the current list, which never exceeds that half either, and take the
+    // upper half from the top.  An iteration whose appends overflow the half
+    // (dense graphs) hands the frontier to the grid kernels, which rebuild their
+    // lists from the bitmap (every in-bucket improvement is in nbm) - the JIT
+    // controller's "overflow -> ballot".
+    const uint32_t acap = lcap / 2 < 0xFFFFFFFFull ? (uint32_t)(lcap / 2) : 0xFFFFFFFFu;
     // relax edges [e0, e1) of v, 8 in flight per step: the chain is
     // ids/weights -> atomicMin -> claim (atomicOr) -> append
     // Far-pile minimum kept incrementally (B200 addition): every far insertion
@@ -627,7 +636,7 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
                 }
             }
             // the step's appends with one returning atomic per warp, not one per edge slot
-            cl_append8(NL, ncnt, u, sel);
+            cl_append8(NL, ncnt, u, sel, acap);
         }
     };
     // the current list's size: read once at entry, then carried from the previous
@@ -672,6 +681,7 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
         ++it;
         ++iters;
         uint32_t filt = 0;
+        const bool overflow = nnext > acap;
         if (nnext == 0) {
             if (p.delta == 0) {
                 done = 1;
@@ -745,7 +755,7 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
             done = 1;
             break;
         }
-        if (nnext > 8u * p.s.cluster_enter) {  // frontier too big for one cluster: back to the grid
+        if (overflow || nnext > 8u * p.s.cluster_enter) {  // frontier too big for one cluster: back to the grid
             dir = DIR_PUSH;
             break;
         }

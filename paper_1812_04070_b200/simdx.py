@@ -137,10 +137,26 @@ def _ptr(x) -> Optional[int]:
     if x is None:
         return None
     if _is_torch(x):
-        assert x.is_contiguous()
+        if not x.is_contiguous():
+            raise ValueError("tensors passed to the C ABI must be contiguous")
         return x.data_ptr()
-    assert isinstance(x, np.ndarray) and x.flags["C_CONTIGUOUS"], "host arrays must be C-contiguous numpy arrays"
+    if not (isinstance(x, np.ndarray) and x.flags["C_CONTIGUOUS"]):
+        raise ValueError("host arrays must be C-contiguous numpy arrays")
     return x.ctypes.data
+
+
+def _ptr_n(x, n: int, what: str) -> Optional[int]:
+    """Pointer to a caller array the C side reads or writes n 4-byte elements of:
+    checked for length and element size (the C ABI cannot see either)."""
+    if x is None:
+        return None
+    size = x.numel() if _is_torch(x) else getattr(x, "size", None)
+    item = x.element_size() if _is_torch(x) else getattr(getattr(x, "dtype", None), "itemsize", None)
+    if item != 4:
+        raise ValueError(f"{what}: 4-byte elements required (got itemsize {item})")
+    if size is None or size < n:
+        raise ValueError(f"{what}: {n} elements required (got {size})")
+    return _ptr(x)
 
 
 def _on_device(x) -> bool:
@@ -256,39 +272,50 @@ def sx_graph_info(g):
     return a.value, b.value, c.value, d.value
 
 
-def _run(fn, name, g, out, opts, args_before, args_after=()):
+def _nv(g, n):
+    """Vertex count of g's output arrays (this rank's slice); n given by the caller skips the query."""
+    if n is not None:
+        return n
+    a, _, lo, hi = sx_graph_info(g)
+    return hi - lo
+
+
+def _run(fn, name, g, out, opts, args_before, args_after=(), n=None):
     st = sx_stats()
     o = opts if opts is not None else sx_opts_default()
-    _check(fn(g, *args_before, ctypes.byref(o), *args_after, _ptr(out), ctypes.byref(st)), name)
+    _check(fn(g, *args_before, ctypes.byref(o), *args_after, _ptr_n(out, _nv(g, n), name + " out"),
+              ctypes.byref(st)), name)
     return st
 
 
-def sx_bfs(g, src, opts, level_out):
-    return _run(_lib.sx_bfs, "sx_bfs", g, level_out, opts, (src,))
+def sx_bfs(g, src, opts, level_out, n=None):
+    return _run(_lib.sx_bfs, "sx_bfs", g, level_out, opts, (src,), n=n)
 
 
-def sx_sssp(g, src, delta, opts, dist_out):
-    return _run(_lib.sx_sssp, "sx_sssp", g, dist_out, opts, (src, delta))
+def sx_sssp(g, src, delta, opts, dist_out, n=None):
+    return _run(_lib.sx_sssp, "sx_sssp", g, dist_out, opts, (src, delta), n=n)
 
 
-def sx_pagerank(g, damping, iters, opts, rank_out):
-    return _run(_lib.sx_pagerank, "sx_pagerank", g, rank_out, opts, (damping, iters))
+def sx_pagerank(g, damping, iters, opts, rank_out, n=None):
+    return _run(_lib.sx_pagerank, "sx_pagerank", g, rank_out, opts, (damping, iters), n=n)
 
 
-def sx_kcore(g, k, opts, core_out):
-    return _run(_lib.sx_kcore, "sx_kcore", g, core_out, opts, (k,))
+def sx_kcore(g, k, opts, core_out, n=None):
+    return _run(_lib.sx_kcore, "sx_kcore", g, core_out, opts, (k,), n=n)
 
 
-def sx_spmv(g, x, iters, opts, y_out):
-    return _run(_lib.sx_spmv, "sx_spmv", g, y_out, opts, (_ptr(x), iters))
+def sx_spmv(g, x, iters, opts, y_out, n=None):
+    n = _nv(g, n)
+    return _run(_lib.sx_spmv, "sx_spmv", g, y_out, opts, (_ptr_n(x, n, "sx_spmv x"), iters), n=n)
 
 
-def sx_wcc(g, opts, label_out):
-    return _run(_lib.sx_wcc, "sx_wcc", g, label_out, opts, ())
+def sx_wcc(g, opts, label_out, n=None):
+    return _run(_lib.sx_wcc, "sx_wcc", g, label_out, opts, (), n=n)
 
 
-def sx_bp(g, prior, iters, opts, out):
-    return _run(_lib.sx_bp, "sx_bp", g, out, opts, (_ptr(prior), iters))
+def sx_bp(g, prior, iters, opts, out, n=None):
+    n = _nv(g, n)
+    return _run(_lib.sx_bp, "sx_bp", g, out, opts, (_ptr_n(prior, n, "sx_bp prior"), iters), n=n)
 
 
 # ---------------------------------------------------------------- conveniences
@@ -392,43 +419,43 @@ class Graph:
     def bfs(self, src: int, out=None, **kw):
         out = np.empty(self.n, np.uint32) if out is None else out
         o, buf = self._opts(dict(kw))
-        st = sx_bfs(self.h, src, o, out)
+        st = sx_bfs(self.h, src, o, out, self.n)
         return out, st.as_dict(), self._trace(buf, st)
 
     def sssp(self, src: int, delta: int = 0, out=None, **kw):
         out = np.empty(self.n, np.uint32) if out is None else out
         o, buf = self._opts(dict(kw))
-        st = sx_sssp(self.h, src, delta, o, out)
+        st = sx_sssp(self.h, src, delta, o, out, self.n)
         return out, st.as_dict(), self._trace(buf, st)
 
     def pagerank(self, damping: float = 0.85, iters: int = 20, out=None, **kw):
         out = np.empty(self.n, np.float32) if out is None else out
         o, buf = self._opts(dict(kw))
-        st = sx_pagerank(self.h, damping, iters, o, out)
+        st = sx_pagerank(self.h, damping, iters, o, out, self.n)
         return out, st.as_dict(), self._trace(buf, st)
 
     def kcore(self, k: int = 0, out=None, **kw):
         out = np.empty(self.n, np.uint32) if out is None else out
         o, buf = self._opts(dict(kw))
-        st = sx_kcore(self.h, k, o, out)
+        st = sx_kcore(self.h, k, o, out, self.n)
         return out, st.as_dict(), self._trace(buf, st)
 
     def wcc(self, out=None, **kw):
         out = np.empty(self.n, np.uint32) if out is None else out
         o, buf = self._opts(dict(kw))
-        st = sx_wcc(self.h, o, out)
+        st = sx_wcc(self.h, o, out, self.n)
         return out, st.as_dict(), self._trace(buf, st)
 
     def spmv(self, x, iters: int = 1, out=None, **kw):
         out = np.empty(self.n, np.float32) if out is None else out
         o, buf = self._opts(dict(kw))
-        st = sx_spmv(self.h, x, iters, o, out)
+        st = sx_spmv(self.h, x, iters, o, out, self.n)
         return out, st.as_dict(), self._trace(buf, st)
 
     def bp(self, prior, iters: int = 10, out=None, **kw):
         out = np.empty(self.n, np.float32) if out is None else out
         o, buf = self._opts(dict(kw))
-        st = sx_bp(self.h, prior, iters, o, out)
+        st = sx_bp(self.h, prior, iters, o, out, self.n)
         return out, st.as_dict(), self._trace(buf, st)
 
 

@@ -67,3 +67,20 @@ def test_trace_and_stats_struct_sizes():
     from paper_1812_04070_b200 import simdx
     assert ctypes.sizeof(simdx.sx_trace_rec) == 64
     assert ctypes.sizeof(simdx.sx_stats) == 4 * 4 + 3 * 8 + 6 * 8 + 2 * 4
+
+
+def test_binding_checks_caller_buffers():
+    """Output / input arrays are checked for length and element size before the
+    C call (the C side writes n 4-byte elements and cannot see either)."""
+    import numpy as np
+    from paper_1812_04070_b200 import simdx
+    with pytest.raises(ValueError):
+        simdx.sx_bfs(None, 0, None, np.empty(3, np.uint32), n=10)
+    with pytest.raises(ValueError):
+        simdx.sx_sssp(None, 0, 0, None, np.empty(10, np.uint64), n=10)
+    with pytest.raises(ValueError):
+        simdx.sx_pagerank(None, 0.85, 20, None, np.empty((10, 2), np.float32)[:, 0], n=10)
+    with pytest.raises(ValueError):
+        simdx.sx_spmv(None, np.empty(9, np.float32), 1, None, np.empty(10, np.float32), n=10)
+    with pytest.raises(ValueError):
+        simdx.sx_bp(None, np.empty(10, np.float64), 1, None, np.empty(10, np.float32), n=10)

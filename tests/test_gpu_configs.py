@@ -42,7 +42,7 @@ def test_c2_sssp_road_grid(ctx):
     g = simgen.grid(2048, 2048, seed=1, wmin=1, wmax=255)
     ref = oracle.sssp(g, 0)
     G = ctx.upload(g)
-    for delta in (0, 1024):
+    for delta in (0, 1024, 4096):  # 4096 = bench.py's delta
         d, st, tr = G.sssp(0, delta, trace_cap=16)
         assert np.array_equal(d, ref), delta
         if delta == 0:
@@ -110,6 +110,20 @@ def test_barrier_roofline(ctx):
     from paper_1812_04070_b200 import simdx
     us, ctas = simdx.sx_barrier_bench(ctx.h, 20000)
     assert ctas >= 148 and 0.1 < us < 50.0
+
+
+def test_bench_extra_sssp_rmat24(ctx):
+    """bench.py's SSSP extra: R-MAT scale 24, weights 1..255, src 0, delta 4096
+    (and 1024), every distance against the oracle's Dijkstra."""
+    import torch
+    g = simgen.rmat(24, 16, 1, wmin=1, wmax=255)
+    ref = oracle.sssp(g, 0)
+    G = ctx.upload(g)
+    out = torch.empty(g.n, dtype=torch.int32, device="cuda:0")
+    for delta in (4096, 1024):
+        G.sssp(0, delta, out=out)
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), ref), delta
+    G.free()
 
 
 def test_wcc_rmat24(ctx, rmat24):

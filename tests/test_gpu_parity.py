@@ -230,6 +230,34 @@ def test_errors(ctx):
     assert e.value.status == simdx.SX_E_INVALID
 
 
+@pytest.mark.parametrize("directed", [False, True])
+def test_dense_sssp_wcc_cluster_tail(ctx, directed):
+    """Dense weighted graphs in the one-cluster tail: without a claim
+    every improvement is an append, so an iteration can produce several times n
+    entries; the appends are bounded and an overflowing iteration goes back to
+    the grid kernels.  K_1200 with random u8 weights, push only, delta 0 and 64."""
+    n = 1200
+    rng = np.random.default_rng(11)
+    edges = [(a, b) for a in range(n) for b in range(a + 1, n)]
+    if directed:
+        edges += [(b, a) for a, b in edges]
+    w = rng.integers(1, 256, len(edges))
+    g = simgen.from_edges(n, edges, w, symmetric=not directed)
+    G = up(ctx, g)
+    try:
+        for src in (0, n - 1):
+            ref = oracle.sssp(g, src)
+            for delta in (0, 64):
+                for mode in (dict(force_dir=1, cluster_enter=1 << 20), dict(cluster_enter=1 << 20), dict()):
+                    d, _, _ = G.sssp(src, delta, **mode)
+                    assert np.array_equal(d, ref), (src, delta, mode)
+        if not directed:
+            lab, _, _ = G.wcc(force_dir=1, cluster_enter=1 << 20)
+            assert np.array_equal(lab, oracle.wcc(g))
+    finally:
+        G.free()
+
+
 def test_directed_bfs_sssp_with_csc(ctx):
     g = simgen.random_graph(2000, 12000, 9, wmin=1, wmax=255, symmetric=False)
     G = up(ctx, g)
