@@ -165,9 +165,10 @@ def run_single(args):
     G = ctx.upload_device(dg)
     n = dg.n
     level = torch.empty(n, dtype=torch.int32, device=dev)
+    bkw = {} if args.fusion == 1 else {"fusion": args.fusion}
     for _ in range(args.warmup):
-        G.bfs(0, out=level)
-    _, st, trace = G.bfs(0, out=level, trace_cap=64)
+        G.bfs(0, out=level, **bkw)
+    _, st, trace = G.bfs(0, out=level, trace_cap=64, **bkw)
     lv = level.cpu().numpy().view(np.uint32)
     log(f"[bench] BFS stats: {st}")
     log("[bench] BFS trace: " + " | ".join(
@@ -178,7 +179,7 @@ def run_single(args):
     acc = dict(launches=0, ms_push=0.0, ms_pull=0.0, b_push=0.0, b_pull=0.0, l_push=0, l_pull=0)
 
     def step():
-        _, s, _ = G.bfs(0, out=level)
+        _, s, _ = G.bfs(0, out=level, **bkw)
         acc["launches"] += 2 + s["launches"]  # bfs_init + persistent launches + the control-tail copy kernel
         acc["ms_push"] += s["ms_push"]
         acc["ms_pull"] += s["ms_pull"]
@@ -458,6 +459,8 @@ def main():
     ap.add_argument("--scale", type=int, default=24, help="R-MAT scale per GPU")
     ap.add_argument("--ef", type=int, default=16)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--fusion", type=int, default=1, choices=[0, 1, 2],
+                    help="0 none, 1 selective (P:773-778), 2 all (one launch per BFS)")
     ap.add_argument("--delta", type=int, default=4096)  # measured best for C2 (profiles/r1/delta_sweep.txt)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)

@@ -86,15 +86,30 @@ __device__ __forceinline__ uint32_t hub_id(uint32_t h) { return h == INF ? INF :
 __device__ __forceinline__ bool hub_sole(uint32_t h) { return h != INF && (h & HUB_SOLE); }
 
 constexpr uint32_t CL_EDGES = 32;
+constexpr uint32_t DIR_NOCLUSTER = 0x100;  // bfs_init flag: no cluster start (all fusion)
 __device__ __forceinline__ bool cluster_ok(const Sched& s, uint64_t nf, uint64_t mf) {
     return s.cluster_enter && s.fusion && s.force_filter != 2 && s.force_dir != 2 && nf > 0 &&
            nf <= s.cluster_enter && mf <= (uint64_t)CL_EDGES * s.cluster_enter;
 }
 
+// SX_BFS_MARKS (profiling builds): extra trace records from CTA 0 (dir = 16 + id)
+#ifdef SX_BFS_MARKS
+#define BFS_MARK(id)                                                          \
+    do {                                                                      \
+        const uint32_t z_[NCLS] = {0u, 0u, 0u, 0u};                           \
+        trace_put(p.s, 1000u + (id), 16u + (id), 0u, z_, 0, 0, 0);            \
+    } while (0)
+#else
+#define BFS_MARK(id) \
+    do {             \
+    } while (0)
+#endif
+
 // Per-run state in one grid-stride pass: level = INF (0 at src), visited and
 // the three frontier bitmaps zero (src's bit set in visited and bm[0]); block 0
 // also seeds the control block and the first list.
-__global__ void __launch_bounds__(BLOCK) bfs_init(BfsP p, uint32_t src, uint32_t dir) {
+template <bool ALL, bool CLUSTER = !ALL>
+__device__ __forceinline__ void bfs_init_body(const BfsP& p, uint32_t src, uint32_t dir) {
     const uint64_t n = p.g.n, T = gthreads(), tid = gtid();
     if (((uintptr_t)p.level & 15u) == 0) {
         uint4* L4 = reinterpret_cast<uint4*>(p.level);
@@ -133,11 +148,16 @@ __global__ void __launch_bounds__(BLOCK) bfs_init(BfsP p, uint32_t src, uint32_t
     }
     if (blockIdx.x != 0) return;
     Ctl* c = p.s.ctl;
-    {   // the whole control block starts at zero (replaces a host-enqueued memset per call)
+    if (!ALL) {  // the whole control block starts at zero (replaces a host-enqueued memset per call)
         uint4* C4 = reinterpret_cast<uint4*>(c);
         for (uint32_t i = threadIdx.x; i < sizeof(Ctl) / 16; i += BLOCK) C4[i] = make_uint4(0u, 0u, 0u, 0u);
-        __syncthreads();
+    } else {  // inside the fused launch: not the barrier halves in use, not the launch count
+        uint32_t* W = reinterpret_cast<uint32_t*>(c);
+        constexpr uint32_t w0 = offsetof(Ctl, line) / 4, wl = offsetof(Ctl, launch) / 4;
+        for (uint32_t i = w0 + threadIdx.x; i < sizeof(Ctl) / 4; i += BLOCK)
+            if (i != wl) W[i] = 0u;
     }
+    __syncthreads();
     if (threadIdx.x < 32)
         for (int i = 0; i < 3; ++i) reset_line_warp(&c->line[i]);
     if (threadIdx.x != 0) return;
@@ -148,7 +168,7 @@ __global__ void __launch_bounds__(BLOCK) bfs_init(BfsP p, uint32_t src, uint32_t
     p.s.lists[0][(uint64_t)k * p.s.cstride] = src;
     c->m_u = p.g.m - d;
     c->nf_prev = 1;
-    if (dir == DIR_PUSH && cluster_ok(p.s, 1, d)) dir = DIR_CLUSTER;  // low-degree source: start on one cluster
+    if (CLUSTER && dir == DIR_PUSH && cluster_ok(p.s, 1, d)) dir = DIR_CLUSTER;  // low-degree source: start on one cluster
     c->dir = dir;
     c->k = dir;  // the start direction, for the host (k is unused by BFS)
     c->lists_ready = dir == DIR_PUSH ? 1u : 0u;
@@ -157,10 +177,20 @@ __global__ void __launch_bounds__(BLOCK) bfs_init(BfsP p, uint32_t src, uint32_t
     c->done = 0;
     c->st[0].reached = 1;
 }
+__global__ void __launch_bounds__(BLOCK) bfs_init(BfsP p, uint32_t src, uint32_t dir) {
+    if (dir & DIR_NOCLUSTER) bfs_init_body<false, false>(p, src, dir & ~DIR_NOCLUSTER);
+    else bfs_init_body<false, true>(p, src, dir);
+}
 
+// End of a direction phase.  Selective fusion (ALL = false): the kernel exits;
+// CTA 0 leaves the run state in the control block for the next launch.  All
+// fusion (ALL = true): the next phase runs in the same launch; every CTA took
+// the same decisions from the same counters, so each writes its own copy of
+// the run state (shared memory) and CTA 0 also stores it for the host.
+template <bool ALL>
 __device__ __forceinline__ void bfs_exit(const BfsP& p, uint32_t kdir, uint32_t it, uint64_t m_u, uint32_t nf_prev,
                                          uint32_t dir, uint32_t done, uint32_t ready, uint32_t slotted,
-                                         const uint32_t (&cnt)[NCLS], Stats& st) {
+                                         const uint32_t (&cnt)[NCLS], Stats& st, RunState* rs_next) {
     Ctl* c = p.s.ctl;
     flush_stats(c, st, kdir);
     if (lead()) {
@@ -172,8 +202,24 @@ __device__ __forceinline__ void bfs_exit(const BfsP& p, uint32_t kdir, uint32_t 
         c->lists_ready = ready;
         c->slotted = slotted;
         for (int i = 0; i < NCLS; ++i) c->cur_count[i] = cnt[i];
-        grid_end(c);
-        c->launch += 1;
+        if (!ALL) {
+            grid_end(c);
+            c->launch += 1;
+        }
+    }
+    if (ALL) {
+        __syncthreads();  // every thread has read the current copy
+        if (threadIdx.x == 0) {
+            rs_next->iter = it;
+            rs_next->m_u = m_u;
+            rs_next->nf_prev = nf_prev;
+            rs_next->dir = dir;
+            rs_next->done = done;
+            rs_next->lists_ready = ready;
+            rs_next->slotted = slotted;
+            for (int i = 0; i < NCLS; ++i) rs_next->cur_count[i] = cnt[i];
+        }
+        __syncthreads();
     }
 }
 
@@ -181,24 +227,30 @@ __device__ __forceinline__ void bfs_exit(const BfsP& p, uint32_t kdir, uint32_t 
 #ifndef SX_PUSH_MINB
 #define SX_PUSH_MINB 3  // measured: 3 CTAs/SM beat 4 (s24 push 58.6 -> 54.5 us; profiles/r1/bfs_variant_sweep.txt)
 #endif
-__global__ void __launch_bounds__(BLOCK, SX_PUSH_MINB) bfs_push(BfsP p) {
+template <bool ALL>
+__device__ __forceinline__ bool push_phase(const BfsP& p, RunState& rs) {
     Ctl* c = p.s.ctl;
-    const RunState& rs = run_state(c);
-    if (rs.done || rs.dir != DIR_PUSH) return;
     stage_init();
-    grid_begin(rs.launch);
+    __syncthreads();
     uint32_t it = rs.iter;
     uint64_t m_u = rs.m_u;
     uint32_t nf_prev = rs.nf_prev;
     uint32_t cnt[NCLS];
     Stats st;
     uint32_t dir = DIR_PUSH, done = 0, ready = 1, slotted = 0;
-    if (!rs.lists_ready) {
+    uint32_t local_n = 0;  // > 0: this iteration's tasks are the flat found list of the pull (CTA-local binning)
+    if (rs.lists_ready == 2) {
+        // entering push from pull with the found vertices recorded as one list
+        // (online filter, <= FREC_MAX entries): no bitmap scan, no class split
+        local_n = vload(&c->cl.cnt[it % 3]);
+        for (int i = 0; i < NCLS; ++i) cnt[i] = 0;
+        if (local_n == 0) view_contig(cnt);
+    } else if (!rs.lists_ready) {
         // entering push from pull: the frontier exists only as a bitmap -> ballot filter
         if (!ballot_filter(BitmapWords{p.s.bm[it % 3]}, p.s, BallotOut{p.s.lists[it & 1], p.s.cstride, p.g.dout}, cnt))
-            return;
+            return false;
         st.scanned += p.s.nwords * 32;
-        if (!grid_sync(c)) return;
+        if (!grid_sync(c)) return false;
         view_contig(cnt);
     } else if (rs.slotted) {
         view_slots(&c->line[it % 3], p.s, cnt);
@@ -214,7 +266,7 @@ __global__ void __launch_bounds__(BLOCK, SX_PUSH_MINB) bfs_push(BfsP p) {
         uint32_t* nbm = p.s.bm[(it + 1) % 3];
         const uint32_t lvl = it + 1;
         uint64_t mdeg = 0, edges = 0, reached = 0;
-        for_tasks(p.s.lists[it & 1], p.s, cnt, [&](uint32_t v, uint64_t rank, uint64_t size, uint32_t) {
+        auto visit = [&](uint32_t v, uint64_t rank, uint64_t size, uint32_t) {
             const uint64_t beg = __ldg(p.g.rp + v), end = __ldg(p.g.rp + v + 1);
             // up to 4 edges per step: visited words, claims and the claimed
             // vertices' degrees are each issued together
@@ -245,17 +297,24 @@ __global__ void __launch_bounds__(BLOCK, SX_PUSH_MINB) bfs_push(BfsP p) {
                     online_record(nx, nlists, p.s, u[j], cls_of(du[j], p.s));
                 }
             });
-        });
+        };
+        if (local_n) for_list_local(p.s.lists[it & 1], local_n, p.s, p.g.dout, visit);
+        else for_tasks(p.s.lists[it & 1], p.s, cnt, visit);
+        BFS_MARK(2);
         stage_flush(nx, nlists, p.s);
         st.edges += edges;
         st.reached += reached;
-        if (lead()) st.entries += sum4(cnt);
+        if (lead()) st.entries += local_n ? local_n : sum4(cnt);
         {
             uint64_t v[1] = {mdeg};
             block_sum<1>(v);
             if (threadIdx.x == 0 && v[0]) atomicAdd(&nx->s[my_slot()].mdeg, (unsigned long long)v[0]);
         }
-        if (!grid_sync(c)) return;
+        if (!grid_sync(c)) return false;
+        if (local_n) {
+            if (lead()) c->cl.cnt[it % 3] = 0;  // every CTA read the count before the barrier above
+            local_n = 0;
+        }
         LineSum ls;
         uint32_t vcnt[NCLS];
         read_line_view(nx, p.s, ls, vcnt);
@@ -282,7 +341,7 @@ __global__ void __launch_bounds__(BLOCK, SX_PUSH_MINB) bfs_push(BfsP p) {
             ready = 0;
             break;
         }
-        if (cluster_ok(p.s, nf, mf)) {
+        if (!ALL && cluster_ok(p.s, nf, mf)) {
             dir = DIR_CLUSTER;
             ready = 0;
             break;
@@ -290,8 +349,8 @@ __global__ void __launch_bounds__(BLOCK, SX_PUSH_MINB) bfs_push(BfsP p) {
         if (overflow) {
             ++st.ballot;
             st.scanned += p.s.nwords * 32;
-            if (!ballot_filter(BitmapWords{nbm}, p.s, BallotOut{p.s.lists[it & 1], p.s.cstride, p.g.dout}, cnt)) return;
-            if (!grid_sync(c)) return;
+            if (!ballot_filter(BitmapWords{nbm}, p.s, BallotOut{p.s.lists[it & 1], p.s.cstride, p.g.dout}, cnt)) return false;
+            if (!grid_sync(c)) return false;
             view_contig(cnt);
             slotted = 0;
         } else {
@@ -300,7 +359,14 @@ __global__ void __launch_bounds__(BLOCK, SX_PUSH_MINB) bfs_push(BfsP p) {
         }
         if (!p.s.fusion) break;
     }
-    bfs_exit(p, DIR_PUSH, it, m_u, nf_prev, dir, done, ready, slotted, cnt, st);
+    bfs_exit<ALL>(p, DIR_PUSH, it, m_u, nf_prev, dir, done, ready, slotted, cnt, st, &rs);
+    return true;
+}
+__global__ void __launch_bounds__(BLOCK, SX_PUSH_MINB) bfs_push(BfsP p) {
+    RunState& rs = const_cast<RunState&>(run_state(p.s.ctl));
+    if (rs.done || rs.dir != DIR_PUSH) return;
+    grid_begin(rs.launch);
+    push_phase<false>(p, rs);
 }
 
 // ------------------------------------------------------------------ pull
@@ -336,16 +402,21 @@ constexpr int HUB_ILP = SX_HUB_ILP;             // phase 1: rounds of 32 candida
 #ifndef SX_LIST_DIV
 #define SX_LIST_DIV 8
 #endif
-constexpr uint32_t LIST_DIV = SX_LIST_DIV;  // LIST mode when open candidates <= n / LIST_DIV
+constexpr uint32_t LIST_DIV = SX_LIST_DIV;
+#ifndef SX_TILE_ILP
+#define SX_TILE_ILP 8
+#endif
+#ifndef SX_TILE_STREAM
+#define SX_TILE_STREAM 0  // TILE-mode phase 1 streamed per bitmap word (1) or over a compacted candidate list (0)
+#endif
+constexpr uint32_t TILE_ILP = SX_TILE_ILP;  // TILE mode phase 1: bitmap words (x 32 vertices) in flight per warp  // LIST mode when open candidates <= n / LIST_DIV
 constexpr uint32_t FREC_MAX = 32768;   // record the found vertices as a list when candidates <= this
 constexpr uint32_t CAND_CLS = 2;       // class region of lists[] holding the LIST-mode candidate lists
 constexpr uint32_t REC_STAGE = 256;    // per-warp staging of the LIST-mode record
 
-__global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) bfs_pull(BfsP p) {
+template <bool ALL>
+__device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
     Ctl* c = p.s.ctl;
-    const RunState& rs = run_state(c);
-    if (rs.done || rs.dir != DIR_PULL) return;
-    grid_begin(rs.launch);
     const uint64_t n = p.g.n;
     const uint64_t nw = (n + 31) >> 5;
     uint32_t it = rs.iter;
@@ -358,12 +429,15 @@ __global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) bfs_pull(BfsP p) {
     __shared__ uint32_t s_cand[WARPS][1024];
     __shared__ uint32_t s_found[WARPS][32];
     __shared__ uint32_t s_cpre[NSLOT + 1];  // LIST mode: prefix of the candidate regions' counts
-    __shared__ uint32_t s_rec[WARPS][REC_STAGE];
+    // the record staging shares the push phase's online-filter stage (8 KB): the
+    // phases never overlap, and the fused kernel then fits 48 KB of static smem
+    static_assert(WARPS * REC_STAGE <= NCLS * STAGE, "record staging fits the online stage");
     uint32_t* s_c = s_cand[warp_id()];
-    uint32_t* s_r = s_rec[warp_id()];
+    uint32_t* s_r = &stage().e[0][0] + warp_id() * REC_STAGE;
     uint32_t* s_f = s_found[warp_id()];
     uint32_t ncand = 0;    // LIST mode when > 0: candidates recorded by the previous iteration
     uint32_t handoff = 0;  // the next frontier was recorded as a contiguous list
+    uint32_t to_list = 0;  // 2: ... and the push takes it as its lists (lists_ready = 2)
     for (;;) {
         IterLine* nx = &c->line[(it + 1) % 3];
         maybe_reset_line(&c->line[(it + 2) % 3]);
@@ -438,43 +512,8 @@ __global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) bfs_pull(BfsP p) {
             edges += k;
             e += k;
         };
-        // the warp's `total` candidates in s_c through phases 1 and 2
-        auto run_cands = [&](uint32_t total, uint64_t w0) {
-            uint32_t nopen = 0;
-            for (uint32_t r0 = 0; r0 < total; r0 += 32 * HUB_ILP) {
-                uint32_t v[HUB_ILP], h[HUB_ILP], wd[HUB_ILP];
-                bool sole[HUB_ILP];
-#pragma unroll
-                for (int k = 0; k < HUB_ILP; ++k) {
-                    const uint32_t i = r0 + 32 * k + lane;
-                    v[k] = i < total ? s_c[i] : INF;
-                }
-#pragma unroll
-                for (int k = 0; k < HUB_ILP; ++k) {
-                    const uint32_t x = v[k] != INF ? __ldg(p.hub + v[k]) : INF;
-                    h[k] = hub_id(x);
-                    sole[k] = hub_sole(x);
-                }
-#pragma unroll
-                for (int k = 0; k < HUB_ILP; ++k) wd[k] = h[k] != INF ? cur[h[k] >> 5] : 0u;
-                __syncwarp();
-#pragma unroll
-                for (int k = 0; k < HUB_ILP; ++k) {
-                    const bool f = h[k] != INF && ((wd[k] >> (h[k] & 31)) & 1u);
-                    edges += h[k] != INF;
-                    if (f) on_found(v[k], w0);
-                    const bool settled = v[k] != INF && !f && sole[k];
-                    if (settled) mopen += 1;
-                    record_open(settled, v[k]);
-                    // open ones are compacted in place at the front of s_c (stable)
-                    const bool open = v[k] != INF && !f && !sole[k];
-                    const uint32_t bal = __ballot_sync(FULL, open);
-                    if (open) s_c[nopen + __popc(bal & lanemask_lt())] = v[k];
-                    nopen += __popc(bal);
-                }
-                __syncwarp();
-            }
-            // phase 2 — the open candidates walk their in-edge rows
+        // phase 2 — the warp's `nopen` open candidates in s_c walk their in-edge rows
+        auto walk_open = [&](uint32_t nopen, uint64_t w0) {
             uint32_t v_n = 0;
             uint64_t beg_n = 0, end_n = 0;
             if (lane < nopen) {
@@ -530,7 +569,45 @@ __global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) bfs_pull(BfsP p) {
                 record_open(still, v);
             }
         };
-        uint32_t s_cur = my_slot(), tries = 0;
+        // the warp's `total` candidates in s_c through phases 1 and 2
+        auto run_cands = [&](uint32_t total, uint64_t w0) {
+            uint32_t nopen = 0;
+            for (uint32_t r0 = 0; r0 < total; r0 += 32 * HUB_ILP) {
+                uint32_t v[HUB_ILP], h[HUB_ILP], wd[HUB_ILP];
+                bool sole[HUB_ILP];
+#pragma unroll
+                for (int k = 0; k < HUB_ILP; ++k) {
+                    const uint32_t i = r0 + 32 * k + lane;
+                    v[k] = i < total ? s_c[i] : INF;
+                }
+#pragma unroll
+                for (int k = 0; k < HUB_ILP; ++k) {
+                    const uint32_t x = v[k] != INF ? __ldg(p.hub + v[k]) : INF;
+                    h[k] = hub_id(x);
+                    sole[k] = hub_sole(x);
+                }
+#pragma unroll
+                for (int k = 0; k < HUB_ILP; ++k) wd[k] = h[k] != INF ? cur[h[k] >> 5] : 0u;
+                __syncwarp();
+#pragma unroll
+                for (int k = 0; k < HUB_ILP; ++k) {
+                    const bool f = h[k] != INF && ((wd[k] >> (h[k] & 31)) & 1u);
+                    edges += h[k] != INF;
+                    if (f) on_found(v[k], w0);
+                    const bool settled = v[k] != INF && !f && sole[k];
+                    if (settled) mopen += 1;
+                    record_open(settled, v[k]);
+                    // open ones are compacted in place at the front of s_c (stable)
+                    const bool open = v[k] != INF && !f && !sole[k];
+                    const uint32_t bal = __ballot_sync(FULL, open);
+                    if (open) s_c[nopen + __popc(bal & lanemask_lt())] = v[k];
+                    nopen += __popc(bal);
+                }
+                __syncwarp();
+            }
+            walk_open(nopen, w0);
+        };
+        uint32_t s_cur = my_slot();
         uint32_t chunk = 0;
         if (list_mode) {
             // chunks of the recorded candidates; the chunk size adapts so that
@@ -551,11 +628,9 @@ __global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) bfs_pull(BfsP p) {
             const uint64_t per_warp = (ncand + gwarps() - 1) / gwarps();
             const uint32_t csz = per_warp >= 192 ? 256u : per_warp >= 96 ? 128u : per_warp >= 48 ? 64u : 32u;
             const uint32_t nchunks = (ncand + csz - 1) / csz;
-            if (lane == 0) chunk = grab_chunk(nx, nchunks, s_cur, tries);
-            chunk = __shfl_sync(FULL, chunk, 0);
+            chunk = grab_chunk(nx, nchunks, s_cur);
             while (chunk != INF) {
-                uint32_t chunk_n = 0;
-                if (lane == 0) chunk_n = grab_chunk(nx, nchunks, s_cur, tries);
+                const uint32_t chunk_n = grab_chunk(nx, nchunks, s_cur);
                 const uint32_t i0 = chunk * csz;
                 const uint32_t total = min(csz, ncand - i0);
                 for (uint32_t j = lane; j < total; j += 32) {
@@ -573,21 +648,66 @@ __global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) bfs_pull(BfsP p) {
                 run_cands(total, 0);
                 __syncwarp();
                 flush_rec();
-                chunk = __shfl_sync(FULL, chunk_n, 0);
+                chunk = chunk_n;
             }
         } else {
             const uint32_t nchunks = (uint32_t)((nw + 31) >> 5);
-            if (lane == 0) chunk = grab_chunk(nx, nchunks, s_cur, tries);
-            chunk = __shfl_sync(FULL, chunk, 0);
+            chunk = grab_chunk(nx, nchunks, s_cur);
             while (chunk != INF) {
-                uint32_t chunk_n = 0;
-                if (lane == 0) chunk_n = grab_chunk(nx, nchunks, s_cur, tries);
+                const uint32_t chunk_n = grab_chunk(nx, nchunks, s_cur);
                 const uint64_t w0 = (uint64_t)chunk << 5;
                 const uint64_t wl = w0 + lane;
                 const uint32_t vis_l = wl < nw ? p.visited[wl] : FULL;
                 const uint32_t cand_l = wl < nw ? (~vis_l & __ldg(p.g.nz_in + wl)) : 0u;
-                const uint32_t cnt_l = __popc(cand_l);
-                uint32_t incl = cnt_l;
+#if SX_TILE_STREAM
+                if (__any_sync(FULL, cand_l != 0)) {
+                    // phase 1, streamed: word k of the chunk is handled by the whole warp,
+                    // lane l testing vertex 32 (w0 + k) + l — the hub loads of a word are one
+                    // coalesced 128-B request, TILE_ILP words in flight, no shared-memory
+                    // candidate list.  Found bits come out of a ballot (lane k keeps word k's);
+                    // open non-sole candidates are compacted into s_c for the row walks.
+                    uint32_t fm_mine = 0, nopen = 0;
+#pragma unroll 1
+                    for (uint32_t kb = 0; kb < 32; kb += TILE_ILP) {
+                        uint32_t cw[TILE_ILP], x[TILE_ILP], wd[TILE_ILP];
+#pragma unroll
+                        for (int k = 0; k < TILE_ILP; ++k) {
+                            cw[k] = __shfl_sync(FULL, cand_l, kb + k);
+                            const uint32_t v = (uint32_t)((w0 + kb + k) << 5) + lane;
+                            x[k] = (cw[k] >> lane) & 1u ? __ldg(p.hub + v) : INF;
+                        }
+#pragma unroll
+                        for (int k = 0; k < TILE_ILP; ++k) {
+                            const uint32_t h = hub_id(x[k]);
+                            wd[k] = h != INF ? cur[h >> 5] : 0u;
+                        }
+#pragma unroll
+                        for (int k = 0; k < TILE_ILP; ++k) {
+                            const uint32_t v = (uint32_t)((w0 + kb + k) << 5) + lane;
+                            const bool isc = (cw[k] >> lane) & 1u;
+                            const uint32_t h = hub_id(x[k]);
+                            const bool f = h != INF && ((wd[k] >> (h & 31)) & 1u);
+                            edges += h != INF;
+                            if (f) {
+                                p.level[v] = lvl;
+                                if (!p.sym) mdeg += __ldg(p.g.dout + v);
+                            }
+                            const uint32_t fb = __ballot_sync(FULL, f);
+                            if (lane == kb + k) fm_mine = fb;
+                            const bool settled = isc && !f && hub_sole(x[k]);
+                            if (settled) mopen += 1;
+                            record_open(settled, v);
+                            const bool open = isc && !f && !hub_sole(x[k]);
+                            const uint32_t ob = __ballot_sync(FULL, open);
+                            if (open) s_c[nopen + __popc(ob & lanemask_lt())] = v;
+                            nopen += __popc(ob);
+                        }
+                    }
+                    s_f[lane] = fm_mine;
+                    __syncwarp();
+                    walk_open(nopen, w0);
+#else
+                uint32_t incl = __popc(cand_l);
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const uint32_t y = __shfl_up_sync(FULL, incl, o);
@@ -595,11 +715,12 @@ __global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) bfs_pull(BfsP p) {
                 }
                 const uint32_t total = __shfl_sync(FULL, incl, 31);
                 if (total) {
-                    uint32_t pos = incl - cnt_l;
+                    uint32_t pos = incl - __popc(cand_l);
                     for (uint32_t w = cand_l; w; w &= w - 1) s_c[pos++] = (uint32_t)(wl << 5) + (__ffs(w) - 1);
                     s_f[lane] = 0;
                     __syncwarp();
                     run_cands(total, w0);
+#endif
                     __syncwarp();
                     flush_rec();
                     const uint32_t fm = s_f[lane];
@@ -610,7 +731,7 @@ __global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) bfs_pull(BfsP p) {
                     }
                     __syncwarp();
                 }
-                chunk = __shfl_sync(FULL, chunk_n, 0);
+                chunk = chunk_n;
             }
         }
         st.edges += edges;
@@ -628,7 +749,7 @@ __global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) bfs_pull(BfsP p) {
         }
         st.entries += rows;
         st.scanned += (lead() && !list_mode ? nw * 32 : 0);
-        if (!grid_sync(c)) return;
+        if (!grid_sync(c)) return false;
         LineSum ls;
         read_line(nx, ls);
         const uint64_t nf = ls.found;
@@ -649,7 +770,12 @@ __global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) bfs_pull(BfsP p) {
                              (p.s.force_dir == 0 && (double)nf < (double)n / p.s.beta && nf < nf_prev);
         nf_prev = (uint32_t)nf;
         if (to_push) {
-            dir = cluster_ok(p.s, nf, mf) ? DIR_CLUSTER : DIR_PUSH;
+            dir = !ALL && cluster_ok(p.s, nf, mf) ? DIR_CLUSTER : DIR_PUSH;
+            // the grid push takes the recorded found list (class split, no bitmap scan)
+            if (dir == DIR_PUSH && rec_found && p.s.force_filter != 2) {
+                to_list = 2;
+                handoff = 1;
+            }
             if (dir == DIR_CLUSTER && rec_found && p.s.force_filter != 2) {
                 // hand the frontier over as the list recorded in flist / fcnt: the
                 // cluster kernel skips its bitmap scan; the stale bitmap it would
@@ -677,11 +803,67 @@ __global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) bfs_pull(BfsP p) {
         // the found-list counters stay zero outside a hand-over
         for (int i = 0; i < 3; ++i)
             if (!(handoff && i == (int)(it % 3))) c->cl.cnt[i] = 0;
-        c->cl.ready = handoff;
+        c->cl.ready = handoff && dir == DIR_CLUSTER;
     }
-    bfs_exit(p, DIR_PULL, it, m_u, nf_prev, dir, done, 0u, 0u, cnt, st);
+    bfs_exit<ALL>(p, DIR_PULL, it, m_u, nf_prev, dir, done, to_list, 0u, cnt, st, &rs);
+    return true;
+}
+__global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) bfs_pull(BfsP p) {
+    RunState& rs = const_cast<RunState&>(run_state(p.s.ctl));
+    if (rs.done || rs.dir != DIR_PULL) return;
+    grid_begin(rs.launch);
+    pull_phase<false>(p, rs);
 }
 
+
+
+// ------------------------------------------------------------------ all fusion
+// fusion = 2 ("all-fusion", one kernel for the whole run).
+// One cooperative launch: the state init, then push and pull phases back to
+// back (a direction switch costs a grid barrier, not a kernel exit and a
+// relaunch), small frontiers on the grid (no cluster kernel).  The paper's
+// all-fusion kernel lost occupancy to the union of the push and pull register
+// demands (110 registers); here the launch bounds hold it at the
+// occupancy of the separate kernels (3 CTAs x 256 threads per SM), because the
+// phases are disjoint code regions and registers are allocated for the
+// larger of the two, not their sum.  At the end one more barrier, then CTA 0
+// copies the control block's tail into the mapped host mirror (no tail-copy
+// kernel).
+#ifndef SX_ALL_MINB
+#define SX_ALL_MINB 3
+#endif
+__global__ void __launch_bounds__(BLOCK, SX_ALL_MINB) bfs_all(BfsP p, uint32_t src, uint32_t dir0, Ctl* hctl,
+                                                              int fuse_init) {
+    Ctl* c = p.s.ctl;
+    grid_begin(c);  // parity of this launch (the previous launch's exit zeroed this half)
+    if (fuse_init) {
+        bfs_init_body<true>(p, src, dir0);
+        BFS_MARK(3);
+        if (!grid_sync(c)) return;
+    }
+    {
+        const uint32_t z[NCLS] = {0u, 0u, 0u, 0u};
+        trace_put(p.s, 0, DIR_PUSH, 0u, z, 1, 0, 0);  // end of the state init (iteration 0)
+    }
+    RunState& rs = const_cast<RunState&>(run_state(c));
+    while (!rs.done) {
+        const bool ok = rs.dir == DIR_PULL ? pull_phase<true>(p, rs) : push_phase<true>(p, rs);
+        if (!ok) return;
+    }
+    BFS_MARK(4);
+    if (!grid_sync(c)) return;  // every CTA's statistics are in
+    if (blockIdx.x != 0) return;
+    if (threadIdx.x == 0) {
+        grid_end(c);
+        c->launch += 1;
+    }
+    __syncthreads();
+    constexpr size_t off = offsetof(Ctl, iter);
+    constexpr size_t nw = (sizeof(Ctl) - off) / 4;
+    const uint32_t* sw = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(c) + off);
+    uint32_t* dw = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(hctl) + off);
+    for (uint32_t i = threadIdx.x; i < nw; i += BLOCK) dw[i] = vload(sw + i);
+}
 
 // ------------------------------------------------------------------ small-frontier cluster mode
 // Push on one 16-CTA cluster (engine.cuh: cluster_entry / cluster_leave) while
@@ -892,8 +1074,26 @@ extern "C" sx_status sx_bfs(sx_graph g, uint32_t src, const sx_opts* opts, uint3
     p.visited = g->aux_bm;
     p.hub = g->hub;
     p.sym = !g->directed;
-    const uint32_t dir0 = run.o.force_dir == 2 ? DIR_PULL : DIR_PUSH;
+    uint32_t dir0 = run.o.force_dir == 2 ? DIR_PULL : DIR_PUSH;
     hm.mark("prologue");
+    if (run.o.fusion == 2) {  // all fusion: every phase in one cooperative launch
+        // the state init stays a separate, wider launch (8 CTAs/SM of stores:
+        // measured 13 us, against ~25 us inside the 3-CTA/SM persistent grid);
+        // SX_ALL_INIT=1 folds it into the persistent kernel
+        static const int fuse_init = [] { const char* e = getenv("SX_ALL_INIT"); return e && e[0] == '1'; }();
+        if (!fuse_init) {
+            bfs_init<<<g->ctx->prop.multiProcessorCount * 8, BLOCK, 0, s>>>(p, src, dir0 | DIR_NOCLUSTER);
+            SX_CU(cudaGetLastError());
+        }
+        Ctl* hctl = g->ctx->d_hctl;
+        int fi = fuse_init;
+        void* args2[] = {&p, &src, &dir0, &hctl, &fi};
+        if ((rc = run.launch((const void*)bfs_all, args2, false)) != SX_OK) return rc;
+        if ((rc = run.sync(false)) != SX_OK) return rc;
+        if ((rc = run.end(bfs_bytes)) != SX_OK) return rc;
+        hm.mark("end");
+        return dev_out ? SX_OK : sxh::copy_out(g, level_out, p.level, g->n * 4);
+    }
     bfs_init<<<g->ctx->prop.multiProcessorCount * 8, BLOCK, 0, s>>>(p, src, dir0);
     SX_CU(cudaGetLastError());
     void* args[] = {&p};

@@ -236,15 +236,17 @@ __global__ void k_tail_copy(const Ctl* src, Ctl* dst_host) {
     for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) d[i] = vload(s + i);
 }
 
-sx_status Run::sync() {
+sx_status Run::sync(bool tail_copy) {
     sx_ctx c = g->ctx;
     // end-of-run event and the host-visible tail of the control block (from
     // `iter` on: run state, cluster line, statistics), one stream sync
     SX_CU(cudaEventRecord(c->ev1, c->stream));
     // one small kernel stores the tail into the mapped host mirror (a DMA copy of
     // these ~0.6 KB cost more per call: copy-engine start-up)
-    k_tail_copy<<<1, 256, 0, c->stream>>>(g->ctl, c->d_hctl);
-    SX_CU(cudaGetLastError());
+    if (tail_copy) {
+        k_tail_copy<<<1, 256, 0, c->stream>>>(g->ctl, c->d_hctl);
+        SX_CU(cudaGetLastError());
+    }
     cudaError_t e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) {
         c->poisoned = true;

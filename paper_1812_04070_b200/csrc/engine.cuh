@@ -607,21 +607,36 @@ template <class T> __device__ __forceinline__ void slot_add(T* field_of_slot0, T
     if (v) atomicAdd(p, v);
 }
 
-// Dynamic work distribution: chunks [0, nchunks) split into NSLOT ranges; a
-// warp takes chunks from its CTA's slot range, then steals from at most three
-// other slots (an exhausted range is detected with a plain load first).
-__device__ __forceinline__ uint32_t grab_chunk(IterLine* L, uint32_t nchunks, uint32_t& s_cur, uint32_t& tries) {
+// Dynamic work distribution (warp-collective; every lane gets the same chunk):
+// chunks [0, nchunks) split into NSLOT ranges, range s counted by slot s's
+// `tile` counter.  A warp takes chunks from its current range (one atomicAdd by
+// lane 0); once that range is exhausted the warp reads all NSLOT counters at
+// once (lane l loads slot l: one round trip) and moves to a range with work
+// left — the first such range after a per-warp rotation, so the thieves spread
+// over the ranges instead of queueing on one counter.  Returns INF only when
+// every range is exhausted (no warp leaves while another still has work).
+#ifndef SX_STEAL_MAX
+#define SX_STEAL_MAX 1000000  // range moves per warp and level (round 1 stopped after 3)
+#endif
+__device__ __forceinline__ uint32_t grab_chunk(IterLine* L, uint32_t nchunks, uint32_t& s_cur) {
     const uint32_t per = (nchunks + NSLOT - 1) / NSLOT;
-    while (tries < 4) {
-        if (vload(&L->s[s_cur].tile) < per) {
+    const uint32_t lane = lane_id();
+    for (uint32_t moves = 0;; ++moves) {
+        uint32_t ch = INF;
+        if (lane == 0 && vload(&L->s[s_cur].tile) < per) {
             const uint32_t k = atomicAdd(&L->s[s_cur].tile, 1u);
-            const uint32_t ch = s_cur * per + k;
-            if (k < per && ch < nchunks) return ch;
+            if (k < per && s_cur * per + k < nchunks) ch = s_cur * per + k;
         }
-        s_cur = (s_cur + 7 + tries * 6) % NSLOT;
-        ++tries;
+        ch = __shfl_sync(FULL, ch, 0);
+        if (ch != INF || moves >= SX_STEAL_MAX) return ch;
+        const uint32_t lo = lane * per;
+        const uint32_t size = lo < nchunks ? min(per, nchunks - lo) : 0u;
+        const uint32_t left = __ballot_sync(FULL, vload(&L->s[lane].tile) < size);
+        if (!left) return INF;
+        const uint32_t rot = (uint32_t)(gwarp() * 7u) & 31u;
+        const uint32_t r = (left >> rot) | (rot ? left << (32u - rot) : 0u);  // rotate right by rot
+        s_cur = ((uint32_t)(__ffs(r) - 1) + rot) & 31u;
     }
-    return INF;
 }
 
 // ---------------------------------------------------------------- ballot filter
@@ -991,6 +1006,40 @@ __device__ __forceinline__ void for_tasks(const uint32_t* lists, const Sched& s,
     for (uint64_t ch = wslot; ch < nch; ch += gwarps()) {
         const uint64_t i = (ch << 5) + lane_id();
         if (i < cnt[0]) vf(task_at(lists, s, 0, (uint32_t)i), 0ull, 1ull, 0u);
+    }
+}
+
+// CTA-local binning of a short flat task list (the found list a pull iteration
+// recorded with the online filter): CTA b takes the contiguous chunk
+// [b0, b1) of the list, classifies its entries by degree in shared memory and
+// runs small ones at thread, medium ones at warp and large / huge ones at CTA
+// granularity — no grid-wide class lists, so no barrier before the
+// iteration.  Balance across CTAs is by entry count; the lists this serves are
+// the last levels of a traversal (few, low-degree vertices).
+template <class VFn>
+__device__ __forceinline__ void for_list_local(const uint32_t* list, uint32_t n, const Sched& s, const uint32_t* deg,
+                                               VFn&& vf) {
+    __shared__ uint32_t q_w[BLOCK], q_c[BLOCK];
+    __shared__ uint32_t nq[2];
+    const uint32_t per = (n + gridDim.x - 1) / gridDim.x;
+    const uint32_t b0 = min(n, blockIdx.x * per), b1 = min(n, b0 + per);
+    for (uint32_t base = b0; base < b1; base += BLOCK) {  // CTA-uniform
+        if (threadIdx.x < 2) nq[threadIdx.x] = 0;
+        __syncthreads();
+        const uint32_t i = base + threadIdx.x;
+        uint32_t v = INF, c = NCLS;
+        if (i < b1) {
+            v = list[i];
+            c = cls_of(__ldg(deg + v), s);
+        }
+        if (c == 1) q_w[atomicAdd(&nq[0], 1u)] = v;
+        else if (c == 2 || c == 3) q_c[atomicAdd(&nq[1], 1u)] = v;
+        if (c == 0) vf(v, 0ull, 1ull, 0u);
+        __syncthreads();
+        const uint32_t nw = nq[0], nc = nq[1];
+        for (uint32_t j = warp_id(); j < nw; j += WARPS) vf(q_w[j], (uint64_t)lane_id(), 32ull, 1u);
+        for (uint32_t j = 0; j < nc; ++j) vf(q_c[j], (uint64_t)threadIdx.x, (uint64_t)BLOCK, 2u);
+        __syncthreads();
     }
 }
 

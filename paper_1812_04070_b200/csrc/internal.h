@@ -111,7 +111,8 @@ struct Run {
     // Same for a non-cooperative launch with an explicit shape (e.g. one cluster).
     sx_status launch_plain(const void* fn, void** args, int grid, int block, bool pull);
     // Read back the control block, accumulate the pending launches' times, check errors.
-    sx_status sync();
+    // tail_copy = false: the kernel itself stored the control block's tail into the host mirror.
+    sx_status sync(bool tail_copy = true);
     sx_status end(BytesFn bytes);
 };
 

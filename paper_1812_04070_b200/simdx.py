@@ -390,11 +390,19 @@ class Graph:
 
     _default_opts = None
 
+    _opts_cache: dict = {}
+
     def _opts(self, kw):
         if not kw:  # the common call: default options, built once
             if Graph._default_opts is None:
                 Graph._default_opts = make_opts()
             return Graph._default_opts, None
+        if "trace_cap" not in kw:  # repeated option sets without a trace: built once each
+            key = tuple(sorted(kw.items()))
+            o = Graph._opts_cache.get(key)
+            if o is None:
+                o = Graph._opts_cache[key] = make_opts(**kw)
+            return o, None
         trace_cap = kw.pop("trace_cap", 0)
         o = make_opts(**kw)
         buf = None
@@ -410,7 +418,7 @@ class Graph:
             return None
         recs = []
         for r in buf:
-            if r.iter == 0:
+            if r.t_ns == 0:
                 break
             recs.append(dict(iter=r.iter, dir=r.dir, filter=r.filter, launch=r.launch, n_active=list(r.n_active),
                              n_frontier=r.n_frontier, m_active=r.m_active, aux=r.aux, t_ns=r.t_ns))

@@ -90,7 +90,9 @@ def test_fig1_reconstruction_sssp(ctx):
 MODES = [dict(), dict(force_dir=1), dict(force_dir=2), dict(force_filter=1), dict(force_filter=2),
          dict(fusion=0), dict(overflow_threshold=1), dict(overflow_threshold=1 << 20),
          dict(sep_small=4, sep_large=8, sep_huge=64), dict(force_dir=2, fusion=0),
-         dict(cluster_enter=0), dict(cluster_enter=64), dict(cluster_enter=1 << 20)]
+         dict(cluster_enter=0), dict(cluster_enter=64), dict(cluster_enter=1 << 20),
+         dict(fusion=2), dict(fusion=2, force_dir=1), dict(fusion=2, force_dir=2), dict(fusion=2, force_filter=2),
+         dict(fusion=2, force_filter=1, overflow_threshold=1)]
 
 
 @pytest.fixture(scope="module")
@@ -108,7 +110,7 @@ def test_bfs_modes_rmat(ctx, rmat14, mode):
         assert np.array_equal(lv, r), mode
         # per-level frontier sizes = the oracle's level histogram (exact)
         hist = oracle.level_histogram(r)
-        got = [t["n_frontier"] for t in tr]
+        got = [t["n_frontier"] for t in tr if t["iter"] > 0]  # iteration 0: the fused init record
         assert got[:len(hist) - 1] == list(hist[1:]), (got, hist)
     G.free()
 
