@@ -111,14 +111,14 @@ def timed_loop(fn, steps, stream):
 
 # ---------------------------------------------------------------------------- reference arm
 def run_reference(args):
-    """--impl reference: the oracle (single-threaded C on the host) on the same workload and metric."""
-    from paper_1812_04070_b200 import dist_host
-    world, rank, _ = dist_host.env_rank()
+    """--impl reference: the oracle (single-threaded C on the host) on the same workload and metric.
+    Nothing of the product package is imported here (its __init__ would load libsimdx.so)."""
+    world, rank = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import oracle
     import simgen
-    scale = dist_host.weak_scale(args.scale, world)
+    scale = args.scale + max(0, world - 1).bit_length()  # weak scaling: 2^scale vertices per GPU
     t = time.time()
     g = simgen.rmat(scale, args.ef, args.seed)
     log(f"[bench:ref] R-MAT s{scale}: generated on the host in {time.time() - t:.1f}s")
@@ -165,9 +165,13 @@ def run_single(args):
     G = ctx.upload_device(dg)
     n = dg.n
     level = torch.empty(n, dtype=torch.int32, device=dev)
-    bkw = {} if args.fusion == 1 else {"fusion": args.fusion}
+    bkw = {"fusion": 2, "cluster_enter": 0} if args.mode == "async" else {} if args.fusion == 1 else {
+        "fusion": args.fusion}
     for _ in range(args.warmup):
-        G.bfs(0, out=level, **bkw)
+        if args.mode == "async":
+            G.bfs_async(0, level)
+        else:
+            G.bfs(0, out=level, **bkw)
     _, st, trace = G.bfs(0, out=level, trace_cap=64, **bkw)
     lv = level.cpu().numpy().view(np.uint32)
     log(f"[bench] BFS stats: {st}")
@@ -176,31 +180,55 @@ def run_single(args):
         f"|F'|={t['n_frontier']} L{t['launch']}" for t in trace))
 
     # ---- timed region: K BFS steps
-    acc = dict(launches=0, ms_push=0.0, ms_pull=0.0, b_push=0.0, b_pull=0.0, l_push=0, l_pull=0)
-
-    def step():
-        _, s, _ = G.bfs(0, out=level, **bkw)
-        acc["launches"] += 2 + s["launches"]  # bfs_init + persistent launches + the control-tail copy kernel
-        acc["ms_push"] += s["ms_push"]
-        acc["ms_pull"] += s["ms_pull"]
-        acc["b_push"] += s["bytes_push"]
-        acc["b_pull"] += s["bytes_pull"]
-        acc["l_push"] += s["launches_push"]
-        acc["l_pull"] += s["launches_pull"]
-
-    with Clocks(0) as clk:
-        ms = timed_loop(step, args.steps, stream)
-    clocks = clk.summary()
-
     host = dg.to_host()  # input generator output (bit-identical to simgen.rmat), for m_cc / e2e / oracle
     deg = np.diff(host.row_ptr).astype(np.int64)
     m_cc = int(deg[lv != 0xFFFFFFFF].sum() // 2)
-    gteps = m_cc / (ms * 1e-3) / 1e9
-
     K = args.steps
-    dom = "bfs_pull" if acc["ms_pull"] >= acc["ms_push"] else "bfs_push"
-    dms, dbytes, dl = ((acc["ms_pull"], acc["b_pull"], acc["l_pull"]) if dom == "bfs_pull"
-                       else (acc["ms_push"], acc["b_push"], acc["l_push"]))
+    if args.mode == "async":
+        # sx_bfs_async: each step = the state-init kernel + ONE all-fusion persistent
+        # launch, enqueued without a host round trip; the device-side
+        # statistics and per-run CUDA events come back at sx_graph_sync
+        G.sync()
+
+        def step():
+            G.bfs_async(0, level)
+
+        with Clocks(0) as clk:
+            ms = timed_loop(step, K, stream)
+        clocks = clk.summary()
+        sa = G.sync()
+        assert sa["runs"] == K, sa
+        launches = 2 * K  # bfs_init + bfs_all per step
+        dom, dms, dbytes, dl = "bfs_all", sa["ms_fused"], sa["bytes_model"], sa["launches_fused"]
+        step_bytes = sa["bytes_model"]
+    else:
+        acc = dict(launches=0, ms_push=0.0, ms_pull=0.0, ms_fused=0.0, b_push=0.0, b_pull=0.0, l_push=0, l_pull=0,
+                   l_fused=0)
+
+        def step():
+            _, s, _ = G.bfs(0, out=level, **bkw)
+            # bfs_init + persistent launches (+ the control-tail copy kernel unless all fusion)
+            acc["launches"] += 1 + s["launches"] + (0 if s["launches_fused"] else 1)
+            for k in ("ms_push", "ms_pull", "ms_fused"):
+                acc[k] += s[k]
+            acc["b_push"] += s["bytes_push"]
+            acc["b_pull"] += s["bytes_pull"]
+            acc["l_push"] += s["launches_push"]
+            acc["l_pull"] += s["launches_pull"]
+            acc["l_fused"] += s["launches_fused"]
+
+        with Clocks(0) as clk:
+            ms = timed_loop(step, K, stream)
+        clocks = clk.summary()
+        launches = acc["launches"]
+        step_bytes = acc["b_push"] + acc["b_pull"]
+        if acc["l_fused"]:
+            dom, dms, dbytes, dl = "bfs_all", acc["ms_fused"], step_bytes, acc["l_fused"]
+        elif acc["ms_pull"] >= acc["ms_push"]:
+            dom, dms, dbytes, dl = "bfs_pull", acc["ms_pull"], acc["b_pull"], acc["l_pull"]
+        else:
+            dom, dms, dbytes, dl = "bfs_push", acc["ms_push"], acc["b_push"], acc["l_push"]
+    gteps = m_cc / (ms * 1e-3) / 1e9
     achieved = (dbytes / K) / (dms / K * 1e-3) / 1e9 if dms > 0 else 0.0
     traffic = None
     try:
@@ -210,12 +238,39 @@ def run_single(args):
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "peak_source": peak_src,
                 "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                 "bytes_per_step": dbytes / K, "kernel_ms_per_step": dms / K, "kernel_share_of_step": (dms / K) / ms,
-                "launches_per_step": dl / K, "step_bytes_model": (acc["b_push"] + acc["b_pull"]) / K,
-                "step_gbs": (acc["b_push"] + acc["b_pull"]) / K / (ms * 1e-3) / 1e9}
+                "launches_per_step": dl / K, "step_bytes_model": step_bytes / K,
+                "step_gbs": step_bytes / K / (ms * 1e-3) / 1e9}
 
     # ---- extras on the same graph (outside the timed step)
     extras = {}
     if not args.no_extras:
+        # Graph500-style: BFS from random roots of degree >= 1 (the timed step always
+        # starts at vertex 0, the hub); harmonic mean of per-root GTEPS, device time
+        # of each run (sx_stats.ms, CUDA events), all fusion
+        rng = np.random.default_rng(args.seed)
+        cand = np.flatnonzero(deg > 0)
+        roots = rng.choice(cand, size=min(args.roots, cand.size), replace=False)
+        deg_t = torch.from_numpy(deg).to(dev)
+        tg = []
+        for r in roots:
+            _, s, _ = G.bfs(int(r), out=level, fusion=2, cluster_enter=0)
+            mc = int(deg_t[level != -1].sum().item()) // 2
+            tg.append(mc / (s["ms"] * 1e-3) / 1e9)
+        extras["bfs_random_roots"] = {"roots": len(tg), "gteps_hmean": len(tg) / sum(1.0 / x for x in tg),
+                                      "gteps_min": min(tg), "gteps_max": max(tg),
+                                      "what": "device time per run (init + fused kernel), fusion = 2"}
+        # fusion / filter ablation on this graph (Fig. 12/13 analogue):
+        # device ms per BFS from vertex 0, best of 3
+        abl = {}
+        for name, kw in (("fusion0_none", dict(fusion=0)), ("fusion1_selective", {}),
+                         ("fusion2_all", dict(fusion=2, cluster_enter=0)),
+                         ("online_only", dict(force_filter=1)), ("ballot_only", dict(force_filter=2)),
+                         ("push_only", dict(force_dir=1)), ("pull_only", dict(force_dir=2))):
+            best = min((G.bfs(0, out=level, **kw)[1] for _ in range(3)), key=lambda x: x["ms"])
+            abl[name] = {"ms": best["ms"], "launches": best["launches"], "iterations": best["iterations"]}
+        extras["bfs_ablation"] = abl
+        level.zero_()
+        G.bfs(0, out=level)
         out = torch.empty(n, dtype=torch.int32, device=dev)
         G.sssp(0, args.delta, out=out)
         best = None
@@ -344,7 +399,7 @@ def run_single(args):
                                f"(Graph500 A,B,C=.57,.19,.19, seed {args.seed}), 1 GPU",
                    "scale": args.scale, "edgefactor": args.ef, "n": n, "m_directed": int(host.m), "m_cc": m_cc,
                    "l2": "inputs larger than L2 (col array 4*m bytes >> 126 MB); no flush", "parallelism": "1d1"},
-        "gpu_launches": acc["launches"], "clocks": clocks, "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu,
+        "gpu_launches": launches, "clocks": clocks, "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu,
         "bfs": {"iterations": st["iterations"], "launches": st["launches"], "pull_iters": st["pull_iters"],
                 "ballot_iters": st["ballot_iters"], "edges_examined": st["edges_examined"]},
         "extras": extras,
@@ -460,7 +515,10 @@ def main():
     ap.add_argument("--ef", type=int, default=16)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--fusion", type=int, default=1, choices=[0, 1, 2],
-                    help="0 none, 1 selective (P:773-778), 2 all (one launch per BFS)")
+                    help="--mode sync: 0 none, 1 selective (P:773-778), 2 all (one launch per BFS)")
+    ap.add_argument("--mode", default="async", choices=["async", "sync"],
+                    help="async: sx_bfs_async steps (all fusion, no host round trip); sync: sx_bfs per step")
+    ap.add_argument("--roots", type=int, default=64, help="random-root BFS extra (Graph500 style, P:1003)")
     ap.add_argument("--delta", type=int, default=4096)  # measured best for C2 (profiles/r1/delta_sweep.txt)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)

@@ -91,6 +91,18 @@ sx_status sx_ctx_info(sx_ctx ctx, sx_device_info* out);
  * out), SX_E_BARRIER (watchdog), SX_E_CUDA.
  */
 sx_status sx_barrier_bench(sx_ctx ctx, uint32_t iters, double* us_per_barrier, int* ctas);
+/*
+ * Fault injection for the grid barrier (a software barrier over
+ * CTAs that are not all co-resident deadlocks).
+ *   mode 1: cooperatively launch one CTA more than occupancy x SMs; the
+ *           driver must refuse it -> SX_E_BARRIER (nothing runs).
+ *   mode 2: a co-resident grid in which the last CTA never arrives at the
+ *           barrier; the watchdog, lowered to timeout_ms for this launch, fires
+ *           -> SX_E_BARRIER, every CTA leaves, and the context stays usable.
+ * Returns SX_OK only if the fault was NOT detected.  Errors: SX_E_INVALID
+ * (mode not 1/2, mode 2 with timeout_ms = 0), SX_E_CUDA.
+ */
+sx_status sx_barrier_fault(sx_ctx ctx, uint32_t mode, uint32_t timeout_ms);
 /* Diagnostic: cost of the small-frontier cluster mode's pieces on one 16-CTA
    cluster.  mode 0: empty launch; 1: one cluster barrier (reps barriers in one
    launch); 2: zero a bitmap of nwords words; 3: zero + compact an empty bitmap.
@@ -197,7 +209,8 @@ typedef struct {
     float alpha, beta;           /* push->pull when m_f > m_u/alpha, pull->push when n_f < n/beta (Beamer; reading 8); 14, 24 */
     int32_t force_filter;        /* 0 JIT, 1 online only, 2 ballot only */
     int32_t force_dir;           /* 0 auto, 1 push only, 2 pull only */
-    int32_t fusion;              /* 1 selective push/pull fusion (default); 0 no fusion (one launch per iteration) */
+    int32_t fusion;              /* 1 selective push/pull fusion (default); 0 no fusion (one launch per
+                                    iteration); 2 all fusion (BFS: one launch for every phase) */
     uint32_t max_iters;          /* 0 = unlimited */
     sx_trace_rec* trace;         /* nullable host buffer of trace_cap records (P:623-626 activation patterns) */
     uint64_t trace_cap;
@@ -229,6 +242,9 @@ typedef struct {
     double ms_push, ms_pull;     /* device time inside push / pull persistent kernels (CUDA events around each launch) */
     double bytes_push, bytes_pull; /* bytes_model split by the direction of the launch that moved them */
     uint32_t launches_push, launches_pull;
+    double ms_fused;             /* device time inside all-phase fused launches (fusion = 2) */
+    uint32_t launches_fused;
+    uint32_t runs;               /* algorithm runs these statistics cover (1; sx_graph_sync: the runs it drained) */
 } sx_stats;
 
 #define SX_CLUSTER_AUTO 0xFFFFFFFFu
@@ -244,6 +260,24 @@ void sx_opts_default(sx_opts* o);
  * 0xFFFFFFFF if unreachable.  Push/pull switch per opts.
  * Errors: SX_E_INVALID (src >= n, NULL level_out), SX_E_NO_REVERSE (pull on a directed graph without CSC). */
 sx_status sx_bfs(sx_graph g, uint32_t src, const sx_opts* opts, uint32_t* level_out, sx_stats* stats);
+
+/* Asynchronous BFS (the same result as sx_bfs): enqueue the whole run on the
+ * ctx stream — one state-init kernel and ONE all-fusion persistent launch
+ * (fusion = 2 whatever opts says; no trace, no cluster tail)
+ * — and return without waiting, so back-to-back runs pay no host round trip.
+ * level_out must be DEVICE memory (n u32) and stays undefined until the
+ * stream reaches the run (stream order: later work on the ctx stream sees it).
+ * Statistics (summed over the graph's async runs) come from sx_graph_sync.
+ * Errors found while enqueuing are returned here (as sx_bfs, plus
+ * SX_E_INVALID for a host level_out); a barrier watchdog during a run is
+ * reported by the next sx_graph_sync. */
+sx_status sx_bfs_async(sx_graph g, uint32_t src, const sx_opts* opts, uint32_t* level_out);
+/* Wait for every run enqueued with sx_bfs_async on g's context and return g's
+ * async statistics since the previous sx_graph_sync (stats nullable; then
+ * reset them): runs, iterations, edges, bytes_model, ms = device time of the
+ * runs (init + fused kernel, CUDA events), ms_fused = the fused kernels alone.
+ * Errors: SX_E_BARRIER (a watchdog fired in one of the runs), SX_E_CUDA. */
+sx_status sx_graph_sync(sx_graph g, sx_stats* stats);
 
 /* SSSP: dist_out[v] = min path weight from src
  * (u32, 0xFFFFFFFF unreachable).  delta-stepping with bucket width `delta` (0 = infinity:

@@ -833,13 +833,21 @@ __global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) bfs_pull(BfsP p) {
 #define SX_ALL_MINB 3
 #endif
 __global__ void __launch_bounds__(BLOCK, SX_ALL_MINB) bfs_all(BfsP p, uint32_t src, uint32_t dir0, Ctl* hctl,
-                                                              int fuse_init) {
+                                                              int fuse_init, AsyncAcc* acc) {
     Ctl* c = p.s.ctl;
+    // a broken barrier (watchdog): every CTA leaves; CTA 0 reports it to the
+    // host mirror (sync run) or the async accumulator
+    auto failed = [&]() {
+        if (lead()) {
+            if (hctl) hctl->error = ERR_BARRIER;
+            if (acc) atomicAdd(&acc->errors, 1u);
+        }
+    };
     grid_begin(c);  // parity of this launch (the previous launch's exit zeroed this half)
     if (fuse_init) {
         bfs_init_body<true>(p, src, dir0);
         BFS_MARK(3);
-        if (!grid_sync(c)) return;
+        if (!grid_sync(c)) return failed();
     }
     {
         const uint32_t z[NCLS] = {0u, 0u, 0u, 0u};
@@ -848,15 +856,30 @@ __global__ void __launch_bounds__(BLOCK, SX_ALL_MINB) bfs_all(BfsP p, uint32_t s
     RunState& rs = const_cast<RunState&>(run_state(c));
     while (!rs.done) {
         const bool ok = rs.dir == DIR_PULL ? pull_phase<true>(p, rs) : push_phase<true>(p, rs);
-        if (!ok) return;
+        if (!ok) return failed();
     }
     BFS_MARK(4);
-    if (!grid_sync(c)) return;  // every CTA's statistics are in
+    if (!grid_sync(c)) return failed();  // every CTA's statistics are in
     if (blockIdx.x != 0) return;
     if (threadIdx.x == 0) {
         grid_end(c);
         c->launch += 1;
+        if (acc) {  // async run: add this run's statistics (the next run's init zeroes them)
+            for (int d = 0; d < 2; ++d) {
+                const Ctl::StatBlock& b = c->st[d];
+                Ctl::StatBlock& a = acc->st[d];
+                a.edges += vload(&b.edges);
+                a.entries += vload(&b.entries);
+                a.scanned += vload(&b.scanned);
+                a.reached += vload(&b.reached);
+                a.ballot += vload(&b.ballot);
+                a.pull += vload(&b.pull);
+                a.iters += vload(&b.iters);
+            }
+            acc->runs += 1;
+        }
     }
+    if (!hctl) return;
     __syncthreads();
     constexpr size_t off = offsetof(Ctl, iter);
     constexpr size_t nw = (sizeof(Ctl) - off) / 4;
@@ -1061,11 +1084,7 @@ extern "C" sx_status sx_bfs(sx_graph g, uint32_t src, const sx_opts* opts, uint3
     cudaStream_t s = g->ctx->stream;
     BfsP p;
     p.g = sxh::dev_graph(g);
-    if (!g->hub && g->has_rev) {  // first BFS on this graph: build the hub-first probe table
-        if ((rc = sxh::dmalloc(g->ctx, &g->hub, g->n * 4 + 16)) != SX_OK) return rc;
-        bfs_hub<<<g->ctx->prop.multiProcessorCount * 8, BLOCK, 0, s>>>(p.g, g->hub);
-        SX_CU(cudaGetLastError());
-    }
+    if ((rc = sxh::bfs_prepare(g)) != SX_OK) return rc;  // normally done at upload
     if ((rc = run.begin(/*zero_ctl=*/false)) != SX_OK) return rc;  // bfs_init zeroes the control block
     p.s = sxh::make_sched(g, run.o);
     // write levels straight into a device output buffer (no copy-out)
@@ -1087,8 +1106,9 @@ extern "C" sx_status sx_bfs(sx_graph g, uint32_t src, const sx_opts* opts, uint3
         }
         Ctl* hctl = g->ctx->d_hctl;
         int fi = fuse_init;
-        void* args2[] = {&p, &src, &dir0, &hctl, &fi};
-        if ((rc = run.launch((const void*)bfs_all, args2, false)) != SX_OK) return rc;
+        AsyncAcc* acc = nullptr;
+        void* args2[] = {&p, &src, &dir0, &hctl, &fi, &acc};
+        if ((rc = run.launch((const void*)bfs_all, args2, sxh::KIND_FUSED)) != SX_OK) return rc;
         if ((rc = run.sync(false)) != SX_OK) return rc;
         if ((rc = run.end(bfs_bytes)) != SX_OK) return rc;
         hm.mark("end");
@@ -1110,7 +1130,7 @@ extern "C" sx_status sx_bfs(sx_graph g, uint32_t src, const sx_opts* opts, uint3
     };
     auto enqueue = [&](uint32_t d) -> sx_status {
         if (d == DIR_CLUSTER) return run.launch_plain((const void*)bfs_cluster, args, CL_CTAS, CL_BLOCK, false);
-        return run.launch(d == DIR_PULL ? (const void*)bfs_pull : (const void*)bfs_push, args, d == DIR_PULL);
+        return run.launch(d == DIR_PULL ? (const void*)bfs_pull : (const void*)bfs_push, args, d == DIR_PULL ? sxh::KIND_PULL : sxh::KIND_PUSH);
     };
     g->ctx->h_ctl->done = 0;
     // the device picks cluster mode at init for a low-degree source; the host
@@ -1143,6 +1163,143 @@ extern "C" sx_status sx_bfs(sx_graph g, uint32_t src, const sx_opts* opts, uint3
     if ((rc = run.end(bfs_bytes)) != SX_OK) return rc;
     hm.mark("end");
     return dev_out ? SX_OK : sxh::copy_out(g, level_out, p.level, g->n * 4);
+}
+
+namespace sxh {
+// The hub-first probe table (bfs_hub) of a graph with in-neighbour rows: built
+// once, at upload, so no BFS call pays for it.
+sx_status bfs_prepare(sx_graph g) {
+    if (g->hub || !g->has_rev || g->n == 0) return SX_OK;
+    sx_status rc = dmalloc(g->ctx, &g->hub, g->n * 4 + 16);
+    if (rc != SX_OK) return rc;
+    bfs_hub<<<g->ctx->prop.multiProcessorCount * 8, BLOCK, 0, g->ctx->stream>>>(dev_graph(g), g->hub);
+    SX_CU(cudaGetLastError());
+    return SX_OK;
+}
+
+sx_status drain_async(sx_ctx c) {
+    if (c->nasync == 0) return SX_OK;
+    cudaError_t e = cudaEventSynchronize(c->eva[3 * (c->nasync - 1) + 2]);
+    if (e != cudaSuccess) {
+        c->poisoned = true;
+        return cuda_fail(e, "async BFS");
+    }
+    for (int i = 0; i < c->nasync; ++i) {
+        float t = 0, k = 0;
+        SX_CU(cudaEventElapsedTime(&t, c->eva[3 * i], c->eva[3 * i + 2]));
+        SX_CU(cudaEventElapsedTime(&k, c->eva[3 * i + 1], c->eva[3 * i + 2]));
+        sx_graph g = c->async_g[i];
+        g->async_ms += t;
+        g->async_ms_fused += k;
+        g->async_runs += 1;
+        c->async_g[i] = nullptr;
+    }
+    c->nasync = 0;
+    return SX_OK;
+}
+}  // namespace sxh
+
+// Enqueue one BFS (all fusion: the init kernel and one persistent launch,
+// P:742-743) on the ctx stream and return at once.
+extern "C" sx_status sx_bfs_async(sx_graph g, uint32_t src, const sx_opts* opts, uint32_t* level_out) {
+    if (!g || !level_out) return sxh::fail(SX_E_INVALID, "sx_bfs_async: NULL graph or level_out");
+    sx_status rc = sxh::check_ctx(g->ctx);
+    if (rc != SX_OK) return rc;
+    if (g->n == 0) return sxh::fail(SX_E_INVALID, "sx_bfs_async: empty graph has no source");
+    if (src >= g->n) return sxh::fail(SX_E_INVALID, "sx_bfs_async: src >= n");
+    if (!sxh::is_device_ptr(level_out)) return sxh::fail(SX_E_INVALID, "sx_bfs_async: level_out must be device memory");
+    sx_opts o = sxh::resolve_opts(opts);
+    o.fusion = 2;
+    o.trace = nullptr;
+    o.trace_cap = 0;
+    o.cluster_enter = 0;
+    if (g->directed && !g->has_rev && o.force_dir != 1)
+        return sxh::fail(SX_E_NO_REVERSE, "sx_bfs_async: pull needs in-neighbour rows (CSC); use force_dir=1 (push)");
+    sx_ctx c = g->ctx;
+    cudaStream_t s = c->stream;
+    if ((rc = sxh::bfs_prepare(g)) != SX_OK) return rc;
+    if (!g->async_acc) {
+        if ((rc = sxh::dmalloc(c, &g->async_acc, sizeof(AsyncAcc))) != SX_OK) return rc;
+        SX_CU(cudaMemsetAsync(g->async_acc, 0, sizeof(AsyncAcc), s));
+    }
+    if (c->nasync == sx_ctx_s::ASYNC_POOL && (rc = sxh::drain_async(c)) != SX_OK) return rc;
+    BfsP p;
+    p.g = sxh::dev_graph(g);
+    p.s = sxh::make_sched(g, o);
+    p.level = level_out;
+    p.visited = g->aux_bm;
+    p.hub = g->hub;
+    p.sym = !g->directed;
+    uint32_t dir0 = o.force_dir == 2 ? DIR_PULL : DIR_PUSH;
+    const int i = c->nasync;
+    SX_CU(cudaEventRecord(c->eva[3 * i], s));
+    bfs_init<<<c->prop.multiProcessorCount * 8, BLOCK, 0, s>>>(p, src, dir0 | DIR_NOCLUSTER);
+    SX_CU(cudaGetLastError());
+    SX_CU(cudaEventRecord(c->eva[3 * i + 1], s));
+    Ctl* hctl = nullptr;
+    int fi = 0;
+    AsyncAcc* acc = g->async_acc;
+    void* args[] = {&p, &src, &dir0, &hctl, &fi, &acc};
+    if ((rc = sxh::coop_launch(g, (const void*)bfs_all, args, nullptr)) != SX_OK) return rc;
+    SX_CU(cudaEventRecord(c->eva[3 * i + 2], s));
+    c->async_g[i] = g;
+    c->nasync = i + 1;
+    return SX_OK;
+}
+
+// Wait for the graph's enqueued async runs; report and reset their statistics.
+extern "C" sx_status sx_graph_sync(sx_graph g, sx_stats* stats) {
+    if (!g) return sxh::fail(SX_E_INVALID, "sx_graph_sync: NULL graph");
+    sx_status rc = sxh::check_ctx(g->ctx);
+    if (rc != SX_OK) return rc;
+    sx_ctx c = g->ctx;
+    if ((rc = sxh::drain_async(c)) != SX_OK) return rc;
+    AsyncAcc h{};
+    if (g->async_acc) {
+        SX_CU(cudaMemcpyAsync(&h, g->async_acc, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+        SX_CU(cudaMemsetAsync(g->async_acc, 0, sizeof(AsyncAcc), c->stream));
+    }
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) {
+        c->poisoned = true;
+        return sxh::cuda_fail(e, "sx_graph_sync");
+    }
+    if (stats) {
+        std::memset(stats, 0, sizeof(*stats));
+        const Ctl::StatBlock& a = h.st[0];
+        const Ctl::StatBlock& b = h.st[1];
+        auto cnt = [](const Ctl::StatBlock& x) {
+            sxh::Counters k;
+            k.entries = (double)x.entries;
+            k.edges = (double)x.edges;
+            k.reached = (double)x.reached;
+            k.scanned = (double)x.scanned;
+            k.iters = (double)x.iters;
+            k.pull = (double)x.pull;
+            k.ballot = (double)x.ballot;
+            return k;
+        };
+        stats->iterations = a.iters + b.iters;
+        stats->launches = g->async_runs;
+        stats->launches_fused = g->async_runs;
+        stats->ballot_iters = a.ballot + b.ballot;
+        stats->pull_iters = a.pull + b.pull;
+        stats->edges_examined = a.edges + b.edges;
+        stats->vertices_scanned = a.scanned + b.scanned;
+        stats->list_entries = a.entries + b.entries;
+        stats->bytes_push = bfs_bytes(g, cnt(a));
+        stats->bytes_pull = bfs_bytes(g, cnt(b));
+        stats->bytes_model = stats->bytes_push + stats->bytes_pull;
+        stats->ms = g->async_ms;
+        stats->ms_fused = g->async_ms_fused;
+        stats->runs = g->async_runs;
+    }
+    const uint32_t runs = g->async_runs;
+    g->async_ms = g->async_ms_fused = 0;
+    g->async_runs = 0;
+    if (h.errors) return sxh::fail(SX_E_BARRIER, "grid barrier watchdog fired in an async run");
+    if (h.runs != runs) return sxh::fail(SX_E_STATE, "async run count mismatch");
+    return SX_OK;
 }
 
 extern "C" sx_status sx_ctx_info(sx_ctx c, sx_device_info* out) {

@@ -190,7 +190,7 @@ sx_status Run::begin(bool zero_ctl) {
     return SX_OK;
 }
 
-sx_status Run::launch(const void* fn, void** args, bool pull, int smem) {
+sx_status Run::launch(const void* fn, void** args, int kind, int smem) {
     sx_ctx c = g->ctx;
     if (npending == EV_POOL) {
         sx_status rc = sync();
@@ -200,8 +200,8 @@ sx_status Run::launch(const void* fn, void** args, bool pull, int smem) {
     sx_status rc = coop_launch(g, fn, args, nullptr, smem);
     if (rc != SX_OK) return rc;
     SX_CU(cudaEventRecord(c->evp[2 * npending + 1], c->stream));
-    pend_pull[npending++] = pull;
-    ++(pull ? launches_pull : launches_push);
+    pend_kind[npending++] = kind;
+    ++(kind == KIND_PULL ? launches_pull : kind == KIND_FUSED ? launches_fused : launches_push);
     ++launches;
     if (launches > 10000000) return fail(SX_E_STATE, "runaway launch loop");
     return SX_OK;
@@ -222,7 +222,7 @@ sx_status Run::launch_plain(const void* fn, void** args, int grid, int block, bo
         return cuda_fail(e, "cudaLaunchKernel");
     }
     SX_CU(cudaEventRecord(c->evp[2 * npending + 1], c->stream));
-    pend_pull[npending++] = pull;
+    pend_kind[npending++] = pull ? KIND_PULL : KIND_PUSH;
     ++(pull ? launches_pull : launches_push);
     ++launches;
     return SX_OK;
@@ -255,7 +255,7 @@ sx_status Run::sync(bool tail_copy) {
     for (int i = 0; i < npending; ++i) {
         float ms = 0;
         SX_CU(cudaEventElapsedTime(&ms, c->evp[2 * i], c->evp[2 * i + 1]));
-        (pend_pull[i] ? ms_pull : ms_push) += ms;
+        (pend_kind[i] == KIND_PULL ? ms_pull : pend_kind[i] == KIND_FUSED ? ms_fused : ms_push) += ms;
     }
     npending = 0;
     if (c->h_ctl->error) return fail(SX_E_BARRIER, "grid barrier watchdog fired");
@@ -302,6 +302,9 @@ sx_status Run::end(BytesFn bytes) {
         st->ms_pull = ms_pull;
         st->launches_push = launches_push;
         st->launches_pull = launches_pull;
+        st->ms_fused = ms_fused;
+        st->launches_fused = launches_fused;
+        st->runs = 1;
     }
     if (o.trace && o.trace_cap) {
         const uint64_t nrec = std::min<uint64_t>(std::min<uint64_t>(h.ntrace, o.trace_cap), g->trace_cap);
@@ -392,6 +395,12 @@ sx_status sx_ctx_create(int device, void* cuda_stream, sx_ctx* out) {
             return sxh::cuda_fail(e, "cudaEventCreate");
         }
     }
+    for (auto& ev : c->eva) {
+        if ((e = cudaEventCreate(&ev)) != cudaSuccess) {
+            sx_ctx_destroy(c);
+            return sxh::cuda_fail(e, "cudaEventCreate");
+        }
+    }
     if ((e = cudaHostAlloc(&c->h_ctl, sizeof(Ctl), cudaHostAllocMapped)) != cudaSuccess ||
         (e = cudaHostGetDevicePointer((void**)&c->d_hctl, c->h_ctl, 0)) != cudaSuccess) {
         sx_ctx_destroy(c);
@@ -422,6 +431,8 @@ void sx_ctx_destroy(sx_ctx c) {
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     for (auto ev : c->evp)
+        if (ev) cudaEventDestroy(ev);
+    for (auto ev : c->eva)
         if (ev) cudaEventDestroy(ev);
     if (c->h_ctl) cudaFreeHost(c->h_ctl);
     if (c->pool) {

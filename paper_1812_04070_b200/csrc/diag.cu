@@ -18,9 +18,50 @@ __global__ void __launch_bounds__(BLOCK, 4) barrier_loop(Ctl* c, uint32_t iters)
     }
 }
 
+// Fault injection (P:707-711 deadlock, P:724-729 co-residency): CTA `skip`
+// never arrives at the barrier, so the others wait until the watchdog fires;
+// every CTA then leaves (the kernel ends normally, the context stays usable).
+__global__ void __launch_bounds__(BLOCK, 4) barrier_skip(Ctl* c, uint32_t skip) {
+    grid_begin(c);
+    if (blockIdx.x == skip) return;
+    grid_sync(c);
+}
+
 }  // namespace sx
 
 using namespace sx;
+
+extern "C" sx_status sx_barrier_fault(sx_ctx c, uint32_t mode, uint32_t timeout_ms) {
+    if (mode < 1 || mode > 2 || (mode == 2 && timeout_ms == 0))
+        return sxh::fail(SX_E_INVALID, "sx_barrier_fault: mode must be 1 or 2 (2 needs timeout_ms > 0)");
+    sx_status rc = sxh::check_ctx(c);
+    if (rc != SX_OK) return rc;
+    int per_sm = 0;
+    SX_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, barrier_skip, BLOCK, 0));
+    const int grid = per_sm * c->prop.multiProcessorCount;
+    Ctl* d = nullptr;
+    SX_CU(cudaMalloc(&d, sizeof(Ctl)));
+    SX_CU(cudaMemsetAsync(d, 0, sizeof(Ctl), c->stream));
+    uint32_t skip = mode == 2 ? (uint32_t)grid - 1 : 0xFFFFFFFFu;
+    void* args[] = {&d, &skip};
+    const unsigned long long wd = (unsigned long long)timeout_ms * 1000000ull, wd0 = 20000000000ull;
+    if (mode == 2) SX_CU(cudaMemcpyToSymbolAsync(g_watchdog_ns, &wd, sizeof(wd), 0, cudaMemcpyHostToDevice, c->stream));
+    // mode 1: one CTA more than can be co-resident; the driver must refuse the
+    // cooperative launch (a software barrier over such a grid could deadlock)
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)barrier_skip, dim3(mode == 1 ? grid + 1 : grid),
+                                                dim3(BLOCK), args, 0, c->stream);
+    const cudaError_t le = e;
+    if (e != cudaSuccess) cudaGetLastError();
+    Ctl h{};
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e == cudaSuccess) e = cudaMemcpy(&h, d, sizeof(Ctl), cudaMemcpyDeviceToHost);
+    if (mode == 2) cudaMemcpyToSymbol(g_watchdog_ns, &wd0, sizeof(wd0));
+    cudaFree(d);
+    if (le == cudaErrorCooperativeLaunchTooLarge) return sxh::cuda_fail(le, "cudaLaunchCooperativeKernel(grid + 1)");
+    if (e != cudaSuccess) return sxh::cuda_fail(e, "barrier_skip");
+    if (h.error) return sxh::fail(SX_E_BARRIER, "barrier watchdog fired");
+    return SX_OK;
+}
 
 extern "C" sx_status sx_barrier_bench(sx_ctx c, uint32_t iters, double* us_per_barrier, int* ctas) {
     if (!us_per_barrier || iters == 0) return sxh::fail(SX_E_INVALID, "sx_barrier_bench: bad argument");

@@ -108,6 +108,14 @@ struct Ctl {
     } st[2];
 };
 
+// Statistics of the runs enqueued without a host sync (sx_bfs_async): the
+// fused kernel's CTA 0 adds each run's stat blocks here at its end; the host
+// reads and zeroes them at sx_graph_sync.
+struct AsyncAcc {
+    Ctl::StatBlock st[2];
+    unsigned int runs, errors;
+};
+
 // The run state carried across launches (Ctl from `iter` to `ntrace`), as one
 // CTA sees it: run_state() reads the 128-B line once per CTA (warp 0, lane l
 // word l) instead of every thread loading each field from the same L2 line.
@@ -242,6 +250,9 @@ __device__ __forceinline__ void grid_end(Ctl* c) {
     c->bar_top[q].count = 0;
 }
 
+// Barrier watchdog in ns (20 s); sx_barrier_fault lowers it for its test and restores it.
+static __device__ unsigned long long g_watchdog_ns = 20000000000ull;
+
 __device__ __forceinline__ bool grid_sync(Ctl* c) {
     __shared__ uint32_t s_err;
     __syncthreads();
@@ -265,7 +276,7 @@ __device__ __forceinline__ bool grid_sync(Ctl* c) {
             if (((++spins) & 1023u) == 0) {
                 const uint64_t t = globaltimer();
                 if (t0 == 0) t0 = t;
-                else if (t - t0 > 20000000000ull) atomicExch(&c->error, ERR_BARRIER);
+                else if (t - t0 > g_watchdog_ns) atomicExch(&c->error, ERR_BARRIER);
                 if (vload(&c->error)) break;
             }
         }

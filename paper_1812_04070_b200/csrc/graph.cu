@@ -216,6 +216,7 @@ sx_status sx_graph_upload(sx_ctx ctx, const sx_csr_desc* d, sx_graph* out) {
     TRY(dalloc(ctx, &g->cta_cnt, NCLS * MAX_GRID));
     TRY(dalloc(ctx, (char**)&g->ctl, sizeof(Ctl)));
     for (int i = 0; i < 4; ++i) TRY(dalloc(ctx, &g->st[i], n));
+    TRY(sxh::bfs_prepare(g));  // BFS hub-first probe table (graph residency, not per-run work)
     e = cudaStreamSynchronize(s);
     pt.mark("upload: workspace");
     if (e != cudaSuccess) return bail(sxh::cuda_fail(e, "graph upload"));
@@ -237,6 +238,7 @@ void sx_graph_free(sx_graph g) {
     if (!g) return;
     sx_ctx c = g->ctx;
     cudaSetDevice(c->device);
+    sxh::drain_async(c);  // book (and forget) enqueued async runs: none may point at g afterwards
     cudaStreamSynchronize(c->stream);
     PhaseTimer pt(c->stream);
     auto F = [&](void* p) { sxh::dfree(c, p); };
@@ -267,6 +269,7 @@ void sx_graph_free(sx_graph g) {
     F(g->hacc);
     F(g->dstate);
     F(g->hub);
+    F(g->async_acc);
     F(g->pp_hcol);
     F(g->pp_rs);
     F(g->pp_hubs);

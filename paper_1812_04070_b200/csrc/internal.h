@@ -18,6 +18,13 @@ struct sx_ctx_s {
     sx::Ctl* h_ctl = nullptr;  // pinned, device-mapped host mirror of the control block
     sx::Ctl* d_hctl = nullptr; // device address of h_ctl (the tail-copy kernel writes it directly)
     cudaMemPool_t pool = nullptr;  // stream-ordered pool of graph memory (kept, not returned to the driver)
+    // runs enqueued without a host sync (sx_bfs_async): three events each
+    // (before the init, between init and the fused kernel, after it), drained
+    // into the owning graph's accumulators at sx_graph_sync or when the ring is full
+    static constexpr int ASYNC_POOL = 64;
+    cudaEvent_t eva[3 * ASYNC_POOL] = {};
+    sx_graph async_g[ASYNC_POOL] = {};
+    int nasync = 0;
 };
 
 struct sx_graph_s {
@@ -50,7 +57,11 @@ struct sx_graph_s {
     uint32_t* st[4] = {nullptr, nullptr, nullptr, nullptr};  // 4N-byte state arrays
     double* hacc = nullptr;       // n+1 doubles, pull-all split-row partial sums (lazy)
     double* dstate = nullptr;     // 2n doubles, BP beliefs (lazy)
-    uint32_t* hub = nullptr;      // n entries, BFS hub-first probe table (lazy)
+    uint32_t* hub = nullptr;      // n entries, BFS hub-first probe table (built at upload)
+    // sx_bfs_async bookkeeping: device stat accumulator, host-side event times
+    sx::AsyncAcc* async_acc = nullptr;
+    double async_ms = 0, async_ms_fused = 0;
+    uint32_t async_runs = 0;
     // tiled pull-all plan (lazy, pull_all.cu)
     uint32_t* pp_hcol = nullptr;  // encoded in-edge sources (padded)
     uint32_t* pp_rs = nullptr;    // row-start bitmap over in-edges
@@ -76,6 +87,11 @@ sx_status cuda_fail(cudaError_t e, const char* what);
     } while (0)
 
 sx::DevGraph dev_graph(const sx_graph g);
+enum { KIND_PUSH = 0, KIND_PULL = 1, KIND_FUSED = 2 };
+// BFS per-graph preparation (the hub-first probe table), run by sx_graph_upload.
+sx_status bfs_prepare(sx_graph g);
+// Wait for every run enqueued on the ctx without a sync and book its event times.
+sx_status drain_async(sx_ctx c);
 // Slot region size of a class list: NSLOT regions of R entries cover n.
 inline uint32_t region_size(uint64_t n) { return (uint32_t)((n + sx::NSLOT - 1) / sx::NSLOT + 3) & ~3u; }
 // Fill the scheduling parameters common to every persistent kernel.
@@ -101,13 +117,14 @@ struct Run {
     sx_graph g;
     sx_opts o;
     sx_stats* st;
-    float ms_push = 0, ms_pull = 0;
-    uint32_t launches = 0, launches_push = 0, launches_pull = 0;
+    float ms_push = 0, ms_pull = 0, ms_fused = 0;
+    uint32_t launches = 0, launches_push = 0, launches_pull = 0, launches_fused = 0;
     int npending = 0;
-    bool pend_pull[EV_POOL] = {};
+    int pend_kind[EV_POOL] = {};
     sx_status begin(bool zero_ctl = true);  // zero_ctl = false: the algorithm's init kernel zeroes it
     // Enqueue one persistent kernel (timed with an event pair); no host sync.
-    sx_status launch(const void* fn, void** args, bool pull, int smem = 0);
+    // kind: KIND_PUSH / KIND_PULL (a direction phase), KIND_FUSED (all phases, fusion = 2).
+    sx_status launch(const void* fn, void** args, int kind, int smem = 0);
     // Same for a non-cooperative launch with an explicit shape (e.g. one cluster).
     sx_status launch_plain(const void* fn, void** args, int grid, int block, bool pull);
     // Read back the control block, accumulate the pending launches' times, check errors.

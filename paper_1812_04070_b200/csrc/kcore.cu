@@ -319,7 +319,7 @@ extern "C" sx_status sx_kcore(sx_graph g, uint32_t k, const sx_opts* opts, uint3
     void* args[] = {&p};
     g->ctx->h_ctl->done = 0;
     for (;;) {
-        if ((rc = run.launch((const void*)kcore_push, args, false)) != SX_OK) return rc;
+        if ((rc = run.launch((const void*)kcore_push, args, sxh::KIND_PUSH)) != SX_OK) return rc;
         if ((rc = run.sync()) != SX_OK) return rc;
         if (g->ctx->h_ctl->done) break;
     }

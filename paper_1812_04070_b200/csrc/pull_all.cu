@@ -639,7 +639,7 @@ sx_status run_pull(sx_graph g, const sx_opts* opts, sx_stats* stats, const Op& o
     p.acc = g->hacc;
     void* args[] = {&p};
     const int smem = (int)(PULL_HUBS * sizeof(typename Op::HubT));
-    if ((rc = run.launch((const void*)pull_all<Op>, args, true, smem)) != SX_OK) return rc;
+    if ((rc = run.launch((const void*)pull_all<Op>, args, sxh::KIND_PULL, smem)) != SX_OK) return rc;
     t_edge_bytes = edge_bytes;
     t_vertex_bytes = vertex_bytes;
     return run.end(pull_bytes);

@@ -843,7 +843,7 @@ static sx_status run_sssp(sx_graph g, uint32_t src, uint32_t delta, const sx_opt
     uint32_t dir = DIR_PUSH;
     auto enqueue = [&](uint32_t d) -> sx_status {
         if (d == DIR_CLUSTER) return run.launch_plain((const void*)sssp_cluster, args, CL_CTAS, CL_BLOCK, false);
-        return run.launch(d == DIR_PULL ? (const void*)sssp_pull : (const void*)sssp_push, args, d == DIR_PULL);
+        return run.launch(d == DIR_PULL ? (const void*)sssp_pull : (const void*)sssp_push, args, d == DIR_PULL ? sxh::KIND_PULL : sxh::KIND_PUSH);
     };
     for (;;) {
         const uint32_t seq[3] = {dir, dir == DIR_PUSH ? DIR_PULL : DIR_PUSH, dir == DIR_PUSH ? DIR_CLUSTER : dir};

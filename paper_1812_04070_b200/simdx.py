@@ -55,7 +55,8 @@ class sx_stats(ctypes.Structure):
                 ("edges_examined", _u64), ("vertices_scanned", _u64), ("list_entries", _u64),
                 ("bytes_model", ctypes.c_double), ("ms", ctypes.c_double), ("ms_push", ctypes.c_double),
                 ("ms_pull", ctypes.c_double), ("bytes_push", ctypes.c_double), ("bytes_pull", ctypes.c_double),
-                ("launches_push", _u32), ("launches_pull", _u32)]
+                ("launches_push", _u32), ("launches_pull", _u32), ("ms_fused", ctypes.c_double),
+                ("launches_fused", _u32), ("runs", _u32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -87,6 +88,9 @@ _lib.sx_graph_free.restype = None
 _lib.sx_opts_default.argtypes = [_P(sx_opts)]
 _lib.sx_opts_default.restype = None
 _lib.sx_bfs.argtypes = [_vp, _u32, _P(sx_opts), _vp, _P(sx_stats)]
+_lib.sx_bfs_async.argtypes = [_vp, _u32, _P(sx_opts), _vp]
+_lib.sx_graph_sync.argtypes = [_vp, _P(sx_stats)]
+_lib.sx_barrier_fault.argtypes = [_vp, _u32, _u32]
 _lib.sx_sssp.argtypes = [_vp, _u32, _u32, _P(sx_opts), _vp, _P(sx_stats)]
 _lib.sx_pagerank.argtypes = [_vp, _f32, _u32, _P(sx_opts), _vp, _P(sx_stats)]
 _lib.sx_kcore.argtypes = [_vp, _u32, _P(sx_opts), _vp, _P(sx_stats)]
@@ -105,13 +109,15 @@ _lib.sx_dist_free.restype = None
 _lib.sx_dist_bfs.argtypes = [_vp, _u32, _P(sx_opts), _P(_vp), _P(sx_stats)]
 _lib.sx_dist_sssp.argtypes = [_vp, _u32, _u32, _P(sx_opts), _P(_vp), _P(sx_stats)]
 for _f in ("sx_ctx_create", "sx_ctx_info", "sx_graph_upload", "sx_graph_info", "sx_graph_rmat", "sx_graph_grid",
-           "sx_graph_download", "sx_bfs", "sx_sssp", "sx_pagerank",
+           "sx_graph_download", "sx_bfs", "sx_bfs_async", "sx_graph_sync", "sx_barrier_fault", "sx_sssp",
+           "sx_pagerank",
            "sx_kcore", "sx_spmv", "sx_bp", "sx_wcc", "sx_barrier_bench", "sx_cluster_bench", "sx_launch_bench",
            "sx_nccl_unique_id", "sx_dist_create", "sx_dist_range", "sx_dist_upload", "sx_dist_bfs", "sx_dist_sssp"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 EXPORTED = ["sx_status_str", "sx_last_error", "sx_version", "sx_ctx_create", "sx_ctx_destroy", "sx_ctx_info",
-            "sx_graph_upload", "sx_graph_info", "sx_graph_free", "sx_graph_rmat", "sx_graph_grid", "sx_graph_download", "sx_opts_default", "sx_bfs", "sx_sssp",
+            "sx_graph_upload", "sx_graph_info", "sx_graph_free", "sx_graph_rmat", "sx_graph_grid", "sx_graph_download",
+            "sx_opts_default", "sx_bfs", "sx_bfs_async", "sx_graph_sync", "sx_barrier_fault", "sx_sssp",
             "sx_pagerank", "sx_kcore", "sx_spmv", "sx_bp", "sx_wcc", "sx_barrier_bench", "sx_cluster_bench", "sx_launch_bench",
             "sx_nccl_unique_id", "sx_dist_create", "sx_dist_range", "sx_dist_upload", "sx_dist_free", "sx_dist_bfs", "sx_dist_sssp"]
 
@@ -292,6 +298,26 @@ def sx_bfs(g, src, opts, level_out, n=None):
     return _run(_lib.sx_bfs, "sx_bfs", g, level_out, opts, (src,), n=n)
 
 
+def sx_bfs_async(g, src, opts, level_out, n=None):
+    """Enqueue a BFS (all fusion) without waiting; level_out must be a CUDA tensor."""
+    if not _on_device(level_out):
+        raise ValueError("sx_bfs_async: level_out must be a CUDA tensor")
+    o = opts if opts is not None else sx_opts_default()
+    _check(_lib.sx_bfs_async(g, src, ctypes.byref(o), _ptr_n(level_out, _nv(g, n), "sx_bfs_async out")),
+           "sx_bfs_async")
+
+
+def sx_graph_sync(g) -> sx_stats:
+    st = sx_stats()
+    _check(_lib.sx_graph_sync(g, ctypes.byref(st)), "sx_graph_sync")
+    return st
+
+
+def sx_barrier_fault(ctx, mode: int, timeout_ms: int = 0) -> int:
+    """Status code of the injected barrier fault (SX_E_BARRIER = detected)."""
+    return _lib.sx_barrier_fault(ctx, mode, timeout_ms)
+
+
 def sx_sssp(g, src, delta, opts, dist_out, n=None):
     return _run(_lib.sx_sssp, "sx_sssp", g, dist_out, opts, (src, delta), n=n)
 
@@ -429,6 +455,15 @@ class Graph:
         o, buf = self._opts(dict(kw))
         st = sx_bfs(self.h, src, o, out, self.n)
         return out, st.as_dict(), self._trace(buf, st)
+
+    def bfs_async(self, src: int, out, **kw):
+        """sx_bfs_async: enqueue one BFS into the CUDA tensor `out`; no wait."""
+        o, _ = self._opts(dict(kw))
+        sx_bfs_async(self.h, src, o, out, self.n)
+
+    def sync(self) -> dict:
+        """sx_graph_sync: wait for the enqueued runs; their summed statistics."""
+        return sx_graph_sync(self.h).as_dict()
 
     def sssp(self, src: int, delta: int = 0, out=None, **kw):
         out = np.empty(self.n, np.uint32) if out is None else out
