@@ -11,6 +11,7 @@ path) and never imports it; its only inputs are simgen CSR graphs and vectors.
   coreness   C-K  Batagelj-Zaversnik buckets
   kcore_mask C-K  core(v) >= k
   pagerank   C-P  fp64 Jacobi, T steps          (reading 14)
+  pagerank_conv C-PC fp64 Jacobi until L1 delta < eps (readings 25-26: both recurrences)
   spmv       C-V  fp64 y = A^T x over in-edges  (north_star)
   bp         C-BP fp64 log-odds Jacobi          (model = reading 15; T=1..4 closed forms)
   wcc        C-W  min vertex id per component   (P:345 names WCC)
@@ -50,6 +51,9 @@ def _L():
         lib.oracle_sssp.argtypes = [u64, vp, vp, vp, i32, u32, vp]
         lib.oracle_coreness.argtypes = [u64, vp, vp, vp]
         lib.oracle_pagerank.argtypes = [u64, vp, vp, vp, ctypes.c_double, u32, vp]
+        lib.oracle_pagerank_conv.argtypes = [u64, vp, vp, vp, ctypes.c_double, ctypes.c_double, u32, i32, vp,
+                                             ctypes.POINTER(u32), ctypes.POINTER(ctypes.c_double)]
+        lib.oracle_pagerank_conv.restype = ctypes.c_int
         lib.oracle_spmv.argtypes = [u64, vp, vp, vp, i32, vp, vp]
         lib.oracle_bp.argtypes = [u64, vp, vp, vp, i32, vp, u32, vp, vp]
         lib.oracle_wcc.argtypes = [u64, vp, vp, vp]
@@ -110,6 +114,19 @@ def pagerank(g, damping: float = 0.85, iters: int = 20) -> np.ndarray:
     _chk(_L().oracle_pagerank(g.n, _p(g.row_ptr), _p(g.in_ptr()), _p(g.in_idx()), damping, iters, _p(out)),
          "pagerank")
     return out
+
+
+def pagerank_conv(g, damping: float = 0.85, eps: float = 1e-6, max_iter: int = 1000, variant: int = 0):
+    """oracle.c:oracle_pagerank_conv — Jacobi until the L1 change < eps.
+    variant 0: normalised, dangling redistributed (reading 14); 1: SPEC S:487 (1-d) + d*sum, dangling dropped.
+    Returns (ranks fp64, iterations, last L1 change)."""
+    _full(g)
+    out = np.empty(g.n, np.float64)
+    it = ctypes.c_uint32()
+    dl = ctypes.c_double()
+    _chk(_L().oracle_pagerank_conv(g.n, _p(g.row_ptr), _p(g.in_ptr()), _p(g.in_idx()), damping, eps, max_iter,
+                                   variant, _p(out), ctypes.byref(it), ctypes.byref(dl)), "pagerank_conv")
+    return out, it.value, dl.value
 
 
 def spmv(g, x: np.ndarray) -> np.ndarray:

@@ -216,6 +216,53 @@ int oracle_pagerank(uint64_t n, const uint64_t* out_ptr, const uint64_t* in_ptr,
     return 0;
 }
 
+/* C-PC, PageRank to convergence ("updates the rank value of one vertex
+ * ... iteratively till all vertices have stable rank values"; the stopping
+ * test and both recurrences are readings 25-26 of DESIGN.md):
+ *   variant 0 (reading 14, normalised):  r_0 = 1/N,
+ *       r_{t+1}(u) = (1-d)/N + d * ( sum_{v in in(u)} r_t(v)/outdeg(v) + D_t/N ),
+ *       D_t = sum_{outdeg(v)=0} r_t(v)
+ *   variant 1 (un-normalised, dangling mass dropped): r_0 = 1,
+ *       r_{t+1}(u) = (1-d) + d * sum_{v in in(u)} r_t(v)/outdeg(v)
+ * Jacobi steps until the L1 change delta_t = sum_u |r_{t+1}(u) - r_t(u)| < eps
+ * ("converged when L1 delta < epsilon"), at most max_iter steps.
+ * *iters = steps taken; *last_delta = the last delta_t. */
+int oracle_pagerank_conv(uint64_t n, const uint64_t* out_ptr, const uint64_t* in_ptr, const uint32_t* in_idx,
+                         double d, double eps, uint32_t max_iter, int variant, double* rank, uint32_t* iters,
+                         double* last_delta) {
+    *iters = 0;
+    *last_delta = 0.0;
+    if (n == 0) return 0;
+    double* r = (double*)malloc(n * sizeof(double));
+    double* rn = (double*)malloc(n * sizeof(double));
+    if (!r || !rn) { free(r); free(rn); return -2; }
+    const double N = (double)n;
+    for (uint64_t v = 0; v < n; ++v) r[v] = variant == 0 ? 1.0 / N : 1.0;
+    for (uint32_t t = 0; t < max_iter; ++t) {
+        double D = 0.0;
+        if (variant == 0)
+            for (uint64_t v = 0; v < n; ++v)
+                if (out_ptr[v + 1] == out_ptr[v]) D += r[v];
+        double delta = 0.0;
+        for (uint64_t u = 0; u < n; ++u) {
+            double s = 0.0;
+            for (uint64_t e = in_ptr[u]; e < in_ptr[u + 1]; ++e) {
+                uint32_t v = in_idx[e];
+                s += r[v] / (double)(out_ptr[v + 1] - out_ptr[v]);
+            }
+            rn[u] = variant == 0 ? (1.0 - d) / N + d * (s + D / N) : (1.0 - d) + d * s;
+            delta += fabs(rn[u] - r[u]);
+        }
+        double* tmp = r; r = rn; rn = tmp;
+        *iters = t + 1;
+        *last_delta = delta;
+        if (delta < eps) break;
+    }
+    memcpy(rank, r, n * sizeof(double));
+    free(r); free(rn);
+    return 0;
+}
+
 /* C-V, SpMV (north_star; not in the paper): y[u] = sum_{(v,u) in E} w(v,u) * x[v],
  * w = float(weight) or 1 when unweighted; fp64 accumulation. */
 int oracle_spmv(uint64_t n, const uint64_t* in_ptr, const uint32_t* in_idx, const void* in_w, int wbytes,

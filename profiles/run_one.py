@@ -1,6 +1,6 @@
 """Run one algorithm call on one config (for ncu captures).
 
-usage: python profiles/run_one.py {bfs24|sssp_grid|pr22|kcore24|sssp24} [reps]
+usage: python profiles/run_one.py {bfs24|bfs24all|sssp_grid|pr22|kcore24|sssp24} [reps]
 """
 import os
 import sys
@@ -28,6 +28,8 @@ out = torch.empty(g.n, dtype=torch.int32, device="cuda:0")
 for _ in range(reps):
     if what == "bfs24":
         _, st, _ = G.bfs(0, out=out)
+    elif what == "bfs24all":
+        _, st, _ = G.bfs(0, out=out, fusion=2, cluster_enter=0)
     elif what == "sssp_grid":
         _, st, _ = G.sssp(0, 1024, out=out)
     elif what == "sssp24":

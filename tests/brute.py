@@ -93,6 +93,21 @@ def pagerank_eigvec(n, src, dst, d):
     return v / v.sum()
 
 
+def pagerank_linear_solve(n, src, dst, d, variant):
+    """Exact fixed point of the PageRank recurrence by a dense linear solve
+    (numpy.linalg.solve), matrices from the tuples.
+    variant 0: r = (1-d)/n + d (P r + (e_dang . r)/n)   (column-stochastic, dangling redistributed)
+    variant 1: r = (1-d) + d P r                          (dangling dropped)"""
+    outdeg = np.bincount(src, minlength=n).astype(float)
+    P = np.zeros((n, n))
+    for a, b in zip(src, dst):
+        P[b, a] += 1.0 / outdeg[a]
+    if variant == 0:
+        P[:, outdeg == 0] = 1.0 / n
+        return np.linalg.solve(np.eye(n) - d * P, np.full(n, (1 - d) / n))
+    return np.linalg.solve(np.eye(n) - d * P, np.full(n, 1 - d))
+
+
 def spmv_dense(n, src, dst, w, x):
     A = np.zeros((n, n))
     for a, b, c in zip(src, dst, w):

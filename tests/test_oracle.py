@@ -288,6 +288,66 @@ def test_pagerank_star_recurrence():
     assert abs(r[0] - (1 + d * k) / (N * (1 + d))) < 1e-14
 
 
+# ---------------------------------------------------------------- PageRank to convergence (C-PC)
+# Both recurrences are contractions of factor d in L1 (column-(sub)stochastic
+# transition matrix), so a Jacobi iterate whose last L1 change is delta lies
+# within d/(1-d) * delta of the exact fixed point ("till all vertices
+# have stable rank values"; "converged when L1 delta < epsilon").
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("eps", [1e-4, 1e-8])
+def test_pagerank_conv_within_contraction_bound_of_linear_solve(variant, eps):
+    d = 0.85
+    for seed, sym in ((1, True), (2, False), (3, True), (4, False)):
+        g = simgen.random_graph(30, 50, seed, symmetric=sym)
+        s, t, _ = brute.tuples_of(g)
+        ref = brute.pagerank_linear_solve(g.n, s, t, d, variant)
+        r, it, delta = oracle.pagerank_conv(g, d, eps, 10000, variant)
+        assert delta < eps and it >= 1
+        assert np.abs(r - ref).sum() <= d / (1 - d) * delta + 1e-12, (seed, variant)
+
+
+def test_pagerank_conv_stops_at_first_step_below_eps():
+    # variant 0 is the fixed-T oracle's recurrence: step `it` is the first whose L1 change is < eps
+    g = simgen.rmat(9)
+    eps = 1e-7
+    r, it, delta = oracle.pagerank_conv(g, 0.85, eps, 10000, 0)
+    assert np.array_equal(r, oracle.pagerank(g, 0.85, it))
+    prev = np.abs(oracle.pagerank(g, 0.85, it - 1) - oracle.pagerank(g, 0.85, it - 2)).sum()
+    assert prev >= eps and delta < eps
+    assert abs(r.sum() - 1.0) < 1e-12  # mass conservation (dangling redistributed)
+
+
+def test_pagerank_conv_spec_examples_and_closed_forms():
+    d = 0.85
+    one = simgen.from_edges(1, [])
+    r, _, _ = oracle.pagerank_conv(one, d, 1e-12, 100, 1)
+    assert abs(r[0] - 0.15) < 1e-15  # S:489 single vertex -> 1 - d
+    two = simgen.from_edges(2, [(0, 1)])
+    for v in (0, 1):
+        r, _, _ = oracle.pagerank_conv(two, d, 1e-12, 1000, v)
+        assert r[0] == r[1]  # S:488 symmetry
+    # directed cycle: every vertex has one in- and one out-edge; the fixed point is the start
+    cyc = simgen.from_edges(7, [(i, (i + 1) % 7) for i in range(7)], symmetric=False)
+    r, it, delta = oracle.pagerank_conv(cyc, d, 1e-12, 100, 1)
+    assert it == 1 and delta == 0.0 and np.all(r == 1.0)
+    # star K_{1,k}: normalised c* = (1 + d k) / (N (1 + d)); SPEC variant c* = (1 + d k) / (1 + d)
+    k = 9
+    N = k + 1
+    star = simgen.from_edges(N, [(0, i) for i in range(1, N)])
+    r, _, delta = oracle.pagerank_conv(star, d, 1e-13, 10000, 0)
+    assert abs(r[0] - (1 + d * k) / (N * (1 + d))) < 1e-12
+    r, _, delta = oracle.pagerank_conv(star, d, 1e-13, 10000, 1)
+    c = (1 + d * k) / (1 + d)
+    assert abs(r[0] - c) < 1e-12 and np.allclose(r[1:], (1 - d) + d * c / k, rtol=0, atol=1e-12)
+    # SPEC invariant: every rank >= 1 - d (the empty sum is the minimum)
+    g = simgen.random_graph(500, 3000, 7, symmetric=False)
+    r, _, _ = oracle.pagerank_conv(g, d, 1e-9, 10000, 1)
+    assert r.min() >= 1 - d - 1e-15
+    # random G(500, 3000) against dense power iteration within 1e-6 L1
+    s, t, _ = brute.tuples_of(g)
+    assert np.abs(r - brute.pagerank_linear_solve(g.n, s, t, d, 1)).sum() < 1e-6
+
+
 # ---------------------------------------------------------------- SpMV (C-V)
 @pytest.mark.parametrize("sym", [True, False])
 def test_spmv_vs_dense_matvec(sym):
