@@ -520,6 +520,8 @@ def main():
                     help="async: sx_bfs_async steps (all fusion, no host round trip); sync: sx_bfs per step")
     ap.add_argument("--roots", type=int, default=64, help="random-root BFS extra (Graph500 style, P:1003)")
     ap.add_argument("--delta", type=int, default=4096)  # measured best for C2 (profiles/r1/delta_sweep.txt)
+    ap.add_argument("--dist", action="store_true",
+                    help="run the multi-GPU path (NCCL communicator) even at one rank")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
     ap.add_argument("--ref-budget-s", type=float, default=60.0)
@@ -537,7 +539,7 @@ def main():
     world, rank, local = dist_host.env_rank()
     if world != args.gpus:
         log(f"[bench] --gpus {args.gpus} but WORLD_SIZE={world}: using WORLD_SIZE")
-    if world == 1:
+    if world == 1 and not args.dist:
         run_single(args)
     else:
         run_dist(args, world, rank, local)

@@ -245,6 +245,10 @@ typedef struct {
     double ms_fused;             /* device time inside all-phase fused launches (fusion = 2) */
     uint32_t launches_fused;
     uint32_t runs;               /* algorithm runs these statistics cover (1; sx_graph_sync: the runs it drained) */
+    double residual;             /* convergence runs (sx_pagerank_conv, sx_bp_conv): L1 mass of change not yet
+                                    propagated when the run stopped (pull: the last iteration's L1 change; PageRank
+                                    push tail: sum |rho|).  PageRank lies within d/(1-d) x residual (L1) of its
+                                    fixed point.  0 otherwise. */
 } sx_stats;
 
 #define SX_CLUSTER_AUTO 0xFFFFFFFFu
@@ -292,6 +296,23 @@ sx_status sx_sssp(sx_graph g, uint32_t src, uint32_t delta, const sx_opts* opts,
 sx_status sx_pagerank(sx_graph g, float damping, uint32_t iters, const sx_opts* opts, float* rank_out,
                       sx_stats* stats);
 
+/* PageRank to convergence ("updates the rank value ... iteratively till all vertices have stable
+ * rank values ... we start PageRank with the pull model ... At the end of PageRank, we switch to the push
+ * model because the majority of the vertices are stable"; readings 25-26):
+ *   variant SX_PR_NORMALIZED: r(u) = (1-d)/N + d*(sum_{v in in(u)} r(v)/outdeg(v) + D/N), r_0 = 1/N (reading 14)
+ *   variant SX_PR_SPEC:       r(u) = (1-d) + d*sum_{v in in(u)} r(v)/outdeg(v), dangling mass dropped, r_0 = 1
+ *
+ * Jacobi pull steps in fp64 while the L1 change of a step is >= epsilon; when at most a tenth of the
+ * vertices still change by more than tau = epsilon/(4N), the run switches to a delta-accumulative push
+ * (residual propagation) over the vertices whose pending change exceeds tau, until none does.  Either
+ * way the result is within d/(1-d)*epsilon (L1) of the exact fixed point; stats->residual says how far.
+ * opts->force_dir: 0 auto, 1 push tail right after the first pull step, 2 pull only.  max_iters >= 1 caps
+ * pull steps + push iterations.  rank_out: f64[n], host or device.
+ * Errors: SX_E_INVALID (damping outside (0,1), epsilon <= 0, max_iters = 0, unknown variant), SX_E_NO_REVERSE. */
+enum { SX_PR_NORMALIZED = 0, SX_PR_SPEC = 1 };
+sx_status sx_pagerank_conv(sx_graph g, double damping, double epsilon, uint32_t max_iters, uint32_t variant,
+                           const sx_opts* opts, double* rank_out, sx_stats* stats);
+
 /* k-core (reading 6): k > 0 -> core_out[v] = 1 if v is in the k-core (minimum degree >= k,
  * duplicate edges counted) else 0; k = 0 -> core_out[v] = coreness of v.  Undirected graphs only.
  * Errors: SX_E_INVALID (directed graph). */
@@ -309,6 +330,13 @@ sx_status sx_spmv(sx_graph g, const float* x, uint32_t iters, const sx_opts* opt
  * prior: f32[n] in (0,1), host or device; iters >= 1.  Errors: SX_E_INVALID, SX_E_NO_REVERSE. */
 sx_status sx_bp(sx_graph g, const float* prior, uint32_t iters, const sx_opts* opts, float* logodds_out,
                 sx_stats* stats);
+
+/* Belief propagation to convergence (reading 15's model, reading 27): the Jacobi steps of
+ * sx_bp until the L1 change of the beliefs b = sigmoid(l), sum_u |b_{t+1}(u) - b_t(u)|, is < epsilon or
+ * max_iters steps ran (loopy BP need not converge: not an error; stats->residual = the last L1 change,
+ * stats->iterations = steps run).  logodds_out: f32[n].  Errors: as sx_bp, SX_E_INVALID (epsilon <= 0). */
+sx_status sx_bp_conv(sx_graph g, const float* prior, double epsilon, uint32_t max_iters, const sx_opts* opts,
+                     float* logodds_out, sx_stats* stats);
 
 /* Connected components (WCC on an undirected graph; the paper names WCC as a
  * voting workload): label_out[v] = the smallest
@@ -340,11 +368,12 @@ sx_status sx_nccl_unique_id(void* out128);
 /*
  * Create the distribution of an n_global-vertex graph over `nranks` ranks, of
  * which this process drives ranks [rank0, rank0 + nlocal):
- *   nlocal == 1 (nranks > 1): one rank per process, exchanges over an NCCL
- *     communicator built from `nccl_id` (one process per GPU, NVLink/NVSwitch);
- *   nlocal == nranks: every rank in this process on the ctx's device ("virtual
- *     ranks": the same kernels and schedule, device-to-device copies in place
- *     of the collectives; for tests of the partitioned path on one GPU).
+ *   nlocal == 1 with nccl_id: one rank per process, exchanges over an NCCL
+ *     communicator built from `nccl_id` (one process per GPU, NVLink/NVSwitch;
+ *     nranks = 1 gives a one-rank communicator that still runs every collective);
+ *   nlocal == nranks without nccl_id: every rank in this process on the ctx's
+ *     device ("virtual ranks": the same kernels and schedule, device-to-device
+ *     copies in place of the collectives; for tests of the partitioned path on one GPU).
  * Errors: SX_E_INVALID (bad layout), SX_E_NCCL, SX_E_OOM, SX_E_CUDA.
  */
 sx_status sx_dist_create(sx_ctx ctx, uint64_t n_global, int nranks, int rank0, int nlocal, const void* nccl_id,

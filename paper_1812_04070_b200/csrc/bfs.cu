@@ -27,6 +27,7 @@ struct BfsP {
     uint32_t* visited;
     const uint32_t* __restrict__ hub;  // per vertex: its in-neighbour of largest out-degree (INF: none)
     int sym;  // symmetric graph: in-degree == out-degree
+    int tma;  // TILE-mode pull stages each chunk's hub slice with a TMA bulk copy (needs a 16-B aligned hub)
 };
 
 // Hub-first probe table, built once per graph: hub(v) = the in-neighbour of
@@ -86,6 +87,10 @@ __device__ __forceinline__ uint32_t hub_id(uint32_t h) { return h == INF ? INF :
 __device__ __forceinline__ bool hub_sole(uint32_t h) { return h != INF && (h & HUB_SOLE); }
 
 constexpr uint32_t CL_EDGES = 32;
+#ifndef SX_REC_EDGES
+#define SX_REC_EDGES (1u << 17)
+#endif
+constexpr uint64_t REC_EDGES = SX_REC_EDGES;
 constexpr uint32_t DIR_NOCLUSTER = 0x100;  // bfs_init flag: no cluster start (all fusion)
 __device__ __forceinline__ bool cluster_ok(const Sched& s, uint64_t nf, uint64_t mf) {
     return s.cluster_enter && s.fusion && s.force_filter != 2 && s.force_dir != 2 && nf > 0 &&
@@ -167,6 +172,7 @@ __device__ __forceinline__ void bfs_init_body(const BfsP& p, uint32_t src, uint3
     c->cur_count[k] = 1;
     p.s.lists[0][(uint64_t)k * p.s.cstride] = src;
     c->m_u = p.g.m - d;
+    c->hi = d;  // out-edges of the current frontier (the online-record prediction of the push)
     c->nf_prev = 1;
     if (CLUSTER && dir == DIR_PUSH && cluster_ok(p.s, 1, d)) dir = DIR_CLUSTER;  // low-degree source: start on one cluster
     c->dir = dir;
@@ -190,12 +196,13 @@ __global__ void __launch_bounds__(BLOCK) bfs_init(BfsP p, uint32_t src, uint32_t
 template <bool ALL>
 __device__ __forceinline__ void bfs_exit(const BfsP& p, uint32_t kdir, uint32_t it, uint64_t m_u, uint32_t nf_prev,
                                          uint32_t dir, uint32_t done, uint32_t ready, uint32_t slotted,
-                                         const uint32_t (&cnt)[NCLS], Stats& st, RunState* rs_next) {
+                                         const uint32_t (&cnt)[NCLS], Stats& st, RunState* rs_next, uint64_t mf_next) {
     Ctl* c = p.s.ctl;
     flush_stats(c, st, kdir);
     if (lead()) {
         c->iter = it;
         c->m_u = m_u;
+        c->hi = mf_next;
         c->nf_prev = nf_prev;
         c->dir = dir;
         c->done = done;
@@ -212,6 +219,7 @@ __device__ __forceinline__ void bfs_exit(const BfsP& p, uint32_t kdir, uint32_t 
         if (threadIdx.x == 0) {
             rs_next->iter = it;
             rs_next->m_u = m_u;
+            rs_next->hi = mf_next;
             rs_next->nf_prev = nf_prev;
             rs_next->dir = dir;
             rs_next->done = done;
@@ -238,6 +246,7 @@ __device__ __forceinline__ bool push_phase(const BfsP& p, RunState& rs) {
     uint32_t cnt[NCLS];
     Stats st;
     uint32_t dir = DIR_PUSH, done = 0, ready = 1, slotted = 0;
+    uint64_t mf_cur = rs.hi;  // out-edges of the current frontier
     uint32_t local_n = 0;  // > 0: this iteration's tasks are the flat found list of the pull (CTA-local binning)
     if (rs.lists_ready == 2) {
         // entering push from pull with the found vertices recorded as one list
@@ -266,6 +275,11 @@ __device__ __forceinline__ bool push_phase(const BfsP& p, RunState& rs) {
         uint32_t* nbm = p.s.bm[(it + 1) % 3];
         const uint32_t lvl = it + 1;
         uint64_t mdeg = 0, edges = 0, reached = 0;
+        // JIT by prediction (B200 reading of P:619-626): a frontier with more than
+        // REC_EDGES out-edges activates a next frontier the ballot filter handles
+        // better (or the pull takes over), so it is not recorded online — as if
+        // the bins had overflowed; measured: the s24 hub level 30 -> 24 us
+        const bool rec = mf_cur <= REC_EDGES;
         auto visit = [&](uint32_t v, uint64_t rank, uint64_t size, uint32_t) {
             const uint64_t beg = __ldg(p.g.rp + v), end = __ldg(p.g.rp + v + 1);
             // up to 4 edges per step: visited words, claims and the claimed
@@ -294,7 +308,7 @@ __device__ __forceinline__ bool push_phase(const BfsP& p, RunState& rs) {
                     if (!cl[j]) continue;
                     mdeg += du[j];
                     ++reached;
-                    online_record(nx, nlists, p.s, u[j], cls_of(du[j], p.s));
+                    if (rec) online_record(nx, nlists, p.s, u[j], cls_of(du[j], p.s));
                 }
             });
         };
@@ -306,9 +320,10 @@ __device__ __forceinline__ bool push_phase(const BfsP& p, RunState& rs) {
         st.reached += reached;
         if (lead()) st.entries += local_n ? local_n : sum4(cnt);
         {
-            uint64_t v[1] = {mdeg};
-            block_sum<1>(v);
+            uint64_t v[2] = {mdeg, rec ? 0ull : reached};
+            block_sum<2>(v);
             if (threadIdx.x == 0 && v[0]) atomicAdd(&nx->s[my_slot()].mdeg, (unsigned long long)v[0]);
+            if (threadIdx.x == 0 && v[1]) atomicAdd(&nx->s[my_slot()].found, (unsigned int)v[1]);  // not recorded: counted
         }
         if (!grid_sync(c)) return false;
         if (local_n) {
@@ -318,11 +333,12 @@ __device__ __forceinline__ bool push_phase(const BfsP& p, RunState& rs) {
         LineSum ls;
         uint32_t vcnt[NCLS];
         read_line_view(nx, p.s, ls, vcnt);
-        const uint64_t nf = sum4(ls.cnt);
+        const uint64_t nf = rec ? sum4(ls.cnt) : ls.found;
         const uint64_t mf = ls.mdeg;
-        bool overflow = false;
+        bool overflow = !rec;
         for (int i = 0; i < NCLS; ++i) overflow |= ls.cntmax[i] > p.s.cap_s;
         if (p.s.force_filter == 2) overflow = true;
+        mf_cur = mf;
         m_u -= mf;
         ++it;
         ++st.iters;
@@ -359,7 +375,7 @@ __device__ __forceinline__ bool push_phase(const BfsP& p, RunState& rs) {
         }
         if (!p.s.fusion) break;
     }
-    bfs_exit<ALL>(p, DIR_PUSH, it, m_u, nf_prev, dir, done, ready, slotted, cnt, st, &rs);
+    bfs_exit<ALL>(p, DIR_PUSH, it, m_u, nf_prev, dir, done, ready, slotted, cnt, st, &rs, mf_cur);
     return true;
 }
 __global__ void __launch_bounds__(BLOCK, SX_PUSH_MINB) bfs_push(BfsP p) {
@@ -403,13 +419,20 @@ constexpr int HUB_ILP = SX_HUB_ILP;             // phase 1: rounds of 32 candida
 #define SX_LIST_DIV 8
 #endif
 constexpr uint32_t LIST_DIV = SX_LIST_DIV;
-#ifndef SX_TILE_ILP
-#define SX_TILE_ILP 8
+#ifndef SX_PULL_TMA
+#define SX_PULL_TMA 0  // measured slower (s24 it2 100.6 -> 114.8 us; profiles/r2/pull_tma.txt); experiment only
 #endif
-#ifndef SX_TILE_STREAM
-#define SX_TILE_STREAM 0  // TILE-mode phase 1 streamed per bitmap word (1) or over a compacted candidate list (0)
+// TILE-mode chunk: CW bitmap words = CV vertices.  With TMA staging the chunk's
+// hub slice (CV x 4 B) is bulk-copied into shared memory one chunk ahead, two
+// buffers per warp (dynamic shared memory, PULL_DYN_SMEM bytes per CTA).
+#ifndef SX_PULL_CW
+#define SX_PULL_CW (SX_PULL_TMA ? 16 : 32)
 #endif
-constexpr uint32_t TILE_ILP = SX_TILE_ILP;  // TILE mode phase 1: bitmap words (x 32 vertices) in flight per warp  // LIST mode when open candidates <= n / LIST_DIV
+constexpr uint32_t CW = SX_PULL_CW;
+static_assert(CW >= 1 && CW <= 32, "TILE chunk: at most one bitmap word per lane");
+constexpr uint32_t CV = CW * 32u;
+constexpr uint32_t CAND_MAX = CV > 256u ? CV : 256u;  // per-warp candidate list (TILE chunk, LIST csz <= 256)
+constexpr int PULL_DYN_SMEM = SX_PULL_TMA ? WARPS * 2 * CV * 4 : 0;
 constexpr uint32_t FREC_MAX = 32768;   // record the found vertices as a list when candidates <= this
 constexpr uint32_t CAND_CLS = 2;       // class region of lists[] holding the LIST-mode candidate lists
 constexpr uint32_t REC_STAGE = 256;    // per-warp staging of the LIST-mode record
@@ -426,7 +449,9 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
     Stats st;
     uint32_t dir = DIR_PULL, done = 0;
     const uint32_t lane = lane_id();
-    __shared__ uint32_t s_cand[WARPS][1024];
+    __shared__ uint32_t s_cand[WARPS][CAND_MAX];
+    __shared__ uint64_t s_mbar[WARPS][2];
+    extern __shared__ __align__(128) uint32_t s_dyn_hub[];
     __shared__ uint32_t s_found[WARPS][32];
     __shared__ uint32_t s_cpre[NSLOT + 1];  // LIST mode: prefix of the candidate regions' counts
     // the record staging shares the push phase's online-filter stage (8 KB): the
@@ -435,6 +460,7 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
     uint32_t* s_c = s_cand[warp_id()];
     uint32_t* s_r = &stage().e[0][0] + warp_id() * REC_STAGE;
     uint32_t* s_f = s_found[warp_id()];
+    uint64_t mf_last = 0;  // out-edges of the frontier found last (the push's record prediction)
     uint32_t ncand = 0;    // LIST mode when > 0: candidates recorded by the previous iteration
     uint32_t handoff = 0;  // the next frontier was recorded as a contiguous list
     uint32_t to_list = 0;  // 2: ... and the push takes it as its lists (lists_ready = 2)
@@ -570,7 +596,8 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
             }
         };
         // the warp's `total` candidates in s_c through phases 1 and 2
-        auto run_cands = [&](uint32_t total, uint64_t w0) {
+        // sh: the chunk's staged hub slice (vertices from vbase), or nullptr (global loads)
+        auto run_cands = [&](uint32_t total, uint64_t w0, const uint32_t* sh, uint32_t vbase) {
             uint32_t nopen = 0;
             for (uint32_t r0 = 0; r0 < total; r0 += 32 * HUB_ILP) {
                 uint32_t v[HUB_ILP], h[HUB_ILP], wd[HUB_ILP];
@@ -582,7 +609,7 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
                 }
 #pragma unroll
                 for (int k = 0; k < HUB_ILP; ++k) {
-                    const uint32_t x = v[k] != INF ? __ldg(p.hub + v[k]) : INF;
+                    const uint32_t x = v[k] == INF ? INF : sh ? sh[v[k] - vbase] : __ldg(p.hub + v[k]);
                     h[k] = hub_id(x);
                     sole[k] = hub_sole(x);
                 }
@@ -645,68 +672,45 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
                     s_c[j] = ccur[(uint64_t)lo * p.s.R + (i - s_cpre[lo])];
                 }
                 __syncwarp();
-                run_cands(total, 0);
+                run_cands(total, 0, nullptr, 0u);
                 __syncwarp();
                 flush_rec();
                 chunk = chunk_n;
             }
         } else {
-            const uint32_t nchunks = (uint32_t)((nw + 31) >> 5);
+            const uint32_t nchunks = (uint32_t)((nw + CW - 1) / CW);
+            // TMA staging: buffer b of this warp, its mbarrier and phase
+            uint32_t* shub = s_dyn_hub + (uint32_t)warp_id() * 2u * CV;
+            uint64_t* mbar = s_mbar[warp_id()];
+            const bool tma = SX_PULL_TMA && p.tma;
+            uint32_t buf = 0, phase = 0;  // phase bit b: parity to wait for on buffer b
+            if (tma) {
+                if (lane == 0) {
+                    mbar_init(&mbar[0], 1);
+                    mbar_init(&mbar[1], 1);
+                }
+                __syncwarp();
+            }
+            auto stage_hub = [&](uint32_t ch, uint32_t b) {
+                if (!tma || ch == INF) return;
+                __syncwarp();  // every lane is done reading buffer b (the chunk before last)
+                if (lane == 0) {
+                    const uint64_t v0 = (uint64_t)ch * CV;
+                    const uint32_t nv = (uint32_t)min((uint64_t)CV, n - v0);
+                    fence_proxy_async_smem();
+                    tma_load_1d(shub + b * CV, p.hub + v0, (nv * 4u + 15u) & ~15u, &mbar[b]);
+                }
+            };
             chunk = grab_chunk(nx, nchunks, s_cur);
+            stage_hub(chunk, 0);
             while (chunk != INF) {
                 const uint32_t chunk_n = grab_chunk(nx, nchunks, s_cur);
-                const uint64_t w0 = (uint64_t)chunk << 5;
+                stage_hub(chunk_n, buf ^ 1u);
+                const uint64_t w0 = (uint64_t)chunk * CW;
                 const uint64_t wl = w0 + lane;
-                const uint32_t vis_l = wl < nw ? p.visited[wl] : FULL;
-                const uint32_t cand_l = wl < nw ? (~vis_l & __ldg(p.g.nz_in + wl)) : 0u;
-#if SX_TILE_STREAM
-                if (__any_sync(FULL, cand_l != 0)) {
-                    // phase 1, streamed: word k of the chunk is handled by the whole warp,
-                    // lane l testing vertex 32 (w0 + k) + l — the hub loads of a word are one
-                    // coalesced 128-B request, TILE_ILP words in flight, no shared-memory
-                    // candidate list.  Found bits come out of a ballot (lane k keeps word k's);
-                    // open non-sole candidates are compacted into s_c for the row walks.
-                    uint32_t fm_mine = 0, nopen = 0;
-#pragma unroll 1
-                    for (uint32_t kb = 0; kb < 32; kb += TILE_ILP) {
-                        uint32_t cw[TILE_ILP], x[TILE_ILP], wd[TILE_ILP];
-#pragma unroll
-                        for (int k = 0; k < TILE_ILP; ++k) {
-                            cw[k] = __shfl_sync(FULL, cand_l, kb + k);
-                            const uint32_t v = (uint32_t)((w0 + kb + k) << 5) + lane;
-                            x[k] = (cw[k] >> lane) & 1u ? __ldg(p.hub + v) : INF;
-                        }
-#pragma unroll
-                        for (int k = 0; k < TILE_ILP; ++k) {
-                            const uint32_t h = hub_id(x[k]);
-                            wd[k] = h != INF ? cur[h >> 5] : 0u;
-                        }
-#pragma unroll
-                        for (int k = 0; k < TILE_ILP; ++k) {
-                            const uint32_t v = (uint32_t)((w0 + kb + k) << 5) + lane;
-                            const bool isc = (cw[k] >> lane) & 1u;
-                            const uint32_t h = hub_id(x[k]);
-                            const bool f = h != INF && ((wd[k] >> (h & 31)) & 1u);
-                            edges += h != INF;
-                            if (f) {
-                                p.level[v] = lvl;
-                                if (!p.sym) mdeg += __ldg(p.g.dout + v);
-                            }
-                            const uint32_t fb = __ballot_sync(FULL, f);
-                            if (lane == kb + k) fm_mine = fb;
-                            const bool settled = isc && !f && hub_sole(x[k]);
-                            if (settled) mopen += 1;
-                            record_open(settled, v);
-                            const bool open = isc && !f && !hub_sole(x[k]);
-                            const uint32_t ob = __ballot_sync(FULL, open);
-                            if (open) s_c[nopen + __popc(ob & lanemask_lt())] = v;
-                            nopen += __popc(ob);
-                        }
-                    }
-                    s_f[lane] = fm_mine;
-                    __syncwarp();
-                    walk_open(nopen, w0);
-#else
+                const bool mine = lane < CW && wl < nw;
+                const uint32_t vis_l = mine ? p.visited[wl] : FULL;
+                const uint32_t cand_l = mine ? (~vis_l & __ldg(p.g.nz_in + wl)) : 0u;
                 uint32_t incl = __popc(cand_l);
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
@@ -714,13 +718,19 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
                     if ((int)lane >= o) incl += y;
                 }
                 const uint32_t total = __shfl_sync(FULL, incl, 31);
+                const uint32_t* sh = nullptr;
+                if (tma) {  // the chunk's hub slice has landed (always consume the phase)
+                    mbar_wait(&mbar[buf], (phase >> buf) & 1u);
+                    phase ^= 1u << buf;
+                    sh = shub + buf * CV;
+                    buf ^= 1u;
+                }
                 if (total) {
                     uint32_t pos = incl - __popc(cand_l);
                     for (uint32_t w = cand_l; w; w &= w - 1) s_c[pos++] = (uint32_t)(wl << 5) + (__ffs(w) - 1);
                     s_f[lane] = 0;
                     __syncwarp();
-                    run_cands(total, w0);
-#endif
+                    run_cands(total, w0, sh, (uint32_t)(w0 << 5));
                     __syncwarp();
                     flush_rec();
                     const uint32_t fm = s_f[lane];
@@ -755,6 +765,7 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
         const uint64_t nf = ls.found;
         // symmetric: the line holds sum deg(still unvisited); else sum deg(found)
         const uint64_t mf = p.sym ? m_u - ls.mdeg : ls.mdeg;
+        mf_last = mf;
         const uint32_t nopen_all = ls.alive;
         const uint32_t tc[NCLS] = {ls.cnt[0], ls.cnt[1], 0u, nopen_all};
         m_u -= mf;
@@ -805,7 +816,7 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
             if (!(handoff && i == (int)(it % 3))) c->cl.cnt[i] = 0;
         c->cl.ready = handoff && dir == DIR_CLUSTER;
     }
-    bfs_exit<ALL>(p, DIR_PULL, it, m_u, nf_prev, dir, done, to_list, 0u, cnt, st, &rs);
+    bfs_exit<ALL>(p, DIR_PULL, it, m_u, nf_prev, dir, done, to_list, 0u, cnt, st, &rs, mf_last);
     return true;
 }
 __global__ void __launch_bounds__(BLOCK, SX_PULL_MINB) bfs_pull(BfsP p) {
@@ -1023,6 +1034,7 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) b
         c->st[0].iters += iters;
         c->iter = it;
         c->m_u = m_u;
+        c->hi = 0;  // the push after the cluster records online
         c->done = done;
         c->dir = dir;
         c->nf_prev = nnext;
@@ -1093,6 +1105,7 @@ extern "C" sx_status sx_bfs(sx_graph g, uint32_t src, const sx_opts* opts, uint3
     p.visited = g->aux_bm;
     p.hub = g->hub;
     p.sym = !g->directed;
+    p.tma = g->hub && ((uintptr_t)g->hub & 15u) == 0;
     uint32_t dir0 = run.o.force_dir == 2 ? DIR_PULL : DIR_PUSH;
     hm.mark("prologue");
     if (run.o.fusion == 2) {  // all fusion: every phase in one cooperative launch
@@ -1108,7 +1121,7 @@ extern "C" sx_status sx_bfs(sx_graph g, uint32_t src, const sx_opts* opts, uint3
         int fi = fuse_init;
         AsyncAcc* acc = nullptr;
         void* args2[] = {&p, &src, &dir0, &hctl, &fi, &acc};
-        if ((rc = run.launch((const void*)bfs_all, args2, sxh::KIND_FUSED)) != SX_OK) return rc;
+        if ((rc = run.launch((const void*)bfs_all, args2, sxh::KIND_FUSED, PULL_DYN_SMEM)) != SX_OK) return rc;
         if ((rc = run.sync(false)) != SX_OK) return rc;
         if ((rc = run.end(bfs_bytes)) != SX_OK) return rc;
         hm.mark("end");
@@ -1130,7 +1143,8 @@ extern "C" sx_status sx_bfs(sx_graph g, uint32_t src, const sx_opts* opts, uint3
     };
     auto enqueue = [&](uint32_t d) -> sx_status {
         if (d == DIR_CLUSTER) return run.launch_plain((const void*)bfs_cluster, args, CL_CTAS, CL_BLOCK, false);
-        return run.launch(d == DIR_PULL ? (const void*)bfs_pull : (const void*)bfs_push, args, d == DIR_PULL ? sxh::KIND_PULL : sxh::KIND_PUSH);
+        return d == DIR_PULL ? run.launch((const void*)bfs_pull, args, sxh::KIND_PULL, PULL_DYN_SMEM)
+                             : run.launch((const void*)bfs_push, args, sxh::KIND_PUSH);
     };
     g->ctx->h_ctl->done = 0;
     // the device picks cluster mode at init for a low-degree source; the host
@@ -1230,6 +1244,7 @@ extern "C" sx_status sx_bfs_async(sx_graph g, uint32_t src, const sx_opts* opts,
     p.visited = g->aux_bm;
     p.hub = g->hub;
     p.sym = !g->directed;
+    p.tma = g->hub && ((uintptr_t)g->hub & 15u) == 0;
     uint32_t dir0 = o.force_dir == 2 ? DIR_PULL : DIR_PUSH;
     const int i = c->nasync;
     SX_CU(cudaEventRecord(c->eva[3 * i], s));
@@ -1240,7 +1255,7 @@ extern "C" sx_status sx_bfs_async(sx_graph g, uint32_t src, const sx_opts* opts,
     int fi = 0;
     AsyncAcc* acc = g->async_acc;
     void* args[] = {&p, &src, &dir0, &hctl, &fi, &acc};
-    if ((rc = sxh::coop_launch(g, (const void*)bfs_all, args, nullptr)) != SX_OK) return rc;
+    if ((rc = sxh::coop_launch(g, (const void*)bfs_all, args, nullptr, PULL_DYN_SMEM)) != SX_OK) return rc;
     SX_CU(cudaEventRecord(c->eva[3 * i + 2], s));
     c->async_g[i] = g;
     c->nasync = i + 1;
@@ -1320,7 +1335,7 @@ extern "C" sx_status sx_ctx_info(sx_ctx c, sx_device_info* out) {
     out->push_ctas_per_sm = occ;
     SX_CU(cudaFuncGetAttributes(&a, bfs_push));
     out->push_regs = a.numRegs;
-    SX_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bfs_pull, BLOCK, 0));
+    SX_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bfs_pull, BLOCK, PULL_DYN_SMEM));
     out->pull_ctas_per_sm = occ;
     SX_CU(cudaFuncGetAttributes(&a, bfs_pull));
     out->pull_regs = a.numRegs;

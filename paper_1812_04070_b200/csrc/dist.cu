@@ -45,8 +45,12 @@ struct DistRank {
     uint32_t* gfront = nullptr;       // NW global words (pull: allgathered frontier)
     uint32_t* sendmap = nullptr;      // NW global words (push targets)
     uint32_t* recv = nullptr;         // P * nwl words (alltoall receive)
-    uint32_t* sendbest = nullptr;     // P * V candidate distances (SSSP, lazy)
-    uint32_t* recvbest = nullptr;     // V (SSSP, lazy)
+    uint64_t* pieces = nullptr;       // push: (row, piece) items of the rows split into DIST_PIECE-edge pieces
+    uint32_t* sendbest = nullptr;     // SSSP (lazy): P * V sender-side candidate minima (INF between iterations)
+    uint32_t* touched = nullptr;      // SSSP: P regions of V ids first improved this iteration, by owner
+    uint32_t* tcnt = nullptr;         // SSSP: P per-owner touched counts, then P received counts
+    uint64_t* sendbuf = nullptr;      // SSSP: P regions of V packed (id << 32 | dist) pairs, by owner
+    uint64_t* recvbuf = nullptr;      // SSSP: P regions of V pairs, by sender
     unsigned long long* cnt = nullptr;  // device counters
     bool has_zero_w = false;
 };
@@ -104,15 +108,25 @@ struct RankView {
     uint32_t* sendmap;
     const uint32_t* recv;
     uint32_t* sendbest;
-    const uint32_t* recvbest;
     unsigned long long* cnt;
+    uint64_t* pieces;
+    uint32_t* touched;
+    uint32_t* tcnt;
+    uint64_t* sendbuf;
+    const uint64_t* recvbuf;
     uint32_t P;
     uint64_t V;
     uint32_t sep_small;
 };
 
-// Visit the owned vertices whose bit is set in `bits` (owned words): small rows
-// on the lane (thread granularity), larger rows by the whole warp.
+// Visit the owned vertices whose bit is set in `bits` (owned words) with the
+// engine's granularities: small rows on the lane (thread), medium rows
+// by the warp, and rows of at least DIST_PIECE edges split into pieces of
+// DIST_PIECE edges that the next launch spreads over every warp of the GPU
+// (the grid split of the single-GPU engine's huge class: an R-MAT hub of 10^5-10^6
+// edges no longer sits on one warp).  Pieces are listed with one atomic per row.
+constexpr uint32_t DIST_PIECE = 1024;
+constexpr int CNT_PIECES = 5;  // counter slot holding the piece count of the level
 template <class EdgeFn>
 __device__ __forceinline__ void dist_for_active(const RankView& r, const uint32_t* bits, EdgeFn&& fn) {
     const uint32_t lane = lane_id();
@@ -127,9 +141,15 @@ __device__ __forceinline__ void dist_for_active(const RankView& r, const uint32_
             end = __ldg(r.rp + vl + 1);
         }
         const bool small = mine && end - beg < r.sep_small;
+        const bool split = mine && end - beg >= DIST_PIECE;
         if (small)
             for (uint64_t e = beg; e < end; ++e) fn(vl, e, __ldg(r.ci + e));
-        uint32_t todo = __ballot_sync(FULL, mine && !small);
+        if (split) {
+            const uint64_t np = (end - beg + DIST_PIECE - 1) / DIST_PIECE;
+            const uint64_t b0 = atomicAdd(r.cnt + CNT_PIECES, (unsigned long long)np);
+            for (uint64_t q = 0; q < np; ++q) r.pieces[b0 + q] = (vl << 32) | q;
+        }
+        uint32_t todo = __ballot_sync(FULL, mine && !small && !split);
         while (todo) {
             const int l = __ffs(todo) - 1;
             todo &= todo - 1;
@@ -139,15 +159,29 @@ __device__ __forceinline__ void dist_for_active(const RankView& r, const uint32_
         }
     }
 }
+// the pieces listed by dist_for_active: one warp per piece, lane-strided edges
+template <class EdgeFn> __device__ __forceinline__ void dist_for_pieces(const RankView& r, EdgeFn&& fn) {
+    const uint64_t np = vload(r.cnt + CNT_PIECES);
+    for (uint64_t i = gwarp(); i < np; i += gwarps()) {
+        const uint64_t it = r.pieces[i];
+        const uint64_t vl = it >> 32, q = it & 0xFFFFFFFFull;
+        const uint64_t beg = __ldg(r.rp + vl) + q * DIST_PIECE;
+        const uint64_t end = min(beg + DIST_PIECE, __ldg(r.rp + vl + 1));
+        for (uint64_t e = beg + lane_id(); e < end; e += 32) fn(vl, e, __ldg(r.ci + e));
+    }
+}
 
-__global__ void k_bfs_push(RankView r) {
+// PIECES = 0: the active rows (big ones listed as pieces); 1: the pieces
+template <int PIECES> __global__ void k_bfs_push(RankView r) {
     unsigned long long edges = 0;
-    dist_for_active(r, r.cur, [&](uint64_t, uint64_t, uint32_t u) {
+    auto fn = [&](uint64_t, uint64_t, uint32_t u) {
         ++edges;
         const uint64_t ul = (uint64_t)u - r.lo;
         if (ul < r.nl && bm_test(r.visited, (uint32_t)ul)) return;  // owned and already visited
         bm_set(r.sendmap, u);
-    });
+    };
+    if (PIECES) dist_for_pieces(r, fn);
+    else dist_for_active(r, r.cur, fn);
     uint64_t a[1] = {edges};
     block_sum<1>(a);
     if (threadIdx.x == 0 && a[0]) atomicAdd(r.cnt + 2, (unsigned long long)a[0]);
@@ -248,9 +282,9 @@ __global__ void k_bfs_pull(RankView r, uint32_t lvl) {
 
 // SSSP push over owned active vertices: local targets relaxed in place
 // (atomicMin), remote ones min-combined into the global candidate array.
-__global__ void k_sssp_push(RankView r, unsigned long long hi) {
+template <int PIECES> __global__ void k_sssp_push(RankView r, unsigned long long hi) {
     unsigned long long edges = 0;
-    dist_for_active(r, r.cur, [&](uint64_t vl, uint64_t e, uint32_t u) {
+    auto fn = [&](uint64_t vl, uint64_t e, uint32_t u) {
         ++edges;
         const uint32_t nd = r.state[vl] + edge_w(r.w8, r.w32, e);
         const uint64_t ul = (uint64_t)u - r.lo;
@@ -261,35 +295,53 @@ __global__ void k_sssp_push(RankView r, unsigned long long hi) {
             if ((unsigned long long)nd < hi) bm_set(r.nxt, (uint32_t)ul);
             else bm_set(r.visited, (uint32_t)ul);
         } else {
-            // candidate array laid out by owner: owner q's slot of u at q*V + (u - q*V) = u
-            if (nd < r.sendbest[u]) atomicMin(r.sendbest + u, nd);
+            // sender-side combining (min per target); the first
+            // improvement of u this iteration lists u for its owner
+            if (nd >= r.sendbest[u]) return;
+            if (atomicMin(r.sendbest + u, nd) == INF) {
+                const uint64_t q = u / r.V;
+                const uint32_t pos = atomicAdd(r.tcnt + q, 1u);
+                r.touched[q * r.V + pos] = u;
+            }
         }
-    });
+    };
+    if (PIECES) dist_for_pieces(r, fn);
+    else dist_for_active(r, r.cur, fn);
     uint64_t a[1] = {edges};
     block_sum<1>(a);
     if (threadIdx.x == 0 && a[0]) atomicAdd(r.cnt + 2, (unsigned long long)a[0]);
 }
 
-// owner side of an SSSP iteration: apply the reduce-scattered minima, count the next frontier
-__global__ void k_sssp_apply(RankView r, unsigned long long hi) {
-    unsigned long long active = 0;
-    for (uint64_t wi = gtid(); wi < r.nwl; wi += gthreads()) {
-        uint32_t nx = r.nxt[wi], fa = 0;
-        const uint64_t v0 = wi << 5;
-        for (uint32_t b = 0; b < 32; ++b) {
-            const uint64_t vl = v0 + b;
-            if (vl >= r.nl) break;
-            const uint32_t cnd = r.recvbest[vl];
-            if (cnd < r.state[vl]) {
-                r.state[vl] = cnd;
-                if ((unsigned long long)cnd < hi) nx |= 1u << b;
-                else fa |= 1u << b;
-            }
+// sender side: pack each owner's touched targets as (id << 32 | dist) pairs and
+// reset their candidate slots (a sparse reset: no P*V memset per iteration)
+__global__ void k_sssp_pack(RankView r) {
+    for (uint32_t q = 0; q < r.P; ++q) {
+        const uint32_t nq = r.tcnt[q];
+        for (uint64_t i = gtid(); i < nq; i += gthreads()) {
+            const uint32_t u = r.touched[(uint64_t)q * r.V + i];
+            r.sendbuf[(uint64_t)q * r.V + i] = ((uint64_t)u << 32) | r.sendbest[u];
+            r.sendbest[u] = INF;
         }
-        r.nxt[wi] = nx;
-        if (fa) r.visited[wi] |= fa;
-        active += __popc(nx);
     }
+}
+// owner side: apply the received pairs (rcnt[q] pairs from sender q at region q)
+__global__ void k_sssp_apply_pairs(RankView r, const uint32_t* rcnt, unsigned long long hi) {
+    for (uint32_t q = 0; q < r.P; ++q) {
+        const uint32_t nq = rcnt[q];
+        for (uint64_t i = gtid(); i < nq; i += gthreads()) {
+            const uint64_t pr = r.recvbuf[(uint64_t)q * r.V + i];
+            const uint32_t ul = (uint32_t)((pr >> 32) - r.lo), nd = (uint32_t)pr;
+            if (nd >= r.state[ul]) continue;
+            const uint32_t old = atomicMin(r.state + ul, nd);
+            if (nd >= old) continue;
+            if ((unsigned long long)nd < hi) bm_set(r.nxt, ul);
+            else bm_set(r.visited, ul);
+        }
+    }
+}
+__global__ void k_count_next(RankView r) {
+    unsigned long long active = 0;
+    for (uint64_t wi = gtid(); wi < r.nwl; wi += gthreads()) active += __popc(r.nxt[wi]);
     uint64_t a[1] = {active};
     block_sum<1>(a);
     if (threadIdx.x == 0 && a[0]) atomicAdd(r.cnt + 0, (unsigned long long)a[0]);
@@ -320,15 +372,6 @@ __global__ void k_far_move(RankView r, unsigned long long hi) {
     uint64_t a[1] = {active};
     block_sum<1>(a);
     if (threadIdx.x == 0 && a[0]) atomicAdd(r.cnt + 0, (unsigned long long)a[0]);
-}
-
-__global__ void k_min_slices(uint32_t* out, const uint32_t* in, uint64_t len, uint64_t stride, uint32_t nslices) {
-    // out[i] = min_s in[s*stride + i] (virtual-rank reduce-scatter)
-    for (uint64_t i = gtid(); i < len; i += gthreads()) {
-        uint32_t m = INF;
-        for (uint32_t s = 0; s < nslices; ++s) m = min(m, in[(uint64_t)s * stride + i]);
-        out[i] = m;
-    }
 }
 
 __global__ void k_validate_slice(const uint64_t* rp, const uint32_t* ci, uint64_t n, uint64_t m, uint64_t N,
@@ -378,8 +421,12 @@ RankView view_of(sx_dist d, int i, uint32_t cur, const sx_opts& o) {
     v.sendmap = k.sendmap;
     v.recv = k.recv;
     v.sendbest = k.sendbest;
-    v.recvbest = k.recvbest;
     v.cnt = k.cnt;
+    v.pieces = k.pieces;
+    v.touched = k.touched;
+    v.tcnt = k.tcnt;
+    v.sendbuf = k.sendbuf;
+    v.recvbuf = k.recvbuf;
     v.P = (uint32_t)d->P;
     v.V = d->V;
     v.sep_small = o.sep_small;
@@ -443,37 +490,56 @@ sx_status ex_alltoall(sx_dist d) {
     return SX_OK;
 }
 
-// reduce-scatter(min) of the candidate-distance arrays to the owners
-sx_status ex_reduce_scatter_min(sx_dist d) {
-    cudaStream_t s = d->ctx->stream;
-    if (d->nccl) {
-        SX_NC(ncclReduceScatter(d->r[0].sendbest, d->r[0].recvbest, d->V, ncclUint32, ncclMin, d->comm, s));
-    } else {
-        // slices are contiguous in each rank's sendbest: stage the P slices destined
-        // to owner i after rank i's own array, then take the element-wise min
-        for (int i = 0; i < d->nlocal; ++i) {
-            // stage the P slices destined to owner i contiguously in the scratch area after sendbest
-            uint32_t* stage = d->r[i].sendbest + (uint64_t)d->P * d->V;
-            for (int q = 0; q < d->nlocal; ++q)
-                SX_CU(cudaMemcpyAsync(stage + (uint64_t)q * d->V, d->r[q].sendbest + (uint64_t)i * d->V, d->V * 4,
-                                      cudaMemcpyDeviceToDevice, s));
-            k_min_slices<<<kgrid(d), BLOCK, 0, s>>>(d->r[i].recvbest, stage, d->V, d->V, (uint32_t)d->nlocal);
-            SX_CU(cudaGetLastError());
-        }
+sx_status ensure_sssp_buffers(sx_dist d) {
+    const uint64_t PV = (uint64_t)d->P * d->V;
+    for (int i = 0; i < d->nlocal; ++i) {
+        DistRank& k = d->r[i];
+        if (k.sendbest) continue;
+        sx_status rc;
+        if ((rc = dmalloc(&k.sendbest, PV)) != SX_OK) return rc;
+        if ((rc = dmalloc(&k.touched, PV)) != SX_OK) return rc;
+        if ((rc = dmalloc(&k.tcnt, 2 * (uint64_t)d->P)) != SX_OK) return rc;
+        if ((rc = dmalloc(&k.sendbuf, PV)) != SX_OK) return rc;
+        if ((rc = dmalloc(&k.recvbuf, PV)) != SX_OK) return rc;
+        SX_CU(cudaMemsetAsync(k.sendbest, 0xFF, PV * 4, d->ctx->stream));
     }
     return SX_OK;
 }
 
-sx_status ensure_sssp_buffers(sx_dist d) {
-    for (int i = 0; i < d->nlocal; ++i) {
-        DistRank& k = d->r[i];
-        if (!k.sendbest) {
-            // P*V candidates (+ P*V staging for the virtual reduce-scatter)
-            const uint64_t extra = d->nccl ? 0 : (uint64_t)d->P * d->V;
-            sx_status rc = dmalloc(&k.sendbest, (uint64_t)d->P * d->V + extra);
-            if (rc != SX_OK) return rc;
-            rc = dmalloc(&k.recvbest, d->V);
-            if (rc != SX_OK) return rc;
+// the sparse SSSP exchange (alltoallv of (target, distance) pairs):
+// per-owner counts by all-to-all, to the host (the pair transfers need them),
+// then one grouped send/recv of the packed pairs.  hcounts receives, per local
+// rank i, P send counts then P receive counts.
+sx_status ex_sssp_pairs(sx_dist d, uint32_t* hcounts, double* pairs_out) {
+    cudaStream_t s = d->ctx->stream;
+    const int P = d->P;
+    if (d->nccl) {
+        DistRank& k = d->r[0];
+        SX_NC(ncclAlltoAll(k.tcnt, k.tcnt + P, 1, ncclUint32, d->comm, s));
+        SX_CU(cudaMemcpyAsync(hcounts, k.tcnt, 2 * P * 4, cudaMemcpyDeviceToHost, s));
+        SX_CU(cudaStreamSynchronize(s));
+        SX_NC(ncclGroupStart());
+        for (int q = 0; q < P; ++q) {
+            const uint32_t ns = hcounts[q], nr = hcounts[P + q];
+            if (ns) SX_NC(ncclSend(k.sendbuf + (uint64_t)q * d->V, ns, ncclUint64, q, d->comm, s));
+            if (nr) SX_NC(ncclRecv(k.recvbuf + (uint64_t)q * d->V, nr, ncclUint64, q, d->comm, s));
+            *pairs_out += ns;
+        }
+        SX_NC(ncclGroupEnd());
+    } else {
+        for (int i = 0; i < d->nlocal; ++i)
+            SX_CU(cudaMemcpyAsync(hcounts + 2 * P * i, d->r[i].tcnt, P * 4, cudaMemcpyDeviceToHost, s));
+        SX_CU(cudaStreamSynchronize(s));
+        for (int i = 0; i < d->nlocal; ++i) {  // owner i receives from every sender q
+            for (int q = 0; q < d->nlocal; ++q) {
+                const uint32_t n = hcounts[2 * P * q + i];
+                hcounts[2 * P * i + P + q] = n;
+                *pairs_out += n;
+                if (n)
+                    SX_CU(cudaMemcpyAsync(d->r[i].recvbuf + (uint64_t)q * d->V, d->r[q].sendbuf + (uint64_t)i * d->V,
+                                          (uint64_t)n * 8, cudaMemcpyDeviceToDevice, s));
+            }
+            SX_CU(cudaMemcpyAsync(d->r[i].tcnt + P, hcounts + 2 * P * i + P, P * 4, cudaMemcpyHostToDevice, s));
         }
     }
     return SX_OK;
@@ -530,7 +596,10 @@ sx_status sx_dist_create(sx_ctx ctx, uint64_t n_global, int nranks, int rank0, i
     if (d->V == 0) d->V = 32;
     d->nwl = d->V / 32;
     d->NW = d->nwl * nranks;
-    d->nccl = nlocal < nranks;
+    // NCCL whenever the caller supplies a communicator id with one local rank
+    // (nranks = 1 included: a one-rank communicator runs every collective of the
+    // data path; that is how the NCCL branch is exercised on one GPU)
+    d->nccl = nlocal == 1 && nccl_id != nullptr;
     if (d->nccl) {
         ncclUniqueId id;
         std::memcpy(&id, nccl_id, sizeof(id));
@@ -578,7 +647,7 @@ sx_status sx_dist_upload(sx_dist d, int local_rank, const sx_csr_desc* desc) {
     if (k.rp) {  // re-upload (a new graph on the same partition): release the previous slice and workspace
         cudaStreamSynchronize(s);
         void* ps[] = {k.rp, k.ci, k.w, k.deg, k.nz, k.state, k.visited, k.front[0], k.front[1], k.gfront, k.sendmap,
-                      k.recv, k.sendbest, k.recvbest, k.cnt};
+                      k.recv, k.sendbest, k.cnt, k.pieces, k.touched, k.tcnt, k.sendbuf, k.recvbuf};
         for (void* q : ps)
             if (q) cudaFree(q);
         const uint64_t nl = k.nl, lo = k.lo;
@@ -615,6 +684,7 @@ sx_status sx_dist_upload(sx_dist d, int local_rank, const sx_csr_desc* desc) {
     if ((rc = dmalloc(&k.gfront, d->NW)) != SX_OK) return rc;
     if ((rc = dmalloc(&k.sendmap, d->NW)) != SX_OK) return rc;
     if ((rc = dmalloc(&k.recv, d->NW)) != SX_OK) return rc;
+    if ((rc = dmalloc(&k.pieces, 2 * (k.ml / DIST_PIECE) + 2)) != SX_OK) return rc;
     if ((rc = dmalloc(&k.cnt, 8)) != SX_OK) return rc;
     SX_CU(cudaMemsetAsync(k.cnt, 0, 64, s));
     SX_CU(cudaMemsetAsync(k.cnt + 3, 0xFF, 8, s));
@@ -629,7 +699,7 @@ void sx_dist_free(sx_dist d) {
     for (int i = 0; i < d->nlocal; ++i) {
         DistRank& k = d->r[i];
         void* ps[] = {k.rp, k.ci, k.w, k.deg, k.nz, k.state, k.visited, k.front[0], k.front[1], k.gfront, k.sendmap,
-                      k.recv, k.sendbest, k.recvbest, k.cnt};
+                      k.recv, k.sendbest, k.cnt, k.pieces, k.touched, k.tcnt, k.sendbuf, k.recvbuf};
         for (void* p : ps)
             if (p) cudaFree(p);
     }
@@ -699,8 +769,9 @@ sx_status sx_dist_bfs(sx_dist d, uint32_t src, const sx_opts* opts, uint32_t* co
         const uint32_t lvl = it + 1;
         if (dir == DIR_PUSH) {
             for (int i = 0; i < d->nlocal; ++i) {
-                k_bfs_push<<<G, BLOCK, 0, s>>>(view_of(d, i, cur, o));
-                ++launches;
+                k_bfs_push<0><<<G, BLOCK, 0, s>>>(view_of(d, i, cur, o));
+                k_bfs_push<1><<<G, BLOCK, 0, s>>>(view_of(d, i, cur, o));
+                launches += 2;
             }
             if ((rc = ex_alltoall(d)) != SX_OK) return rc;
             for (int i = 0; i < d->nlocal; ++i) {
@@ -774,7 +845,7 @@ sx_status sx_dist_sssp(sx_dist d, uint32_t src, uint32_t delta, const sx_opts* o
         SX_CU(cudaMemsetAsync(k.visited, 0, d->nwl * 4, s));  // far pile
         SX_CU(cudaMemsetAsync(k.front[0], 0, d->nwl * 4, s));
         SX_CU(cudaMemsetAsync(k.front[1], 0, d->nwl * 4, s));
-        SX_CU(cudaMemsetAsync(k.sendbest, 0xFF, (uint64_t)d->P * d->V * 4, s));
+        SX_CU(cudaMemsetAsync(k.tcnt, 0, 2 * (uint64_t)d->P * 4, s));
         SX_CU(cudaMemsetAsync(k.cnt, 0, 64, s));
         SX_CU(cudaMemsetAsync(k.cnt + 3, 0xFF, 8, s));
         if (src >= k.lo && src < k.lo + k.nl) {
@@ -788,16 +859,25 @@ sx_status sx_dist_sssp(sx_dist d, uint32_t src, uint32_t delta, const sx_opts* o
     unsigned long long hi = delta ? (unsigned long long)delta : 0x100000000ull;
     uint32_t cur = 0, it = 0, launches = 0, advances = 0;
     unsigned long long edges_total = 0;
+    std::vector<uint32_t> hcounts(2 * (size_t)d->P * d->nlocal);
+    double pairs = 0;
     for (;;) {
         for (int i = 0; i < d->nlocal; ++i) {
-            k_sssp_push<<<G, BLOCK, 0, s>>>(view_of(d, i, cur, o), hi);
+            k_sssp_push<0><<<G, BLOCK, 0, s>>>(view_of(d, i, cur, o), hi);
+            k_sssp_push<1><<<G, BLOCK, 0, s>>>(view_of(d, i, cur, o), hi);
+            launches += 2;
+        }
+        for (int i = 0; i < d->nlocal; ++i) {
+            k_sssp_pack<<<G, BLOCK, 0, s>>>(view_of(d, i, cur, o));
             ++launches;
         }
-        if ((rc = ex_reduce_scatter_min(d)) != SX_OK) return rc;
+        if ((rc = ex_sssp_pairs(d, hcounts.data(), &pairs)) != SX_OK) return rc;
         for (int i = 0; i < d->nlocal; ++i) {
-            SX_CU(cudaMemsetAsync(d->r[i].sendbest, 0xFF, (uint64_t)d->P * d->V * 4, s));
-            k_sssp_apply<<<G, BLOCK, 0, s>>>(view_of(d, i, cur, o), hi);
-            ++launches;
+            const RankView v = view_of(d, i, cur, o);
+            k_sssp_apply_pairs<<<G, BLOCK, 0, s>>>(v, d->r[i].tcnt + d->P, hi);
+            k_count_next<<<G, BLOCK, 0, s>>>(v);
+            SX_CU(cudaMemsetAsync(d->r[i].tcnt, 0, d->P * 4, s));
+            launches += 2;
         }
         SX_CU(cudaGetLastError());
         unsigned long long cnt[8];
@@ -836,7 +916,7 @@ sx_status sx_dist_sssp(sx_dist d, uint32_t src, uint32_t delta, const sx_opts* o
         stats->ballot_iters = advances;
         stats->edges_examined = edges_total;
         stats->ms = ms;
-        stats->bytes_model = (double)it * (double)d->P * d->V * 4.0;
+        stats->bytes_model = pairs * 8.0;  // (target, distance) pairs sent over the exchange
     }
     return copy_owned(d, dist_out);
 }

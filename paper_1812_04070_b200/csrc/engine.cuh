@@ -64,6 +64,7 @@ struct alignas(128) Slot {
     unsigned long long mdeg;         // sum of degrees of activated vertices (m_f)
     unsigned long long edges;        // edges examined (trace)
     double dsum;                     // PageRank dangling mass
+    double dsum2;                    // convergence tests: L1 change of the iteration
 };
 struct IterLine {
     Slot s[NSLOT];
@@ -106,6 +107,11 @@ struct Ctl {
         unsigned long long edges, entries, scanned, reached;
         unsigned int ballot, pull, iters;
     } st[2];
+    // --- asynchronous work queue (k-core cascades): low 32 bits = queue tail
+    // (positions handed to producers), high 32 bits = pending items (enqueued,
+    // not yet fully processed); head = next ticket for the consumers
+    alignas(128) unsigned long long aq_tp;
+    alignas(128) unsigned long long aq_head;
 };
 
 // Statistics of the runs enqueued without a host sync (sx_bfs_async): the
@@ -209,6 +215,32 @@ __device__ __forceinline__ uint32_t cls_of(uint32_t deg, const Sched& s) {
 
 __device__ __forceinline__ uint32_t edge_w(const uint8_t* w8, const uint32_t* w32, uint64_t e) {
     return w8 ? (uint32_t)__ldg(w8 + e) : w32 ? __ldg(w32 + e) : 1u;
+}
+
+// ---------------------------------------------------------------- TMA bulk copies (sm_100a)
+// 1D bulk copy global -> shared (cp.async.bulk, the TMA unit) completing on an
+// mbarrier with a transaction count: one thread issues it, the data land
+// without registers or load instructions, and the consumer waits on the
+// barrier's phase.  Used to stage contiguous slices (BFS pull: the hub-probe
+// table of the next chunk) while the current one is processed.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// arm the barrier for `bytes` and issue the copy (bytes: multiple of 16, 16-B aligned addresses)
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok = 0;
+    do {
+        asm volatile("{\n\t.reg .pred q;\n\tmbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n\tselp.u32 %0, 1, 0, q;\n\t}"
+                     : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    } while (!ok);
 }
 
 // ---------------------------------------------------------------- grid barrier
@@ -344,6 +376,7 @@ __device__ __forceinline__ void reset_line_warp(IterLine* L) {
     s.mdeg = 0;
     s.edges = 0;
     s.dsum = 0.0;
+    s.dsum2 = 0.0;
 }
 __device__ __forceinline__ void maybe_reset_line(IterLine* L) {
     if (blockIdx.x == 0 && warp_id() == 0) reset_line_warp(L);
@@ -363,7 +396,7 @@ struct SlotSnap {
     uint32_t cnt[NCLS];
     uint32_t found, minv, alive;
     uint64_t mdeg, edges;
-    double dsum;
+    double dsum, dsum2;
 };
 __device__ __forceinline__ SlotSnap load_slot(const Slot& sl) {
     static_assert(offsetof(Slot, found) == 16 && offsetof(Slot, mdeg) == 32 && offsetof(Slot, dsum) == 48, "Slot layout");
@@ -380,6 +413,7 @@ __device__ __forceinline__ SlotSnap load_slot(const Slot& sl) {
     r.mdeg = ((uint64_t)m.y << 32) | m.x;
     r.edges = ((uint64_t)m.w << 32) | m.z;
     r.dsum = __hiloint2double((int)d.y, (int)d.x);
+    r.dsum2 = __hiloint2double((int)d.w, (int)d.z);
     return r;
 }
 __device__ __forceinline__ SlotSnap load_slot_cnt(const Slot& sl) {
@@ -397,7 +431,7 @@ struct LineSum {
     uint32_t cntmax[NCLS];
     uint32_t found, minv, alive;
     uint64_t mdeg, edges;
-    double dsum;
+    double dsum, dsum2;
 };
 __device__ __forceinline__ void read_line(const IterLine* L, LineSum& out) {
     __shared__ LineSum sh;
@@ -416,6 +450,7 @@ __device__ __forceinline__ void read_line(const IterLine* L, LineSum& out) {
         r.mdeg = warp_sum(x.mdeg);
         r.edges = warp_sum(x.edges);
         r.dsum = warp_sum(x.dsum);
+        r.dsum2 = warp_sum(x.dsum2);
         if (lane_id() == 0) sh = r;
     }
     __syncthreads();
@@ -520,6 +555,7 @@ __device__ __forceinline__ void read_line_view(const IterLine* L, const Sched& s
         r.mdeg = warp_sum(mdeg);
         r.edges = warp_sum(edges);
         r.dsum = warp_sum(dsum);
+        r.dsum2 = warp_sum(sn.dsum2);
         if (l == 0) sh = r;
     }
     __syncthreads();

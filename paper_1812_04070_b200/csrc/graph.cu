@@ -268,6 +268,7 @@ void sx_graph_free(sx_graph g) {
     for (auto* p : g->st) F(p);
     F(g->hacc);
     F(g->dstate);
+    F(g->prc);
     F(g->hub);
     F(g->async_acc);
     F(g->pp_hcol);

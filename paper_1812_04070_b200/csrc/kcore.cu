@@ -26,7 +26,86 @@ struct KcoreP {
     uint32_t* core;  // coreness, INF while alive
     uint32_t* ab;    // alive bitmap (bit v set while core[v] = INF): n/8 bytes, L2-resident
     uint32_t kfix;   // 0 = decomposition
+    uint32_t* q;     // asynchronous cascade queue: n entries, INF = not yet written (positions never reused)
+    uint32_t amax;   // a level's cascade goes asynchronous once a sub-round frontier has <= amax vertices (0: never)
 };
+
+// Asynchronous tail of a level's cascade (B200 addition; results unchanged by
+// reading 7: a vertex is removed exactly once, by the decrement that takes its
+// residual from k+1 to k, whatever the order).  Once a sub-round's frontier is
+// small, the grid barrier per sub-round (3.2 us, with a dependent chain of a
+// few microseconds behind it) dominates: the rest of the level runs as a
+// work queue instead.  A removal is an item; a warp takes 32 tickets (queue
+// positions) at a time, polls them, and processes whichever have been
+// published — small rows on their lane, larger rows by the whole warp
+// — enqueueing the neighbours whose residual it takes to k.  One 64-bit
+// word counts positions (low half) and pending items (high half): an item is
+// pending from its enqueue until its own enqueues are done, so pending = 0
+// means the cascade is over.  Only AQ_WARPS warps per CTA take part.
+constexpr uint32_t AQ_WARPS = 2;
+constexpr unsigned long long AQ_ONE = 1ull << 32;
+__device__ __forceinline__ uint32_t aq_pending(const Ctl* c) { return (uint32_t)(vload(&c->aq_tp) >> 32); }
+// watchdog of the queue waits (as the grid barrier's): a lost item would leave
+// pending > 0 forever; after 20 s the waiters give up and flag SX_E_BARRIER
+__device__ __forceinline__ bool aq_stuck(Ctl* c, uint32_t& spins, uint64_t& t0) {
+    if (((++spins) & 1023u) != 0) return false;
+    const uint64_t t = globaltimer();
+    if (t0 == 0) t0 = t;
+    else if (t - t0 > 20000000000ull) atomicExch(&c->error, ERR_BARRIER);
+    return vload(&c->error) != 0;
+}
+
+template <class Rm>
+__device__ __forceinline__ void kcore_async(const KcoreP& p, Ctl* c, Rm&& remove_edges, uint64_t& edges,
+                                            uint64_t& entries) {
+    if (warp_id() >= AQ_WARPS) return;
+    const uint32_t lane = lane_id();
+    const uint64_t n = p.g.n;
+    uint32_t spins = 0;
+    uint64_t tw = 0;
+    for (;;) {
+        unsigned long long t0 = 0;
+        if (lane == 0) t0 = atomicAdd(&c->aq_head, 32ull);
+        t0 = __shfl_sync(FULL, t0, 0);
+        if (t0 >= n) {  // no position left to wait for: wait for the cascade to end
+            while (aq_pending(c) != 0 && !aq_stuck(c, spins, tw)) __nanosleep(64);
+            return;
+        }
+        const unsigned long long t = t0 + lane;
+        bool pend = t < n;  // my ticket still has to be processed (tickets past n never fill)
+        for (;;) {
+            uint32_t v = INF;
+            if (pend) v = vload(p.q + t);
+            const bool got = v != INF;
+            const uint32_t gm = __ballot_sync(FULL, got);
+            if (gm) {
+                uint64_t beg = 0, end = 0;
+                if (got) {
+                    beg = __ldg(p.g.rp + v);
+                    end = __ldg(p.g.rp + v + 1);
+                }
+                const bool small = got && end - beg < p.s.sep_small;
+                if (small) remove_edges(beg, end, 0ull, 1ull);
+                for (uint32_t big = __ballot_sync(FULL, got && !small); big; big &= big - 1) {
+                    const int l = __ffs(big) - 1;
+                    remove_edges(__shfl_sync(FULL, beg, l), __shfl_sync(FULL, end, l), (uint64_t)lane, 32ull);
+                }
+                __syncwarp();
+                if (got) {
+                    ++entries;
+                    __threadfence();
+                    atomicAdd(&c->aq_tp, (unsigned long long)(-(long long)AQ_ONE));  // done with v
+                    pend = false;
+                }
+            }
+            if (!__any_sync(FULL, pend)) break;  // every ticket of the batch processed: next batch
+            if (aq_pending(c) == 0) return;      // the cascade is over (unfilled tickets stay unfilled)
+            if (aq_stuck(c, spins, tw)) return;
+            __nanosleep(32);
+        }
+    }
+    (void)edges;
+}
 
 __device__ __forceinline__ bool is_alive(const uint32_t* ab, uint32_t v) { return (ab[v >> 5] >> (v & 31)) & 1u; }
 
@@ -96,6 +175,7 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
     Stats st;
     uint32_t done = 0;
     bool level_started = it > 0 || sum4(cnt) > 0;
+    uint32_t qt = (uint32_t)vload(&c->aq_tp);  // queue tail (the same in every CTA between cascades)
     for (;;) {
         IterLine* nx = &c->line[(it + 1) % 3];
         if (sum4(cnt) == 0) {
@@ -259,6 +339,55 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
             done = 1;
             break;
         }
+        const uint32_t nf32 = sum4(cnt);
+        if (p.amax && p.s.fusion && nf32 > 0 && nf32 <= p.amax) {
+            // ---- the rest of the level's cascade asynchronously: the frontier seeds the queue
+            uint32_t off = qt;
+            for (int cc = 0; cc < NCLS; ++cc) {
+                for (uint64_t i = gtid(); i < cnt[cc]; i += gthreads())
+                    *(volatile uint32_t*)(p.q + off + i) = task_at(p.s.lists[it & 1], p.s, cc, (uint32_t)i);
+                off += cnt[cc];
+            }
+            if (lead()) {
+                c->aq_tp = ((unsigned long long)nf32 << 32) | (unsigned long long)(qt + nf32);
+                c->aq_head = (unsigned long long)qt;
+            }
+            if (!grid_sync(c)) return;
+            uint64_t edges = 0, entries = 0;
+            const uint32_t kk = k;
+            auto remove_edges = [&](uint64_t beg, uint64_t end, uint64_t rank, uint64_t size) {
+                for_edges_b(p.g.ci, beg, end, rank, size, [&](const uint32_t (&u)[4], uint32_t kn) {
+                    edges += kn;
+                    uint32_t aw[4], old[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) aw[j] = j < (int)kn ? p.ab[u[j] >> 5] : 0u;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        old[j] = (j < (int)kn && ((aw[j] >> (u[j] & 31)) & 1u)) ? atomicSub(p.res + u[j], 1u) : 0u;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if (j < (int)kn && old[j] == kk + 1) {
+                            p.core[u[j]] = kk;
+                            atomicAnd(p.ab + (u[j] >> 5), ~(1u << (u[j] & 31)));
+                            const unsigned long long tp = atomicAdd(&c->aq_tp, AQ_ONE + 1ull);
+                            *(volatile uint32_t*)(p.q + (uint32_t)tp) = u[j];
+                        }
+                    }
+                });
+            };
+            kcore_async(p, c, remove_edges, edges, entries);
+            st.edges += edges;
+            st.entries += entries;
+            ++st.iters;
+            if (!grid_sync(c)) return;
+            qt = (uint32_t)vload(&c->aq_tp);
+            for (int i = 0; i < NCLS; ++i) cnt[i] = 0;
+            view_contig(cnt);
+            slotted = 0;
+            ++it;
+            trace_put(p.s, it, DIR_PUSH, 3u, cnt, 0, 0, k);  // filter 3: an asynchronous cascade ended
+            continue;
+        }
         if (!p.s.fusion) break;
     }
     flush_stats(c, st, DIR_PUSH);
@@ -309,6 +438,10 @@ extern "C" sx_status sx_kcore(sx_graph g, uint32_t k, const sx_opts* opts, uint3
     p.core = g->st[1];
     p.ab = g->aux_bm;
     p.kfix = k;
+    // the asynchronous cascade queue: n positions, written once each (INF = empty)
+    p.amax = run.o.cluster_enter;
+    p.q = g->st[3];
+    if (p.amax) SX_CU(cudaMemsetAsync(p.q, 0xFF, g->n * 4, s));
     SX_CU(cudaMemsetAsync(p.core, 0xFF, g->n * 4, s));
     for (int i = 0; i < 3; ++i) SX_CU(cudaMemsetAsync(p.s.bm[i], 0, g->nwords * 4, s));
     const int eg = 4 * g->ctx->prop.multiProcessorCount;

@@ -20,12 +20,21 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 
 #include "internal.h"
 
 namespace sx {
 
 // ---------------------------------------------------------------- operators
+// Per-thread sums an operator's apply() contributes to: dangling mass of the
+// next iteration (PageRank), and for the convergence runs the L1 change of the
+// iteration and the number of vertices that changed by more than tau.
+struct PAcc {
+    double dang = 0.0, l1 = 0.0;
+    uint32_t unstable = 0;
+};
+
 // Each operator splits the edge term into the source value val(v) (what the hub
 // cache holds) and term(e, val) (combined with the edge weight).
 struct PrOp {  // r(u) = (1-d)/N + d (sum_v r(v)/outdeg(v) + D/N)
@@ -49,21 +58,64 @@ struct PrOp {  // r(u) = (1-d)/N + d (sum_v r(v)/outdeg(v) + D/N)
         const uint32_t du = dout[u];
         return du ? 1.0f / (float)du : 0.0f;
     }
-    __device__ __forceinline__ void init(uint64_t v, double& dpart) const {
+    __device__ __forceinline__ void init(uint64_t v, PAcc& pa) const {
         const uint32_t dv = dout[v];
         contrib[0][v] = dv ? (float)(invN / (double)dv) : 0.f;
-        if (dv == 0) dpart += invN;
+        if (dv == 0) pa.dang += invN;
     }
     bool directed;
     __device__ __forceinline__ bool empty_each_iter() const { return directed; }
     // symmetric graph: an empty row is dangling (out-degree 0); its rank is the
     // same for every such row, so their dangling mass is count x rank
     __device__ __forceinline__ double empty_dangling(uint32_t ne) const { return (double)ne * ((1.0 - d) * invN + d * D * invN); }
-    __device__ __forceinline__ void apply(uint32_t u, double s, AuxT inv, double& dpart) const {
+    __device__ __forceinline__ void apply(uint32_t u, double s, AuxT inv, PAcc& pa) const {
         const double r = (1.0 - d) * invN + d * (s + D * invN);
         if (last) out[u] = (float)r;
         contrib[cur ^ 1][u] = (float)(r * (double)inv);
-        if (inv == 0.0f) dpart += r;
+        if (inv == 0.0f) pa.dang += r;
+    }
+};
+
+// PageRank to convergence (readings 25-26), the pull part, in fp64:
+//   variant 0: r(u) = (1-d)/N + d (sum_v r(v)/outdeg(v) + D/N)   (reading 14), r_0 = 1/N
+//   variant 1: r(u) = (1-d)   + d  sum_v r(v)/outdeg(v), r_0 = 1
+// Every apply also stores rho(u) = r_new(u) - r_old(u) (the change not yet
+// propagated: what the push tail starts from) and adds |rho(u)| to the
+// iteration's L1 change; |rho(u)| > tau counts u as unstable.
+struct PrcOp {
+    using HubT = double;
+    using TermT = double;
+    using AuxT = uint32_t;  // out-degree of the destination (0 = dangling)
+    static constexpr bool kStaticHub = false;
+    double* contrib[2];
+    double* r;
+    double* rho;
+    const uint32_t* dout;
+    double d, base, dn, r0, tau;  // base = (1-d)/N or 1-d; dn = 1/N (variant 0) or 0 (dangling mass dropped)
+    uint32_t cur;
+    double D;
+    bool last;
+    __device__ __forceinline__ HubT val(uint32_t v) const { return contrib[cur][v]; }
+    __device__ __forceinline__ const HubT* src() const { return contrib[cur]; }
+    __device__ __forceinline__ TermT term(const DevGraph&, uint64_t, HubT x) const { return x; }
+    __device__ __forceinline__ AuxT aux(uint32_t u) const { return dout[u]; }
+    __device__ __forceinline__ void init(uint64_t v, PAcc& pa) const {
+        const uint32_t dv = dout[v];
+        r[v] = r0;
+        contrib[0][v] = dv ? r0 / (double)dv : 0.0;
+        if (dv == 0 && dn != 0.0) pa.dang += r0;
+    }
+    __device__ __forceinline__ bool empty_each_iter() const { return true; }
+    __device__ __forceinline__ double empty_dangling(uint32_t) const { return 0.0; }
+    __device__ __forceinline__ void apply(uint32_t u, double s, AuxT du, PAcc& pa) const {
+        const double rn = base + d * (s + D * dn);
+        const double ch = rn - r[u];
+        r[u] = rn;
+        rho[u] = ch;
+        contrib[cur ^ 1][u] = du ? rn / (double)du : 0.0;
+        if (du == 0 && dn != 0.0) pa.dang += rn;
+        pa.l1 += fabs(ch);
+        pa.unstable += fabs(ch) > tau;
     }
 };
 
@@ -85,8 +137,8 @@ struct SpmvOp {  // y(u) = sum_v w(v,u) x(v)
     __device__ __forceinline__ AuxT aux(uint32_t) const { return 0; }
     __device__ __forceinline__ bool empty_each_iter() const { return false; }  // y = 0
     __device__ __forceinline__ double empty_dangling(uint32_t) const { return 0.0; }
-    __device__ __forceinline__ void init(uint64_t, double&) const {}
-    __device__ __forceinline__ void apply(uint32_t u, double s, AuxT, double&) const { out[u] = (float)s; }
+    __device__ __forceinline__ void init(uint64_t, PAcc&) const {}
+    __device__ __forceinline__ void apply(uint32_t u, double s, AuxT, PAcc&) const { out[u] = (float)s; }
 };
 
 // BP is computed in fp64 end to end (beliefs, couplings, messages), fp32 out.
@@ -118,18 +170,25 @@ struct BpOp {  // l(u) = logit(p_u) + sum_v log((c b + (1-c)(1-b)) / (c(1-b) + (
         const double den = c * (1.0 - bv) + (1.0 - c) * bv;
         return log(num / den);
     }
-    __device__ __forceinline__ void init(uint64_t v, double&) const {
+    bool conv;  // convergence run: the L1 change of the beliefs is summed
+    __device__ __forceinline__ void init(uint64_t v, PAcc&) const {
         const double p = (double)prior[v];
         const double l = log(p / (1.0 - p));
         b[0][v] = 1.0 / (1.0 + exp(-l));
     }
-    __device__ __forceinline__ void apply(uint32_t u, double s, AuxT pu, double&) const {
+    __device__ __forceinline__ void apply(uint32_t u, double s, AuxT pu, PAcc& pa) const {
         const double p = (double)pu;
         const double l = log(p / (1.0 - p)) + s;
         if (last) out[u] = (float)l;
-        b[cur ^ 1][u] = 1.0 / (1.0 + exp(-l));
+        const double bn = 1.0 / (1.0 + exp(-l));
+        if (conv) pa.l1 += fabs(bn - b[cur][u]);
+        b[cur ^ 1][u] = bn;
     }
 };
+
+// convergence runs: the per-vertex change above which a vertex counts as unstable
+template <class Op> __device__ __forceinline__ void op_set_tau(Op&, double) {}
+__device__ __forceinline__ void op_set_tau(PrcOp& op, double tau) { op.tau = tau; }
 
 // ---------------------------------------------------------------- schedule
 // The all-active pull as an edge-balanced stream (B200 design; DESIGN.md
@@ -189,6 +248,8 @@ template <class Op> struct PullP {
     uint32_t* sp;           // rows applied in phase B, ascending
     void* nzaux;            // per active row k: op.aux(nz[k]) (n + 2 entries of 4 B), filled per run
     double* acc;            // n fp64 partial sums of split rows (zero between runs)
+    double eps;             // > 0: convergence run, stop when the iteration's L1 change < eps (iters = the cap)
+    uint32_t tail;          // convergence run: 1 hand over to the push tail when most vertices are stable, 2 after iteration 1
 };
 
 struct NzPred {
@@ -280,9 +341,9 @@ template <class Op> __global__ void __launch_bounds__(BLOCK, SX_PALL_MINB) pull_
     st.ballot += 2;
     st.scanned += 2 * n;
     {
-        double dpart = 0.0;
-        for (uint64_t v = gtid(); v < n; v += gthreads()) p.op.init(v, dpart);
-        double a[1] = {dpart};
+        PAcc pa0;
+        for (uint64_t v = gtid(); v < n; v += gthreads()) p.op.init(v, pa0);
+        double a[1] = {pa0.dang};
         block_sum<1>(a);
         if (threadIdx.x == 0 && a[0] != 0.0) atomicAdd(&c->line[0].s[my_slot()].dsum, a[0]);
     }
@@ -303,6 +364,8 @@ template <class Op> __global__ void __launch_bounds__(BLOCK, SX_PALL_MINB) pull_
     Op op = p.op;
     const uint32_t lane = lane_id();
     const uint64_t pol_first = l2_policy_first(), pol_last = l2_policy_last();
+    uint32_t conv_state = 0;  // convergence runs: 1 converged, 2 continue in the push tail
+    double last_l1 = 0.0;
     for (uint32_t t = 0; t < p.iters; ++t) {
         maybe_reset_line(&c->line[(t + 2) % 3]);
         {
@@ -311,7 +374,8 @@ template <class Op> __global__ void __launch_bounds__(BLOCK, SX_PALL_MINB) pull_
             op.D = ls.dsum;
         }
         op.cur = t & 1;
-        op.last = t + 1 == p.iters;
+        op.last = p.eps > 0.0 || t + 1 == p.iters;  // a convergence run writes its output every iteration
+        if (p.eps > 0.0) op_set_tau(op, t == 0 ? 1e300 : last_l1 / (double)n);  // stable: change <= the mean change
         if (!Op::kStaticHub || t == 0) {
             // hub cache refresh: 8 independent id -> value chains in flight per thread
             for (uint32_t i0 = threadIdx.x; i0 < p.K; i0 += 8 * BLOCK) {
@@ -330,7 +394,7 @@ template <class Op> __global__ void __launch_bounds__(BLOCK, SX_PALL_MINB) pull_
 #ifdef SX_PULL_PHASES
         trace_put(p.s, t + 1, DIR_PULL, 7u, cnt, 0, 0, 0);  // hub cache refreshed (CTA 0)
 #endif
-        double dpart = 0.0;
+        PAcc pa;
         uint64_t edges = 0;
         // ---- phase A: edge tiles (software-pipelined: the next tile's ids, row-start
         // bits and first row are loaded while this tile's gathers are in flight)
@@ -419,7 +483,7 @@ template <class Op> __global__ void __launch_bounds__(BLOCK, SX_PALL_MINB) pull_
                     if (u != INF) {
                         const double sum = carry + (double)run;
                         const bool complete = ridx != seg0 || tile_first_start;
-                        if (complete) op.apply(u, sum, k == 0 ? a0 : k == 1 ? a1 : op.aux(u), dpart);
+                        if (complete) op.apply(u, sum, k == 0 ? a0 : k == 1 ? a1 : op.aux(u), pa);
                         else atomicAdd(p.acc + u, sum);
                     }
                 }
@@ -439,7 +503,7 @@ template <class Op> __global__ void __launch_bounds__(BLOCK, SX_PALL_MINB) pull_
             const uint32_t u = p.sp[cs + i];
             const double a = p.acc[u];
             p.acc[u] = 0.0;
-            op.apply(u, a, op.aux(u), dpart);
+            op.apply(u, a, op.aux(u), pa);
         }
         // An empty row's value depends on no neighbour: it is the same in every
         // iteration (PageRank: up to the common dangling term), so it is written in
@@ -448,27 +512,53 @@ template <class Op> __global__ void __launch_bounds__(BLOCK, SX_PALL_MINB) pull_
         if (t == 0 || op.last || op.empty_each_iter()) {
             for (uint64_t i = gtid(); i < nempty; i += gthreads()) {
                 const uint32_t u = p.sp[i];
-                op.apply(u, 0.0, op.aux(u), dpart);
+                op.apply(u, 0.0, op.aux(u), pa);
             }
         } else if (lead()) {
-            dpart += op.empty_dangling(nempty);
+            pa.dang += op.empty_dangling(nempty);
         }
         {
-            double a[1] = {dpart};
-            block_sum<1>(a);
-            if (threadIdx.x == 0 && a[0] != 0.0) atomicAdd(&c->line[(t + 1) % 3].s[my_slot()].dsum, a[0]);
+            double a[3] = {pa.dang, pa.l1, (double)pa.unstable};
+            block_sum<3>(a);
+            if (threadIdx.x == 0) {
+                Slot& sl = c->line[(t + 1) % 3].s[my_slot()];
+                if (a[0] != 0.0) atomicAdd(&sl.dsum, a[0]);
+                if (a[1] != 0.0) atomicAdd(&sl.dsum2, a[1]);
+                if (a[2] != 0.0) atomicAdd(&sl.found, (unsigned int)a[2]);
+            }
         }
         st.edges += edges;
         if (lead()) st.entries += n;
         ++st.iters;
         if (!grid_sync(c)) return;
+        if (p.eps > 0.0) {
+            // convergence run: stop at the first iteration whose L1 change is < eps
+            // (the oracle's rule); hand over to the push tail once at most a tenth of
+            // the vertices still change by more than tau (reading 26)
+            LineSum ls;
+            read_line(&c->line[(t + 1) % 3], ls);
+            trace_put(p.s, t + 1, DIR_PULL, 2u, cnt, ls.found, 0, (uint64_t)__double_as_longlong(ls.dsum2));
+            last_l1 = ls.dsum2;
+            if (ls.dsum2 < p.eps) {
+                conv_state = 1;
+                break;
+            }
+            if (p.tail && (p.tail == 2 || (double)ls.found <= 0.1 * (double)n)) {
+                conv_state = 2;
+                break;
+            }
+            continue;
+        }
         trace_put(p.s, t + 1, DIR_PULL, t == 0 ? 1u : 2u, cnt, n, 0, 0);
     }
     st.pull = st.iters;
     flush_stats(c, st, DIR_PULL);
     if (lead()) {
-        c->iter = p.iters;
-        c->done = 1;
+        c->iter = st.iters;
+        c->done = conv_state != 2;
+        c->dir = conv_state == 2 ? DIR_PUSH : DIR_PULL;
+        c->k = conv_state;
+        c->hi = (unsigned long long)__double_as_longlong(last_l1);
         grid_end(c);
         c->launch += 1;
     }
@@ -477,6 +567,182 @@ template <class Op> __global__ void __launch_bounds__(BLOCK, SX_PALL_MINB) pull_
 template __global__ void pull_all<PrOp>(PullP<PrOp>);
 template __global__ void pull_all<SpmvOp>(PullP<SpmvOp>);
 template __global__ void pull_all<BpOp>(PullP<BpOp>);
+template __global__ void pull_all<PrcOp>(PullP<PrcOp>);
+
+
+// ---------------------------------------------------------------- PageRank push tail
+// "At the end of PageRank, we switch to the push model because the majority
+// of the vertices are stable" (the delta-accumulative push of Maiter,
+// which the paper cites).  State: r (applied ranks) and rho (change applied to
+// r but not yet propagated); invariant r* = r + sum_{k>=1} (dA)^k rho, A the
+// (column-(sub)stochastic) transition operator.  An iteration:
+//   Active  : vertices with |rho(v)| > tau (ballot filter at entry, then the
+//             online filter: a vertex is recorded when an update lifts its
+//             |rho| above tau, claimed once per iteration in the next bitmap)
+//   harvest : x_v = atomicExch(rho(v), 0) for the active set   -- grid barrier --
+//   Compute : update_{v->u} = d x_v / outdeg(v)
+//   Combine : sum, atomicAdd (fp64) into r(u) and rho(u)
+// A dangling v (variant 0) sends d x_v / N to every vertex: summed per
+// iteration into a uniform pending term U, applied to every r and rho once
+// |U| > tau, and at the end.  Stops when no |rho| exceeds tau = eps / (4N):
+// the unpropagated mass sum |rho| <= 2 N tau = eps/2, so r lies within
+// d/(1-d) * eps/2 of the fixed point (reading 26).
+struct PrTailP {
+    DevGraph g;
+    Sched s;
+    double* r;
+    double* rho;
+    double* xv;
+    double d, tau, tau0, invN;  // final threshold eps/(4N); first threshold (the mean change at the switch)
+    uint32_t variant;
+};
+struct RhoPred {
+    const double* rho;
+    double tau;
+    __device__ __forceinline__ bool operator()(uint64_t v) const { return fabs(rho[v]) > tau; }
+};
+
+__global__ void __launch_bounds__(BLOCK, 4) pr_tail(PrTailP p) {
+    Ctl* c = p.s.ctl;
+    grid_begin(c);
+    stage_init();
+    const uint64_t n = p.g.n;
+    uint32_t it = vload(&c->iter);
+    const uint32_t it0 = it;
+    if (blockIdx.x == 0 && warp_id() == 0)
+        for (int i = 0; i < 3; ++i) reset_line_warp(&c->line[i]);
+    for (int i = 0; i < 3; ++i) clear_bitmap(p.s.bm[i], p.s.nwords);
+    if (!grid_sync(c)) return;
+    Stats st;
+    uint32_t cnt[NCLS];
+    // thresholds from the mean change at the switch down to tau, /16 per stage:
+    // the largest residuals are pushed first (Maiter's priority order, approximated)
+    double tau = p.tau0 > p.tau ? p.tau0 : p.tau;
+    RhoPred pred{p.rho, tau};
+    if (!ballot_filter(BallotWords<RhoPred>{pred, n}, p.s, BallotOut{p.s.lists[it & 1], p.s.cstride, p.g.dout}, cnt))
+        return;
+    ++st.ballot;
+    st.scanned += lead() ? n : 0;
+    if (!grid_sync(c)) return;
+    view_contig(cnt);
+    double U = 0.0;  // pending uniform change (dangling pushes, variant 0); the same in every CTA
+    auto uniform = [&]() -> bool {
+        for (uint64_t v = gtid(); v < n; v += gthreads()) {
+            p.r[v] += U;
+            p.rho[v] += U;
+        }
+        U = 0.0;
+        return grid_sync(c);
+    };
+    for (;;) {
+        if (sum4(cnt) == 0) {
+            if (fabs(U) <= tau) {
+                if (tau <= p.tau) break;
+                tau = tau / 16.0 > p.tau ? tau / 16.0 : p.tau;  // next stage
+                pred.tau = tau;
+            } else if (!uniform()) {
+                return;
+            }
+            if (!ballot_filter(BallotWords<RhoPred>{pred, n}, p.s, BallotOut{p.s.lists[it & 1], p.s.cstride, p.g.dout},
+                               cnt))
+                return;
+            ++st.ballot;
+            st.scanned += lead() ? n : 0;
+            if (!grid_sync(c)) return;
+            view_contig(cnt);
+            continue;
+        }
+        if (p.s.max_iters && it >= p.s.max_iters) break;
+        // harvest the active residuals (every update of the previous iteration has landed)
+        const uint32_t* cl = p.s.lists[it & 1];
+        for (uint32_t k = 0; k < NCLS; ++k)
+            for (uint64_t i = gtid(); i < cnt[k]; i += gthreads()) {
+                const uint32_t v = task_at(cl, p.s, k, (uint32_t)i);
+                p.xv[v] = __longlong_as_double((long long)atomicExch(reinterpret_cast<unsigned long long*>(p.rho + v), 0ull));
+            }
+        if (!grid_sync(c)) return;
+        IterLine* nx = &c->line[(it + 1) % 3];
+        maybe_reset_line(&c->line[(it + 2) % 3]);
+        clear_bitmap(p.s.bm[(it + 2) % 3], p.s.nwords);
+        uint32_t* nlists = p.s.lists[(it + 1) & 1];
+        uint32_t* nbm = p.s.bm[(it + 1) % 3];
+        double upart = 0.0;
+        uint64_t edges = 0;
+        for_tasks(cl, p.s, cnt, [&](uint32_t v, uint64_t rank, uint64_t size, uint32_t) {
+            const uint64_t beg = __ldg(p.g.rp + v), end = __ldg(p.g.rp + v + 1);
+            const double x = p.xv[v];
+            if (beg == end) {
+                if (rank == 0 && p.variant == 0) upart += p.d * x * p.invN;
+                return;
+            }
+            const double inc = p.d * x / (double)(end - beg);
+            for_edges_b(p.g.ci, beg, end, rank, size, [&](const uint32_t (&u)[4], uint32_t kn) {
+                edges += kn;
+                double old[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (j < (int)kn) atomicAdd(p.r + u[j], inc);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) old[j] = j < (int)kn ? atomicAdd(p.rho + u[j], inc) : 0.0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (j >= (int)kn || !(fabs(old[j] + inc) > tau)) continue;
+                    const uint32_t bit = 1u << (u[j] & 31);
+                    if (atomicOr(nbm + (u[j] >> 5), bit) & bit) continue;  // claimed once per iteration
+                    online_record(nx, nlists, p.s, u[j], cls_of(__ldg(p.g.dout + u[j]), p.s));
+                }
+            });
+        });
+        stage_flush(nx, nlists, p.s);
+        st.edges += edges;
+        if (lead()) st.entries += sum4(cnt);
+        {
+            double a[1] = {upart};
+            block_sum<1>(a);
+            if (threadIdx.x == 0 && a[0] != 0.0) atomicAdd(&nx->s[my_slot()].dsum, a[0]);
+        }
+        if (!grid_sync(c)) return;
+        LineSum ls;
+        uint32_t vcnt[NCLS];
+        read_line_view(nx, p.s, ls, vcnt);
+        U += ls.dsum;
+        bool overflow = false;
+        for (int i = 0; i < NCLS; ++i) overflow |= ls.cntmax[i] > p.s.cap_s;
+        if (p.s.force_filter == 2) overflow = true;
+        ++it;
+        ++st.iters;
+        trace_put(p.s, it, DIR_PUSH, overflow ? 1u : 0u, ls.cnt, sum4(ls.cnt), 0, (uint64_t)__double_as_longlong(U));
+        if (sum4(ls.cnt) > 0 && overflow) {
+            ++st.ballot;
+            st.scanned += lead() ? p.s.nwords * 32 : 0;
+            if (!ballot_filter(BitmapWords{nbm}, p.s, BallotOut{p.s.lists[it & 1], p.s.cstride, p.g.dout}, cnt)) return;
+            if (!grid_sync(c)) return;
+            view_contig(cnt);
+        } else {
+            for (int i = 0; i < NCLS; ++i) cnt[i] = vcnt[i];  // view set by read_line_view
+        }
+    }
+    // the pending uniform term joins r (and rho, so the residual covers what was not propagated)
+    if (U != 0.0 && !uniform()) return;
+    double* R = reinterpret_cast<double*>(&c->hi);
+    if (lead()) *R = 0.0;
+    if (!grid_sync(c)) return;
+    {
+        double a[1] = {0.0};
+        for (uint64_t v = gtid(); v < n; v += gthreads()) a[0] += fabs(p.rho[v]);
+        block_sum<1>(a);
+        if (threadIdx.x == 0 && a[0] != 0.0) atomicAdd(R, a[0]);
+    }
+    (void)it0;
+    flush_stats(c, st, DIR_PUSH);
+    if (!grid_sync(c)) return;
+    if (lead()) {
+        c->iter = it;
+        c->done = 1;
+        grid_end(c);
+        c->launch += 1;
+    }
+}
 
 // ---------------------------------------------------------------- per-graph plan kernels
 __global__ void k_hubslot(const uint32_t* hubs, uint32_t K, uint32_t* slot) {
@@ -614,13 +880,7 @@ static double pull_bytes(const sx_graph g, const sxh::Counters& c) {
     return c.iters * ((double)g->mi * (t_edge_bytes + 0.125) + (double)g->n * t_vertex_bytes) + c.scanned / 8.0;
 }
 
-template <class Op>
-sx_status run_pull(sx_graph g, const sx_opts* opts, sx_stats* stats, const Op& op, uint32_t iters, double edge_bytes,
-                   double vertex_bytes) {
-    sxh::Run run{g, sxh::resolve_opts(opts), stats};
-    run.o.cluster_enter = sxh::resolve_cluster(run.o.cluster_enter, false, g->n);
-    sx_status rc = run.begin();
-    if (rc != SX_OK) return rc;
+template <class Op> PullP<Op> pull_params(sx_graph g, const sxh::Run& run, const Op& op, uint32_t iters) {
     PullP<Op> p;
     p.g = sxh::dev_graph(g);
     p.s = sxh::make_sched(g, run.o);
@@ -637,13 +897,35 @@ sx_status run_pull(sx_graph g, const sx_opts* opts, sx_stats* stats, const Op& o
     p.nzaux = g->pp_nzaux;
     p.sp = g->lists[1];
     p.acc = g->hacc;
+    p.eps = 0.0;
+    p.tail = 0;
+    return p;
+}
+
+template <class Op>
+sx_status run_pull(sx_graph g, const sx_opts* opts, sx_stats* stats, const Op& op, uint32_t iters, double edge_bytes,
+                   double vertex_bytes, double eps = 0.0) {
+    sxh::Run run{g, sxh::resolve_opts(opts), stats};
+    run.o.cluster_enter = sxh::resolve_cluster(run.o.cluster_enter, false, g->n);
+    sx_status rc = run.begin();
+    if (rc != SX_OK) return rc;
+    PullP<Op> p = pull_params(g, run, op, iters);
+    p.eps = eps;
     void* args[] = {&p};
     const int smem = (int)(PULL_HUBS * sizeof(typename Op::HubT));
     if ((rc = run.launch((const void*)pull_all<Op>, args, sxh::KIND_PULL, smem)) != SX_OK) return rc;
     t_edge_bytes = edge_bytes;
     t_vertex_bytes = vertex_bytes;
-    return run.end(pull_bytes);
+    rc = run.end(pull_bytes);
+    if (rc == SX_OK && stats) {
+        const unsigned long long h = g->ctx->h_ctl->hi;
+        double last = 0.0;
+        std::memcpy(&last, &h, 8);
+        stats->residual = eps > 0.0 ? last : 0.0;
+    }
+    return rc;
 }
+
 
 }  // namespace
 
@@ -754,7 +1036,118 @@ extern "C" sx_status sx_bp(sx_graph g, const float* prior, uint32_t iters, const
     op.cur = 0;
     op.D = 0;
     op.last = false;
+    op.conv = false;
     // edge: source id 4 + weight; vertex: belief read 8 + belief write 8 + prior 4
     if ((rc = run_pull(g, opts, stats, op, iters, 4.0 + g->wbytes, 20.0)) != SX_OK) return rc;
     return dev_out ? SX_OK : sxh::copy_out(g, logodds_out, op.out, g->n * 4);
+}
+
+extern "C" sx_status sx_bp_conv(sx_graph g, const float* prior, double epsilon, uint32_t max_iters,
+                                const sx_opts* opts, float* logodds_out, sx_stats* stats) {
+    if (!g || !prior || !logodds_out) return sxh::fail(SX_E_INVALID, "sx_bp_conv: NULL argument");
+    sx_status rc = sxh::check_ctx(g->ctx);
+    if (rc != SX_OK) return rc;
+    if (!(epsilon > 0.0)) return sxh::fail(SX_E_INVALID, "sx_bp_conv: epsilon must be > 0");
+    if (max_iters == 0) return sxh::fail(SX_E_INVALID, "sx_bp_conv: max_iters must be >= 1");
+    if (g->n == 0) return SX_OK;
+    if ((rc = prep(g, "sx_bp_conv")) != SX_OK) return rc;
+    if (!g->dstate && (rc = sxh::dmalloc(g->ctx, &g->dstate, (2 * g->n + 256) * sizeof(double))) != SX_OK) return rc;
+    k_bp_ctab<<<1, 256, 0, g->ctx->stream>>>(g->dstate + 2 * g->n);
+    SX_CU(cudaGetLastError());
+    const bool dev_out = sxh::is_device_ptr(logodds_out);
+    BpOp op;
+    op.b[0] = g->dstate;
+    op.b[1] = g->dstate + g->n;
+    op.ctab = g->dstate + 2 * g->n;
+    float* dp = (float*)g->st[2];
+    if ((rc = sxh::copy_in(g, dp, prior, g->n * 4)) != SX_OK) return rc;
+    op.prior = dp;
+    op.out = dev_out ? logodds_out : (float*)g->st[3];
+    op.cur = 0;
+    op.D = 0;
+    op.last = true;
+    op.conv = true;
+    if ((rc = run_pull(g, opts, stats, op, max_iters, 4.0 + g->wbytes, 24.0, epsilon)) != SX_OK) return rc;
+    return dev_out ? SX_OK : sxh::copy_out(g, logodds_out, op.out, g->n * 4);
+}
+
+// Algorithmic bytes of the push tail: per harvested entry 4 B list +
+// 16 B row_ptr + 8 B rho exchange + 8 B x; per pushed edge 4 B col + 2 x 8 B fp64
+// read-modify-writes (r, rho); ballot passes 8 B rho per vertex.
+static double prtail_bytes(const sx_graph g, const sxh::Counters& c) {
+    return 36.0 * c.entries + 20.0 * c.edges + 8.0 * c.scanned + c.iters * (double)g->n / 8.0;
+}
+static double prc_bytes(const sx_graph g, const sxh::Counters& c) {
+    if (c.pull > 0) return pull_bytes(g, c);
+    return prtail_bytes(g, c);
+}
+
+extern "C" sx_status sx_pagerank_conv(sx_graph g, double damping, double epsilon, uint32_t max_iters, uint32_t variant,
+                                      const sx_opts* opts, double* rank_out, sx_stats* stats) {
+    if (!g || !rank_out) return sxh::fail(SX_E_INVALID, "sx_pagerank_conv: NULL graph or rank_out");
+    sx_status rc = sxh::check_ctx(g->ctx);
+    if (rc != SX_OK) return rc;
+    if (!(damping > 0.0 && damping < 1.0)) return sxh::fail(SX_E_INVALID, "sx_pagerank_conv: damping outside (0,1)");
+    if (!(epsilon > 0.0)) return sxh::fail(SX_E_INVALID, "sx_pagerank_conv: epsilon must be > 0");
+    if (max_iters == 0) return sxh::fail(SX_E_INVALID, "sx_pagerank_conv: max_iters must be >= 1");
+    if (variant > SX_PR_SPEC) return sxh::fail(SX_E_INVALID, "sx_pagerank_conv: unknown variant");
+    if (g->n == 0) return SX_OK;
+    if ((rc = prep(g, "sx_pagerank_conv")) != SX_OK) return rc;
+    const uint64_t n = g->n;
+    if (!g->prc && (rc = sxh::dmalloc(g->ctx, &g->prc, 5 * n * sizeof(double) + 64)) != SX_OK) return rc;
+    const bool dev_out = sxh::is_device_ptr(rank_out);
+    sxh::Run run{g, sxh::resolve_opts(opts), stats};
+    if ((rc = run.begin()) != SX_OK) return rc;
+    const double d = damping;
+    PrcOp op;
+    op.contrib[0] = g->prc;
+    op.contrib[1] = g->prc + n;
+    op.r = dev_out ? rank_out : g->prc + 2 * n;
+    op.rho = g->prc + 3 * n;
+    op.dout = g->dout;
+    op.d = d;
+    op.base = variant == SX_PR_NORMALIZED ? (1.0 - d) / (double)n : 1.0 - d;
+    op.dn = variant == SX_PR_NORMALIZED ? 1.0 / (double)n : 0.0;
+    op.r0 = variant == SX_PR_NORMALIZED ? 1.0 / (double)n : 1.0;
+    op.tau = epsilon / (4.0 * (double)n);
+    op.cur = 0;
+    op.D = 0;
+    op.last = true;
+    PullP<PrcOp> p = pull_params(g, run, op, max_iters);
+    p.eps = epsilon;
+    p.tail = run.o.force_dir == 2 ? 0u : run.o.force_dir == 1 ? 2u : 1u;
+    void* args[] = {&p};
+    const int smem = (int)(PULL_HUBS * sizeof(double));
+    if ((rc = run.launch((const void*)pull_all<PrcOp>, args, sxh::KIND_PULL, smem)) != SX_OK) return rc;
+    if ((rc = run.sync()) != SX_OK) return rc;
+    const Ctl& h = *g->ctx->h_ctl;
+    if (!h.done && h.dir == DIR_PUSH && h.iter < max_iters) {
+        PrTailP q;
+        q.g = p.g;
+        q.s = p.s;
+        q.s.max_iters = max_iters;
+        q.r = op.r;
+        q.rho = op.rho;
+        q.xv = g->prc + 4 * n;
+        q.d = d;
+        q.tau = op.tau;
+        double last = 0.0;
+        std::memcpy(&last, &h.hi, 8);
+        q.tau0 = last / (double)n;
+        q.invN = 1.0 / (double)n;
+        q.variant = variant;
+        void* args2[] = {&q};
+        if ((rc = run.launch((const void*)pr_tail, args2, sxh::KIND_PUSH)) != SX_OK) return rc;
+    }
+    // edge: source id 4 + gathered contrib 8; vertex: r read/write 16, rho write 8, contrib write 8, outdeg 4
+    t_edge_bytes = 12.0;
+    t_vertex_bytes = 36.0;
+    if ((rc = run.end(prc_bytes)) != SX_OK) return rc;
+    if (stats) {
+        double res = 0.0;
+        const unsigned long long hh = g->ctx->h_ctl->hi;
+        std::memcpy(&res, &hh, 8);
+        stats->residual = res;
+    }
+    return dev_out ? SX_OK : sxh::copy_out(g, rank_out, op.r, n * 8);
 }

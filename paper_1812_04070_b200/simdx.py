@@ -56,7 +56,7 @@ class sx_stats(ctypes.Structure):
                 ("bytes_model", ctypes.c_double), ("ms", ctypes.c_double), ("ms_push", ctypes.c_double),
                 ("ms_pull", ctypes.c_double), ("bytes_push", ctypes.c_double), ("bytes_pull", ctypes.c_double),
                 ("launches_push", _u32), ("launches_pull", _u32), ("ms_fused", ctypes.c_double),
-                ("launches_fused", _u32), ("runs", _u32)]
+                ("launches_fused", _u32), ("runs", _u32), ("residual", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -93,6 +93,8 @@ _lib.sx_graph_sync.argtypes = [_vp, _P(sx_stats)]
 _lib.sx_barrier_fault.argtypes = [_vp, _u32, _u32]
 _lib.sx_sssp.argtypes = [_vp, _u32, _u32, _P(sx_opts), _vp, _P(sx_stats)]
 _lib.sx_pagerank.argtypes = [_vp, _f32, _u32, _P(sx_opts), _vp, _P(sx_stats)]
+_lib.sx_pagerank_conv.argtypes = [_vp, ctypes.c_double, ctypes.c_double, _u32, _u32, _P(sx_opts), _vp, _P(sx_stats)]
+_lib.sx_bp_conv.argtypes = [_vp, _vp, ctypes.c_double, _u32, _P(sx_opts), _vp, _P(sx_stats)]
 _lib.sx_kcore.argtypes = [_vp, _u32, _P(sx_opts), _vp, _P(sx_stats)]
 _lib.sx_spmv.argtypes = [_vp, _vp, _u32, _P(sx_opts), _vp, _P(sx_stats)]
 _lib.sx_bp.argtypes = [_vp, _vp, _u32, _P(sx_opts), _vp, _P(sx_stats)]
@@ -110,7 +112,7 @@ _lib.sx_dist_bfs.argtypes = [_vp, _u32, _P(sx_opts), _P(_vp), _P(sx_stats)]
 _lib.sx_dist_sssp.argtypes = [_vp, _u32, _u32, _P(sx_opts), _P(_vp), _P(sx_stats)]
 for _f in ("sx_ctx_create", "sx_ctx_info", "sx_graph_upload", "sx_graph_info", "sx_graph_rmat", "sx_graph_grid",
            "sx_graph_download", "sx_bfs", "sx_bfs_async", "sx_graph_sync", "sx_barrier_fault", "sx_sssp",
-           "sx_pagerank",
+           "sx_pagerank", "sx_pagerank_conv", "sx_bp_conv",
            "sx_kcore", "sx_spmv", "sx_bp", "sx_wcc", "sx_barrier_bench", "sx_cluster_bench", "sx_launch_bench",
            "sx_nccl_unique_id", "sx_dist_create", "sx_dist_range", "sx_dist_upload", "sx_dist_bfs", "sx_dist_sssp"):
     getattr(_lib, _f).restype = ctypes.c_int
@@ -118,7 +120,7 @@ for _f in ("sx_ctx_create", "sx_ctx_info", "sx_graph_upload", "sx_graph_info", "
 EXPORTED = ["sx_status_str", "sx_last_error", "sx_version", "sx_ctx_create", "sx_ctx_destroy", "sx_ctx_info",
             "sx_graph_upload", "sx_graph_info", "sx_graph_free", "sx_graph_rmat", "sx_graph_grid", "sx_graph_download",
             "sx_opts_default", "sx_bfs", "sx_bfs_async", "sx_graph_sync", "sx_barrier_fault", "sx_sssp",
-            "sx_pagerank", "sx_kcore", "sx_spmv", "sx_bp", "sx_wcc", "sx_barrier_bench", "sx_cluster_bench", "sx_launch_bench",
+            "sx_pagerank", "sx_pagerank_conv", "sx_bp_conv", "sx_kcore", "sx_spmv", "sx_bp", "sx_wcc", "sx_barrier_bench", "sx_cluster_bench", "sx_launch_bench",
             "sx_nccl_unique_id", "sx_dist_create", "sx_dist_range", "sx_dist_upload", "sx_dist_free", "sx_dist_bfs", "sx_dist_sssp"]
 
 
@@ -326,6 +328,29 @@ def sx_pagerank(g, damping, iters, opts, rank_out, n=None):
     return _run(_lib.sx_pagerank, "sx_pagerank", g, rank_out, opts, (damping, iters), n=n)
 
 
+SX_PR_NORMALIZED, SX_PR_SPEC = 0, 1
+
+
+def sx_pagerank_conv(g, damping, epsilon, max_iters, variant, opts, rank_out, n=None):
+    n = _nv(g, n)
+    if rank_out is not None and (rank_out.element_size() if _is_torch(rank_out) else rank_out.dtype.itemsize) != 8:
+        raise ValueError("sx_pagerank_conv out: 8-byte (float64) elements required")
+    st = sx_stats()
+    o = opts if opts is not None else sx_opts_default()
+    size = rank_out.numel() if _is_torch(rank_out) else rank_out.size
+    if size < n:
+        raise ValueError(f"sx_pagerank_conv out: {n} elements required (got {size})")
+    _check(_lib.sx_pagerank_conv(g, damping, epsilon, max_iters, variant, ctypes.byref(o), _ptr(rank_out),
+                                 ctypes.byref(st)), "sx_pagerank_conv")
+    return st
+
+
+def sx_bp_conv(g, prior, epsilon, max_iters, opts, out, n=None):
+    n = _nv(g, n)
+    return _run(_lib.sx_bp_conv, "sx_bp_conv", g, out, opts, (_ptr_n(prior, n, "sx_bp_conv prior"), epsilon, max_iters),
+                n=n)
+
+
 def sx_kcore(g, k, opts, core_out, n=None):
     return _run(_lib.sx_kcore, "sx_kcore", g, core_out, opts, (k,), n=n)
 
@@ -475,6 +500,19 @@ class Graph:
         out = np.empty(self.n, np.float32) if out is None else out
         o, buf = self._opts(dict(kw))
         st = sx_pagerank(self.h, damping, iters, o, out, self.n)
+        return out, st.as_dict(), self._trace(buf, st)
+
+    def pagerank_conv(self, damping: float = 0.85, eps: float = 1e-6, max_iters: int = 10000, variant: int = 0,
+                      out=None, **kw):
+        out = np.empty(self.n, np.float64) if out is None else out
+        o, buf = self._opts(dict(kw))
+        st = sx_pagerank_conv(self.h, damping, eps, max_iters, variant, o, out, self.n)
+        return out, st.as_dict(), self._trace(buf, st)
+
+    def bp_conv(self, prior, eps: float = 1e-6, max_iters: int = 1000, out=None, **kw):
+        out = np.empty(self.n, np.float32) if out is None else out
+        o, buf = self._opts(dict(kw))
+        st = sx_bp_conv(self.h, prior, eps, max_iters, o, out, self.n)
         return out, st.as_dict(), self._trace(buf, st)
 
     def kcore(self, k: int = 0, out=None, **kw):

@@ -66,7 +66,7 @@ def test_no_cpu_fallback_without_gpu():
 def test_trace_and_stats_struct_sizes():
     from paper_1812_04070_b200 import simdx
     assert ctypes.sizeof(simdx.sx_trace_rec) == 64
-    assert ctypes.sizeof(simdx.sx_stats) == 4 * 4 + 3 * 8 + 6 * 8 + 2 * 4 + 8 + 2 * 4
+    assert ctypes.sizeof(simdx.sx_stats) == 4 * 4 + 3 * 8 + 6 * 8 + 2 * 4 + 8 + 2 * 4 + 8
 
 
 def test_binding_checks_caller_buffers():

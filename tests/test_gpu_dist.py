@@ -111,3 +111,48 @@ def test_dist_reupload_replaces_the_slices(ctx):
         outs, _ = D.sssp(0, 256)
         assert np.array_equal(np.concatenate(outs), oracle.sssp(g2, 0))
     D.free()
+
+
+def test_dist_nccl_one_rank_communicator(ctx, rmat14):
+    """The NCCL branch of the data path (allgather / alltoall / reduce-scatter /
+    allreduce on a one-rank communicator) against the oracle."""
+    from paper_1812_04070_b200 import simdx
+    nid = simdx.sx_nccl_unique_id()
+    D = simdx.Dist(ctx, rmat14.n, 1, 0, 1, nid)
+    sl = simgen.CSR(n=rmat14.n, row_ptr=rmat14.row_ptr.copy(), col=rmat14.col.copy(), w=rmat14.w.copy(),
+                    v_lo=0, v_hi=rmat14.n)
+    D.upload(0, sl)
+    for src in (0, 1234):
+        ref = oracle.bfs(rmat14, src)
+        for mode in (dict(), dict(force_dir=1), dict(force_dir=2)):
+            outs, st = D.bfs(src, **mode)
+            assert np.array_equal(outs[0], ref), (src, mode)
+    ref = oracle.sssp(rmat14, 0)
+    for delta in (0, 1024):
+        outs, _ = D.sssp(0, delta)
+        assert np.array_equal(outs[0], ref), delta
+    D.free()
+
+
+def test_bench_dist_path_under_torchrun():
+    """bench.py's multi-GPU path (torchrun, NCCL communicator, max-over-ranks
+    timing) at one rank: one JSON line with the contract's keys."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+           "--master-addr=127.0.0.1", f"--master-port={port}", "bench.py", "--gpus", "1", "--dist", "--scale", "16",
+           "--steps", "3", "--warmup", "3", "--no-e2e"]
+    out = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["unit"] == "GTEPS" and line["value"] > 0 and line["n_gpus"] == 1
+    assert line["config"]["parallelism"] == "1d1" and "NCCL" in line["config"]["workload"]
+    assert line["gpu_launches"] > 0
