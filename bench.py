@@ -293,6 +293,10 @@ def run_single(args):
         _, s, _ = G.kcore(0, out=out)
         extras["kcore"] = {"k": 0, "ms": s["ms"], "iterations": s["iterations"],
                            "hbm_gbs": s["bytes_model"] / (s["ms"] * 1e-3) / 1e9}
+        _, s, _ = G.kcore(0, out=out, cluster_enter=0)
+        extras["kcore_bsp_only"] = {"k": 0, "ms": s["ms"], "iterations": s["iterations"]}
+        _, s, _ = G.kcore(16, out=out)
+        extras["kcore_k16"] = {"k": 16, "ms": s["ms"], "iterations": s["iterations"]}
         G.wcc(out=out)
         _, s, _ = G.wcc(out=out)
         extras["wcc"] = {"ms": s["ms"], "iterations": s["iterations"], "launches": s["launches"]}
@@ -309,6 +313,15 @@ def run_single(args):
             best = s if best is None or s["ms"] < best["ms"] else best
         gbs = best["bytes_model"] / (best["ms"] * 1e-3) / 1e9
         extras["c3_pagerank_s22"] = {"iters": 20, "ms": best["ms"], "hbm_gbs": gbs, "frac": gbs / peak}
+        # NEXT-3: PageRank to convergence (both recurrences; pull -> push tail) and BP to convergence
+        r64 = torch.empty(1 << 22, dtype=torch.float64, device=dev)
+        for var, eps in ((0, 1e-6), (1, 1e-6 * (1 << 22))):
+            G3.pagerank_conv(0.85, eps, 10000, var, out=r64)
+            _, s, _ = G3.pagerank_conv(0.85, eps, 10000, var, out=r64)
+            extras[f"c3_pagerank_conv_v{var}"] = {"eps": eps, "ms": s["ms"], "iterations": s["iterations"],
+                                                  "pull_iters": s["pull_iters"], "launches": s["launches"],
+                                                  "residual": s["residual"]}
+        del r64
         # SpMV (1 product) and BP (10 iterations) on the same graph, the same tiled pull
         x3 = torch.from_numpy(simgen.uniform_f32(args.seed, 1, 1 << 22, 0.0, 1.0)).to(dev)
         G3.spmv(x3, 1, out=r3)
@@ -318,6 +331,9 @@ def run_single(args):
         G3.bp(pr3, 10, out=r3)
         _, s, _ = G3.bp(pr3, 10, out=r3)
         extras["bp_s22"] = {"iters": 10, "ms": s["ms"], "hbm_gbs": s["bytes_model"] / (s["ms"] * 1e-3) / 1e9}
+        _, s, _ = G3.bp_conv(pr3, 1e-3 * (1 << 22), 200, out=r3)
+        extras["bp_conv_s22"] = {"eps": 1e-3 * (1 << 22), "ms": s["ms"], "iterations": s["iterations"],
+                                 "residual": s["residual"]}
         G3.free()
         # C5 at P = 1: R-MAT s27 (4.3 G edges) built on the device; BFS and SSSP device time
         try:
@@ -347,7 +363,27 @@ def run_single(args):
         extras["c2_sssp_grid2048"] = {"delta": args.delta, "ms": s["ms"], "iterations": s["iterations"],
                                       "us_per_iteration": s["ms"] * 1e3 / max(1, s["iterations"]),
                                       "launches": s["launches"]}
+        # filter / fusion ablation on the synthetic configs (the paper's Figs. 12-13,
+        # P:1082-1093): device ms, best of 2; batch = every update recorded with duplicates
+        # (P:536-545); k-core rows run BSP sub-rounds (cluster_enter = 0) unless named
+        modes = (("jit", {}), ("online", dict(force_filter=1)), ("ballot", dict(force_filter=2)),
+                 ("batch", dict(force_filter=3)), ("no_fusion", dict(fusion=0)))
+
+        def best(fn, **kw):
+            return min((fn(**kw)[1] for _ in range(2)), key=lambda x: x["ms"])["ms"]
+
+        abl = {"c2_sssp_grid2048": {k: best(lambda **kw: G2.sssp(0, args.delta, out=d2, **kw), **kw) for k, kw in modes}}
         G2.free()
+        abl["bfs_s24"] = {k: best(lambda **kw: G.bfs(0, out=level, **kw), **kw)
+                          for k, kw in modes + (("all_fusion", dict(fusion=2, cluster_enter=0)),)}
+        abl["c4_kcore_s24"] = {k: best(lambda **kw: G.kcore(0, out=out, cluster_enter=0, **kw), **kw) for k, kw in modes}
+        abl["c4_kcore_s24"]["jit_async_tail"] = best(lambda **kw: G.kcore(0, out=out, **kw))
+        G1 = ctx.rmat(16, args.ef, args.seed)
+        l1 = torch.empty(1 << 16, dtype=torch.int32, device=dev)
+        abl["c1_bfs_s16"] = {k: best(lambda **kw: G1.bfs(0, out=l1, **kw), **kw)
+                             for k, kw in modes + (("all_fusion", dict(fusion=2, cluster_enter=0)),)}
+        G1.free()
+        extras["ablation_ms"] = abl
         log(f"[bench] extras: {extras}")
 
     # ---- e2e: pinned host CSR -> upload -> BFS -> host levels -> free, through the C ABI

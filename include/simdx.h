@@ -207,7 +207,9 @@ typedef struct {
     uint32_t sep_large;          /* degree separator warp|CTA; default 128 */
     uint32_t sep_huge;           /* degree separator CTA|grid-split (B200 addition); default 16384 */
     float alpha, beta;           /* push->pull when m_f > m_u/alpha, pull->push when n_f < n/beta (Beamer; reading 8); 14, 24 */
-    int32_t force_filter;        /* 0 JIT, 1 online only, 2 ballot only */
+    int32_t force_filter;        /* 0 JIT, 1 online only, 2 ballot only, 3 batch (the baseline of
+                                    P:536-545: every update recorded, duplicates kept, no claim; BFS and
+                                    SSSP/WCC push; k-core removals are exactly-once, so 3 = online there) */
     int32_t force_dir;           /* 0 auto, 1 push only, 2 pull only */
     int32_t fusion;              /* 1 selective push/pull fusion (default); 0 no fusion (one launch per
                                     iteration); 2 all fusion (BFS: one launch for every phase) */
@@ -226,7 +228,10 @@ typedef struct {
                                     barrier; back to the full grid above 8x this size (BFS: or 256x this
                                     many out-edges).  Results unchanged.  0 = never.  Default
                                     SX_CLUSTER_AUTO = 4096, except BFS on graphs below 2^21 vertices
-                                    where the tail measured slower (0). */
+                                    where the tail measured slower (0).
+                                    k-core: once a sub-round frontier of a level has at most this many
+                                    vertices, the rest of the level's cascade runs as an asynchronous work
+                                    queue (no grid barrier per sub-round; reading 28); 0 = BSP. */
 } sx_opts;
 
 typedef struct {

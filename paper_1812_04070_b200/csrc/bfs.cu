@@ -93,7 +93,7 @@ constexpr uint32_t CL_EDGES = 32;
 constexpr uint64_t REC_EDGES = SX_REC_EDGES;
 constexpr uint32_t DIR_NOCLUSTER = 0x100;  // bfs_init flag: no cluster start (all fusion)
 __device__ __forceinline__ bool cluster_ok(const Sched& s, uint64_t nf, uint64_t mf) {
-    return s.cluster_enter && s.fusion && s.force_filter != 2 && s.force_dir != 2 && nf > 0 &&
+    return s.cluster_enter && s.fusion && s.force_filter < 2 && s.force_dir != 2 && nf > 0 &&
            nf <= s.cluster_enter && mf <= (uint64_t)CL_EDGES * s.cluster_enter;
 }
 
@@ -279,7 +279,8 @@ __device__ __forceinline__ bool push_phase(const BfsP& p, RunState& rs) {
         // REC_EDGES out-edges activates a next frontier the ballot filter handles
         // better (or the pull takes over), so it is not recorded online — as if
         // the bins had overflowed; measured: the s24 hub level 30 -> 24 us
-        const bool rec = mf_cur <= REC_EDGES;
+        const bool batch = p.s.force_filter == 3;
+        const bool rec = batch || mf_cur <= REC_EDGES;
         auto visit = [&](uint32_t v, uint64_t rank, uint64_t size, uint32_t) {
             const uint64_t beg = __ldg(p.g.rp + v), end = __ldg(p.g.rp + v + 1);
             // up to 4 edges per step: visited words, claims and the claimed
@@ -293,7 +294,11 @@ __device__ __forceinline__ bool push_phase(const BfsP& p, RunState& rs) {
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const uint32_t bit = 1u << (u[j] & 31);
-                    cl[j] = j < (int)k && !(vw[j] & bit) && !(atomicOr(p.visited + (u[j] >> 5), bit) & bit);
+                    // batch filter (force_filter = 3): no claim, so a vertex reached by
+                    // several frontier vertices in the iteration is updated and recorded by each
+                    cl[j] = j < (int)k && !(vw[j] & bit) &&
+                            (batch ? (atomicOr(p.visited + (u[j] >> 5), bit), true)
+                                   : !(atomicOr(p.visited + (u[j] >> 5), bit) & bit));
                 }
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
@@ -1135,7 +1140,7 @@ extern "C" sx_status sx_bfs(sx_graph g, uint32_t src, const sx_opts* opts, uint3
     // without a host round trip — a launch whose direction does not match the
     // device-side state exits at once — and the host syncs once per sequence.
     // likely successor of each phase: push -> pull -> cluster tail (-> push)
-    const bool cl_on = run.o.cluster_enter && run.o.fusion && run.o.force_filter != 2 && run.o.force_dir != 2;
+    const bool cl_on = run.o.cluster_enter && run.o.fusion && run.o.force_filter < 2 && run.o.force_dir != 2;
     auto next = [&](uint32_t d) -> uint32_t {
         if (d == DIR_PUSH) return DIR_PULL;
         if (d == DIR_PULL) return cl_on ? DIR_CLUSTER : DIR_PUSH;

@@ -132,7 +132,8 @@ Sched make_sched(const sx_graph g, const sx_opts& o) {
     s.cstride = (uint64_t)NSLOT * s.R;
     const uint64_t warps = (uint64_t)g->ctx->prop.multiProcessorCount * (2048 / 32);
     uint64_t cap = ((uint64_t)o.overflow_threshold * warps + NSLOT - 1) / NSLOT;
-    if (o.force_filter == 1 || cap > s.R) cap = s.R;  // online only: regions are never capped below their size
+    // online only / batch: regions are never capped below their size (overflow = a full region)
+    if (o.force_filter == 1 || o.force_filter == 3 || cap > s.R) cap = s.R;
     s.cap_s = (uint32_t)cap;
     s.alpha = o.alpha;
     s.beta = o.beta;

@@ -269,6 +269,7 @@ void sx_graph_free(sx_graph g) {
     F(g->hacc);
     F(g->dstate);
     F(g->prc);
+    F(g->kq);
     F(g->hub);
     F(g->async_acc);
     F(g->pp_hcol);

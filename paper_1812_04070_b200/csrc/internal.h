@@ -57,6 +57,7 @@ struct sx_graph_s {
     uint32_t* st[4] = {nullptr, nullptr, nullptr, nullptr};  // 4N-byte state arrays
     double* hacc = nullptr;       // n+1 doubles, pull-all split-row partial sums (lazy)
     double* dstate = nullptr;     // 2n doubles, BP beliefs (lazy)
+    unsigned long long* kq = nullptr;  // k-core asynchronous cascade queue (lazy)
     double* prc = nullptr;        // 5n doubles, PageRank to convergence: contrib x2, r, rho, harvested x (lazy)
     uint32_t* hub = nullptr;      // n entries, BFS hub-first probe table (built at upload)
     // sx_bfs_async bookkeeping: device stat accumulator, host-side event times

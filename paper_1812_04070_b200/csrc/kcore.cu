@@ -26,8 +26,10 @@ struct KcoreP {
     uint32_t* core;  // coreness, INF while alive
     uint32_t* ab;    // alive bitmap (bit v set while core[v] = INF): n/8 bytes, L2-resident
     uint32_t kfix;   // 0 = decomposition
-    uint32_t* q;     // asynchronous cascade queue: n entries, INF = not yet written (positions never reused)
+    unsigned long long* q;  // asynchronous cascade queue: qcap items (v << 32 | piece), all ones = not yet written
+    uint64_t qcap;          // positions are never reused within a run: n removals + the pieces of split rows
     uint32_t amax;   // a level's cascade goes asynchronous once a sub-round frontier has <= amax vertices (0: never)
+    uint32_t* al[2];  // the alive vertices as a list, compacted at every level start (two buffers)
 };
 
 // Asynchronous tail of a level's cascade (B200 addition; results unchanged by
@@ -35,14 +37,15 @@ struct KcoreP {
 // residual from k+1 to k, whatever the order).  Once a sub-round's frontier is
 // small, the grid barrier per sub-round (3.2 us, with a dependent chain of a
 // few microseconds behind it) dominates: the rest of the level runs as a
-// work queue instead.  A removal is an item; a warp takes 32 tickets (queue
-// positions) at a time, polls them, and processes whichever have been
-// published — small rows on their lane, larger rows by the whole warp
-// — enqueueing the neighbours whose residual it takes to k.  One 64-bit
+// work queue instead.  A removal is an item; a warp takes one ticket (queue
+// position) at a time, waits for it to be published and processes the item
+// with the whole warp (warp granularity; rows longer than AQ_PIECE
+// edges are split into pieces, themselves items), enqueueing the neighbours
+// whose residual it takes to k.  One 64-bit
 // word counts positions (low half) and pending items (high half): an item is
 // pending from its enqueue until its own enqueues are done, so pending = 0
 // means the cascade is over.  Only AQ_WARPS warps per CTA take part.
-constexpr uint32_t AQ_WARPS = 2;
+constexpr uint32_t AQ_WARPS = 4;
 constexpr unsigned long long AQ_ONE = 1ull << 32;
 __device__ __forceinline__ uint32_t aq_pending(const Ctl* c) { return (uint32_t)(vload(&c->aq_tp) >> 32); }
 // watchdog of the queue waits (as the grid barrier's): a lost item would leave
@@ -55,59 +58,55 @@ __device__ __forceinline__ bool aq_stuck(Ctl* c, uint32_t& spins, uint64_t& t0) 
     return vload(&c->error) != 0;
 }
 
+constexpr uint32_t AQ_PIECE = 1024;  // a removal of a longer row is split into pieces of this many edges
+constexpr unsigned long long AQ_EMPTY = ~0ull;
 template <class Rm>
-__device__ __forceinline__ void kcore_async(const KcoreP& p, Ctl* c, Rm&& remove_edges, uint64_t& edges,
-                                            uint64_t& entries) {
+__device__ __forceinline__ void kcore_async(const KcoreP& p, Ctl* c, Rm&& remove_edges, uint64_t& entries) {
     if (warp_id() >= AQ_WARPS) return;
     const uint32_t lane = lane_id();
-    const uint64_t n = p.g.n;
     uint32_t spins = 0;
     uint64_t tw = 0;
     for (;;) {
-        unsigned long long t0 = 0;
-        if (lane == 0) t0 = atomicAdd(&c->aq_head, 32ull);
-        t0 = __shfl_sync(FULL, t0, 0);
-        if (t0 >= n) {  // no position left to wait for: wait for the cascade to end
-            while (aq_pending(c) != 0 && !aq_stuck(c, spins, tw)) __nanosleep(64);
-            return;
-        }
-        const unsigned long long t = t0 + lane;
-        bool pend = t < n;  // my ticket still has to be processed (tickets past n never fill)
-        for (;;) {
-            uint32_t v = INF;
-            if (pend) v = vload(p.q + t);
-            const bool got = v != INF;
-            const uint32_t gm = __ballot_sync(FULL, got);
-            if (gm) {
-                uint64_t beg = 0, end = 0;
-                if (got) {
-                    beg = __ldg(p.g.rp + v);
-                    end = __ldg(p.g.rp + v + 1);
-                }
-                const bool small = got && end - beg < p.s.sep_small;
-                if (small) remove_edges(beg, end, 0ull, 1ull);
-                for (uint32_t big = __ballot_sync(FULL, got && !small); big; big &= big - 1) {
-                    const int l = __ffs(big) - 1;
-                    remove_edges(__shfl_sync(FULL, beg, l), __shfl_sync(FULL, end, l), (uint64_t)lane, 32ull);
-                }
-                __syncwarp();
-                if (got) {
-                    ++entries;
-                    __threadfence();
-                    atomicAdd(&c->aq_tp, (unsigned long long)(-(long long)AQ_ONE));  // done with v
-                    pend = false;
-                }
+        // one ticket (queue position) per warp; the item is processed by the whole warp
+        unsigned long long t = 0;
+        if (lane == 0) t = atomicAdd(&c->aq_head, 1ull);
+        t = __shfl_sync(FULL, t, 0);
+        unsigned long long it = AQ_EMPTY;
+        if (lane == 0) {
+            for (;;) {
+                if (t < p.qcap && (it = vload(p.q + t)) != AQ_EMPTY) break;
+                // the cascade is over when nothing is pending: this position stays empty
+                if (aq_pending(c) == 0 || aq_stuck(c, spins, tw)) break;
+                __nanosleep(64);
             }
-            if (!__any_sync(FULL, pend)) break;  // every ticket of the batch processed: next batch
-            if (aq_pending(c) == 0) return;      // the cascade is over (unfilled tickets stay unfilled)
-            if (aq_stuck(c, spins, tw)) return;
-            __nanosleep(32);
+        }
+        it = __shfl_sync(FULL, it, 0);
+        if (it == AQ_EMPTY) return;
+        // item = (v, piece): piece 0 = a removal; k > 0 = edges [(k-1) P, k P) of v's row
+        const uint32_t v = (uint32_t)(it >> 32), pc = (uint32_t)it;
+        uint64_t beg = __ldg(p.g.rp + v), end = __ldg(p.g.rp + v + 1);
+        if (pc > 0) {
+            beg += (uint64_t)(pc - 1) * AQ_PIECE;
+            end = min(end, beg + AQ_PIECE);
+        } else if (end - beg > AQ_PIECE) {
+            // a long row: its pieces become items, spread over the waiting warps
+            const uint32_t np = (uint32_t)((end - beg + AQ_PIECE - 1) / AQ_PIECE);
+            unsigned long long tp = 0;
+            if (lane == 0) tp = atomicAdd(&c->aq_tp, (unsigned long long)np * (AQ_ONE + 1ull));
+            tp = __shfl_sync(FULL, tp, 0);
+            for (uint32_t k = lane; k < np; k += 32)
+                *(volatile unsigned long long*)(p.q + (uint32_t)tp + k) = ((unsigned long long)v << 32) | (k + 1);
+            end = beg;
+        }
+        remove_edges(beg, end, (uint64_t)lane, 32ull);
+        __syncwarp();
+        if (lane == 0) {
+            ++entries;
+            __threadfence();
+            atomicAdd(&c->aq_tp, (unsigned long long)(-(long long)AQ_ONE));  // done with this item
         }
     }
-    (void)edges;
 }
-
-__device__ __forceinline__ bool is_alive(const uint32_t* ab, uint32_t v) { return (ab[v >> 5] >> (v & 31)) & 1u; }
 
 __global__ void k_alive_init(uint32_t* ab, uint64_t n, uint64_t nwords) {
     const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
@@ -124,10 +123,17 @@ __global__ void kcore_init(KcoreP p) {
     if (threadIdx.x != 0) return;
     for (int i = 0; i < NCLS; ++i) c->cur_count[i] = 0;
     c->k = 0;
+    c->al_cnt[0] = (unsigned int)p.g.n;  // the alive list starts as every vertex (buffer 0)
+    c->al_cnt[1] = 0;
     c->iter = 0;
     c->done = 0;
     c->slotted = 0;
     c->dir = DIR_PUSH;
+}
+
+__global__ void k_iota_u32(uint32_t* a, uint64_t n) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        a[i] = (uint32_t)i;
 }
 
 __global__ void k_copy_deg(const uint32_t* deg, uint64_t n, uint32_t* res) {
@@ -163,7 +169,7 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
     grid_begin(rs.launch);
     const uint64_t n = p.g.n;
     uint32_t it = rs.iter;
-    uint32_t k = rs.k;
+    uint32_t k = rs.k & 0x7FFFFFFFu;
     uint32_t cnt[NCLS];
     uint32_t slotted = rs.slotted;
     if (slotted) {
@@ -176,6 +182,34 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
     uint32_t done = 0;
     bool level_started = it > 0 || sum4(cnt) > 0;
     uint32_t qt = (uint32_t)vload(&c->aq_tp);  // queue tail (the same in every CTA between cascades)
+    uint32_t lvl_par = rs.k >> 31;  // alive-list buffer of the next level start (kept in bit 31 of Ctl::k)
+    uint64_t aedges = 0;  // edges of the asynchronous cascades
+    // one removal's edges in the asynchronous cascade (level k): decrement the
+    // alive neighbours; the one whose residual crosses k+1 -> k is removed and enqueued
+    auto remove_edges = [&](uint64_t beg, uint64_t end, uint64_t rank, uint64_t size) {
+        const uint32_t kk = k;
+        for_edges_b(p.g.ci, beg, end, rank, size, [&](const uint32_t (&u)[4], uint32_t kn) {
+            aedges += kn;
+            uint32_t aw[4], old[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) aw[j] = j < (int)kn ? p.ab[u[j] >> 5] : 0u;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                old[j] = (j < (int)kn && ((aw[j] >> (u[j] & 31)) & 1u)) ? atomicSub(p.res + u[j], 1u) : 0u;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (j < (int)kn && old[j] == kk + 1) {
+                    // removal claimed on the alive bit: an asynchronous level's seeding pass
+                    // may see the same vertex at residual <= k at the same time
+                    const uint32_t bit = 1u << (u[j] & 31);
+                    if (!(atomicAnd(p.ab + (u[j] >> 5), ~bit) & bit)) continue;
+                    p.core[u[j]] = kk;
+                    const unsigned long long tp = atomicAdd(&c->aq_tp, AQ_ONE + 1ull);
+                    *(volatile unsigned long long*)(p.q + (uint32_t)tp) = (unsigned long long)u[j] << 32;
+                }
+            }
+        });
+    };
     for (;;) {
         IterLine* nx = &c->line[(it + 1) % 3];
         if (sum4(cnt) == 0) {
@@ -190,43 +224,66 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
             // level is k + 1 unless the minimum jumps; then the count pass is redone.
             const uint32_t kspec = p.kfix ? p.kfix - 1 : (level_started ? k + 1 : k);
             const LevelWords lw_spec{p.ab, p.res, kspec};
-            uint32_t mn = INF;
-            uint64_t alive = 0;
+            // One pass over the ALIVE LIST (compacted here into the other buffer)
+            // computes the minimum residual and the number of seeds of the
+            // speculative level kspec: after a level's cascade every alive vertex has
+            // residual > k, so the next level is k + 1 unless the minimum jumps.  The
+            // list keeps the pass proportional to the alive count (the bitmap scan
+            // it replaces walked every word and each word's bits one after another).
+            const uint32_t par = lvl_par;
+            const uint32_t na = vload(&c->al_cnt[par]);
+            const uint32_t* AL = p.al[par];
+            uint32_t* NL = p.al[par ^ 1];
+            uint32_t mn = INF, nseed = 0, nsurv = 0;
             {
-                uint64_t w0, w1;
-                ballot_chunk(p.s.nwords, w0, w1);
-                uint32_t acc[NCLS] = {0, 0, 0, 0};
-                for (uint64_t t = w0; t < w1; t += TILE_WORDS) {
-                    const uint64_t wi = t + threadIdx.x;
-                    uint32_t w = p.ab[wi];
-                    alive += __popc(w);
-                    while (w) {
-                        const int b = __ffs(w) - 1;
-                        w &= w - 1;
-                        const uint32_t v = (uint32_t)((wi << 5) + b);
-                        const uint32_t r = p.res[v];
-                        mn = min(mn, r);
-                        if (r <= kspec) acc[cls_of(__ldg(p.g.dout + v), p.s)]++;
-                    }
-                }
-                block_sum<NCLS>(acc);
-                if (threadIdx.x == 0) {
+                const uint32_t lane = lane_id();
+                constexpr int ILP = 8;
+                const uint64_t T = gthreads();
+                for (uint64_t b0 = gtid() - lane; b0 < (uint64_t)na; b0 += ILP * T) {  // warp-uniform
+                    const uint64_t i0 = b0 + lane;
+                    uint32_t v[ILP], aw[ILP], r[ILP];
 #pragma unroll
-                    for (int cc = 0; cc < NCLS; ++cc) p.s.cta_cnt[cc * MAX_GRID + blockIdx.x] = acc[cc];
+                    for (int j = 0; j < ILP; ++j) v[j] = i0 + j * T < na ? AL[i0 + j * T] : INF;
+#pragma unroll
+                    for (int j = 0; j < ILP; ++j) aw[j] = v[j] != INF ? p.ab[v[j] >> 5] : 0u;
+#pragma unroll
+                    for (int j = 0; j < ILP; ++j) r[j] = (aw[j] >> (v[j] & 31)) & 1u ? p.res[v[j]] : INF;
+#pragma unroll
+                    for (int j = 0; j < ILP; ++j) {
+                        const bool alive = r[j] != INF;
+                        mn = min(mn, r[j]);
+                        nseed += alive && r[j] <= kspec;
+                        // survivors appended warp-aggregated (order is irrelevant)
+                        const uint32_t bal = __ballot_sync(FULL, alive);
+                        uint32_t base = 0;
+                        if (lane == 0 && bal) base = atomicAdd(&c->al_cnt[par ^ 1], (unsigned int)__popc(bal));
+                        base = __shfl_sync(FULL, base, 0);
+                        if (alive) NL[base + __popc(bal & lanemask_lt())] = v[j];
+                        nsurv += alive;
+                    }
                 }
             }
             mn = block_min(mn);
+            uint64_t alive = 0;
             {
-                uint64_t a[1] = {alive};
-                block_sum<1>(a);
+                uint64_t a[2] = {nsurv, nseed};
+                block_sum<2>(a);
                 alive = a[0];
+                nseed = (uint32_t)a[1];
+            }
+            if (lead() && p.amax) {  // an asynchronous level starts with one token per CTA pending
+                c->aq_tp = ((unsigned long long)gridDim.x << 32) | (unsigned long long)qt;
+                c->aq_head = (unsigned long long)qt;
             }
             if (threadIdx.x == 0) {
                 Slot& sl = nx->s[my_slot()];
                 if (mn != INF) atomicMin(&sl.minv, mn);
                 if (alive) atomicAdd(&sl.alive, (unsigned int)alive);
+                if (nseed) atomicAdd(&sl.found, nseed);
             }
+            lvl_par ^= 1u;
             if (!grid_sync(c)) return;
+            if (lead()) c->al_cnt[par] = 0;  // read by every CTA before the barrier; the next level start appends to it
             LineSum ls;
             read_line(nx, ls);
             mn = ls.minv;
@@ -244,6 +301,58 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
                 k = max(k, mn);
             }
             level_started = true;
+            if (p.amax && p.s.fusion && k == kspec && ls.found <= p.amax) {
+                // ---- a small level entirely asynchronous: the seeds go straight into
+                // the queue (no class lists, no sub-rounds); each CTA releases its token
+                ++st.ballot;
+                if (lead()) st.scanned += 2 * ls.alive;
+                maybe_reset_line(&c->line[(it + 2) % 3]);  // the next level start's line (nx after ++it)
+                clear_bitmap(p.s.bm[(it + 2) % 3], p.s.nwords);  // the rotation a sub-round keeps
+                // the seeds: survivors of the list pass with residual <= k, each claimed
+                // on its alive bit (the queue workers of CTAs already past this pass
+                // remove vertices of this level concurrently)
+                const uint32_t* SL = p.al[lvl_par];  // the list compacted by this level start
+                const uint32_t ns = vload(&c->al_cnt[lvl_par]);
+                const uint32_t lane = lane_id();
+                for (uint64_t i = gtid(); i < (uint64_t)ns + 31; i += gthreads()) {
+                    if ((i & ~31ull) >= ns) break;  // warp-uniform
+                    bool sd = false;
+                    uint32_t v = INF;
+                    if (i < ns) {
+                        v = SL[i];
+                        if (p.res[v] <= k) {
+                            const uint32_t bit = 1u << (v & 31);
+                            sd = (atomicAnd(p.ab + (v >> 5), ~bit) & bit) != 0;
+                            if (sd) p.core[v] = k;
+                        }
+                    }
+                    const uint32_t bal = __ballot_sync(FULL, sd);
+                    if (bal) {
+                        unsigned long long base = 0;
+                        if (lane == 0) base = atomicAdd(&c->aq_tp, (unsigned long long)__popc(bal) * (AQ_ONE + 1ull));
+                        base = __shfl_sync(FULL, base, 0);
+                        if (sd)
+                            *(volatile unsigned long long*)(p.q + (uint32_t)base + __popc(bal & lanemask_lt())) =
+                                (unsigned long long)v << 32;
+                    }
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    __threadfence();
+                    atomicAdd(&c->aq_tp, (unsigned long long)(-(long long)AQ_ONE));  // this CTA's seeds are in
+                }
+                uint64_t entries = 0;
+                kcore_async(p, c, remove_edges, entries);
+                st.edges += aedges;
+                aedges = 0;
+                st.entries += entries;
+                ++st.iters;
+                if (!grid_sync(c)) return;
+                qt = (uint32_t)vload(&c->aq_tp);
+                ++it;
+                trace_put(p.s, it, DIR_PUSH, 4u, cnt, ls.found, 0, k);  // filter 4: an asynchronous level
+                continue;  // cnt stays empty: the next level start
+            }
             // ---- ballot filter selects the level's seeds; their coreness is k
             ++st.ballot;
             // the thread owning word v >> 5 in the write pass clears the seeds' alive bits
@@ -252,13 +361,8 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
                 p.ab[v >> 5] &= ~(1u << (v & 31));
             };
             const BallotOut bo{p.s.lists[it & 1], p.s.cstride, p.g.dout};
-            if (k == kspec) {  // the counts of the fused pass stand: write pass only
-                if (lead()) st.scanned += 2 * ls.alive;
-                ballot_write(lw_spec, p.s, bo, cnt, seed);
-            } else {
-                if (lead()) st.scanned += 3 * ls.alive;
-                if (!ballot_filter(LevelWords{p.ab, p.res, k}, p.s, bo, cnt, seed)) return;
-            }
+            if (lead()) st.scanned += 2 * ls.alive;
+            if (!ballot_filter(LevelWords{p.ab, p.res, k}, p.s, bo, cnt, seed)) return;
             if (!grid_sync(c)) return;
             view_contig(cnt);
             trace_put(p.s, it + 1, DIR_PUSH, 1u, cnt, sum4(cnt), 0, k);  // level start (seeds)
@@ -345,7 +449,8 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
             uint32_t off = qt;
             for (int cc = 0; cc < NCLS; ++cc) {
                 for (uint64_t i = gtid(); i < cnt[cc]; i += gthreads())
-                    *(volatile uint32_t*)(p.q + off + i) = task_at(p.s.lists[it & 1], p.s, cc, (uint32_t)i);
+                    *(volatile unsigned long long*)(p.q + off + i) =
+                        (unsigned long long)task_at(p.s.lists[it & 1], p.s, cc, (uint32_t)i) << 32;
                 off += cnt[cc];
             }
             if (lead()) {
@@ -353,30 +458,12 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
                 c->aq_head = (unsigned long long)qt;
             }
             if (!grid_sync(c)) return;
-            uint64_t edges = 0, entries = 0;
-            const uint32_t kk = k;
-            auto remove_edges = [&](uint64_t beg, uint64_t end, uint64_t rank, uint64_t size) {
-                for_edges_b(p.g.ci, beg, end, rank, size, [&](const uint32_t (&u)[4], uint32_t kn) {
-                    edges += kn;
-                    uint32_t aw[4], old[4];
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) aw[j] = j < (int)kn ? p.ab[u[j] >> 5] : 0u;
-#pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        old[j] = (j < (int)kn && ((aw[j] >> (u[j] & 31)) & 1u)) ? atomicSub(p.res + u[j], 1u) : 0u;
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        if (j < (int)kn && old[j] == kk + 1) {
-                            p.core[u[j]] = kk;
-                            atomicAnd(p.ab + (u[j] >> 5), ~(1u << (u[j] & 31)));
-                            const unsigned long long tp = atomicAdd(&c->aq_tp, AQ_ONE + 1ull);
-                            *(volatile uint32_t*)(p.q + (uint32_t)tp) = u[j];
-                        }
-                    }
-                });
-            };
-            kcore_async(p, c, remove_edges, edges, entries);
-            st.edges += edges;
+            uint64_t entries = 0;
+            maybe_reset_line(&c->line[(it + 2) % 3]);  // the next level start's line (nx after ++it)
+            clear_bitmap(p.s.bm[(it + 2) % 3], p.s.nwords);  // the rotation a sub-round keeps
+            kcore_async(p, c, remove_edges, entries);
+            st.edges += aedges;
+            aedges = 0;
             st.entries += entries;
             ++st.iters;
             if (!grid_sync(c)) return;
@@ -393,7 +480,7 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
     flush_stats(c, st, DIR_PUSH);
     if (lead()) {
         c->iter = it;
-        c->k = k;
+        c->k = k | (lvl_par << 31);
         c->done = done;
         c->slotted = slotted;
         for (int i = 0; i < NCLS; ++i) c->cur_count[i] = cnt[i];
@@ -440,13 +527,21 @@ extern "C" sx_status sx_kcore(sx_graph g, uint32_t k, const sx_opts* opts, uint3
     p.kfix = k;
     // the asynchronous cascade queue: n positions, written once each (INF = empty)
     p.amax = run.o.cluster_enter;
-    p.q = g->st[3];
-    if (p.amax) SX_CU(cudaMemsetAsync(p.q, 0xFF, g->n * 4, s));
+    p.al[0] = g->st[2];  // free during the run (st[2] is the host-output staging after it)
+    p.al[1] = g->st[3];
+    p.qcap = g->n + g->m / AQ_PIECE + 64;
+    p.q = nullptr;
+    if (p.amax) {
+        if (!g->kq && (rc = sxh::dmalloc(g->ctx, &g->kq, p.qcap * 8)) != SX_OK) return rc;
+        p.q = g->kq;
+        SX_CU(cudaMemsetAsync(p.q, 0xFF, p.qcap * 8, s));
+    }
     SX_CU(cudaMemsetAsync(p.core, 0xFF, g->n * 4, s));
     for (int i = 0; i < 3; ++i) SX_CU(cudaMemsetAsync(p.s.bm[i], 0, g->nwords * 4, s));
     const int eg = 4 * g->ctx->prop.multiProcessorCount;
     k_copy_deg<<<eg, 256, 0, s>>>(g->dout, g->n, p.res);
     k_alive_init<<<eg, 256, 0, s>>>(p.ab, g->n, g->nwords);
+    k_iota_u32<<<eg, 256, 0, s>>>(p.al[0], g->n);
     kcore_init<<<1, 32, 0, s>>>(p);
     SX_CU(cudaGetLastError());
     void* args[] = {&p};

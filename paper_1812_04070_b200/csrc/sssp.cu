@@ -155,7 +155,14 @@ __global__ void __launch_bounds__(BLOCK, SX_SSSP_PUSH_MINB) sssp_push(SsspP p) {
         uint64_t edges = 0, mdeg = 0;
         // record u for the next iteration (claimed once per iteration on the bitmap)
         auto record = [&](uint32_t u) {
-            if (!bm_test(nbm, u) && bm_claim(nbm, u)) {
+            if (p.s.force_filter == 3) {
+                // batch filter: every improvement is recorded, duplicates
+                // included (the bitmap still marks u for a ballot on overflow)
+                bm_set(nbm, u);
+                const uint32_t du = __ldg(p.g.dout + u);
+                mdeg += du;
+                online_record(nx, nlists, p.s, u, cls_of(du, p.s));
+            } else if (!bm_test(nbm, u) && bm_claim(nbm, u)) {
                 const uint32_t du = __ldg(p.g.dout + u);
                 mdeg += du;
                 online_record(nx, nlists, p.s, u, cls_of(du, p.s));
@@ -288,7 +295,7 @@ __global__ void __launch_bounds__(BLOCK, SX_SSSP_PUSH_MINB) sssp_push(SsspP p) {
             ready = 0;
             break;
         }
-        if (nf > 0 && nf <= p.s.cluster_enter && p.s.force_filter != 2 && p.s.fusion) {
+        if (nf > 0 && nf <= p.s.cluster_enter && p.s.force_filter < 2 && p.s.fusion) {
             // small frontier: continue on one thread-block cluster (frontier handed over as bm[it % 3])
             trace_put(p.s, it, DIR_PUSH, filt, ls.cnt, nf, mf, hi);
             nf_prev = (uint32_t)nf;

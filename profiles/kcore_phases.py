@@ -20,15 +20,22 @@ out = torch.empty(d.n, dtype=torch.int32, device="cuda:0")
 G.kcore(0, out=out)
 _, st, tr = G.kcore(0, out=out, trace_cap=8192)
 print(f"kcore s{scale}: ms={st['ms']:.3f} records={len(tr)} iters={st['iterations']} ballot={st['ballot_iters']}")
-lvl, sub = [], {}
+lvl, sub, alv, acas = [], {}, [], []
 for a, b in zip(tr, tr[1:]):
     dt = (b["t_ns"] - a["t_ns"]) / 1e3
     if b["filter"] == 1:
         lvl.append(dt)  # previous record -> level start done
+    elif b["filter"] == 4:
+        alv.append(dt)  # a whole level run asynchronously (level start + queue)
+    elif b["filter"] == 3:
+        acas.append(dt)  # the asynchronous rest of a level's cascade
     else:
         nf = a["n_frontier"]
         key = "<=1e2" if nf <= 100 else "<=1e4" if nf <= 10000 else "<=1e6" if nf <= 1000000 else ">1e6"
         sub.setdefault(key, []).append(dt)
 print(f"  level starts: n={len(lvl)} total={sum(lvl) / 1e3:.2f} ms mean={sum(lvl) / max(1, len(lvl)):.1f} us")
+for name, v in (("asynchronous levels", alv), ("asynchronous cascade tails", acas)):
+    if v:
+        print(f"  {name}: n={len(v)} total={sum(v) / 1e3:.2f} ms mean={sum(v) / len(v):.1f} us")
 for k, v in sorted(sub.items()):
     print(f"  sub-rounds with |F| {k}: n={len(v)} total={sum(v) / 1e3:.2f} ms mean={sum(v) / len(v):.1f} us")
