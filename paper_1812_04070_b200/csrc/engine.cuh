@@ -112,7 +112,6 @@ struct Ctl {
     // not yet fully processed); head = next ticket for the consumers
     alignas(128) unsigned long long aq_tp;
     alignas(128) unsigned long long aq_head;
-    alignas(128) unsigned int al_cnt[2];  // k-core: sizes of the two alive-list buffers (by level-start parity)
 };
 
 // Statistics of the runs enqueued without a host sync (sx_bfs_async): the

@@ -29,7 +29,6 @@ struct KcoreP {
     unsigned long long* q;  // asynchronous cascade queue: qcap items (v << 32 | piece), all ones = not yet written
     uint64_t qcap;          // positions are never reused within a run: n removals + the pieces of split rows
     uint32_t amax;   // a level's cascade goes asynchronous once a sub-round frontier has <= amax vertices (0: never)
-    uint32_t* al[2];  // the alive vertices as a list, compacted at every level start (two buffers)
 };
 
 // Asynchronous tail of a level's cascade (B200 addition; results unchanged by
@@ -123,17 +122,10 @@ __global__ void kcore_init(KcoreP p) {
     if (threadIdx.x != 0) return;
     for (int i = 0; i < NCLS; ++i) c->cur_count[i] = 0;
     c->k = 0;
-    c->al_cnt[0] = (unsigned int)p.g.n;  // the alive list starts as every vertex (buffer 0)
-    c->al_cnt[1] = 0;
     c->iter = 0;
     c->done = 0;
     c->slotted = 0;
     c->dir = DIR_PUSH;
-}
-
-__global__ void k_iota_u32(uint32_t* a, uint64_t n) {
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        a[i] = (uint32_t)i;
 }
 
 __global__ void k_copy_deg(const uint32_t* deg, uint64_t n, uint32_t* res) {
@@ -169,7 +161,7 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
     grid_begin(rs.launch);
     const uint64_t n = p.g.n;
     uint32_t it = rs.iter;
-    uint32_t k = rs.k & 0x7FFFFFFFu;
+    uint32_t k = rs.k;
     uint32_t cnt[NCLS];
     uint32_t slotted = rs.slotted;
     if (slotted) {
@@ -182,7 +174,6 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
     uint32_t done = 0;
     bool level_started = it > 0 || sum4(cnt) > 0;
     uint32_t qt = (uint32_t)vload(&c->aq_tp);  // queue tail (the same in every CTA between cascades)
-    uint32_t lvl_par = rs.k >> 31;  // alive-list buffer of the next level start (kept in bit 31 of Ctl::k)
     uint64_t aedges = 0;  // edges of the asynchronous cascades
     // one removal's edges in the asynchronous cascade (level k): decrement the
     // alive neighbours; the one whose residual crosses k+1 -> k is removed and enqueued
@@ -224,66 +215,49 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
             // level is k + 1 unless the minimum jumps; then the count pass is redone.
             const uint32_t kspec = p.kfix ? p.kfix - 1 : (level_started ? k + 1 : k);
             const LevelWords lw_spec{p.ab, p.res, kspec};
-            // One pass over the ALIVE LIST (compacted here into the other buffer)
-            // computes the minimum residual and the number of seeds of the
-            // speculative level kspec: after a level's cascade every alive vertex has
-            // residual > k, so the next level is k + 1 unless the minimum jumps.  The
-            // list keeps the pass proportional to the alive count (the bitmap scan
-            // it replaces walked every word and each word's bits one after another).
-            const uint32_t par = lvl_par;
-            const uint32_t na = vload(&c->al_cnt[par]);
-            const uint32_t* AL = p.al[par];
-            uint32_t* NL = p.al[par ^ 1];
-            uint32_t mn = INF, nseed = 0, nsurv = 0;
-            {
-                const uint32_t lane = lane_id();
-                constexpr int ILP = 8;
-                const uint64_t T = gthreads();
-                for (uint64_t b0 = gtid() - lane; b0 < (uint64_t)na; b0 += ILP * T) {  // warp-uniform
-                    const uint64_t i0 = b0 + lane;
-                    uint32_t v[ILP], aw[ILP], r[ILP];
-#pragma unroll
-                    for (int j = 0; j < ILP; ++j) v[j] = i0 + j * T < na ? AL[i0 + j * T] : INF;
-#pragma unroll
-                    for (int j = 0; j < ILP; ++j) aw[j] = v[j] != INF ? p.ab[v[j] >> 5] : 0u;
-#pragma unroll
-                    for (int j = 0; j < ILP; ++j) r[j] = (aw[j] >> (v[j] & 31)) & 1u ? p.res[v[j]] : INF;
-#pragma unroll
-                    for (int j = 0; j < ILP; ++j) {
-                        const bool alive = r[j] != INF;
-                        mn = min(mn, r[j]);
-                        nseed += alive && r[j] <= kspec;
-                        // survivors appended warp-aggregated (order is irrelevant)
-                        const uint32_t bal = __ballot_sync(FULL, alive);
-                        uint32_t base = 0;
-                        if (lane == 0 && bal) base = atomicAdd(&c->al_cnt[par ^ 1], (unsigned int)__popc(bal));
-                        base = __shfl_sync(FULL, base, 0);
-                        if (alive) NL[base + __popc(bal & lanemask_lt())] = v[j];
-                        nsurv += alive;
-                    }
-                }
-            }
-            mn = block_min(mn);
+            uint32_t mn = INF;
             uint64_t alive = 0;
             {
-                uint64_t a[2] = {nsurv, nseed};
-                block_sum<2>(a);
-                alive = a[0];
-                nseed = (uint32_t)a[1];
+                uint64_t w0, w1;
+                ballot_chunk(p.s.nwords, w0, w1);
+                uint32_t acc[NCLS] = {0, 0, 0, 0};
+                for (uint64_t t = w0; t < w1; t += TILE_WORDS) {
+                    const uint64_t wi = t + threadIdx.x;
+                    uint32_t w = p.ab[wi];
+                    alive += __popc(w);
+                    while (w) {
+                        const int b = __ffs(w) - 1;
+                        w &= w - 1;
+                        const uint32_t v = (uint32_t)((wi << 5) + b);
+                        const uint32_t r = p.res[v];
+                        mn = min(mn, r);
+                        if (r <= kspec) acc[cls_of(__ldg(p.g.dout + v), p.s)]++;
+                    }
+                }
+                block_sum<NCLS>(acc);
+                if (threadIdx.x == 0) {
+#pragma unroll
+                    for (int cc = 0; cc < NCLS; ++cc) p.s.cta_cnt[cc * MAX_GRID + blockIdx.x] = acc[cc];
+                    const uint32_t ns = acc[0] + acc[1] + acc[2] + acc[3];
+                    if (ns) atomicAdd(&nx->s[my_slot()].found, ns);
+                }
             }
             if (lead() && p.amax) {  // an asynchronous level starts with one token per CTA pending
                 c->aq_tp = ((unsigned long long)gridDim.x << 32) | (unsigned long long)qt;
                 c->aq_head = (unsigned long long)qt;
             }
+            mn = block_min(mn);
+            {
+                uint64_t a[1] = {alive};
+                block_sum<1>(a);
+                alive = a[0];
+            }
             if (threadIdx.x == 0) {
                 Slot& sl = nx->s[my_slot()];
                 if (mn != INF) atomicMin(&sl.minv, mn);
                 if (alive) atomicAdd(&sl.alive, (unsigned int)alive);
-                if (nseed) atomicAdd(&sl.found, nseed);
             }
-            lvl_par ^= 1u;
             if (!grid_sync(c)) return;
-            if (lead()) c->al_cnt[par] = 0;  // read by every CTA before the barrier; the next level start appends to it
             LineSum ls;
             read_line(nx, ls);
             mn = ls.minv;
@@ -308,32 +282,33 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
                 if (lead()) st.scanned += 2 * ls.alive;
                 maybe_reset_line(&c->line[(it + 2) % 3]);  // the next level start's line (nx after ++it)
                 clear_bitmap(p.s.bm[(it + 2) % 3], p.s.nwords);  // the rotation a sub-round keeps
-                // the seeds: survivors of the list pass with residual <= k, each claimed
-                // on its alive bit (the queue workers of CTAs already past this pass
-                // remove vertices of this level concurrently)
-                const uint32_t* SL = p.al[lvl_par];  // the list compacted by this level start
-                const uint32_t ns = vload(&c->al_cnt[lvl_par]);
+                uint64_t w0, w1;
+                ballot_chunk(p.s.nwords, w0, w1);
                 const uint32_t lane = lane_id();
-                for (uint64_t i = gtid(); i < (uint64_t)ns + 31; i += gthreads()) {
-                    if ((i & ~31ull) >= ns) break;  // warp-uniform
-                    bool sd = false;
-                    uint32_t v = INF;
-                    if (i < ns) {
-                        v = SL[i];
-                        if (p.res[v] <= k) {
-                            const uint32_t bit = 1u << (v & 31);
-                            sd = (atomicAnd(p.ab + (v >> 5), ~bit) & bit) != 0;
-                            if (sd) p.core[v] = k;
-                        }
+                for (uint64_t t = w0; t < w1; t += TILE_WORDS) {
+                    const uint64_t wi = t + threadIdx.x;
+                    uint32_t m = lw_spec.word(wi);
+                    if (m) {
+                        // claimed on the alive bits: the queue workers of CTAs already past
+                        // their seeding remove vertices of this level concurrently
+                        m &= atomicAnd(p.ab + wi, ~m);
+                        for (uint32_t x = m; x; x &= x - 1) p.core[(wi << 5) + (__ffs(x) - 1)] = k;
                     }
-                    const uint32_t bal = __ballot_sync(FULL, sd);
-                    if (bal) {
+                    const uint32_t nm = __popc(m);
+                    uint32_t incl = nm;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t y = __shfl_up_sync(FULL, incl, o);
+                        if ((int)lane >= o) incl += y;
+                    }
+                    const uint32_t tot = __shfl_sync(FULL, incl, 31);
+                    if (tot) {
                         unsigned long long base = 0;
-                        if (lane == 0) base = atomicAdd(&c->aq_tp, (unsigned long long)__popc(bal) * (AQ_ONE + 1ull));
+                        if (lane == 0) base = atomicAdd(&c->aq_tp, (unsigned long long)tot * (AQ_ONE + 1ull));
                         base = __shfl_sync(FULL, base, 0);
-                        if (sd)
-                            *(volatile unsigned long long*)(p.q + (uint32_t)base + __popc(bal & lanemask_lt())) =
-                                (unsigned long long)v << 32;
+                        uint32_t pos = (uint32_t)base + incl - nm;
+                        for (uint32_t x = m; x; x &= x - 1)
+                            *(volatile unsigned long long*)(p.q + pos++) = (unsigned long long)((wi << 5) + (__ffs(x) - 1)) << 32;
                     }
                 }
                 __syncthreads();
@@ -361,8 +336,13 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
                 p.ab[v >> 5] &= ~(1u << (v & 31));
             };
             const BallotOut bo{p.s.lists[it & 1], p.s.cstride, p.g.dout};
-            if (lead()) st.scanned += 2 * ls.alive;
-            if (!ballot_filter(LevelWords{p.ab, p.res, k}, p.s, bo, cnt, seed)) return;
+            if (k == kspec) {  // the counts of the fused pass stand: write pass only
+                if (lead()) st.scanned += 2 * ls.alive;
+                ballot_write(lw_spec, p.s, bo, cnt, seed);
+            } else {
+                if (lead()) st.scanned += 3 * ls.alive;
+                if (!ballot_filter(LevelWords{p.ab, p.res, k}, p.s, bo, cnt, seed)) return;
+            }
             if (!grid_sync(c)) return;
             view_contig(cnt);
             trace_put(p.s, it + 1, DIR_PUSH, 1u, cnt, sum4(cnt), 0, k);  // level start (seeds)
@@ -480,7 +460,7 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
     flush_stats(c, st, DIR_PUSH);
     if (lead()) {
         c->iter = it;
-        c->k = k | (lvl_par << 31);
+        c->k = k;
         c->done = done;
         c->slotted = slotted;
         for (int i = 0; i < NCLS; ++i) c->cur_count[i] = cnt[i];
@@ -527,8 +507,6 @@ extern "C" sx_status sx_kcore(sx_graph g, uint32_t k, const sx_opts* opts, uint3
     p.kfix = k;
     // the asynchronous cascade queue: n positions, written once each (INF = empty)
     p.amax = run.o.cluster_enter;
-    p.al[0] = g->st[2];  // free during the run (st[2] is the host-output staging after it)
-    p.al[1] = g->st[3];
     p.qcap = g->n + g->m / AQ_PIECE + 64;
     p.q = nullptr;
     if (p.amax) {
@@ -541,7 +519,6 @@ extern "C" sx_status sx_kcore(sx_graph g, uint32_t k, const sx_opts* opts, uint3
     const int eg = 4 * g->ctx->prop.multiProcessorCount;
     k_copy_deg<<<eg, 256, 0, s>>>(g->dout, g->n, p.res);
     k_alive_init<<<eg, 256, 0, s>>>(p.ab, g->n, g->nwords);
-    k_iota_u32<<<eg, 256, 0, s>>>(p.al[0], g->n);
     kcore_init<<<1, 32, 0, s>>>(p);
     SX_CU(cudaGetLastError());
     void* args[] = {&p};

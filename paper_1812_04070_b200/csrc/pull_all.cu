@@ -375,7 +375,7 @@ template <class Op> __global__ void __launch_bounds__(BLOCK, SX_PALL_MINB) pull_
         }
         op.cur = t & 1;
         op.last = p.eps > 0.0 || t + 1 == p.iters;  // a convergence run writes its output every iteration
-        if (p.eps > 0.0) op_set_tau(op, t == 0 ? 1e300 : last_l1 / (double)n);  // stable: change <= the mean change
+        if (p.eps > 0.0) op_set_tau(op, t == 0 ? 0.0 : last_l1 / (double)n);  // stable: change <= the mean change
         if (!Op::kStaticHub || t == 0) {
             // hub cache refresh: 8 independent id -> value chains in flight per thread
             for (uint32_t i0 = threadIdx.x; i0 < p.K; i0 += 8 * BLOCK) {
