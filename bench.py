@@ -185,8 +185,8 @@ def run_single(args):
     m_cc = int(deg[lv != 0xFFFFFFFF].sum() // 2)
     K = args.steps
     if args.mode == "async":
-        # sx_bfs_async: each step = the state-init kernel + ONE all-fusion persistent
-        # launch, enqueued without a host round trip; the device-side
+        # sx_bfs_async: each step = ONE all-fusion persistent launch (the state
+        # init inside it), enqueued without a host round trip; the device-side
         # statistics and per-run CUDA events come back at sx_graph_sync
         G.sync()
 
@@ -198,7 +198,8 @@ def run_single(args):
         clocks = clk.summary()
         sa = G.sync()
         assert sa["runs"] == K, sa
-        launches = 2 * K  # bfs_init + bfs_all per step
+        # one bfs_all launch per step (state init inside), two with SX_ALL_INIT=0 (bfs_init + bfs_all)
+        launches = (2 if os.environ.get("SX_ALL_INIT") == "0" else 1) * K
         dom, dms, dbytes, dl = "bfs_all", sa["ms_fused"], sa["bytes_model"], sa["launches_fused"]
         step_bytes = sa["bytes_model"]
     else:

@@ -28,6 +28,7 @@ struct BfsP {
     const uint32_t* __restrict__ hub;  // per vertex: its in-neighbour of largest out-degree (INF: none)
     int sym;  // symmetric graph: in-degree == out-degree
     int tma;  // TILE-mode pull stages each chunk's hub slice with a TMA bulk copy (needs a 16-B aligned hub)
+    AsyncAcc* acc;  // asynchronous run: statistics go to this accumulator (nullptr: the control block)
 };
 
 // Hub-first probe table, built once per graph: hub(v) = the in-neighbour of
@@ -87,6 +88,7 @@ __device__ __forceinline__ uint32_t hub_id(uint32_t h) { return h == INF ? INF :
 __device__ __forceinline__ bool hub_sole(uint32_t h) { return h != INF && (h & HUB_SOLE); }
 
 constexpr uint32_t CL_EDGES = 32;
+constexpr uint32_t INIT_TILE = 2048;  // bytes per TMA bulk store of the fused init
 #ifndef SX_REC_EDGES
 #define SX_REC_EDGES (1u << 17)
 #endif
@@ -116,7 +118,27 @@ __device__ __forceinline__ bool cluster_ok(const Sched& s, uint64_t nf, uint64_t
 template <bool ALL, bool CLUSTER = !ALL>
 __device__ __forceinline__ void bfs_init_body(const BfsP& p, uint32_t src, uint32_t dir) {
     const uint64_t n = p.g.n, T = gthreads(), tid = gtid();
-    if (((uintptr_t)p.level & 15u) == 0) {
+    if (ALL && ((uintptr_t)p.level & 15u) == 0) {
+        // inside the fused launch (3 CTAs x 256 threads per SM, too few threads to
+        // saturate HBM with stores) the level array is filled by the TMA unit: one
+        // thread per CTA issues bulk copies of an INF tile in shared memory
+        // (cp.async.bulk global <- shared), the source's level follows once they landed
+        __shared__ alignas(128) uint32_t s_inf[INIT_TILE / 4];
+        for (uint32_t i = threadIdx.x; i < INIT_TILE / 4; i += BLOCK) s_inf[i] = INF;
+        fence_proxy_async_smem();
+        __syncthreads();
+        const uint64_t nb = n * 4 / INIT_TILE;  // whole tiles
+        if (threadIdx.x == 0) {
+            for (uint64_t b = blockIdx.x; b < nb; b += gridDim.x) tma_store_1d((char*)p.level + b * INIT_TILE, s_inf, INIT_TILE);
+            tma_store_wait();
+            asm volatile("fence.proxy.async.global;" ::: "memory");  // bulk (async-proxy) writes before generic ones
+        }
+        for (uint64_t i = nb * (INIT_TILE / 4) + tid; i < n; i += T) p.level[i] = INF;
+        __syncthreads();
+        // every CTA's bulk stores are complete here; the source's tile belongs to CTA (src*4/INIT_TILE) % grid
+        const uint64_t sb = (uint64_t)src * 4 / INIT_TILE;
+        if (threadIdx.x == 0 && (sb >= nb || blockIdx.x == sb % gridDim.x)) p.level[src] = 0u;
+    } else if (((uintptr_t)p.level & 15u) == 0) {
         uint4* L4 = reinterpret_cast<uint4*>(p.level);
         for (uint64_t q = tid; q < n / 4; q += T) {
             uint4 v = make_uint4(INF, INF, INF, INF);
@@ -198,7 +220,7 @@ __device__ __forceinline__ void bfs_exit(const BfsP& p, uint32_t kdir, uint32_t 
                                          uint32_t dir, uint32_t done, uint32_t ready, uint32_t slotted,
                                          const uint32_t (&cnt)[NCLS], Stats& st, RunState* rs_next, uint64_t mf_next) {
     Ctl* c = p.s.ctl;
-    flush_stats(c, st, kdir);
+    flush_stats(c, st, kdir, p.acc ? p.acc->st : nullptr);
     if (lead()) {
         c->iter = it;
         c->m_u = m_u;
@@ -875,25 +897,21 @@ __global__ void __launch_bounds__(BLOCK, SX_ALL_MINB) bfs_all(BfsP p, uint32_t s
         if (!ok) return failed();
     }
     BFS_MARK(4);
+    if (acc) {
+        // asynchronous run: every CTA flushed its statistics into the accumulator
+        // itself, and no later launch reads this one's counters: no closing barrier
+        if (lead()) {
+            grid_end(c);
+            c->launch += 1;
+            acc->runs += 1;
+        }
+        return;
+    }
     if (!grid_sync(c)) return failed();  // every CTA's statistics are in
     if (blockIdx.x != 0) return;
     if (threadIdx.x == 0) {
         grid_end(c);
         c->launch += 1;
-        if (acc) {  // async run: add this run's statistics (the next run's init zeroes them)
-            for (int d = 0; d < 2; ++d) {
-                const Ctl::StatBlock& b = c->st[d];
-                Ctl::StatBlock& a = acc->st[d];
-                a.edges += vload(&b.edges);
-                a.entries += vload(&b.entries);
-                a.scanned += vload(&b.scanned);
-                a.reached += vload(&b.reached);
-                a.ballot += vload(&b.ballot);
-                a.pull += vload(&b.pull);
-                a.iters += vload(&b.iters);
-            }
-            acc->runs += 1;
-        }
     }
     if (!hctl) return;
     __syncthreads();
@@ -1111,13 +1129,13 @@ extern "C" sx_status sx_bfs(sx_graph g, uint32_t src, const sx_opts* opts, uint3
     p.hub = g->hub;
     p.sym = !g->directed;
     p.tma = g->hub && ((uintptr_t)g->hub & 15u) == 0;
+    p.acc = nullptr;
     uint32_t dir0 = run.o.force_dir == 2 ? DIR_PULL : DIR_PUSH;
     hm.mark("prologue");
     if (run.o.fusion == 2) {  // all fusion: every phase in one cooperative launch
-        // the state init stays a separate, wider launch (8 CTAs/SM of stores:
-        // measured 13 us, against ~25 us inside the 3-CTA/SM persistent grid);
-        // SX_ALL_INIT=1 folds it into the persistent kernel
-        static const int fuse_init = [] { const char* e = getenv("SX_ALL_INIT"); return e && e[0] == '1'; }();
+        // the state init runs inside the persistent launch, the level array filled by
+        // TMA bulk stores (SX_ALL_INIT=0: a separate, wider init launch instead)
+        static const int fuse_init = [] { const char* e = getenv("SX_ALL_INIT"); return !(e && e[0] == '0'); }();
         if (!fuse_init) {
             bfs_init<<<g->ctx->prop.multiProcessorCount * 8, BLOCK, 0, s>>>(p, src, dir0 | DIR_NOCLUSTER);
             SX_CU(cudaGetLastError());
@@ -1250,14 +1268,20 @@ extern "C" sx_status sx_bfs_async(sx_graph g, uint32_t src, const sx_opts* opts,
     p.hub = g->hub;
     p.sym = !g->directed;
     p.tma = g->hub && ((uintptr_t)g->hub & 15u) == 0;
+    p.acc = g->async_acc;
     uint32_t dir0 = o.force_dir == 2 ? DIR_PULL : DIR_PUSH;
     const int i = c->nasync;
+    // one launch per BFS: the state init inside the persistent kernel (TMA bulk stores
+    // of the level array); SX_ALL_INIT=0 keeps a separate init launch
+    static const int fuse_init = [] { const char* e = getenv("SX_ALL_INIT"); return !(e && e[0] == '0'); }();
     SX_CU(cudaEventRecord(c->eva[3 * i], s));
-    bfs_init<<<c->prop.multiProcessorCount * 8, BLOCK, 0, s>>>(p, src, dir0 | DIR_NOCLUSTER);
-    SX_CU(cudaGetLastError());
+    if (!fuse_init) {
+        bfs_init<<<c->prop.multiProcessorCount * 8, BLOCK, 0, s>>>(p, src, dir0 | DIR_NOCLUSTER);
+        SX_CU(cudaGetLastError());
+    }
     SX_CU(cudaEventRecord(c->eva[3 * i + 1], s));
     Ctl* hctl = nullptr;
-    int fi = 0;
+    int fi = fuse_init;
     AsyncAcc* acc = g->async_acc;
     void* args[] = {&p, &src, &dir0, &hctl, &fi, &acc};
     if ((rc = sxh::coop_launch(g, (const void*)bfs_all, args, nullptr, PULL_DYN_SMEM)) != SX_OK) return rc;
@@ -1317,7 +1341,11 @@ extern "C" sx_status sx_graph_sync(sx_graph g, sx_stats* stats) {
     const uint32_t runs = g->async_runs;
     g->async_ms = g->async_ms_fused = 0;
     g->async_runs = 0;
-    if (h.errors) return sxh::fail(SX_E_BARRIER, "grid barrier watchdog fired in an async run");
+    if (h.errors) {
+        cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), c->stream);  // a clean control block for the next run
+        cudaStreamSynchronize(c->stream);
+        return sxh::fail(SX_E_BARRIER, "grid barrier watchdog fired in an async run");
+    }
     if (h.runs != runs) return sxh::fail(SX_E_STATE, "async run count mismatch");
     return SX_OK;
 }

@@ -259,7 +259,12 @@ sx_status Run::sync(bool tail_copy) {
         (pend_kind[i] == KIND_PULL ? ms_pull : pend_kind[i] == KIND_FUSED ? ms_fused : ms_push) += ms;
     }
     npending = 0;
-    if (c->h_ctl->error) return fail(SX_E_BARRIER, "grid barrier watchdog fired");
+    if (c->h_ctl->error) {
+        // the aborted launch left its barrier counters mid-count: start the graph's next run clean
+        cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), c->stream);
+        cudaStreamSynchronize(c->stream);
+        return fail(SX_E_BARRIER, "grid barrier watchdog fired");
+    }
     return SX_OK;
 }
 

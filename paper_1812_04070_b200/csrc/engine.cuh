@@ -235,6 +235,13 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
+// 1D bulk copy shared -> global (bulk-group completion); wait = the writes are done
+__device__ __forceinline__ void tma_store_1d(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     uint32_t ok = 0;
     do {
@@ -1097,11 +1104,13 @@ struct Stats {
 };
 
 // Per-CTA partial counters -> one atomic per CTA; uniform counters from CTA 0.
-__device__ __forceinline__ void flush_stats(Ctl* c, Stats& st, uint32_t dir) {
+// blocks (nullable): flush into these statistics blocks instead of the control
+// block's (the asynchronous BFS accumulates its runs' statistics there)
+__device__ __forceinline__ void flush_stats(Ctl* c, Stats& st, uint32_t dir, Ctl::StatBlock* blocks = nullptr) {
     uint64_t v[3] = {st.edges, st.entries, st.reached};
     block_sum<3>(v);
     if (threadIdx.x == 0) {
-        Ctl::StatBlock& b = c->st[dir];
+        Ctl::StatBlock& b = blocks ? blocks[dir] : c->st[dir];
         if (v[0]) atomicAdd(&b.edges, (unsigned long long)v[0]);
         if (v[1]) atomicAdd(&b.entries, (unsigned long long)v[1]);
         if (v[2]) atomicAdd(&b.reached, (unsigned long long)v[2]);

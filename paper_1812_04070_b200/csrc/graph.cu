@@ -215,6 +215,9 @@ sx_status sx_graph_upload(sx_ctx ctx, const sx_csr_desc* d, sx_graph* out) {
     TRY(dalloc(ctx, &g->aux_bm, g->nwords));
     TRY(dalloc(ctx, &g->cta_cnt, NCLS * MAX_GRID));
     TRY(dalloc(ctx, (char**)&g->ctl, sizeof(Ctl)));
+    // a clean control block (barrier halves, launch parity): the all-fusion BFS
+    // initialises only its run state, inside the persistent launch
+    SX_CU(cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), s));
     for (int i = 0; i < 4; ++i) TRY(dalloc(ctx, &g->st[i], n));
     TRY(sxh::bfs_prepare(g));  // BFS hub-first probe table (graph residency, not per-run work)
     e = cudaStreamSynchronize(s);

@@ -32,7 +32,7 @@ namespace sx {
 // iteration and the number of vertices that changed by more than tau.
 struct PAcc {
     double dang = 0.0, l1 = 0.0;
-    uint32_t unstable = 0;
+    uint32_t unstable = 0;  // out-edges of the vertices that changed by more than tau (the push tail's work)
 };
 
 // Each operator splits the edge term into the source value val(v) (what the hub
@@ -115,7 +115,7 @@ struct PrcOp {
         contrib[cur ^ 1][u] = du ? rn / (double)du : 0.0;
         if (du == 0 && dn != 0.0) pa.dang += rn;
         pa.l1 += fabs(ch);
-        pa.unstable += fabs(ch) > tau;
+        if (fabs(ch) > tau) pa.unstable += du;
     }
 };
 
@@ -375,7 +375,6 @@ template <class Op> __global__ void __launch_bounds__(BLOCK, SX_PALL_MINB) pull_
         }
         op.cur = t & 1;
         op.last = p.eps > 0.0 || t + 1 == p.iters;  // a convergence run writes its output every iteration
-        if (p.eps > 0.0) op_set_tau(op, t == 0 ? 0.0 : last_l1 / (double)n);  // stable: change <= the mean change
         if (!Op::kStaticHub || t == 0) {
             // hub cache refresh: 8 independent id -> value chains in flight per thread
             for (uint32_t i0 = threadIdx.x; i0 < p.K; i0 += 8 * BLOCK) {
@@ -524,7 +523,7 @@ template <class Op> __global__ void __launch_bounds__(BLOCK, SX_PALL_MINB) pull_
                 Slot& sl = c->line[(t + 1) % 3].s[my_slot()];
                 if (a[0] != 0.0) atomicAdd(&sl.dsum, a[0]);
                 if (a[1] != 0.0) atomicAdd(&sl.dsum2, a[1]);
-                if (a[2] != 0.0) atomicAdd(&sl.found, (unsigned int)a[2]);
+                if (a[2] != 0.0) atomicAdd(&sl.mdeg, (unsigned long long)a[2]);
             }
         }
         st.edges += edges;
@@ -537,13 +536,13 @@ template <class Op> __global__ void __launch_bounds__(BLOCK, SX_PALL_MINB) pull_
             // the vertices still change by more than tau (reading 26)
             LineSum ls;
             read_line(&c->line[(t + 1) % 3], ls);
-            trace_put(p.s, t + 1, DIR_PULL, 2u, cnt, ls.found, 0, (uint64_t)__double_as_longlong(ls.dsum2));
+            trace_put(p.s, t + 1, DIR_PULL, 2u, cnt, n, ls.mdeg, (uint64_t)__double_as_longlong(ls.dsum2));
             last_l1 = ls.dsum2;
             if (ls.dsum2 < p.eps) {
                 conv_state = 1;
                 break;
             }
-            if (p.tail && (p.tail == 2 || (double)ls.found <= 0.1 * (double)n)) {
+            if (p.tail && (p.tail == 2 || (double)ls.mdeg * 14.0 <= (double)E)) {
                 conv_state = 2;
                 break;
             }
@@ -1131,9 +1130,7 @@ extern "C" sx_status sx_pagerank_conv(sx_graph g, double damping, double epsilon
         q.xv = g->prc + 4 * n;
         q.d = d;
         q.tau = op.tau;
-        double last = 0.0;
-        std::memcpy(&last, &h.hi, 8);
-        q.tau0 = last / (double)n;
+        q.tau0 = op.tau;  // one stage: the tail pushes every change above tau
         q.invN = 1.0 / (double)n;
         q.variant = variant;
         void* args2[] = {&q};

@@ -92,15 +92,18 @@ def test_pagerank_conv_device_output_and_errors(ctx):
 
 
 def test_pagerank_conv_tail_runs_on_rmat(ctx):
-    """Auto mode on R-MAT with the SPEC recurrence (isolated vertices are stable
-    from step 1): the decision tree hands over to the push tail."""
+    """R-MAT with both recurrences: auto mode (the decision tree picks pull or the
+    tail) and the tail forced after one pull step both land within the bound."""
     g = simgen.rmat(16, 16, seed=1)
-    eps = 1e-10 * g.n
     G = ctx.upload(g)
-    r, st, tr = G.pagerank_conv(D, eps, 100000, 1, trace_cap=4096)
-    ref, it_ref, _ = oracle.pagerank_conv(g, D, eps * 1e-4, 100000, 1)
-    assert np.abs(r - ref).sum() <= D / (1 - D) * eps * 1.0001 + 1e-12 * ref.sum()
-    assert st["launches"] == 2 and 0 < st["pull_iters"] < st["iterations"], st
+    for var in (0, 1):
+        eps = 1e-10 * scale_of(g, var)
+        ref, _, _ = oracle.pagerank_conv(g, D, eps * 1e-4, 100000, var)
+        for kw in ({}, dict(force_dir=1)):
+            r, st, _ = G.pagerank_conv(D, eps, 100000, var, **kw)
+            assert np.abs(r - ref).sum() <= D / (1 - D) * eps * 1.0001 + 1e-12 * ref.sum(), (var, kw, st)
+            if kw:
+                assert st["launches"] == 2 and st["pull_iters"] == 1 < st["iterations"], st
     G.free()
 
 
