@@ -135,17 +135,33 @@ __global__ void k_copy_deg(const uint32_t* deg, uint64_t n, uint32_t* res) {
 
 // Ballot-filter source of a level start: the alive vertices with residual <= k.
 // Word wi = alive word wi restricted to those bits (dead words cost one load).
+// The alive vertices of word wi, eight at a time: their residual loads are
+// issued together (a dense word's bits were a chain of dependent-latency loads)
+template <class Fn> __device__ __forceinline__ void for_alive_bits(const uint32_t* res, uint64_t wi, uint32_t w, Fn&& fn) {
+    while (w) {
+        int b[8];
+        uint32_t r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            b[j] = w ? __ffs(w) - 1 : -1;
+            w &= w - 1;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = b[j] >= 0 ? res[(wi << 5) + b[j]] : INF;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (b[j] >= 0) fn(b[j], r[j]);
+    }
+}
 struct LevelWords {
     const uint32_t* ab;
     const uint32_t* res;
     uint32_t k;
     __device__ __forceinline__ uint32_t word(uint64_t wi) const {
-        uint32_t w = ab[wi], m = 0;
-        for (uint32_t x = w; x;) {
-            const int b = __ffs(x) - 1;
-            x &= x - 1;
-            if (res[(wi << 5) + b] <= k) m |= 1u << b;
-        }
+        uint32_t m = 0;
+        for_alive_bits(res, wi, ab[wi], [&](int b, uint32_t r) {
+            if (r <= k) m |= 1u << b;
+        });
         return m;
     }
 };
@@ -223,16 +239,12 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
                 uint32_t acc[NCLS] = {0, 0, 0, 0};
                 for (uint64_t t = w0; t < w1; t += TILE_WORDS) {
                     const uint64_t wi = t + threadIdx.x;
-                    uint32_t w = p.ab[wi];
+                    const uint32_t w = p.ab[wi];
                     alive += __popc(w);
-                    while (w) {
-                        const int b = __ffs(w) - 1;
-                        w &= w - 1;
-                        const uint32_t v = (uint32_t)((wi << 5) + b);
-                        const uint32_t r = p.res[v];
+                    for_alive_bits(p.res, wi, w, [&](int b, uint32_t r) {
                         mn = min(mn, r);
-                        if (r <= kspec) acc[cls_of(__ldg(p.g.dout + v), p.s)]++;
-                    }
+                        if (r <= kspec) acc[cls_of(__ldg(p.g.dout + (uint32_t)((wi << 5) + b)), p.s)]++;
+                    });
                 }
                 block_sum<NCLS>(acc);
                 if (threadIdx.x == 0) {
