@@ -466,12 +466,15 @@ def run_dist(args, world, rank, local):
     D = simdx.Dist(ctx, n, world, rank, 1, nid)
     D.upload_device(0, dg)
     out = torch.empty(hi - lo, dtype=torch.int32, device=dev)
+    # --fusion 2: the device-initiated BFS (one persistent kernel per rank, exchanges
+    # over the NCCL device API); otherwise per-level host-issued collectives
+    dkw = {"fusion": 2} if args.fusion == 2 else {}
     for _ in range(args.warmup):
-        D.bfs(0, outs=[out])
+        D.bfs(0, outs=[out], **dkw)
     acc = dict(launches=0)
 
     def step():
-        _, s = D.bfs(0, outs=[out])
+        _, s = D.bfs(0, outs=[out], **dkw)
         acc["launches"] += s["launches"]
 
     dist_host.allreduce(0.0)  # barrier
@@ -486,7 +489,7 @@ def run_dist(args, world, rank, local):
     m_cc = int(dist_host.allreduce(float(deg[lv != 0xFFFFFFFF].sum()), "sum") // 2)
     m_dir = int(dist_host.allreduce(float(dg.m), "sum"))
     gteps = m_cc / (ms * 1e-3) / 1e9
-    _, st = D.bfs(0, outs=[out])
+    _, st = D.bfs(0, outs=[out], **dkw)
     # ---- e2e at N GPUs: every rank re-uploads its slice from pinned host memory
     # (sx_dist_upload replaces the slice), runs the distributed BFS into a pinned
     # host level array; max over ranks of the wall time per step
@@ -507,7 +510,7 @@ def run_dist(args, world, rank, local):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             D.upload(0, _Slice)
-            D.bfs(0, outs=[out_h])
+            D.bfs(0, outs=[out_h], **dkw)
             torch.cuda.synchronize()
             dt = dist_host.allreduce(time.perf_counter() - t0, "max")
             if i:

@@ -398,7 +398,15 @@ void sx_dist_free(sx_dist d);
 /*
  * Distributed BFS with the push/pull switch (Beamer
  * alpha/beta from opts): level_out[i] receives local rank i's owned slice
- * (v_end - v_begin entries, host or device).  Errors as sx_bfs.
+ * (v_end - v_begin entries, host or device).
+ * opts->fusion = 2 (NCCL backend only): the whole BFS is ONE
+ * persistent cooperative kernel per rank; the per-level exchange runs inside it
+ * over the NCCL device API — push marks atomically OR'ed into the owner's inbox
+ * and frontier slices stored into every rank's global bitmap through LSA
+ * pointers into a symmetric window (ncclMemAlloc + ncclCommWindowRegister),
+ * counters stored into every rank's slots, one ncclLsaBarrierSession per level
+ * step — no host round trip per level.  Needs every rank in one LSA team (one
+ * NVLink/NVSwitch domain): SX_E_NCCL otherwise.  Errors as sx_bfs.
  */
 sx_status sx_dist_bfs(sx_dist d, uint32_t src, const sx_opts* opts, uint32_t* const* level_out, sx_stats* stats);
 /* Distributed SSSP, delta-stepping as sx_sssp; dist_out[i] = local rank i's owned slice. */

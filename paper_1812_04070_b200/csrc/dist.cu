@@ -19,6 +19,7 @@
 // process on one device ("virtual ranks", for tests), the same schedule with
 // device-to-device copies standing in for the collectives.
 #include <nccl.h>
+#include <nccl_device.h>
 
 #include <cstring>
 #include <vector>
@@ -67,6 +68,16 @@ struct sx_dist_s {
     DistRank r[DIST_MAX_LOCAL];
     unsigned long long* hcnt = nullptr;  // pinned host counters [nlocal][8]
     unsigned long long* dred = nullptr;  // device allreduce buffer (8)
+    // device-initiated BFS (fusion = 2; NCCL device API): one
+    // symmetric window per rank (global frontier bitmap | push inbox | counter slots),
+    // a device communicator with one LSA barrier, and the fused kernel's control block
+    void* sym = nullptr;
+    size_t sym_bytes = 0, off_in = 0, off_cnt = 0;
+    ncclWindow_t win = nullptr;
+    ncclDevComm dcomm{};
+    bool dcomm_ok = false;
+    sx::Ctl* fctl = nullptr;
+    unsigned long long* fstats = nullptr;  // device: iterations, pull levels, edges, reached, error
 };
 
 namespace {
@@ -400,6 +411,271 @@ __global__ void k_deg_nz(const uint64_t* rp, uint64_t n, uint64_t nwl, uint32_t*
     }
 }
 
+
+// ------------------------------------------------------------------ device-initiated BFS
+// the P:773-778 persistent loop across GPUs.  Every rank
+// runs ONE cooperative kernel for the whole BFS; the per-level exchange is done
+// from inside it over the NCCL device API instead of host-issued collectives:
+//   push level: a remote target's bit is atomicOr'ed straight into its owner's
+//               inbox slice through an LSA (load/store-accessible, NVLink) pointer
+//               into the owner's symmetric window; the owner folds the inbox;
+//   pull level: every owner stores its new frontier slice into every rank's
+//               copy of the global frontier bitmap (LSA stores) before the level;
+//   counters:   each rank stores (|F'|, m_f, edges) into every rank's counter
+//               slots; every CTA of every rank sums the same P slots and takes the
+//               same Beamer decision (reading 8);
+//   barrier:    a local grid barrier, CTA 0 crosses one ncclLsaBarrierSession with
+//               the peers (release/acquire at system scope), a local grid barrier.
+// Requires every rank in one LSA team (one NVLink/NVSwitch domain).
+struct FusedBfsP {
+    RankView r;
+    uint32_t* front[2];
+    Ctl* ctl;
+    ncclDevComm dc;
+    ncclWindow_t win;
+    uint32_t* gfront;           // this rank's window: global frontier bitmap (NW words)
+    uint32_t* inbox;            // this rank's window: push marks for its slice (nwl words)
+    unsigned long long* slots;  // this rank's window: counter slots [2 parities][P ranks][4]
+    uint64_t off_in, off_cnt;
+    uint32_t P, me, src;
+    uint64_t N, m_total;
+    float alpha, beta;
+    int force_dir;
+    uint32_t max_iters;
+    unsigned long long* fstats;
+};
+
+__device__ __forceinline__ bool xsync(const FusedBfsP& p) {
+    __threadfence_system();  // this thread's peer writes precede the barrier chain
+    if (!grid_sync(p.ctl)) return false;
+    if (blockIdx.x == 0) {
+        ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), p.dc, ncclTeamTagLsa(), 0u);
+        bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+    }
+    return grid_sync(p.ctl);
+}
+
+__global__ void __launch_bounds__(BLOCK, 4) k_dist_bfs_fused(FusedBfsP p) {
+    Ctl* c = p.ctl;
+    grid_begin(c);
+    const RankView& r = p.r;
+    const uint64_t T = gthreads(), tid = gtid();
+    const uint32_t lane = lane_id();
+    const uint64_t NW = p.N ? (uint64_t)p.P * r.nwl : 0;
+    // ---- state init (inside the timed kernel, as on one GPU)
+    for (uint64_t i = tid; i < r.V; i += T) r.state[i] = INF;
+    for (uint64_t w = tid; w < r.nwl; w += T) {
+        r.visited[w] = 0;
+        p.front[0][w] = 0;
+        p.front[1][w] = 0;
+        p.inbox[w] = 0;
+    }
+    for (uint64_t w = tid; w < NW; w += T) p.gfront[w] = 0;
+    if (blockIdx.x == 0 && warp_id() == 0)
+        for (int i = 0; i < 3; ++i) reset_line_warp(&c->line[i]);
+    if (!xsync(p)) return;  // every rank's window is clean before anyone writes into it
+    if (tid == 0) {
+        p.gfront[p.src >> 5] |= 1u << (p.src & 31);
+        const uint64_t sl = (uint64_t)p.src - r.lo;
+        if (sl < r.nl) {
+            r.state[sl] = 0;
+            r.visited[sl >> 5] |= 1u << (sl & 31);
+            p.front[0][sl >> 5] |= 1u << (sl & 31);
+        }
+    }
+    if (!grid_sync(c)) return;
+    uint32_t it = 0, cur = 0, pulls = 0;
+    uint32_t dir = p.force_dir == 2 ? DIR_PULL : DIR_PUSH;
+    uint64_t m_u = p.m_total, nf_prev = 1, edges_all = 0, reached = 1;
+    for (;;) {
+        const uint32_t lvl = it + 1;
+        uint32_t* curb = p.front[cur];
+        uint32_t* nxt = p.front[cur ^ 1];
+        IterLine* nx = &c->line[(it + 1) % 3];
+        maybe_reset_line(&c->line[(it + 2) % 3]);
+        unsigned long long found = 0, mdeg = 0, edges = 0;
+        if (dir == DIR_PUSH) {
+            auto visit = [&](uint32_t u) {
+                ++edges;
+                const uint64_t q = (uint64_t)u / r.V;
+                const uint32_t bit = 1u << (u & 31);  // V is a multiple of 32: the same bit in the slice
+                if (q == p.me) {
+                    const uint64_t ul = (uint64_t)u - r.lo;
+                    if (r.visited[ul >> 5] & bit) return;
+                    if (atomicOr(r.visited + (ul >> 5), bit) & bit) return;
+                    r.state[ul] = lvl;
+                    atomicOr(nxt + (ul >> 5), bit);
+                    ++found;
+                    mdeg += __ldg(r.deg + ul);
+                } else {
+                    uint32_t* pin = (uint32_t*)ncclGetLsaPointer(p.win, p.off_in + (((uint64_t)u - q * r.V) >> 5) * 4, (int)q);
+                    atomicOr(pin, bit);
+                }
+            };
+            for (uint64_t wi = gwarp(); wi < r.nwl; wi += gwarps()) {
+                const uint32_t word = curb[wi];
+                if (!word) continue;
+                const uint64_t vl = (wi << 5) + lane;
+                const bool mine = (word >> lane) & 1u;
+                uint64_t beg = 0, end = 0;
+                if (mine) {
+                    beg = __ldg(r.rp + vl);
+                    end = __ldg(r.rp + vl + 1);
+                }
+                if (mine && end - beg < r.sep_small)
+                    for (uint64_t e = beg; e < end; ++e) visit(__ldg(r.ci + e));
+                // rows of >= DIST_PIECE edges: listed as pieces for the whole grid (below)
+                const bool split = mine && end - beg >= DIST_PIECE;
+                if (split) {
+                    const uint64_t np = (end - beg + DIST_PIECE - 1) / DIST_PIECE;
+                    const uint64_t b0 = atomicAdd(r.cnt + CNT_PIECES, (unsigned long long)np);
+                    for (uint64_t q = 0; q < np; ++q) r.pieces[b0 + q] = (vl << 32) | q;
+                }
+                for (uint32_t todo = __ballot_sync(FULL, mine && end - beg >= r.sep_small && !split); todo;
+                     todo &= todo - 1) {
+                    const int l = __ffs(todo) - 1;
+                    const uint64_t b0 = __shfl_sync(FULL, beg, l), e0 = __shfl_sync(FULL, end, l);
+                    for (uint64_t e = b0 + lane; e < e0; e += 32) visit(__ldg(r.ci + e));
+                }
+            }
+            if (!grid_sync(c)) return;
+            {
+                const uint64_t np = vload(r.cnt + CNT_PIECES);
+                for (uint64_t i = gwarp(); i < np; i += gwarps()) {  // the hub rows, one warp per piece
+                    const uint64_t item = r.pieces[i];
+                    const uint64_t vl = item >> 32, q = item & 0xFFFFFFFFull;
+                    const uint64_t b0 = __ldg(r.rp + vl) + q * DIST_PIECE;
+                    const uint64_t e0 = min(b0 + DIST_PIECE, __ldg(r.rp + vl + 1));
+                    for (uint64_t e = b0 + lane; e < e0; e += 32) visit(__ldg(r.ci + e));
+                }
+            }
+            if (!xsync(p)) return;  // every rank's marks are in the owners' inboxes
+            if (lead()) r.cnt[CNT_PIECES] = 0;  // read by every CTA before the barrier
+            for (uint64_t w = tid; w < r.nwl; w += T) {
+                uint32_t m = p.inbox[w];
+                if (!m) continue;
+                p.inbox[w] = 0;
+                m &= ~r.visited[w];
+                if (!m) continue;
+                r.visited[w] |= m;
+                nxt[w] |= m;
+                found += __popc(m);
+                for (uint32_t x = m; x; x &= x - 1) {
+                    const uint64_t ul = (w << 5) + (__ffs(x) - 1);
+                    r.state[ul] = lvl;
+                    mdeg += __ldg(r.deg + ul);
+                }
+            }
+        } else {
+            ++pulls;
+            for (uint64_t wi = gwarp(); wi < r.nwl; wi += gwarps()) {
+                const uint32_t vis = r.visited[wi];
+                const uint32_t cand = ~vis & __ldg(r.nz + wi);
+                if (!cand) continue;
+                const uint64_t vl = (wi << 5) + lane;
+                const bool mine = (cand >> lane) & 1u;
+                uint64_t beg = 0, end = 0;
+                if (mine) {
+                    beg = __ldg(r.rp + vl);
+                    end = __ldg(r.rp + vl + 1);
+                }
+                bool hit = false;
+                const bool small = mine && end - beg < r.sep_small;
+                if (small)
+                    for (uint64_t e = beg; e < end && !hit; ++e) {
+                        ++edges;
+                        hit = bm_test(p.gfront, __ldg(r.ci + e));
+                    }
+                for (uint32_t todo = __ballot_sync(FULL, mine && !small); todo; todo &= todo - 1) {
+                    const int l = __ffs(todo) - 1;
+                    const uint64_t b0 = __shfl_sync(FULL, beg, l), e0 = __shfl_sync(FULL, end, l);
+                    bool any = false;
+                    for (uint64_t b = b0; b < e0 && !any; b += 32) {
+                        const uint64_t e = b + lane;
+                        bool h = false;
+                        if (e < e0) {
+                            ++edges;
+                            h = bm_test(p.gfront, __ldg(r.ci + e));
+                        }
+                        any = __any_sync(FULL, h);
+                    }
+                    if ((int)lane == l) hit = any;
+                }
+                const uint32_t fm = __ballot_sync(FULL, hit);
+                if (hit) {
+                    r.state[vl] = lvl;
+                    mdeg += end - beg;
+                }
+                if (lane == 0 && fm) {
+                    r.visited[wi] = vis | fm;
+                    nxt[wi] = fm;
+                    found += __popc(fm);
+                }
+            }
+        }
+        {
+            uint64_t a[3] = {found, mdeg, edges};
+            block_sum<3>(a);
+            if (threadIdx.x == 0) {
+                Slot& sl = nx->s[my_slot()];
+                if (a[0]) atomicAdd(&sl.found, (unsigned int)a[0]);
+                if (a[1]) atomicAdd(&sl.mdeg, (unsigned long long)a[1]);
+                if (a[2]) atomicAdd(&sl.edges, (unsigned long long)a[2]);
+            }
+        }
+        for (uint64_t w = tid; w < r.nwl; w += T) curb[w] = 0;  // read no more this level; the next level's output
+        if (!grid_sync(c)) return;
+        LineSum ls;
+        read_line(nx, ls);
+        const uint32_t par = it & 1u;
+        if (blockIdx.x == 0 && threadIdx.x < p.P) {  // this rank's counts into every rank's slot [par][me]
+            const uint64_t off = p.off_cnt + ((uint64_t)(par * p.P + p.me) * 4) * 8;
+            unsigned long long* dst = (unsigned long long*)ncclGetLsaPointer(p.win, off, (int)threadIdx.x);
+            dst[0] = ls.found;
+            dst[1] = ls.mdeg;
+            dst[2] = ls.edges;
+        }
+        if (!xsync(p)) return;
+        uint64_t nf = 0, mf = 0, ed = 0;
+        for (uint32_t q = 0; q < p.P; ++q) {
+            const unsigned long long* sq = p.slots + (uint64_t)(par * p.P + q) * 4;
+            nf += vload(sq);
+            mf += vload(sq + 1);
+            ed += vload(sq + 2);
+        }
+        edges_all += ed;
+        reached += nf;
+        ++it;
+        m_u -= mf < m_u ? mf : m_u;
+        cur ^= 1u;
+        if (nf == 0 || (p.max_iters && it >= p.max_iters)) break;
+        if (dir == DIR_PUSH) {
+            if (p.force_dir == 2 || (p.force_dir == 0 && (double)mf > (double)m_u / p.alpha && nf > nf_prev)) dir = DIR_PULL;
+        } else {
+            if (p.force_dir == 1 || (p.force_dir == 0 && (double)nf < (double)p.N / p.beta && nf < nf_prev)) dir = DIR_PUSH;
+        }
+        nf_prev = nf;
+        if (dir == DIR_PULL) {
+            // the new frontier (front[cur] now) into every rank's global bitmap, slice me
+            const uint32_t* fr = p.front[cur];
+            for (uint64_t w = tid; w < r.nwl; w += T) {
+                const uint32_t x = fr[w];
+                for (uint32_t q = 0; q < p.P; ++q)
+                    *(uint32_t*)ncclGetLsaPointer(p.win, ((uint64_t)p.me * r.nwl + w) * 4, (int)q) = x;
+            }
+            if (!xsync(p)) return;
+        }
+    }
+    if (lead()) {
+        p.fstats[0] = it;
+        p.fstats[1] = pulls;
+        p.fstats[2] = edges_all;
+        p.fstats[3] = reached;
+        grid_end(c);
+        c->launch += 1;
+    }
+}
+
 // ------------------------------------------------------------------ host helpers
 RankView view_of(sx_dist d, int i, uint32_t cur, const sx_opts& o) {
     DistRank& k = d->r[i];
@@ -562,6 +838,108 @@ sx_status copy_owned(sx_dist d, uint32_t* const* out) {
     return SX_OK;
 }
 
+
+// Symmetric window, device communicator and control block of the fused BFS (once per dist).
+sx_status fused_prepare(sx_dist d) {
+    if (d->dcomm_ok) return SX_OK;
+    if (!d->nccl) return sxh::fail(SX_E_INVALID, "sx_dist_bfs fusion=2: needs the NCCL backend (one rank per process)");
+    const ncclTeam_t lsa = ncclTeamLsa(d->comm);
+    if (lsa.nRanks != d->P)
+        return sxh::fail(SX_E_NCCL, "sx_dist_bfs fusion=2: every rank must be in one LSA team (one NVLink domain)");
+    d->off_in = (d->NW * 4 + 127) / 128 * 128;
+    d->off_cnt = (d->off_in + d->nwl * 4 + 127) / 128 * 128;
+    d->sym_bytes = (d->off_cnt + 2 * (uint64_t)d->P * 4 * 8 + 4095) / 4096 * 4096;
+    SX_NC(ncclMemAlloc(&d->sym, d->sym_bytes));
+    SX_NC(ncclCommWindowRegister(d->comm, d->sym, d->sym_bytes, &d->win, NCCL_WIN_COLL_SYMMETRIC));
+    ncclDevCommRequirements reqs;
+    std::memset(&reqs, 0, sizeof(reqs));
+    reqs.lsaBarrierCount = 1;
+    SX_NC(ncclDevCommCreate(d->comm, &reqs, &d->dcomm));
+    d->dcomm_ok = true;
+    SX_CU(cudaMalloc(&d->fctl, sizeof(Ctl)));
+    SX_CU(cudaMemset(d->fctl, 0, sizeof(Ctl)));
+    SX_CU(cudaMalloc(&d->fstats, 8 * sizeof(unsigned long long)));
+    return SX_OK;
+}
+
+sx_status dist_bfs_fused(sx_dist d, uint32_t src, const sx_opts& o, uint32_t* const* level_out, sx_stats* stats) {
+    sx_status rc = fused_prepare(d);
+    if (rc != SX_OK) return rc;
+    sx_ctx c = d->ctx;
+    cudaStream_t s = c->stream;
+    DistRank& k = d->r[0];
+    // global edge count (allreduced once; the Beamer test needs m_u)
+    unsigned long long msum = k.ml;
+    {
+        SX_CU(cudaMemcpyAsync(d->dred, &msum, 8, cudaMemcpyHostToDevice, s));
+        SX_NC(ncclAllReduce(d->dred, d->dred, 1, ncclUint64, ncclSum, d->comm, s));
+        SX_CU(cudaMemcpyAsync(&msum, d->dred, 8, cudaMemcpyDeviceToHost, s));
+        SX_CU(cudaStreamSynchronize(s));
+    }
+    FusedBfsP p;
+    p.r = view_of(d, 0, 0, o);
+    p.front[0] = k.front[0];
+    p.front[1] = k.front[1];
+    p.ctl = d->fctl;
+    p.dc = d->dcomm;
+    p.win = d->win;
+    p.gfront = (uint32_t*)d->sym;
+    p.inbox = (uint32_t*)((char*)d->sym + d->off_in);
+    p.slots = (unsigned long long*)((char*)d->sym + d->off_cnt);
+    p.off_in = d->off_in;
+    p.off_cnt = d->off_cnt;
+    p.P = (uint32_t)d->P;
+    p.me = (uint32_t)d->rank0;
+    p.src = src;
+    p.N = d->N;
+    p.m_total = msum;
+    p.alpha = o.alpha;
+    p.beta = o.beta;
+    p.force_dir = o.force_dir;
+    p.max_iters = o.max_iters;
+    p.fstats = d->fstats;
+    int per_sm = 0;
+    SX_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dist_bfs_fused, BLOCK, 0));
+    const int grid = per_sm * c->prop.multiProcessorCount;
+    if (grid <= 0) return sxh::fail(SX_E_BARRIER, "fused dist BFS cannot be co-resident");
+    void* args[] = {&p};
+    SX_CU(cudaEventRecord(c->ev0, s));
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_dist_bfs_fused, dim3(grid), dim3(BLOCK), args, 0, s);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return sxh::cuda_fail(e, "cudaLaunchCooperativeKernel(k_dist_bfs_fused)");
+    }
+    SX_CU(cudaEventRecord(c->ev1, s));
+    unsigned long long hs[4] = {0, 0, 0, 0};
+    SX_CU(cudaMemcpyAsync(hs, d->fstats, sizeof(hs), cudaMemcpyDeviceToHost, s));
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        c->poisoned = true;
+        return sxh::cuda_fail(e, "k_dist_bfs_fused");
+    }
+    Ctl hc;
+    SX_CU(cudaMemcpy(&hc, d->fctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
+    if (hc.error) {
+        cudaMemset(d->fctl, 0, sizeof(Ctl));
+        return sxh::fail(SX_E_BARRIER, "fused dist BFS: grid barrier watchdog fired");
+    }
+    float ms = 0;
+    SX_CU(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    if (stats) {
+        std::memset(stats, 0, sizeof(*stats));
+        stats->iterations = (uint32_t)hs[0];
+        stats->pull_iters = (uint32_t)hs[1];
+        stats->edges_examined = hs[2];
+        stats->list_entries = hs[3];
+        stats->launches = 1;
+        stats->launches_fused = 1;
+        stats->ms = ms;
+        stats->ms_fused = ms;
+        stats->runs = 1;
+        stats->bytes_model = (double)hs[0] * (double)d->NW * 4.0;  // at most one frontier slice broadcast per level
+    }
+    return copy_owned(d, level_out);
+}
 }  // namespace
 
 // ====================================================================== C ABI
@@ -704,6 +1082,11 @@ void sx_dist_free(sx_dist d) {
             if (p) cudaFree(p);
     }
     if (d->hcnt) cudaFreeHost(d->hcnt);
+    if (d->dcomm_ok) ncclDevCommDestroy(d->comm, &d->dcomm);
+    if (d->win) ncclCommWindowDeregister(d->comm, d->win);
+    if (d->sym) ncclMemFree(d->sym);
+    if (d->fctl) cudaFree(d->fctl);
+    if (d->fstats) cudaFree(d->fstats);
     if (d->dred) cudaFree(d->dred);
     if (d->comm) ncclCommDestroy(d->comm);
     delete d;
@@ -715,6 +1098,7 @@ sx_status sx_dist_bfs(sx_dist d, uint32_t src, const sx_opts* opts, uint32_t* co
     if (!level_out) return sxh::fail(SX_E_INVALID, "sx_dist_bfs: NULL level_out");
     if (src >= d->N) return sxh::fail(SX_E_INVALID, "sx_dist_bfs: src >= n");
     const sx_opts o = sxh::resolve_opts(opts);
+    if (o.fusion == 2) return dist_bfs_fused(d, src, o, level_out, stats);  // device-initiated (NEXT-1)
     sx_ctx c = d->ctx;
     cudaStream_t s = c->stream;
     const int G = kgrid(d);

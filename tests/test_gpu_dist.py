@@ -127,6 +127,11 @@ def test_dist_nccl_one_rank_communicator(ctx, rmat14):
         for mode in (dict(), dict(force_dir=1), dict(force_dir=2)):
             outs, st = D.bfs(src, **mode)
             assert np.array_equal(outs[0], ref), (src, mode)
+            # the device-initiated BFS (NCCL device API: symmetric window, LSA
+            # stores and barrier inside one persistent kernel; §8(f) NEXT-1)
+            outs, st = D.bfs(src, fusion=2, **mode)
+            assert np.array_equal(outs[0], ref), ("fused", src, mode)
+            assert st["launches"] == 1 and st["iterations"] == len(oracle.level_histogram(ref))
     ref = oracle.sssp(rmat14, 0)
     for delta in (0, 1024):
         outs, _ = D.sssp(0, delta)
