@@ -47,6 +47,7 @@ struct DistRank {
     uint32_t* sendmap = nullptr;      // NW global words (push targets)
     uint32_t* recv = nullptr;         // P * nwl words (alltoall receive)
     uint64_t* pieces = nullptr;       // push: (row, piece) items of the rows split into DIST_PIECE-edge pieces
+    uint32_t* hub = nullptr;          // pull: per owned row, its neighbour of largest GLOBAL degree among the first 64 (lazy)
     uint32_t* sendbest = nullptr;     // SSSP (lazy): P * V sender-side candidate minima (INF between iterations)
     uint32_t* touched = nullptr;      // SSSP: P regions of V ids first improved this iteration, by owner
     uint32_t* tcnt = nullptr;         // SSSP: P per-owner touched counts, then P received counts
@@ -121,6 +122,7 @@ struct RankView {
     uint32_t* sendbest;
     unsigned long long* cnt;
     uint64_t* pieces;
+    const uint32_t* hub;
     uint32_t* touched;
     uint32_t* tcnt;
     uint64_t* sendbuf;
@@ -241,7 +243,16 @@ __global__ void k_bfs_pull(RankView r, uint32_t lvl) {
             beg = __ldg(r.rp + vl);
             end = __ldg(r.rp + vl + 1);
         }
+        // hub-first probe (as on one GPU): the neighbour of largest global degree is
+        // the one most likely to sit in a dense frontier — one bitmap test instead of a row walk
         bool hit = false;
+        if (mine && r.hub) {
+            const uint32_t h = __ldg(r.hub + vl);
+            if (h != INF) {
+                ++edges;
+                hit = bm_test(r.gfront, h);
+            }
+        }
         const bool small = mine && end - beg < r.sep_small;
         if (small) {
             for (uint64_t e = beg; e < end && !hit; ++e) {
@@ -249,7 +260,7 @@ __global__ void k_bfs_pull(RankView r, uint32_t lvl) {
                 hit = bm_test(r.gfront, __ldg(r.ci + e));
             }
         }
-        uint32_t todo = __ballot_sync(FULL, mine && !small);
+        uint32_t todo = __ballot_sync(FULL, mine && !small && !hit);
         while (todo) {
             const int l = __ffs(todo) - 1;
             todo &= todo - 1;
@@ -580,13 +591,20 @@ __global__ void __launch_bounds__(BLOCK, 4) k_dist_bfs_fused(FusedBfsP p) {
                     end = __ldg(r.rp + vl + 1);
                 }
                 bool hit = false;
+                if (mine && r.hub) {  // hub-first probe
+                    const uint32_t h = __ldg(r.hub + vl);
+                    if (h != INF) {
+                        ++edges;
+                        hit = bm_test(p.gfront, h);
+                    }
+                }
                 const bool small = mine && end - beg < r.sep_small;
                 if (small)
                     for (uint64_t e = beg; e < end && !hit; ++e) {
                         ++edges;
                         hit = bm_test(p.gfront, __ldg(r.ci + e));
                     }
-                for (uint32_t todo = __ballot_sync(FULL, mine && !small); todo; todo &= todo - 1) {
+                for (uint32_t todo = __ballot_sync(FULL, mine && !small && !hit); todo; todo &= todo - 1) {
                     const int l = __ffs(todo) - 1;
                     const uint64_t b0 = __shfl_sync(FULL, beg, l), e0 = __shfl_sync(FULL, end, l);
                     bool any = false;
@@ -676,6 +694,24 @@ __global__ void __launch_bounds__(BLOCK, 4) k_dist_bfs_fused(FusedBfsP p) {
     }
 }
 
+
+// Hub table of a rank's rows: the neighbour of largest global degree (gdeg: N
+// entries, allgathered once) among a row's first 64 edges; INF for an empty row.
+__global__ void k_dist_hub(const uint64_t* rp, const uint32_t* ci, uint64_t nl, const uint32_t* gdeg, uint32_t* hub) {
+    for (uint64_t v = gtid(); v < nl; v += gthreads()) {
+        const uint64_t b = rp[v], e = min(rp[v + 1], b + 64);
+        uint64_t best = 0;
+        for (uint64_t x = b; x < e; ++x) {
+            const uint32_t u = __ldg(ci + x);
+            best = max(best, ((uint64_t)(__ldg(gdeg + u) + 1u) << 32) | (uint64_t)(~u));
+        }
+        hub[v] = best ? ~(uint32_t)best : INF;
+    }
+}
+__global__ void k_deg_pad(const uint32_t* deg, uint64_t nl, uint64_t V, uint32_t* out) {
+    for (uint64_t i = gtid(); i < V; i += gthreads()) out[i] = i < nl ? deg[i] : 0u;
+}
+
 // ------------------------------------------------------------------ host helpers
 RankView view_of(sx_dist d, int i, uint32_t cur, const sx_opts& o) {
     DistRank& k = d->r[i];
@@ -699,6 +735,7 @@ RankView view_of(sx_dist d, int i, uint32_t cur, const sx_opts& o) {
     v.sendbest = k.sendbest;
     v.cnt = k.cnt;
     v.pieces = k.pieces;
+    v.hub = k.hub;
     v.touched = k.touched;
     v.tcnt = k.tcnt;
     v.sendbuf = k.sendbuf;
@@ -763,6 +800,46 @@ sx_status ex_alltoall(sx_dist d) {
                 SX_CU(cudaMemcpyAsync(d->r[i].recv + (uint64_t)q * d->nwl, d->r[q].sendmap + (uint64_t)i * d->nwl,
                                       d->nwl * 4, cudaMemcpyDeviceToDevice, s));
     }
+    return SX_OK;
+}
+
+
+// The pull's hub tables (once per upload): the global degree array is assembled
+// (allgather of the V-padded slices; device copies for virtual ranks), then each
+// rank picks its rows' hubs.
+sx_status ensure_hubs(sx_dist d) {
+    bool all = true;  // a re-upload drops its rank's table; then every table is rebuilt
+    for (int i = 0; i < d->nlocal; ++i) all &= d->r[i].hub != nullptr;
+    if (all) return SX_OK;
+    for (int i = 0; i < d->nlocal; ++i)
+        if (d->r[i].hub) {
+            cudaFree(d->r[i].hub);
+            d->r[i].hub = nullptr;
+        }
+    cudaStream_t s = d->ctx->stream;
+    const int G = kgrid(d);
+    uint32_t* gdeg = nullptr;
+    sx_status rc = dmalloc(&gdeg, d->NW * 32);
+    if (rc != SX_OK) return rc;
+    if (d->nccl) {
+        uint32_t* pad = nullptr;
+        if ((rc = dmalloc(&pad, d->V)) != SX_OK) return rc;
+        k_deg_pad<<<G, BLOCK, 0, s>>>(d->r[0].deg, d->r[0].nl, d->V, pad);
+        SX_NC(ncclAllGather(pad, gdeg, d->V, ncclUint32, d->comm, s));
+        SX_CU(cudaStreamSynchronize(s));
+        cudaFree(pad);
+    } else {
+        for (int i = 0; i < d->nlocal; ++i)
+            k_deg_pad<<<G, BLOCK, 0, s>>>(d->r[i].deg, d->r[i].nl, d->V, gdeg + (uint64_t)i * d->V);
+    }
+    for (int i = 0; i < d->nlocal; ++i) {
+        DistRank& k = d->r[i];
+        if ((rc = dmalloc(&k.hub, k.nl ? k.nl : 1)) != SX_OK) return rc;
+        k_dist_hub<<<G, BLOCK, 0, s>>>(k.rp, k.ci, k.nl, gdeg, k.hub);
+    }
+    SX_CU(cudaGetLastError());
+    SX_CU(cudaStreamSynchronize(s));
+    cudaFree(gdeg);
     return SX_OK;
 }
 
@@ -1025,7 +1102,7 @@ sx_status sx_dist_upload(sx_dist d, int local_rank, const sx_csr_desc* desc) {
     if (k.rp) {  // re-upload (a new graph on the same partition): release the previous slice and workspace
         cudaStreamSynchronize(s);
         void* ps[] = {k.rp, k.ci, k.w, k.deg, k.nz, k.state, k.visited, k.front[0], k.front[1], k.gfront, k.sendmap,
-                      k.recv, k.sendbest, k.cnt, k.pieces, k.touched, k.tcnt, k.sendbuf, k.recvbuf};
+                      k.recv, k.sendbest, k.cnt, k.pieces, k.touched, k.tcnt, k.sendbuf, k.recvbuf, k.hub};
         for (void* q : ps)
             if (q) cudaFree(q);
         const uint64_t nl = k.nl, lo = k.lo;
@@ -1077,7 +1154,7 @@ void sx_dist_free(sx_dist d) {
     for (int i = 0; i < d->nlocal; ++i) {
         DistRank& k = d->r[i];
         void* ps[] = {k.rp, k.ci, k.w, k.deg, k.nz, k.state, k.visited, k.front[0], k.front[1], k.gfront, k.sendmap,
-                      k.recv, k.sendbest, k.cnt, k.pieces, k.touched, k.tcnt, k.sendbuf, k.recvbuf};
+                      k.recv, k.sendbest, k.cnt, k.pieces, k.touched, k.tcnt, k.sendbuf, k.recvbuf, k.hub};
         for (void* p : ps)
             if (p) cudaFree(p);
     }
@@ -1098,6 +1175,7 @@ sx_status sx_dist_bfs(sx_dist d, uint32_t src, const sx_opts* opts, uint32_t* co
     if (!level_out) return sxh::fail(SX_E_INVALID, "sx_dist_bfs: NULL level_out");
     if (src >= d->N) return sxh::fail(SX_E_INVALID, "sx_dist_bfs: src >= n");
     const sx_opts o = sxh::resolve_opts(opts);
+    if ((rc = ensure_hubs(d)) != SX_OK) return rc;
     if (o.fusion == 2) return dist_bfs_fused(d, src, o, level_out, stats);  // device-initiated (NEXT-1)
     sx_ctx c = d->ctx;
     cudaStream_t s = c->stream;
