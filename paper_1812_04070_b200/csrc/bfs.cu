@@ -438,6 +438,14 @@ __global__ void __launch_bounds__(BLOCK, SX_PUSH_MINB) bfs_push(BfsP p) {
 // walked its whole row (or had one in-edge), so m_u(next) = sum of the open
 // candidates' degrees and m_f = m_u - m_u(next).
 constexpr int PROBE = SX_PROBE;
+#ifndef SX_WALK_K
+#define SX_WALK_K 1
+#endif
+constexpr int WALK_K = SX_WALK_K;
+#ifndef SX_LIST_CSZ_MAX
+#define SX_LIST_CSZ_MAX 128  // measured: 256 leaves it3 of s24 imbalanced (CTA finish spread 21 us median), 64 adds grab overhead (profiles/r2/list_csz.txt)
+#endif
+constexpr uint32_t LIST_CSZ_MAX = SX_LIST_CSZ_MAX;  // LIST-mode chunk (candidates) at most  // pull row walks at warp granularity: edges per lane per step
 #ifndef SX_HUB_ILP
 #define SX_HUB_ILP 4
 #endif
@@ -601,13 +609,22 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
                     todo &= todo - 1;
                     const uint64_t b0 = __shfl_sync(FULL, e, l), e0 = __shfl_sync(FULL, end, l);
                     bool hit = false;
-                    for (uint64_t b = b0; b < e0; b += 32) {
-                        const uint64_t x = b + lane;
-                        bool hh = false;
-                        if (x < e0) {
-                            ++edges;
-                            hh = bm_test(cur, __ldg(p.g.ici + x));
+                    // WALK_K edges per lane per step, their loads in flight together (the
+                    // tail of a level is a few long walks; fewer, wider steps shorten them)
+                    for (uint64_t b = b0; b < e0; b += 32 * WALK_K) {
+                        uint32_t u[WALK_K];
+#pragma unroll
+                        for (int k = 0; k < WALK_K; ++k) {
+                            const uint64_t x = b + k * 32 + lane;
+                            u[k] = x < e0 ? __ldg(p.g.ici + x) : INF;
                         }
+                        bool hh = false;
+#pragma unroll
+                        for (int k = 0; k < WALK_K; ++k)
+                            if (u[k] != INF) {
+                                ++edges;
+                                hh |= bm_test(cur, u[k]);
+                            }
                         if (__any_sync(FULL, hh)) {
                             hit = true;
                             break;
@@ -680,7 +697,8 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
             }
             __syncthreads();
             const uint64_t per_warp = (ncand + gwarps() - 1) / gwarps();
-            const uint32_t csz = per_warp >= 192 ? 256u : per_warp >= 96 ? 128u : per_warp >= 48 ? 64u : 32u;
+            uint32_t csz = per_warp >= 192 ? 256u : per_warp >= 96 ? 128u : per_warp >= 48 ? 64u : 32u;
+            if (csz > LIST_CSZ_MAX) csz = LIST_CSZ_MAX;
             const uint32_t nchunks = (ncand + csz - 1) / csz;
             chunk = grab_chunk(nx, nchunks, s_cur);
             while (chunk != INF) {
@@ -773,6 +791,13 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
         }
         st.edges += edges;
         st.reached += found_cnt;
+#ifdef SX_BFS_SPREAD
+        // profiling build: when each CTA finished its work of this pull level
+        // (globaltimer), per level and CTA, into the trace buffer's tail area
+        __syncthreads();
+        if (threadIdx.x == 0 && p.s.trace)
+            reinterpret_cast<uint64_t*>(p.s.trace + 32)[(it % 8) * MAX_GRID + blockIdx.x] = globaltimer();
+#endif
         {
             uint64_t v4[4] = {p.sym ? mopen : mdeg, found_cnt, cand_small, cand_warp};
             block_sum<4>(v4);

@@ -313,7 +313,11 @@ sx_status Run::end(BytesFn bytes) {
         st->runs = 1;
     }
     if (o.trace && o.trace_cap) {
+#ifdef SX_BFS_SPREAD  // profiling build: the whole buffer (per-CTA stamps live past the records)
+        const uint64_t nrec = std::min<uint64_t>(o.trace_cap, g->trace_cap);
+#else
         const uint64_t nrec = std::min<uint64_t>(std::min<uint64_t>(h.ntrace, o.trace_cap), g->trace_cap);
+#endif
         std::memset(o.trace, 0, o.trace_cap * sizeof(sx_trace_rec));
         if (nrec) {
             SX_CU(cudaMemcpyAsync(o.trace, g->trace, nrec * sizeof(TraceRec), cudaMemcpyDefault, c->stream));
