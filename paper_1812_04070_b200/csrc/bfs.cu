@@ -702,7 +702,7 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
             const uint32_t nchunks = (ncand + csz - 1) / csz;
             chunk = grab_chunk(nx, nchunks, s_cur);
             while (chunk != INF) {
-                const uint32_t chunk_n = grab_chunk(nx, nchunks, s_cur);
+                const uint32_t s_iss = s_cur, raw_n = grab_issue(nx, s_cur);  // next claim in flight
                 const uint32_t i0 = chunk * csz;
                 const uint32_t total = min(csz, ncand - i0);
                 for (uint32_t j = lane; j < total; j += 32) {
@@ -720,7 +720,7 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
                 run_cands(total, 0, nullptr, 0u);
                 __syncwarp();
                 flush_rec();
-                chunk = chunk_n;
+                chunk = grab_finish(nx, nchunks, s_cur, raw_n, s_iss);
             }
         } else {
             const uint32_t nchunks = (uint32_t)((nw + CW - 1) / CW);
@@ -749,8 +749,12 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
             chunk = grab_chunk(nx, nchunks, s_cur);
             stage_hub(chunk, 0);
             while (chunk != INF) {
-                const uint32_t chunk_n = grab_chunk(nx, nchunks, s_cur);
+#if SX_PULL_TMA
+                const uint32_t chunk_n = grab_chunk(nx, nchunks, s_cur);  // the TMA prefetch needs it now
                 stage_hub(chunk_n, buf ^ 1u);
+#else
+                const uint32_t s_iss = s_cur, raw_n = grab_issue(nx, s_cur);  // next claim in flight
+#endif
                 const uint64_t w0 = (uint64_t)chunk * CW;
                 const uint64_t wl = w0 + lane;
                 const bool mine = lane < CW && wl < nw;
@@ -786,7 +790,11 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
                     }
                     __syncwarp();
                 }
+#if SX_PULL_TMA
                 chunk = chunk_n;
+#else
+                chunk = grab_finish(nx, nchunks, s_cur, raw_n, s_iss);
+#endif
             }
         }
         st.edges += edges;

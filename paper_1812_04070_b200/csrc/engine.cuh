@@ -693,6 +693,25 @@ __device__ __forceinline__ uint32_t grab_chunk(IterLine* L, uint32_t nchunks, ui
     }
 }
 
+// The same distribution with the next chunk's claim in flight while the
+// current one is processed: grab_issue sends lane 0's atomicAdd on the current
+// range and returns the raw ticket WITHOUT consuming it (the warp does not stall
+// on the atomic's round trip); grab_finish turns it into a chunk once the
+// current chunk is done, falling back to grab_chunk (the steal path) when the
+// range is exhausted.
+__device__ __forceinline__ uint32_t grab_issue(IterLine* L, uint32_t s_cur) {
+    return lane_id() == 0 ? atomicAdd(&L->s[s_cur].tile, 1u) : 0u;
+}
+__device__ __forceinline__ uint32_t grab_finish(IterLine* L, uint32_t nchunks, uint32_t& s_cur, uint32_t raw,
+                                                uint32_t s_issued) {
+    const uint32_t per = (nchunks + NSLOT - 1) / NSLOT;
+    uint32_t ch = INF;
+    if (lane_id() == 0 && raw < per && s_issued * per + raw < nchunks) ch = s_issued * per + raw;
+    ch = __shfl_sync(FULL, ch, 0);
+    if (ch != INF) return ch;
+    return grab_chunk(L, nchunks, s_cur);
+}
+
 // ---------------------------------------------------------------- ballot filter
 // Word sources: word(wi) is called warp-collectively for wi = base + lane.
 struct BitmapWords {  // frontier bitmap
