@@ -281,6 +281,14 @@ void sx_graph_free(sx_graph g) {
     F(g->pp_tile_seg);
     F(g->pp_nzaux);
     F(g->pp_gnz);
+    F(g->pa_order);
+    F(g->pa_newid);
+    F(g->pa_irp);
+    F(g->pa_ici);
+    F(g->pa_iw);
+    F(g->pa_dout);
+    F(g->pa_din);
+    F(g->pa_rs);
     F(g->pp_gseg);
     pt.mark("free");
     delete g;

@@ -71,6 +71,16 @@ struct sx_graph_s {
     uint32_t* pp_tile_seg = nullptr;
     uint32_t* pp_nzaux = nullptr;   // per active row: the operator's per-row operand
     uint32_t bfs_last_src = 0xFFFFFFFFu, bfs_last_key = 0, bfs_last_ce = 0, bfs_last_dir0 = 0xFFFFFFFFu;  // sx_bfs start-direction cache
+    // degree-ordered view of the in-rows for the all-active pulls (lazy, pull_all.cu):
+    // vertex ids renumbered by descending out-degree, so the most-gathered values share lines
+    uint32_t* pa_order = nullptr;   // new id -> old id
+    uint32_t* pa_newid = nullptr;   // old id -> new id
+    uint64_t* pa_irp = nullptr;
+    uint32_t* pa_ici = nullptr;
+    void* pa_iw = nullptr;
+    uint32_t* pa_dout = nullptr;
+    uint32_t* pa_din = nullptr;
+    uint32_t* pa_rs = nullptr;      // row-start bitmap over the renumbered in-edges
     uint32_t* pp_gnz = nullptr;     // per graph: rows with in-degree > 0 (+ sentinel), for the frontier pulls
     uint32_t* pp_gseg = nullptr;    // per graph: tile -> index in pp_gnz of its first edge's row
     uint64_t pp_gnnz = 0, pp_gntiles = 0;
