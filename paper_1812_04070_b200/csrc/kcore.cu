@@ -190,6 +190,7 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
     uint32_t done = 0;
     bool level_started = it > 0 || sum4(cnt) > 0;
     uint32_t qt = (uint32_t)vload(&c->aq_tp);  // queue tail (the same in every CTA between cascades)
+    bool pred_async = false;  // the last level start was small: seed the next one into the queue at once
     uint64_t aedges = 0;  // edges of the asynchronous cascades
     // one removal's edges in the asynchronous cascade (level k): decrement the
     // alive neighbours; the one whose residual crosses k+1 -> k is removed and enqueued
@@ -231,20 +232,52 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
             // level is k + 1 unless the minimum jumps; then the count pass is redone.
             const uint32_t kspec = p.kfix ? p.kfix - 1 : (level_started ? k + 1 : k);
             const LevelWords lw_spec{p.ab, p.res, kspec};
+            const bool spec = pred_async && level_started && !p.kfix;
             uint32_t mn = INF;
             uint64_t alive = 0;
             {
                 uint64_t w0, w1;
                 ballot_chunk(p.s.nwords, w0, w1);
                 uint32_t acc[NCLS] = {0, 0, 0, 0};
+                const uint32_t lane = lane_id();
                 for (uint64_t t = w0; t < w1; t += TILE_WORDS) {
                     const uint64_t wi = t + threadIdx.x;
                     const uint32_t w = p.ab[wi];
                     alive += __popc(w);
+                    uint32_t m = 0;  // this word's seeds of kspec
                     for_alive_bits(p.res, wi, w, [&](int b, uint32_t r) {
                         mn = min(mn, r);
-                        if (r <= kspec) acc[cls_of(__ldg(p.g.dout + (uint32_t)((wi << 5) + b)), p.s)]++;
+                        if (r <= kspec) {
+                            m |= 1u << b;
+                            if (!spec) acc[cls_of(__ldg(p.g.dout + (uint32_t)((wi << 5) + b)), p.s)]++;
+                        }
                     });
+                    if (spec) {
+                        // speculative asynchronous level (the previous one was small): the seeds of
+                        // kspec go into the queue now — no second pass; the workers start after
+                        // the barrier (if the minimum jumped past kspec, there are none)
+                        if (m) {
+                            p.ab[wi] = w & ~m;  // this thread owns the word; no worker runs yet
+                            for (uint32_t x = m; x; x &= x - 1) p.core[(wi << 5) + (__ffs(x) - 1)] = kspec;
+                        }
+                        const uint32_t nm = __popc(m);
+                        acc[0] += nm;
+                        uint32_t incl = nm;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const uint32_t y = __shfl_up_sync(FULL, incl, o);
+                            if ((int)lane >= o) incl += y;
+                        }
+                        const uint32_t tot = __shfl_sync(FULL, incl, 31);
+                        if (tot) {
+                            unsigned long long base = 0;
+                            if (lane == 0) base = atomicAdd(&c->aq_tp, (unsigned long long)tot * (AQ_ONE + 1ull));
+                            base = __shfl_sync(FULL, base, 0);
+                            uint32_t pos = (uint32_t)base + incl - nm;
+                            for (uint32_t x = m; x; x &= x - 1)
+                                *(volatile unsigned long long*)(p.q + pos++) = (unsigned long long)((wi << 5) + (__ffs(x) - 1)) << 32;
+                        }
+                    }
                 }
                 block_sum<NCLS>(acc);
                 if (threadIdx.x == 0) {
@@ -254,10 +287,10 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
                     if (ns) atomicAdd(&nx->s[my_slot()].found, ns);
                 }
             }
-            if (lead() && p.amax) {  // an asynchronous level starts with one token per CTA pending
-                c->aq_tp = ((unsigned long long)gridDim.x << 32) | (unsigned long long)qt;
-                c->aq_head = (unsigned long long)qt;
-            }
+            // one token per CTA pending (released by the path taken after the barrier):
+            // an asynchronous level's seeding overlaps its workers (added atomically: a
+            // speculative level enqueues concurrently)
+            if (lead() && p.amax) atomicAdd(&c->aq_tp, (unsigned long long)gridDim.x << 32);
             mn = block_min(mn);
             {
                 uint64_t a[1] = {alive};
@@ -287,6 +320,30 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
                 k = max(k, mn);
             }
             level_started = true;
+            const bool was_spec = spec;
+            pred_async = p.amax && p.s.fusion && ls.found <= p.amax;
+            if (was_spec && k == kspec) {
+                // ---- the speculative asynchronous level: its seeds are already queued
+                ++st.ballot;
+                if (lead()) {
+                    st.scanned += ls.alive;
+                    atomicAdd(&c->aq_tp, (unsigned long long)(-(long long)((unsigned long long)gridDim.x << 32)));
+                }
+                maybe_reset_line(&c->line[(it + 2) % 3]);
+                clear_bitmap(p.s.bm[(it + 2) % 3], p.s.nwords);
+                uint64_t entries = 0;
+                kcore_async(p, c, remove_edges, entries);
+                st.edges += aedges;
+                aedges = 0;
+                st.entries += entries;
+                ++st.iters;
+                if (!grid_sync(c)) return;
+                qt = (uint32_t)vload(&c->aq_tp);
+                if (lead()) c->aq_head = (unsigned long long)qt;  // the next cascade's tickets start at the tail
+                ++it;
+                trace_put(p.s, it, DIR_PUSH, 4u, cnt, ls.found, 0, k);
+                continue;
+            }
             if (p.amax && p.s.fusion && k == kspec && ls.found <= p.amax) {
                 // ---- a small level entirely asynchronous: the seeds go straight into
                 // the queue (no class lists, no sub-rounds); each CTA releases its token
@@ -336,11 +393,13 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
                 ++st.iters;
                 if (!grid_sync(c)) return;
                 qt = (uint32_t)vload(&c->aq_tp);
+                if (lead()) c->aq_head = (unsigned long long)qt;  // the next cascade's tickets start at the tail
                 ++it;
                 trace_put(p.s, it, DIR_PUSH, 4u, cnt, ls.found, 0, k);  // filter 4: an asynchronous level
                 continue;  // cnt stays empty: the next level start
             }
             // ---- ballot filter selects the level's seeds; their coreness is k
+            if (lead() && p.amax) atomicAdd(&c->aq_tp, (unsigned long long)(-(long long)((unsigned long long)gridDim.x << 32)));
             ++st.ballot;
             // the thread owning word v >> 5 in the write pass clears the seeds' alive bits
             auto seed = [&](uint32_t v, uint32_t) {
@@ -460,6 +519,7 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
             ++st.iters;
             if (!grid_sync(c)) return;
             qt = (uint32_t)vload(&c->aq_tp);
+            if (lead()) c->aq_head = (unsigned long long)qt;  // the next cascade's tickets start at the tail
             for (int i = 0; i < NCLS; ++i) cnt[i] = 0;
             view_contig(cnt);
             slotted = 0;
