@@ -208,7 +208,7 @@ sx_status Run::launch(const void* fn, void** args, int kind, int smem) {
     return SX_OK;
 }
 
-sx_status Run::launch_plain(const void* fn, void** args, int grid, int block, bool pull) {
+sx_status Run::launch_plain(const void* fn, void** args, int grid, int block, bool pull, int smem) {
     sx_ctx c = g->ctx;
     if (npending == EV_POOL) {
         sx_status rc = sync();
@@ -216,8 +216,9 @@ sx_status Run::launch_plain(const void* fn, void** args, int grid, int block, bo
     }
     // cluster kernels of 16 CTAs need the non-portable size opt-in (idempotent)
     SX_CU(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    if (smem > 0) SX_CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     SX_CU(cudaEventRecord(c->evp[2 * npending], c->stream));
-    cudaError_t e = cudaLaunchKernel(fn, dim3(grid), dim3(block), args, 0, c->stream);
+    cudaError_t e = cudaLaunchKernel(fn, dim3(grid), dim3(block), args, (size_t)smem, c->stream);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return cuda_fail(e, "cudaLaunchKernel");

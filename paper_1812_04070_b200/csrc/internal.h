@@ -138,7 +138,7 @@ struct Run {
     // kind: KIND_PUSH / KIND_PULL (a direction phase), KIND_FUSED (all phases, fusion = 2).
     sx_status launch(const void* fn, void** args, int kind, int smem = 0);
     // Same for a non-cooperative launch with an explicit shape (e.g. one cluster).
-    sx_status launch_plain(const void* fn, void** args, int grid, int block, bool pull);
+    sx_status launch_plain(const void* fn, void** args, int grid, int block, bool pull, int smem = 0);
     // Read back the control block, accumulate the pending launches' times, check errors.
     // tail_copy = false: the kernel itself stored the control block's tail into the host mirror.
     sx_status sync(bool tail_copy = true);
