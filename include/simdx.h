@@ -227,8 +227,8 @@ typedef struct {
                                     synchronised by the hardware cluster barrier instead of the grid
                                     barrier; back to the full grid above 8x this size (BFS: or 256x this
                                     many out-edges).  Results unchanged.  0 = never.  Default
-                                    SX_CLUSTER_AUTO = 4096, except BFS on graphs below 2^21 vertices
-                                    where the tail measured slower (0).
+                                    SX_CLUSTER_AUTO = 4096 for SSSP / WCC / k-core, 0 for BFS (measured:
+                                    the cluster start costs Graph500-style random roots 20%).
                                     k-core: once a sub-round frontier of a level has at most this many
                                     vertices, the rest of the level's cascade runs as an asynchronous work
                                     queue (no grid barrier per sub-round; reading 28); 0 = BSP. */

@@ -970,6 +970,7 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) b
     const bool lead0 = tid == 0;
     uint32_t it = rs.iter;
     uint64_t m_u = rs.m_u;
+    uint32_t nf_prev = rs.nf_prev;
     Ctl::ClusterLine* cl = &c->cl;
     uint64_t edges = 0, entries = 0, reached = 0;
     uint32_t iters = 0, done = 0, dir = DIR_CLUSTER, nnext = 0;
@@ -1073,8 +1074,16 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) b
             done = 1;
             break;
         }
+        const bool grown = nnext > nf_prev;
+        nf_prev = nnext;
         if (nnext > 8u * p.s.cluster_enter || mf > (uint64_t)CL_EDGES * 2u * p.s.cluster_enter) {
-            dir = DIR_PUSH;  // too big for one cluster: back to the grid
+            // too big for one cluster: back to the grid, in the direction Beamer's
+            // test picks (reading 8) — a push of a frontier whose edges
+            // outweigh m_u / alpha costs milliseconds (the bottom-up pull reads the
+            // frontier bitmap this kernel kept)
+            dir = p.s.force_dir == 2 || (p.s.force_dir == 0 && (double)mf > (double)m_u / p.s.alpha && grown)
+                      ? DIR_PULL
+                      : DIR_PUSH;
             break;
         }
         ncur = nnext;

@@ -107,10 +107,13 @@ int coop_grid(sx_graph g, const void* fn, int smem) {
 
 uint32_t resolve_cluster(uint32_t ce, bool bfs, uint64_t n) {
     if (ce != SX_CLUSTER_AUTO) return ce;
-    // measured (profiles/r1/cluster_sweep.txt): the BFS cluster tail pays off on
-    // R-MAT from scale 21 up (s22 -7%, s24 -7%) and costs 1.4-2x below; the SSSP
-    // tail always pays (C2 grid 1.93x)
-    return bfs && n < (1ull << 21) ? 0u : 4096u;
+    // measured: the SSSP tail always pays (C2 grid 1.93x, profiles/r1/cluster_sweep.txt);
+    // for BFS the tail saved 7% from the s24 hub but Graph500-style random roots
+    // lose 20% (harmonic mean 387 vs 480 GTEPS, profiles/r2/bfs_roots.txt): the
+    // cluster start and its hand-over to the grid cost more than the grid
+    // barriers it saves, so BFS leaves it off by default
+    (void)n;
+    return bfs ? 0u : 4096u;
 }
 
 Sched make_sched(const sx_graph g, const sx_opts& o) {
