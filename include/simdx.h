@@ -206,7 +206,9 @@ typedef struct {
     uint32_t sep_small;          /* degree separator thread|warp; default 32 */
     uint32_t sep_large;          /* degree separator warp|CTA; default 128 */
     uint32_t sep_huge;           /* degree separator CTA|grid-split (B200 addition); default 16384 */
-    float alpha, beta;           /* push->pull when m_f > m_u/alpha, pull->push when n_f < n/beta (Beamer; reading 8); 14, 24 */
+    float alpha, beta;           /* push->pull when m_f > m_u/alpha, pull->push when n_f < n/beta (Beamer's test;
+                                    reading 8); defaults 60, 512 — measured on B200 (Beamer's CPU values 14, 24
+                                    cost Graph500-style random roots 20%) */
     int32_t force_filter;        /* 0 JIT, 1 online only, 2 ballot only, 3 batch (the baseline of
                                     P:536-545: every update recorded, duplicates kept, no claim; BFS and
                                     SSSP/WCC push; k-core removals are exactly-once, so 3 = online there) */

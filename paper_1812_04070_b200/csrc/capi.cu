@@ -85,8 +85,8 @@ sx_opts resolve_opts(const sx_opts* o) {
     if (r.sep_huge == 0) r.sep_huge = 16384;
     if (r.sep_large < r.sep_small) r.sep_large = r.sep_small;
     if (r.sep_huge < r.sep_large) r.sep_huge = r.sep_large;
-    if (!(r.alpha > 0)) r.alpha = 14.f;
-    if (!(r.beta > 0)) r.beta = 24.f;
+    if (!(r.alpha > 0)) r.alpha = 60.f;
+    if (!(r.beta > 0)) r.beta = 512.f;
     return r;
 }
 
@@ -364,8 +364,8 @@ void sx_opts_default(sx_opts* o) {
     o->sep_small = 32;
     o->sep_large = 128;
     o->sep_huge = 16384;
-    o->alpha = 14.f;
-    o->beta = 24.f;
+    o->alpha = 60.f;  // measured on B200 (profiles/r2/bfs_ab_sweep.txt); Beamer's CPU values are 14, 24
+    o->beta = 512.f;
     o->force_filter = 0;
     o->force_dir = 0;
     o->fusion = 1;
