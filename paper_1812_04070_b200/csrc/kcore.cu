@@ -44,7 +44,10 @@ struct KcoreP {
 // word counts positions (low half) and pending items (high half): an item is
 // pending from its enqueue until its own enqueues are done, so pending = 0
 // means the cascade is over.  Only AQ_WARPS warps per CTA take part.
-constexpr uint32_t AQ_WARPS = 4;
+#ifndef SX_AQ_WARPS
+#define SX_AQ_WARPS 4
+#endif
+constexpr uint32_t AQ_WARPS = SX_AQ_WARPS;
 constexpr unsigned long long AQ_ONE = 1ull << 32;
 __device__ __forceinline__ uint32_t aq_pending(const Ctl* c) { return (uint32_t)(vload(&c->aq_tp) >> 32); }
 // watchdog of the queue waits (as the grid barrier's): a lost item would leave
