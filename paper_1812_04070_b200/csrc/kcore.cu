@@ -570,7 +570,8 @@ extern "C" sx_status sx_kcore(sx_graph g, uint32_t k, const sx_opts* opts, uint3
     if (g->directed) return sxh::fail(SX_E_INVALID, "sx_kcore: k-core is defined on undirected graphs");
     if (g->n == 0) return SX_OK;
     sxh::Run run{g, sxh::resolve_opts(opts), stats};
-    run.o.cluster_enter = sxh::resolve_cluster(run.o.cluster_enter, false, g->n);
+    // asynchronous-level threshold: 16384 measured best on s24 (profiles/r2/kcore_sweep.txt)
+    if (run.o.cluster_enter == SX_CLUSTER_AUTO) run.o.cluster_enter = 16384;
     cudaStream_t s = g->ctx->stream;
     KcoreP p;
     if ((rc = run.begin()) != SX_OK) return rc;
