@@ -60,6 +60,7 @@ __device__ __forceinline__ bool aq_stuck(Ctl* c, uint32_t& spins, uint64_t& t0) 
     return vload(&c->error) != 0;
 }
 
+constexpr double KCORE_ALPHA = 4.0;  // pull a sub-round whose frontier has > m / 4 out-edges (R-MAT: never)
 constexpr uint32_t AQ_PIECE = 1024;  // a removal of a longer row is split into pieces of this many edges
 constexpr unsigned long long AQ_EMPTY = ~0ull;
 template <class Rm>
@@ -194,6 +195,7 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
     bool level_started = it > 0 || sum4(cnt) > 0;
     uint32_t qt = (uint32_t)vload(&c->aq_tp);  // queue tail (the same in every CTA between cascades)
     bool pred_async = false;  // the last level start was small: seed the next one into the queue at once
+    uint64_t mf_cur = 0;      // out-edges of the current frontier (0 after a level start: the seeds' are not summed)
     uint64_t aedges = 0;  // edges of the asynchronous cascades
     // one removal's edges in the asynchronous cascade (level k): decrement the
     // alive neighbours; the one whose residual crosses k+1 -> k is removed and enqueued
@@ -405,9 +407,11 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
             if (lead() && p.amax) atomicAdd(&c->aq_tp, (unsigned long long)(-(long long)((unsigned long long)gridDim.x << 32)));
             ++st.ballot;
             // the thread owning word v >> 5 in the write pass clears the seeds' alive bits
+            uint32_t* fbm = p.s.bm[it % 3];  // the seeds are the frontier of sub-round `it`
             auto seed = [&](uint32_t v, uint32_t) {
                 p.core[v] = k;
                 p.ab[v >> 5] &= ~(1u << (v & 31));
+                fbm[v >> 5] |= 1u << (v & 31);  // the word's single owner in the write pass
             };
             const BallotOut bo{p.s.lists[it & 1], p.s.cstride, p.g.dout};
             if (k == kspec) {  // the counts of the fused pass stand: write pass only
@@ -420,18 +424,54 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
             if (!grid_sync(c)) return;
             view_contig(cnt);
             trace_put(p.s, it + 1, DIR_PUSH, 1u, cnt, sum4(cnt), 0, k);  // level start (seeds)
+            mf_cur = 0;  // the seeds' degrees are not summed: their sub-round pushes unless forced
         }
         // ---- one sub-round: removals push -1 to alive neighbours
         maybe_reset_line(&c->line[(it + 2) % 3]);
         clear_bitmap(p.s.bm[(it + 2) % 3], p.s.nwords);
         uint32_t* nlists = p.s.lists[(it + 1) & 1];
         uint32_t* nbm = p.s.bm[(it + 1) % 3];
-        uint64_t edges = 0;
+        uint64_t edges = 0, mrec = 0;
         const uint32_t kk = k;
         auto record = [&](uint32_t u) {
             bm_set(nbm, u);
-            online_record(nx, nlists, p.s, u, cls_of(__ldg(p.g.dout + u), p.s));
+            const uint32_t du = __ldg(p.g.dout + u);
+            mrec += du;
+            online_record(nx, nlists, p.s, u, cls_of(du, p.s));
         };
+        // direction ("pull at the beginning, push in the end"; reading 8's test
+        // with m = all edges): a frontier whose out-edges exceed m / KCORE_ALPHA is
+        // pulled — every alive vertex counts its frontier neighbours and subtracts
+        // them at once (single owner, no atomics) — otherwise pushed
+        const bool pull_sub = p.s.force_dir == 2 || (p.s.force_dir == 0 && (double)mf_cur * KCORE_ALPHA > (double)p.g.m);
+        if (pull_sub) {
+            const uint32_t* F = p.s.bm[it % 3];
+            for (uint64_t wi = gtid(); wi < p.s.nwords; wi += gthreads()) {
+                const uint32_t w = p.ab[wi];
+                if (!w) continue;
+                uint32_t dead = 0;
+                for (uint32_t x = w; x; x &= x - 1) {
+                    const int b = __ffs(x) - 1;
+                    const uint32_t u = (uint32_t)((wi << 5) + b);
+                    const uint64_t beg = __ldg(p.g.rp + u), end = __ldg(p.g.rp + u + 1);
+                    uint32_t cnt_f = 0;
+                    for_edges_b(p.g.ci, beg, end, 0ull, 1ull, [&](const uint32_t (&v)[4], uint32_t kn) {
+                        edges += kn;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) cnt_f += j < (int)kn && bm_test(F, v[j]);
+                    });
+                    if (!cnt_f) continue;
+                    const uint32_t r = p.res[u], rn = r > cnt_f ? r - cnt_f : 0u;
+                    p.res[u] = rn;
+                    if (r > kk && rn <= kk) {  // crosses k+1 -> k in this sub-round: removed once
+                        p.core[u] = kk;
+                        dead |= 1u << b;
+                        record(u);
+                    }
+                }
+                if (dead) p.ab[wi] = w & ~dead;  // this thread owns the word
+            }
+        } else
         for_tasks(p.s.lists[it & 1], p.s, cnt, [&](uint32_t v, uint64_t rank, uint64_t size, uint32_t) {
             // Local chain (B200 addition, reading 12): a removal that a thread-granularity
             // task triggers is processed at once (the cascade continues within the
@@ -472,10 +512,17 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
         stage_flush(nx, nlists, p.s);
         st.edges += edges;
         if (lead()) st.entries += sum4(cnt);
+        {
+            uint64_t a[1] = {mrec};
+            block_sum<1>(a);
+            if (threadIdx.x == 0 && a[0]) atomicAdd(&nx->s[my_slot()].mdeg, (unsigned long long)a[0]);
+        }
+        if (pull_sub) ++st.pull;
         if (!grid_sync(c)) return;
         LineSum ls;
         uint32_t vcnt[NCLS];
         read_line_view(nx, p.s, ls, vcnt);
+        mf_cur = ls.mdeg;  // out-edges of the next frontier (its removals' degrees)
         const uint64_t nf = sum4(ls.cnt);
         bool overflow = false;
         for (int i = 0; i < NCLS; ++i) overflow |= ls.cntmax[i] > p.s.cap_s;

@@ -68,6 +68,9 @@ def test_tiny_bfs_sssp_kcore(ctx, name):
                 d, _, _ = G.sssp(src, delta)
                 assert np.array_equal(d, oracle.sssp(g, src)), (name, src, delta)
         core, _, _ = G.kcore(0)
+        for kw in (dict(force_dir=2, cluster_enter=0), dict(force_dir=2)):  # pull sub-rounds
+            c2, _, _ = G.kcore(0, **kw)
+            assert np.array_equal(c2, oracle.coreness(g)), (name, kw)
         assert np.array_equal(core, oracle.coreness(g)), name
         for k in (1, 2, 3, 32):
             m, _, _ = G.kcore(k)
@@ -120,7 +123,7 @@ def test_bfs_modes_rmat(ctx, rmat14, mode):
     G.free()
 
 
-SK_MODES = MODES[:6] + [dict(force_filter=3), dict(force_filter=3, cluster_enter=0), dict(force_dir=2, fusion=0), dict(local_chain=0), dict(local_chain=100000),
+SK_MODES = MODES[:6] + [dict(force_filter=3), dict(force_filter=3, cluster_enter=0), dict(force_dir=2, cluster_enter=0), dict(force_dir=2, fusion=0), dict(local_chain=0), dict(local_chain=100000),
                         dict(local_chain=3, force_filter=2), dict(cluster_enter=0), dict(cluster_enter=1 << 20)]
 
 
@@ -153,7 +156,6 @@ def test_cluster_mode_grid_and_star(ctx, ce):
 @pytest.mark.parametrize("mode", SK_MODES, ids=[str(m) for m in SK_MODES])
 def test_sssp_kcore_modes_rmat(ctx, rmat14, mode):
     G = up(ctx, rmat14)
-    m = {k: v for k, v in mode.items() if k != "force_dir"}
     for delta in (0, 64, 1024):
         d, st, _ = G.sssp(0, delta, **mode)
         assert np.array_equal(d, oracle.sssp(rmat14, 0)), (mode, delta)
@@ -161,9 +163,14 @@ def test_sssp_kcore_modes_rmat(ctx, rmat14, mode):
             assert st["pull_iters"] > 0
         if mode.get("force_dir") == 1:
             assert st["pull_iters"] == 0
-    core, _, _ = G.kcore(0, **m)
+    # k-core takes force_dir too: 2 = pull sub-rounds, 1 = push only
+    core, st, _ = G.kcore(0, **mode)
     assert np.array_equal(core, oracle.coreness(rmat14)), mode
-    mk, _, _ = G.kcore(16, **m)
+    if mode.get("force_dir") == 2 and mode.get("cluster_enter") == 0:
+        assert st["pull_iters"] > 0
+    if mode.get("force_dir") == 1:
+        assert st["pull_iters"] == 0
+    mk, _, _ = G.kcore(16, **mode)
     assert np.array_equal(mk, oracle.kcore_mask(rmat14, 16)), mode
     G.free()
 
