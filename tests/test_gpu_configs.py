@@ -86,7 +86,22 @@ def test_bench_config_bfs_rmat24(ctx, rmat24):
     G = ctx.upload(rmat24)
     out = torch.empty(rmat24.n, dtype=torch.int32, device="cuda:0")
     G.bfs(0, out=out)
-    assert np.array_equal(out.cpu().numpy().view(np.uint32), oracle.bfs(rmat24, 0))
+    ref = oracle.bfs(rmat24, 0)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), ref)
+    # the launch configuration bench.py times: sx_bfs_async back to back into the
+    # same buffer (all fusion, state init inside the launch), then one sync
+    out.fill_(-7)
+    for _ in range(4):
+        G.bfs_async(0, out)
+    st = G.sync()
+    assert st["runs"] == 4 and st["launches_fused"] == 4
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), ref)
+    # Graph500-style roots (degree >= 1) in the async path too
+    deg = np.diff(rmat24.row_ptr)
+    for r in np.random.default_rng(3).choice(np.flatnonzero(deg > 0), 3, replace=False):
+        G.bfs_async(int(r), out)
+        G.sync()
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), oracle.bfs(rmat24, int(r))), int(r)
     G.free()
 
 
