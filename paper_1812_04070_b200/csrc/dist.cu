@@ -747,12 +747,13 @@ RankView view_of(sx_dist d, int i, uint32_t cur, const sx_opts& o) {
 }
 
 // allreduce of the ranks' 8 counters: slot 3 is a min, the others sums
-sx_status reduce_counters(sx_dist d, unsigned long long (&out)[8]) {
+// need_min = false (BFS): the min slot is not reduced (one collective per level, not two)
+sx_status reduce_counters(sx_dist d, unsigned long long (&out)[8], bool need_min = true) {
     cudaStream_t s = d->ctx->stream;
     if (d->nccl) {
         DistRank& k = d->r[0];
         SX_NC(ncclAllReduce(k.cnt, d->dred, 3, ncclUint64, ncclSum, d->comm, s));
-        SX_NC(ncclAllReduce(k.cnt + 3, d->dred + 3, 1, ncclUint64, ncclMin, d->comm, s));
+        if (need_min) SX_NC(ncclAllReduce(k.cnt + 3, d->dred + 3, 1, ncclUint64, ncclMin, d->comm, s));
         SX_CU(cudaMemcpyAsync(d->hcnt, d->dred, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
         SX_CU(cudaStreamSynchronize(s));
         std::memcpy(out, d->hcnt, sizeof(out));
@@ -1251,7 +1252,7 @@ sx_status sx_dist_bfs(sx_dist d, uint32_t src, const sx_opts* opts, uint32_t* co
         }
         SX_CU(cudaGetLastError());
         unsigned long long cnt[8];
-        if ((rc = reduce_counters(d, cnt)) != SX_OK) return rc;
+        if ((rc = reduce_counters(d, cnt, false)) != SX_OK) return rc;
         const unsigned long long nf = cnt[0], mf = cnt[1];
         edges_total += cnt[2];
         reached += nf;

@@ -61,7 +61,10 @@ __device__ __forceinline__ bool aq_stuck(Ctl* c, uint32_t& spins, uint64_t& t0) 
 }
 
 constexpr double KCORE_ALPHA = 4.0;  // pull a sub-round whose frontier has > m / 4 out-edges (R-MAT: never)
-constexpr uint32_t AQ_PIECE = 1024;  // a removal of a longer row is split into pieces of this many edges
+#ifndef SX_AQ_PIECE
+#define SX_AQ_PIECE 1024
+#endif
+constexpr uint32_t AQ_PIECE = SX_AQ_PIECE;  // a removal of a longer row is split into pieces of this many edges
 constexpr unsigned long long AQ_EMPTY = ~0ull;
 template <class Rm>
 __device__ __forceinline__ void kcore_async(const KcoreP& p, Ctl* c, Rm&& remove_edges, uint64_t& entries) {
@@ -336,8 +339,15 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
                 }
                 maybe_reset_line(&c->line[(it + 2) % 3]);
                 clear_bitmap(p.s.bm[(it + 2) % 3], p.s.nwords);
+#ifdef SX_KCORE_MARKS  // profiling build: the level start is done (CTA 0)
+                trace_put(p.s, it + 1, DIR_PUSH, 5u, cnt, ls.found, 0, k);
+#endif
                 uint64_t entries = 0;
                 kcore_async(p, c, remove_edges, entries);
+#ifdef SX_KCORE_MARKS  // CTA 0's queue warps saw the cascade end
+                __syncthreads();
+                trace_put(p.s, it + 1, DIR_PUSH, 6u, cnt, entries, 0, k);
+#endif
                 st.edges += aedges;
                 aedges = 0;
                 st.entries += entries;
