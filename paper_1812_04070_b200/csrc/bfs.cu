@@ -1117,7 +1117,8 @@ using namespace sx;
 // (col); per reached vertex 4 B (level write); per iteration one frontier-bitmap
 // clear (n/8); ballot scans n/8 per scanned vertex / 8.
 // Pull (tile scan): per row visit 16 B (row_ptr pair); per examined edge 4 B (the
-// hub probe counts as one); per reached vertex 8 B (level write + out-degree);
+// hub probe counts as one); per reached vertex 4 B level write + 4 B out-degree
+// (directed graphs only: on a symmetric graph m_u needs no degree loads);
 // per iteration visited + in-degree>0 + frontier bitmaps and one bitmap clear (4 n/8).
 // the state init (level array + visited and three frontier bitmaps), counted when it
 // runs inside the fused launch whose bytes the bench's roofline divides
@@ -1125,7 +1126,8 @@ static double bfs_init_bytes(const sx_graph g) { return 4.0 * (double)g->n + 4.0
 
 static double bfs_bytes(const sx_graph g, const sxh::Counters& c) {
     const double n = (double)g->n;
-    if (c.pull > 0) return 16.0 * c.entries + 4.0 * c.edges + 8.0 * c.reached + c.pull * 4.0 * n / 8.0;
+    const double per_reached = g->directed ? 8.0 : 4.0;
+    if (c.pull > 0) return 16.0 * c.entries + 4.0 * c.edges + per_reached * c.reached + c.pull * 4.0 * n / 8.0;
     return 20.0 * c.entries + 4.0 * c.edges + 4.0 * c.reached + c.iters * n / 8.0 + c.scanned / 8.0;
 }
 

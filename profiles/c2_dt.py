@@ -8,7 +8,7 @@ torch.cuda.set_device(0)
 ctx = simdx.Context(0, torch.cuda.current_stream().cuda_stream)
 g = simgen.grid(2048, 2048, 1, 1, 255)
 G = ctx.upload(g)
-for delta in (1024,):
+for delta in (1024, 4096):
     G.sssp(0, delta)
     _, st, tr = G.sssp(0, delta, trace_cap=20000)
     t = np.array([r["t_ns"] for r in tr], dtype=np.float64)
