@@ -473,13 +473,21 @@ def run_dist(args, world, rank, local):
         D.bfs(0, outs=[out], **dkw)
     acc = dict(launches=0)
 
-    def step():
-        _, s = D.bfs(0, outs=[out], **dkw)
-        acc["launches"] += s["launches"]
+    if args.fusion == 2:
+        # device-initiated runs enqueued back to back (sx_dist_bfs_async), as the
+        # single-GPU bench's async steps: no host round trip between steps
+        def step():
+            D.bfs_async(0, [out])
+    else:
+        def step():
+            _, s = D.bfs(0, outs=[out], **dkw)
+            acc["launches"] += s["launches"]
 
     dist_host.allreduce(0.0)  # barrier
     with Clocks(local) as clk:
         ms_local = timed_loop(step, args.steps, stream)
+    if args.fusion == 2:
+        acc["launches"] = D.sync()["launches"]
     ms = dist_host.allreduce(ms_local, "max")
     lv = out.cpu().numpy().view(np.uint32)
     host_rp = np.empty(hi - lo + 1, np.uint64)
@@ -532,7 +540,8 @@ def run_dist(args, world, rank, local):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {"workload": f"BFS from vertex 0, R-MAT scale {scale} edge factor {args.ef} "
-                                   f"(2^{args.scale} vertices per GPU), 1D vertex partition over {world} GPUs, NCCL",
+                                   f"(2^{args.scale} vertices per GPU), 1D vertex partition over {world} GPUs, NCCL"
+                                   + (" device API (one persistent kernel per rank, async steps)" if args.fusion == 2 else ""),
                        "scale": scale, "edgefactor": args.ef, "n": n, "m_directed": m_dir, "m_cc": m_cc,
                        "l2": "inputs larger than L2; no flush", "parallelism": f"1d{world}"},
             "gpu_launches": acc["launches"], "clocks": clk.summary(),

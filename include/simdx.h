@@ -411,6 +411,19 @@ void sx_dist_free(sx_dist d);
  * NVLink/NVSwitch domain): SX_E_NCCL otherwise.  Errors as sx_bfs.
  */
 sx_status sx_dist_bfs(sx_dist d, uint32_t src, const sx_opts* opts, uint32_t* const* level_out, sx_stats* stats);
+/* Asynchronous device-initiated distributed BFS (the fusion = 2 run of sx_dist_bfs, the same result):
+ * enqueue this rank's ONE persistent kernel on the ctx stream and return without waiting, so
+ * back-to-back runs pay no host round trip (as sx_bfs_async on one GPU).  NCCL backend, one rank per
+ * process; level_out[0] must be DEVICE memory (the owned slice, v_end - v_begin u32), written in place
+ * and undefined until the stream reaches the run.  Every rank must enqueue the same runs.
+ * Errors: SX_E_INVALID (host or NULL level_out, src >= n, virtual ranks), SX_E_NCCL (ranks not in one
+ * LSA team); a barrier watchdog during a run is reported by the next sx_dist_sync. */
+sx_status sx_dist_bfs_async(sx_dist d, uint32_t src, const sx_opts* opts, uint32_t* const* level_out);
+/* Wait for the runs enqueued with sx_dist_bfs_async and return their statistics (stats nullable):
+ * runs, ms = device time from the first run's start to the last run's end (CUDA events), iterations /
+ * pull_iters / edges_examined / list_entries (reached vertices) of the LAST run.  Resets the count.
+ * Errors: SX_E_BARRIER (a watchdog fired), SX_E_CUDA. */
+sx_status sx_dist_sync(sx_dist d, sx_stats* stats);
 /* Distributed SSSP, delta-stepping as sx_sssp; dist_out[i] = local rank i's owned slice. */
 sx_status sx_dist_sssp(sx_dist d, uint32_t src, uint32_t delta, const sx_opts* opts, uint32_t* const* dist_out,
                        sx_stats* stats);

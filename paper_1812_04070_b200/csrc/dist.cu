@@ -21,6 +21,7 @@
 #include <nccl.h>
 #include <nccl_device.h>
 
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
@@ -78,7 +79,13 @@ struct sx_dist_s {
     ncclDevComm dcomm{};
     bool dcomm_ok = false;
     sx::Ctl* fctl = nullptr;
-    unsigned long long* fstats = nullptr;  // device: iterations, pull levels, edges, reached, error
+    unsigned long long* fstats = nullptr;  // device: iterations, pull levels, edges, reached, error; level stamps
+    unsigned long long m_total = 0;        // global directed edge count (allreduced once per upload)
+    bool m_total_ok = false;
+    int fgrid = 0;                         // the fused kernel's cooperative grid
+    // asynchronous fused runs (sx_dist_bfs_async): count, device-time events
+    uint32_t async_runs = 0;
+    cudaEvent_t aev[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -138,14 +145,29 @@ struct RankView {
 // DIST_PIECE edges that the next launch spreads over every warp of the GPU
 // (the grid split of the single-GPU engine's huge class: an R-MAT hub of 10^5-10^6
 // edges no longer sits on one warp).  Pieces are listed with one atomic per row.
-constexpr uint32_t DIST_PIECE = 1024;
+constexpr uint32_t DIST_PIECE = 256;  // 8 edges per lane: a hub row's pieces fill the GPU in one round
 constexpr int CNT_PIECES = 5;  // counter slot holding the piece count of the level
+// Word batches: a warp loads 32 consecutive words of an owned bitmap at once
+// (lane = word) and visits only the nonzero ones (ballot), instead of one
+// dependent word load per warp step — a sparse frontier costs one coalesced
+// pass over the bitmap.  f(word index, word), warp-collective.
+template <class WordFn>
+__device__ __forceinline__ void dist_for_words(const uint32_t* bits, uint64_t nwl, WordFn&& f) {
+    const uint32_t lane = lane_id();
+    const uint64_t nb = (nwl + 31) >> 5;
+    for (uint64_t bi = gwarp(); bi < nb; bi += gwarps()) {
+        const uint64_t wl = (bi << 5) + lane;
+        const uint32_t myw = wl < nwl ? bits[wl] : 0u;
+        for (uint32_t act = __ballot_sync(FULL, myw != 0); act; act &= act - 1) {
+            const int j = __ffs(act) - 1;
+            f((bi << 5) + j, __shfl_sync(FULL, myw, j));
+        }
+    }
+}
 template <class EdgeFn>
 __device__ __forceinline__ void dist_for_active(const RankView& r, const uint32_t* bits, EdgeFn&& fn) {
     const uint32_t lane = lane_id();
-    for (uint64_t wi = gwarp(); wi < r.nwl; wi += gwarps()) {
-        const uint32_t word = bits[wi];
-        if (!word) continue;  // warp-uniform
+    dist_for_words(bits, r.nwl, [&](uint64_t wi, uint32_t word) {
         const uint64_t vl = (wi << 5) + lane;
         const bool mine = (word >> lane) & 1u;
         uint64_t beg = 0, end = 0;
@@ -157,10 +179,14 @@ __device__ __forceinline__ void dist_for_active(const RankView& r, const uint32_
         const bool split = mine && end - beg >= DIST_PIECE;
         if (small)
             for (uint64_t e = beg; e < end; ++e) fn(vl, e, __ldg(r.ci + e));
-        if (split) {
-            const uint64_t np = (end - beg + DIST_PIECE - 1) / DIST_PIECE;
-            const uint64_t b0 = atomicAdd(r.cnt + CNT_PIECES, (unsigned long long)np);
-            for (uint64_t q = 0; q < np; ++q) r.pieces[b0 + q] = (vl << 32) | q;
+        for (uint32_t sp = __ballot_sync(FULL, split); sp; sp &= sp - 1) {  // the warp lists each row's pieces
+            const int l = __ffs(sp) - 1;
+            const uint64_t b0 = __shfl_sync(FULL, beg, l), e0 = __shfl_sync(FULL, end, l);
+            const uint64_t vr = (wi << 5) + l, np = (e0 - b0 + DIST_PIECE - 1) / DIST_PIECE;
+            uint64_t base = 0;
+            if (lane == 0) base = atomicAdd(r.cnt + CNT_PIECES, (unsigned long long)np);
+            base = __shfl_sync(FULL, base, 0);
+            for (uint64_t q = lane; q < np; q += 32) r.pieces[base + q] = (vr << 32) | q;
         }
         uint32_t todo = __ballot_sync(FULL, mine && !small && !split);
         while (todo) {
@@ -170,7 +196,7 @@ __device__ __forceinline__ void dist_for_active(const RankView& r, const uint32_
             const uint64_t v0 = (wi << 5) + l;
             for (uint64_t e = b0 + lane; e < e0; e += 32) fn(v0, e, __ldg(r.ci + e));
         }
-    }
+    });
 }
 // the pieces listed by dist_for_active: one warp per piece, lane-strided edges
 template <class EdgeFn> __device__ __forceinline__ void dist_for_pieces(const RankView& r, EdgeFn&& fn) {
@@ -180,7 +206,14 @@ template <class EdgeFn> __device__ __forceinline__ void dist_for_pieces(const Ra
         const uint64_t vl = it >> 32, q = it & 0xFFFFFFFFull;
         const uint64_t beg = __ldg(r.rp + vl) + q * DIST_PIECE;
         const uint64_t end = min(beg + DIST_PIECE, __ldg(r.rp + vl + 1));
-        for (uint64_t e = beg + lane_id(); e < end; e += 32) fn(vl, e, __ldg(r.ci + e));
+        for (uint64_t e = beg + lane_id(); e < end; e += 32 * 4) {  // 4 ids in flight per lane
+            uint32_t u[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) u[k] = e + 32 * k < end ? __ldg(r.ci + e + 32 * k) : INF;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (u[k] != INF) fn(vl, e + 32 * k, u[k]);
+        }
     }
 }
 
@@ -190,7 +223,9 @@ template <int PIECES> __global__ void k_bfs_push(RankView r) {
     auto fn = [&](uint64_t, uint64_t, uint32_t u) {
         ++edges;
         const uint64_t ul = (uint64_t)u - r.lo;
-        if (ul < r.nl && bm_test(r.visited, (uint32_t)ul)) return;  // owned and already visited
+        // owned and already visited (read-only during the push: the non-coherent path
+        // lets the loads of several edges issue ahead of the marks)
+        if (ul < r.nl && ((__ldg(r.visited + (ul >> 5)) >> (ul & 31)) & 1u)) return;
         bm_set(r.sendmap, u);
     };
     if (PIECES) dist_for_pieces(r, fn);
@@ -228,71 +263,145 @@ __global__ void k_bfs_apply(RankView r, uint32_t lvl) {
     }
 }
 
-// bottom-up over owned unvisited candidates against the allgathered frontier
-__global__ void k_bfs_pull(RankView r, uint32_t lvl) {
+// Bottom-up over the owned unvisited candidates against a global frontier
+// bitmap, the single-GPU pull's TILE scheme (bfs.cu) on a rank's slice: a warp
+// takes a batch of 32 owned words (1024 vertices, lane = word), compacts the
+// candidates (unvisited, in-degree > 0) into shared memory in vertex order,
+// probes each one's hub entry first (DP_ILP rounds of 32 in flight: one hub load
+// and one frontier-bit test each; a vain probe of a sole in-edge settles the
+// vertex), then walks the rows of the candidates the hub left open — small rows
+// on the lane, 4 probes in flight, larger ones by the whole warp with the
+// voting early exit.  Found bits are merged per word in shared memory
+// and stored once by the word's lane: no global atomics.
+constexpr int DP_ILP = 4;
+constexpr uint32_t DHUB_SOLE = 0x80000000u;  // hub entry: bit 31 = the hub is the row's only edge (N <= 2^31)
+__device__ __forceinline__ uint32_t dhub_id(uint32_t h) { return h == INF ? INF : h & ~DHUB_SOLE; }
+__device__ __forceinline__ bool dhub_sole(uint32_t h) { return h != INF && (h & DHUB_SOLE); }
+// clr (nullable): owned words zeroed on the way (the fused kernel's next output buffer)
+__device__ __forceinline__ void dist_pull_batches(const RankView& r, const uint32_t* front, uint32_t* nxt, uint32_t lvl,
+                                                  unsigned long long& found, unsigned long long& mdeg,
+                                                  unsigned long long& edges, uint32_t* clr = nullptr) {
+    __shared__ uint32_t s_c[WARPS][1024];
+    __shared__ uint32_t s_f[WARPS][32];
     const uint32_t lane = lane_id();
-    unsigned long long found = 0, mdeg = 0, edges = 0;
-    for (uint64_t wi = gwarp(); wi < r.nwl; wi += gwarps()) {
-        const uint32_t vis = r.visited[wi];
-        const uint32_t cand = ~vis & __ldg(r.nz + wi);
-        if (!cand) continue;
-        const uint64_t vl = (wi << 5) + lane;
-        const bool mine = (cand >> lane) & 1u;
-        uint64_t beg = 0, end = 0;
-        if (mine) {
-            beg = __ldg(r.rp + vl);
-            end = __ldg(r.rp + vl + 1);
+    uint32_t* sc = s_c[warp_id()];
+    uint32_t* sf = s_f[warp_id()];
+    const uint64_t nb = (r.nwl + 31) >> 5;
+    for (uint64_t bi = gwarp(); bi < nb; bi += gwarps()) {
+        const uint64_t wl = (bi << 5) + lane;
+        const bool own = wl < r.nwl;
+        const uint32_t vis = own ? r.visited[wl] : FULL;
+        const uint32_t cand = own ? (~vis & __ldg(r.nz + wl)) : 0u;
+        if (clr && own) clr[wl] = 0;
+        uint32_t incl = __popc(cand);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, incl, o);
+            if ((int)lane >= o) incl += y;
         }
-        // hub-first probe (as on one GPU): the neighbour of largest global degree is
-        // the one most likely to sit in a dense frontier — one bitmap test instead of a row walk
-        bool hit = false;
-        if (mine && r.hub) {
-            const uint32_t h = __ldg(r.hub + vl);
-            if (h != INF) {
-                ++edges;
-                hit = bm_test(r.gfront, h);
+        const uint32_t total = __shfl_sync(FULL, incl, 31);
+        if (!total) continue;  // warp-uniform
+        uint32_t pos = incl - __popc(cand);
+        for (uint32_t w = cand; w; w &= w - 1) sc[pos++] = (lane << 5) | (uint32_t)(__ffs(w) - 1);
+        sf[lane] = 0;
+        __syncwarp();
+        const uint64_t vb = bi << 10;  // first vertex of the batch
+        // phase 1: hub-first probes; the open candidates are compacted in place (stable)
+        uint32_t nopen = 0;
+        for (uint32_t r0 = 0; r0 < total; r0 += 32 * DP_ILP) {
+            uint32_t ix[DP_ILP], hx[DP_ILP], wd[DP_ILP];
+#pragma unroll
+            for (int k = 0; k < DP_ILP; ++k) {
+                const uint32_t i = r0 + 32 * k + lane;
+                ix[k] = i < total ? sc[i] : INF;
             }
-        }
-        const bool small = mine && end - beg < r.sep_small;
-        if (small) {
-            for (uint64_t e = beg; e < end && !hit; ++e) {
-                ++edges;
-                hit = bm_test(r.gfront, __ldg(r.ci + e));
+#pragma unroll
+            for (int k = 0; k < DP_ILP; ++k) hx[k] = ix[k] != INF && r.hub ? __ldg(r.hub + vb + ix[k]) : INF;
+#pragma unroll
+            for (int k = 0; k < DP_ILP; ++k) {
+                const uint32_t h = dhub_id(hx[k]);
+                wd[k] = h != INF ? front[h >> 5] : 0u;
             }
-        }
-        uint32_t todo = __ballot_sync(FULL, mine && !small && !hit);
-        while (todo) {
-            const int l = __ffs(todo) - 1;
-            todo &= todo - 1;
-            const uint64_t b0 = __shfl_sync(FULL, beg, l), e0 = __shfl_sync(FULL, end, l);
-            bool any = false;
-            for (uint64_t b = b0; b < e0; b += 32) {
-                const uint64_t e = b + lane;
-                bool h = false;
-                if (e < e0) {
-                    ++edges;
-                    h = bm_test(r.gfront, __ldg(r.ci + e));
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < DP_ILP; ++k) {
+                const uint32_t h = dhub_id(hx[k]);
+                const bool f = h != INF && ((wd[k] >> (h & 31)) & 1u);
+                edges += h != INF;
+                if (f) {
+                    const uint64_t vl = vb + ix[k];
+                    r.state[vl] = lvl;
+                    atomicOr(sf + (ix[k] >> 5), 1u << (ix[k] & 31));
+                    mdeg += __ldg(r.deg + vl);
                 }
-                if (__any_sync(FULL, h)) {
-                    any = true;
-                    break;
+                const bool open = ix[k] != INF && !f && !dhub_sole(hx[k]);
+                const uint32_t bal = __ballot_sync(FULL, open);
+                if (open) sc[nopen + __popc(bal & lanemask_lt())] = ix[k];
+                nopen += __popc(bal);
+            }
+            __syncwarp();
+        }
+        // phase 2: row walks of the open candidates
+        for (uint32_t o0 = 0; o0 < nopen; o0 += 32) {
+            const bool mine = o0 + lane < nopen;
+            const uint32_t ix = mine ? sc[o0 + lane] : 0u;
+            const uint64_t vl = vb + ix;
+            uint64_t beg = 0, end = 0;
+            if (mine) {
+                beg = __ldg(r.rp + vl);
+                end = __ldg(r.rp + vl + 1);
+            }
+            bool hit = false;
+            const bool small = mine && end - beg < r.sep_small;
+            if (small) {
+                for (uint64_t e = beg; e < end && !hit; e += 4) {
+                    uint32_t u[4], w[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) u[k] = e + k < end ? __ldg(r.ci + e + k) : INF;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) w[k] = u[k] != INF ? front[u[k] >> 5] : 0u;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (u[k] != INF) {
+                            ++edges;
+                            hit |= (w[k] >> (u[k] & 31)) & 1u;
+                        }
                 }
             }
-            if ((int)lane == l) hit = any;
-        }
-        const uint32_t fm = __ballot_sync(FULL, hit);
-        if (hit) {
-            r.state[vl] = lvl;
-            mdeg += end - beg;
-        }
-        if (lane == 0) {
-            r.nxt[wi] = fm;
-            if (fm) {
-                r.visited[wi] = vis | fm;
-                found += __popc(fm);
+            for (uint32_t todo = __ballot_sync(FULL, mine && !small); todo; todo &= todo - 1) {
+                const int l = __ffs(todo) - 1;
+                const uint64_t b0 = __shfl_sync(FULL, beg, l), e0 = __shfl_sync(FULL, end, l);
+                bool any = false;
+                for (uint64_t b = b0; b < e0 && !any; b += 32) {
+                    const uint64_t e = b + lane;
+                    bool h = false;
+                    if (e < e0) {
+                        ++edges;
+                        h = bm_test(front, __ldg(r.ci + e));
+                    }
+                    any = __any_sync(FULL, h);
+                }
+                if ((int)lane == l) hit = any;
+            }
+            if (hit) {
+                r.state[vl] = lvl;
+                atomicOr(sf + (ix >> 5), 1u << (ix & 31));
+                mdeg += end - beg;
             }
         }
+        __syncwarp();
+        const uint32_t fm = sf[lane];
+        if (own && fm) {
+            r.visited[wl] = vis | fm;  // this warp owns the batch's words during the level
+            nxt[wl] = fm;
+            found += __popc(fm);
+        }
+        __syncwarp();
     }
+}
+__global__ void k_bfs_pull(RankView r, uint32_t lvl) {
+    unsigned long long found = 0, mdeg = 0, edges = 0;
+    dist_pull_batches(r, r.gfront, r.nxt, lvl, found, mdeg, edges);
     uint64_t a[3] = {found, mdeg, edges};
     block_sum<3>(a);
     if (threadIdx.x == 0) {
@@ -410,6 +519,18 @@ __global__ void k_validate_slice(const uint64_t* rp, const uint32_t* ci, uint64_
     if (f) atomicOr(flags, f);
 }
 
+// BFS start on the source's owner: level 0, visited and frontier bits, and the
+// source's degree in counter slot 4 (the first level's counter reduction
+// carries it to every rank: m_u = m - deg(src) without a host round trip)
+__global__ void k_dist_bfs_start(RankView r, uint32_t src) {
+    const uint64_t sl = (uint64_t)src - r.lo;
+    if (threadIdx.x != 0 || blockIdx.x != 0 || sl >= r.nl) return;
+    const uint32_t bit = 1u << (sl & 31);
+    r.state[sl] = 0;
+    r.visited[sl >> 5] |= bit;
+    r.cur[sl >> 5] |= bit;
+    r.cnt[4] = r.deg[sl];
+}
 __global__ void k_deg_nz(const uint64_t* rp, uint64_t n, uint64_t nwl, uint32_t* deg, uint32_t* nz) {
     for (uint64_t i = gtid(); i < n; i += gthreads()) deg[i] = (uint32_t)(rp[i + 1] - rp[i]);
     for (uint64_t wi = gtid(); wi < nwl; wi += gthreads()) {
@@ -438,6 +559,9 @@ __global__ void k_deg_nz(const uint64_t* rp, uint64_t n, uint64_t nwl, uint32_t*
 //   barrier:    a local grid barrier, CTA 0 crosses one ncclLsaBarrierSession with
 //               the peers (release/acquire at system scope), a local grid barrier.
 // Requires every rank in one LSA team (one NVLink/NVSwitch domain).
+constexpr int FS_STAMPS = 8, FS_NSTAMP = 24;  // fstats[8 + i]: globaltimer at the end of level i (bit 63: pull)
+constexpr int FS_SUB = FS_STAMPS + FS_NSTAMP, FS_NSUB = 8;  // fstats[FS_SUB + 4 i + k]: sub-steps k of level i < 8
+constexpr int FS_TOTAL = FS_SUB + 4 * FS_NSUB;
 struct FusedBfsP {
     RankView r;
     uint32_t* front[2];
@@ -456,8 +580,15 @@ struct FusedBfsP {
     unsigned long long* fstats;
 };
 
+// Cross-rank barrier: a local grid barrier, CTA 0 crosses the LSA barrier with
+// the peers, a local grid barrier.  The CTA's peer writes are ordered before it
+// by __syncthreads + one system-scope fence per CTA (cumulativity), not a fence
+// per thread.  With one rank there are no peers (no peer writes, no system-scope
+// fence — measured 5-9 us per barrier): one grid barrier.
 __device__ __forceinline__ bool xsync(const FusedBfsP& p) {
-    __threadfence_system();  // this thread's peer writes precede the barrier chain
+    if (p.P == 1) return grid_sync(p.ctl);
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence_system();
     if (!grid_sync(p.ctl)) return false;
     if (blockIdx.x == 0) {
         ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), p.dc, ncclTeamTagLsa(), 0u);
@@ -466,6 +597,24 @@ __device__ __forceinline__ bool xsync(const FusedBfsP& p) {
     return grid_sync(p.ctl);
 }
 
+// x[0, n) = v with 16-B stores where aligned (grid-stride: thread tid of T)
+__device__ __forceinline__ void fill_u32(uint32_t* x, uint64_t n, uint32_t v, uint64_t tid, uint64_t T) {
+    const uint64_t head = (((16u - ((uintptr_t)x & 15u)) & 15u) / 4u) < n ? ((16u - ((uintptr_t)x & 15u)) & 15u) / 4u : n;
+    if ((uintptr_t)x & 3u) {  // not even 4-B aligned: plain stores
+        for (uint64_t i = tid; i < n; i += T) x[i] = v;
+        return;
+    }
+    if (tid < head) x[tid] = v;
+    uint4* q = reinterpret_cast<uint4*>(x + head);
+    const uint64_t nq = (n - head) / 4;
+    const uint4 vv = make_uint4(v, v, v, v);
+    for (uint64_t i = tid; i < nq; i += T) q[i] = vv;
+    for (uint64_t i = head + nq * 4 + tid; i < n; i += T) x[i] = v;
+}
+#define FSUB(k)                                                                          \
+    do {                                                                                 \
+        if (lead() && it < FS_NSUB) p.fstats[FS_SUB + 4 * it + (k)] = globaltimer();   \
+    } while (0)
 __global__ void __launch_bounds__(BLOCK, 4) k_dist_bfs_fused(FusedBfsP p) {
     Ctl* c = p.ctl;
     grid_begin(c);
@@ -473,17 +622,15 @@ __global__ void __launch_bounds__(BLOCK, 4) k_dist_bfs_fused(FusedBfsP p) {
     const uint64_t T = gthreads(), tid = gtid();
     const uint32_t lane = lane_id();
     const uint64_t NW = p.N ? (uint64_t)p.P * r.nwl : 0;
-    // ---- state init (inside the timed kernel, as on one GPU)
-    for (uint64_t i = tid; i < r.V; i += T) r.state[i] = INF;
-    for (uint64_t w = tid; w < r.nwl; w += T) {
-        r.visited[w] = 0;
-        p.front[0][w] = 0;
-        p.front[1][w] = 0;
-        p.inbox[w] = 0;
-    }
-    for (uint64_t w = tid; w < NW; w += T) p.gfront[w] = 0;
-    if (blockIdx.x == 0 && warp_id() == 0)
-        for (int i = 0; i < 3; ++i) reset_line_warp(&c->line[i]);
+    if (lead()) p.fstats[7] = globaltimer();  // kernel start (SX_DIST_LEVELS)
+    // ---- state init (inside the timed kernel, as on one GPU), 16-B stores
+    fill_u32(r.state, r.nl, INF, tid, T);  // the level output (owned rows)
+    fill_u32(r.visited, r.nwl, 0u, tid, T);
+    fill_u32(p.front[0], r.nwl, 0u, tid, T);
+    fill_u32(p.front[1], r.nwl, 0u, tid, T);
+    fill_u32(p.inbox, r.nwl, 0u, tid, T);
+    fill_u32(p.gfront, NW, 0u, tid, T);
+    if (tid < 8) p.slots[tid] = 0;  // counter slots, both parities (added into by every rank)
     if (!xsync(p)) return;  // every rank's window is clean before anyone writes into it
     if (tid == 0) {
         p.gfront[p.src >> 5] |= 1u << (p.src & 31);
@@ -495,37 +642,64 @@ __global__ void __launch_bounds__(BLOCK, 4) k_dist_bfs_fused(FusedBfsP p) {
         }
     }
     if (!grid_sync(c)) return;
+    if (lead()) p.fstats[FS_STAMPS] = globaltimer();  // end of the state init
     uint32_t it = 0, cur = 0, pulls = 0;
     uint32_t dir = p.force_dir == 2 ? DIR_PULL : DIR_PUSH;
     uint64_t m_u = p.m_total, nf_prev = 1, edges_all = 0, reached = 1;
+    uint64_t mf_prev = ~0ull;  // out-edges of the current frontier (unknown for the source)
     for (;;) {
         const uint32_t lvl = it + 1;
         uint32_t* curb = p.front[cur];
         uint32_t* nxt = p.front[cur ^ 1];
-        IterLine* nx = &c->line[(it + 1) % 3];
-        maybe_reset_line(&c->line[(it + 2) % 3]);
         unsigned long long found = 0, mdeg = 0, edges = 0;
         if (dir == DIR_PUSH) {
-            auto visit = [&](uint32_t u) {
-                ++edges;
-                const uint64_t q = (uint64_t)u / r.V;
-                const uint32_t bit = 1u << (u & 31);  // V is a multiple of 32: the same bit in the slice
-                if (q == p.me) {
-                    const uint64_t ul = (uint64_t)u - r.lo;
-                    if (r.visited[ul >> 5] & bit) return;
-                    if (atomicOr(r.visited + (ul >> 5), bit) & bit) return;
-                    r.state[ul] = lvl;
-                    atomicOr(nxt + (ul >> 5), bit);
+            // up to 4 targets at a time (INF: none): the visited pre-tests, then the
+            // claims, then the claimed vertices' updates — each group issued together
+            auto visit4 = [&](const uint32_t (&u)[4]) {
+                uint64_t ul[4];
+                uint32_t vw[4], old[4];
+                bool own[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint64_t q = u[k] == INF ? ~0ull : (uint64_t)u[k] / r.V;
+                    own[k] = q == p.me;
+                    ul[k] = own[k] ? (uint64_t)u[k] - r.lo : 0;
+                    edges += u[k] != INF;
+                    if (u[k] != INF && !own[k]) {  // V is a multiple of 32: the same bit in the owner's slice
+                        uint32_t* pin =
+                            (uint32_t*)ncclGetLsaPointer(p.win, p.off_in + (((uint64_t)u[k] - q * r.V) >> 5) * 4, (int)q);
+                        atomicOr(pin, 1u << (u[k] & 31));
+                    }
+                }
+                // pre-test on the non-coherent path (bits are only ever set during the
+                // run, so a stale word only sends the vertex on to the atomic claim)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) vw[k] = own[k] ? __ldg(r.visited + (ul[k] >> 5)) : FULL;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t bit = 1u << (ul[k] & 31);
+                    old[k] = own[k] && !(vw[k] & bit) ? atomicOr(r.visited + (ul[k] >> 5), bit) : FULL;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t bit = 1u << (ul[k] & 31);
+                    if (old[k] & bit) continue;
+                    r.state[ul[k]] = lvl;
+                    atomicOr(nxt + (ul[k] >> 5), bit);
                     ++found;
-                    mdeg += __ldg(r.deg + ul);
-                } else {
-                    uint32_t* pin = (uint32_t*)ncclGetLsaPointer(p.win, p.off_in + (((uint64_t)u - q * r.V) >> 5) * 4, (int)q);
-                    atomicOr(pin, bit);
+                    mdeg += __ldg(r.deg + ul[k]);
                 }
             };
-            for (uint64_t wi = gwarp(); wi < r.nwl; wi += gwarps()) {
-                const uint32_t word = curb[wi];
-                if (!word) continue;
+            // edges [b, e) with stride st, 4 per lane step
+            auto visit_range = [&](uint64_t b, uint64_t e, uint64_t st) {
+                for (; b < e; b += 4 * st) {
+                    uint32_t u[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) u[k] = b + k * st < e ? __ldg(r.ci + b + k * st) : INF;
+                    visit4(u);
+                }
+            };
+            dist_for_words(curb, r.nwl, [&](uint64_t wi, uint32_t word) {
                 const uint64_t vl = (wi << 5) + lane;
                 const bool mine = (word >> lane) & 1u;
                 uint64_t beg = 0, end = 0;
@@ -533,36 +707,47 @@ __global__ void __launch_bounds__(BLOCK, 4) k_dist_bfs_fused(FusedBfsP p) {
                     beg = __ldg(r.rp + vl);
                     end = __ldg(r.rp + vl + 1);
                 }
-                if (mine && end - beg < r.sep_small)
-                    for (uint64_t e = beg; e < end; ++e) visit(__ldg(r.ci + e));
-                // rows of >= DIST_PIECE edges: listed as pieces for the whole grid (below)
-                const bool split = mine && end - beg >= DIST_PIECE;
-                if (split) {
-                    const uint64_t np = (end - beg + DIST_PIECE - 1) / DIST_PIECE;
-                    const uint64_t b0 = atomicAdd(r.cnt + CNT_PIECES, (unsigned long long)np);
-                    for (uint64_t q = 0; q < np; ++q) r.pieces[b0 + q] = (vl << 32) | q;
+                if (mine && end - beg < r.sep_small) visit_range(beg, end, 1);  // thread granularity
+                // rows of >= DIST_PIECE edges: listed as pieces for the whole grid (below),
+                // the warp writing each row's items together
+                for (uint32_t sp = __ballot_sync(FULL, mine && end - beg >= DIST_PIECE); sp; sp &= sp - 1) {
+                    const int l = __ffs(sp) - 1;
+                    const uint64_t b0 = __shfl_sync(FULL, beg, l), e0 = __shfl_sync(FULL, end, l);
+                    const uint64_t vr = (wi << 5) + l;
+                    const uint64_t np = (e0 - b0 + DIST_PIECE - 1) / DIST_PIECE;
+                    uint64_t base = 0;
+                    if (lane == 0) base = atomicAdd(r.cnt + CNT_PIECES, (unsigned long long)np);
+                    base = __shfl_sync(FULL, base, 0);
+                    for (uint64_t q = lane; q < np; q += 32) r.pieces[base + q] = (vr << 32) | q;
                 }
-                for (uint32_t todo = __ballot_sync(FULL, mine && end - beg >= r.sep_small && !split); todo;
-                     todo &= todo - 1) {
+                // warp granularity: medium rows, 32 lanes x 4 edges per step
+                for (uint32_t todo = __ballot_sync(FULL, mine && end - beg >= r.sep_small && end - beg < DIST_PIECE);
+                     todo; todo &= todo - 1) {
                     const int l = __ffs(todo) - 1;
                     const uint64_t b0 = __shfl_sync(FULL, beg, l), e0 = __shfl_sync(FULL, end, l);
-                    for (uint64_t e = b0 + lane; e < e0; e += 32) visit(__ldg(r.ci + e));
+                    visit_range(b0 + lane, e0, 32);
                 }
-            }
-            if (!grid_sync(c)) return;
-            {
+            });
+            FSUB(0);
+            // pieces exist only if some frontier row has >= DIST_PIECE edges: not when the
+            // frontier's out-edges (all ranks) are fewer — then no barrier for them either
+            if (mf_prev >= DIST_PIECE) {
+                if (!grid_sync(c)) return;
                 const uint64_t np = vload(r.cnt + CNT_PIECES);
                 for (uint64_t i = gwarp(); i < np; i += gwarps()) {  // the hub rows, one warp per piece
                     const uint64_t item = r.pieces[i];
                     const uint64_t vl = item >> 32, q = item & 0xFFFFFFFFull;
                     const uint64_t b0 = __ldg(r.rp + vl) + q * DIST_PIECE;
                     const uint64_t e0 = min(b0 + DIST_PIECE, __ldg(r.rp + vl + 1));
-                    for (uint64_t e = b0 + lane; e < e0; e += 32) visit(__ldg(r.ci + e));
+                    visit_range(b0 + lane, e0, 32);
                 }
             }
+            FSUB(1);
             if (!xsync(p)) return;  // every rank's marks are in the owners' inboxes
+            FSUB(2);
             if (lead()) r.cnt[CNT_PIECES] = 0;  // read by every CTA before the barrier
             for (uint64_t w = tid; w < r.nwl; w += T) {
+                curb[w] = 0;  // scanned by every CTA before the barriers above: the next level's output
                 uint32_t m = p.inbox[w];
                 if (!m) continue;
                 p.inbox[w] = 0;
@@ -579,92 +764,43 @@ __global__ void __launch_bounds__(BLOCK, 4) k_dist_bfs_fused(FusedBfsP p) {
             }
         } else {
             ++pulls;
-            for (uint64_t wi = gwarp(); wi < r.nwl; wi += gwarps()) {
-                const uint32_t vis = r.visited[wi];
-                const uint32_t cand = ~vis & __ldg(r.nz + wi);
-                if (!cand) continue;
-                const uint64_t vl = (wi << 5) + lane;
-                const bool mine = (cand >> lane) & 1u;
-                uint64_t beg = 0, end = 0;
-                if (mine) {
-                    beg = __ldg(r.rp + vl);
-                    end = __ldg(r.rp + vl + 1);
-                }
-                bool hit = false;
-                if (mine && r.hub) {  // hub-first probe
-                    const uint32_t h = __ldg(r.hub + vl);
-                    if (h != INF) {
-                        ++edges;
-                        hit = bm_test(p.gfront, h);
-                    }
-                }
-                const bool small = mine && end - beg < r.sep_small;
-                if (small)
-                    for (uint64_t e = beg; e < end && !hit; ++e) {
-                        ++edges;
-                        hit = bm_test(p.gfront, __ldg(r.ci + e));
-                    }
-                for (uint32_t todo = __ballot_sync(FULL, mine && !small && !hit); todo; todo &= todo - 1) {
-                    const int l = __ffs(todo) - 1;
-                    const uint64_t b0 = __shfl_sync(FULL, beg, l), e0 = __shfl_sync(FULL, end, l);
-                    bool any = false;
-                    for (uint64_t b = b0; b < e0 && !any; b += 32) {
-                        const uint64_t e = b + lane;
-                        bool h = false;
-                        if (e < e0) {
-                            ++edges;
-                            h = bm_test(p.gfront, __ldg(r.ci + e));
-                        }
-                        any = __any_sync(FULL, h);
-                    }
-                    if ((int)lane == l) hit = any;
-                }
-                const uint32_t fm = __ballot_sync(FULL, hit);
-                if (hit) {
-                    r.state[vl] = lvl;
-                    mdeg += end - beg;
-                }
-                if (lane == 0 && fm) {
-                    r.visited[wi] = vis | fm;
-                    nxt[wi] = fm;
-                    found += __popc(fm);
-                }
-            }
+            dist_pull_batches(r, p.gfront, nxt, lvl, found, mdeg, edges, curb);
+            FSUB(0);
         }
         {
+            // the CTA's counts go straight into every rank's slot[par] (peer atomics
+            // through the LSA pointers): one cross-rank barrier, no local reduction line
             uint64_t a[3] = {found, mdeg, edges};
             block_sum<3>(a);
-            if (threadIdx.x == 0) {
-                Slot& sl = nx->s[my_slot()];
-                if (a[0]) atomicAdd(&sl.found, (unsigned int)a[0]);
-                if (a[1]) atomicAdd(&sl.mdeg, (unsigned long long)a[1]);
-                if (a[2]) atomicAdd(&sl.edges, (unsigned long long)a[2]);
+            const uint32_t par = it & 1u;
+            if (threadIdx.x < p.P && (a[0] | a[1] | a[2])) {
+                unsigned long long* dst =
+                    (unsigned long long*)ncclGetLsaPointer(p.win, p.off_cnt + (uint64_t)par * 4 * 8, (int)threadIdx.x);
+                if (a[0]) atomicAdd(dst, (unsigned long long)a[0]);
+                if (a[1]) atomicAdd(dst + 1, (unsigned long long)a[1]);
+                if (a[2]) atomicAdd(dst + 2, (unsigned long long)a[2]);
             }
         }
-        for (uint64_t w = tid; w < r.nwl; w += T) curb[w] = 0;  // read no more this level; the next level's output
-        if (!grid_sync(c)) return;
-        LineSum ls;
-        read_line(nx, ls);
-        const uint32_t par = it & 1u;
-        if (blockIdx.x == 0 && threadIdx.x < p.P) {  // this rank's counts into every rank's slot [par][me]
-            const uint64_t off = p.off_cnt + ((uint64_t)(par * p.P + p.me) * 4) * 8;
-            unsigned long long* dst = (unsigned long long*)ncclGetLsaPointer(p.win, off, (int)threadIdx.x);
-            dst[0] = ls.found;
-            dst[1] = ls.mdeg;
-            dst[2] = ls.edges;
-        }
+        // curb (read no more this level) is the next level's output: cleared by the
+        // push's inbox fold or on the way through the pull's batches
+        FSUB(3);
         if (!xsync(p)) return;
-        uint64_t nf = 0, mf = 0, ed = 0;
-        for (uint32_t q = 0; q < p.P; ++q) {
-            const unsigned long long* sq = p.slots + (uint64_t)(par * p.P + q) * 4;
-            nf += vload(sq);
-            mf += vload(sq + 1);
-            ed += vload(sq + 2);
+        const uint32_t par = it & 1u;
+        const unsigned long long* sq = p.slots + (uint64_t)par * 4;
+        const uint64_t nf = vload(sq), mf = vload(sq + 1), ed = vload(sq + 2);
+        // the other parity's slot was read by every local CTA at the previous level (before
+        // the barrier just crossed); the next adds into it come after the next cross-rank
+        // barrier (push marks or frontier broadcast), which this store precedes
+        if (lead()) {
+            unsigned long long* z = p.slots + (uint64_t)(par ^ 1u) * 4;
+            z[0] = z[1] = z[2] = 0;
         }
         edges_all += ed;
         reached += nf;
+        if (lead() && it + 1 < FS_NSTAMP) p.fstats[FS_STAMPS + it + 1] = globaltimer() | ((uint64_t)(dir == DIR_PULL) << 63);
         ++it;
         m_u -= mf < m_u ? mf : m_u;
+        mf_prev = mf;
         cur ^= 1u;
         if (nf == 0 || (p.max_iters && it >= p.max_iters)) break;
         if (dir == DIR_PUSH) {
@@ -697,7 +833,9 @@ __global__ void __launch_bounds__(BLOCK, 4) k_dist_bfs_fused(FusedBfsP p) {
 
 // Hub table of a rank's rows: the neighbour of largest global degree (gdeg: N
 // entries, allgathered once) among a row's first 64 edges; INF for an empty row.
-__global__ void k_dist_hub(const uint64_t* rp, const uint32_t* ci, uint64_t nl, const uint32_t* gdeg, uint32_t* hub) {
+// With sole_ok (N <= 2^31), bit 31 marks a row whose hub is its only edge.
+__global__ void k_dist_hub(const uint64_t* rp, const uint32_t* ci, uint64_t nl, const uint32_t* gdeg, uint32_t* hub,
+                           bool sole_ok) {
     for (uint64_t v = gtid(); v < nl; v += gthreads()) {
         const uint64_t b = rp[v], e = min(rp[v + 1], b + 64);
         uint64_t best = 0;
@@ -705,7 +843,7 @@ __global__ void k_dist_hub(const uint64_t* rp, const uint32_t* ci, uint64_t nl, 
             const uint32_t u = __ldg(ci + x);
             best = max(best, ((uint64_t)(__ldg(gdeg + u) + 1u) << 32) | (uint64_t)(~u));
         }
-        hub[v] = best ? ~(uint32_t)best : INF;
+        hub[v] = best ? (~(uint32_t)best | (sole_ok && rp[v + 1] - b == 1 ? DHUB_SOLE : 0u)) : INF;
     }
 }
 __global__ void k_deg_pad(const uint32_t* deg, uint64_t nl, uint64_t V, uint32_t* out) {
@@ -752,7 +890,8 @@ sx_status reduce_counters(sx_dist d, unsigned long long (&out)[8], bool need_min
     cudaStream_t s = d->ctx->stream;
     if (d->nccl) {
         DistRank& k = d->r[0];
-        SX_NC(ncclAllReduce(k.cnt, d->dred, 3, ncclUint64, ncclSum, d->comm, s));
+        // slots 0-2 and 4 are sums (slot 3, a min, is overwritten by the min reduction when needed)
+        SX_NC(ncclAllReduce(k.cnt, d->dred, 5, ncclUint64, ncclSum, d->comm, s));
         if (need_min) SX_NC(ncclAllReduce(k.cnt + 3, d->dred + 3, 1, ncclUint64, ncclMin, d->comm, s));
         SX_CU(cudaMemcpyAsync(d->hcnt, d->dred, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
         SX_CU(cudaStreamSynchronize(s));
@@ -836,7 +975,7 @@ sx_status ensure_hubs(sx_dist d) {
     for (int i = 0; i < d->nlocal; ++i) {
         DistRank& k = d->r[i];
         if ((rc = dmalloc(&k.hub, k.nl ? k.nl : 1)) != SX_OK) return rc;
-        k_dist_hub<<<G, BLOCK, 0, s>>>(k.rp, k.ci, k.nl, gdeg, k.hub);
+        k_dist_hub<<<G, BLOCK, 0, s>>>(k.rp, k.ci, k.nl, gdeg, k.hub, d->N <= (1ull << 31));
     }
     SX_CU(cudaGetLastError());
     SX_CU(cudaStreamSynchronize(s));
@@ -911,10 +1050,44 @@ sx_status check_dist(sx_dist d) {
 sx_status copy_owned(sx_dist d, uint32_t* const* out) {
     cudaStream_t s = d->ctx->stream;
     for (int i = 0; i < d->nlocal; ++i)
-        if (out[i] && d->r[i].nl) SX_CU(cudaMemcpyAsync(out[i], d->r[i].state, d->r[i].nl * 4, cudaMemcpyDefault, s));
+        if (out[i] && d->r[i].nl && out[i] != d->r[i].state)
+            SX_CU(cudaMemcpyAsync(out[i], d->r[i].state, d->r[i].nl * 4, cudaMemcpyDefault, s));
     SX_CU(cudaStreamSynchronize(s));
     return SX_OK;
 }
+
+// global directed edge count: one allreduce per upload
+sx_status ensure_m_total(sx_dist d) {
+    if (d->m_total_ok) return SX_OK;
+    unsigned long long m = 0;
+    for (int i = 0; i < d->nlocal; ++i) m += d->r[i].ml;
+    if (d->nccl) {
+        cudaStream_t s = d->ctx->stream;
+        SX_CU(cudaMemcpyAsync(d->dred, &m, 8, cudaMemcpyHostToDevice, s));
+        SX_NC(ncclAllReduce(d->dred, d->dred, 1, ncclUint64, ncclSum, d->comm, s));
+        SX_CU(cudaMemcpyAsync(&m, d->dred, 8, cudaMemcpyDeviceToHost, s));
+        SX_CU(cudaStreamSynchronize(s));
+    }
+    d->m_total = m;
+    d->m_total_ok = true;
+    return SX_OK;
+}
+
+// A device level output is written in place by the BFS kernels (no copy-out):
+// the rank's state pointer is redirected for the run and restored on exit.
+struct StateRedirect {
+    sx_dist d;
+    uint32_t* saved[DIST_MAX_LOCAL];
+    StateRedirect(sx_dist d_, uint32_t* const* out) : d(d_) {
+        for (int i = 0; i < d->nlocal; ++i) {
+            saved[i] = d->r[i].state;
+            if (out[i] && d->r[i].nl && sxh::is_device_ptr(out[i])) d->r[i].state = out[i];
+        }
+    }
+    ~StateRedirect() {
+        for (int i = 0; i < d->nlocal; ++i) d->r[i].state = saved[i];
+    }
+};
 
 
 // Symmetric window, device communicator and control block of the fused BFS (once per dist).
@@ -936,26 +1109,22 @@ sx_status fused_prepare(sx_dist d) {
     d->dcomm_ok = true;
     SX_CU(cudaMalloc(&d->fctl, sizeof(Ctl)));
     SX_CU(cudaMemset(d->fctl, 0, sizeof(Ctl)));
-    SX_CU(cudaMalloc(&d->fstats, 8 * sizeof(unsigned long long)));
+    SX_CU(cudaMalloc(&d->fstats, FS_TOTAL * sizeof(unsigned long long)));
     return SX_OK;
 }
 
-sx_status dist_bfs_fused(sx_dist d, uint32_t src, const sx_opts& o, uint32_t* const* level_out, sx_stats* stats) {
+// Enqueue one device-initiated BFS of this rank (no sync).  state: the owned
+// level array the kernel writes (a device output, or the rank's own state).
+sx_status enqueue_fused(sx_dist d, uint32_t src, const sx_opts& o, uint32_t* state) {
     sx_status rc = fused_prepare(d);
     if (rc != SX_OK) return rc;
     sx_ctx c = d->ctx;
-    cudaStream_t s = c->stream;
     DistRank& k = d->r[0];
-    // global edge count (allreduced once; the Beamer test needs m_u)
-    unsigned long long msum = k.ml;
-    {
-        SX_CU(cudaMemcpyAsync(d->dred, &msum, 8, cudaMemcpyHostToDevice, s));
-        SX_NC(ncclAllReduce(d->dred, d->dred, 1, ncclUint64, ncclSum, d->comm, s));
-        SX_CU(cudaMemcpyAsync(&msum, d->dred, 8, cudaMemcpyDeviceToHost, s));
-        SX_CU(cudaStreamSynchronize(s));
-    }
+    // global edge count (the Beamer test needs m_u): allreduced once per upload
+    if ((rc = ensure_m_total(d)) != SX_OK) return rc;
     FusedBfsP p;
     p.r = view_of(d, 0, 0, o);
+    p.r.state = state;
     p.front[0] = k.front[0];
     p.front[1] = k.front[1];
     p.ctl = d->fctl;
@@ -970,34 +1139,76 @@ sx_status dist_bfs_fused(sx_dist d, uint32_t src, const sx_opts& o, uint32_t* co
     p.me = (uint32_t)d->rank0;
     p.src = src;
     p.N = d->N;
-    p.m_total = msum;
+    p.m_total = d->m_total;
     p.alpha = o.alpha;
     p.beta = o.beta;
     p.force_dir = o.force_dir;
     p.max_iters = o.max_iters;
     p.fstats = d->fstats;
-    int per_sm = 0;
-    SX_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dist_bfs_fused, BLOCK, 0));
-    const int grid = per_sm * c->prop.multiProcessorCount;
-    if (grid <= 0) return sxh::fail(SX_E_BARRIER, "fused dist BFS cannot be co-resident");
+    if (d->fgrid == 0) {  // occupancy-sized cooperative grid, once per dist
+        int per_sm = 0;
+        SX_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dist_bfs_fused, BLOCK, 0));
+        d->fgrid = per_sm * c->prop.multiProcessorCount;
+        if (d->fgrid <= 0) {
+            d->fgrid = 0;
+            return sxh::fail(SX_E_BARRIER, "fused dist BFS cannot be co-resident");
+        }
+    }
     void* args[] = {&p};
-    SX_CU(cudaEventRecord(c->ev0, s));
-    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_dist_bfs_fused, dim3(grid), dim3(BLOCK), args, 0, s);
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_dist_bfs_fused, dim3(d->fgrid), dim3(BLOCK), args, 0,
+                                                c->stream);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return sxh::cuda_fail(e, "cudaLaunchCooperativeKernel(k_dist_bfs_fused)");
     }
+    return SX_OK;
+}
+
+sx_status dist_bfs_fused(sx_dist d, uint32_t src, const sx_opts& o, uint32_t* const* level_out, sx_stats* stats) {
+    sx_ctx c = d->ctx;
+    cudaStream_t s = c->stream;
+    StateRedirect redirect(d, level_out);
+    SX_CU(cudaEventRecord(c->ev0, s));
+    sx_status rc = enqueue_fused(d, src, o, d->r[0].state);
+    if (rc != SX_OK) return rc;
     SX_CU(cudaEventRecord(c->ev1, s));
-    unsigned long long hs[4] = {0, 0, 0, 0};
-    SX_CU(cudaMemcpyAsync(hs, d->fstats, sizeof(hs), cudaMemcpyDeviceToHost, s));
+    cudaError_t e;
+    // statistics and the watchdog flag in one pinned read-back, one sync
+    static const bool levels = [] { const char* v = getenv("SX_DIST_LEVELS"); return v && v[0] == '1'; }();
+    const int nst = levels ? FS_TOTAL : 4;
+    unsigned long long* hs = d->hcnt;
+    SX_CU(cudaMemcpyAsync(hs, d->fstats, nst * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    SX_CU(cudaMemcpyAsync(hs + FS_TOTAL, &d->fctl->error, 4, cudaMemcpyDeviceToHost, s));
     e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) {
         c->poisoned = true;
         return sxh::cuda_fail(e, "k_dist_bfs_fused");
     }
-    Ctl hc;
-    SX_CU(cudaMemcpy(&hc, d->fctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
-    if (hc.error) {
+    if (levels) {  // SX_DIST_LEVELS=1: per-level device time of the fused kernel on stderr
+        std::string line = "[sx_dist_bfs fused] init us: " + std::to_string(((hs[FS_STAMPS] & ~(1ull << 63)) - hs[7]) / 1e3) + "; levels us:";
+        const uint32_t nl = (uint32_t)std::min<unsigned long long>(hs[0], FS_NSTAMP - 1);
+        const unsigned long long msk = ~(1ull << 63);
+        for (uint32_t i = 1; i <= nl; ++i) {
+            char b[64];
+            snprintf(b, sizeof(b), " it%u:%s:%.1f", i, (hs[FS_STAMPS + i] >> 63) ? "pull" : "push",
+                     ((hs[FS_STAMPS + i] & msk) - (hs[FS_STAMPS + i - 1] & msk)) / 1e3);
+            line += b;
+            if (i - 1 < (uint32_t)FS_NSUB) {  // sub-steps (0: scan/pull, 1: pieces, 2: marks barrier, 3: fold+count)
+                const unsigned long long* q = hs + FS_SUB + 4 * (i - 1);
+                unsigned long long t = hs[FS_STAMPS + i - 1] & msk;
+                line += " [";
+                for (int k = 0; k < 4; ++k) {
+                    if (!q[k] || q[k] < t) continue;
+                    snprintf(b, sizeof(b), "%s%d:%.1f", k ? " " : "", k, (q[k] - t) / 1e3);
+                    line += b;
+                    t = q[k];
+                }
+                line += "]";
+            }
+        }
+        fprintf(stderr, "%s\n", line.c_str());
+    }
+    if ((uint32_t)hs[FS_TOTAL]) {
         cudaMemset(d->fctl, 0, sizeof(Ctl));
         return sxh::fail(SX_E_BARRIER, "fused dist BFS: grid barrier watchdog fired");
     }
@@ -1065,7 +1276,7 @@ sx_status sx_dist_create(sx_ctx ctx, uint64_t n_global, int nranks, int rank0, i
             return nccl_fail(r, "ncclCommInitRank");
         }
     }
-    cudaError_t e = cudaMallocHost(&d->hcnt, 8 * sizeof(unsigned long long) * nlocal);
+    cudaError_t e = cudaMallocHost(&d->hcnt, sizeof(unsigned long long) * std::max(8 * nlocal, 96));
     if (e == cudaSuccess) e = cudaMalloc(&d->dred, 8 * sizeof(unsigned long long));
     if (e != cudaSuccess) {
         sx_dist_free(d);
@@ -1094,6 +1305,7 @@ sx_status sx_dist_upload(sx_dist d, int local_rank, const sx_csr_desc* desc) {
     if (rc != SX_OK) return rc;
     DistRank& k = d->r[local_rank];
     if (desc->n != k.nl) return sxh::fail(SX_E_INVALID, "sx_dist_upload: desc->n must equal the owned row count");
+    d->m_total_ok = false;
     if (desc->flags & SX_DIRECTED) return sxh::fail(SX_E_INVALID, "sx_dist_upload: symmetric graphs only (1D rows serve as in-rows)");
     if (desc->w && desc->w_bytes != 1 && desc->w_bytes != 4) return sxh::fail(SX_E_INVALID, "sx_dist_upload: w_bytes");
     if (local_rank > 0 && d->wbytes != (desc->w ? desc->w_bytes : 0))
@@ -1152,6 +1364,8 @@ void sx_dist_free(sx_dist d) {
     if (!d) return;
     cudaSetDevice(d->ctx->device);
     cudaStreamSynchronize(d->ctx->stream);
+    for (cudaEvent_t& ev : d->aev)
+        if (ev) cudaEventDestroy(ev);
     for (int i = 0; i < d->nlocal; ++i) {
         DistRank& k = d->r[i];
         void* ps[] = {k.rp, k.ci, k.w, k.deg, k.nz, k.state, k.visited, k.front[0], k.front[1], k.gfront, k.sendmap,
@@ -1178,54 +1392,27 @@ sx_status sx_dist_bfs(sx_dist d, uint32_t src, const sx_opts* opts, uint32_t* co
     const sx_opts o = sxh::resolve_opts(opts);
     if ((rc = ensure_hubs(d)) != SX_OK) return rc;
     if (o.fusion == 2) return dist_bfs_fused(d, src, o, level_out, stats);  // device-initiated (NEXT-1)
+    if ((rc = ensure_m_total(d)) != SX_OK) return rc;
     sx_ctx c = d->ctx;
     cudaStream_t s = c->stream;
     const int G = kgrid(d);
+    StateRedirect redirect(d, level_out);
     SX_CU(cudaEventRecord(c->ev0, s));
-    // state init: levels INF, bitmaps zero, the source on its owner
-    unsigned long long m_local = 0;
+    // state init (no host round trip): levels INF, bitmaps zero, the source on its
+    // owner, whose degree rides in counter slot 4 of the first level's reduction
     for (int i = 0; i < d->nlocal; ++i) {
         DistRank& k = d->r[i];
-        SX_CU(cudaMemsetAsync(k.state, 0xFF, d->V * 4, s));
+        SX_CU(cudaMemsetAsync(k.state, 0xFF, k.nl * 4, s));
         SX_CU(cudaMemsetAsync(k.visited, 0, d->nwl * 4, s));
         SX_CU(cudaMemsetAsync(k.front[0], 0, d->nwl * 4, s));
         SX_CU(cudaMemsetAsync(k.front[1], 0, d->nwl * 4, s));
         SX_CU(cudaMemsetAsync(k.sendmap, 0, d->NW * 4, s));
         SX_CU(cudaMemsetAsync(k.cnt, 0, 64, s));
         SX_CU(cudaMemsetAsync(k.cnt + 3, 0xFF, 8, s));
-        m_local += k.ml;
-        if (src >= k.lo && src < k.lo + k.nl) {
-            const uint64_t sl = src - k.lo;
-            const uint32_t zero = 0, bit = 1u << (sl & 31);
-            SX_CU(cudaMemcpyAsync(k.state + sl, &zero, 4, cudaMemcpyHostToDevice, s));
-            SX_CU(cudaMemcpyAsync(k.visited + (sl >> 5), &bit, 4, cudaMemcpyHostToDevice, s));
-            SX_CU(cudaMemcpyAsync(k.front[0] + (sl >> 5), &bit, 4, cudaMemcpyHostToDevice, s));
-            SX_CU(cudaStreamSynchronize(s));
-        }
+        if (src >= k.lo && src < k.lo + k.nl) k_dist_bfs_start<<<1, 32, 0, s>>>(view_of(d, i, 0, o), src);
     }
-    SX_CU(cudaStreamSynchronize(s));
-    // global edge count and the source degree (allreduced once)
-    unsigned long long msum = m_local, dsrc = 0;
-    {
-        for (int i = 0; i < d->nlocal; ++i) {
-            DistRank& k = d->r[i];
-            if (src >= k.lo && src < k.lo + k.nl) {
-                uint64_t rp2[2];
-                SX_CU(cudaMemcpy(rp2, k.rp + (src - k.lo), 16, cudaMemcpyDeviceToHost));
-                dsrc = rp2[1] - rp2[0];
-            }
-        }
-        if (d->nccl) {
-            unsigned long long hv[2] = {msum, dsrc};
-            SX_CU(cudaMemcpyAsync(d->dred, hv, 16, cudaMemcpyHostToDevice, s));
-            SX_NC(ncclAllReduce(d->dred, d->dred, 2, ncclUint64, ncclSum, d->comm, s));
-            SX_CU(cudaMemcpyAsync(hv, d->dred, 16, cudaMemcpyDeviceToHost, s));
-            SX_CU(cudaStreamSynchronize(s));
-            msum = hv[0];
-            dsrc = hv[1];
-        }
-    }
-    unsigned long long m_u = msum - dsrc, nf_prev = 1;
+    const unsigned long long msum = d->m_total;
+    unsigned long long m_u = msum, nf_prev = 1, mf_prev = ~0ull;
     uint32_t dir = o.force_dir == 2 ? DIR_PULL : DIR_PUSH, cur = 0, it = 0, launches = 0, pulls = 0;
     unsigned long long edges_total = 0, reached = 1;
     for (;;) {
@@ -1233,8 +1420,11 @@ sx_status sx_dist_bfs(sx_dist d, uint32_t src, const sx_opts* opts, uint32_t* co
         if (dir == DIR_PUSH) {
             for (int i = 0; i < d->nlocal; ++i) {
                 k_bfs_push<0><<<G, BLOCK, 0, s>>>(view_of(d, i, cur, o));
-                k_bfs_push<1><<<G, BLOCK, 0, s>>>(view_of(d, i, cur, o));
-                launches += 2;
+                ++launches;
+                if (mf_prev >= DIST_PIECE) {  // otherwise no frontier row was split into pieces
+                    k_bfs_push<1><<<G, BLOCK, 0, s>>>(view_of(d, i, cur, o));
+                    ++launches;
+                }
             }
             if ((rc = ex_alltoall(d)) != SX_OK) return rc;
             for (int i = 0; i < d->nlocal; ++i) {
@@ -1256,8 +1446,10 @@ sx_status sx_dist_bfs(sx_dist d, uint32_t src, const sx_opts* opts, uint32_t* co
         const unsigned long long nf = cnt[0], mf = cnt[1];
         edges_total += cnt[2];
         reached += nf;
+        if (it == 0) m_u -= cnt[4];  // deg(src), from the start kernel
         ++it;
         m_u -= mf;
+        mf_prev = mf;
         // the new frontier is front[cur ^ 1]; the old one becomes next iteration's output and is cleared
         for (int i = 0; i < d->nlocal; ++i) SX_CU(cudaMemsetAsync(d->r[i].front[cur], 0, d->nwl * 4, s));
         cur ^= 1;
@@ -1285,6 +1477,68 @@ sx_status sx_dist_bfs(sx_dist d, uint32_t src, const sx_opts* opts, uint32_t* co
         stats->bytes_model = (double)it * (double)d->NW * 4.0;
     }
     return copy_owned(d, level_out);
+}
+
+sx_status sx_dist_bfs_async(sx_dist d, uint32_t src, const sx_opts* opts, uint32_t* const* level_out) {
+    sx_status rc = check_dist(d);
+    if (rc != SX_OK) return rc;
+    if (!level_out || !level_out[0]) return sxh::fail(SX_E_INVALID, "sx_dist_bfs_async: NULL level_out");
+    if (src >= d->N) return sxh::fail(SX_E_INVALID, "sx_dist_bfs_async: src >= n");
+    if (!sxh::is_device_ptr(level_out[0]))
+        return sxh::fail(SX_E_INVALID, "sx_dist_bfs_async: level_out[0] must be device memory");
+    if (!d->nccl || d->nlocal != 1)
+        return sxh::fail(SX_E_INVALID, "sx_dist_bfs_async: needs the NCCL backend (one rank per process)");
+    if ((rc = ensure_hubs(d)) != SX_OK) return rc;
+    sx_opts o = sxh::resolve_opts(opts);
+    o.fusion = 2;
+    cudaStream_t s = d->ctx->stream;
+    for (int i = 0; i < 2; ++i)
+        if (!d->aev[i]) SX_CU(cudaEventCreate(&d->aev[i]));
+    if (d->async_runs == 0) SX_CU(cudaEventRecord(d->aev[0], s));
+    if ((rc = enqueue_fused(d, src, o, level_out[0])) != SX_OK) return rc;
+    SX_CU(cudaEventRecord(d->aev[1], s));
+    ++d->async_runs;
+    return SX_OK;
+}
+
+sx_status sx_dist_sync(sx_dist d, sx_stats* stats) {
+    sx_status rc = check_dist(d);
+    if (rc != SX_OK) return rc;
+    cudaStream_t s = d->ctx->stream;
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    if (d->async_runs == 0) {
+        SX_CU(cudaStreamSynchronize(s));
+        return SX_OK;
+    }
+    unsigned long long* hs = d->hcnt;
+    SX_CU(cudaMemcpyAsync(hs, d->fstats, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    SX_CU(cudaMemcpyAsync(hs + 4, &d->fctl->error, 4, cudaMemcpyDeviceToHost, s));
+    cudaError_t e = cudaStreamSynchronize(s);
+    const uint32_t runs = d->async_runs;
+    d->async_runs = 0;
+    if (e != cudaSuccess) {
+        d->ctx->poisoned = true;
+        return sxh::cuda_fail(e, "sx_dist_sync");
+    }
+    if ((uint32_t)hs[4]) {
+        cudaMemset(d->fctl, 0, sizeof(Ctl));
+        return sxh::fail(SX_E_BARRIER, "fused dist BFS: grid barrier watchdog fired");
+    }
+    float ms = 0;
+    SX_CU(cudaEventElapsedTime(&ms, d->aev[0], d->aev[1]));
+    if (stats) {
+        stats->iterations = (uint32_t)hs[0];  // of the last run
+        stats->pull_iters = (uint32_t)hs[1];
+        stats->edges_examined = hs[2];
+        stats->list_entries = hs[3];
+        stats->launches = runs;
+        stats->launches_fused = runs;
+        stats->runs = runs;
+        stats->ms = ms;
+        stats->ms_fused = ms;
+        stats->bytes_model = (double)runs * (double)hs[0] * (double)d->NW * 4.0;
+    }
+    return SX_OK;
 }
 
 sx_status sx_dist_sssp(sx_dist d, uint32_t src, uint32_t delta, const sx_opts* opts, uint32_t* const* dist_out,

@@ -110,18 +110,22 @@ _lib.sx_dist_free.argtypes = [_vp]
 _lib.sx_dist_free.restype = None
 _lib.sx_dist_bfs.argtypes = [_vp, _u32, _P(sx_opts), _P(_vp), _P(sx_stats)]
 _lib.sx_dist_sssp.argtypes = [_vp, _u32, _u32, _P(sx_opts), _P(_vp), _P(sx_stats)]
+_lib.sx_dist_bfs_async.argtypes = [_vp, _u32, _P(sx_opts), _P(_vp)]
+_lib.sx_dist_sync.argtypes = [_vp, _P(sx_stats)]
 for _f in ("sx_ctx_create", "sx_ctx_info", "sx_graph_upload", "sx_graph_info", "sx_graph_rmat", "sx_graph_grid",
            "sx_graph_download", "sx_bfs", "sx_bfs_async", "sx_graph_sync", "sx_barrier_fault", "sx_sssp",
            "sx_pagerank", "sx_pagerank_conv", "sx_bp_conv",
            "sx_kcore", "sx_spmv", "sx_bp", "sx_wcc", "sx_barrier_bench", "sx_cluster_bench", "sx_launch_bench",
-           "sx_nccl_unique_id", "sx_dist_create", "sx_dist_range", "sx_dist_upload", "sx_dist_bfs", "sx_dist_sssp"):
+           "sx_nccl_unique_id", "sx_dist_create", "sx_dist_range", "sx_dist_upload", "sx_dist_bfs", "sx_dist_sssp",
+           "sx_dist_bfs_async", "sx_dist_sync"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 EXPORTED = ["sx_status_str", "sx_last_error", "sx_version", "sx_ctx_create", "sx_ctx_destroy", "sx_ctx_info",
             "sx_graph_upload", "sx_graph_info", "sx_graph_free", "sx_graph_rmat", "sx_graph_grid", "sx_graph_download",
             "sx_opts_default", "sx_bfs", "sx_bfs_async", "sx_graph_sync", "sx_barrier_fault", "sx_sssp",
             "sx_pagerank", "sx_pagerank_conv", "sx_bp_conv", "sx_kcore", "sx_spmv", "sx_bp", "sx_wcc", "sx_barrier_bench", "sx_cluster_bench", "sx_launch_bench",
-            "sx_nccl_unique_id", "sx_dist_create", "sx_dist_range", "sx_dist_upload", "sx_dist_free", "sx_dist_bfs", "sx_dist_sssp"]
+            "sx_nccl_unique_id", "sx_dist_create", "sx_dist_range", "sx_dist_upload", "sx_dist_free", "sx_dist_bfs", "sx_dist_sssp",
+            "sx_dist_bfs_async", "sx_dist_sync"]
 
 
 class SimdxError(RuntimeError):
@@ -600,7 +604,13 @@ class Dist:
             for i in range(self.nlocal):
                 lo, hi = self.range(i)
                 outs.append(np.empty(hi - lo, np.uint32))
-        arr = (_vp * self.nlocal)(*[_ptr(o) for o in outs])
+        if len(outs) != self.nlocal:
+            raise ValueError(f"Dist: {self.nlocal} output slices required (got {len(outs)})")
+        ptrs = []
+        for i, o in enumerate(outs):
+            lo, hi = self.range(i)
+            ptrs.append(_ptr_n(o, hi - lo, f"Dist output slice {i}"))
+        arr = (_vp * self.nlocal)(*ptrs)
         return outs, arr
 
     def bfs(self, src: int, outs=None, **kw):
@@ -609,6 +619,19 @@ class Dist:
         o = make_opts(**kw)
         _check(_lib.sx_dist_bfs(self.h, src, ctypes.byref(o), arr, ctypes.byref(st)), "sx_dist_bfs")
         return outs, st.as_dict()
+
+    def bfs_async(self, src: int, outs, **kw):
+        """Enqueue a device-initiated BFS (sx_dist_bfs_async); outs: device tensors (owned slice)."""
+        outs, arr = self._outs(outs)
+        o = make_opts(**kw)
+        _check(_lib.sx_dist_bfs_async(self.h, src, ctypes.byref(o), arr), "sx_dist_bfs_async")
+        return outs
+
+    def sync(self):
+        """Wait for the async runs (sx_dist_sync); their statistics."""
+        st = sx_stats()
+        _check(_lib.sx_dist_sync(self.h, ctypes.byref(st)), "sx_dist_sync")
+        return st.as_dict()
 
     def sssp(self, src: int, delta: int = 0, outs=None, **kw):
         outs, arr = self._outs(outs)

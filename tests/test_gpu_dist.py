@@ -132,6 +132,18 @@ def test_dist_nccl_one_rank_communicator(ctx, rmat14):
             outs, st = D.bfs(src, fusion=2, **mode)
             assert np.array_equal(outs[0], ref), ("fused", src, mode)
             assert st["launches"] == 1 and st["iterations"] == len(oracle.level_histogram(ref))
+    # asynchronous device-initiated runs (sx_dist_bfs_async): enqueued back to back,
+    # levels written in place into a device slice, statistics from sx_dist_sync
+    import torch
+    dev = torch.full((rmat14.n,), -7, dtype=torch.int32, device="cuda")
+    for src in (1234, 0):
+        D.bfs_async(src, [dev])
+    st = D.sync()
+    ref0 = oracle.bfs(rmat14, 0)
+    assert np.array_equal(dev.cpu().numpy().view(np.uint32), ref0)
+    assert st["runs"] == 2 and st["iterations"] == len(oracle.level_histogram(ref0)) and st["ms"] > 0
+    with pytest.raises(simdx.SimdxError):
+        D.bfs_async(0, [np.empty(rmat14.n, np.uint32)])  # host slice refused
     ref = oracle.sssp(rmat14, 0)
     for delta in (0, 1024):
         outs, _ = D.sssp(0, delta)
