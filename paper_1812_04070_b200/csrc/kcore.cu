@@ -66,28 +66,41 @@ constexpr double KCORE_ALPHA = 4.0;  // pull a sub-round whose frontier has > m 
 #endif
 constexpr uint32_t AQ_PIECE = SX_AQ_PIECE;  // a removal of a longer row is split into pieces of this many edges
 constexpr unsigned long long AQ_EMPTY = ~0ull;
+// Work-first (KEEP): the first neighbour an item's warp removes stays with the
+// warp as its next item — no ticket, no queue publish and no spin on the
+// dependent chain of a cascade; the item's pending token passes to it.  The
+// others go to the queue for the idle warps.
+#ifndef SX_AQ_KEEP
+#define SX_AQ_KEEP 1
+#endif
 template <class Rm>
 __device__ __forceinline__ void kcore_async(const KcoreP& p, Ctl* c, Rm&& remove_edges, uint64_t& entries) {
     if (warp_id() >= AQ_WARPS) return;
+    __shared__ uint32_t s_keep[AQ_WARPS];
+    uint32_t* keep = SX_AQ_KEEP ? &s_keep[warp_id()] : nullptr;
     const uint32_t lane = lane_id();
     uint32_t spins = 0;
     uint64_t tw = 0;
+    unsigned long long kept = AQ_EMPTY;
     for (;;) {
-        // one ticket (queue position) per warp; the item is processed by the whole warp
-        unsigned long long t = 0;
-        if (lane == 0) t = atomicAdd(&c->aq_head, 1ull);
-        t = __shfl_sync(FULL, t, 0);
-        unsigned long long it = AQ_EMPTY;
-        if (lane == 0) {
-            for (;;) {
-                if (t < p.qcap && (it = vload(p.q + t)) != AQ_EMPTY) break;
-                // the cascade is over when nothing is pending: this position stays empty
-                if (aq_pending(c) == 0 || aq_stuck(c, spins, tw)) break;
-                __nanosleep(64);
+        unsigned long long it = kept;
+        kept = AQ_EMPTY;
+        if (it == AQ_EMPTY) {
+            // one ticket (queue position) per warp; the item is processed by the whole warp
+            unsigned long long t = 0;
+            if (lane == 0) t = atomicAdd(&c->aq_head, 1ull);
+            t = __shfl_sync(FULL, t, 0);
+            if (lane == 0) {
+                for (;;) {
+                    if (t < p.qcap && (it = vload(p.q + t)) != AQ_EMPTY) break;
+                    // the cascade is over when nothing is pending: this position stays empty
+                    if (aq_pending(c) == 0 || aq_stuck(c, spins, tw)) break;
+                    __nanosleep(64);
+                }
             }
+            it = __shfl_sync(FULL, it, 0);
+            if (it == AQ_EMPTY) return;
         }
-        it = __shfl_sync(FULL, it, 0);
-        if (it == AQ_EMPTY) return;
         // item = (v, piece): piece 0 = a removal; k > 0 = edges [(k-1) P, k P) of v's row
         const uint32_t v = (uint32_t)(it >> 32), pc = (uint32_t)it;
         uint64_t beg = __ldg(p.g.rp + v), end = __ldg(p.g.rp + v + 1);
@@ -104,10 +117,19 @@ __device__ __forceinline__ void kcore_async(const KcoreP& p, Ctl* c, Rm&& remove
                 *(volatile unsigned long long*)(p.q + (uint32_t)tp + k) = ((unsigned long long)v << 32) | (k + 1);
             end = beg;
         }
-        remove_edges(beg, end, (uint64_t)lane, 32ull);
+        if (keep && lane == 0) *keep = INF;
         __syncwarp();
+        remove_edges(beg, end, (uint64_t)lane, 32ull, keep);
+        __syncwarp();
+        if (lane == 0) ++entries;
+        if (keep) {
+            const uint32_t u = *keep;
+            if (u != INF) {  // the next item of this warp; this item's pending token passes to it
+                kept = (unsigned long long)u << 32;
+                continue;
+            }
+        }
         if (lane == 0) {
-            ++entries;
             __threadfence();
             atomicAdd(&c->aq_tp, (unsigned long long)(-(long long)AQ_ONE));  // done with this item
         }
@@ -202,7 +224,8 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
     uint64_t aedges = 0;  // edges of the asynchronous cascades
     // one removal's edges in the asynchronous cascade (level k): decrement the
     // alive neighbours; the one whose residual crosses k+1 -> k is removed and enqueued
-    auto remove_edges = [&](uint64_t beg, uint64_t end, uint64_t rank, uint64_t size) {
+    // keep (shared memory, nullable): the first removal is kept by the warp instead of enqueued
+    auto remove_edges = [&](uint64_t beg, uint64_t end, uint64_t rank, uint64_t size, uint32_t* keep) {
         const uint32_t kk = k;
         for_edges_b(p.g.ci, beg, end, rank, size, [&](const uint32_t (&u)[4], uint32_t kn) {
             aedges += kn;
@@ -220,6 +243,7 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
                     const uint32_t bit = 1u << (u[j] & 31);
                     if (!(atomicAnd(p.ab + (u[j] >> 5), ~bit) & bit)) continue;
                     p.core[u[j]] = kk;
+                    if (keep && atomicCAS(keep, INF, u[j]) == INF) continue;  // the warp's next item
                     const unsigned long long tp = atomicAdd(&c->aq_tp, AQ_ONE + 1ull);
                     *(volatile unsigned long long*)(p.q + (uint32_t)tp) = (unsigned long long)u[j] << 32;
                 }
