@@ -16,6 +16,8 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <type_traits>
+
 #include "internal.h"
 
 namespace sx {
@@ -454,6 +456,22 @@ constexpr int HUB_ILP = SX_HUB_ILP;             // phase 1: rounds of 32 candida
 #define SX_LIST_DIV 8
 #endif
 constexpr uint32_t LIST_DIV = SX_LIST_DIV;
+#ifndef SX_PULL_REC
+#define SX_PULL_REC 1
+#endif
+#ifndef SX_PULL_STATIC
+#define SX_PULL_STATIC 0
+#endif
+constexpr bool PULL_REC = SX_PULL_REC;        // record the open candidates for a LIST-mode next level
+#ifndef SX_REC_OPEN_DIV
+#define SX_REC_OPEN_DIV 16
+#endif
+// ... only when this level's candidates are at most n / REC_OPEN_DIV: recording costs
+// the level that records (s24: the first pull 84.6 -> 98.6 us) and a LIST level is
+// slower than a TILE scan for large candidate sets (s24 it3: 38.8 vs 30.1 us); the
+// first pull never records (its candidate count is unknown and large)
+constexpr uint32_t REC_OPEN_DIV = SX_REC_OPEN_DIV;
+constexpr bool PULL_STATIC = SX_PULL_STATIC;  // TILE chunks assigned statically (no claims / stealing)
 #ifndef SX_PULL_TMA
 #define SX_PULL_TMA 0  // measured slower (s24 it2 100.6 -> 114.8 us; profiles/r2/pull_tma.txt); experiment only
 #endif
@@ -497,6 +515,7 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
     uint32_t* s_f = s_found[warp_id()];
     uint64_t mf_last = 0;  // out-edges of the frontier found last (the push's record prediction)
     uint32_t ncand = 0;    // LIST mode when > 0: candidates recorded by the previous iteration
+    uint64_t cand_cnt = ~0ull;  // this level's candidates (the previous level's open count; unknown at first)
     uint32_t handoff = 0;  // the next frontier was recorded as a contiguous list
     uint32_t to_list = 0;  // 2: ... and the push takes it as its lists (lists_ready = 2)
     for (;;) {
@@ -508,7 +527,11 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
         uint32_t* nbm = p.s.bm[(it + 1) % 3];
         const uint32_t lvl = it + 1;
         const bool list_mode = ncand > 0;
-        const bool rec_found = list_mode && ncand <= FREC_MAX;
+        // the found vertices go to a list (the push hand-over) when few can be found
+        const bool rec_found = cand_cnt <= FREC_MAX && p.s.force_filter != 2;
+        // the open candidates are recorded (LIST mode next) only when this level's candidates are few
+        const bool rec_open = PULL_REC && cand_cnt <= n / REC_OPEN_DIV && p.s.force_filter != 2;
+        uint32_t open_cnt = 0;  // open candidates counted, not recorded (!rec_open)
         uint32_t* cnext = p.s.lists[(it + 1) & 1] + (uint64_t)CAND_CLS * p.s.cstride;
         uint32_t* flist = p.s.lists[(it + 1) & 1];  // class-0 region: the found list (hand-over)
         unsigned int* fcnt = &c->cl.cnt[(it + 1) % 3];
@@ -550,7 +573,13 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
             __syncwarp();
             nrec = 0;
         };
-        auto record_open = [&](bool still, uint32_t v) {
+        // R (a compile-time tag, so the two variants of the probe loops are separate
+        // code): record the open candidates, or only count them
+        auto record_open = [&](auto R, bool still, uint32_t v) {
+            if constexpr (!decltype(R)::value) {  // counted only (per lane: the block sum adds the lanes up)
+                open_cnt += still;
+                return;
+            }
             const uint32_t bal = __ballot_sync(FULL, still);
             if (still) s_r[nrec + __popc(bal & lanemask_lt())] = v;
             nrec += __popc(bal);
@@ -574,7 +603,7 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
             e += k;
         };
         // phase 2 — the warp's `nopen` open candidates in s_c walk their in-edge rows
-        auto walk_open = [&](uint32_t nopen, uint64_t w0) {
+        auto walk_open = [&](auto R, uint32_t nopen, uint64_t w0) {
             uint32_t v_n = 0;
             uint64_t beg_n = 0, end_n = 0;
             if (lane < nopen) {
@@ -636,12 +665,12 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
                 if (found) on_found(v, w0);
                 const bool still = open && !found;
                 if (still) mopen += end - beg;
-                record_open(still, v);
+                record_open(R, still, v);
             }
         };
         // the warp's `total` candidates in s_c through phases 1 and 2
         // sh: the chunk's staged hub slice (vertices from vbase), or nullptr (global loads)
-        auto run_cands = [&](uint32_t total, uint64_t w0, const uint32_t* sh, uint32_t vbase) {
+        auto run_cands = [&](auto R, uint32_t total, uint64_t w0, const uint32_t* sh, uint32_t vbase) {
             uint32_t nopen = 0;
             for (uint32_t r0 = 0; r0 < total; r0 += 32 * HUB_ILP) {
                 uint32_t v[HUB_ILP], h[HUB_ILP], wd[HUB_ILP];
@@ -667,7 +696,7 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
                     if (f) on_found(v[k], w0);
                     const bool settled = v[k] != INF && !f && sole[k];
                     if (settled) mopen += 1;
-                    record_open(settled, v[k]);
+                    record_open(R, settled, v[k]);
                     // open ones are compacted in place at the front of s_c (stable)
                     const bool open = v[k] != INF && !f && !sole[k];
                     const uint32_t bal = __ballot_sync(FULL, open);
@@ -676,7 +705,7 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
                 }
                 __syncwarp();
             }
-            walk_open(nopen, w0);
+            walk_open(R, nopen, w0);
         };
         uint32_t s_cur = my_slot();
         uint32_t chunk = 0;
@@ -717,7 +746,8 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
                     s_c[j] = ccur[(uint64_t)lo * p.s.R + (i - s_cpre[lo])];
                 }
                 __syncwarp();
-                run_cands(total, 0, nullptr, 0u);
+                if (rec_open) run_cands(std::true_type{}, total, 0, nullptr, 0u);
+                else run_cands(std::false_type{}, total, 0, nullptr, 0u);
                 __syncwarp();
                 flush_rec();
                 chunk = grab_finish(nx, nchunks, s_cur, raw_n, s_iss);
@@ -746,14 +776,14 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
                     tma_load_1d(shub + b * CV, p.hub + v0, (nv * 4u + 15u) & ~15u, &mbar[b]);
                 }
             };
-            chunk = grab_chunk(nx, nchunks, s_cur);
+            chunk = PULL_STATIC ? (gwarp() < nchunks ? (uint32_t)gwarp() : INF) : grab_chunk(nx, nchunks, s_cur);
             stage_hub(chunk, 0);
             while (chunk != INF) {
 #if SX_PULL_TMA
                 const uint32_t chunk_n = grab_chunk(nx, nchunks, s_cur);  // the TMA prefetch needs it now
                 stage_hub(chunk_n, buf ^ 1u);
 #else
-                const uint32_t s_iss = s_cur, raw_n = grab_issue(nx, s_cur);  // next claim in flight
+                const uint32_t s_iss = s_cur, raw_n = PULL_STATIC ? 0u : grab_issue(nx, s_cur);  // next claim in flight
 #endif
                 const uint64_t w0 = (uint64_t)chunk * CW;
                 const uint64_t wl = w0 + lane;
@@ -779,7 +809,8 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
                     for (uint32_t w = cand_l; w; w &= w - 1) s_c[pos++] = (uint32_t)(wl << 5) + (__ffs(w) - 1);
                     s_f[lane] = 0;
                     __syncwarp();
-                    run_cands(total, w0, sh, (uint32_t)(w0 << 5));
+                    if (rec_open) run_cands(std::true_type{}, total, w0, sh, (uint32_t)(w0 << 5));
+                    else run_cands(std::false_type{}, total, w0, sh, (uint32_t)(w0 << 5));
                     __syncwarp();
                     flush_rec();
                     const uint32_t fm = s_f[lane];
@@ -788,12 +819,29 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
                         nbm[wl] = fm;
                         found_cnt += __popc(fm);
                     }
+                    if (rec_found && __any_sync(FULL, fm != 0)) {  // the chunk's found vertices onto the hand-over list, one atomic per warp
+                        const uint32_t nfl = __popc(fm);
+                        uint32_t inc = nfl;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const uint32_t y = __shfl_up_sync(FULL, inc, o);
+                            if ((int)lane >= o) inc += y;
+                        }
+                        const uint32_t tot = __shfl_sync(FULL, inc, 31);
+                        if (tot) {
+                            uint32_t base = 0;
+                            if (lane == 0) base = atomicAdd(fcnt, tot);
+                            base = __shfl_sync(FULL, base, 0) + inc - nfl;
+                            for (uint32_t x = fm; x; x &= x - 1) flist[base++] = (uint32_t)(wl << 5) + (__ffs(x) - 1);
+                        }
+                    }
                     __syncwarp();
                 }
 #if SX_PULL_TMA
                 chunk = chunk_n;
 #else
-                chunk = grab_finish(nx, nchunks, s_cur, raw_n, s_iss);
+                if (PULL_STATIC) chunk = chunk + gwarps() < nchunks ? chunk + (uint32_t)gwarps() : INF;
+                else chunk = grab_finish(nx, nchunks, s_cur, raw_n, s_iss);
 #endif
             }
         }
@@ -807,14 +855,15 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
             reinterpret_cast<uint64_t*>(p.s.trace + 32)[(it % 8) * MAX_GRID + blockIdx.x] = globaltimer();
 #endif
         {
-            uint64_t v4[4] = {p.sym ? mopen : mdeg, found_cnt, cand_small, cand_warp};
-            block_sum<4>(v4);
+            uint64_t v4[5] = {p.sym ? mopen : mdeg, found_cnt, cand_small, cand_warp, open_cnt};
+            block_sum<5>(v4);
             if (threadIdx.x == 0) {
                 Slot& sl = nx->s[my_slot()];
                 if (v4[0]) atomicAdd(&sl.mdeg, (unsigned long long)v4[0]);
                 if (v4[1]) atomicAdd(&sl.found, (unsigned int)v4[1]);
                 if (v4[2]) atomicAdd(&sl.cnt[0], (unsigned int)v4[2]);
                 if (v4[3]) atomicAdd(&sl.cnt[1], (unsigned int)(v4[3] / 32));
+                if (v4[4]) atomicAdd(&sl.alive, (unsigned int)v4[4]);  // counted, not recorded
             }
         }
         st.entries += rows;
@@ -859,7 +908,8 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
         if (!p.s.fusion) break;
         // LIST mode next when the open candidates are few and every slot region held its share
         ncand = 0;
-        if (p.s.force_filter != 2 && nopen_all > 0 && nopen_all <= n / LIST_DIV) {
+        cand_cnt = nopen_all;  // the next level's candidates
+        if (rec_open && nopen_all > 0 && nopen_all <= n / LIST_DIV) {
             __shared__ uint32_t s_ok;
             if (threadIdx.x < 32) {
                 const uint32_t ok = __all_sync(FULL, vload(&nx->s[lane].alive) <= p.s.R);
