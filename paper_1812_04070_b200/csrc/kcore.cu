@@ -62,7 +62,7 @@ __device__ __forceinline__ bool aq_stuck(Ctl* c, uint32_t& spins, uint64_t& t0) 
 
 constexpr double KCORE_ALPHA = 4.0;  // pull a sub-round whose frontier has > m / 4 out-edges (R-MAT: never)
 #ifndef SX_AQ_PIECE
-#define SX_AQ_PIECE 1024
+#define SX_AQ_PIECE 256  // measured s24 (session 3): 1024 25.64, 256 25.16 ms at cluster_enter 16384
 #endif
 constexpr uint32_t AQ_PIECE = SX_AQ_PIECE;  // a removal of a longer row is split into pieces of this many edges
 constexpr unsigned long long AQ_EMPTY = ~0ull;
