@@ -272,14 +272,18 @@ __global__ void k_bfs_apply(RankView r, uint32_t lvl) {
 // vertex), then walks the rows of the candidates the hub left open — small rows
 // on the lane, 4 probes in flight, larger ones by the whole warp with the
 // voting early exit.  Found bits are merged per word in shared memory
-// and stored once by the word's lane: no global atomics.
+// and stored once by the word's lane: no global atomics.  `mopen` returns the
+// degree sum of the candidates still open after the level (walked rows: their
+// length; settled sole edges: 1): on a symmetric graph that is m_u of the next
+// level, so m_f = m_u - mopen with no degree load per found vertex (a found
+// vertex's degree load stalled the probe loop: 15% of the kernel's samples).
 constexpr int DP_ILP = 4;
 constexpr uint32_t DHUB_SOLE = 0x80000000u;  // hub entry: bit 31 = the hub is the row's only edge (N <= 2^31)
 __device__ __forceinline__ uint32_t dhub_id(uint32_t h) { return h == INF ? INF : h & ~DHUB_SOLE; }
 __device__ __forceinline__ bool dhub_sole(uint32_t h) { return h != INF && (h & DHUB_SOLE); }
 // clr (nullable): owned words zeroed on the way (the fused kernel's next output buffer)
 __device__ __forceinline__ void dist_pull_batches(const RankView& r, const uint32_t* front, uint32_t* nxt, uint32_t lvl,
-                                                  unsigned long long& found, unsigned long long& mdeg,
+                                                  unsigned long long& found, unsigned long long& mopen,
                                                   unsigned long long& edges, uint32_t* clr = nullptr) {
     __shared__ uint32_t s_c[WARPS][1024];
     __shared__ uint32_t s_f[WARPS][32];
@@ -329,11 +333,10 @@ __device__ __forceinline__ void dist_pull_batches(const RankView& r, const uint3
                 const bool f = h != INF && ((wd[k] >> (h & 31)) & 1u);
                 edges += h != INF;
                 if (f) {
-                    const uint64_t vl = vb + ix[k];
-                    r.state[vl] = lvl;
+                    r.state[vb + ix[k]] = lvl;
                     atomicOr(sf + (ix[k] >> 5), 1u << (ix[k] & 31));
-                    mdeg += __ldg(r.deg + vl);
                 }
+                if (ix[k] != INF && !f && dhub_sole(hx[k])) mopen += 1;  // settled: its one edge stays
                 const bool open = ix[k] != INF && !f && !dhub_sole(hx[k]);
                 const uint32_t bal = __ballot_sync(FULL, open);
                 if (open) sc[nopen + __popc(bal & lanemask_lt())] = ix[k];
@@ -386,7 +389,8 @@ __device__ __forceinline__ void dist_pull_batches(const RankView& r, const uint3
             if (hit) {
                 r.state[vl] = lvl;
                 atomicOr(sf + (ix >> 5), 1u << (ix & 31));
-                mdeg += end - beg;
+            } else if (mine) {
+                mopen += end - beg;
             }
         }
         __syncwarp();
@@ -636,6 +640,10 @@ __global__ void __launch_bounds__(BLOCK, 4) k_dist_bfs_fused(FusedBfsP p) {
         p.gfront[p.src >> 5] |= 1u << (p.src & 31);
         const uint64_t sl = (uint64_t)p.src - r.lo;
         if (sl < r.nl) {
+            // the source's degree into every rank's slot[0][3] (read after the first level's
+            // cross-rank barrier: m_u = m - deg(src) everywhere)
+            for (uint32_t q = 0; q < p.P; ++q)
+                *(unsigned long long*)ncclGetLsaPointer(p.win, p.off_cnt + 3 * 8, (int)q) = __ldg(r.deg + sl);
             r.state[sl] = 0;
             r.visited[sl >> 5] |= 1u << (sl & 31);
             p.front[0][sl >> 5] |= 1u << (sl & 31);
@@ -787,13 +795,16 @@ __global__ void __launch_bounds__(BLOCK, 4) k_dist_bfs_fused(FusedBfsP p) {
         if (!xsync(p)) return;
         const uint32_t par = it & 1u;
         const unsigned long long* sq = p.slots + (uint64_t)par * 4;
-        const uint64_t nf = vload(sq), mf = vload(sq + 1), ed = vload(sq + 2);
+        if (it == 0) m_u -= vload(sq + 3);  // deg(src)
+        const uint64_t nf = vload(sq), ed = vload(sq + 2);
+        // push: m_f; pull: the still-open candidates' degrees = the next m_u (symmetric graphs)
+        const uint64_t mf = dir == DIR_PULL ? (m_u > vload(sq + 1) ? m_u - vload(sq + 1) : 0ull) : vload(sq + 1);
         // the other parity's slot was read by every local CTA at the previous level (before
         // the barrier just crossed); the next adds into it come after the next cross-rank
         // barrier (push marks or frontier broadcast), which this store precedes
         if (lead()) {
             unsigned long long* z = p.slots + (uint64_t)(par ^ 1u) * 4;
-            z[0] = z[1] = z[2] = 0;
+            z[0] = z[1] = z[2] = z[3] = 0;
         }
         edges_all += ed;
         reached += nf;
@@ -1443,10 +1454,13 @@ sx_status sx_dist_bfs(sx_dist d, uint32_t src, const sx_opts* opts, uint32_t* co
         SX_CU(cudaGetLastError());
         unsigned long long cnt[8];
         if ((rc = reduce_counters(d, cnt, false)) != SX_OK) return rc;
-        const unsigned long long nf = cnt[0], mf = cnt[1];
+        const unsigned long long nf = cnt[0];
         edges_total += cnt[2];
         reached += nf;
         if (it == 0) m_u -= cnt[4];  // deg(src), from the start kernel
+        // push: cnt[1] = m_f (degrees of the found vertices); pull: cnt[1] = degrees of the
+        // candidates still open = m_u of the next level (symmetric graphs), m_f = m_u - that
+        const unsigned long long mf = dir == DIR_PULL ? (m_u > cnt[1] ? m_u - cnt[1] : 0ull) : cnt[1];
         ++it;
         m_u -= mf;
         mf_prev = mf;
