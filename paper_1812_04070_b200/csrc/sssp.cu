@@ -571,6 +571,27 @@ __global__ void __launch_bounds__(BLOCK, 4) sssp_pull(SsspP p) {
 // (engine.cuh: cluster_entry / cluster_leave).  Delta-stepping continues inside
 // the cluster, bucket advances included; the frontier goes back to the grid
 // kernels once it exceeds 8 x cluster_enter vertices.
+#ifdef SX_C2_MARKS
+// profiling build (profiles/c2_marks.py): where thread 0's iteration goes — SM cycles per
+// segment of its dependent chain, summed over the iterations in which it had a task; read
+// with sx_debug_c2_marks (not part of the ABI).  A volatile store of the segment's last
+// value makes the clock read wait for it.
+__device__ unsigned long long g_c2_marks[16];
+__device__ volatile uint32_t g_c2_sink;
+#define C2MARK(k, dep)                                        \
+    do {                                                       \
+        if (mk_on) {                                           \
+            g_c2_sink = (uint32_t)(dep);                       \
+            const unsigned long long t_ = clock64();           \
+            mk[k] += t_ - mk_last;                             \
+            mk_last = t_;                                      \
+        }                                                      \
+    } while (0)
+#else
+#define C2MARK(k, dep) \
+    do {               \
+    } while (0)
+#endif
 __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) sssp_cluster(SsspP p) {
     Ctl* c = p.s.ctl;
     const RunState& rs = run_state(c);
@@ -606,6 +627,10 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
     // reads the exact minimum its compaction left.
     uint32_t fins = INF, fsel = 0;
     bool fvalid = false;
+#ifdef SX_C2_MARKS
+    unsigned long long mk[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, mk_last = clock64();
+    bool mk_on = false;
+#endif
     auto flush_fins = [&]() {
         const uint32_t m = warp_min(fins);
         if (lane_id() == 0 && m != INF) atomicMin(&cl->fmin[fsel], m);
@@ -625,6 +650,10 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
             }
 #pragma unroll
             for (int k = 0; k < 8; ++k) old[k] = ok[k] ? atomicMin(p.dist + u[k], nd[k]) : 0u;
+            C2MARK(10, u[0]);        // ids
+            C2MARK(11, nd[0] - dv);  // weights
+            C2MARK(3, nd[1]);        // dist(v)
+            C2MARK(4, old[0] ^ old[1]);  // the atomicMin results
             uint32_t sel = 0;
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -644,6 +673,7 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
             }
             // the step's appends with one returning atomic per warp, not one per edge slot
             cl_append8(NL, ncnt, u, sel, acap);
+            C2MARK(5, sel);
         }
     };
     // the current list's size: read once at entry, then carried from the previous
@@ -659,10 +689,19 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
         uint32_t* cur = p.s.bm[it % 3];
         uint32_t* nbm = p.s.bm[(it + 1) % 3];
         unsigned int* ncnt = &cl->cnt[(it + 1) % 3];
+#ifdef SX_C2_MARKS
+        mk_on = tid == 0 && ncur > 0;
+        if (mk_on) {
+            mk[9] += 1;
+            mk_last = clock64();
+        }
+#endif
         for (uint32_t i = tid; i < ncur; i += T) {
             const uint32_t v = L[i];
+            C2MARK(1, v);
             atomicAnd(cur + (v >> 5), ~(1u << (v & 31)));  // consumed: keep the bitmaps clean
             const uint64_t beg = __ldg(p.g.rp + v), end = __ldg(p.g.rp + v + 1);
+            C2MARK(2, (uint32_t)(beg ^ end));
             ++entries;
             if (end - beg > CL_BIG) {
                 NL[lcap - 1 - atomicAdd(&cl->nbig[it % 3], 1u)] = v;
@@ -671,10 +710,16 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
             relax(p.dist[v], beg, end, 1, nbm, NL, ncnt);
         }
         flush_fins();
+        C2MARK(6, 0u);
         cluster_barrier();
+        C2MARK(7, 0u);
         const uint32_t nbig = vload(&cl->nbig[it % 3]);
         uint32_t nnext = vload(ncnt);  // issued together with nbig and the far minimum
         uint32_t fmin = vload(&cl->fmin[fsel]);
+        C2MARK(8, nbig ^ nnext ^ fmin);
+#ifdef SX_C2_MARKS
+        mk_on = false;
+#endif
         if (nbig) {  // high-degree tasks: their edges spread over the whole cluster
             for (uint32_t j = 0; j < nbig; ++j) {
                 const uint32_t v = NL[lcap - 1 - j];
@@ -768,6 +813,10 @@ __global__ void __cluster_dims__(CL_CTAS, 1, 1) __launch_bounds__(CL_BLOCK, 1) s
         }
         ncur = nnext;
     }
+#ifdef SX_C2_MARKS
+    if (tid == 0)
+        for (int k = 0; k < 12; ++k) atomicAdd(&g_c2_marks[k], mk[k]);
+#endif
     // statistics: warp sums, one atomic per warp
     const uint64_t e = warp_sum(edges), en = warp_sum(entries);
     if (lane_id() == 0) {
@@ -884,3 +933,15 @@ extern "C" sx_status sx_wcc(sx_graph g, const sx_opts* opts, uint32_t* label_out
     if (g->n == 0) return SX_OK;
     return run_sssp(g, 0, 0, opts, label_out, stats, true);
 }
+
+#ifdef SX_C2_MARKS
+extern "C" int sx_debug_c2_marks(unsigned long long* out16, int reset) {
+    cudaDeviceSynchronize();
+    if (cudaMemcpyFromSymbol(out16, sx::g_c2_marks, 16 * 8) != cudaSuccess) return 1;
+    if (reset) {
+        unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(sx::g_c2_marks, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
