@@ -144,6 +144,10 @@ def test_dist_nccl_one_rank_communicator(ctx, rmat14):
     assert st["runs"] == 2 and st["iterations"] == len(oracle.level_histogram(ref0)) and st["ms"] > 0
     with pytest.raises(simdx.SimdxError):
         D.bfs_async(0, [np.empty(rmat14.n, np.uint32)])  # host slice refused
+    with pytest.raises(ValueError):
+        D.bfs(0, outs=[np.empty(rmat14.n - 1, np.uint32)])  # short slice: checked before the C call
+    with pytest.raises(ValueError):
+        D.bfs(0, outs=[np.empty(rmat14.n, np.uint64)])  # 8-byte elements
     ref = oracle.sssp(rmat14, 0)
     for delta in (0, 1024):
         outs, _ = D.sssp(0, delta)
