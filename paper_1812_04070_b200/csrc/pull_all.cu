@@ -48,12 +48,14 @@ struct PrOp {  // r(u) = (1-d)/N + d (sum_v r(v)/outdeg(v) + D/N)
     float* out;
     const uint32_t* dout;
     double d, invN;
-    // per-iteration
+    // per-iteration.  The double buffer is chosen with a select, never indexed by
+    // `cur`: a dynamically indexed member array put the kernel's copy of the
+    // operator in local memory (an LDL on every tile's gather address)
     uint32_t cur;
     double D;
     bool last;
-    __device__ __forceinline__ HubT val(uint32_t v) const { return contrib[cur][v]; }
-    __device__ __forceinline__ const HubT* src() const { return contrib[cur]; }
+    __device__ __forceinline__ HubT val(uint32_t v) const { return (cur ? contrib[1] : contrib[0])[v]; }
+    __device__ __forceinline__ const HubT* src() const { return (cur ? contrib[1] : contrib[0]); }
     __device__ __forceinline__ TermT term(const DevGraph&, uint64_t, HubT x) const { return x; }
     __device__ __forceinline__ AuxT aux(uint32_t u) const {
         const uint32_t du = dout[u];
@@ -72,7 +74,7 @@ struct PrOp {  // r(u) = (1-d)/N + d (sum_v r(v)/outdeg(v) + D/N)
     __device__ __forceinline__ void apply(uint32_t u, double s, AuxT inv, PAcc& pa) const {
         const double r = (1.0 - d) * invN + d * (s + D * invN);
         if (last) out[u] = (float)r;
-        contrib[cur ^ 1][u] = (float)(r * (double)inv);
+        (cur ? contrib[0] : contrib[1])[u] = (float)(r * (double)inv);
         if (inv == 0.0f) pa.dang += r;
     }
 };
@@ -96,8 +98,8 @@ struct PrcOp {
     uint32_t cur;
     double D;
     bool last;
-    __device__ __forceinline__ HubT val(uint32_t v) const { return contrib[cur][v]; }
-    __device__ __forceinline__ const HubT* src() const { return contrib[cur]; }
+    __device__ __forceinline__ HubT val(uint32_t v) const { return (cur ? contrib[1] : contrib[0])[v]; }
+    __device__ __forceinline__ const HubT* src() const { return (cur ? contrib[1] : contrib[0]); }
     __device__ __forceinline__ TermT term(const DevGraph&, uint64_t, HubT x) const { return x; }
     __device__ __forceinline__ AuxT aux(uint32_t u) const { return dout[u]; }
     __device__ __forceinline__ void init(uint64_t v, PAcc& pa) const {
@@ -113,7 +115,7 @@ struct PrcOp {
         const double ch = rn - r[u];
         r[u] = rn;
         rho[u] = ch;
-        contrib[cur ^ 1][u] = du ? rn / (double)du : 0.0;
+        (cur ? contrib[0] : contrib[1])[u] = du ? rn / (double)du : 0.0;
         if (du == 0 && dn != 0.0) pa.dang += rn;
         pa.l1 += fabs(ch);
         if (fabs(ch) > tau) pa.unstable += du;
@@ -159,8 +161,8 @@ struct BpOp {  // l(u) = logit(p_u) + sum_v log((c b + (1-c)(1-b)) / (c(1-b) + (
     double D;
     bool last;
     __device__ static __forceinline__ double coupling(double wt) { return 0.25 + 0.5 * (wt - 1.0) / 254.0; }
-    __device__ __forceinline__ HubT val(uint32_t v) const { return b[cur][v]; }
-    __device__ __forceinline__ const HubT* src() const { return b[cur]; }
+    __device__ __forceinline__ HubT val(uint32_t v) const { return (cur ? b[1] : b[0])[v]; }
+    __device__ __forceinline__ const HubT* src() const { return (cur ? b[1] : b[0]); }
     __device__ __forceinline__ AuxT aux(uint32_t u) const { return prior[u]; }
     // l = logit(p): written to b[1] in the first iteration (b[0] by init), out in the last
     __device__ __forceinline__ bool empty_each_iter() const { return false; }
@@ -182,8 +184,8 @@ struct BpOp {  // l(u) = logit(p_u) + sum_v log((c b + (1-c)(1-b)) / (c(1-b) + (
         const double l = log(p / (1.0 - p)) + s;
         if (last) out[u] = (float)l;
         const double bn = 1.0 / (1.0 + exp(-l));
-        if (conv) pa.l1 += fabs(bn - b[cur][u]);
-        b[cur ^ 1][u] = bn;
+        if (conv) pa.l1 += fabs(bn - (cur ? b[1] : b[0])[u]);
+        (cur ? b[0] : b[1])[u] = bn;
     }
 };
 
