@@ -761,6 +761,21 @@ __device__ __forceinline__ void ballot_chunk(uint64_t nwords, uint64_t& w0, uint
     if (w1 > nwords) w1 = nwords;
 }
 
+// Per-class counters indexed by a runtime class without dynamic indexing (a local
+// array indexed by a runtime value lives in local memory: an LDL/STL pair per use).
+__device__ __forceinline__ void cls_count(uint32_t (&acc)[NCLS], uint32_t c) {
+#pragma unroll
+    for (int k = 0; k < NCLS; ++k) acc[k] += c == (uint32_t)k;
+}
+__device__ __forceinline__ uint32_t cls_take(uint32_t (&pos)[NCLS], uint32_t c) {
+    uint32_t r = pos[0];
+#pragma unroll
+    for (int k = 1; k < NCLS; ++k) r = c == (uint32_t)k ? pos[k] : r;
+#pragma unroll
+    for (int k = 0; k < NCLS; ++k) pos[k] += c == (uint32_t)k;
+    return r;
+}
+
 // Pass 1: per-CTA class counts of set bits in its contiguous word range.
 template <class Src>
 __device__ void ballot_count(const Src& src, const Sched& s, const uint32_t* deg) {

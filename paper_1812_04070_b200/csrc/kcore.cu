@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(BLOCK, SX_KCORE_MINB) kcore_push(KcoreP p) {
                         mn = min(mn, r);
                         if (r <= kspec) {
                             m |= 1u << b;
-                            if (!spec) acc[cls_of(__ldg(p.g.dout + (uint32_t)((wi << 5) + b)), p.s)]++;
+                            if (!spec) cls_count(acc, cls_of(__ldg(p.g.dout + (uint32_t)((wi << 5) + b)), p.s));
                         }
                     });
                     if (spec) {
