@@ -49,6 +49,9 @@ struct KcoreP {
 #endif
 constexpr uint32_t AQ_WARPS = SX_AQ_WARPS;
 constexpr unsigned long long AQ_ONE = 1ull << 32;
+#ifndef SX_AQ_RELEASE
+#define SX_AQ_RELEASE 1
+#endif
 __device__ __forceinline__ uint32_t aq_pending(const Ctl* c) { return (uint32_t)(vload(&c->aq_tp) >> 32); }
 // watchdog of the queue waits (as the grid barrier's): a lost item would leave
 // pending > 0 forever; after 20 s the waiters give up and flag SX_E_BARRIER
@@ -66,6 +69,20 @@ constexpr double KCORE_ALPHA = 4.0;  // pull a sub-round whose frontier has > m 
 #endif
 constexpr uint32_t AQ_PIECE = SX_AQ_PIECE;  // a removal of a longer row is split into pieces of this many edges
 constexpr unsigned long long AQ_EMPTY = ~0ull;
+// An item is done: its pending count drops with a RELEASE reduction (the warp's
+// enqueues, ordered before it by __syncwarp, are visible first).  A
+// __threadfence + atomicAdd did the same with a full fence, which also
+// invalidates L1 (CCTL.IVALL): the spilled locals of the queue loop were then
+// reloaded from L2 on every item of a cascade's dependent chain.
+__device__ __forceinline__ void aq_done(unsigned long long* tp) {
+#if SX_AQ_RELEASE
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(tp), "l"((unsigned long long)(-(long long)AQ_ONE))
+                 : "memory");
+#else
+    __threadfence();
+    atomicAdd(tp, (unsigned long long)(-(long long)AQ_ONE));
+#endif
+}
 // Work-first (KEEP): the first neighbour an item's warp removes stays with the
 // warp as its next item — no ticket, no queue publish and no spin on the
 // dependent chain of a cascade; the item's pending token passes to it.  The
@@ -129,10 +146,7 @@ __device__ __forceinline__ void kcore_async(const KcoreP& p, Ctl* c, Rm&& remove
                 continue;
             }
         }
-        if (lane == 0) {
-            __threadfence();
-            atomicAdd(&c->aq_tp, (unsigned long long)(-(long long)AQ_ONE));  // done with this item
-        }
+        if (lane == 0) aq_done(&c->aq_tp);  // done with this item
     }
 }
 
