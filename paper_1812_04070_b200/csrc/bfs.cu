@@ -427,8 +427,14 @@ __global__ void __launch_bounds__(BLOCK, SX_PUSH_MINB) bfs_push(BfsP p) {
 //  * LIST mode (small candidate sets — the online side): the candidates still
 //    open at the end of the previous pull iteration were recorded in slotted
 //    lists (online filter); the iteration walks those lists in warp
-//    chunks instead of scanning every tile.  Chosen after the barrier when the
-//    recorded total is <= n / LIST_DIV and no region overflowed.
+//    chunks instead of scanning every tile.  A level records its open
+//    candidates only when its own candidates are <= n / REC_OPEN_DIV (never the
+//    first pull): recording costs the recording level, and a LIST level over a
+//    large set is slower than a TILE scan.  Otherwise they are only counted (the
+//    next level's candidate count).  LIST mode follows a recorded level when the
+//    recorded total is <= n / LIST_DIV and no region overflowed.  When at most
+//    FREC_MAX vertices can be found, the found ones also go onto a list (TILE
+//    or LIST mode) that a switch back to push takes as its task list.
 // A warp's candidates then go through two phases.  (1) Hub-first probe, HUB_ILP
 // rounds of 32 in flight: one load of hub[v] and one bitmap test each; a sole
 // in-edge probed in vain settles v (still open, no row walk).  (2) Row walks of
