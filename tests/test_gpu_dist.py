@@ -155,9 +155,11 @@ def test_dist_nccl_one_rank_communicator(ctx, rmat14):
     D.free()
 
 
-def test_bench_dist_path_under_torchrun():
+@pytest.mark.parametrize("fusion", [1, 2])
+def test_bench_dist_path_under_torchrun(fusion):
     """bench.py's multi-GPU path (torchrun, NCCL communicator, max-over-ranks
-    timing) at one rank: one JSON line with the contract's keys."""
+    timing) at one rank: one JSON line with the contract's keys.  fusion 2: the
+    device-initiated BFS with asynchronous steps (sx_dist_bfs_async)."""
     import json
     import os
     import socket
@@ -170,10 +172,12 @@ def test_bench_dist_path_under_torchrun():
     s.close()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
            "--master-addr=127.0.0.1", f"--master-port={port}", "bench.py", "--gpus", "1", "--dist", "--scale", "16",
-           "--steps", "3", "--warmup", "3", "--no-e2e"]
+           "--steps", "3", "--warmup", "3", "--no-e2e", "--fusion", str(fusion)]
     out = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
     assert line["unit"] == "GTEPS" and line["value"] > 0 and line["n_gpus"] == 1
     assert line["config"]["parallelism"] == "1d1" and "NCCL" in line["config"]["workload"]
     assert line["gpu_launches"] > 0
+    if fusion == 2:
+        assert "device API" in line["config"]["workload"] and line["gpu_launches"] == 3  # one kernel per step
