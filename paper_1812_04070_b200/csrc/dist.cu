@@ -236,9 +236,15 @@ template <int PIECES> __global__ void k_bfs_push(RankView r) {
 }
 
 // owner side of a push level: OR the P received slices, keep the unvisited bits
+// Also clears, in the same launch, the level's pushed frontier (r.cur: the next
+// level's output buffer) and this rank's send bitmap (consumed by the exchange
+// before this launch) — no memset launches per level.
 __global__ void k_bfs_apply(RankView r, uint32_t lvl) {
     unsigned long long found = 0, mdeg = 0;
+    const uint64_t NW = (uint64_t)r.P * r.nwl;
+    for (uint64_t w = gtid(); w < NW; w += gthreads()) r.sendmap[w] = 0;
     for (uint64_t wi = gtid(); wi < r.nwl; wi += gthreads()) {
+        r.cur[wi] = 0;
         uint32_t m = 0;
         for (uint32_t q = 0; q < r.P; ++q) m |= r.recv[(uint64_t)q * r.nwl + wi];
         const uint64_t v0 = wi << 5;
@@ -405,7 +411,7 @@ __device__ __forceinline__ void dist_pull_batches(const RankView& r, const uint3
 }
 __global__ void k_bfs_pull(RankView r, uint32_t lvl) {
     unsigned long long found = 0, mdeg = 0, edges = 0;
-    dist_pull_batches(r, r.gfront, r.nxt, lvl, found, mdeg, edges);
+    dist_pull_batches(r, r.gfront, r.nxt, lvl, found, mdeg, edges, r.cur);  // r.cur: the next output, cleared on the way
     uint64_t a[3] = {found, mdeg, edges};
     block_sum<3>(a);
     if (threadIdx.x == 0) {
@@ -1439,7 +1445,6 @@ sx_status sx_dist_bfs(sx_dist d, uint32_t src, const sx_opts* opts, uint32_t* co
             }
             if ((rc = ex_alltoall(d)) != SX_OK) return rc;
             for (int i = 0; i < d->nlocal; ++i) {
-                SX_CU(cudaMemsetAsync(d->r[i].sendmap, 0, d->NW * 4, s));
                 k_bfs_apply<<<G, BLOCK, 0, s>>>(view_of(d, i, cur, o), lvl);
                 ++launches;
             }
@@ -1464,8 +1469,8 @@ sx_status sx_dist_bfs(sx_dist d, uint32_t src, const sx_opts* opts, uint32_t* co
         ++it;
         m_u -= mf;
         mf_prev = mf;
-        // the new frontier is front[cur ^ 1]; the old one becomes next iteration's output and is cleared
-        for (int i = 0; i < d->nlocal; ++i) SX_CU(cudaMemsetAsync(d->r[i].front[cur], 0, d->nwl * 4, s));
+        // the new frontier is front[cur ^ 1]; the old one (the next output) was cleared by the
+        // level's apply / pull launch
         cur ^= 1;
         if (nf == 0 || (o.max_iters && it >= o.max_iters)) break;
         if (dir == DIR_PUSH) {
