@@ -970,6 +970,11 @@ __global__ void __launch_bounds__(BLOCK, SX_ALL_MINB) bfs_all(BfsP p, uint32_t s
             if (acc) atomicAdd(&acc->errors, 1u);
         }
     };
+#ifdef SX_BFS_MARKS
+    const uint64_t t_start = globaltimer();  // profiling build: record 0's aux = ns from kernel start
+#else
+    const uint64_t t_start = 0;
+#endif
     grid_begin(c);  // parity of this launch (the previous launch's exit zeroed this half)
     if (fuse_init) {
         bfs_init_body<true>(p, src, dir0);
@@ -978,7 +983,7 @@ __global__ void __launch_bounds__(BLOCK, SX_ALL_MINB) bfs_all(BfsP p, uint32_t s
     }
     {
         const uint32_t z[NCLS] = {0u, 0u, 0u, 0u};
-        trace_put(p.s, 0, DIR_PUSH, 0u, z, 1, 0, 0);  // end of the state init (iteration 0)
+        trace_put(p.s, 0, DIR_PUSH, 0u, z, 1, 0, t_start ? globaltimer() - t_start : 0);  // end of the state init (iteration 0)
     }
     RunState& rs = const_cast<RunState&>(run_state(c));
     while (!rs.done) {

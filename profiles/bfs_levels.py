@@ -35,5 +35,9 @@ tr = runs[0][2]
 def _nm(t):
     return ('push', 'pull', 'clus')[t['dir']] if t['dir'] < 3 else f"mark{t['dir'] - 16}"
 lv = " ".join(f"it{tr[i]['iter'] % 1000}:{_nm(tr[i])}:{dts[i - 1]:.1f}" for i in range(1, nl))
+init = statistics.median(next((t["aux"] for t in r[2] if t["iter"] == 0 and t["dir"] == 0), 0) for r in runs) / 1e3
+# (profiling builds: the iteration-0 record's aux = ns from the kernel start to the end of the state init)
+if init > 0:
+    lv = f"[init {init:.1f}] " + lv
 print(f"{os.path.basename(os.environ.get('SIMDX_LIB', 'main'))} fusion={kw.get('fusion', 1)}: bfs s{scale} {ms * 1e3:.1f} us "
       f"(pull {mp * 1e3:.1f}, push {mpu * 1e3:.1f}) levels us: {lv}")
