@@ -406,9 +406,10 @@ void sx_dist_free(sx_dist d);
  * over the NCCL device API — push marks atomically OR'ed into the owner's inbox
  * and frontier slices stored into every rank's global bitmap through LSA
  * pointers into a symmetric window (ncclMemAlloc + ncclCommWindowRegister),
- * counters stored into every rank's slots, one ncclLsaBarrierSession per level
- * step — no host round trip per level.  Needs every rank in one LSA team (one
- * NVLink/NVSwitch domain): SX_E_NCCL otherwise.  Errors as sx_bfs.
+ * counters added into every rank's slots with peer atomics, one
+ * ncclLsaBarrierSession per level step — no host round trip per level.  Needs
+ * every rank in one LSA team (one NVLink/NVSwitch domain): SX_E_NCCL otherwise.
+ * A DEVICE level_out[i] is written in place (no copy-out).  Errors as sx_bfs.
  */
 sx_status sx_dist_bfs(sx_dist d, uint32_t src, const sx_opts* opts, uint32_t* const* level_out, sx_stats* stats);
 /* Asynchronous device-initiated distributed BFS (the fusion = 2 run of sx_dist_bfs, the same result):
