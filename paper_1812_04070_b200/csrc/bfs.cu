@@ -114,6 +114,28 @@ __device__ __forceinline__ bool cluster_ok(const Sched& s, uint64_t nf, uint64_t
     } while (0)
 #endif
 
+// SX_BFS_ANAT (profiling builds): anatomy of the first pull level's TILE chunks —
+// SM cycles per segment summed over CTA 0's warps (profiles/bfs_anatomy.py reads
+// them through sx_debug_bfs_anat, a symbol outside the ABI).  A volatile store of
+// the segment's last value makes the clock read wait for it.
+#ifdef SX_BFS_ANAT
+__device__ unsigned long long g_bfs_anat[16];
+__device__ volatile uint32_t g_bfs_sink;
+#define ANAT(k, dep)                                         \
+    do {                                                      \
+        if (an_on) {                                          \
+            g_bfs_sink = (uint32_t)(dep);                     \
+            const unsigned long long t_ = clock64();          \
+            an[k] += t_ - an_last;                            \
+            an_last = t_;                                     \
+        }                                                     \
+    } while (0)
+#else
+#define ANAT(k, dep) \
+    do {             \
+    } while (0)
+#endif
+
 // Per-run state in one grid-stride pass: level = INF (0 at src), visited and
 // the three frontier bitmaps zero (src's bit set in visited and bm[0]); block 0
 // also seeds the control block and the first list.
@@ -457,7 +479,11 @@ constexpr uint32_t LIST_CSZ_MAX = SX_LIST_CSZ_MAX;  // LIST-mode chunk (candidat
 #ifndef SX_HUB_ILP
 #define SX_HUB_ILP 4
 #endif
-constexpr int HUB_ILP = SX_HUB_ILP;             // phase 1: rounds of 32 candidates in flight per warp
+constexpr int HUB_ILP = SX_HUB_ILP;
+#ifndef SX_HUB_PIPE
+#define SX_HUB_PIPE 0  // measured (session 3): probe rounds 9.8 -> 9.1 us per chunk, level total unchanged (issue-bound, not latency-bound)
+#endif
+constexpr bool HUB_PIPE = SX_HUB_PIPE;  // next probe round's hub loads issued before this round's processing             // phase 1: rounds of 32 candidates in flight per warp
 #ifndef SX_LIST_DIV
 #define SX_LIST_DIV 8
 #endif
@@ -538,6 +564,10 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
         // the open candidates are recorded (LIST mode next) only when this level's candidates are few
         const bool rec_open = PULL_REC && cand_cnt <= n / REC_OPEN_DIV && p.s.force_filter != 2;
         uint32_t open_cnt = 0;  // open candidates counted, not recorded (!rec_open)
+#ifdef SX_BFS_ANAT
+        const bool an_on = blockIdx.x == 0 && !list_mode && cand_cnt == ~0ull;  // CTA 0, the first pull level
+        unsigned long long an[8] = {0, 0, 0, 0, 0, 0, 0, 0}, an_last = clock64();
+#endif
         uint32_t* cnext = p.s.lists[(it + 1) & 1] + (uint64_t)CAND_CLS * p.s.cstride;
         uint32_t* flist = p.s.lists[(it + 1) & 1];  // class-0 region: the found list (hand-over)
         unsigned int* fcnt = &c->cl.cnt[(it + 1) % 3];
@@ -678,22 +708,34 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
         // sh: the chunk's staged hub slice (vertices from vbase), or nullptr (global loads)
         auto run_cands = [&](auto R, uint32_t total, uint64_t w0, const uint32_t* sh, uint32_t vbase) {
             uint32_t nopen = 0;
+            // a round's candidates and their hub entries (the in-place compaction below
+            // only writes positions before the round, so a later round can be read early)
+            uint32_t vn[HUB_ILP], xn[HUB_ILP];
+            auto load_round = [&](uint32_t r0) {
+#pragma unroll
+                for (int k = 0; k < HUB_ILP; ++k) {
+                    const uint32_t i = r0 + 32 * k + lane;
+                    vn[k] = i < total ? s_c[i] : INF;
+                }
+#pragma unroll
+                for (int k = 0; k < HUB_ILP; ++k)
+                    xn[k] = vn[k] == INF ? INF : sh ? sh[vn[k] - vbase] : __ldg(p.hub + vn[k]);
+            };
+            load_round(0);
             for (uint32_t r0 = 0; r0 < total; r0 += 32 * HUB_ILP) {
                 uint32_t v[HUB_ILP], h[HUB_ILP], wd[HUB_ILP];
                 bool sole[HUB_ILP];
 #pragma unroll
                 for (int k = 0; k < HUB_ILP; ++k) {
-                    const uint32_t i = r0 + 32 * k + lane;
-                    v[k] = i < total ? s_c[i] : INF;
-                }
-#pragma unroll
-                for (int k = 0; k < HUB_ILP; ++k) {
-                    const uint32_t x = v[k] == INF ? INF : sh ? sh[v[k] - vbase] : __ldg(p.hub + v[k]);
-                    h[k] = hub_id(x);
-                    sole[k] = hub_sole(x);
+                    v[k] = vn[k];
+                    h[k] = hub_id(xn[k]);
+                    sole[k] = hub_sole(xn[k]);
                 }
 #pragma unroll
                 for (int k = 0; k < HUB_ILP; ++k) wd[k] = h[k] != INF ? cur[h[k] >> 5] : 0u;
+                // software pipeline (SX_HUB_PIPE): the next round's hub loads fly while this
+                // round's frontier tests and bookkeeping run
+                if (HUB_PIPE && r0 + 32 * HUB_ILP < total) load_round(r0 + 32 * HUB_ILP);
                 __syncwarp();
 #pragma unroll
                 for (int k = 0; k < HUB_ILP; ++k) {
@@ -710,7 +752,9 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
                     nopen += __popc(bal);
                 }
                 __syncwarp();
+                if (!HUB_PIPE && r0 + 32 * HUB_ILP < total) load_round(r0 + 32 * HUB_ILP);
             }
+            ANAT(3, nopen);  // hub-first probe rounds
             walk_open(R, nopen, w0);
         };
         uint32_t s_cur = my_slot();
@@ -796,6 +840,10 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
                 const bool mine = lane < CW && wl < nw;
                 const uint32_t vis_l = mine ? p.visited[wl] : FULL;
                 const uint32_t cand_l = mine ? (~vis_l & __ldg(p.g.nz_in + wl)) : 0u;
+#ifdef SX_BFS_ANAT
+                if (an_on) an[7] += 1;  // chunks
+#endif
+                ANAT(0, cand_l);  // chunk claim -> visited / in-degree words
                 uint32_t incl = __popc(cand_l);
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
@@ -815,9 +863,11 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
                     for (uint32_t w = cand_l; w; w &= w - 1) s_c[pos++] = (uint32_t)(wl << 5) + (__ffs(w) - 1);
                     s_f[lane] = 0;
                     __syncwarp();
+                    ANAT(1, pos);  // scan + compaction into shared memory
                     if (rec_open) run_cands(std::true_type{}, total, w0, sh, (uint32_t)(w0 << 5));
                     else run_cands(std::false_type{}, total, w0, sh, (uint32_t)(w0 << 5));
                     __syncwarp();
+                    ANAT(4, s_f[lane]);  // row walks of the open candidates
                     flush_rec();
                     const uint32_t fm = s_f[lane];
                     if (fm) {
@@ -843,14 +893,20 @@ __device__ __forceinline__ bool pull_phase(const BfsP& p, RunState& rs) {
                     }
                     __syncwarp();
                 }
+                ANAT(5, found_cnt);  // merge + stores of the chunk's words
 #if SX_PULL_TMA
                 chunk = chunk_n;
 #else
                 if (PULL_STATIC) chunk = chunk + gwarps() < nchunks ? chunk + (uint32_t)gwarps() : INF;
                 else chunk = grab_finish(nx, nchunks, s_cur, raw_n, s_iss);
 #endif
+                ANAT(6, chunk);  // the next chunk's claim
             }
         }
+#ifdef SX_BFS_ANAT
+        if (an_on && lane == 0)
+            for (int k = 0; k < 8; ++k) atomicAdd(&g_bfs_anat[k], an[k]);
+#endif
         st.edges += edges;
         st.reached += found_cnt;
 #ifdef SX_BFS_SPREAD
@@ -1488,3 +1544,15 @@ extern "C" sx_status sx_ctx_info(sx_ctx c, sx_device_info* out) {
     out->pull_regs = a.numRegs;
     return SX_OK;
 }
+
+#ifdef SX_BFS_ANAT
+extern "C" int sx_debug_bfs_anat(unsigned long long* out16, int reset) {
+    cudaDeviceSynchronize();
+    if (cudaMemcpyFromSymbol(out16, sx::g_bfs_anat, 16 * 8) != cudaSuccess) return 1;
+    if (reset) {
+        unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(sx::g_bfs_anat, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
