@@ -34,6 +34,18 @@ def test_c1_bfs_rmat16(ctx):
     dirs = [t["dir"] for t in tr]
     switches = sum(1 for a, b in zip(dirs, dirs[1:]) if a != b)
     assert len({t["launch"] for t in tr}) == 1 + switches
+    # the launch counts Table 2 prints (tests/golden/table2.txt): selective fusion
+    # push -> pull -> push = 3 launches, all fusion = 1
+    import os
+    gold = {}
+    for line in open(os.path.join(os.path.dirname(__file__), "golden", "table2.txt")):
+        if line.strip() and not line.startswith("#"):
+            k, v = line.split()
+            gold[k] = int(v)
+    assert [d for i, d in enumerate(dirs) if i == 0 or d != dirs[i - 1]] == [0, 1, 0]  # push, pull, push
+    assert st["launches"] == gold["selective_bfs_push_pull_push"]
+    lv2, st2, _ = G.bfs(0, fusion=2)
+    assert np.array_equal(lv2, ref) and st2["launches"] == gold["all_fusion"]
     G.free()
 
 
