@@ -119,7 +119,10 @@ sx_status sx_launch_bench(sx_ctx ctx, uint32_t mode, uint32_t reps, double* us);
 enum {
     SX_DIRECTED = 1,    /* csc_* describe the in-neighbour rows; otherwise the graph is symmetric and CSR serves as CSC */
     SX_DEVICE_PTRS = 2, /* row_ptr/col/w (and csc_*) are device pointers */
-    SX_BORROW = 4       /* with SX_DEVICE_PTRS: do not copy; the caller keeps the arrays alive until sx_graph_free */
+    SX_BORROW = 4,      /* with SX_DEVICE_PTRS: do not copy; the caller keeps the arrays alive until sx_graph_free */
+    SX_DEDUP = 8        /* collapse duplicate edges at upload (reading 19 keeps them by default): one edge per
+                           (row, neighbour) with the minimum weight of its duplicates, neighbours ascending per
+                           row; m (and the CSC's) shrink accordingly.  Implies a copy (no SX_BORROW) */
 };
 
 /*

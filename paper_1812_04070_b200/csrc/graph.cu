@@ -11,6 +11,9 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
 #include "internal.h"
 
 using namespace sx;
@@ -102,6 +105,120 @@ struct PhaseTimer {
     }
 };
 
+// ---- SX_DEDUP: duplicate edges collapsed (reading 19 keeps
+// duplicates by default).  Per graph, at upload: keys (row << 32 | col) sorted
+// by one 64-bit radix sort (rows stay in place, each row's neighbours ascend),
+// a run of equal keys keeps one edge with the run's MINIMUM weight (so shortest
+// paths are unchanged), survivors are compacted by an exclusive scan, and
+// row_ptr'[r] = the scan at the row's old start.
+__global__ void k_dd_keys(const uint64_t* rp, const uint32_t* ci, uint64_t n, uint64_t* keys) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t r = gw; r < n; r += nw)
+        for (uint64_t e = rp[r] + lane; e < rp[r + 1]; e += 32) keys[e] = (r << 32) | ci[e];
+}
+template <class W>
+__global__ void k_dd_flags(const uint64_t* keys, const W* w, uint64_t m, uint64_t* flag, W* wmin) {
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e <= m; e += (uint64_t)gridDim.x * blockDim.x) {
+        const bool head = e < m && (e == 0 || keys[e] != keys[e - 1]);
+        flag[e] = head ? 1u : 0u;
+        if (head && w) {  // the run's minimum weight (runs are short: the duplicates of one edge)
+            W x = w[e];
+            for (uint64_t f = e + 1; f < m && keys[f] == keys[e]; ++f) x = w[f] < x ? w[f] : x;
+            wmin[e] = x;
+        }
+    }
+}
+template <class W>
+__global__ void k_dd_scatter(const uint64_t* keys, const uint64_t* flag, const uint64_t* pos, const W* wmin, uint64_t m,
+                             uint32_t* ci, W* w) {
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x)
+        if (flag[e]) {
+            ci[pos[e]] = (uint32_t)keys[e];
+            if (w) w[pos[e]] = wmin[e];
+        }
+}
+__global__ void k_dd_rowptr(const uint64_t* rp, const uint64_t* pos, uint64_t n, uint64_t* rp2) {
+    for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r <= n; r += (uint64_t)gridDim.x * blockDim.x)
+        rp2[r] = pos[rp[r]];
+}
+
+// Collapse the duplicates of one CSR (rp/ci/w owned by the graph) in place of the
+// arrays: new arrays replace the old ones, *m gets the new edge count.
+sx_status dedup_csr(sx_ctx ctx, uint64_t n, uint64_t* m, uint64_t** rp, uint32_t** ci, void** w, uint32_t wbytes) {
+    cudaStream_t s = ctx->stream;
+    const uint64_t M = *m;
+    const int g = 8 * ctx->prop.multiProcessorCount;
+    uint64_t *keys = nullptr, *keys2 = nullptr, *flag = nullptr, *pos = nullptr, *rp2 = nullptr;
+    void *w2 = nullptr, *wmin = nullptr, *tmp = nullptr, *wn = nullptr;
+    uint32_t* ci2 = nullptr;
+    auto cleanup = [&]() {
+        for (void* q : {(void*)keys, (void*)keys2, (void*)flag, (void*)pos, w2, wmin, tmp}) sxh::dfree(ctx, q);
+    };
+#define DTRY(x)                             \
+    do {                                    \
+        sx_status r__ = (x);                \
+        if (r__ != SX_OK) {                 \
+            cleanup();                      \
+            return r__;                     \
+        }                                   \
+    } while (0)
+    DTRY(sxh::dmalloc(ctx, (void**)&keys, M * 8 + 8));
+    DTRY(sxh::dmalloc(ctx, (void**)&keys2, M * 8 + 8));
+    DTRY(sxh::dmalloc(ctx, (void**)&flag, (M + 1) * 8));
+    DTRY(sxh::dmalloc(ctx, (void**)&pos, (M + 1) * 8));
+    if (*w) {
+        DTRY(sxh::dmalloc(ctx, &w2, M * wbytes + 16));
+        DTRY(sxh::dmalloc(ctx, &wmin, M * wbytes + 16));
+    }
+    k_dd_keys<<<g, 256, 0, s>>>(*rp, *ci, n, keys);
+    size_t tb = 0;
+    if (*w && wbytes == 1) {
+        SX_CU(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, (const uint8_t*)*w, (uint8_t*)w2, (int64_t)M, 0, 64, s));
+    } else if (*w) {
+        SX_CU(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, (const uint32_t*)*w, (uint32_t*)w2, (int64_t)M, 0, 64, s));
+    } else {
+        SX_CU(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, keys2, (int64_t)M, 0, 64, s));
+    }
+    size_t tb2 = 0;
+    SX_CU(cub::DeviceScan::ExclusiveSum(nullptr, tb2, flag, pos, (int64_t)(M + 1), s));
+    DTRY(sxh::dmalloc(ctx, &tmp, std::max(tb, tb2) + 16));
+    if (*w && wbytes == 1) {
+        SX_CU(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, (const uint8_t*)*w, (uint8_t*)w2, (int64_t)M, 0, 64, s));
+        k_dd_flags<uint8_t><<<g, 256, 0, s>>>(keys2, (const uint8_t*)w2, M, flag, (uint8_t*)wmin);
+    } else if (*w) {
+        SX_CU(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, (const uint32_t*)*w, (uint32_t*)w2, (int64_t)M, 0, 64, s));
+        k_dd_flags<uint32_t><<<g, 256, 0, s>>>(keys2, (const uint32_t*)w2, M, flag, (uint32_t*)wmin);
+    } else {
+        SX_CU(cub::DeviceRadixSort::SortKeys(tmp, tb, keys, keys2, (int64_t)M, 0, 64, s));
+        k_dd_flags<uint32_t><<<g, 256, 0, s>>>(keys2, (const uint32_t*)nullptr, M, flag, (uint32_t*)nullptr);
+    }
+    SX_CU(cub::DeviceScan::ExclusiveSum(tmp, tb2, flag, pos, (int64_t)(M + 1), s));
+    uint64_t M2 = 0;
+    SX_CU(cudaMemcpyAsync(&M2, pos + M, 8, cudaMemcpyDeviceToHost, s));
+    SX_CU(cudaStreamSynchronize(s));
+    DTRY(sxh::dmalloc(ctx, (void**)&ci2, M2 * 4 + 16));
+    DTRY(sxh::dmalloc(ctx, (void**)&rp2, (n + 1) * 8 + 16));
+    if (*w) DTRY(sxh::dmalloc(ctx, &wn, M2 * wbytes + 16));
+    if (*w && wbytes == 1)
+        k_dd_scatter<uint8_t><<<g, 256, 0, s>>>(keys2, flag, pos, (const uint8_t*)wmin, M, ci2, (uint8_t*)wn);
+    else
+        k_dd_scatter<uint32_t><<<g, 256, 0, s>>>(keys2, flag, pos, (const uint32_t*)wmin, M, ci2, (uint32_t*)wn);
+    k_dd_rowptr<<<g, 256, 0, s>>>(*rp, pos, n, rp2);
+    SX_CU(cudaGetLastError());
+    SX_CU(cudaStreamSynchronize(s));
+    cleanup();
+#undef DTRY
+    sxh::dfree(ctx, *rp);
+    sxh::dfree(ctx, *ci);
+    if (*w) sxh::dfree(ctx, *w);
+    *rp = rp2;
+    *ci = ci2;
+    if (*w) *w = wn;
+    *m = M2;
+    return SX_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -116,7 +233,9 @@ sx_status sx_graph_upload(sx_ctx ctx, const sx_csr_desc* d, sx_graph* out) {
     if (d->w && d->w_bytes != 1 && d->w_bytes != 4) return sxh::fail(SX_E_INVALID, "sx_graph_upload: w_bytes must be 1 or 4");
     const bool directed = d->flags & SX_DIRECTED;
     const bool devp = d->flags & SX_DEVICE_PTRS;
-    const bool borrow = devp && (d->flags & SX_BORROW) && aligned16(d->col) && (!directed || !d->csc_idx || aligned16(d->csc_idx));
+    const bool dedup = d->flags & SX_DEDUP;  // the deduplicated arrays are the graph's own: no borrowing
+    const bool borrow = !dedup && devp && (d->flags & SX_BORROW) && aligned16(d->col) &&
+                        (!directed || !d->csc_idx || aligned16(d->csc_idx));
     cudaStream_t s = ctx->stream;
     PhaseTimer pt(s);
     sx_graph g = new sx_graph_s();
@@ -195,6 +314,19 @@ sx_status sx_graph_upload(sx_ctx ctx, const sx_csr_desc* d, sx_graph* out) {
     }
     if (hflags & 16) return bail(sxh::fail(SX_E_INVALID, "sx_graph_upload: a degree exceeds 2^32-2"));
     g->has_zero_w = (hflags & 8) != 0;
+    if (dedup) {  // SX_DEDUP: duplicate edges collapsed (one edge, the minimum weight)
+        const bool rev = directed && g->has_rev;
+        TRY(dedup_csr(ctx, n, &g->m, &g->rp, &g->ci, &g->w, g->wbytes));
+        if (rev) {
+            TRY(dedup_csr(ctx, n, &g->mi, &g->irp, &g->ici, &g->iw, g->wbytes));
+        } else {
+            g->irp = g->rp;
+            g->ici = g->ci;
+            g->iw = g->w;
+            g->mi = g->m;
+        }
+        pt.mark("upload: dedup");
+    }
     // degrees + in-degree>0 bitmap
     g->nwords = ((n + 31) / 32 + TILE_WORDS - 1) / TILE_WORDS * TILE_WORDS;
     if (g->nwords == 0) g->nwords = TILE_WORDS;

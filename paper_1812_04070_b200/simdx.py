@@ -27,7 +27,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 # ---------------------------------------------------------------- constants
 SX_OK, SX_E_INVALID, SX_E_OOM, SX_E_CUDA, SX_E_NCCL, SX_E_NO_REVERSE, SX_E_WEIGHT, SX_E_BARRIER, SX_E_STATE = range(9)
-SX_DIRECTED, SX_DEVICE_PTRS, SX_BORROW = 1, 2, 4
+SX_DIRECTED, SX_DEVICE_PTRS, SX_BORROW, SX_DEDUP = 1, 2, 4, 8
 INF = 0xFFFFFFFF
 
 _u64, _u32, _i32, _f32, _vp = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int32, ctypes.c_float, ctypes.c_void_p
@@ -238,7 +238,7 @@ def sx_barrier_bench(ctx, iters: int = 10000):
 
 
 def sx_graph_upload(ctx, n, row_ptr, col, w=None, csc_ptr=None, csc_idx=None, csc_w=None, directed=False,
-                    borrow=False):
+                    borrow=False, dedup=False):
     """row_ptr u64[n+1], col u32[m], w u8/u32[m] or None — numpy (host) or torch CUDA tensors (device)."""
     dev = _on_device(row_ptr)
     d = sx_csr_desc()
@@ -247,7 +247,8 @@ def sx_graph_upload(ctx, n, row_ptr, col, w=None, csc_ptr=None, csc_idx=None, cs
     d.row_ptr, d.col, d.w = _ptr(row_ptr), _ptr(col), _ptr(w)
     d.w_bytes = 0 if w is None else w.element_size() if _is_torch(w) else w.dtype.itemsize
     d.csc_ptr, d.csc_idx, d.csc_w = _ptr(csc_ptr), _ptr(csc_idx), _ptr(csc_w)
-    d.flags = (SX_DIRECTED if directed else 0) | (SX_DEVICE_PTRS if dev else 0) | (SX_BORROW if borrow else 0)
+    d.flags = (SX_DIRECTED if directed else 0) | (SX_DEVICE_PTRS if dev else 0) | (SX_BORROW if borrow else 0) | \
+        (SX_DEDUP if dedup else 0)
     h = _vp()
     _check(_lib.sx_graph_upload(ctx, ctypes.byref(d), ctypes.byref(h)), "sx_graph_upload")
     return h
@@ -402,11 +403,11 @@ class Context:
         """sx_graph_grid: the simgen rows x cols grid built on the device."""
         return Graph(self, sx_graph_grid(self.h, rows, cols, seed, wmin, wmax), rows * cols)
 
-    def upload(self, csr) -> "Graph":
-        """Upload a simgen.CSR-like object (fields n,row_ptr,col,w,directed,csc_*)."""
+    def upload(self, csr, dedup: bool = False) -> "Graph":
+        """Upload a simgen.CSR-like object (fields n,row_ptr,col,w,directed,csc_*); dedup: SX_DEDUP."""
         h = sx_graph_upload(self.h, csr.n, csr.row_ptr, csr.col, csr.w,
                             getattr(csr, "csc_ptr", None), getattr(csr, "csc_idx", None),
-                            getattr(csr, "csc_w", None), bool(getattr(csr, "directed", False)))
+                            getattr(csr, "csc_w", None), bool(getattr(csr, "directed", False)), dedup=dedup)
         return Graph(self, h, csr.n)
 
     def close(self):
