@@ -23,7 +23,8 @@ cand = torch.nonzero(deg > 0).flatten().cpu().numpy()
 roots = np.random.default_rng(1).choice(cand, 64, replace=False)
 out = torch.empty(1 << scale, dtype=torch.int32, device="cuda:0")
 mcs = {}
-for alpha, beta in ((14, 24), (30, 24), (30, 128), (60, 24), (60, 128), (100, 128), (200, 128), (60, 512)):
+AB = [tuple(map(int, x.split(","))) for x in sys.argv[2:]] or [(14, 24), (30, 24), (30, 128), (60, 24), (60, 128), (100, 128), (200, 128), (60, 512)]
+for alpha, beta in AB:
     kw = dict(fusion=2, cluster_enter=0, alpha=alpha, beta=beta)
     hub = min(G.bfs(0, out=out, **kw)[1]["ms"] for _ in range(4))
     g = []
